@@ -1,0 +1,185 @@
+/*
+ * brownout.h - C ABI of the B200-native brownout MoE-layer forward.
+ *
+ * The method is BrownoutServe's BrownoutMoE layer (arXiv 2507.17133):
+ *   router logits     Eq. 8       s_{i,t} = x_t^T e_i
+ *   top-K gate        Eq. 7            g = softmax over the K largest s
+ *   brownout plan     Alg. 1            S1 / S2 / united groups / special case
+ *   expert FFNs       Eq. 5, SwiGLU        process_tokens (Alg. 1)
+ *   gate weighting    Eq. 6            p = g for S1, q = g for S2
+ *   combine           Eq. 5                h_t = [x_t] + sum of weighted outputs
+ * "United experts" (one per group of `way` experts) are passed in
+ * by the caller; bo_build_united() makes a deterministic initialisation.
+ *
+ * Conventions for every call:
+ *  - All tensor arguments are DEVICE pointers owned by the caller (PyTorch).
+ *    The library never allocates or frees device memory; bo_moe_forward uses
+ *    only the caller's workspace.  Layouts are dense row-major (C order).
+ *  - `stream` is a cudaStream_t passed as void*; every call that launches work
+ *    enqueues it on that stream and returns without synchronising (except where
+ *    noted).  The single-GPU forward has no host<->device synchronisation and is
+ *    CUDA-graph capturable.
+ *  - Every call returns a bo_status.  Nothing throws or aborts across the ABI.
+ *    bo_last_error() returns a thread-local message for the last failure.
+ *    Asynchronous CUDA errors surface as BO_ERR_CUDA on a later call.
+ *  - A handle is not thread-safe: use one host thread per handle.
+ *  - Element dtype of x, y, Wr, experts and united is the handle's dtype:
+ *    BO_BF16 (bf16 storage, tcgen05 kind::f16 MMAs with fp32 accumulation) or
+ *    BO_FP32 (fp32 storage, tcgen05 kind::tf32 MMAs with fp32 accumulation).
+ */
+#ifndef BROWNOUT_H_
+#define BROWNOUT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define BO_API __attribute__((visibility("default")))
+#else
+#define BO_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BO_OK = 0,
+  BO_ERR_INVALID_ARG = 1,  /* null pointer, ratio outside [0,1], way < 1, K outside [1, min(m,16)], T > max_tokens */
+  BO_ERR_SHAPE = 2,        /* hidden or ffn not a multiple of 64 (bf16) / 32 (fp32), m > 256, misaligned pointer */
+  BO_ERR_UNSUPPORTED = 3,  /* dtype / mode / init not built */
+  BO_ERR_CUDA = 4,         /* a CUDA runtime / driver call failed (message in bo_last_error) */
+  BO_ERR_NCCL = 5,         /* reserved for the expert-parallel path */
+  BO_ERR_WORKSPACE = 6     /* workspace null or smaller than bo_workspace_size() */
+} bo_status;
+
+typedef enum { BO_BF16 = 0, BO_FP32 = 1 } bo_dtype;
+
+/* Alg. 1 `use_full_brownout`: PARTIAL delegates S2 experts'
+ * tokens to united experts; FULL ignores them.  Ratio 0 is
+ * zero-brownout in either mode. */
+typedef enum { BO_PARTIAL = 0, BO_FULL = 1 } bo_mode;
+
+/* United-expert initialisation (reading D14): element-wise mean of
+ * the group's member weights, computed in fp64 and rounded once (RNE). */
+typedef enum { BO_UNITED_MEAN = 0 } bo_united_init;
+
+typedef struct {
+  int32_t hidden;        /* d   */
+  int32_t ffn;           /* f   */
+  int32_t num_experts;   /* m   (<= 256) */
+  int32_t top_k;         /* K   (1 <= K <= min(m, 16)) */
+  int32_t way;           /* k of the paper: experts per united group, G = ceil(m / way) */
+  int32_t dtype;         /* bo_dtype */
+  int32_t add_residual;  /* 1: h_t = x_t + ... (Eq. 5 first term); 0: omit x_t (parity, reading D12) */
+  int32_t reserved;
+  int64_t max_tokens;    /* largest T a forward will be called with */
+} bo_config;
+
+/* Plan statistics (int64 each, written by the device into the workspace). */
+typedef struct {
+  int64_t executors_accessed;  /* executors with >= 1 row ("access 5 experts") */
+  int64_t n_s1;                /* |S1| */
+  int64_t n_united;            /* united executors used (groups with >= 2 S2 members) */
+  int64_t n_singleton;         /* S2 experts kept original by the special case */
+  int64_t rows_original;       /* rows processed by original experts */
+  int64_t rows_united;         /* rows processed by united experts */
+  int64_t rows_dropped;        /* rows ignored (BO_FULL only) */
+  int64_t rows_total;          /* S = T*K */
+} bo_plan_stats;
+
+/* Byte offsets of the arrays inside a workspace sized for T tokens.  Every
+ * array is 256-byte aligned.  Index arrays are exported for parity tests. */
+typedef struct {
+  size_t total_bytes;
+  size_t logits;          /* float [T, m]       router logits (Eq. 8)                    */
+  size_t topk_id;         /* int32 [T, K]       selected experts, logit desc / id asc   */
+  size_t topk_w;          /* float [T, K]       gate weights g (Eq. 7)                  */
+  size_t tile_cnt;        /* int32 [ntiles, m]  per-tile expert histogram              */
+  size_t tile_base;       /* int32 [ntiles, m]  exclusive prefix of tile_cnt over tiles */
+  size_t counts;          /* int32 [m]          cnt_i of Alg. 1                          */
+  size_t exec_of_expert;  /* int32 [m]          executor of expert (-1 inactive, -2 dropped) */
+  size_t expert_row_off;  /* int32 [m]          first row of expert's tokens (-1 if none) */
+  size_t exec_off;        /* int32 [E+1]        first row of each executor              */
+  size_t mtile_off;       /* int32 [E+1]        prefix of ceil(rows/128) per executor    */
+  size_t stats;           /* bo_plan_stats                                              */
+  size_t row_of;          /* int32 [T*K]        row of assignment (t,s), -1 if dropped  */
+  size_t row_tok;         /* int32 [T*K]        token of each row (first R entries)     */
+  size_t row_w;           /* float [T*K]        gate weight carried by each row (Eq. 6) */
+  size_t xp;              /* dtype [T*K, d]     gathered rows (concat_tokens)     */
+  size_t h;               /* dtype [T*K, f]     SwiGLU activations                      */
+  size_t yp;              /* dtype [T*K, d]     weighted executor outputs               */
+  int64_t T;              /* tokens the layout was computed for                          */
+  int64_t ntiles;         /* token tiles of the histogram (128 tokens each)              */
+  int64_t num_executors;  /* E = m + G                                                   */
+} bo_ws_layout;
+
+typedef struct bo_handle bo_handle;
+
+/* Create / destroy a layer handle.  bo_create validates the config (errors as
+ * listed in bo_status) and queries the current device; no device memory. */
+BO_API bo_status bo_create(const bo_config* cfg, bo_handle** out);
+BO_API bo_status bo_destroy(bo_handle* h);
+
+/* Workspace needed for a forward over T tokens (T <= max_tokens). */
+BO_API bo_status bo_workspace_size(const bo_handle* h, int64_t T, size_t* bytes);
+BO_API bo_status bo_workspace_layout(const bo_handle* h, int64_t T, bo_ws_layout* out);
+
+/* United experts from the original experts (D14, grouping P:149/P:154-155):
+ *   Wg, Wu [m, f, d], Wd [m, d, f]  ->  UWg, UWu [G, f, d], UWd [G, d, f],
+ * UW*[j] = mean over experts e in [j*way, min((j+1)*way, m)) of W*[e]
+ * (fp64 sum in ascending member order, divide, round once to the dtype, RNE).
+ * Runs once per layer; not part of the timed forward. */
+BO_API bo_status bo_build_united(bo_handle* h, const void* Wg, const void* Wu, const void* Wd,
+                          int32_t init, void* UWg, void* UWu, void* UWd, void* stream);
+
+/* The brownout knob: ratio = 1 - threshold, in [0, 1].
+ * Host state only; snapshotted by the next forward (may change every
+ * iteration).  mode is a bo_mode. */
+BO_API bo_status bo_set_brownout(bo_handle* h, double ratio, int32_t mode);
+BO_API bo_status bo_get_brownout(const bo_handle* h, double* ratio, int32_t* mode);
+
+/* moe_forward(tokens, router, experts, united) (B:5):
+ *   x   [T, d]       tokens
+ *   Wr  [m, d]       router centroids e_i (Eq. 8)
+ *   Wg, Wu [m, f, d], Wd [m, d, f]   original experts (nn.Linear [out, in])
+ *   UWg, UWu [G, f, d], UWd [G, d, f] united experts (may be NULL only if the
+ *                    plan never selects a united executor, e.g. ratio 0)
+ *   y   [T, d]       output h_t of Eq. 5 (written, never read)
+ *   workspace        >= bo_workspace_size(T) bytes, 256-byte aligned
+ * T = 0 is a no-op.  T > max_tokens -> BO_ERR_INVALID_ARG. */
+BO_API bo_status bo_moe_forward(bo_handle* h, const void* x, int64_t T, const void* Wr,
+                         const void* Wg, const void* Wu, const void* Wd,
+                         const void* UWg, const void* UWu, const void* UWd,
+                         void* y, void* workspace, size_t ws_bytes, void* stream);
+
+/* Parity / debug variant.  If logits_in (device, fp32 [T, m]) is non-NULL the
+ * router GEMM is skipped and these logits are routed instead ("given
+ * identical fp32 logits", B:5).  All intermediate arrays stay readable in the
+ * workspace at the offsets of bo_workspace_layout(T). */
+BO_API bo_status bo_moe_forward_ex(bo_handle* h, const void* x, int64_t T, const void* Wr,
+                            const void* Wg, const void* Wu, const void* Wd,
+                            const void* UWg, const void* UWu, const void* UWd,
+                            void* y, void* workspace, size_t ws_bytes,
+                            const float* logits_in, void* stream);
+
+/* Alg. 1 alone on given per-expert counts (device int32 [m]) with the
+ * handle's ratio/mode/way (parity entry for the plan).  Outputs (device):
+ * exec_of_expert [m], expert_row_off [m], stats (bo_plan_stats, device) and
+ * exec_off, a buffer of at least 2*(E+1) + m int32 whose first E+1 entries
+ * receive the executor row offsets (the rest is scratch). */
+BO_API bo_status bo_plan_from_counts(bo_handle* h, const int32_t* counts, int32_t* exec_of_expert,
+                              int32_t* expert_row_off, int32_t* exec_off, void* stats,
+                              void* stream);
+
+/* Number of GPU kernels the last forward on this handle enqueued. */
+BO_API int32_t bo_last_launch_count(const bo_handle* h);
+
+BO_API const char* bo_status_string(bo_status s);
+BO_API const char* bo_last_error(void);
+BO_API const char* bo_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BROWNOUT_H_ */

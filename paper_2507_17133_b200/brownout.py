@@ -1,0 +1,234 @@
+"""ctypes binding of libbrownout.so (include/brownout.h).
+
+Argument marshalling only: every step of the forward runs in the library's
+CUDA kernels.  torch is used for device memory and streams.  If the shared
+library is missing or fails to load, importing this module raises: there is
+no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbrownout.so")
+
+BO_OK, BO_ERR_INVALID_ARG, BO_ERR_SHAPE, BO_ERR_UNSUPPORTED, BO_ERR_CUDA, BO_ERR_NCCL, BO_ERR_WORKSPACE = range(7)
+BO_BF16, BO_FP32 = 0, 1
+BO_PARTIAL, BO_FULL = 0, 1
+BO_UNITED_MEAN = 0
+
+EXPORTED = (
+    "bo_create", "bo_destroy", "bo_workspace_size", "bo_workspace_layout", "bo_build_united",
+    "bo_set_brownout", "bo_get_brownout", "bo_moe_forward", "bo_moe_forward_ex", "bo_plan_from_counts",
+    "bo_last_launch_count", "bo_status_string", "bo_last_error", "bo_version",
+)
+
+
+class bo_config(C.Structure):
+    _fields_ = [("hidden", C.c_int32), ("ffn", C.c_int32), ("num_experts", C.c_int32), ("top_k", C.c_int32),
+                ("way", C.c_int32), ("dtype", C.c_int32), ("add_residual", C.c_int32), ("reserved", C.c_int32),
+                ("max_tokens", C.c_int64)]
+
+
+class bo_plan_stats(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("executors_accessed", "n_s1", "n_united", "n_singleton",
+                                         "rows_original", "rows_united", "rows_dropped", "rows_total")]
+
+
+STATS_FIELDS = [f[0] for f in bo_plan_stats._fields_]
+
+
+class bo_ws_layout(C.Structure):
+    _fields_ = [(n, C.c_size_t) for n in ("total_bytes", "logits", "topk_id", "topk_w", "tile_cnt", "tile_base",
+                                          "counts", "exec_of_expert", "expert_row_off", "exec_off", "mtile_off",
+                                          "stats", "row_of", "row_tok", "row_w", "xp", "h", "yp")] + \
+               [("T", C.c_int64), ("ntiles", C.c_int64), ("num_executors", C.c_int64)]
+
+
+class BrownoutError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{msg} (status {status})")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run paper_2507_17133_b200.build.build() "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    vp, i64, i32 = C.c_void_p, C.c_int64, C.c_int32
+    sig = {
+        "bo_create": ([C.POINTER(bo_config), C.POINTER(vp)], C.c_int),
+        "bo_destroy": ([vp], C.c_int),
+        "bo_workspace_size": ([vp, i64, C.POINTER(C.c_size_t)], C.c_int),
+        "bo_workspace_layout": ([vp, i64, C.POINTER(bo_ws_layout)], C.c_int),
+        "bo_build_united": ([vp, vp, vp, vp, i32, vp, vp, vp, vp], C.c_int),
+        "bo_set_brownout": ([vp, C.c_double, i32], C.c_int),
+        "bo_get_brownout": ([vp, C.POINTER(C.c_double), C.POINTER(i32)], C.c_int),
+        "bo_moe_forward": ([vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp], C.c_int),
+        "bo_moe_forward_ex": ([vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp, vp], C.c_int),
+        "bo_plan_from_counts": ([vp, vp, vp, vp, vp, vp, vp], C.c_int),
+        "bo_last_launch_count": ([vp], i32),
+        "bo_status_string": ([C.c_int], C.c_char_p),
+        "bo_last_error": ([], C.c_char_p),
+        "bo_version": ([], C.c_char_p),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    return lib
+
+
+_lib = _load()
+
+
+def lib():
+    return _lib
+
+
+def _check(status: int):
+    if status != BO_OK:
+        raise BrownoutError(status, f"{_lib.bo_status_string(status).decode()}: {_lib.bo_last_error().decode()}")
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+_TORCH_DTYPE = {BO_BF16: torch.bfloat16, BO_FP32: torch.float32}
+
+
+class BrownoutMoE:
+    """One MoE layer handle: bo_create / bo_set_brownout / bo_moe_forward."""
+
+    def __init__(self, hidden, ffn, num_experts, top_k, way, dtype="bf16", add_residual=False,
+                 max_tokens=16384):
+        self.cfg = bo_config(hidden=hidden, ffn=ffn, num_experts=num_experts, top_k=top_k, way=way,
+                             dtype=BO_BF16 if dtype in ("bf16", torch.bfloat16) else BO_FP32,
+                             add_residual=1 if add_residual else 0, reserved=0, max_tokens=max_tokens)
+        h = C.c_void_p()
+        _check(_lib.bo_create(C.byref(self.cfg), C.byref(h)))
+        self._h = h
+        self.torch_dtype = _TORCH_DTYPE[self.cfg.dtype]
+        self.G = -(-num_experts // way)
+        self.E = num_experts + self.G
+        self._ws = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib.bo_destroy(h)
+            self._h = None
+
+    # -- knob ------------------------------------------------------------
+    def set_brownout(self, ratio: float, mode: str = "partial"):
+        _check(_lib.bo_set_brownout(self._h, float(ratio), BO_FULL if mode == "full" else BO_PARTIAL))
+
+    def get_brownout(self):
+        r, m = C.c_double(), C.c_int32()
+        _check(_lib.bo_get_brownout(self._h, C.byref(r), C.byref(m)))
+        return r.value, ("full" if m.value == BO_FULL else "partial")
+
+    # -- workspace -------------------------------------------------------
+    def workspace_size(self, T: int) -> int:
+        n = C.c_size_t()
+        _check(_lib.bo_workspace_size(self._h, int(T), C.byref(n)))
+        return n.value
+
+    def workspace_layout(self, T: int) -> bo_ws_layout:
+        L = bo_ws_layout()
+        _check(_lib.bo_workspace_layout(self._h, int(T), C.byref(L)))
+        return L
+
+    def workspace(self, T: int, device="cuda") -> torch.Tensor:
+        need = self.workspace_size(T)
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=device)
+        return self._ws
+
+    # -- calls -----------------------------------------------------------
+    def build_united(self, Wg, Wu, Wd, stream=None):
+        m, f, d = Wg.shape
+        G = self.G
+        UWg = torch.empty(G, f, d, dtype=Wg.dtype, device=Wg.device)
+        UWu = torch.empty(G, f, d, dtype=Wu.dtype, device=Wu.device)
+        UWd = torch.empty(G, d, f, dtype=Wd.dtype, device=Wd.device)
+        _check(_lib.bo_build_united(self._h, _ptr(Wg), _ptr(Wu), _ptr(Wd), BO_UNITED_MEAN, _ptr(UWg), _ptr(UWu),
+                                    _ptr(UWd), _stream(stream)))
+        return UWg, UWu, UWd
+
+    def forward(self, x, Wr, experts, united, y=None, workspace=None, logits=None, stream=None):
+        """moe_forward(tokens, router, experts, united) -> y [T, d]."""
+        T = x.shape[0]
+        Wg, Wu, Wd = experts
+        UWg, UWu, UWd = united if united is not None else (None, None, None)
+        if y is None:
+            y = torch.empty_like(x)
+        ws = workspace if workspace is not None else self.workspace(T, x.device)
+        if logits is None:
+            _check(_lib.bo_moe_forward(self._h, _ptr(x), T, _ptr(Wr), _ptr(Wg), _ptr(Wu), _ptr(Wd), _ptr(UWg),
+                                       _ptr(UWu), _ptr(UWd), _ptr(y), _ptr(ws), ws.numel(), _stream(stream)))
+        else:
+            _check(_lib.bo_moe_forward_ex(self._h, _ptr(x), T, _ptr(Wr), _ptr(Wg), _ptr(Wu), _ptr(Wd), _ptr(UWg),
+                                          _ptr(UWu), _ptr(UWd), _ptr(y), _ptr(ws), ws.numel(), _ptr(logits),
+                                          _stream(stream)))
+        return y
+
+    def last_launch_count(self) -> int:
+        return int(_lib.bo_last_launch_count(self._h))
+
+    def debug_arrays(self, T: int, workspace=None) -> dict:
+        """Views of the workspace arrays of the last forward over T tokens."""
+        ws = self._ws if workspace is None else workspace
+        L = self.workspace_layout(T)
+        m, K = self.cfg.num_experts, self.cfg.top_k
+        d, f = self.cfg.hidden, self.cfg.ffn
+        E = int(L.num_executors)
+        R = T * K
+        eb = 2 if self.cfg.dtype == BO_BF16 else 4
+
+        def view(off, n, dt):
+            nbytes = n * torch.tensor([], dtype=dt).element_size()
+            return ws[off:off + nbytes].view(dt)
+
+        out = {
+            "logits": view(L.logits, T * m, torch.float32).view(T, m),
+            "topk_id": view(L.topk_id, R, torch.int32).view(T, K),
+            "topk_w": view(L.topk_w, R, torch.float32).view(T, K),
+            "counts": view(L.counts, m, torch.int32),
+            "exec_of_expert": view(L.exec_of_expert, m, torch.int32),
+            "expert_row_off": view(L.expert_row_off, m, torch.int32),
+            "exec_off": view(L.exec_off, E + 1, torch.int32),
+            "mtile_off": view(L.mtile_off, E + 1, torch.int32),
+            "stats": view(L.stats, 8, torch.int64),
+            "row_of": view(L.row_of, R, torch.int32),
+            "row_tok": view(L.row_tok, R, torch.int32),
+            "row_w": view(L.row_w, R, torch.float32),
+            "xp": view(L.xp, R * d, self.torch_dtype).view(R, d),
+            "h": view(L.h, R * f, self.torch_dtype).view(R, f),
+            "yp": view(L.yp, R * d, self.torch_dtype).view(R, d),
+        }
+        del eb
+        return out
+
+    def plan_from_counts(self, counts: torch.Tensor, stream=None):
+        """Alg. 1 on device counts (int32 [m]) -> dict of device tensors."""
+        m = self.cfg.num_experts
+        dev = counts.device
+        exec_of = torch.empty(m, dtype=torch.int32, device=dev)
+        erow = torch.empty(m, dtype=torch.int32, device=dev)
+        eoff = torch.empty(2 * (self.E + 1) + m, dtype=torch.int32, device=dev)
+        stats = torch.empty(8, dtype=torch.int64, device=dev)
+        _check(_lib.bo_plan_from_counts(self._h, _ptr(counts), _ptr(exec_of), _ptr(erow), _ptr(eoff), _ptr(stats),
+                                        _stream(stream)))
+        return {"exec_of_expert": exec_of, "expert_row_off": erow, "exec_off": eoff[:self.E + 1], "stats": stats}

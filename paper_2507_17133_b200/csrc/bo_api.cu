@@ -1,0 +1,424 @@
+// bo_api.cu - the C ABI (include/brownout.h): validation, workspace carving,
+// TMA descriptor encoding and the stream-ordered launch sequence of the
+// brownout MoE-layer forward.  No device memory is allocated here.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <cstdarg>
+#include <mutex>
+#include <string>
+
+#include "../../include/brownout.h"
+#include "bo_kernels.h"
+
+struct bo_handle {
+  bo_config cfg;
+  double ratio;
+  int32_t mode;
+  int num_sms;
+  int device;
+  int32_t last_launches;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+bo_status fail(bo_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return s;
+}
+
+bo_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(BO_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+#define BO_CUDA(call, what)                 \
+  do {                                      \
+    cudaError_t e_ = (call);                \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
+
+int elem_bytes(int32_t dtype) { return dtype == BO_BF16 ? 2 : 4; }
+
+// ---- TMA descriptor encoding through the driver entry point (no -lcuda)
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled get_encode() {
+  static PFN_encodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled>(p);
+  });
+  return fn;
+}
+
+// 2-D K-major tile map over a row-major [rows, k] matrix: box [box_rows, 128 B], SWIZZLE_128B.
+bo_status make_map(CUtensorMap* m, const void* base, int32_t dtype, uint64_t rows, uint64_t k, uint32_t box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return fail(BO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const int eb = elem_bytes(dtype);
+  cuuint64_t dims[2] = {k, rows};
+  cuuint64_t strides[1] = {k * static_cast<cuuint64_t>(eb)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / eb), box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, dtype == BO_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(BO_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) rows=%llu k=%llu box_rows=%u", static_cast<int>(r),
+                static_cast<unsigned long long>(rows), static_cast<unsigned long long>(k), box_rows);
+  return BO_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int router_bn(int m) {
+  int bn = 16;
+  while (bn < m) bn <<= 1;
+  return bn;
+}
+
+int gemm2_bn(int d) { return d % 256 == 0 ? 256 : d % 128 == 0 ? 128 : 64; }
+int gemm1_bn(int f) { return f % 128 == 0 ? 256 : 128; }   // gate + up columns
+
+bo_status compute_layout(const bo_handle* h, int64_t T, bo_ws_layout* L) {
+  const bo_config& c = h->cfg;
+  const int64_t m = c.num_experts, K = c.top_k, d = c.hidden, f = c.ffn;
+  const int64_t G = (m + c.way - 1) / c.way, E = m + G;
+  const int64_t ntiles = (T + bo::kTileTok - 1) / bo::kTileTok;
+  const int64_t R = T * K;
+  const int eb = elem_bytes(c.dtype);
+  memset(L, 0, sizeof(*L));
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = align256(off + (bytes ? bytes : 1));
+    return o;
+  };
+  L->logits = take(sizeof(float) * T * m);
+  L->topk_id = take(sizeof(int32_t) * R);
+  L->topk_w = take(sizeof(float) * R);
+  L->tile_cnt = take(sizeof(int32_t) * ntiles * m);
+  L->tile_base = take(sizeof(int32_t) * ntiles * m);
+  L->counts = take(sizeof(int32_t) * m);
+  L->exec_of_expert = take(sizeof(int32_t) * m);
+  L->expert_row_off = take(sizeof(int32_t) * m);
+  L->exec_off = take(sizeof(int32_t) * (E + 1));
+  L->mtile_off = take(sizeof(int32_t) * (E + 1));
+  L->stats = take(sizeof(bo_plan_stats));
+  L->row_of = take(sizeof(int32_t) * R);
+  L->row_tok = take(sizeof(int32_t) * R);
+  L->row_w = take(sizeof(float) * R);
+  L->xp = take(static_cast<size_t>(eb) * R * d);
+  L->h = take(static_cast<size_t>(eb) * R * f);
+  L->yp = take(static_cast<size_t>(eb) * R * d);
+  L->total_bytes = off;
+  L->T = T;
+  L->ntiles = ntiles;
+  L->num_executors = E;
+  return BO_OK;
+}
+
+template <typename P>
+P* at(void* ws, size_t off) {
+  return reinterpret_cast<P*>(static_cast<char*>(ws) + off);
+}
+
+bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, const void* Wg, const void* Wu,
+                       const void* Wd, const void* UWg, const void* UWu, const void* UWd, void* y, void* ws,
+                       size_t ws_bytes, const float* logits_in, void* stream) {
+  if (!h) return fail(BO_ERR_INVALID_ARG, "null handle");
+  h->last_launches = 0;
+  const bo_config& c = h->cfg;
+  if (T < 0 || T > c.max_tokens) return fail(BO_ERR_INVALID_ARG, "T=%lld outside [0, max_tokens=%lld]",
+                                             static_cast<long long>(T), static_cast<long long>(c.max_tokens));
+  if (T == 0) return BO_OK;
+  if (!x || !Wg || !Wu || !Wd || !y || (!Wr && !logits_in))
+    return fail(BO_ERR_INVALID_ARG, "null tensor pointer");
+  const bool may_use_united = h->mode == BO_PARTIAL && h->ratio > 0.0;
+  if (may_use_united && (!UWg || !UWu || !UWd))
+    return fail(BO_ERR_INVALID_ARG, "united weights are required when ratio > 0 in partial mode");
+  if (!UWg) { UWg = Wg; UWu = Wu; UWd = Wd; }   // never selected by the plan (ratio 0 or full mode)
+  const void* ptrs[] = {x, Wr ? Wr : x, Wg, Wu, Wd, UWg, UWu, UWd, y, ws};
+  for (const void* p : ptrs)
+    if (!aligned16(p)) return fail(BO_ERR_SHAPE, "tensor pointers must be 16-byte aligned");
+  bo_ws_layout L;
+  compute_layout(h, T, &L);
+  if (!ws || ws_bytes < L.total_bytes)
+    return fail(BO_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, L.total_bytes);
+
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int dt = c.dtype == BO_BF16 ? 0 : 1;
+  const int m = c.num_experts, K = c.top_k, d = c.hidden, f = c.ffn;
+  const int G = (m + c.way - 1) / c.way, E = m + G;
+  const int64_t R = T * K;
+  const int ntiles = static_cast<int>(L.ntiles);
+  int launches = 0;
+
+  float* logits = at<float>(ws, L.logits);
+  int32_t* topk_id = at<int32_t>(ws, L.topk_id);
+  float* topk_w = at<float>(ws, L.topk_w);
+  int32_t* tile_cnt = at<int32_t>(ws, L.tile_cnt);
+  int32_t* tile_base = at<int32_t>(ws, L.tile_base);
+  int32_t* counts = at<int32_t>(ws, L.counts);
+  int32_t* exec_of = at<int32_t>(ws, L.exec_of_expert);
+  int32_t* erow = at<int32_t>(ws, L.expert_row_off);
+  int32_t* exec_off = at<int32_t>(ws, L.exec_off);
+  int32_t* mtile_off = at<int32_t>(ws, L.mtile_off);
+  int64_t* stats = at<int64_t>(ws, L.stats);
+  int32_t* row_of = at<int32_t>(ws, L.row_of);
+  int32_t* row_tok = at<int32_t>(ws, L.row_tok);
+  float* row_w = at<float>(ws, L.row_w);
+  void* xp = at<char>(ws, L.xp);
+  void* hb = at<char>(ws, L.h);
+  void* yp = at<char>(ws, L.yp);
+  bo_status st;
+
+  // 1. router logits, Eq. 8 (tcgen05 GEMM, fp32 out) -- or injected logits
+  const float* L_use = logits_in;
+  if (!logits_in) {
+    CUtensorMap mA, mB;
+    const int bn = router_bn(m);
+    if ((st = make_map(&mA, x, c.dtype, T, d, bo::kBM)) != BO_OK) return st;
+    if ((st = make_map(&mB, Wr, c.dtype, m, d, bn)) != BO_OK) return st;
+    bo::GemmParams p{};
+    p.Kdim = d;
+    p.n_tiles = 1;
+    p.ldo = m;
+    p.n_valid = m;
+    p.m_orig = 1;
+    p.b_rows_per_exec = 0;
+    p.num_exec = 1;
+    p.single_rows = static_cast<int>(T);
+    p.out = logits;
+    const int work = static_cast<int>((T + bo::kBM - 1) / bo::kBM);
+    const int grid = work < h->num_sms ? work : h->num_sms;
+    BO_CUDA(bo::launch_grouped_gemm(dt, bo::EPI_F32OUT, bn, mA, mB, mB, mB, mB, p, grid, s), "router gemm");
+    ++launches;
+    L_use = logits;
+  }
+  // 2. top-K + softmax (Eq. 7) + per-tile histogram
+  BO_CUDA(bo::launch_topk_hist(L_use, static_cast<int>(T), m, K, topk_id, topk_w, tile_cnt, s), "topk");
+  ++launches;
+  // 3. Algorithm 1 plan (snapshot of the knob at enqueue time)
+  BO_CUDA(bo::launch_plan(tile_cnt, ntiles, m, c.way, h->ratio, h->mode, tile_base, counts, exec_of, erow,
+                          exec_off, mtile_off, stats, s),
+          "plan");
+  ++launches;
+  // 4. permutation (rows) and gather (Xp)
+  BO_CUDA(bo::launch_permute(topk_id, topk_w, static_cast<int>(T), K, m, tile_base, exec_of, erow, row_of,
+                             row_tok, row_w, s),
+          "permute");
+  ++launches;
+  BO_CUDA(bo::launch_gather(dt, x, static_cast<int>(T), d, K, row_of, xp, h->num_sms, s), "gather");
+  ++launches;
+  // 5. GEMM1 + SwiGLU over executors
+  {
+    const int bn = gemm1_bn(f);
+    CUtensorMap mA, mG, mU, mUG, mUU;
+    if ((st = make_map(&mA, xp, c.dtype, R, d, bo::kBM)) != BO_OK) return st;
+    if ((st = make_map(&mG, Wg, c.dtype, static_cast<uint64_t>(m) * f, d, bn / 2)) != BO_OK) return st;
+    if ((st = make_map(&mU, Wu, c.dtype, static_cast<uint64_t>(m) * f, d, bn / 2)) != BO_OK) return st;
+    const uint64_t urows = UWg == Wg ? static_cast<uint64_t>(m) * f : static_cast<uint64_t>(G) * f;
+    if ((st = make_map(&mUG, UWg, c.dtype, urows, d, bn / 2)) != BO_OK) return st;
+    if ((st = make_map(&mUU, UWu, c.dtype, urows, d, bn / 2)) != BO_OK) return st;
+    bo::GemmParams p{};
+    p.Kdim = d;
+    p.n_tiles = f / (bn / 2);
+    p.ldo = f;
+    p.n_valid = f;
+    p.m_orig = m;
+    p.b_rows_per_exec = f;
+    p.num_exec = E;
+    p.single_rows = -1;
+    p.exec_off = exec_off;
+    p.mtile_off = mtile_off;
+    p.out = hb;
+    const int64_t max_work = ((R + bo::kBM - 1) / bo::kBM + E) * p.n_tiles;
+    const int grid = static_cast<int>(max_work < h->num_sms ? max_work : h->num_sms);
+    BO_CUDA(bo::launch_grouped_gemm(dt, bo::EPI_SWIGLU, bn, mA, mG, mU, mUG, mUU, p, grid, s), "gemm1");
+    ++launches;
+  }
+  // 6. GEMM2, rows scaled by their gate weight (Eq. 6)
+  {
+    const int bn = gemm2_bn(d);
+    CUtensorMap mA, mD, mUD;
+    if ((st = make_map(&mA, hb, c.dtype, R, f, bo::kBM)) != BO_OK) return st;
+    if ((st = make_map(&mD, Wd, c.dtype, static_cast<uint64_t>(m) * d, f, bn)) != BO_OK) return st;
+    const uint64_t urows = UWd == Wd ? static_cast<uint64_t>(m) * d : static_cast<uint64_t>(G) * d;
+    if ((st = make_map(&mUD, UWd, c.dtype, urows, f, bn)) != BO_OK) return st;
+    bo::GemmParams p{};
+    p.Kdim = f;
+    p.n_tiles = d / bn;
+    p.ldo = d;
+    p.n_valid = d;
+    p.m_orig = m;
+    p.b_rows_per_exec = d;
+    p.num_exec = E;
+    p.single_rows = -1;
+    p.exec_off = exec_off;
+    p.mtile_off = mtile_off;
+    p.out = yp;
+    p.row_w = row_w;
+    const int64_t max_work = ((R + bo::kBM - 1) / bo::kBM + E) * p.n_tiles;
+    const int grid = static_cast<int>(max_work < h->num_sms ? max_work : h->num_sms);
+    BO_CUDA(bo::launch_grouped_gemm(dt, bo::EPI_WEIGHTED, bn, mA, mD, mD, mUD, mUD, p, grid, s), "gemm2");
+    ++launches;
+  }
+  // 7. combine (Eq. 5 sum over the token's K slots)
+  BO_CUDA(bo::launch_combine(dt, yp, x, static_cast<int>(T), d, K, row_of, c.add_residual, y, h->num_sms, s),
+          "combine");
+  ++launches;
+  h->last_launches = launches;
+  return BO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bo_version(void) { return "brownout-b200 0.1 (sm_100a)"; }
+
+const char* bo_status_string(bo_status s) {
+  switch (s) {
+    case BO_OK: return "BO_OK";
+    case BO_ERR_INVALID_ARG: return "BO_ERR_INVALID_ARG";
+    case BO_ERR_SHAPE: return "BO_ERR_SHAPE";
+    case BO_ERR_UNSUPPORTED: return "BO_ERR_UNSUPPORTED";
+    case BO_ERR_CUDA: return "BO_ERR_CUDA";
+    case BO_ERR_NCCL: return "BO_ERR_NCCL";
+    case BO_ERR_WORKSPACE: return "BO_ERR_WORKSPACE";
+  }
+  return "BO_ERR_UNKNOWN";
+}
+
+const char* bo_last_error(void) { return g_last_error.c_str(); }
+
+bo_status bo_create(const bo_config* cfg, bo_handle** out) {
+  if (!cfg || !out) return fail(BO_ERR_INVALID_ARG, "null argument");
+  *out = nullptr;
+  const bo_config& c = *cfg;
+  if (c.dtype != BO_BF16 && c.dtype != BO_FP32) return fail(BO_ERR_UNSUPPORTED, "dtype %d not built", c.dtype);
+  if (c.num_experts < 1 || c.num_experts > bo::kMaxExperts)
+    return fail(BO_ERR_SHAPE, "num_experts=%d outside [1, %d]", c.num_experts, bo::kMaxExperts);
+  const int kmax = c.num_experts < 16 ? c.num_experts : 16;
+  if (c.top_k < 1 || c.top_k > kmax) return fail(BO_ERR_INVALID_ARG, "top_k=%d outside [1, %d]", c.top_k, kmax);
+  if (c.way < 1) return fail(BO_ERR_INVALID_ARG, "way=%d < 1", c.way);
+  const int mult = c.dtype == BO_BF16 ? 64 : 32;
+  if (c.hidden <= 0 || c.hidden % mult || c.ffn <= 0 || c.ffn % mult)
+    return fail(BO_ERR_SHAPE, "hidden=%d / ffn=%d must be positive multiples of %d", c.hidden, c.ffn, mult);
+  if (c.ffn % 64) return fail(BO_ERR_SHAPE, "ffn=%d must be a multiple of 64", c.ffn);
+  if (c.max_tokens < 0 || c.max_tokens * c.top_k > (int64_t(1) << 31) - 1)
+    return fail(BO_ERR_INVALID_ARG, "max_tokens=%lld out of range", static_cast<long long>(c.max_tokens));
+  int dev = 0, sms = 0;
+  BO_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+  BO_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
+  bo_handle* h = new bo_handle();
+  h->cfg = c;
+  h->ratio = 0.0;
+  h->mode = BO_PARTIAL;
+  h->num_sms = sms;
+  h->device = dev;
+  h->last_launches = 0;
+  *out = h;
+  return BO_OK;
+}
+
+bo_status bo_destroy(bo_handle* h) {
+  delete h;
+  return BO_OK;
+}
+
+bo_status bo_workspace_layout(const bo_handle* h, int64_t T, bo_ws_layout* out) {
+  if (!h || !out) return fail(BO_ERR_INVALID_ARG, "null argument");
+  if (T < 0 || T > h->cfg.max_tokens) return fail(BO_ERR_INVALID_ARG, "T out of range");
+  return compute_layout(h, T, out);
+}
+
+bo_status bo_workspace_size(const bo_handle* h, int64_t T, size_t* bytes) {
+  if (!bytes) return fail(BO_ERR_INVALID_ARG, "null argument");
+  bo_ws_layout L;
+  bo_status s = bo_workspace_layout(h, T, &L);
+  if (s == BO_OK) *bytes = L.total_bytes;
+  return s;
+}
+
+bo_status bo_set_brownout(bo_handle* h, double ratio, int32_t mode) {
+  if (!h) return fail(BO_ERR_INVALID_ARG, "null handle");
+  if (!(ratio >= 0.0 && ratio <= 1.0)) return fail(BO_ERR_INVALID_ARG, "ratio %g outside [0, 1]", ratio);
+  if (mode != BO_PARTIAL && mode != BO_FULL) return fail(BO_ERR_INVALID_ARG, "mode %d invalid", mode);
+  h->ratio = ratio;
+  h->mode = mode;
+  return BO_OK;
+}
+
+bo_status bo_get_brownout(const bo_handle* h, double* ratio, int32_t* mode) {
+  if (!h || !ratio || !mode) return fail(BO_ERR_INVALID_ARG, "null argument");
+  *ratio = h->ratio;
+  *mode = h->mode;
+  return BO_OK;
+}
+
+bo_status bo_build_united(bo_handle* h, const void* Wg, const void* Wu, const void* Wd, int32_t init, void* UWg,
+                          void* UWu, void* UWd, void* stream) {
+  if (!h || !Wg || !Wu || !Wd || !UWg || !UWu || !UWd) return fail(BO_ERR_INVALID_ARG, "null argument");
+  if (init != BO_UNITED_MEAN) return fail(BO_ERR_UNSUPPORTED, "united init %d not built", init);
+  const bo_config& c = h->cfg;
+  const int dt = c.dtype == BO_BF16 ? 0 : 1;
+  const int64_t per = static_cast<int64_t>(c.ffn) * c.hidden;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  BO_CUDA(bo::launch_build_united(dt, Wg, c.num_experts, c.way, per, UWg, s), "build_united Wg");
+  BO_CUDA(bo::launch_build_united(dt, Wu, c.num_experts, c.way, per, UWu, s), "build_united Wu");
+  BO_CUDA(bo::launch_build_united(dt, Wd, c.num_experts, c.way, per, UWd, s), "build_united Wd");
+  return BO_OK;
+}
+
+bo_status bo_moe_forward(bo_handle* h, const void* x, int64_t T, const void* Wr, const void* Wg, const void* Wu,
+                         const void* Wd, const void* UWg, const void* UWu, const void* UWd, void* y,
+                         void* workspace, size_t ws_bytes, void* stream) {
+  if (!Wr) return fail(BO_ERR_INVALID_ARG, "null router");
+  return forward_impl(h, x, T, Wr, Wg, Wu, Wd, UWg, UWu, UWd, y, workspace, ws_bytes, nullptr, stream);
+}
+
+bo_status bo_moe_forward_ex(bo_handle* h, const void* x, int64_t T, const void* Wr, const void* Wg,
+                            const void* Wu, const void* Wd, const void* UWg, const void* UWu, const void* UWd,
+                            void* y, void* workspace, size_t ws_bytes, const float* logits_in, void* stream) {
+  return forward_impl(h, x, T, Wr, Wg, Wu, Wd, UWg, UWu, UWd, y, workspace, ws_bytes, logits_in, stream);
+}
+
+bo_status bo_plan_from_counts(bo_handle* h, const int32_t* counts, int32_t* exec_of_expert,
+                              int32_t* expert_row_off, int32_t* exec_off, void* stats, void* stream) {
+  if (!h || !counts || !exec_of_expert || !expert_row_off || !exec_off || !stats)
+    return fail(BO_ERR_INVALID_ARG, "null argument");
+  const bo_config& c = h->cfg;
+  const int m = c.num_experts;
+  const int E = m + (m + c.way - 1) / c.way;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int32_t* mtile_scratch = exec_off + (E + 1);   // exec_off holds 2*(E+1) + m ints (brownout.h)
+  int32_t* counts_out = mtile_scratch + (E + 1);
+  BO_CUDA(bo::launch_plan(counts, 1, m, c.way, h->ratio, h->mode, nullptr, counts_out, exec_of_expert,
+                          expert_row_off, exec_off, mtile_scratch, static_cast<int64_t*>(stats), s),
+          "plan_from_counts");
+  return BO_OK;
+}
+
+int32_t bo_last_launch_count(const bo_handle* h) { return h ? h->last_launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,343 @@
+// bo_gemm.cu - persistent, warp-specialised grouped GEMM on tcgen05 / TMEM / TMA.
+//
+// One engine serves the three dense contractions of the brownout MoE forward:
+//   router   (Eq. 8):  logits[T, m]  = x  Wr^T                (EPI_F32OUT)
+//   GEMM1    (Eq. 5 FFN, SwiGLU, D13): H[r] = silu(Xp[r] Wg_x^T) * (Xp[r] Wu_x^T)  (EPI_SWIGLU)
+//   GEMM2    (Eq. 5-6):       Yp[r] = row_w[r] * (H[r] Wd_x^T)          (EPI_WEIGHTED)
+// where x is the executor (original expert or united expert, Alg. 1)
+// that owns row r.  Executor row ranges come from the device-side plan
+// (exec_off / mtile_off), so no host synchronisation is needed.
+//
+// CTA layout (192 threads, 1 CTA per SM, persistent over a static round-robin
+// work list):
+//   warp 0      TMA producer: A tile [128 x BK] + B tile [BN x BK] per stage
+//   warp 1      MMA issuer: tcgen05.mma.cta_group::1 M=128 N=BN K=16(bf16)/8(tf32)
+//               into a double-buffered TMEM accumulator (2 x BN fp32 columns)
+//   warps 2-5   epilogue: tcgen05.ld 32x32b -> registers -> fused op -> global
+// Work item w -> (executor x, n-tile, m-tile) with the m-tile fastest, so
+// concurrently running CTAs share the same weight tile (B) through L2.
+#include "bo_kernels.h"
+#include "bo_ptx.cuh"
+
+namespace bo {
+
+template <int BN, int EPI>
+struct GemmShape {
+  static constexpr int kTmemCols = (2 * BN + (BN < 32 ? 32 : 0)) <= 32    ? 32
+                                   : (2 * BN + (BN < 32 ? 32 : 0)) <= 64  ? 64
+                                   : (2 * BN + (BN < 32 ? 32 : 0)) <= 128 ? 128
+                                   : (2 * BN + (BN < 32 ? 32 : 0)) <= 256 ? 256
+                                                                          : 512;
+};
+
+template <typename T, int BN>
+struct GemmCfg {
+  static constexpr int BM = kBM;
+  static constexpr int BK = 128 / (int)sizeof(T);       // one 128-byte swizzle row
+  static constexpr int UK = 32 / (int)sizeof(T);        // MMA K per instruction
+  static constexpr int A_BYTES = BM * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int BAR_BYTES = 1024;                 // barriers + tmem slot
+  static constexpr int SCHED_BYTES = 2 * (kMaxExec + 1) * 4;
+  static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE_BYTES + BAR_BYTES + SCHED_BYTES;
+};
+
+__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+
+template <typename T>
+__device__ __forceinline__ void store_row32(T* dst, const float (&v)[32]);
+
+template <>
+__device__ __forceinline__ void store_row32<__nv_bfloat16>(__nv_bfloat16* dst, const float (&v)[32]) {
+  uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 u;
+    u.x = pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+    u.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+    u.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+    u.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+    d[q] = u;
+  }
+}
+template <>
+__device__ __forceinline__ void store_row32<float>(float* dst, const float (&v)[32]) {
+  float4* d = reinterpret_cast<float4*>(dst);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) d[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+}
+
+template <typename T, int BN, int EPI>
+__global__ void __launch_bounds__(192, 1)
+    k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
+                   const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmB2,
+                   const __grid_constant__ CUtensorMap tmB3, const GemmParams p) {
+  using C = GemmCfg<T, BN>;
+  constexpr int STAGES = C::STAGES;
+  constexpr int TMEM_COLS = GemmShape<BN, EPI>::kTmemCols;
+  constexpr uint32_t IDESC = idesc_f32acc<T>(128, BN);
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  int* s_mtile = reinterpret_cast<int*>(smem + STAGES * C::STAGE_BYTES + C::BAR_BYTES);
+  int* s_eoff = s_mtile + (kMaxExec + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB0);
+    tma_prefetch_desc(&tmB1);
+    tma_prefetch_desc(&tmB2);
+    tma_prefetch_desc(&tmB3);
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, TMEM_COLS);
+    tmem_relinquish();
+  }
+  const int nexec = p.single_rows >= 0 ? 1 : p.num_exec;
+  if (p.single_rows >= 0) {
+    if (threadIdx.x == 0) {
+      s_mtile[0] = 0;
+      s_mtile[1] = (p.single_rows + kBM - 1) / kBM;
+      s_eoff[0] = 0;
+      s_eoff[1] = p.single_rows;
+    }
+  } else {
+    for (int i = threadIdx.x; i <= nexec; i += blockDim.x) {
+      s_mtile[i] = p.mtile_off[i];
+      s_eoff[i] = p.exec_off[i];
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int n_tiles = p.n_tiles;
+  const int total_work = s_mtile[nexec] * n_tiles;
+  const int num_kb = p.Kdim / C::BK;
+
+  // work item -> (executor, m-tile inside executor, n-tile)
+  auto decode = [&](int w, int& x, int& mi, int& n) {
+    int lo = 0, hi = nexec;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (s_mtile[mid] * n_tiles <= w) lo = mid; else hi = mid;
+    }
+    x = lo;
+    const int mt = s_mtile[x + 1] - s_mtile[x];
+    const int local = w - s_mtile[x] * n_tiles;
+    n = local / mt;
+    mi = local - n * mt;
+  };
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      const uint64_t pol_a = policy_evict_last();   // activations are re-read per n-tile
+      const uint64_t pol_b = policy_evict_first();  // weights stream through once per m-tile group
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
+        int x, mi, n;
+        decode(w, x, mi, n);
+        const int arow = s_eoff[x] + mi * kBM;
+        const bool orig = x < p.m_orig;
+        const CUtensorMap* mb0 = orig ? &tmB0 : &tmB2;
+        const CUtensorMap* mb1 = orig ? &tmB1 : &tmB3;
+        const int brow = (orig ? x : x - p.m_orig) * p.b_rows_per_exec;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * C::STAGE_BYTES;
+          uint8_t* sb = sa + C::A_BYTES;
+          mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
+          tma_load_2d(sa, &tmA, &full_bar[stage], kb * C::BK, arow, pol_a);
+          if constexpr (EPI == EPI_SWIGLU) {
+            tma_load_2d(sb, mb0, &full_bar[stage], kb * C::BK, brow + n * (BN / 2), pol_b);
+            tma_load_2d(sb + (BN / 2) * 128, mb1, &full_bar[stage], kb * C::BK, brow + n * (BN / 2), pol_b);
+          } else {
+            tma_load_2d(sb, mb0, &full_bar[stage], kb * C::BK, brow + n * BN, pol_b);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // --------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + stage * C::STAGE_BYTES);
+          const uint32_t b_addr = a_addr + C::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < C::BK / C::UK; ++k) {
+            mma_ss<T>(sdesc_k_sw128(a_addr + k * 32), sdesc_k_sw128(b_addr + k * 32), d_tmem, IDESC,
+                      (kb | k) != 0 ? 1u : 0u);
+          }
+          tc_commit(&empty_bar[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&tfull_bar[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;   // TMEM lane quarter this warp may access
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
+      int x, mi, n;
+      decode(w, x, mi, n);
+      const int rows_x = s_eoff[x + 1] - s_eoff[x];
+      const int r_local = mi * kBM + q * 32 + lane;
+      const bool valid = r_local < rows_x;
+      const int64_t grow = static_cast<int64_t>(s_eoff[x]) + r_local;
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t0 = tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(q * 32) << 16);
+      if constexpr (EPI == EPI_SWIGLU) {
+        T* out = reinterpret_cast<T*>(p.out) + grow * p.ldo + n * (BN / 2);
+#pragma unroll 1
+        for (int c = 0; c < BN / 2; c += 32) {
+          uint32_t g[32], u[32];
+          tmem_ld32(t0 + c, g);
+          tmem_ld32(t0 + BN / 2 + c, u);
+          tmem_ld_wait();
+          float h[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) h[i] = silu_f(__uint_as_float(g[i])) * __uint_as_float(u[i]);
+          if (valid) store_row32<T>(out + c, h);
+        }
+      } else if constexpr (EPI == EPI_WEIGHTED) {
+        const float wr = valid ? p.row_w[grow] : 0.0f;
+        T* out = reinterpret_cast<T*>(p.out) + grow * p.ldo + n * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t a[32];
+          tmem_ld32(t0 + c, a);
+          tmem_ld_wait();
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(a[i]) * wr;
+          if (valid) store_row32<T>(out + c, v);
+        }
+      } else {
+        float* out = reinterpret_cast<float*>(p.out) + grow * p.ldo;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t a[32];
+          tmem_ld32(t0 + c, a);
+          tmem_ld_wait();
+          if (valid) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (c + i < p.n_valid) out[c + i] = __uint_as_float(a[i]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+template <typename T, int BN, int EPI>
+static cudaError_t launch_t(const CUtensorMap& A, const CUtensorMap& B0, const CUtensorMap& B1,
+                            const CUtensorMap& B2, const CUtensorMap& B3, const GemmParams& p, int grid,
+                            cudaStream_t s) {
+  using C = GemmCfg<T, BN>;
+  static bool attr_set = false;
+  auto kern = k_grouped_gemm<T, BN, EPI>;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  kern<<<grid, 192, C::SMEM, s>>>(A, B0, B1, B2, B3, p);
+  return cudaGetLastError();
+}
+
+template <typename T>
+static cudaError_t dispatch(int epi, int bn, const CUtensorMap& A, const CUtensorMap& B0, const CUtensorMap& B1,
+                            const CUtensorMap& B2, const CUtensorMap& B3, const GemmParams& p, int grid,
+                            cudaStream_t s) {
+  if (epi == EPI_SWIGLU) {
+    if (bn == 256) return launch_t<T, 256, EPI_SWIGLU>(A, B0, B1, B2, B3, p, grid, s);
+    if (bn == 128) return launch_t<T, 128, EPI_SWIGLU>(A, B0, B1, B2, B3, p, grid, s);
+  } else if (epi == EPI_WEIGHTED) {
+    if (bn == 256) return launch_t<T, 256, EPI_WEIGHTED>(A, B0, B1, B2, B3, p, grid, s);
+    if (bn == 128) return launch_t<T, 128, EPI_WEIGHTED>(A, B0, B1, B2, B3, p, grid, s);
+    if (bn == 64) return launch_t<T, 64, EPI_WEIGHTED>(A, B0, B1, B2, B3, p, grid, s);
+  } else if (epi == EPI_F32OUT) {
+    if (bn == 256) return launch_t<T, 256, EPI_F32OUT>(A, B0, B1, B2, B3, p, grid, s);
+    if (bn == 128) return launch_t<T, 128, EPI_F32OUT>(A, B0, B1, B2, B3, p, grid, s);
+    if (bn == 64) return launch_t<T, 64, EPI_F32OUT>(A, B0, B1, B2, B3, p, grid, s);
+    if (bn == 32) return launch_t<T, 32, EPI_F32OUT>(A, B0, B1, B2, B3, p, grid, s);
+    if (bn == 16) return launch_t<T, 16, EPI_F32OUT>(A, B0, B1, B2, B3, p, grid, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_grouped_gemm(int dtype, int epi, int bn, const CUtensorMap& A, const CUtensorMap& B0,
+                                const CUtensorMap& B1, const CUtensorMap& B2, const CUtensorMap& B3,
+                                const GemmParams& p, int grid, cudaStream_t s) {
+  if (grid <= 0) return cudaSuccess;
+  if (dtype == 0) return dispatch<__nv_bfloat16>(epi, bn, A, B0, B1, B2, B3, p, grid, s);
+  return dispatch<float>(epi, bn, A, B0, B1, B2, B3, p, grid, s);
+}
+
+int gemm_smem_bytes(int dtype, int epi, int bn) {
+  (void)epi;
+  // STAGE_BYTES depends only on BN (128-byte rows for both dtypes)
+  switch (bn) {
+    case 256: return dtype == 0 ? GemmCfg<__nv_bfloat16, 256>::SMEM : GemmCfg<float, 256>::SMEM;
+    case 128: return dtype == 0 ? GemmCfg<__nv_bfloat16, 128>::SMEM : GemmCfg<float, 128>::SMEM;
+    case 64: return dtype == 0 ? GemmCfg<__nv_bfloat16, 64>::SMEM : GemmCfg<float, 64>::SMEM;
+    case 32: return dtype == 0 ? GemmCfg<__nv_bfloat16, 32>::SMEM : GemmCfg<float, 32>::SMEM;
+    case 16: return dtype == 0 ? GemmCfg<__nv_bfloat16, 16>::SMEM : GemmCfg<float, 16>::SMEM;
+  }
+  return -1;
+}
+
+}  // namespace bo

@@ -1,0 +1,61 @@
+// bo_kernels.h - internal launch interface between the C-ABI layer and the kernels.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bo {
+
+constexpr int kTileTok = 128;   // tokens per histogram / rank tile (top-k + permute)
+constexpr int kBM = 128;        // rows per GEMM tile (TMEM lanes)
+constexpr int kMaxExperts = 256;
+constexpr int kMaxExec = 512;   // m + G
+
+enum Epi : int { EPI_SWIGLU = 0, EPI_WEIGHTED = 1, EPI_F32OUT = 2 };
+
+struct GemmParams {
+  int Kdim;              // reduction length
+  int n_tiles;           // output tiles per executor along N
+  int ldo;               // leading dimension of the output (elements)
+  int n_valid;           // valid output columns (router: m)
+  int m_orig;            // executors < m_orig read B maps 0/1, others maps 2/3
+  int b_rows_per_exec;   // rows of B per executor in the stacked [E*rows, K] view
+  int num_exec;          // executors (1 for the router)
+  int single_rows;       // >= 0: one executor with this many rows (no device schedule)
+  const int* exec_off;   // [num_exec+1] first row of each executor (device)
+  const int* mtile_off;  // [num_exec+1] prefix of ceil(rows/128) (device)
+  void* out;             // output base
+  const float* row_w;    // EPI_WEIGHTED: per-row gate weight (Eq. 6)
+};
+
+// Grouped tcgen05 GEMM: for each executor x and each 128-row tile of its rows,
+// D = A[rows] * B_x^T with an epilogue selected by `epi`.
+// dtype: 0 bf16, 1 fp32 (tf32 MMA).  bn: MMA N (SwiGLU: gate+up columns).
+cudaError_t launch_grouped_gemm(int dtype, int epi, int bn, const CUtensorMap& A, const CUtensorMap& B0,
+                                const CUtensorMap& B1, const CUtensorMap& B2, const CUtensorMap& B3,
+                                const GemmParams& p, int grid, cudaStream_t s);
+int gemm_smem_bytes(int dtype, int epi, int bn);
+
+cudaError_t launch_topk_hist(const float* logits, int T, int m, int K, int32_t* topk_id, float* topk_w,
+                             int32_t* tile_cnt, cudaStream_t s);
+
+cudaError_t launch_plan(const int32_t* tile_cnt, int ntiles, int m, int way, double ratio, int mode,
+                        int32_t* tile_base, int32_t* counts, int32_t* exec_of_expert, int32_t* expert_row_off,
+                        int32_t* exec_off, int32_t* mtile_off, int64_t* stats, cudaStream_t s);
+
+cudaError_t launch_permute(const int32_t* topk_id, const float* topk_w, int T, int K, int m,
+                           const int32_t* tile_base, const int32_t* exec_of_expert,
+                           const int32_t* expert_row_off, int32_t* row_of, int32_t* row_tok, float* row_w,
+                           cudaStream_t s);
+
+cudaError_t launch_gather(int dtype, const void* x, int T, int d, int K, const int32_t* row_of, void* xp,
+                          int num_sms, cudaStream_t s);
+
+cudaError_t launch_combine(int dtype, const void* yp, const void* x, int T, int d, int K,
+                           const int32_t* row_of, int add_residual, void* y, int num_sms, cudaStream_t s);
+
+cudaError_t launch_build_united(int dtype, const void* W, int m, int way, int64_t per_expert, void* U,
+                                cudaStream_t s);
+
+}  // namespace bo

@@ -1,0 +1,533 @@
+// bo_route.cu - routing, Algorithm-1 plan, permutation, gather, combine, united init.
+//
+// Kernels (all deterministic, no floating-point atomics):
+//   k_topk_hist   Eq. 7: per token, K largest fp32 logits (ties ->
+//                 lower id, reading D8) by warp-shuffle argmax; softmax over the
+//                 K selected; per-tile expert histogram (Alg. 1 cnt_i).
+//   k_plan        Alg. 1 on one CTA: counts, rank-by-counting sort
+//                 (cnt desc, id asc, D5), exclusive prefix in sorted order,
+//                 S1 iff prefix < T = S * (1 - ratio) in fp64 (D1, D3), S2
+//                 grouped by floor(e / way), special case, executor
+//                 map, row offsets (executor, expert, token order, D11).
+//   k_permute     stable in-expert rank of every (token, slot) assignment via
+//                 __match_any_sync + popc (no atomics) -> row_of / row_tok / row_w.
+//   k_gather      concat_tokens: Xp[row] = x[token], 16-byte vectors,
+//                 each token read once and written to its K rows.
+//   k_combine     Eq. 5 sum: y[t] = [x_t] + sum_s Yp[row_of(t,s)], fp32,
+//                 slot order.
+//   k_united_mean united-expert init (D14): fp64 group mean, one RNE rounding.
+#include <float.h>
+
+#include "bo_kernels.h"
+#include "bo_ptx.cuh"
+
+namespace bo {
+
+// ----------------------------------------------------------------- top-k
+template <int VPL>   // logits per lane = ceil(m / 32)
+__global__ void __launch_bounds__(256) k_topk_hist(const float* __restrict__ logits, int T, int m, int K,
+                                                   int32_t* __restrict__ topk_id, float* __restrict__ topk_w,
+                                                   int32_t* __restrict__ tile_cnt) {
+  __shared__ int hist[kMaxExperts];
+  for (int i = threadIdx.x; i < m; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t0 = blockIdx.x * kTileTok;
+  for (int tt = warp; tt < kTileTok; tt += 8) {
+    const int t = t0 + tt;
+    if (t >= T) break;
+    float v[VPL];
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int e = lane + 32 * j;
+      v[j] = e < m ? logits[static_cast<int64_t>(t) * m + e] : 0.0f;
+    }
+    uint32_t taken = 0;
+    int my_id = -1;
+    float my_v = 0.0f;
+    for (int s = 0; s < K; ++s) {
+      float bv = -FLT_MAX;
+      int bi = 0x7fffffff;
+      bool have = false;
+#pragma unroll
+      for (int j = 0; j < VPL; ++j) {
+        const int e = lane + 32 * j;
+        if (e < m && !((taken >> j) & 1u)) {
+          if (!have || v[j] > bv) { bv = v[j]; bi = e; have = true; }   // j ascending -> id ascending
+        }
+      }
+      if (!have) { bv = -FLT_MAX; bi = 0x7fffffff; }
+      // warp argmax over (value desc, id asc); -0 == +0 by IEEE comparison
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        const bool o_have = oi != 0x7fffffff;
+        const bool better = o_have && (bi == 0x7fffffff || ov > bv || (ov == bv && oi < bi));
+        if (better) { bv = ov; bi = oi; }
+      }
+      if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+      if (lane == s) { my_id = bi; my_v = bv; }
+    }
+    // softmax over the K selected logits (Eq. 7); slot 0 holds the maximum
+    const float vmax = __shfl_sync(0xffffffffu, my_v, 0);
+    const float ex = lane < K ? expf(my_v - vmax) : 0.0f;
+    float sum = ex;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+    if (lane < K) {
+      topk_id[static_cast<int64_t>(t) * K + lane] = my_id;
+      topk_w[static_cast<int64_t>(t) * K + lane] = ex / sum;
+      atomicAdd(&hist[my_id], 1);   // integer count in shared memory: order-independent
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < m; i += blockDim.x) tile_cnt[static_cast<int64_t>(blockIdx.x) * m + i] = hist[i];
+}
+
+cudaError_t launch_topk_hist(const float* logits, int T, int m, int K, int32_t* topk_id, float* topk_w,
+                             int32_t* tile_cnt, cudaStream_t s) {
+  const int ntiles = (T + kTileTok - 1) / kTileTok;
+  if (ntiles == 0) return cudaSuccess;
+  const int vpl = (m + 31) / 32;
+  switch (vpl) {
+#define BO_TOPK_CASE(N) \
+  case N: k_topk_hist<N><<<ntiles, 256, 0, s>>>(logits, T, m, K, topk_id, topk_w, tile_cnt); break;
+    BO_TOPK_CASE(1) BO_TOPK_CASE(2) BO_TOPK_CASE(3) BO_TOPK_CASE(4)
+    BO_TOPK_CASE(5) BO_TOPK_CASE(6) BO_TOPK_CASE(7) BO_TOPK_CASE(8)
+#undef BO_TOPK_CASE
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ Algorithm 1
+// Inclusive block scan over blockDim.x (= 512) ints in shared memory.
+__device__ __forceinline__ void block_scan_incl(int* buf) {
+  for (int off = 1; off < static_cast<int>(blockDim.x); off <<= 1) {
+    const int v = threadIdx.x >= off ? buf[threadIdx.x - off] : 0;
+    __syncthreads();
+    buf[threadIdx.x] += v;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_cnt, int ntiles, int m, int way,
+                                              double ratio, int mode, int32_t* __restrict__ tile_base,
+                                              int32_t* __restrict__ counts, int32_t* __restrict__ exec_of_expert,
+                                              int32_t* __restrict__ expert_row_off, int32_t* __restrict__ exec_off,
+                                              int32_t* __restrict__ mtile_off, int64_t* __restrict__ stats) {
+  __shared__ int s_cnt[kMaxExperts];
+  __shared__ int s_sorted[kMaxExperts];
+  __shared__ long long s_excl[kMaxExperts];
+  __shared__ int s_gsize[kMaxExperts];
+  __shared__ int s_exec[kMaxExperts];
+  __shared__ int s_scan[kMaxExec];
+  __shared__ int s_scan2[kMaxExec];
+  __shared__ long long s_S;
+  const int tid = threadIdx.x;
+  const int G = (m + way - 1) / way;
+  const int E = m + G;
+
+  // cnt_i (Alg. 1 input) and per-tile exclusive prefix (for the permutation)
+  if (tid < m) {
+    int c = 0;
+    for (int t = 0; t < ntiles; ++t) {
+      const int v = tile_cnt[static_cast<int64_t>(t) * m + tid];
+      if (tile_base) tile_base[static_cast<int64_t>(t) * m + tid] = c;
+      c += v;
+    }
+    s_cnt[tid] = c;
+    counts[tid] = c;
+    s_gsize[tid] = 0;
+  }
+  __syncthreads();
+  // Alg. 1 line 5: sort by (cnt desc, id asc) -- rank by counting
+  if (tid < m) {
+    const int c = s_cnt[tid];
+    int pos = 0;
+    for (int j = 0; j < m; ++j) {
+      const int cj = s_cnt[j];
+      pos += (cj > c) || (cj == c && j < tid);
+    }
+    s_sorted[pos] = tid;
+  }
+  if (tid == 0) {
+    long long S = 0;
+    for (int j = 0; j < m; ++j) S += s_cnt[j];   // Alg. 1 line 6
+    s_S = S;
+  }
+  __syncthreads();
+  // exclusive prefix sum_partial in sorted order (lines 8-15)
+  if (tid < m) {
+    long long excl = 0;
+    for (int j = 0; j < tid; ++j) excl += s_cnt[s_sorted[j]];
+    s_excl[s_sorted[tid]] = excl;
+  }
+  __syncthreads();
+  // line 7: T = S * threshold, threshold = 1 - ratio, fp64 (D3)
+  const double threshold = 1.0 - ratio;
+  const double Tcov = static_cast<double>(s_S) * threshold;
+  bool in_s1 = false, in_s2 = false;
+  if (tid < m) {
+    const bool active = s_cnt[tid] > 0;               // D6
+    in_s1 = active && static_cast<double>(s_excl[tid]) < Tcov;   // D1
+    in_s2 = active && !in_s1;
+    if (in_s2) atomicAdd(&s_gsize[tid / way], 1);     // group_experts (line 23); integer
+  }
+  __syncthreads();
+  if (tid < m) {
+    int x;
+    if (in_s1) x = tid;                               // lines 16-18
+    else if (!in_s2) x = -1;                          // inactive
+    else if (mode == 1) x = -2;                       // full brownout: ignored
+    else if (s_gsize[tid / way] == 1) x = tid;        // special case (lines 24-26)
+    else x = m + tid / way;                           // united expert of the group (lines 27-30)
+    s_exec[tid] = x;
+    exec_of_expert[tid] = x;
+  }
+  __syncthreads();
+  // rows per executor, exec_off = exclusive scan
+  int rows = 0;
+  if (tid < E) {
+    if (tid < m) {
+      rows = s_exec[tid] == tid ? s_cnt[tid] : 0;
+    } else {
+      const int j = tid - m;
+      const int e1 = min((j + 1) * way, m);
+      for (int e = j * way; e < e1; ++e)
+        if (s_exec[e] == tid) rows += s_cnt[e];
+    }
+  }
+  s_scan[tid] = tid < E ? rows : 0;
+  s_scan2[tid] = tid < E ? (rows + kBM - 1) / kBM : 0;
+  __syncthreads();
+  block_scan_incl(s_scan);
+  block_scan_incl(s_scan2);
+  if (tid < E) {
+    exec_off[tid + 1] = s_scan[tid];
+    mtile_off[tid + 1] = s_scan2[tid];
+  }
+  if (tid == 0) {
+    exec_off[0] = 0;
+    mtile_off[0] = 0;
+  }
+  // expert_row_off: executor start + earlier members of the same executor (D11)
+  if (tid < m) {
+    const int x = s_exec[tid];
+    int off = -1;
+    if (x >= 0) {
+      off = x == 0 ? 0 : s_scan[x - 1];
+      if (x >= m) {
+        for (int e = (x - m) * way; e < tid; ++e)
+          if (s_exec[e] == x) off += s_cnt[e];
+      }
+    }
+    expert_row_off[tid] = off;
+  }
+  if (tid == 0) {
+    long long accessed = 0, n_s1 = 0, n_united = 0, n_single = 0, r_orig = 0, r_uni = 0, r_drop = 0;
+    for (int x = 0; x < E; ++x) {
+      const int r = s_scan[x] - (x ? s_scan[x - 1] : 0);
+      if (r > 0) {
+        ++accessed;
+        if (x >= m) ++n_united;
+        if (x < m) r_orig += r; else r_uni += r;
+      }
+    }
+    for (int e = 0; e < m; ++e) {
+      if (s_cnt[e] == 0) continue;
+      if (s_exec[e] == -2) r_drop += s_cnt[e];
+      if (static_cast<double>(s_excl[e]) < Tcov) ++n_s1;
+      else if (s_exec[e] == e) ++n_single;
+    }
+    stats[0] = accessed;
+    stats[1] = n_s1;
+    stats[2] = n_united;
+    stats[3] = n_single;
+    stats[4] = r_orig;
+    stats[5] = r_uni;
+    stats[6] = r_drop;
+    stats[7] = s_S;
+  }
+}
+
+cudaError_t launch_plan(const int32_t* tile_cnt, int ntiles, int m, int way, double ratio, int mode,
+                        int32_t* tile_base, int32_t* counts, int32_t* exec_of_expert, int32_t* expert_row_off,
+                        int32_t* exec_off, int32_t* mtile_off, int64_t* stats, cudaStream_t s) {
+  k_plan<<<1, kMaxExec, 0, s>>>(tile_cnt, ntiles, m, way, ratio, mode, tile_base, counts, exec_of_expert,
+                                expert_row_off, exec_off, mtile_off, stats);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------- permutation
+// One CTA per 128-token tile.  Assignments a = t*K + s of the tile are split
+// into 8 contiguous warp ranges; pass 1 counts per (warp, expert), a prefix
+// over warps gives each warp's start, pass 2 assigns ranks in order.  Row of
+// assignment = expert_row_off[e] + tile_base[tile][e] + rank within the tile.
+__global__ void __launch_bounds__(256) k_permute(const int32_t* __restrict__ topk_id,
+                                                 const float* __restrict__ topk_w, int T, int K, int m,
+                                                 const int32_t* __restrict__ tile_base,
+                                                 const int32_t* __restrict__ exec_of_expert,
+                                                 const int32_t* __restrict__ expert_row_off,
+                                                 int32_t* __restrict__ row_of, int32_t* __restrict__ row_tok,
+                                                 float* __restrict__ row_w) {
+  __shared__ int wcnt[8][kMaxExperts];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 8 * kMaxExperts; i += blockDim.x) (&wcnt[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t a0 = static_cast<int64_t>(blockIdx.x) * kTileTok * K;
+  const int64_t a1 = min(static_cast<int64_t>(blockIdx.x + 1) * kTileTok, static_cast<int64_t>(T)) * K;
+  const int n = static_cast<int>(a1 - a0);
+  const int per_warp = ((n + 8 * 32 - 1) / (8 * 32)) * 32;
+  const int w0 = warp * per_warp;
+  const int w1 = min(w0 + per_warp, n);
+  // pass 1: per-warp counts
+  for (int base = w0; base < w1; base += 32) {
+    const int i = base + lane;
+    const int e = i < w1 ? topk_id[a0 + i] : -1;
+    const uint32_t peers = __match_any_sync(0xffffffffu, e);
+    const int leader = __ffs(peers) - 1;
+    if (lane == leader && e >= 0) wcnt[warp][e] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  if (threadIdx.x < m) {
+    int run = 0;
+    for (int w = 0; w < 8; ++w) {
+      const int c = wcnt[w][threadIdx.x];
+      wcnt[w][threadIdx.x] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  // pass 2: ranks in assignment order
+  const uint32_t lt = lanemask_lt();
+  for (int base = w0; base < w1; base += 32) {
+    const int i = base + lane;
+    const int e = i < w1 ? topk_id[a0 + i] : -1;
+    const uint32_t peers = __match_any_sync(0xffffffffu, e);
+    const int leader = __ffs(peers) - 1;
+    const int start = e >= 0 ? wcnt[warp][e] : 0;
+    __syncwarp();
+    if (lane == leader && e >= 0) wcnt[warp][e] = start + __popc(peers);
+    __syncwarp();
+    if (e >= 0) {
+      const int64_t a = a0 + i;
+      if (exec_of_expert[e] >= 0) {
+        const int r = expert_row_off[e] + tile_base[static_cast<int64_t>(blockIdx.x) * m + e] + start +
+                      __popc(peers & lt);
+        row_of[a] = r;
+        row_tok[r] = static_cast<int32_t>(a / K);
+        row_w[r] = topk_w[a];
+      } else {
+        row_of[a] = -1;   // dropped (full brownout)
+      }
+    }
+  }
+}
+
+cudaError_t launch_permute(const int32_t* topk_id, const float* topk_w, int T, int K, int m,
+                           const int32_t* tile_base, const int32_t* exec_of_expert,
+                           const int32_t* expert_row_off, int32_t* row_of, int32_t* row_tok, float* row_w,
+                           cudaStream_t s) {
+  const int ntiles = (T + kTileTok - 1) / kTileTok;
+  if (ntiles == 0) return cudaSuccess;
+  k_permute<<<ntiles, 256, 0, s>>>(topk_id, topk_w, T, K, m, tile_base, exec_of_expert, expert_row_off, row_of,
+                                   row_tok, row_w);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------- gather
+// Warp per token: each 16-byte chunk of x[t] is loaded once and stored to the
+// token's K rows.  Row indices live one per lane (K <= 16) and are broadcast.
+__global__ void __launch_bounds__(256) k_gather(const uint4* __restrict__ x, int T, int vec_per_row, int K,
+                                                const int32_t* __restrict__ row_of, uint4* __restrict__ xp) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = gw; t < T; t += nw) {
+    const int my_row = lane < K ? row_of[static_cast<int64_t>(t) * K + lane] : -1;
+    const uint4* src = x + static_cast<int64_t>(t) * vec_per_row;
+    for (int c0 = 0; c0 < vec_per_row; c0 += 32) {   // warp-uniform trip count (shuffles below)
+      const int c = c0 + lane;
+      const bool ok = c < vec_per_row;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (ok) v = __ldg(src + c);
+      for (int s = 0; s < K; ++s) {
+        const int r = __shfl_sync(0xffffffffu, my_row, s);
+        if (ok && r >= 0) xp[static_cast<int64_t>(r) * vec_per_row + c] = v;
+      }
+    }
+  }
+}
+
+cudaError_t launch_gather(int dtype, const void* x, int T, int d, int K, const int32_t* row_of, void* xp,
+                          int num_sms, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  const int vec = d * (dtype == 0 ? 2 : 4) / 16;
+  int blocks = (T + 7) / 8;
+  const int cap = num_sms * 8;
+  if (blocks > cap) blocks = cap;
+  k_gather<<<blocks, 256, 0, s>>>(static_cast<const uint4*>(x), T, vec, K, row_of, static_cast<uint4*>(xp));
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- combine
+template <typename T>
+struct Vec8;
+template <>
+struct Vec8<__nv_bfloat16> {
+  static constexpr int kElems = 8;
+  __device__ static void load(const void* p, float (&f)[8]) {
+    const uint4 u = __ldg(static_cast<const uint4*>(p));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 t = __bfloat1622float2(h[i]);
+      f[2 * i] = t.x;
+      f[2 * i + 1] = t.y;
+    }
+  }
+  __device__ static void store(void* p, const float (&f)[8]) {
+    uint4 u;
+    u.x = pack_bf16x2(f[0], f[1]);
+    u.y = pack_bf16x2(f[2], f[3]);
+    u.z = pack_bf16x2(f[4], f[5]);
+    u.w = pack_bf16x2(f[6], f[7]);
+    *static_cast<uint4*>(p) = u;
+  }
+};
+template <>
+struct Vec8<float> {
+  static constexpr int kElems = 8;
+  __device__ static void load(const void* p, float (&f)[8]) {
+    const float4 a = __ldg(static_cast<const float4*>(p));
+    const float4 b = __ldg(static_cast<const float4*>(p) + 1);
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+    f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+  }
+  __device__ static void store(void* p, const float (&f)[8]) {
+    static_cast<float4*>(p)[0] = make_float4(f[0], f[1], f[2], f[3]);
+    static_cast<float4*>(p)[1] = make_float4(f[4], f[5], f[6], f[7]);
+  }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_combine(const T* __restrict__ yp, const T* __restrict__ x, int Tn, int d,
+                                                 int K, const int32_t* __restrict__ row_of, int add_residual,
+                                                 T* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int nvec = d / 8;
+  for (int t = gw; t < Tn; t += nw) {
+    const int my_row = lane < K ? row_of[static_cast<int64_t>(t) * K + lane] : -1;
+    for (int c0 = 0; c0 < nvec; c0 += 32) {   // warp-uniform trip count (shuffles below)
+      const int c = c0 + lane;
+      const bool ok = c < nvec;
+      float acc[8];
+      if (add_residual && ok) {
+        Vec8<T>::load(x + static_cast<int64_t>(t) * d + c * 8, acc);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+      }
+      for (int s = 0; s < K; ++s) {   // slot order (Eq. 5 sum)
+        const int r = __shfl_sync(0xffffffffu, my_row, s);
+        if (ok && r >= 0) {
+          float v[8];
+          Vec8<T>::load(yp + static_cast<int64_t>(r) * d + c * 8, v);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i] += v[i];
+        }
+      }
+      if (ok) Vec8<T>::store(y + static_cast<int64_t>(t) * d + c * 8, acc);
+    }
+  }
+}
+
+cudaError_t launch_combine(int dtype, const void* yp, const void* x, int T, int d, int K, const int32_t* row_of,
+                           int add_residual, void* y, int num_sms, cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  int blocks = (T + 7) / 8;
+  const int cap = num_sms * 8;
+  if (blocks > cap) blocks = cap;
+  if (dtype == 0)
+    k_combine<__nv_bfloat16><<<blocks, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(yp),
+                                                    static_cast<const __nv_bfloat16*>(x), T, d, K, row_of,
+                                                    add_residual, static_cast<__nv_bfloat16*>(y));
+  else
+    k_combine<float><<<blocks, 256, 0, s>>>(static_cast<const float*>(yp), static_cast<const float*>(x), T, d, K,
+                                            row_of, add_residual, static_cast<float*>(y));
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ united init
+// Round an fp64 value to bf16, ties to even, directly from the fp64 bits.
+__device__ __forceinline__ uint16_t f64_to_bf16_rne(double v) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+  const unsigned long long sign = b >> 63;
+  const long long exp = static_cast<long long>((b >> 52) & 0x7ff);
+  if (exp == 0x7ff) {   // inf / nan
+    const unsigned long long mant = b & 0xfffffffffffffull;
+    return static_cast<uint16_t>((sign << 15) | 0x7f80u | (mant ? 0x40u : 0u));
+  }
+  if (v == 0.0) return static_cast<uint16_t>(sign << 15);
+  // bf16 significand has 8 bits; drop 45 of the 53 fp64 significand bits.
+  const unsigned long long low = b & ((1ull << 45) - 1);
+  unsigned long long kept = b >> 45;                  // sign | exp(11) | mant(7)
+  const unsigned long long half = 1ull << 44;
+  if (low > half || (low == half && (kept & 1ull))) ++kept;
+  // re-bias the exponent from 1023 to 127 (normal range only; generators stay inside it)
+  const long long e11 = static_cast<long long>((kept >> 7) & 0x7ff);
+  const unsigned long long mant7 = kept & 0x7f;
+  const long long e8 = e11 - 1023 + 127;
+  if (e8 >= 0xff) return static_cast<uint16_t>((sign << 15) | 0x7f80u);
+  if (e8 <= 0) return static_cast<uint16_t>(sign << 15);   // flush (outside the generated range)
+  return static_cast<uint16_t>((sign << 15) | (static_cast<unsigned long long>(e8) << 7) | mant7);
+}
+
+template <typename T>
+__global__ void k_united_mean(const T* __restrict__ W, int m, int way, int64_t per_expert, T* __restrict__ U) {
+  const int G = (m + way - 1) / way;
+  const int64_t total = static_cast<int64_t>(G) * per_expert;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(i / per_expert);
+    const int64_t o = i - static_cast<int64_t>(j) * per_expert;
+    const int e0 = j * way, e1 = min((j + 1) * way, m);
+    double acc = 0.0;
+    for (int e = e0; e < e1; ++e) {   // members ascending
+      double w;
+      if constexpr (sizeof(T) == 2) w = static_cast<double>(__bfloat162float(W[static_cast<int64_t>(e) * per_expert + o]));
+      else w = static_cast<double>(W[static_cast<int64_t>(e) * per_expert + o]);
+      acc += w;
+    }
+    const double mean = acc / static_cast<double>(e1 - e0);
+    if constexpr (sizeof(T) == 2) {
+      const uint16_t bits = f64_to_bf16_rne(mean);
+      U[i] = *reinterpret_cast<const __nv_bfloat16*>(&bits);
+    } else {
+      U[i] = __double2float_rn(mean);
+    }
+  }
+}
+
+cudaError_t launch_build_united(int dtype, const void* W, int m, int way, int64_t per_expert, void* U,
+                                cudaStream_t s) {
+  const int G = (m + way - 1) / way;
+  const int64_t total = static_cast<int64_t>(G) * per_expert;
+  if (total == 0) return cudaSuccess;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (dtype == 0)
+    k_united_mean<__nv_bfloat16><<<static_cast<int>(blocks), 256, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(W), m, way, per_expert, static_cast<__nv_bfloat16*>(U));
+  else
+    k_united_mean<float><<<static_cast<int>(blocks), 256, 0, s>>>(static_cast<const float*>(W), m, way,
+                                                                  per_expert, static_cast<float*>(U));
+  return cudaGetLastError();
+}
+
+}  // namespace bo

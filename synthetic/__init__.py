@@ -133,3 +133,18 @@ def make_logits_with_counts(counts, K: int = 1, seed: int = 0):
 
 def with_(cfg: LayerConfig, **kw) -> LayerConfig:
     return replace(cfg, **kw)
+
+
+def make_logits(T: int, m: int, seed: int = 0, sigma: float = 0.5, device="cpu", ties: bool = False):
+    """fp32 router logits [T, m] drawn directly (for routing parity with
+    injected logits): N(0, 1) plus a per-expert N(0, sigma^2) popularity bias.
+    ties=True draws small integers instead, so equal logits (and -0.0 / +0.0)
+    are frequent."""
+    g = _gen(seed, device)
+    if ties:
+        L = torch.randint(-2, 3, (T, m), generator=g, device=device).to(torch.float32)
+        neg = torch.rand(T, m, generator=g, device=device) < 0.5
+        L = torch.where((L == 0) & neg, torch.full_like(L, -0.0), L)
+        return L
+    bias = torch.randn(m, generator=g, device=device) * sigma
+    return torch.randn(T, m, generator=g, device=device) + bias

@@ -1,0 +1,81 @@
+"""CPU-side checks of the C-ABI library: it loads, exports every symbol that
+include/brownout.h declares, and rejects bad arguments before touching a GPU."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "brownout.h")
+
+
+@pytest.fixture(scope="module")
+def built():
+    from paper_2507_17133_b200.build import build
+    return build()
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(bo_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary_calls():
+    syms = declared_symbols()
+    for need in ("bo_build_united", "bo_set_brownout", "bo_moe_forward"):   # B:5
+        assert need in syms
+
+
+def test_library_exports_every_declared_symbol(built):
+    out = subprocess.run(["nm", "-D", "--defined-only", built], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (bo_[a-z_]+)", out))
+    missing = [s for s in declared_symbols() if s not in exported]
+    assert not missing, missing
+    # nothing else leaks out of the library (hidden visibility by default)
+    assert all(s.startswith("bo_") for s in exported)
+
+
+def test_binding_loads_and_reports_status_strings(built):
+    import paper_2507_17133_b200 as P
+    lib = P.lib()
+    assert lib.bo_status_string(0) == b"BO_OK"
+    assert lib.bo_status_string(6) == b"BO_ERR_WORKSPACE"
+    assert b"sm_100a" in lib.bo_version()
+    for name in declared_symbols():
+        assert hasattr(lib, name)
+
+
+def test_bad_configs_are_rejected_before_device_use(built):
+    import paper_2507_17133_b200 as P
+    from paper_2507_17133_b200.brownout import bo_config, BO_ERR_INVALID_ARG, BO_ERR_SHAPE, BO_ERR_UNSUPPORTED
+    lib = P.lib()
+    h = C.c_void_p()
+
+    def create(**kw):
+        base = dict(hidden=256, ffn=512, num_experts=8, top_k=2, way=4, dtype=0, add_residual=0, reserved=0,
+                    max_tokens=128)
+        base.update(kw)
+        return lib.bo_create(C.byref(bo_config(**base)), C.byref(h))
+
+    assert create(top_k=0) == BO_ERR_INVALID_ARG
+    assert create(top_k=9) == BO_ERR_INVALID_ARG          # K > m
+    assert create(way=0) == BO_ERR_INVALID_ARG
+    assert create(hidden=100) == BO_ERR_SHAPE
+    assert create(num_experts=300) == BO_ERR_SHAPE
+    assert create(dtype=7) == BO_ERR_UNSUPPORTED
+    assert lib.bo_set_brownout(None, 0.5, 0) == BO_ERR_INVALID_ARG
+    assert lib.bo_moe_forward(None, None, 0, None, None, None, None, None, None, None, None, None, 0,
+                              None) == BO_ERR_INVALID_ARG
+    assert b"" != lib.bo_last_error()
+
+
+def test_sass_uses_tcgen05_and_tma(built):
+    """The GEMM engine is tcgen05 (UTC*MMA) fed by TMA (UTMALDG); no legacy HMMA."""
+    sass = subprocess.run(["cuobjdump", "-sass", built], capture_output=True, text=True, check=True).stdout
+    assert re.search(r"UTC\w*MMA", sass)
+    assert "UTMALDG" in sass
+    assert "LDTM" in sass
+    assert not re.search(r"\bHMMA\b", sass)
