@@ -1,0 +1,460 @@
+#!/usr/bin/env python
+"""Benchmark of the brownout MoE-layer forward (BrownoutServe, arXiv 2507.17133).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload mixtral_prefill|mixtral_decode|qwen3_30b_a3b_prefill] [--ratio R]
+                    [--no-sweep] [--no-extra] [--no-cpu]
+
+A step is one whole brownout MoE-layer forward (router GEMM, top-K, Alg. 1
+plan, permutation, gather, grouped SwiGLU GEMM, weighted grouped GEMM,
+combine) over one batch of synthetic tokens already resident in HBM.  At N=1
+the workload is BASELINE.json configs[1]: the Mixtral-8x7B MoE layer (d 4096,
+f 14336, 8 experts, top-2, united groups of 4), prefill T = 4096, bf16, at
+brownout ratio 0.5 (the other ratios of the sweep are reported in
+"ratio_sweep").  For N > 1 (torchrun) every rank runs the same step on its own
+batch (weak scaling, replicas).
+
+Rank 0 prints ONE JSON line.  --impl reference times the fp64 CPU oracle (the
+reference arm of this tier) on a bounded token sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE-layer tokens/s vs brownout ratio at 1/2/4/8 B200; % bf16 / HBM roofline"
+
+
+def load_json(path):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def peaks():
+    mp = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json"))
+    if mp and "hbm_gbs" in mp:
+        return {"hbm_gbs": mp["hbm_gbs"], "bf16_tflops": mp["bf16_tflops"],
+                "bf16_tflops_sustained": mp.get("bf16_tflops_sustained", mp["bf16_tflops"]),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._th = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nvml = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM))
+                r = self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nvml:
+            self._th = threading.Thread(target=self._run, daemon=True)
+            self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._th:
+            self._th.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------- workload
+def algorithmic(cfg, T, stats, d, f, m):
+    """Method's own work: FLOPs = 2 T d m + 6 d f R_kept,
+    bytes = sum over accessed executors of 3 d f * 2 B + x and y (2 T d * 2 B) + Wr."""
+    R = stats["rows_original"] + stats["rows_united"]
+    flops = 2.0 * T * d * m + 6.0 * d * f * R
+    gemm1_flops = 4.0 * d * f * R
+    gemm2_flops = 2.0 * d * f * R
+    w_bytes = stats["executors_accessed"] * 3.0 * d * f * 2
+    bytes_ = w_bytes + 2.0 * T * d * 2 + 2.0 * d * m
+    return {"flops": flops, "bytes": bytes_, "gemm1_flops": gemm1_flops, "gemm2_flops": gemm2_flops,
+            "gemm1_bytes": stats["executors_accessed"] * 2.0 * d * f * 2 + R * d * 2 + R * f * 2,
+            "weight_bytes": w_bytes}
+
+
+KERNELS = ["router_gemm", "topk_hist", "plan", "permute", "gather", "gemm1_swiglu", "gemm2_weighted", "combine"]
+
+
+class Layer:
+    def __init__(self, cfg, device, T=None):
+        import torch
+        import synthetic as S
+        from paper_2507_17133_b200 import BrownoutMoE
+        self.cfg = cfg
+        self.T = cfg.T if T is None else T
+        self.lay = S.make_layer(cfg, device=device)
+        self.moe = BrownoutMoE(cfg.d, cfg.f, cfg.m, cfg.K, cfg.way, dtype=cfg.dtype, max_tokens=self.T)
+        L = self.lay
+        self.united = self.moe.build_united(L["Wg"], L["Wu"], L["Wd"])
+        self.x = S.make_tokens(cfg, T=self.T, device=device)
+        self.y = torch.empty_like(self.x)
+        self.ws = self.moe.workspace(self.T, device)
+        self.stream = torch.cuda.current_stream()
+
+    def step(self):
+        L = self.lay
+        self.moe.forward(self.x, L["Wr"], (L["Wg"], L["Wu"], L["Wd"]), self.united, y=self.y,
+                         workspace=self.ws, stream=self.stream)
+
+    def stats(self):
+        import torch
+        torch.cuda.synchronize()
+        from paper_2507_17133_b200 import STATS_FIELDS
+        st = self.moe.debug_arrays(self.T, self.ws)["stats"].cpu().tolist()
+        return dict(zip(STATS_FIELDS, st))
+
+
+def time_steps(layer, steps, warmup, dist_on, per_kernel=True):
+    """W warm-up steps, then K timed steps between barrier + synchronize; device
+    time with CUDA events on the launching stream; max over ranks."""
+    import torch
+    for _ in range(warmup):
+        layer.step()
+    torch.cuda.synchronize()
+    ev_sets = None
+    if per_kernel:
+        ev_sets = [[torch.cuda.Event(enable_timing=True) for _ in range(len(KERNELS) + 1)] for _ in range(steps)]
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    if dist_on:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    start.record(layer.stream)
+    for i in range(steps):
+        if ev_sets:
+            layer.moe.set_profile_events(ev_sets[i])
+        layer.step()
+    end.record(layer.stream)
+    torch.cuda.synchronize()
+    if ev_sets:
+        layer.moe.set_profile_events(None)
+    ms = start.elapsed_time(end)
+    if dist_on:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    kern = None
+    if ev_sets:
+        kern = {}
+        for j, name in enumerate(KERNELS):
+            kern[name] = sum(ev[j].elapsed_time(ev[j + 1]) for ev in ev_sets) / steps
+    return ms, kern
+
+
+def time_e2e(layer, steps, warmup):
+    """Same metric end to end through the public API: per step, H2D copy of the
+    step's tokens from pinned host memory, the forward, D2H copy of y."""
+    import torch
+    hx = layer.x.cpu().pin_memory()
+    hy = torch.empty(layer.y.shape, dtype=layer.y.dtype, pin_memory=True)
+    dx = torch.empty_like(layer.x)
+    L = layer.lay
+    s = layer.stream
+
+    def one():
+        dx.copy_(hx, non_blocking=True)
+        layer.moe.forward(dx, L["Wr"], (L["Wg"], L["Wu"], L["Wd"]), layer.united, y=layer.y, workspace=layer.ws,
+                          stream=s)
+        hy.copy_(layer.y, non_blocking=True)
+
+    for _ in range(warmup):
+        one()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    for _ in range(steps):
+        one()
+    b.record(s)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    nbytes = hx.numel() * hx.element_size()
+    return {"value": layer.T / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": hy.numel() * hy.element_size()}
+
+
+# ------------------------------------------------------------- CPU oracle
+def oracle_sample(layer_host, cfg, ratio, n_tok, seed=0):
+    """Time the fp64 oracle (as it stands) on a sample of n_tok tokens of the
+    workload: full-batch Eq. 8 / Eq. 7 / Alg. 1, FFN rows of the sampled tokens."""
+    import numpy as np
+    from oracle import brownout_oracle as O
+    x, Wr, ex, un = layer_host
+    T = x.shape[0]
+    toks = np.sort(np.random.default_rng(seed).choice(T, size=min(n_tok, T), replace=False))
+    t0 = time.perf_counter()
+    O.moe_forward(x, Wr, ex, un, cfg.K, cfg.way, ratio, tokens=toks)
+    return time.perf_counter() - t0, len(toks)
+
+
+def host_copy(layer):
+    import numpy as np  # noqa: F401
+    L = layer.lay
+    f32 = lambda t: t.float().cpu().numpy()   # exact widening of bf16
+    ex = tuple(f32(L[k]) for k in ("Wg", "Wu", "Wd"))
+    un = tuple(f32(u) for u in layer.united)
+    return f32(layer.x), f32(L["Wr"]), ex, un
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        n = [i.get("num_threads") for i in threadpool_info() if i.get("user_api") == "blas"]
+        if n:
+            return int(max(n))
+    except Exception:
+        pass
+    return os.cpu_count()
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+# -------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="mixtral_prefill")
+    ap.add_argument("--ratio", type=float, default=0.5)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-tokens", type=int, default=32)
+    args = ap.parse_args()
+
+    import torch
+    import synthetic as S
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = S.with_(S.CONFIGS[args.workload], ratio=args.ratio)
+
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world)
+
+    torch.cuda.set_device(local)
+    dist_on = world > 1
+    if dist_on:
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2507_17133_b200.build import build
+    if rank == 0:
+        build()
+    if dist_on:
+        torch.distributed.barrier()
+
+    pk = peaks()
+    layer = Layer(cfg, "cuda")
+    layer.moe.set_brownout(cfg.ratio)
+    layer.step()
+    st = layer.stats()
+    launches = layer.moe.last_launch_count()
+
+    with ClockSampler(local) as clk:
+        ms, kern = time_steps(layer, args.steps, max(args.warmup, 3), dist_on)
+    clocks = clk.summary()
+    ms_step = ms / args.steps
+    value = world * cfg.T / (ms_step / 1e3)
+    alg = algorithmic(cfg, cfg.T, st, cfg.d, cfg.f, cfg.m)
+
+    # dominant kernel roofline: GEMM1 (SwiGLU), tensor-bound for prefill, HBM-bound for decode
+    g1 = kern["gemm1_swiglu"] / 1e3
+    prefill_like = alg["gemm1_flops"] / max(alg["gemm1_bytes"], 1) > 300
+    if prefill_like:
+        ach = alg["gemm1_flops"] / g1 / 1e12
+        roof = {"kernel": "gemm1_swiglu", "bound": "tensor", "achieved": ach, "peak": pk["bf16_tflops_sustained"],
+                "unit": "TFLOP/s", "frac": ach / pk["bf16_tflops_sustained"],
+                "peak_note": "sustained bf16 (kernel timed inside a long step); " + pk["source"],
+                "algorithmic_per_launch": alg["gemm1_flops"]}
+    else:
+        ach = alg["gemm1_bytes"] / g1 / 1e9
+        roof = {"kernel": "gemm1_swiglu", "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / pk["hbm_gbs"], "peak_note": pk["source"], "algorithmic_per_launch": alg["gemm1_bytes"]}
+    prof = load_json(os.path.join(ROOT, "profiles", "ncu_traffic.json")) or {}
+    roof["traffic"] = prof.get(f"{cfg.name}:{cfg.ratio}:gemm1_swiglu")
+    step_tflops = alg["flops"] / (ms_step / 1e3) / 1e12
+    step_gbs = alg["bytes"] / (ms_step / 1e3) / 1e9
+
+    out = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (seeded; random-init Mixtral-shaped weights)",
+        "config": {"workload": cfg.name, "T": cfg.T, "d": cfg.d, "f": cfg.f, "m": cfg.m, "K": cfg.K,
+                   "way": cfg.way, "ratio": cfg.ratio, "mode": "partial", "sigma": cfg.sigma,
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "inputs larger than L2 (expert weights %.2f GB/step)" % (alg["weight_bytes"] / 1e9)},
+        "roofline": roof,
+        "step_roofline": {"tflops": step_tflops, "frac_bf16_sustained": step_tflops / pk["bf16_tflops_sustained"],
+                          "alg_gbs": step_gbs, "frac_hbm": step_gbs / pk["hbm_gbs"]},
+        "kernel_ms": kern, "plan_stats": st, "gpu_launches": launches * args.steps,
+        "clocks": clocks,
+    }
+    if rank == 0:
+        try:
+            out["e2e"] = time_e2e(layer, max(3, args.steps // 2), 3)
+            out["e2e"]["value"] *= world
+        except Exception as e:   # pragma: no cover
+            out["e2e"] = {"error": str(e)}
+    if not args.no_sweep:
+        sweep = {}
+        for r in S.RATIO_SWEEP:
+            layer.moe.set_brownout(r)
+            layer.step()
+            s_r = layer.stats()
+            ms_r, k_r = time_steps(layer, args.steps, 3, dist_on)
+            sweep[str(r)] = {"tokens_per_s": world * cfg.T / (ms_r / args.steps / 1e3), "ms": ms_r / args.steps,
+                             "executors": s_r["executors_accessed"], "gemm1_ms": k_r["gemm1_swiglu"],
+                             "gemm2_ms": k_r["gemm2_weighted"]}
+        layer.moe.set_brownout(cfg.ratio)
+        out["ratio_sweep"] = sweep
+    if not args.no_extra and cfg.name == "mixtral_prefill":
+        extra = {}
+        for name in ("mixtral_decode", "qwen3_30b_a3b_prefill"):
+            c2 = S.CONFIGS[name]
+            if name == "mixtral_decode":
+                lay2 = Layer.__new__(Layer)
+                lay2.cfg, lay2.T, lay2.lay, lay2.united, lay2.stream = c2, c2.T, layer.lay, layer.united, layer.stream
+                from paper_2507_17133_b200 import BrownoutMoE
+                lay2.moe = BrownoutMoE(c2.d, c2.f, c2.m, c2.K, c2.way, dtype=c2.dtype, max_tokens=c2.T)
+                lay2.x = S.make_tokens(c2, T=c2.T, device="cuda")
+                lay2.y = torch.empty_like(lay2.x)
+                lay2.ws = lay2.moe.workspace(c2.T, "cuda")
+            else:
+                del layer.lay
+                layer.lay = None
+                torch.cuda.empty_cache()
+                lay2 = Layer(c2, "cuda")
+            res = {}
+            for r in ((0.0, 0.5, 1.0) if name == "mixtral_decode" else (0.5,)):
+                lay2.moe.set_brownout(r)
+                lay2.step()
+                s2 = lay2.stats()
+                ms2, k2 = time_steps(lay2, args.steps, 3, dist_on)
+                a2 = algorithmic(c2, c2.T, s2, c2.d, c2.f, c2.m)
+                t2 = ms2 / args.steps / 1e3
+                res[str(r)] = {"tokens_per_s": world * c2.T / t2, "ms": t2 * 1e3,
+                               "executors": s2["executors_accessed"],
+                               "frac_hbm_step": a2["bytes"] / t2 / 1e9 / pk["hbm_gbs"],
+                               "frac_bf16_step": a2["flops"] / t2 / 1e12 / pk["bf16_tflops_sustained"],
+                               "gemm1_ms": k2["gemm1_swiglu"], "gemm2_ms": k2["gemm2_weighted"],
+                               "gemm1_frac_hbm": a2["gemm1_bytes"] / (k2["gemm1_swiglu"] / 1e3) / 1e9 / pk["hbm_gbs"],
+                               "gemm1_frac_bf16": a2["gemm1_flops"] / (k2["gemm1_swiglu"] / 1e3) / 1e12
+                               / pk["bf16_tflops_sustained"]}
+            extra[name] = res
+        out["other_workloads"] = extra
+    if rank == 0 and not args.no_cpu:
+        try:
+            hc = host_copy(layer if layer.lay is not None else Layer(cfg, "cuda"))
+            secs, n = oracle_sample(hc, cfg, cfg.ratio, args.cpu_tokens)
+            out["cpu_baseline"] = {"value": n / secs, "unit": "tokens/s", "cores": cpu_threads(), "kind": "oracle",
+                                   "sample": f"{n} of {cfg.T} tokens (full-batch routing + plan, FFN rows of the "
+                                             f"sampled tokens), fp64 numpy, {secs:.1f} s",
+                                   "cpu": cpu_model()}
+        except Exception as e:   # pragma: no cover
+            out["cpu_baseline"] = {"error": str(e)}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist_on:
+        torch.distributed.destroy_process_group()
+
+
+def run_reference(args, cfg, rank, world):
+    """Reference arm: the fp64 CPU oracle as it stands, rank 0 only."""
+    if rank != 0:
+        return
+    import numpy as np
+    import synthetic as S
+    from oracle import brownout_oracle as O
+    lay = S.make_layer(cfg, device="cpu") if cfg.d * cfg.f * cfg.m < 2e8 else None
+    if lay is None:
+        import torch
+        if torch.cuda.is_available():
+            lay = {k: v.cpu() for k, v in S.make_layer(cfg, device="cuda").items()}
+        else:
+            lay = S.make_layer(cfg, device="cpu")
+    f32 = lambda t: t.float().numpy()
+    ex = tuple(f32(lay[k]) for k in ("Wg", "Wu", "Wd"))
+    un = O.build_united_mean(*ex, cfg.way, out_dtype=cfg.dtype)
+    x = f32(S.make_tokens(cfg, T=cfg.T))
+    hc = (x, f32(lay["Wr"]), ex, un)
+    n_tok = max(1, args.cpu_tokens // 4)
+    for _ in range(args.warmup):
+        oracle_sample(hc, cfg, cfg.ratio, n_tok)
+    tot, ntot = 0.0, 0
+    for i in range(args.steps):
+        s, n = oracle_sample(hc, cfg, cfg.ratio, n_tok, seed=i)
+        tot += s
+        ntot += n
+    v = ntot / tot
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded)",
+           "config": {"workload": cfg.name, "T": cfg.T, "d": cfg.d, "f": cfg.f, "m": cfg.m, "K": cfg.K,
+                      "way": cfg.way, "ratio": cfg.ratio},
+           "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cpu_threads(), "kind": "oracle",
+                            "sample": f"{n_tok} of {cfg.T} tokens per step (full-batch routing + plan)",
+                            "cpu": cpu_model()},
+           "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    del np
+
+
+if __name__ == "__main__":
+    main()

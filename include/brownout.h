@@ -172,6 +172,13 @@ BO_API bo_status bo_plan_from_counts(bo_handle* h, const int32_t* counts, int32_
                               int32_t* expert_row_off, int32_t* exec_off, void* stats,
                               void* stream);
 
+/* Optional per-kernel timing: when `events` (an array of n cudaEvent_t cast
+ * to void*) is non-NULL, each following forward records events[i] on its
+ * stream immediately before its i-th kernel launch and events[L] after the
+ * last one (L = launch count; requires n >= L + 1, else the events are not
+ * recorded).  Pass NULL to disable.  The events stay owned by the caller. */
+BO_API bo_status bo_set_profile_events(bo_handle* h, void** events, int32_t n);
+
 /* Number of GPU kernels the last forward on this handle enqueued. */
 BO_API int32_t bo_last_launch_count(const bo_handle* h);
 

@@ -23,7 +23,7 @@ BO_UNITED_MEAN = 0
 EXPORTED = (
     "bo_create", "bo_destroy", "bo_workspace_size", "bo_workspace_layout", "bo_build_united",
     "bo_set_brownout", "bo_get_brownout", "bo_moe_forward", "bo_moe_forward_ex", "bo_plan_from_counts",
-    "bo_last_launch_count", "bo_status_string", "bo_last_error", "bo_version",
+    "bo_set_profile_events", "bo_last_launch_count", "bo_status_string", "bo_last_error", "bo_version",
 )
 
 
@@ -71,6 +71,7 @@ def _load():
         "bo_moe_forward": ([vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp], C.c_int),
         "bo_moe_forward_ex": ([vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp, vp], C.c_int),
         "bo_plan_from_counts": ([vp, vp, vp, vp, vp, vp, vp], C.c_int),
+        "bo_set_profile_events": ([vp, C.POINTER(vp), i32], C.c_int),
         "bo_last_launch_count": ([vp], i32),
         "bo_status_string": ([C.c_int], C.c_char_p),
         "bo_last_error": ([], C.c_char_p),
@@ -183,6 +184,17 @@ class BrownoutMoE:
                                           _ptr(UWu), _ptr(UWd), _ptr(y), _ptr(ws), ws.numel(), _ptr(logits),
                                           _stream(stream)))
         return y
+
+    def set_profile_events(self, events):
+        """events: list of torch.cuda.Event(enable_timing=True) (>= launches + 1),
+        recorded around every kernel of the following forwards; None disables."""
+        if events is None:
+            self._prof = None
+            _check(_lib.bo_set_profile_events(self._h, None, 0))
+            return
+        arr = (C.c_void_p * len(events))(*[C.c_void_p(e.cuda_event) for e in events])
+        self._prof = (events, arr)
+        _check(_lib.bo_set_profile_events(self._h, arr, len(events)))
 
     def last_launch_count(self) -> int:
         return int(_lib.bo_last_launch_count(self._h))

@@ -20,6 +20,8 @@ struct bo_handle {
   int num_sms;
   int device;
   int32_t last_launches;
+  void** prof_events;
+  int32_t prof_n;
 };
 
 namespace {
@@ -171,6 +173,11 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   const int64_t R = T * K;
   const int ntiles = static_cast<int>(L.ntiles);
   int launches = 0;
+  const int kMaxLaunches = 8;
+  const bool prof = h->prof_events && h->prof_n >= kMaxLaunches + 1;
+  auto mark = [&](int i) {
+    if (prof) cudaEventRecord(static_cast<cudaEvent_t>(h->prof_events[i]), s);
+  };
 
   float* logits = at<float>(ws, L.logits);
   int32_t* topk_id = at<int32_t>(ws, L.topk_id);
@@ -210,23 +217,28 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
     p.out = logits;
     const int work = static_cast<int>((T + bo::kBM - 1) / bo::kBM);
     const int grid = work < h->num_sms ? work : h->num_sms;
+    mark(launches);
     BO_CUDA(bo::launch_grouped_gemm(dt, bo::EPI_F32OUT, bn, mA, mB, mB, mB, mB, p, grid, s), "router gemm");
     ++launches;
     L_use = logits;
   }
   // 2. top-K + softmax (Eq. 7) + per-tile histogram
+  mark(launches);
   BO_CUDA(bo::launch_topk_hist(L_use, static_cast<int>(T), m, K, topk_id, topk_w, tile_cnt, s), "topk");
   ++launches;
   // 3. Algorithm 1 plan (snapshot of the knob at enqueue time)
+  mark(launches);
   BO_CUDA(bo::launch_plan(tile_cnt, ntiles, m, c.way, h->ratio, h->mode, tile_base, counts, exec_of, erow,
                           exec_off, mtile_off, stats, s),
           "plan");
   ++launches;
   // 4. permutation (rows) and gather (Xp)
+  mark(launches);
   BO_CUDA(bo::launch_permute(topk_id, topk_w, static_cast<int>(T), K, m, tile_base, exec_of, erow, row_of,
                              row_tok, row_w, s),
           "permute");
   ++launches;
+  mark(launches);
   BO_CUDA(bo::launch_gather(dt, x, static_cast<int>(T), d, K, row_of, xp, h->num_sms, s), "gather");
   ++launches;
   // 5. GEMM1 + SwiGLU over executors
@@ -253,6 +265,7 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
     p.out = hb;
     const int64_t max_work = ((R + bo::kBM - 1) / bo::kBM + E) * p.n_tiles;
     const int grid = static_cast<int>(max_work < h->num_sms ? max_work : h->num_sms);
+    mark(launches);
     BO_CUDA(bo::launch_grouped_gemm(dt, bo::EPI_SWIGLU, bn, mA, mG, mU, mUG, mUU, p, grid, s), "gemm1");
     ++launches;
   }
@@ -279,13 +292,16 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
     p.row_w = row_w;
     const int64_t max_work = ((R + bo::kBM - 1) / bo::kBM + E) * p.n_tiles;
     const int grid = static_cast<int>(max_work < h->num_sms ? max_work : h->num_sms);
+    mark(launches);
     BO_CUDA(bo::launch_grouped_gemm(dt, bo::EPI_WEIGHTED, bn, mA, mD, mD, mUD, mUD, p, grid, s), "gemm2");
     ++launches;
   }
   // 7. combine (Eq. 5 sum over the token's K slots)
+  mark(launches);
   BO_CUDA(bo::launch_combine(dt, yp, x, static_cast<int>(T), d, K, row_of, c.add_residual, y, h->num_sms, s),
           "combine");
   ++launches;
+  mark(launches);
   h->last_launches = launches;
   return BO_OK;
 }
@@ -337,6 +353,8 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   h->num_sms = sms;
   h->device = dev;
   h->last_launches = 0;
+  h->prof_events = nullptr;
+  h->prof_n = 0;
   *out = h;
   return BO_OK;
 }
@@ -416,6 +434,13 @@ bo_status bo_plan_from_counts(bo_handle* h, const int32_t* counts, int32_t* exec
   BO_CUDA(bo::launch_plan(counts, 1, m, c.way, h->ratio, h->mode, nullptr, counts_out, exec_of_expert,
                           expert_row_off, exec_off, mtile_scratch, static_cast<int64_t*>(stats), s),
           "plan_from_counts");
+  return BO_OK;
+}
+
+bo_status bo_set_profile_events(bo_handle* h, void** events, int32_t n) {
+  if (!h) return fail(BO_ERR_INVALID_ARG, "null handle");
+  h->prof_events = events;
+  h->prof_n = events ? n : 0;
   return BO_OK;
 }
 
