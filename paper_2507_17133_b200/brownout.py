@@ -192,6 +192,9 @@ class BrownoutMoE:
             self._prof = None
             _check(_lib.bo_set_profile_events(self._h, None, 0))
             return
+        for e in events:      # torch creates the underlying cudaEvent_t lazily, on first record
+            if not e.cuda_event:
+                e.record()
         arr = (C.c_void_p * len(events))(*[C.c_void_p(e.cuda_event) for e in events])
         self._prof = (events, arr)
         _check(_lib.bo_set_profile_events(self._h, arr, len(events)))

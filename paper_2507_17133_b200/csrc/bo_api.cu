@@ -175,8 +175,9 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   int launches = 0;
   const int kMaxLaunches = 8;
   const bool prof = h->prof_events && h->prof_n >= kMaxLaunches + 1;
+  cudaError_t prof_err = cudaSuccess;
   auto mark = [&](int i) {
-    if (prof) cudaEventRecord(static_cast<cudaEvent_t>(h->prof_events[i]), s);
+    if (prof && prof_err == cudaSuccess) prof_err = cudaEventRecord(static_cast<cudaEvent_t>(h->prof_events[i]), s);
   };
 
   float* logits = at<float>(ws, L.logits);
@@ -302,6 +303,7 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
           "combine");
   ++launches;
   mark(launches);
+  if (prof_err != cudaSuccess) return cuda_fail(prof_err, "profile event record");
   h->last_launches = launches;
   return BO_OK;
 }
