@@ -104,7 +104,7 @@ bo_status compute_layout(const bo_handle* h, int64_t T, bo_ws_layout* L) {
   const bo_config& c = h->cfg;
   const int64_t m = c.num_experts, K = c.top_k, d = c.hidden, f = c.ffn;
   const int64_t G = (m + c.way - 1) / c.way, E = m + G;
-  const int64_t ntiles = (T + bo::kTileTok - 1) / bo::kTileTok;
+  const int64_t ntiles = (T + bo::kTileSmall - 1) / bo::kTileSmall;   // upper bound over both tile sizes
   const int64_t R = T * K;
   const int eb = elem_bytes(c.dtype);
   memset(L, 0, sizeof(*L));
@@ -171,9 +171,8 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   const int m = c.num_experts, K = c.top_k, d = c.hidden, f = c.ffn;
   const int G = (m + c.way - 1) / c.way, E = m + G;
   const int64_t R = T * K;
-  const int ntiles = static_cast<int>(L.ntiles);
   int launches = 0;
-  const int kMaxLaunches = 8;
+  const int kMaxLaunches = 7;
   const bool prof = h->prof_events && h->prof_n >= kMaxLaunches + 1;
   cudaError_t prof_err = cudaSuccess;
   auto mark = [&](int i) {
@@ -199,9 +198,21 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   void* yp = at<char>(ws, L.yp);
   bo_status st;
 
-  // 1. router logits, Eq. 8 (tcgen05 GEMM, fp32 out) -- or injected logits
-  const float* L_use = logits_in;
-  if (!logits_in) {
+  // 1-2. router logits (Eq. 8) + top-K softmax (Eq. 7) + per-tile expert histogram
+  int tile;
+  if (logits_in) {
+    tile = bo::kTileSmall;
+    mark(launches);
+    BO_CUDA(bo::launch_topk_hist(logits_in, static_cast<int>(T), m, K, tile, topk_id, topk_w, tile_cnt, s), "topk");
+    ++launches;
+  } else if (bo::router_small_ok(dt, m, d)) {
+    tile = bo::kTileSmall;   // m <= 32: CUDA-core router, x read once (HBM-bound)
+    mark(launches);
+    BO_CUDA(bo::launch_router_small(dt, x, Wr, static_cast<int>(T), d, m, K, logits, topk_id, topk_w, tile_cnt, s),
+            "router");
+    ++launches;
+  } else {
+    tile = bo::kTileTok;     // tcgen05 router, top-K fused into the epilogue
     CUtensorMap mA, mB;
     const int bn = router_bn(m);
     if ((st = make_map(&mA, x, c.dtype, T, d, bo::kBM)) != BO_OK) return st;
@@ -216,17 +227,17 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
     p.num_exec = 1;
     p.single_rows = static_cast<int>(T);
     p.out = logits;
+    p.topk_k = K;
+    p.topk_id = topk_id;
+    p.topk_w = topk_w;
+    p.tile_cnt = tile_cnt;
     const int work = static_cast<int>((T + bo::kBM - 1) / bo::kBM);
     const int grid = work < h->num_sms ? work : h->num_sms;
     mark(launches);
-    BO_CUDA(bo::launch_grouped_gemm(dt, bo::EPI_F32OUT, bn, mA, mB, mB, mB, mB, p, grid, s), "router gemm");
+    BO_CUDA(bo::launch_grouped_gemm(dt, bo::EPI_ROUTER, bn, mA, mB, mB, mB, mB, p, grid, s), "router gemm");
     ++launches;
-    L_use = logits;
   }
-  // 2. top-K + softmax (Eq. 7) + per-tile histogram
-  mark(launches);
-  BO_CUDA(bo::launch_topk_hist(L_use, static_cast<int>(T), m, K, topk_id, topk_w, tile_cnt, s), "topk");
-  ++launches;
+  const int ntiles = static_cast<int>((T + tile - 1) / tile);
   // 3. Algorithm 1 plan (snapshot of the knob at enqueue time)
   mark(launches);
   BO_CUDA(bo::launch_plan(tile_cnt, ntiles, m, c.way, h->ratio, h->mode, tile_base, counts, exec_of, erow,
@@ -235,7 +246,7 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   ++launches;
   // 4. permutation (rows) and gather (Xp)
   mark(launches);
-  BO_CUDA(bo::launch_permute(topk_id, topk_w, static_cast<int>(T), K, m, tile_base, exec_of, erow, row_of,
+  BO_CUDA(bo::launch_permute(topk_id, topk_w, static_cast<int>(T), K, m, tile, tile_base, exec_of, erow, row_of,
                              row_tok, row_w, s),
           "permute");
   ++launches;

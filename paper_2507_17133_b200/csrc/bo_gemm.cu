@@ -1,7 +1,7 @@
 // bo_gemm.cu - persistent, warp-specialised grouped GEMM on tcgen05 / TMEM / TMA.
 //
 // One engine serves the three dense contractions of the brownout MoE forward:
-//   router   (Eq. 8):  logits[T, m]  = x  Wr^T                (EPI_F32OUT)
+//   router   (Eq. 8):  logits[T, m]  = x  Wr^T                (EPI_ROUTER, top-K fused)
 //   GEMM1    (Eq. 5 FFN, SwiGLU, D13): H[r] = silu(Xp[r] Wg_x^T) * (Xp[r] Wu_x^T)  (EPI_SWIGLU)
 //   GEMM2    (Eq. 5-6):       Yp[r] = row_w[r] * (H[r] Wd_x^T)          (EPI_WEIGHTED)
 // where x is the executor (original expert or united expert, Alg. 1)
@@ -40,7 +40,7 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-  static constexpr int BAR_BYTES = 1024;                 // barriers + tmem slot
+  static constexpr int BAR_BYTES = 2048;                 // barriers + tmem slot (1 KB) + router histogram (1 KB)
   static constexpr int SCHED_BYTES = 2 * (kMaxExec + 1) * 4;
   static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE_BYTES + BAR_BYTES + SCHED_BYTES;
 };
@@ -70,7 +70,26 @@ __device__ __forceinline__ void store_row32<float>(float* dst, const float (&v)[
   for (int q = 0; q < 8; ++q) d[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
 }
 
-template <typename T, int BN, int EPI>
+// Running top-K list, (value desc, id asc); ids arrive in ascending order so a
+// new element only overtakes strictly smaller values (reading D8).
+template <int KMAX>
+__device__ __forceinline__ void topk_insert(float (&tv)[KMAX], int (&ti)[KMAX], int K, float v, int e) {
+#pragma unroll
+  for (int j = KMAX - 1; j >= 0; --j) {
+    if (j < K) {
+      const bool b_j = ti[j] < 0 || v > tv[j];
+      const bool b_jm1 = j > 0 && (ti[j - 1] < 0 || v > tv[j - 1]);
+      if (b_j) {
+        if (b_jm1) { tv[j] = tv[j - 1]; ti[j] = ti[j - 1]; }
+        else { tv[j] = v; ti[j] = e; }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+template <typename T, int BN, int EPI, int KMAX>
 __global__ void __launch_bounds__(192, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
                    const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmB2,
@@ -87,6 +106,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* tfull_bar = empty_bar + STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  int* s_hist = reinterpret_cast<int*>(smem + STAGES * C::STAGE_BYTES + 1024);
   int* s_mtile = reinterpret_cast<int*>(smem + STAGES * C::STAGE_BYTES + C::BAR_BYTES);
   int* s_eoff = s_mtile + (kMaxExec + 1);
 
@@ -156,7 +176,7 @@ __global__ void __launch_bounds__(192, 1)
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       const uint64_t pol_a = policy_evict_last();   // activations are re-read per n-tile
-      const uint64_t pol_b = policy_evict_first();  // weights stream through once per m-tile group
+      const uint64_t pol_b = policy_evict_normal(); // weight tile is re-read by the executor's other m-tiles
       int stage = 0;
       uint32_t phase = 0;
       for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
@@ -253,18 +273,61 @@ __global__ void __launch_bounds__(192, 1)
           if (valid) store_row32<T>(out + c, v);
         }
       } else {
-        float* out = reinterpret_cast<float*>(p.out) + grow * p.ldo;
+        // Router (Eq. 8) with Eq. 7 fused: this thread owns token `grow`'s m logits.
+        float tv[KMAX];
+        int ti[KMAX];
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) { tv[j] = 0.0f; ti[j] = -1; }
+        float* lrow = reinterpret_cast<float*>(p.out) + grow * p.ldo;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           uint32_t a[32];
           tmem_ld32(t0 + c, a);
           tmem_ld_wait();
-          if (valid) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (c + i < p.n_valid) out[c + i] = __uint_as_float(a[i]);
+          for (int i = 0; i < 32; ++i) {
+            const int col = c + i;
+            if (col < p.n_valid) {
+              const float v = __uint_as_float(a[i]);
+              if (valid) lrow[col] = v;
+              topk_insert<KMAX>(tv, ti, p.topk_k, v, col);
+            }
           }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty_bar[acc]);   // TMEM free: the rest is register work
+        const float vmax = tv[0];
+        float ex[KMAX];
+        float sum = 0.0f;
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+          ex[j] = j < p.topk_k ? expf(tv[j] - vmax) : 0.0f;
+          sum += ex[j];
+        }
+        if (valid) {
+#pragma unroll
+          for (int j = 0; j < KMAX; ++j) {
+            if (j < p.topk_k) {
+              p.topk_id[grow * p.topk_k + j] = ti[j];
+              p.topk_w[grow * p.topk_k + j] = ex[j] / sum;
+            }
+          }
+        }
+        // per-tile expert histogram (tile = this 128-token m-tile)
+        const int et = threadIdx.x - 64;
+        epi_bar();
+        for (int e = et; e < p.n_valid; e += 128) s_hist[e] = 0;
+        epi_bar();
+        if (valid) {
+#pragma unroll
+          for (int j = 0; j < KMAX; ++j)
+            if (j < p.topk_k) atomicAdd(&s_hist[ti[j]], 1);
+        }
+        epi_bar();
+        for (int e = et; e < p.n_valid; e += 128) p.tile_cnt[static_cast<int64_t>(mi) * p.n_valid + e] = s_hist[e];
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        continue;
       }
       tc_fence_before();
       __syncwarp();
@@ -282,13 +345,13 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
-template <typename T, int BN, int EPI>
+template <typename T, int BN, int EPI, int KMAX = 0>
 static cudaError_t launch_t(const CUtensorMap& A, const CUtensorMap& B0, const CUtensorMap& B1,
                             const CUtensorMap& B2, const CUtensorMap& B3, const GemmParams& p, int grid,
                             cudaStream_t s) {
   using C = GemmCfg<T, BN>;
   static bool attr_set = false;
-  auto kern = k_grouped_gemm<T, BN, EPI>;
+  auto kern = k_grouped_gemm<T, BN, EPI, KMAX>;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
@@ -309,12 +372,13 @@ static cudaError_t dispatch(int epi, int bn, const CUtensorMap& A, const CUtenso
     if (bn == 256) return launch_t<T, 256, EPI_WEIGHTED>(A, B0, B1, B2, B3, p, grid, s);
     if (bn == 128) return launch_t<T, 128, EPI_WEIGHTED>(A, B0, B1, B2, B3, p, grid, s);
     if (bn == 64) return launch_t<T, 64, EPI_WEIGHTED>(A, B0, B1, B2, B3, p, grid, s);
-  } else if (epi == EPI_F32OUT) {
-    if (bn == 256) return launch_t<T, 256, EPI_F32OUT>(A, B0, B1, B2, B3, p, grid, s);
-    if (bn == 128) return launch_t<T, 128, EPI_F32OUT>(A, B0, B1, B2, B3, p, grid, s);
-    if (bn == 64) return launch_t<T, 64, EPI_F32OUT>(A, B0, B1, B2, B3, p, grid, s);
-    if (bn == 32) return launch_t<T, 32, EPI_F32OUT>(A, B0, B1, B2, B3, p, grid, s);
-    if (bn == 16) return launch_t<T, 16, EPI_F32OUT>(A, B0, B1, B2, B3, p, grid, s);
+  } else if (epi == EPI_ROUTER) {
+    const bool k8 = p.topk_k <= 8;
+#define BO_R(BNV)                                                                        \
+  if (bn == BNV) return k8 ? launch_t<T, BNV, EPI_ROUTER, 8>(A, B0, B1, B2, B3, p, grid, s) \
+                           : launch_t<T, BNV, EPI_ROUTER, 16>(A, B0, B1, B2, B3, p, grid, s);
+    BO_R(256) BO_R(128) BO_R(64) BO_R(32) BO_R(16)
+#undef BO_R
   }
   return cudaErrorInvalidValue;
 }

@@ -7,12 +7,12 @@
 
 namespace bo {
 
-constexpr int kTileTok = 128;   // tokens per histogram / rank tile (top-k + permute)
+constexpr int kTileTok = 128;   // token tile of the tcgen05 router (= GEMM BM)
 constexpr int kBM = 128;        // rows per GEMM tile (TMEM lanes)
 constexpr int kMaxExperts = 256;
 constexpr int kMaxExec = 512;   // m + G
 
-enum Epi : int { EPI_SWIGLU = 0, EPI_WEIGHTED = 1, EPI_F32OUT = 2 };
+enum Epi : int { EPI_SWIGLU = 0, EPI_WEIGHTED = 1, EPI_ROUTER = 2 };
 
 struct GemmParams {
   int Kdim;              // reduction length
@@ -27,6 +27,10 @@ struct GemmParams {
   const int* mtile_off;  // [num_exec+1] prefix of ceil(rows/128) (device)
   void* out;             // output base
   const float* row_w;    // EPI_WEIGHTED: per-row gate weight (Eq. 6)
+  int topk_k;            // EPI_ROUTER: K of Eq. 7
+  int32_t* topk_id;      // EPI_ROUTER: [T, K]
+  float* topk_w;         // EPI_ROUTER: [T, K]
+  int32_t* tile_cnt;     // EPI_ROUTER: [ceil(T/128), m] histogram per 128-token tile
 };
 
 // Grouped tcgen05 GEMM: for each executor x and each 128-row tile of its rows,
@@ -37,14 +41,20 @@ cudaError_t launch_grouped_gemm(int dtype, int epi, int bn, const CUtensorMap& A
                                 const GemmParams& p, int grid, cudaStream_t s);
 int gemm_smem_bytes(int dtype, int epi, int bn);
 
-cudaError_t launch_topk_hist(const float* logits, int T, int m, int K, int32_t* topk_id, float* topk_w,
+constexpr int kTileSmall = 32;  // token tile of the CUDA-core router / injected-logits top-k
+
+cudaError_t launch_topk_hist(const float* logits, int T, int m, int K, int tile, int32_t* topk_id, float* topk_w,
                              int32_t* tile_cnt, cudaStream_t s);
+
+bool router_small_ok(int dtype, int m, int d);
+cudaError_t launch_router_small(int dtype, const void* x, const void* Wr, int T, int d, int m, int K, float* logits,
+                                int32_t* topk_id, float* topk_w, int32_t* tile_cnt, cudaStream_t s);
 
 cudaError_t launch_plan(const int32_t* tile_cnt, int ntiles, int m, int way, double ratio, int mode,
                         int32_t* tile_base, int32_t* counts, int32_t* exec_of_expert, int32_t* expert_row_off,
                         int32_t* exec_off, int32_t* mtile_off, int64_t* stats, cudaStream_t s);
 
-cudaError_t launch_permute(const int32_t* topk_id, const float* topk_w, int T, int K, int m,
+cudaError_t launch_permute(const int32_t* topk_id, const float* topk_w, int T, int K, int m, int tile,
                            const int32_t* tile_base, const int32_t* exec_of_expert,
                            const int32_t* expert_row_off, int32_t* row_of, int32_t* row_tok, float* row_w,
                            cudaStream_t s);

@@ -24,80 +24,213 @@
 namespace bo {
 
 // ----------------------------------------------------------------- top-k
-template <int VPL>   // logits per lane = ceil(m / 32)
-__global__ void __launch_bounds__(256) k_topk_hist(const float* __restrict__ logits, int T, int m, int K,
+// Warp-cooperative Eq. 7 for one token whose m logits are spread over the
+// lanes (expert e = lane + 32*j in v[j]).  K rounds of a shuffle argmax over
+// (logit desc, id asc) (reading D8; -0 == +0 by IEEE comparison), then the
+// softmax over the K selected.  Lane s < K returns slot s (id, weight).
+template <int VPL>
+__device__ __forceinline__ void warp_topk_softmax(const float (&v)[VPL], int m, int K, int lane, int& my_id,
+                                                  float& my_w) {
+  uint32_t taken = 0;
+  my_id = -1;
+  float my_v = 0.0f;
+  for (int s = 0; s < K; ++s) {
+    float bv = -FLT_MAX;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) {
+      const int e = lane + 32 * j;
+      if (e < m && !((taken >> j) & 1u) && (bi == 0x7fffffff || v[j] > bv)) { bv = v[j]; bi = e; }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+      const bool better = oi != 0x7fffffff && (bi == 0x7fffffff || ov > bv || (ov == bv && oi < bi));
+      if (better) { bv = ov; bi = oi; }
+    }
+    if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+    if (lane == s) { my_id = bi; my_v = bv; }
+  }
+  const float vmax = __shfl_sync(0xffffffffu, my_v, 0);   // slot 0 holds the maximum
+  const float ex = lane < K ? expf(my_v - vmax) : 0.0f;
+  float sum = ex;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+  my_w = ex / sum;
+}
+
+// Top-K of given fp32 logits (parity entry / injected logits) + per-tile histogram.
+template <int VPL>
+__global__ void __launch_bounds__(256) k_topk_hist(const float* __restrict__ logits, int T, int m, int K, int tile,
                                                    int32_t* __restrict__ topk_id, float* __restrict__ topk_w,
                                                    int32_t* __restrict__ tile_cnt) {
   __shared__ int hist[kMaxExperts];
   for (int i = threadIdx.x; i < m; i += blockDim.x) hist[i] = 0;
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t0 = blockIdx.x * kTileTok;
-  for (int tt = warp; tt < kTileTok; tt += 8) {
-    const int t = t0 + tt;
-    if (t >= T) break;
+  const int t0 = blockIdx.x * tile;
+  const int t1 = min(t0 + tile, T);
+  for (int t = t0 + warp; t < t1; t += 8) {
     float v[VPL];
 #pragma unroll
     for (int j = 0; j < VPL; ++j) {
       const int e = lane + 32 * j;
-      v[j] = e < m ? logits[static_cast<int64_t>(t) * m + e] : 0.0f;
+      v[j] = e < m ? __ldg(logits + static_cast<int64_t>(t) * m + e) : 0.0f;
     }
-    uint32_t taken = 0;
-    int my_id = -1;
-    float my_v = 0.0f;
-    for (int s = 0; s < K; ++s) {
-      float bv = -FLT_MAX;
-      int bi = 0x7fffffff;
-      bool have = false;
-#pragma unroll
-      for (int j = 0; j < VPL; ++j) {
-        const int e = lane + 32 * j;
-        if (e < m && !((taken >> j) & 1u)) {
-          if (!have || v[j] > bv) { bv = v[j]; bi = e; have = true; }   // j ascending -> id ascending
-        }
-      }
-      if (!have) { bv = -FLT_MAX; bi = 0x7fffffff; }
-      // warp argmax over (value desc, id asc); -0 == +0 by IEEE comparison
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-        const bool o_have = oi != 0x7fffffff;
-        const bool better = o_have && (bi == 0x7fffffff || ov > bv || (ov == bv && oi < bi));
-        if (better) { bv = ov; bi = oi; }
-      }
-      if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
-      if (lane == s) { my_id = bi; my_v = bv; }
-    }
-    // softmax over the K selected logits (Eq. 7); slot 0 holds the maximum
-    const float vmax = __shfl_sync(0xffffffffu, my_v, 0);
-    const float ex = lane < K ? expf(my_v - vmax) : 0.0f;
-    float sum = ex;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+    int id;
+    float w;
+    warp_topk_softmax<VPL>(v, m, K, lane, id, w);
     if (lane < K) {
-      topk_id[static_cast<int64_t>(t) * K + lane] = my_id;
-      topk_w[static_cast<int64_t>(t) * K + lane] = ex / sum;
-      atomicAdd(&hist[my_id], 1);   // integer count in shared memory: order-independent
+      topk_id[static_cast<int64_t>(t) * K + lane] = id;
+      topk_w[static_cast<int64_t>(t) * K + lane] = w;
+      atomicAdd(&hist[id], 1);   // integer count in shared memory: order-independent
     }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < m; i += blockDim.x) tile_cnt[static_cast<int64_t>(blockIdx.x) * m + i] = hist[i];
 }
 
-cudaError_t launch_topk_hist(const float* logits, int T, int m, int K, int32_t* topk_id, float* topk_w,
+cudaError_t launch_topk_hist(const float* logits, int T, int m, int K, int tile, int32_t* topk_id, float* topk_w,
                              int32_t* tile_cnt, cudaStream_t s) {
-  const int ntiles = (T + kTileTok - 1) / kTileTok;
+  const int ntiles = (T + tile - 1) / tile;
   if (ntiles == 0) return cudaSuccess;
   const int vpl = (m + 31) / 32;
   switch (vpl) {
 #define BO_TOPK_CASE(N) \
-  case N: k_topk_hist<N><<<ntiles, 256, 0, s>>>(logits, T, m, K, topk_id, topk_w, tile_cnt); break;
+  case N: k_topk_hist<N><<<ntiles, 256, 0, s>>>(logits, T, m, K, tile, topk_id, topk_w, tile_cnt); break;
     BO_TOPK_CASE(1) BO_TOPK_CASE(2) BO_TOPK_CASE(3) BO_TOPK_CASE(4)
     BO_TOPK_CASE(5) BO_TOPK_CASE(6) BO_TOPK_CASE(7) BO_TOPK_CASE(8)
 #undef BO_TOPK_CASE
     default: return cudaErrorInvalidValue;
   }
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------- small-m router
+// Eq. 8 + Eq. 7 + histogram in one pass for m <= 32 (Mixtral: 8 experts):
+// the contraction has N = m, far too narrow for a tensor-core tile, and the
+// step is bound by reading x once (HBM), so it runs on the CUDA cores with
+// the router centroids staged in shared memory (m*d elements).  Warp per
+// token, 16-byte loads of x, fp32 accumulation, one shuffle all-reduce per
+// expert, then the warp top-K.  32-token tiles -> T/32 CTAs.
+template <typename T, int MAXM>
+__global__ void __launch_bounds__(256) k_router_small(const T* __restrict__ x, const T* __restrict__ Wr, int Tn,
+                                                      int d, int m, int K, float* __restrict__ logits,
+                                                      int32_t* __restrict__ topk_id, float* __restrict__ topk_w,
+                                                      int32_t* __restrict__ tile_cnt) {
+  extern __shared__ uint4 s_wr_raw[];
+  const T* s_wr = reinterpret_cast<const T*>(s_wr_raw);
+  __shared__ int hist[32];
+  constexpr int EPV = 16 / sizeof(T);   // elements per 16-byte vector
+  const int nvec = d / EPV;
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(Wr);
+    uint4* dst = s_wr_raw;
+    for (int i = threadIdx.x; i < m * nvec; i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  if (threadIdx.x < 32) hist[threadIdx.x] = 0;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kTile = 32;
+  const int t0 = blockIdx.x * kTile;
+  const int t1 = min(t0 + kTile, Tn);
+  for (int t = t0 + warp; t < t1; t += 8) {
+    float acc[MAXM];
+#pragma unroll
+    for (int e = 0; e < MAXM; ++e) acc[e] = 0.0f;
+    const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(t) * d);
+    for (int c = lane; c < nvec; c += 32) {
+      const uint4 xv = __ldg(xr + c);
+      float xf[EPV];
+      if constexpr (sizeof(T) == 2) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&xv);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) { const float2 f = __bfloat1622float2(h[i]); xf[2 * i] = f.x; xf[2 * i + 1] = f.y; }
+      } else {
+        const float* f = reinterpret_cast<const float*>(&xv);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) xf[i] = f[i];
+      }
+#pragma unroll
+      for (int e = 0; e < MAXM; ++e) {
+        if (e < m) {
+          const uint4 wv = reinterpret_cast<const uint4*>(s_wr)[e * nvec + c];
+          if constexpr (sizeof(T) == 2) {
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&wv);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float2 f = __bfloat1622float2(h[i]);
+              acc[e] = fmaf(xf[2 * i], f.x, acc[e]);
+              acc[e] = fmaf(xf[2 * i + 1], f.y, acc[e]);
+            }
+          } else {
+            const float* f = reinterpret_cast<const float*>(&wv);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[e] = fmaf(xf[i], f[i], acc[e]);
+          }
+        }
+      }
+    }
+    float v[1];
+    v[0] = 0.0f;
+#pragma unroll
+    for (int e = 0; e < MAXM; ++e) {
+      if (e < m) {
+        float a = acc[e];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+        if (lane == e) v[0] = a;
+      }
+    }
+    if (lane < m) logits[static_cast<int64_t>(t) * m + lane] = v[0];
+    int id;
+    float w;
+    warp_topk_softmax<1>(v, m, K, lane, id, w);
+    if (lane < K) {
+      topk_id[static_cast<int64_t>(t) * K + lane] = id;
+      topk_w[static_cast<int64_t>(t) * K + lane] = w;
+      atomicAdd(&hist[id], 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < m) tile_cnt[static_cast<int64_t>(blockIdx.x) * m + threadIdx.x] = hist[threadIdx.x];
+}
+
+bool router_small_ok(int dtype, int m, int d) {
+  const int eb = dtype == 0 ? 2 : 4;
+  return m <= 32 && static_cast<int64_t>(m) * d * eb <= 160 * 1024;
+}
+
+cudaError_t launch_router_small(int dtype, const void* x, const void* Wr, int T, int d, int m, int K, float* logits,
+                                int32_t* topk_id, float* topk_w, int32_t* tile_cnt, cudaStream_t s) {
+  const int ntiles = (T + 31) / 32;
+  if (ntiles == 0) return cudaSuccess;
+  const int eb = dtype == 0 ? 2 : 4;
+  const int smem = m * d * eb;
+  cudaError_t e = cudaSuccess;
+#define BO_ROUTER_CASE(TYPE, M)                                                                                \
+  {                                                                                                            \
+    auto k = k_router_small<TYPE, M>;                                                                          \
+    static bool set = false;                                                                                   \
+    if (!set) {                                                                                                \
+      e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);                    \
+      if (e != cudaSuccess) return e;                                                                          \
+      set = true;                                                                                              \
+    }                                                                                                          \
+    k<<<ntiles, 256, smem, s>>>(static_cast<const TYPE*>(x), static_cast<const TYPE*>(Wr), T, d, m, K, logits,  \
+                                topk_id, topk_w, tile_cnt);                                                    \
+  }
+  if (dtype == 0) {
+    if (m <= 8) BO_ROUTER_CASE(__nv_bfloat16, 8)
+    else if (m <= 16) BO_ROUTER_CASE(__nv_bfloat16, 16)
+    else BO_ROUTER_CASE(__nv_bfloat16, 32)
+  } else {
+    if (m <= 8) BO_ROUTER_CASE(float, 8)
+    else if (m <= 16) BO_ROUTER_CASE(float, 16)
+    else BO_ROUTER_CASE(float, 32)
+  }
+#undef BO_ROUTER_CASE
   return cudaGetLastError();
 }
 
@@ -261,12 +394,12 @@ cudaError_t launch_plan(const int32_t* tile_cnt, int ntiles, int m, int way, dou
 }
 
 // ----------------------------------------------------------- permutation
-// One CTA per 128-token tile.  Assignments a = t*K + s of the tile are split
+// One CTA per token tile (the tile of the histogram that produced tile_base).  Assignments a = t*K + s of the tile are split
 // into 8 contiguous warp ranges; pass 1 counts per (warp, expert), a prefix
 // over warps gives each warp's start, pass 2 assigns ranks in order.  Row of
 // assignment = expert_row_off[e] + tile_base[tile][e] + rank within the tile.
 __global__ void __launch_bounds__(256) k_permute(const int32_t* __restrict__ topk_id,
-                                                 const float* __restrict__ topk_w, int T, int K, int m,
+                                                 const float* __restrict__ topk_w, int T, int K, int m, int tile,
                                                  const int32_t* __restrict__ tile_base,
                                                  const int32_t* __restrict__ exec_of_expert,
                                                  const int32_t* __restrict__ expert_row_off,
@@ -276,8 +409,8 @@ __global__ void __launch_bounds__(256) k_permute(const int32_t* __restrict__ top
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < 8 * kMaxExperts; i += blockDim.x) (&wcnt[0][0])[i] = 0;
   __syncthreads();
-  const int64_t a0 = static_cast<int64_t>(blockIdx.x) * kTileTok * K;
-  const int64_t a1 = min(static_cast<int64_t>(blockIdx.x + 1) * kTileTok, static_cast<int64_t>(T)) * K;
+  const int64_t a0 = static_cast<int64_t>(blockIdx.x) * tile * K;
+  const int64_t a1 = min(static_cast<int64_t>(blockIdx.x + 1) * tile, static_cast<int64_t>(T)) * K;
   const int n = static_cast<int>(a1 - a0);
   const int per_warp = ((n + 8 * 32 - 1) / (8 * 32)) * 32;
   const int w0 = warp * per_warp;
@@ -327,13 +460,13 @@ __global__ void __launch_bounds__(256) k_permute(const int32_t* __restrict__ top
   }
 }
 
-cudaError_t launch_permute(const int32_t* topk_id, const float* topk_w, int T, int K, int m,
+cudaError_t launch_permute(const int32_t* topk_id, const float* topk_w, int T, int K, int m, int tile,
                            const int32_t* tile_base, const int32_t* exec_of_expert,
                            const int32_t* expert_row_off, int32_t* row_of, int32_t* row_tok, float* row_w,
                            cudaStream_t s) {
-  const int ntiles = (T + kTileTok - 1) / kTileTok;
+  const int ntiles = (T + tile - 1) / tile;
   if (ntiles == 0) return cudaSuccess;
-  k_permute<<<ntiles, 256, 0, s>>>(topk_id, topk_w, T, K, m, tile_base, exec_of_expert, expert_row_off, row_of,
+  k_permute<<<ntiles, 256, 0, s>>>(topk_id, topk_w, T, K, m, tile, tile_base, exec_of_expert, expert_row_off, row_of,
                                    row_tok, row_w);
   return cudaGetLastError();
 }

@@ -99,6 +99,13 @@ SMALL = [
                   config_id=13),
     S.LayerConfig("tiny_fp32", d=64, f=128, m=8, K=2, way=4, T=32, ratio=0.5, dtype="fp32", sigma=0.0,
                   config_id=1),
+    # tcgen05 router paths: m <= 32 with Wr too large for shared memory (BN 32), K > 8 (KMAX 16), fp32/tf32
+    S.LayerConfig("m32_tc_router", d=3072, f=256, m=32, K=4, way=8, T=200, ratio=0.5, dtype="bf16", sigma=0.5,
+                  config_id=14),
+    S.LayerConfig("m64_k10_ragged_groups", d=256, f=128, m=64, K=10, way=5, T=300, ratio=0.5, dtype="bf16",
+                  sigma=0.5, config_id=15),
+    S.LayerConfig("fp32_m64", d=128, f=64, m=64, K=3, way=4, T=100, ratio=0.5, dtype="fp32", sigma=0.5,
+                  config_id=16),
 ]
 
 
@@ -164,7 +171,7 @@ def test_router_logits_vs_fp64(cfg):
     assert (np.abs(Lg - Lr) <= tol).all()
 
 
-@pytest.mark.parametrize("cfg", SMALL[:3], ids=lambda c: c.name)
+@pytest.mark.parametrize("cfg", SMALL, ids=lambda c: c.name)
 def test_full_path_with_router_matches_oracle_when_margins_are_clear(cfg):
     """End to end with the GPU router: when every token's K-th / (K+1)-th fp64
     logit gap exceeds the router error bound, routing cannot differ, so the
