@@ -138,9 +138,10 @@ class Layer:
         self.stream = torch.cuda.current_stream()
 
     def step(self):
+        """One forward on the current stream (the capture stream under a CUDA graph)."""
         L = self.lay
         self.moe.forward(self.x, L["Wr"], (L["Wg"], L["Wu"], L["Wd"]), self.united, y=self.y,
-                         workspace=self.ws, stream=self.stream)
+                         workspace=self.ws, stream=None)
 
     def stats(self):
         import torch
@@ -150,9 +151,14 @@ class Layer:
         return dict(zip(STATS_FIELDS, st))
 
 
-def time_steps(layer, steps, warmup, dist_on, per_kernel=True):
+def time_steps(layer, steps, warmup, dist_on, per_kernel=True, graph=True):
     """W warm-up steps, then K timed steps between barrier + synchronize; device
-    time with CUDA events on the launching stream; max over ranks."""
+    time with CUDA events on the launching stream; max over ranks.
+
+    graph=True: the K steps (each with its own per-kernel event set recorded by
+    the library around every kernel) are captured once into a CUDA graph and
+    the timed region is one replay of it, so host launch overhead does not
+    leak into the device time of small (decode) steps."""
     import torch
     for _ in range(warmup):
         layer.step()
@@ -162,17 +168,38 @@ def time_steps(layer, steps, warmup, dist_on, per_kernel=True):
         ev_sets = [[torch.cuda.Event(enable_timing=True) for _ in range(len(KERNELS) + 1)] for _ in range(steps)]
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
+    g = None
+    if ev_sets:
+        for ev in ev_sets:          # instantiate torch's lazily created events outside the capture
+            for e in ev:
+                e.record()
+        torch.cuda.synchronize()
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            for i in range(steps):
+                if ev_sets:
+                    layer.moe.set_profile_events(ev_sets[i])
+                layer.step()
+        if ev_sets:
+            layer.moe.set_profile_events(None)
+        g.replay()          # upload + one untimed pass
+        torch.cuda.synchronize()
     if dist_on:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    start.record(layer.stream)
-    for i in range(steps):
-        if ev_sets:
-            layer.moe.set_profile_events(ev_sets[i])
-        layer.step()
-    end.record(layer.stream)
+    stream = torch.cuda.current_stream()
+    start.record(stream)
+    if g is not None:
+        g.replay()
+    else:
+        for i in range(steps):
+            if ev_sets:
+                layer.moe.set_profile_events(ev_sets[i])
+            layer.step()
+    end.record(stream)
     torch.cuda.synchronize()
-    if ev_sets:
+    if ev_sets and g is None:
         layer.moe.set_profile_events(None)
     ms = start.elapsed_time(end)
     if dist_on:
@@ -184,6 +211,7 @@ def time_steps(layer, steps, warmup, dist_on, per_kernel=True):
         kern = {}
         for j, name in enumerate(KERNELS):
             kern[name] = sum(ev[j].elapsed_time(ev[j + 1]) for ev in ev_sets) / steps
+    del g
     return ms, kern
 
 
@@ -276,6 +304,7 @@ def main():
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-tokens", type=int, default=32)
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of one CUDA-graph replay")
     args = ap.parse_args()
 
     import torch
@@ -307,7 +336,7 @@ def main():
     launches = layer.moe.last_launch_count()
 
     with ClockSampler(local) as clk:
-        ms, kern = time_steps(layer, args.steps, max(args.warmup, 3), dist_on)
+        ms, kern = time_steps(layer, args.steps, max(args.warmup, 3), dist_on, graph=not args.no_graph)
     clocks = clk.summary()
     ms_step = ms / args.steps
     value = world * cfg.T / (ms_step / 1e3)
@@ -357,7 +386,7 @@ def main():
             layer.moe.set_brownout(r)
             layer.step()
             s_r = layer.stats()
-            ms_r, k_r = time_steps(layer, args.steps, 3, dist_on)
+            ms_r, k_r = time_steps(layer, args.steps, 3, dist_on, graph=not args.no_graph)
             sweep[str(r)] = {"tokens_per_s": world * cfg.T / (ms_r / args.steps / 1e3), "ms": ms_r / args.steps,
                              "executors": s_r["executors_accessed"], "gemm1_ms": k_r["gemm1_swiglu"],
                              "gemm2_ms": k_r["gemm2_weighted"]}
@@ -385,7 +414,7 @@ def main():
                 lay2.moe.set_brownout(r)
                 lay2.step()
                 s2 = lay2.stats()
-                ms2, k2 = time_steps(lay2, args.steps, 3, dist_on)
+                ms2, k2 = time_steps(lay2, args.steps, 3, dist_on, graph=not args.no_graph)
                 a2 = algorithmic(c2, c2.T, s2, c2.d, c2.f, c2.m)
                 t2 = ms2 / args.steps / 1e3
                 res[str(r)] = {"tokens_per_s": world * c2.T / t2, "ms": t2 * 1e3,

@@ -110,7 +110,7 @@ typedef struct {
   size_t h;               /* dtype [T*K, f]     SwiGLU activations                      */
   size_t yp;              /* dtype [T*K, d]     weighted executor outputs               */
   int64_t T;              /* tokens the layout was computed for                          */
-  int64_t ntiles;         /* histogram tiles the workspace is sized for (32 tokens each) */
+  int64_t ntiles;         /* histogram tiles the workspace is sized for (8 tokens each)  */
   int64_t num_executors;  /* E = m + G                                                   */
 } bo_ws_layout;
 

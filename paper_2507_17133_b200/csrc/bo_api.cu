@@ -104,7 +104,7 @@ bo_status compute_layout(const bo_handle* h, int64_t T, bo_ws_layout* L) {
   const bo_config& c = h->cfg;
   const int64_t m = c.num_experts, K = c.top_k, d = c.hidden, f = c.ffn;
   const int64_t G = (m + c.way - 1) / c.way, E = m + G;
-  const int64_t ntiles = (T + bo::kTileSmall - 1) / bo::kTileSmall;   // upper bound over both tile sizes
+  const int64_t ntiles = (T + bo::kTileMin - 1) / bo::kTileMin;   // upper bound over every tile size
   const int64_t R = T * K;
   const int eb = elem_bytes(c.dtype);
   memset(L, 0, sizeof(*L));
@@ -175,8 +175,13 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   const int kMaxLaunches = 7;
   const bool prof = h->prof_events && h->prof_n >= kMaxLaunches + 1;
   cudaError_t prof_err = cudaSuccess;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (prof) prof_err = cudaStreamIsCapturing(s, &cap);
+  // Under stream capture the events must become graph event-record nodes (external).
+  const unsigned rec_flags = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
   auto mark = [&](int i) {
-    if (prof && prof_err == cudaSuccess) prof_err = cudaEventRecord(static_cast<cudaEvent_t>(h->prof_events[i]), s);
+    if (prof && prof_err == cudaSuccess)
+      prof_err = cudaEventRecordWithFlags(static_cast<cudaEvent_t>(h->prof_events[i]), s, rec_flags);
   };
 
   float* logits = at<float>(ws, L.logits);
@@ -206,9 +211,10 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
     BO_CUDA(bo::launch_topk_hist(logits_in, static_cast<int>(T), m, K, tile, topk_id, topk_w, tile_cnt, s), "topk");
     ++launches;
   } else if (bo::router_small_ok(dt, m, d)) {
-    tile = bo::kTileSmall;   // m <= 32: CUDA-core router, x read once (HBM-bound)
+    tile = bo::router_small_tile(static_cast<int>(T), h->num_sms);   // m <= 32: CUDA-core router (HBM-bound)
     mark(launches);
-    BO_CUDA(bo::launch_router_small(dt, x, Wr, static_cast<int>(T), d, m, K, logits, topk_id, topk_w, tile_cnt, s),
+    BO_CUDA(bo::launch_router_small(dt, x, Wr, static_cast<int>(T), d, m, K, tile, logits, topk_id, topk_w,
+                                    tile_cnt, s),
             "router");
     ++launches;
   } else {

@@ -41,14 +41,16 @@ cudaError_t launch_grouped_gemm(int dtype, int epi, int bn, const CUtensorMap& A
                                 const GemmParams& p, int grid, cudaStream_t s);
 int gemm_smem_bytes(int dtype, int epi, int bn);
 
-constexpr int kTileSmall = 32;  // token tile of the CUDA-core router / injected-logits top-k
+constexpr int kTileMin = 8;     // smallest token tile (workspace histograms are sized for it)
+constexpr int kTileSmall = 32;  // token tile of the injected-logits top-k
 
 cudaError_t launch_topk_hist(const float* logits, int T, int m, int K, int tile, int32_t* topk_id, float* topk_w,
                              int32_t* tile_cnt, cudaStream_t s);
 
 bool router_small_ok(int dtype, int m, int d);
-cudaError_t launch_router_small(int dtype, const void* x, const void* Wr, int T, int d, int m, int K, float* logits,
-                                int32_t* topk_id, float* topk_w, int32_t* tile_cnt, cudaStream_t s);
+int router_small_tile(int T, int num_sms);   // 8..32 tokens per CTA
+cudaError_t launch_router_small(int dtype, const void* x, const void* Wr, int T, int d, int m, int K, int tile,
+                                float* logits, int32_t* topk_id, float* topk_w, int32_t* tile_cnt, cudaStream_t s);
 
 cudaError_t launch_plan(const int32_t* tile_cnt, int ntiles, int m, int way, double ratio, int mode,
                         int32_t* tile_base, int32_t* counts, int32_t* exec_of_expert, int32_t* expert_row_off,

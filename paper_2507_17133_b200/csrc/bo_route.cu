@@ -111,63 +111,83 @@ cudaError_t launch_topk_hist(const float* logits, int T, int m, int K, int tile,
 // Eq. 8 + Eq. 7 + histogram in one pass for m <= 32 (Mixtral: 8 experts):
 // the contraction has N = m, far too narrow for a tensor-core tile, and the
 // step is bound by reading x once (HBM), so it runs on the CUDA cores with
-// the router centroids staged in shared memory (m*d elements).  Warp per
-// token, 16-byte loads of x, fp32 accumulation, one shuffle all-reduce per
-// expert, then the warp top-K.  32-token tiles -> T/32 CTAs.
+// the router centroids staged in shared memory by cp.async.  Warp per token,
+// 16-byte loads of x issued in batches of 8 per lane (memory-level
+// parallelism), fp32 accumulation, one shuffle all-reduce per expert, then the
+// warp top-K.  A CTA covers `tile` tokens (8 warps x tile/8 tokens).
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+template <typename T>
+__device__ __forceinline__ void unpack8(const uint4& v, float (&f)[16 / sizeof(T)]) {
+  if constexpr (sizeof(T) == 2) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 t = __bfloat1622float2(h[i]);
+      f[2 * i] = t.x;
+      f[2 * i + 1] = t.y;
+    }
+  } else {
+    f[0] = __uint_as_float(v.x);
+    f[1] = __uint_as_float(v.y);
+    f[2] = __uint_as_float(v.z);
+    f[3] = __uint_as_float(v.w);
+  }
+}
+
 template <typename T, int MAXM>
 __global__ void __launch_bounds__(256) k_router_small(const T* __restrict__ x, const T* __restrict__ Wr, int Tn,
-                                                      int d, int m, int K, float* __restrict__ logits,
+                                                      int d, int m, int K, int tile, float* __restrict__ logits,
                                                       int32_t* __restrict__ topk_id, float* __restrict__ topk_w,
                                                       int32_t* __restrict__ tile_cnt) {
-  extern __shared__ uint4 s_wr_raw[];
-  const T* s_wr = reinterpret_cast<const T*>(s_wr_raw);
+  extern __shared__ uint4 s_wr[];
   __shared__ int hist[32];
   constexpr int EPV = 16 / sizeof(T);   // elements per 16-byte vector
+  constexpr int BATCH = 8;              // 16-byte loads in flight per lane
   const int nvec = d / EPV;
   {
     const uint4* src = reinterpret_cast<const uint4*>(Wr);
-    uint4* dst = s_wr_raw;
-    for (int i = threadIdx.x; i < m * nvec; i += blockDim.x) dst[i] = __ldg(src + i);
+    for (int i = threadIdx.x; i < m * nvec; i += blockDim.x) cp_async16(s_wr + i, src + i);
   }
   if (threadIdx.x < 32) hist[threadIdx.x] = 0;
-  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int kTile = 32;
-  const int t0 = blockIdx.x * kTile;
-  const int t1 = min(t0 + kTile, Tn);
+  const int t0 = blockIdx.x * tile;
+  const int t1 = min(t0 + tile, Tn);
+  bool waited = false;
   for (int t = t0 + warp; t < t1; t += 8) {
     float acc[MAXM];
 #pragma unroll
     for (int e = 0; e < MAXM; ++e) acc[e] = 0.0f;
     const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(t) * d);
-    for (int c = lane; c < nvec; c += 32) {
-      const uint4 xv = __ldg(xr + c);
-      float xf[EPV];
-      if constexpr (sizeof(T) == 2) {
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&xv);
+    for (int c0 = 0; c0 < nvec; c0 += 32 * BATCH) {
+      uint4 xv[BATCH];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) { const float2 f = __bfloat1622float2(h[i]); xf[2 * i] = f.x; xf[2 * i + 1] = f.y; }
-      } else {
-        const float* f = reinterpret_cast<const float*>(&xv);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) xf[i] = f[i];
+      for (int b = 0; b < BATCH; ++b) {
+        const int c = c0 + b * 32 + lane;
+        xv[b] = c < nvec ? __ldg(xr + c) : make_uint4(0, 0, 0, 0);
+      }
+      if (!waited) {   // centroids land in shared memory while the first x batch is in flight
+        cp_async_wait_all();
+        __syncthreads();
+        waited = true;
       }
 #pragma unroll
-      for (int e = 0; e < MAXM; ++e) {
-        if (e < m) {
-          const uint4 wv = reinterpret_cast<const uint4*>(s_wr)[e * nvec + c];
-          if constexpr (sizeof(T) == 2) {
-            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&wv);
+      for (int b = 0; b < BATCH; ++b) {
+        const int c = c0 + b * 32 + lane;
+        if (c < nvec) {
+          float xf[EPV];
+          unpack8<T>(xv[b], xf);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float2 f = __bfloat1622float2(h[i]);
-              acc[e] = fmaf(xf[2 * i], f.x, acc[e]);
-              acc[e] = fmaf(xf[2 * i + 1], f.y, acc[e]);
+          for (int e = 0; e < MAXM; ++e) {
+            if (e < m) {
+              float wf[EPV];
+              unpack8<T>(s_wr[e * nvec + c], wf);
+#pragma unroll
+              for (int i = 0; i < EPV; ++i) acc[e] = fmaf(xf[i], wf[i], acc[e]);
             }
-          } else {
-            const float* f = reinterpret_cast<const float*>(&wv);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) acc[e] = fmaf(xf[i], f[i], acc[e]);
           }
         }
       }
@@ -193,6 +213,10 @@ __global__ void __launch_bounds__(256) k_router_small(const T* __restrict__ x, c
       atomicAdd(&hist[id], 1);
     }
   }
+  if (!waited) {   // warps without tokens still join the block barrier
+    cp_async_wait_all();
+    __syncthreads();
+  }
   __syncthreads();
   if (threadIdx.x < m) tile_cnt[static_cast<int64_t>(blockIdx.x) * m + threadIdx.x] = hist[threadIdx.x];
 }
@@ -202,9 +226,15 @@ bool router_small_ok(int dtype, int m, int d) {
   return m <= 32 && static_cast<int64_t>(m) * d * eb <= 160 * 1024;
 }
 
-cudaError_t launch_router_small(int dtype, const void* x, const void* Wr, int T, int d, int m, int K, float* logits,
-                                int32_t* topk_id, float* topk_w, int32_t* tile_cnt, cudaStream_t s) {
-  const int ntiles = (T + 31) / 32;
+int router_small_tile(int T, int num_sms) {
+  int tpw = T / (8 * num_sms);   // tokens per warp that still fill every SM
+  tpw = tpw < 1 ? 1 : (tpw > 4 ? 4 : tpw);
+  return 8 * tpw;
+}
+
+cudaError_t launch_router_small(int dtype, const void* x, const void* Wr, int T, int d, int m, int K, int tile,
+                                float* logits, int32_t* topk_id, float* topk_w, int32_t* tile_cnt, cudaStream_t s) {
+  const int ntiles = (T + tile - 1) / tile;
   if (ntiles == 0) return cudaSuccess;
   const int eb = dtype == 0 ? 2 : 4;
   const int smem = m * d * eb;
@@ -218,8 +248,8 @@ cudaError_t launch_router_small(int dtype, const void* x, const void* Wr, int T,
       if (e != cudaSuccess) return e;                                                                          \
       set = true;                                                                                              \
     }                                                                                                          \
-    k<<<ntiles, 256, smem, s>>>(static_cast<const TYPE*>(x), static_cast<const TYPE*>(Wr), T, d, m, K, logits,  \
-                                topk_id, topk_w, tile_cnt);                                                    \
+    k<<<ntiles, 256, smem, s>>>(static_cast<const TYPE*>(x), static_cast<const TYPE*>(Wr), T, d, m, K, tile,    \
+                                logits, topk_id, topk_w, tile_cnt);                                            \
   }
   if (dtype == 0) {
     if (m <= 8) BO_ROUTER_CASE(__nv_bfloat16, 8)
@@ -262,17 +292,30 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
   const int G = (m + way - 1) / way;
   const int E = m + G;
 
-  // cnt_i (Alg. 1 input) and per-tile exclusive prefix (for the permutation)
-  if (tid < m) {
-    int c = 0;
-    for (int t = 0; t < ntiles; ++t) {
-      const int v = tile_cnt[static_cast<int64_t>(t) * m + tid];
-      if (tile_base) tile_base[static_cast<int64_t>(t) * m + tid] = c;
-      c += v;
+  // cnt_i (Alg. 1 input) and per-tile exclusive prefix (for the permutation):
+  // warp per expert, lanes over tiles (loads in parallel), shuffle scan + carry.
+  {
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int e = warp; e < m; e += 16) {
+      int carry = 0;
+      for (int t0 = 0; t0 < ntiles; t0 += 32) {
+        const int t = t0 + lane;
+        const int v = t < ntiles ? tile_cnt[static_cast<int64_t>(t) * m + e] : 0;
+        int incl = v;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int o = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= off) incl += o;
+        }
+        if (tile_base && t < ntiles) tile_base[static_cast<int64_t>(t) * m + e] = carry + incl - v;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (lane == 0) {
+        s_cnt[e] = carry;
+        counts[e] = carry;
+      }
     }
-    s_cnt[tid] = c;
-    counts[tid] = c;
-    s_gsize[tid] = 0;
+    if (tid < m) s_gsize[tid] = 0;
   }
   __syncthreads();
   // Alg. 1 line 5: sort by (cnt desc, id asc) -- rank by counting
