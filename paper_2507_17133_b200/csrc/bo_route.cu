@@ -138,15 +138,15 @@ __device__ __forceinline__ void unpack8(const uint4& v, float (&f)[16 / sizeof(T
   }
 }
 
-template <typename T, int MAXM>
+template <typename T, int MAXM, int TPW>
 __global__ void __launch_bounds__(256) k_router_small(const T* __restrict__ x, const T* __restrict__ Wr, int Tn,
-                                                      int d, int m, int K, int tile, float* __restrict__ logits,
+                                                      int d, int m, int K, float* __restrict__ logits,
                                                       int32_t* __restrict__ topk_id, float* __restrict__ topk_w,
                                                       int32_t* __restrict__ tile_cnt) {
   extern __shared__ uint4 s_wr[];
   __shared__ int hist[32];
-  constexpr int EPV = 16 / sizeof(T);   // elements per 16-byte vector
-  constexpr int BATCH = 8;              // 16-byte loads in flight per lane
+  constexpr int EPV = 16 / sizeof(T);         // elements per 16-byte vector
+  constexpr int BATCH = TPW >= 4 ? 2 : 4;     // 16-byte loads per token in flight per lane
   const int nvec = d / EPV;
   {
     const uint4* src = reinterpret_cast<const uint4*>(Wr);
@@ -154,68 +154,80 @@ __global__ void __launch_bounds__(256) k_router_small(const T* __restrict__ x, c
   }
   if (threadIdx.x < 32) hist[threadIdx.x] = 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t0 = blockIdx.x * tile;
-  const int t1 = min(t0 + tile, Tn);
+  const int tbase = blockIdx.x * (8 * TPW) + warp * TPW;   // this warp's TPW consecutive tokens
+  float acc[TPW][MAXM];
+#pragma unroll
+  for (int i = 0; i < TPW; ++i)
+#pragma unroll
+    for (int e = 0; e < MAXM; ++e) acc[i][e] = 0.0f;
   bool waited = false;
-  for (int t = t0 + warp; t < t1; t += 8) {
-    float acc[MAXM];
+  for (int c0 = 0; c0 < nvec; c0 += 32 * BATCH) {
+    uint4 xv[TPW][BATCH];
 #pragma unroll
-    for (int e = 0; e < MAXM; ++e) acc[e] = 0.0f;
-    const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(t) * d);
-    for (int c0 = 0; c0 < nvec; c0 += 32 * BATCH) {
-      uint4 xv[BATCH];
+    for (int i = 0; i < TPW; ++i) {
+      const int t = tbase + i;
 #pragma unroll
       for (int b = 0; b < BATCH; ++b) {
         const int c = c0 + b * 32 + lane;
-        xv[b] = c < nvec ? __ldg(xr + c) : make_uint4(0, 0, 0, 0);
+        xv[i][b] = (t < Tn && c < nvec) ? __ldg(reinterpret_cast<const uint4*>(x + static_cast<int64_t>(t) * d) + c)
+                                        : make_uint4(0, 0, 0, 0);
       }
-      if (!waited) {   // centroids land in shared memory while the first x batch is in flight
-        cp_async_wait_all();
-        __syncthreads();
-        waited = true;
-      }
+    }
+    if (!waited) {   // centroids land in shared memory while the first x batch is in flight
+      cp_async_wait_all();
+      __syncthreads();
+      waited = true;
+    }
 #pragma unroll
-      for (int b = 0; b < BATCH; ++b) {
-        const int c = c0 + b * 32 + lane;
-        if (c < nvec) {
-          float xf[EPV];
-          unpack8<T>(xv[b], xf);
+    for (int b = 0; b < BATCH; ++b) {
+      const int c = c0 + b * 32 + lane;
+      if (c < nvec) {
+        float xf[TPW][EPV];
 #pragma unroll
-          for (int e = 0; e < MAXM; ++e) {
-            if (e < m) {
-              float wf[EPV];
-              unpack8<T>(s_wr[e * nvec + c], wf);
+        for (int i = 0; i < TPW; ++i) unpack8<T>(xv[i][b], xf[i]);
 #pragma unroll
-              for (int i = 0; i < EPV; ++i) acc[e] = fmaf(xf[i], wf[i], acc[e]);
-            }
+        for (int e = 0; e < MAXM; ++e) {
+          if (e < m) {
+            float wf[EPV];
+            unpack8<T>(s_wr[e * nvec + c], wf);   // one shared load feeds TPW tokens
+#pragma unroll
+            for (int i = 0; i < TPW; ++i)
+#pragma unroll
+              for (int k = 0; k < EPV; ++k) acc[i][e] = fmaf(xf[i][k], wf[k], acc[i][e]);
           }
         }
       }
     }
+  }
+  if (!waited) {
+    cp_async_wait_all();
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < TPW; ++i) {
+    const int t = tbase + i;
     float v[1];
     v[0] = 0.0f;
 #pragma unroll
     for (int e = 0; e < MAXM; ++e) {
       if (e < m) {
-        float a = acc[e];
+        float a = acc[i][e];
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
         if (lane == e) v[0] = a;
       }
     }
-    if (lane < m) logits[static_cast<int64_t>(t) * m + lane] = v[0];
-    int id;
-    float w;
-    warp_topk_softmax<1>(v, m, K, lane, id, w);
-    if (lane < K) {
-      topk_id[static_cast<int64_t>(t) * K + lane] = id;
-      topk_w[static_cast<int64_t>(t) * K + lane] = w;
-      atomicAdd(&hist[id], 1);
+    if (t < Tn) {   // warp-uniform
+      if (lane < m) logits[static_cast<int64_t>(t) * m + lane] = v[0];
+      int id;
+      float w;
+      warp_topk_softmax<1>(v, m, K, lane, id, w);
+      if (lane < K) {
+        topk_id[static_cast<int64_t>(t) * K + lane] = id;
+        topk_w[static_cast<int64_t>(t) * K + lane] = w;
+        atomicAdd(&hist[id], 1);
+      }
     }
-  }
-  if (!waited) {   // warps without tokens still join the block barrier
-    cp_async_wait_all();
-    __syncthreads();
   }
   __syncthreads();
   if (threadIdx.x < m) tile_cnt[static_cast<int64_t>(blockIdx.x) * m + threadIdx.x] = hist[threadIdx.x];
@@ -227,8 +239,7 @@ bool router_small_ok(int dtype, int m, int d) {
 }
 
 int router_small_tile(int T, int num_sms) {
-  int tpw = T / (8 * num_sms);   // tokens per warp that still fill every SM
-  tpw = tpw < 1 ? 1 : (tpw > 4 ? 4 : tpw);
+  const int tpw = T >= 4 * 8 * num_sms ? 4 : (T >= 2 * 8 * num_sms ? 2 : 1);   // tokens per warp, SMs stay full
   return 8 * tpw;
 }
 
@@ -239,131 +250,157 @@ cudaError_t launch_router_small(int dtype, const void* x, const void* Wr, int T,
   const int eb = dtype == 0 ? 2 : 4;
   const int smem = m * d * eb;
   cudaError_t e = cudaSuccess;
-#define BO_ROUTER_CASE(TYPE, M)                                                                                \
+#define BO_ROUTER_CASE(TYPE, M, TPW)                                                                           \
   {                                                                                                            \
-    auto k = k_router_small<TYPE, M>;                                                                          \
+    auto k = k_router_small<TYPE, M, TPW>;                                                                     \
     static bool set = false;                                                                                   \
     if (!set) {                                                                                                \
       e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);                    \
       if (e != cudaSuccess) return e;                                                                          \
       set = true;                                                                                              \
     }                                                                                                          \
-    k<<<ntiles, 256, smem, s>>>(static_cast<const TYPE*>(x), static_cast<const TYPE*>(Wr), T, d, m, K, tile,    \
-                                logits, topk_id, topk_w, tile_cnt);                                            \
+    k<<<ntiles, 256, smem, s>>>(static_cast<const TYPE*>(x), static_cast<const TYPE*>(Wr), T, d, m, K, logits,  \
+                                topk_id, topk_w, tile_cnt);                                                    \
   }
+#define BO_ROUTER_M(TYPE, TPW)                      \
+  if (m <= 8) BO_ROUTER_CASE(TYPE, 8, TPW)          \
+  else if (m <= 16) BO_ROUTER_CASE(TYPE, 16, TPW)   \
+  else BO_ROUTER_CASE(TYPE, 32, TPW)
+  const int tpw = tile / 8;
   if (dtype == 0) {
-    if (m <= 8) BO_ROUTER_CASE(__nv_bfloat16, 8)
-    else if (m <= 16) BO_ROUTER_CASE(__nv_bfloat16, 16)
-    else BO_ROUTER_CASE(__nv_bfloat16, 32)
+    if (tpw == 1) { BO_ROUTER_M(__nv_bfloat16, 1) }
+    else if (tpw == 2) { BO_ROUTER_M(__nv_bfloat16, 2) }
+    else { BO_ROUTER_M(__nv_bfloat16, 4) }
   } else {
-    if (m <= 8) BO_ROUTER_CASE(float, 8)
-    else if (m <= 16) BO_ROUTER_CASE(float, 16)
-    else BO_ROUTER_CASE(float, 32)
+    if (tpw == 1) { BO_ROUTER_M(float, 1) }
+    else if (tpw == 2) { BO_ROUTER_M(float, 2) }
+    else { BO_ROUTER_M(float, 4) }
   }
+#undef BO_ROUTER_M
 #undef BO_ROUTER_CASE
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------ Algorithm 1
-// Inclusive block scan over blockDim.x (= 512) ints in shared memory.
-__device__ __forceinline__ void block_scan_incl(int* buf) {
-  for (int off = 1; off < static_cast<int>(blockDim.x); off <<= 1) {
-    const int v = threadIdx.x >= off ? buf[threadIdx.x - off] : 0;
-    __syncthreads();
-    buf[threadIdx.x] += v;
-    __syncthreads();
+// Exclusive scan of one int per thread over the whole block (16 warps):
+// warp shuffle scan, warp totals through shared memory.  Returns the
+// exclusive prefix; *total receives the block sum.
+__device__ __forceinline__ long long block_excl_scan(long long v, long long* s_warp, long long* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  long long incl = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const long long o = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += o;
   }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    long long w = lane < nw ? s_warp[lane] : 0;
+    long long wi = w;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const long long o = __shfl_up_sync(0xffffffffu, wi, off);
+      if (lane >= off) wi += o;
+    }
+    if (lane < nw) s_warp[lane] = wi - w;            // exclusive warp offsets
+    if (lane == 31) s_warp[32] = wi;                 // block total
+  }
+  __syncthreads();
+  const long long r = s_warp[warp] + incl - v;
+  *total = s_warp[32];
+  __syncthreads();   // s_warp reusable after return
+  return r;
 }
+
+constexpr int kPlanStage = 8192;    // tile histograms staged in shared memory when ntiles*m fits
 
 __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_cnt, int ntiles, int m, int way,
                                               double ratio, int mode, int32_t* __restrict__ tile_base,
                                               int32_t* __restrict__ counts, int32_t* __restrict__ exec_of_expert,
                                               int32_t* __restrict__ expert_row_off, int32_t* __restrict__ exec_off,
                                               int32_t* __restrict__ mtile_off, int64_t* __restrict__ stats) {
+  __shared__ int s_tc[kPlanStage];
   __shared__ int s_cnt[kMaxExperts];
   __shared__ int s_sorted[kMaxExperts];
   __shared__ long long s_excl[kMaxExperts];
   __shared__ int s_gsize[kMaxExperts];
   __shared__ int s_exec[kMaxExperts];
-  __shared__ int s_scan[kMaxExec];
-  __shared__ int s_scan2[kMaxExec];
-  __shared__ long long s_S;
+  __shared__ int s_xoff[kMaxExec];
+  __shared__ long long s_warp[33];
   const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
   const int G = (m + way - 1) / way;
   const int E = m + G;
+  const int n_tc = ntiles * m;
+  const bool staged = n_tc <= kPlanStage;
 
-  // cnt_i (Alg. 1 input) and per-tile exclusive prefix (for the permutation):
-  // warp per expert, lanes over tiles (loads in parallel), shuffle scan + carry.
-  {
-    const int warp = tid >> 5, lane = tid & 31;
-    for (int e = warp; e < m; e += 16) {
-      int carry = 0;
-      for (int t0 = 0; t0 < ntiles; t0 += 32) {
-        const int t = t0 + lane;
-        const int v = t < ntiles ? tile_cnt[static_cast<int64_t>(t) * m + e] : 0;
-        int incl = v;
+  // 1. cnt_i (Alg. 1 input) and the per-tile exclusive prefix used by
+  //    the permutation.  Histograms are staged with coalesced loads, then a
+  //    warp per expert scans over tiles (lanes over tiles, shuffle scan + carry).
+  if (staged)
+    for (int i = tid; i < n_tc; i += blockDim.x) s_tc[i] = __ldg(tile_cnt + i);
+  if (tid < m) s_gsize[tid] = 0;
+  __syncthreads();
+  for (int e = warp; e < m; e += 16) {
+    int carry = 0;
+    for (int t0 = 0; t0 < ntiles; t0 += 32) {
+      const int t = t0 + lane;
+      const int v = t < ntiles ? (staged ? s_tc[t * m + e] : __ldg(tile_cnt + static_cast<int64_t>(t) * m + e)) : 0;
+      int incl = v;
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const int o = __shfl_up_sync(0xffffffffu, incl, off);
-          if (lane >= off) incl += o;
-        }
-        if (tile_base && t < ntiles) tile_base[static_cast<int64_t>(t) * m + e] = carry + incl - v;
-        carry += __shfl_sync(0xffffffffu, incl, 31);
+      for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += o;
       }
-      if (lane == 0) {
-        s_cnt[e] = carry;
-        counts[e] = carry;
-      }
+      if (tile_base && t < ntiles) tile_base[static_cast<int64_t>(t) * m + e] = carry + incl - v;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
     }
-    if (tid < m) s_gsize[tid] = 0;
+    if (lane == 0) {
+      s_cnt[e] = carry;
+      counts[e] = carry;
+    }
   }
   __syncthreads();
-  // Alg. 1 line 5: sort by (cnt desc, id asc) -- rank by counting
+  // 2. Alg. 1 line 5: order by (cnt desc, id asc) (D5) -- rank by counting
+  const int c_me = tid < m ? s_cnt[tid] : 0;
   if (tid < m) {
-    const int c = s_cnt[tid];
     int pos = 0;
     for (int j = 0; j < m; ++j) {
       const int cj = s_cnt[j];
-      pos += (cj > c) || (cj == c && j < tid);
+      pos += (cj > c_me) | ((cj == c_me) & (j < tid));
     }
     s_sorted[pos] = tid;
   }
-  if (tid == 0) {
-    long long S = 0;
-    for (int j = 0; j < m; ++j) S += s_cnt[j];   // Alg. 1 line 6
-    s_S = S;
-  }
   __syncthreads();
-  // exclusive prefix sum_partial in sorted order (lines 8-15)
-  if (tid < m) {
-    long long excl = 0;
-    for (int j = 0; j < tid; ++j) excl += s_cnt[s_sorted[j]];
-    s_excl[s_sorted[tid]] = excl;
-  }
+  // 3. lines 6-15: S and the exclusive prefix sum_partial in sorted order
+  long long S;
+  const long long excl = block_excl_scan(tid < m ? s_cnt[s_sorted[tid]] : 0, s_warp, &S);
+  if (tid < m) s_excl[s_sorted[tid]] = excl;
   __syncthreads();
-  // line 7: T = S * threshold, threshold = 1 - ratio, fp64 (D3)
-  const double threshold = 1.0 - ratio;
-  const double Tcov = static_cast<double>(s_S) * threshold;
+  const double threshold = 1.0 - ratio;                // D2
+  const double Tcov = static_cast<double>(S) * threshold;   // line 7, fp64 (D3)
   bool in_s1 = false, in_s2 = false;
   if (tid < m) {
-    const bool active = s_cnt[tid] > 0;               // D6
-    in_s1 = active && static_cast<double>(s_excl[tid]) < Tcov;   // D1
+    const bool active = c_me > 0;                                 // D6
+    in_s1 = active && static_cast<double>(s_excl[tid]) < Tcov;    // D1
     in_s2 = active && !in_s1;
-    if (in_s2) atomicAdd(&s_gsize[tid / way], 1);     // group_experts (line 23); integer
+    if (in_s2) atomicAdd(&s_gsize[tid / way], 1);     // group_experts (line 23); integer count
   }
   __syncthreads();
+  // 4. executor of each expert (lines 16-30)
+  int x_me = -1;
   if (tid < m) {
-    int x;
-    if (in_s1) x = tid;                               // lines 16-18
-    else if (!in_s2) x = -1;                          // inactive
-    else if (mode == 1) x = -2;                       // full brownout: ignored
-    else if (s_gsize[tid / way] == 1) x = tid;        // special case (lines 24-26)
-    else x = m + tid / way;                           // united expert of the group (lines 27-30)
-    s_exec[tid] = x;
-    exec_of_expert[tid] = x;
+    if (in_s1) x_me = tid;                               // original expert
+    else if (!in_s2) x_me = -1;                          // inactive
+    else if (mode == 1) x_me = -2;                       // full brownout: ignored
+    else if (s_gsize[tid / way] == 1) x_me = tid;        // special case
+    else x_me = m + tid / way;                           // united expert of group tid / way
+    s_exec[tid] = x_me;
+    exec_of_expert[tid] = x_me;
   }
   __syncthreads();
-  // rows per executor, exec_off = exclusive scan
+  // 5. rows per executor, exec_off / mtile_off = exclusive scans over executors
   int rows = 0;
   if (tid < E) {
     if (tid < m) {
@@ -375,56 +412,47 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
         if (s_exec[e] == tid) rows += s_cnt[e];
     }
   }
-  s_scan[tid] = tid < E ? rows : 0;
-  s_scan2[tid] = tid < E ? (rows + kBM - 1) / kBM : 0;
-  __syncthreads();
-  block_scan_incl(s_scan);
-  block_scan_incl(s_scan2);
+  long long R_total;
+  const long long xoff = block_excl_scan(rows, s_warp, &R_total);
+  long long MT_total;
+  const long long moff = block_excl_scan((rows + kBM - 1) / kBM, s_warp, &MT_total);
   if (tid < E) {
-    exec_off[tid + 1] = s_scan[tid];
-    mtile_off[tid + 1] = s_scan2[tid];
+    exec_off[tid] = static_cast<int>(xoff);
+    mtile_off[tid] = static_cast<int>(moff);
+    s_xoff[tid] = static_cast<int>(xoff);
   }
   if (tid == 0) {
-    exec_off[0] = 0;
-    mtile_off[0] = 0;
+    exec_off[E] = static_cast<int>(R_total);
+    mtile_off[E] = static_cast<int>(MT_total);
   }
-  // expert_row_off: executor start + earlier members of the same executor (D11)
+  __syncthreads();
+  // 6. expert_row_off: executor start + earlier members of the same executor (D11)
   if (tid < m) {
-    const int x = s_exec[tid];
     int off = -1;
-    if (x >= 0) {
-      off = x == 0 ? 0 : s_scan[x - 1];
-      if (x >= m) {
-        for (int e = (x - m) * way; e < tid; ++e)
-          if (s_exec[e] == x) off += s_cnt[e];
-      }
+    if (x_me >= 0) {
+      off = s_xoff[x_me];
+      if (x_me >= m)
+        for (int e = (x_me - m) * way; e < tid; ++e)
+          if (s_exec[e] == x_me) off += s_cnt[e];
     }
     expert_row_off[tid] = off;
   }
+  // 7. statistics (P:173 / P:194 access counts, rows per class)
+  const int n_acc = __syncthreads_count(tid < E && rows > 0);
+  const int n_uni = __syncthreads_count(tid >= m && tid < E && rows > 0);
+  const int n_s1 = __syncthreads_count(in_s1);
+  const int n_single = __syncthreads_count(in_s2 && x_me == tid);
+  long long r_orig;
+  block_excl_scan(tid < m ? rows : 0, s_warp, &r_orig);
   if (tid == 0) {
-    long long accessed = 0, n_s1 = 0, n_united = 0, n_single = 0, r_orig = 0, r_uni = 0, r_drop = 0;
-    for (int x = 0; x < E; ++x) {
-      const int r = s_scan[x] - (x ? s_scan[x - 1] : 0);
-      if (r > 0) {
-        ++accessed;
-        if (x >= m) ++n_united;
-        if (x < m) r_orig += r; else r_uni += r;
-      }
-    }
-    for (int e = 0; e < m; ++e) {
-      if (s_cnt[e] == 0) continue;
-      if (s_exec[e] == -2) r_drop += s_cnt[e];
-      if (static_cast<double>(s_excl[e]) < Tcov) ++n_s1;
-      else if (s_exec[e] == e) ++n_single;
-    }
-    stats[0] = accessed;
+    stats[0] = n_acc;
     stats[1] = n_s1;
-    stats[2] = n_united;
+    stats[2] = n_uni;
     stats[3] = n_single;
     stats[4] = r_orig;
-    stats[5] = r_uni;
-    stats[6] = r_drop;
-    stats[7] = s_S;
+    stats[5] = R_total - r_orig;
+    stats[6] = S - R_total;
+    stats[7] = S;
   }
 }
 
