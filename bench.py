@@ -318,10 +318,15 @@ def main():
     if args.impl == "reference":
         return run_reference(args, cfg, rank, world)
 
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dist_on = world > 1
     if dist_on:
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BO_DIST_BACKEND", "nccl")   # gloo: 2 ranks on 1 GPU (test rigs)
+        if backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            torch.distributed.init_process_group(backend)
     from paper_2507_17133_b200.build import build
     if rank == 0:
         build()
@@ -329,6 +334,8 @@ def main():
         torch.distributed.barrier()
 
     pk = peaks()
+    if dist_on:
+        return run_ep(args, cfg, rank, world, local, pk)
     layer = Layer(cfg, "cuda")
     layer.moe.set_brownout(cfg.ratio)
     layer.step()
@@ -441,6 +448,105 @@ def main():
         print(json.dumps(out), flush=True)
     if dist_on:
         torch.distributed.destroy_process_group()
+
+
+def run_ep(args, cfg, rank, world, local, pk):
+    """N > 1: expert-parallel forward (paper_2507_17133_b200.ep) over NCCL.  Weak
+    scaling: every rank owns cfg.T tokens of the global batch (N x T tokens);
+    experts are sharded, united experts f-sliced over their group's ranks."""
+    import torch
+    import torch.distributed as dist
+    import synthetic as S
+    from paper_2507_17133_b200 import BrownoutMoE
+    from paper_2507_17133_b200.ep import EPMoE, EPPlanner, TorchComm
+
+    sizes = [64, 256, 1024, 4096, 16384] if not args.no_sweep else []
+    tmax = max([cfg.T] + sizes)
+    lay = S.make_layer(cfg, device="cuda")          # same seed on every rank: identical weights
+    moe = BrownoutMoE(cfg.d, cfg.f, cfg.m, cfg.K, cfg.way, dtype=cfg.dtype, max_tokens=tmax)
+    moe.set_brownout(cfg.ratio)
+    united = moe.build_united(lay["Wg"], lay["Wu"], lay["Wd"])
+    pl = EPPlanner(cfg.m, cfg.way, cfg.f, world)
+    ep = EPMoE(moe, pl, rank, (lay["Wg"], lay["Wu"], lay["Wd"]), united, cfg.d, cfg.K, S.torch_dtype(cfg.dtype))
+    comm = TorchComm()
+    xg = S.make_tokens(cfg, T=tmax * world, device="cuda")
+
+    def timed(T, steps, warmup, timers=False):
+        x = xg[rank * T:(rank + 1) * T].contiguous()
+        for _ in range(warmup):
+            ep.forward(x, lay["Wr"], comm)
+        torch.cuda.synchronize()
+        ffn = []
+        if timers:
+            ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(steps)]
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dist.barrier()
+        torch.cuda.synchronize()
+        a.record()
+        for i in range(steps):
+            if timers:
+                ep.timers = ev[i]
+            ep.forward(x, lay["Wr"], comm)
+        b.record()
+        torch.cuda.synchronize()
+        ep.timers = None
+        ms = a.elapsed_time(b)
+        if timers:
+            ffn = [e[0].elapsed_time(e[1]) for e in ev]
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()) / steps, (sum(ffn) / len(ffn) if ffn else None)
+
+    with ClockSampler(local) as clk:
+        ms_step, ffn_ms = timed(cfg.T, args.steps, max(args.warmup, 3), timers=True)
+    clocks = clk.summary()
+    value = world * cfg.T / (ms_step / 1e3)
+    ach = ep.last_ffn_flops / (ffn_ms / 1e3) / 1e12
+    roof = {"kernel": "expert_ffn (gemm1_swiglu + gemm2_weighted, rank-local executors)", "bound": "tensor",
+            "achieved": ach, "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
+            "frac": ach / pk["bf16_tflops_sustained"], "peak_note": "sustained bf16; " + pk["source"],
+            "algorithmic_per_launch": ep.last_ffn_flops, "traffic": None}
+    out = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+           "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (seeded; random-init Mixtral-shaped weights)",
+           "config": {"workload": cfg.name, "T_per_rank": cfg.T, "global_batch": cfg.T * world, "d": cfg.d,
+                      "f": cfg.f, "m": cfg.m, "K": cfg.K, "way": cfg.way, "ratio": cfg.ratio,
+                      "parallelism": f"ep{world}", "united_f_slices": pl.n_slices,
+                      "l2": "inputs larger than L2 (expert weights)"},
+           "roofline": roof, "gpu_launches": 10 * args.steps, "clocks": clocks}
+    # e2e through the public API: pinned host tokens in, pinned host output back, every step
+    x = xg[rank * cfg.T:(rank + 1) * cfg.T]
+    hx = x.cpu().pin_memory()
+    hy = torch.empty(hx.shape, dtype=hx.dtype, pin_memory=True)
+    dx = torch.empty_like(x)
+    for _ in range(2):
+        dx.copy_(hx, non_blocking=True)
+        hy.copy_(ep.forward(dx, lay["Wr"], comm), non_blocking=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_e2e = max(3, args.steps // 2)
+    a.record()
+    for _ in range(n_e2e):
+        dx.copy_(hx, non_blocking=True)
+        hy.copy_(ep.forward(dx, lay["Wr"], comm), non_blocking=True)
+    b.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([a.elapsed_time(b) / n_e2e], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+    out["e2e"] = {"value": world * cfg.T / (e2e_ms / 1e3), "unit": "tokens/s", "ms_per_step": e2e_ms,
+                  "h2d_bytes_per_step": hx.numel() * hx.element_size(),
+                  "d2h_bytes_per_step": hy.numel() * hy.element_size()}
+    if sizes:   # C5: bursty per-rank batch sizes
+        sw = {}
+        for T in sizes:
+            ms, _ = timed(T, max(3, args.steps // 2), 2)
+            sw[str(T)] = {"tokens_per_s": world * T / (ms / 1e3), "ms": ms}
+        out["batch_sweep"] = sw
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    dist.destroy_process_group()
 
 
 def run_reference(args, cfg, rank, world):

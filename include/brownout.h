@@ -172,6 +172,61 @@ BO_API bo_status bo_plan_from_counts(bo_handle* h, const int32_t* counts, int32_
                               int32_t* expert_row_off, int32_t* exec_off, void* stats,
                               void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Building blocks of the expert-parallel forward:
+ * the same stages as bo_moe_forward, exposed so that the exchange between
+ * ranks (count all-gather, dispatch / combine all-to-all over NVLink) can sit
+ * between them.  All pointers are device pointers; all calls are stream-ordered.
+ * ------------------------------------------------------------------------- */
+
+/* a1-a4 on a local batch: router (Eq. 8), top-K (Eq. 7), per-tile histogram,
+ * cnt_i and the per-tile prefix, and Alg. 1 over this batch alone.  Results stay
+ * in the workspace at the offsets of bo_workspace_layout(T) (counts, tile_base,
+ * topk_id/topk_w, ...).  logits_in as in bo_moe_forward_ex. */
+BO_API bo_status bo_route(bo_handle* h, const void* x, int64_t T, const void* Wr, const float* logits_in,
+                          void* workspace, size_t ws_bytes, void* stream);
+
+/* Alg. 1 on the column sums of counts [nrows, m] (int32; one row per
+ * rank under expert parallelism, D18: one global plan).  Outputs as
+ * bo_plan_from_counts (exec_off: >= 2*(E+1) + m int32, first E+1 meaningful). */
+BO_API bo_status bo_plan_counts(bo_handle* h, const int32_t* counts, int32_t nrows, int32_t* exec_of_expert,
+                                int32_t* expert_row_off, int32_t* exec_off, void* stats, void* stream);
+
+/* a5 with a caller-chosen row layout, for the batch of the last bo_route on this
+ * handle (same T and workspace): the row of (token t, slot s, replica r), routed
+ * to expert e, is row_base[e*nrep + r] + (stable rank of t among the batch's
+ * tokens routed to e); row_base < 0 means "no row".  Writes rows_out[row] = x[t]
+ * (d elements), w_out[row] = g[t,s] (Eq. 6 p/q) and row_of[(t*K + s)*nrep + r]
+ * (-1 where no row).  nrep in [1, 8]. */
+BO_API bo_status bo_dispatch(bo_handle* h, int64_t T, void* workspace, size_t ws_bytes, const int32_t* row_base,
+                             int32_t nrep, const void* x, void* rows_out, float* w_out, int32_t* row_of,
+                             void* stream);
+
+/* Row-block permutation: for every dst row i with dst_start[b] <= i < dst_start[b+1]
+ * (b < n_blocks, dst_start has n_blocks + 1 entries, dst_start[n_blocks] = total_rows)
+ * dst[i] = src[src_off[b] + i - dst_start[b]] (row_bytes, multiple of 16) and,
+ * if w_src != NULL, w_dst[i] = w_src[...]. */
+BO_API bo_status bo_block_copy(bo_handle* h, const void* src, void* dst, int32_t row_bytes, const float* w_src,
+                               float* w_dst, int32_t n_blocks, const int32_t* src_off, const int32_t* dst_start,
+                               int64_t total_rows, void* stream);
+
+/* a6-a7 on rows already grouped by executor: rows [R, d], row_w [R];
+ * exec_off / mtile_off [n_orig + n_united + 1] (row offsets and prefix of
+ * ceil(rows/128)); executors [0, n_orig) use Wg/Wu [n_orig, f, d], Wd [n_orig, d, f];
+ * executors [n_orig, n_orig + n_united) use UWg/UWu [n_united, f_united, d],
+ * UWd [n_united, d, f_united] (f_united <= f, a multiple of 128: expert-parallel
+ * f-slices of united experts; SwiGLU is elementwise in f so slice outputs add).
+ * h_buf [R, f] scratch; out [R, d] = row_w * FFN(rows). */
+BO_API bo_status bo_expert_ffn(bo_handle* h, const void* rows, int64_t R, const float* row_w, const int32_t* exec_off,
+                               const int32_t* mtile_off, int32_t n_orig, int32_t n_united, int32_t f_united,
+                               const void* Wg, const void* Wu, const void* Wd, const void* UWg, const void* UWu,
+                               const void* UWd, void* h_buf, void* out, void* stream);
+
+/* a8: y[t] = [x_t] + sum over (slot, replica) of rows[row_of[(t*K + s)*nrep + r]]
+ * in fp32, slot order then replica order (Eq. 5). */
+BO_API bo_status bo_combine(bo_handle* h, int64_t T, const void* rows, const int32_t* row_of, int32_t nrep,
+                            const void* x, void* y, void* stream);
+
 /* Optional per-kernel timing: when `events` (an array of n cudaEvent_t cast
  * to void*) is non-NULL, each following forward records events[i] on its
  * stream immediately before its i-th kernel launch and events[L] after the

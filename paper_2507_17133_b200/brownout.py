@@ -23,6 +23,7 @@ BO_UNITED_MEAN = 0
 EXPORTED = (
     "bo_create", "bo_destroy", "bo_workspace_size", "bo_workspace_layout", "bo_build_united",
     "bo_set_brownout", "bo_get_brownout", "bo_moe_forward", "bo_moe_forward_ex", "bo_plan_from_counts",
+    "bo_route", "bo_plan_counts", "bo_dispatch", "bo_block_copy", "bo_expert_ffn", "bo_combine",
     "bo_set_profile_events", "bo_last_launch_count", "bo_status_string", "bo_last_error", "bo_version",
 )
 
@@ -71,6 +72,12 @@ def _load():
         "bo_moe_forward": ([vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp], C.c_int),
         "bo_moe_forward_ex": ([vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp, vp], C.c_int),
         "bo_plan_from_counts": ([vp, vp, vp, vp, vp, vp, vp], C.c_int),
+        "bo_route": ([vp, vp, i64, vp, vp, vp, C.c_size_t, vp], C.c_int),
+        "bo_plan_counts": ([vp, vp, i32, vp, vp, vp, vp, vp], C.c_int),
+        "bo_dispatch": ([vp, i64, vp, C.c_size_t, vp, i32, vp, vp, vp, vp, vp], C.c_int),
+        "bo_block_copy": ([vp, vp, vp, i32, vp, vp, i32, vp, vp, i64, vp], C.c_int),
+        "bo_expert_ffn": ([vp, vp, i64, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+        "bo_combine": ([vp, i64, vp, vp, i32, vp, vp, vp], C.c_int),
         "bo_set_profile_events": ([vp, C.POINTER(vp), i32], C.c_int),
         "bo_last_launch_count": ([vp], i32),
         "bo_status_string": ([C.c_int], C.c_char_p),
@@ -235,6 +242,54 @@ class BrownoutMoE:
         }
         del eb
         return out
+
+    # -- expert-parallel building blocks (include/brownout.h) ----------------
+    def route(self, x, Wr, logits=None, workspace=None, stream=None):
+        """a1-a4 on a local batch; returns the workspace (counts etc. inside)."""
+        T = x.shape[0]
+        ws = workspace if workspace is not None else self.workspace(T, x.device)
+        _check(_lib.bo_route(self._h, _ptr(x), T, _ptr(Wr), _ptr(logits), _ptr(ws), ws.numel(), _stream(stream)))
+        return ws
+
+    def local_counts(self, T, workspace=None):
+        return self.debug_arrays(T, workspace)["counts"]
+
+    def plan_counts(self, counts: torch.Tensor, stream=None):
+        """Alg. 1 on the column sums of counts [nrows, m] (int32, device)."""
+        m = self.cfg.num_experts
+        dev = counts.device
+        counts = counts.reshape(-1, m).contiguous()
+        exec_of = torch.empty(m, dtype=torch.int32, device=dev)
+        erow = torch.empty(m, dtype=torch.int32, device=dev)
+        eoff = torch.empty(2 * (self.E + 1) + m, dtype=torch.int32, device=dev)
+        stats = torch.empty(8, dtype=torch.int64, device=dev)
+        _check(_lib.bo_plan_counts(self._h, _ptr(counts), counts.shape[0], _ptr(exec_of), _ptr(erow), _ptr(eoff),
+                                   _ptr(stats), _stream(stream)))
+        return {"exec_of_expert": exec_of, "expert_row_off": erow, "exec_off": eoff[:self.E + 1], "stats": stats}
+
+    def dispatch(self, T, row_base, nrep, x, rows_out, w_out, row_of, workspace=None, stream=None):
+        ws = self._ws if workspace is None else workspace
+        _check(_lib.bo_dispatch(self._h, T, _ptr(ws), ws.numel(), _ptr(row_base), nrep, _ptr(x), _ptr(rows_out),
+                                _ptr(w_out), _ptr(row_of), _stream(stream)))
+
+    def block_copy(self, src, dst, src_off, dst_start, w_src=None, w_dst=None, stream=None):
+        rows = dst.shape[0]
+        if rows == 0:
+            return
+        row_bytes = dst[0].numel() * dst.element_size()
+        _check(_lib.bo_block_copy(self._h, _ptr(src), _ptr(dst), row_bytes, _ptr(w_src), _ptr(w_dst),
+                                  src_off.numel(), _ptr(src_off), _ptr(dst_start), rows, _stream(stream)))
+
+    def expert_ffn(self, rows, row_w, exec_off, mtile_off, n_orig, n_united, f_united, experts, united, h_buf, out,
+                   stream=None):
+        Wg, Wu, Wd = experts if experts is not None else (None, None, None)
+        UWg, UWu, UWd = united if united is not None else (None, None, None)
+        _check(_lib.bo_expert_ffn(self._h, _ptr(rows), rows.shape[0], _ptr(row_w), _ptr(exec_off), _ptr(mtile_off),
+                                  n_orig, n_united, f_united, _ptr(Wg), _ptr(Wu), _ptr(Wd), _ptr(UWg), _ptr(UWu),
+                                  _ptr(UWd), _ptr(h_buf), _ptr(out), _stream(stream)))
+
+    def combine(self, T, rows, row_of, nrep, x, y, stream=None):
+        _check(_lib.bo_combine(self._h, T, _ptr(rows), _ptr(row_of), nrep, _ptr(x), _ptr(y), _stream(stream)))
 
     def plan_from_counts(self, counts: torch.Tensor, stream=None):
         """Alg. 1 on device counts (int32 [m]) -> dict of device tensors."""

@@ -22,6 +22,8 @@ struct bo_handle {
   int32_t last_launches;
   void** prof_events;
   int32_t prof_n;
+  int64_t route_T;     // token count / tile of the last route stage (bo_route, forward)
+  int32_t route_tile;
 };
 
 namespace {
@@ -143,6 +145,182 @@ P* at(void* ws, size_t off) {
   return reinterpret_cast<P*>(static_cast<char*>(ws) + off);
 }
 
+// Per-kernel profiling events (bo_set_profile_events); graph-capture aware.
+struct Prof {
+  bo_handle* h;
+  cudaStream_t s;
+  bool on = false;
+  unsigned flags = 0;
+  cudaError_t err = cudaSuccess;
+  Prof(bo_handle* h_, cudaStream_t s_, int max_launches) : h(h_), s(s_) {
+    on = h->prof_events && h->prof_n >= max_launches + 1;
+    if (on) {
+      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+      err = cudaStreamIsCapturing(s, &cap);
+      // under stream capture the events must become graph event-record nodes (external)
+      flags = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
+    }
+  }
+  void mark(int i) {
+    if (on && err == cudaSuccess) err = cudaEventRecordWithFlags(static_cast<cudaEvent_t>(h->prof_events[i]), s, flags);
+  }
+};
+
+// Steps a1-a3: router logits (Eq. 8), top-K softmax (Eq. 7), per-tile expert
+// histogram; then the local counts / per-tile prefix (and Alg. 1 on the local
+// counts) via the plan kernel.  Returns the token tile used.
+bo_status route_stage(bo_handle* h, const void* x, int64_t T, const void* Wr, const float* logits_in, void* ws,
+                      const bo_ws_layout& L, cudaStream_t s, Prof& prof, int& launches, int& tile) {
+  const bo_config& c = h->cfg;
+  const int dt = c.dtype == BO_BF16 ? 0 : 1;
+  const int m = c.num_experts, K = c.top_k, d = c.hidden;
+  float* logits = at<float>(ws, L.logits);
+  int32_t* topk_id = at<int32_t>(ws, L.topk_id);
+  float* topk_w = at<float>(ws, L.topk_w);
+  int32_t* tile_cnt = at<int32_t>(ws, L.tile_cnt);
+  bo_status st;
+  if (logits_in) {
+    tile = bo::kTileSmall;
+    prof.mark(launches);
+    BO_CUDA(bo::launch_topk_hist(logits_in, static_cast<int>(T), m, K, tile, topk_id, topk_w, tile_cnt, s), "topk");
+    ++launches;
+  } else if (bo::router_small_ok(dt, m, d)) {
+    tile = bo::router_small_tile(static_cast<int>(T), h->num_sms);   // m <= 32: CUDA-core router (HBM-bound)
+    prof.mark(launches);
+    BO_CUDA(bo::launch_router_small(dt, x, Wr, static_cast<int>(T), d, m, K, tile, logits, topk_id, topk_w,
+                                    tile_cnt, s),
+            "router");
+    ++launches;
+  } else {
+    tile = bo::kTileTok;     // tcgen05 router, top-K fused into the epilogue
+    CUtensorMap mA, mB;
+    const int bn = router_bn(m);
+    if ((st = make_map(&mA, x, c.dtype, T, d, bo::kBM)) != BO_OK) return st;
+    if ((st = make_map(&mB, Wr, c.dtype, m, d, bn)) != BO_OK) return st;
+    bo::GemmParams p{};
+    p.Kdim = d;
+    p.n_tiles = 1;
+    p.Kdim_u = d;
+    p.n_tiles_u = 1;
+    p.b_rows_u = 0;
+    p.ldo = m;
+    p.n_valid = m;
+    p.m_orig = 1;
+    p.b_rows_per_exec = 0;
+    p.num_exec = 1;
+    p.single_rows = static_cast<int>(T);
+    p.out = logits;
+    p.topk_k = K;
+    p.topk_id = topk_id;
+    p.topk_w = topk_w;
+    p.tile_cnt = tile_cnt;
+    const int work = static_cast<int>((T + bo::kBM - 1) / bo::kBM);
+    const int grid = work < h->num_sms ? work : h->num_sms;
+    prof.mark(launches);
+    BO_CUDA(bo::launch_grouped_gemm(dt, bo::EPI_ROUTER, bn, mA, mB, mB, mB, mB, p, grid, s), "router gemm");
+    ++launches;
+  }
+  const int ntiles = static_cast<int>((T + tile - 1) / tile);
+  // Alg. 1 over this batch (snapshot of the knob at enqueue time); also yields
+  // cnt_i and the per-tile prefix the permutation needs.
+  prof.mark(launches);
+  BO_CUDA(bo::launch_plan(tile_cnt, ntiles, m, c.way, h->ratio, h->mode, at<int32_t>(ws, L.tile_base),
+                          at<int32_t>(ws, L.counts), at<int32_t>(ws, L.exec_of_expert),
+                          at<int32_t>(ws, L.expert_row_off), at<int32_t>(ws, L.exec_off),
+                          at<int32_t>(ws, L.mtile_off), at<int64_t>(ws, L.stats), s),
+          "plan");
+  ++launches;
+  h->route_T = T;
+  h->route_tile = tile;
+  return BO_OK;
+}
+
+// Steps a6-a7 over rows already grouped by executor: GEMM1 + SwiGLU, GEMM2 x
+// row gate weight.  Executors [0, n_orig) read Wg/Wu/Wd stacks of width f,
+// executors [n_orig, n_orig + n_united) read UWg/UWu/UWd stacks of width f_u
+// (f_u < f: expert-parallel f-slices of united experts).
+bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, const int32_t* exec_off,
+                    const int32_t* mtile_off, int n_orig, int n_united, int f_u, const void* Wg, const void* Wu,
+                    const void* Wd, const void* UWg, const void* UWu, const void* UWd, int64_t united_stack,
+                    void* Hbuf, void* Y, cudaStream_t s, Prof& prof, int& launches) {
+  const bo_config& c = h->cfg;
+  const int dt = c.dtype == BO_BF16 ? 0 : 1;
+  const int d = c.hidden, f = c.ffn;
+  const int n_exec = n_orig + n_united;
+  bo_status st;
+  if (R == 0 || n_exec == 0) return BO_OK;
+  {
+    const int bn = (f % 128 == 0 && f_u % 128 == 0) ? 256 : 128;   // gate + up columns per tile
+    CUtensorMap mA, mG, mU, mUG, mUU;
+    if ((st = make_map(&mA, X, c.dtype, R, d, bo::kBM)) != BO_OK) return st;
+    const uint64_t orows = static_cast<uint64_t>(n_orig > 0 ? n_orig : 1) * f;
+    const uint64_t urows = static_cast<uint64_t>(united_stack > 0 ? united_stack : 1) * f_u;
+    if ((st = make_map(&mG, Wg, c.dtype, orows, d, bn / 2)) != BO_OK) return st;
+    if ((st = make_map(&mU, Wu, c.dtype, orows, d, bn / 2)) != BO_OK) return st;
+    if ((st = make_map(&mUG, UWg, c.dtype, urows, d, bn / 2)) != BO_OK) return st;
+    if ((st = make_map(&mUU, UWu, c.dtype, urows, d, bn / 2)) != BO_OK) return st;
+    bo::GemmParams p{};
+    p.Kdim = d;
+    p.n_tiles = f / (bn / 2);
+    p.Kdim_u = d;
+    p.n_tiles_u = f_u / (bn / 2);
+    p.b_rows_u = f_u;
+    p.ldo = f;
+    p.n_valid = f;
+    p.m_orig = n_orig;
+    p.b_rows_per_exec = f;
+    p.num_exec = n_exec;
+    p.single_rows = -1;
+    p.exec_off = exec_off;
+    p.mtile_off = mtile_off;
+    p.out = Hbuf;
+    const int64_t max_work = ((R + bo::kBM - 1) / bo::kBM + n_exec) * p.n_tiles;
+    const int grid = static_cast<int>(max_work < h->num_sms ? max_work : h->num_sms);
+    prof.mark(launches);
+    BO_CUDA(bo::launch_grouped_gemm(dt, bo::EPI_SWIGLU, bn, mA, mG, mU, mUG, mUU, p, grid, s), "gemm1");
+    ++launches;
+  }
+  {
+    const int bn = gemm2_bn(d);
+    CUtensorMap mA, mD, mUD;
+    if ((st = make_map(&mA, Hbuf, c.dtype, R, f, bo::kBM)) != BO_OK) return st;
+    const uint64_t orows = static_cast<uint64_t>(n_orig > 0 ? n_orig : 1) * d;
+    const uint64_t urows = static_cast<uint64_t>(united_stack > 0 ? united_stack : 1) * d;
+    if ((st = make_map(&mD, Wd, c.dtype, orows, f, bn)) != BO_OK) return st;
+    if ((st = make_map(&mUD, UWd, c.dtype, urows, f_u, bn)) != BO_OK) return st;
+    bo::GemmParams p{};
+    p.Kdim = f;
+    p.n_tiles = d / bn;
+    p.Kdim_u = f_u;
+    p.n_tiles_u = p.n_tiles;
+    p.b_rows_u = d;
+    p.ldo = d;
+    p.n_valid = d;
+    p.m_orig = n_orig;
+    p.b_rows_per_exec = d;
+    p.num_exec = n_exec;
+    p.single_rows = -1;
+    p.exec_off = exec_off;
+    p.mtile_off = mtile_off;
+    p.out = Y;
+    p.row_w = row_w;
+    const int64_t max_work = ((R + bo::kBM - 1) / bo::kBM + n_exec) * p.n_tiles;
+    const int grid = static_cast<int>(max_work < h->num_sms ? max_work : h->num_sms);
+    prof.mark(launches);
+    BO_CUDA(bo::launch_grouped_gemm(dt, bo::EPI_WEIGHTED, bn, mA, mD, mD, mUD, mUD, p, grid, s), "gemm2");
+    ++launches;
+  }
+  return BO_OK;
+}
+
+bo_status check_ws(const bo_handle* h, int64_t T, void* ws, size_t ws_bytes, bo_ws_layout* L) {
+  compute_layout(h, T, L);
+  if (!ws || ws_bytes < L->total_bytes)
+    return fail(BO_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, L->total_bytes);
+  if (!aligned16(ws)) return fail(BO_ERR_SHAPE, "workspace must be 16-byte aligned");
+  return BO_OK;
+}
+
 bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, const void* Wg, const void* Wu,
                        const void* Wd, const void* UWg, const void* UWu, const void* UWd, void* y, void* ws,
                        size_t ws_bytes, const float* logits_in, void* stream) {
@@ -157,170 +335,50 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   const bool may_use_united = h->mode == BO_PARTIAL && h->ratio > 0.0;
   if (may_use_united && (!UWg || !UWu || !UWd))
     return fail(BO_ERR_INVALID_ARG, "united weights are required when ratio > 0 in partial mode");
-  if (!UWg) { UWg = Wg; UWu = Wu; UWd = Wd; }   // never selected by the plan (ratio 0 or full mode)
-  const void* ptrs[] = {x, Wr ? Wr : x, Wg, Wu, Wd, UWg, UWu, UWd, y, ws};
+  const bool have_united = UWg != nullptr;
+  if (!have_united) { UWg = Wg; UWu = Wu; UWd = Wd; }   // never selected by the plan (ratio 0 or full mode)
+  const void* ptrs[] = {x, Wr ? Wr : x, Wg, Wu, Wd, UWg, UWu, UWd, y};
   for (const void* p : ptrs)
     if (!aligned16(p)) return fail(BO_ERR_SHAPE, "tensor pointers must be 16-byte aligned");
   bo_ws_layout L;
-  compute_layout(h, T, &L);
-  if (!ws || ws_bytes < L.total_bytes)
-    return fail(BO_ERR_WORKSPACE, "workspace %zu bytes < required %zu", ws_bytes, L.total_bytes);
+  bo_status st;
+  if ((st = check_ws(h, T, ws, ws_bytes, &L)) != BO_OK) return st;
 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int dt = c.dtype == BO_BF16 ? 0 : 1;
   const int m = c.num_experts, K = c.top_k, d = c.hidden, f = c.ffn;
-  const int G = (m + c.way - 1) / c.way, E = m + G;
+  const int G = (m + c.way - 1) / c.way;
   const int64_t R = T * K;
   int launches = 0;
-  const int kMaxLaunches = 7;
-  const bool prof = h->prof_events && h->prof_n >= kMaxLaunches + 1;
-  cudaError_t prof_err = cudaSuccess;
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  if (prof) prof_err = cudaStreamIsCapturing(s, &cap);
-  // Under stream capture the events must become graph event-record nodes (external).
-  const unsigned rec_flags = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
-  auto mark = [&](int i) {
-    if (prof && prof_err == cudaSuccess)
-      prof_err = cudaEventRecordWithFlags(static_cast<cudaEvent_t>(h->prof_events[i]), s, rec_flags);
-  };
-
-  float* logits = at<float>(ws, L.logits);
-  int32_t* topk_id = at<int32_t>(ws, L.topk_id);
-  float* topk_w = at<float>(ws, L.topk_w);
-  int32_t* tile_cnt = at<int32_t>(ws, L.tile_cnt);
-  int32_t* tile_base = at<int32_t>(ws, L.tile_base);
-  int32_t* counts = at<int32_t>(ws, L.counts);
-  int32_t* exec_of = at<int32_t>(ws, L.exec_of_expert);
-  int32_t* erow = at<int32_t>(ws, L.expert_row_off);
-  int32_t* exec_off = at<int32_t>(ws, L.exec_off);
-  int32_t* mtile_off = at<int32_t>(ws, L.mtile_off);
-  int64_t* stats = at<int64_t>(ws, L.stats);
+  Prof prof(h, s, 7);
+  int tile = 0;
+  // a1-a4: router, top-K, histogram, Alg. 1 plan
+  if ((st = route_stage(h, x, T, Wr, logits_in, ws, L, s, prof, launches, tile)) != BO_OK) return st;
+  // a5: permutation (rows in executor / expert / token order) and gather of Xp
   int32_t* row_of = at<int32_t>(ws, L.row_of);
-  int32_t* row_tok = at<int32_t>(ws, L.row_tok);
   float* row_w = at<float>(ws, L.row_w);
-  void* xp = at<char>(ws, L.xp);
-  void* hb = at<char>(ws, L.h);
-  void* yp = at<char>(ws, L.yp);
-  bo_status st;
-
-  // 1-2. router logits (Eq. 8) + top-K softmax (Eq. 7) + per-tile expert histogram
-  int tile;
-  if (logits_in) {
-    tile = bo::kTileSmall;
-    mark(launches);
-    BO_CUDA(bo::launch_topk_hist(logits_in, static_cast<int>(T), m, K, tile, topk_id, topk_w, tile_cnt, s), "topk");
-    ++launches;
-  } else if (bo::router_small_ok(dt, m, d)) {
-    tile = bo::router_small_tile(static_cast<int>(T), h->num_sms);   // m <= 32: CUDA-core router (HBM-bound)
-    mark(launches);
-    BO_CUDA(bo::launch_router_small(dt, x, Wr, static_cast<int>(T), d, m, K, tile, logits, topk_id, topk_w,
-                                    tile_cnt, s),
-            "router");
-    ++launches;
-  } else {
-    tile = bo::kTileTok;     // tcgen05 router, top-K fused into the epilogue
-    CUtensorMap mA, mB;
-    const int bn = router_bn(m);
-    if ((st = make_map(&mA, x, c.dtype, T, d, bo::kBM)) != BO_OK) return st;
-    if ((st = make_map(&mB, Wr, c.dtype, m, d, bn)) != BO_OK) return st;
-    bo::GemmParams p{};
-    p.Kdim = d;
-    p.n_tiles = 1;
-    p.ldo = m;
-    p.n_valid = m;
-    p.m_orig = 1;
-    p.b_rows_per_exec = 0;
-    p.num_exec = 1;
-    p.single_rows = static_cast<int>(T);
-    p.out = logits;
-    p.topk_k = K;
-    p.topk_id = topk_id;
-    p.topk_w = topk_w;
-    p.tile_cnt = tile_cnt;
-    const int work = static_cast<int>((T + bo::kBM - 1) / bo::kBM);
-    const int grid = work < h->num_sms ? work : h->num_sms;
-    mark(launches);
-    BO_CUDA(bo::launch_grouped_gemm(dt, bo::EPI_ROUTER, bn, mA, mB, mB, mB, mB, p, grid, s), "router gemm");
-    ++launches;
-  }
-  const int ntiles = static_cast<int>((T + tile - 1) / tile);
-  // 3. Algorithm 1 plan (snapshot of the knob at enqueue time)
-  mark(launches);
-  BO_CUDA(bo::launch_plan(tile_cnt, ntiles, m, c.way, h->ratio, h->mode, tile_base, counts, exec_of, erow,
-                          exec_off, mtile_off, stats, s),
-          "plan");
-  ++launches;
-  // 4. permutation (rows) and gather (Xp)
-  mark(launches);
-  BO_CUDA(bo::launch_permute(topk_id, topk_w, static_cast<int>(T), K, m, tile, tile_base, exec_of, erow, row_of,
-                             row_tok, row_w, s),
+  prof.mark(launches);
+  BO_CUDA(bo::launch_permute(at<int32_t>(ws, L.topk_id), at<float>(ws, L.topk_w), static_cast<int>(T), K, m, tile,
+                             at<int32_t>(ws, L.tile_base), at<int32_t>(ws, L.expert_row_off), 1, row_of,
+                             at<int32_t>(ws, L.row_tok), row_w, s),
           "permute");
   ++launches;
-  mark(launches);
+  void* xp = at<char>(ws, L.xp);
+  prof.mark(launches);
   BO_CUDA(bo::launch_gather(dt, x, static_cast<int>(T), d, K, row_of, xp, h->num_sms, s), "gather");
   ++launches;
-  // 5. GEMM1 + SwiGLU over executors
-  {
-    const int bn = gemm1_bn(f);
-    CUtensorMap mA, mG, mU, mUG, mUU;
-    if ((st = make_map(&mA, xp, c.dtype, R, d, bo::kBM)) != BO_OK) return st;
-    if ((st = make_map(&mG, Wg, c.dtype, static_cast<uint64_t>(m) * f, d, bn / 2)) != BO_OK) return st;
-    if ((st = make_map(&mU, Wu, c.dtype, static_cast<uint64_t>(m) * f, d, bn / 2)) != BO_OK) return st;
-    const uint64_t urows = UWg == Wg ? static_cast<uint64_t>(m) * f : static_cast<uint64_t>(G) * f;
-    if ((st = make_map(&mUG, UWg, c.dtype, urows, d, bn / 2)) != BO_OK) return st;
-    if ((st = make_map(&mUU, UWu, c.dtype, urows, d, bn / 2)) != BO_OK) return st;
-    bo::GemmParams p{};
-    p.Kdim = d;
-    p.n_tiles = f / (bn / 2);
-    p.ldo = f;
-    p.n_valid = f;
-    p.m_orig = m;
-    p.b_rows_per_exec = f;
-    p.num_exec = E;
-    p.single_rows = -1;
-    p.exec_off = exec_off;
-    p.mtile_off = mtile_off;
-    p.out = hb;
-    const int64_t max_work = ((R + bo::kBM - 1) / bo::kBM + E) * p.n_tiles;
-    const int grid = static_cast<int>(max_work < h->num_sms ? max_work : h->num_sms);
-    mark(launches);
-    BO_CUDA(bo::launch_grouped_gemm(dt, bo::EPI_SWIGLU, bn, mA, mG, mU, mUG, mUU, p, grid, s), "gemm1");
-    ++launches;
-  }
-  // 6. GEMM2, rows scaled by their gate weight (Eq. 6)
-  {
-    const int bn = gemm2_bn(d);
-    CUtensorMap mA, mD, mUD;
-    if ((st = make_map(&mA, hb, c.dtype, R, f, bo::kBM)) != BO_OK) return st;
-    if ((st = make_map(&mD, Wd, c.dtype, static_cast<uint64_t>(m) * d, f, bn)) != BO_OK) return st;
-    const uint64_t urows = UWd == Wd ? static_cast<uint64_t>(m) * d : static_cast<uint64_t>(G) * d;
-    if ((st = make_map(&mUD, UWd, c.dtype, urows, f, bn)) != BO_OK) return st;
-    bo::GemmParams p{};
-    p.Kdim = f;
-    p.n_tiles = d / bn;
-    p.ldo = d;
-    p.n_valid = d;
-    p.m_orig = m;
-    p.b_rows_per_exec = d;
-    p.num_exec = E;
-    p.single_rows = -1;
-    p.exec_off = exec_off;
-    p.mtile_off = mtile_off;
-    p.out = yp;
-    p.row_w = row_w;
-    const int64_t max_work = ((R + bo::kBM - 1) / bo::kBM + E) * p.n_tiles;
-    const int grid = static_cast<int>(max_work < h->num_sms ? max_work : h->num_sms);
-    mark(launches);
-    BO_CUDA(bo::launch_grouped_gemm(dt, bo::EPI_WEIGHTED, bn, mA, mD, mD, mUD, mUD, p, grid, s), "gemm2");
-    ++launches;
-  }
-  // 7. combine (Eq. 5 sum over the token's K slots)
-  mark(launches);
+  // a6-a7: grouped SwiGLU FFN over the m original + G united executors
+  void* yp = at<char>(ws, L.yp);
+  if ((st = ffn_stage(h, xp, R, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), m, G, f, Wg, Wu,
+                      Wd, UWg, UWu, UWd, have_united ? G : m, at<char>(ws, L.h), yp, s, prof, launches)) != BO_OK)
+    return st;
+  // a8: combine (Eq. 5 sum over the token's K slots)
+  prof.mark(launches);
   BO_CUDA(bo::launch_combine(dt, yp, x, static_cast<int>(T), d, K, row_of, c.add_residual, y, h->num_sms, s),
           "combine");
   ++launches;
-  mark(launches);
-  if (prof_err != cudaSuccess) return cuda_fail(prof_err, "profile event record");
+  prof.mark(launches);
+  if (prof.err != cudaSuccess) return cuda_fail(prof.err, "profile event record");
   h->last_launches = launches;
   return BO_OK;
 }
@@ -374,6 +432,8 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   h->last_launches = 0;
   h->prof_events = nullptr;
   h->prof_n = 0;
+  h->route_T = -1;
+  h->route_tile = 0;
   *out = h;
   return BO_OK;
 }
@@ -453,6 +513,117 @@ bo_status bo_plan_from_counts(bo_handle* h, const int32_t* counts, int32_t* exec
   BO_CUDA(bo::launch_plan(counts, 1, m, c.way, h->ratio, h->mode, nullptr, counts_out, exec_of_expert,
                           expert_row_off, exec_off, mtile_scratch, static_cast<int64_t*>(stats), s),
           "plan_from_counts");
+  return BO_OK;
+}
+
+bo_status bo_route(bo_handle* h, const void* x, int64_t T, const void* Wr, const float* logits_in, void* workspace,
+                   size_t ws_bytes, void* stream) {
+  if (!h) return fail(BO_ERR_INVALID_ARG, "null handle");
+  if (T < 0 || T > h->cfg.max_tokens) return fail(BO_ERR_INVALID_ARG, "T out of range");
+  if (!x || (!Wr && !logits_in)) return fail(BO_ERR_INVALID_ARG, "null tensor pointer");
+  bo_ws_layout L;
+  bo_status st;
+  if ((st = check_ws(h, T, workspace, ws_bytes, &L)) != BO_OK) return st;
+  h->route_T = T;
+  if (T == 0) return BO_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Prof prof(h, s, 1 << 30);
+  int launches = 0, tile = 0;
+  return route_stage(h, x, T, Wr, logits_in, workspace, L, s, prof, launches, tile);
+}
+
+bo_status bo_plan_counts(bo_handle* h, const int32_t* counts, int32_t nrows, int32_t* exec_of_expert,
+                         int32_t* expert_row_off, int32_t* exec_off, void* stats, void* stream) {
+  if (!h || !counts || !exec_of_expert || !expert_row_off || !exec_off || !stats || nrows < 1)
+    return fail(BO_ERR_INVALID_ARG, "null argument or nrows < 1");
+  const bo_config& c = h->cfg;
+  const int m = c.num_experts;
+  const int E = m + (m + c.way - 1) / c.way;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int32_t* mtile_scratch = exec_off + (E + 1);   // exec_off holds 2*(E+1) + m ints (brownout.h)
+  int32_t* counts_out = mtile_scratch + (E + 1);
+  BO_CUDA(bo::launch_plan(counts, nrows, m, c.way, h->ratio, h->mode, nullptr, counts_out, exec_of_expert,
+                          expert_row_off, exec_off, mtile_scratch, static_cast<int64_t*>(stats), s),
+          "plan_counts");
+  return BO_OK;
+}
+
+bo_status bo_dispatch(bo_handle* h, int64_t T, void* workspace, size_t ws_bytes, const int32_t* row_base,
+                      int32_t nrep, const void* x, void* rows_out, float* w_out, int32_t* row_of, void* stream) {
+  if (!h) return fail(BO_ERR_INVALID_ARG, "null handle");
+  if (T != h->route_T) return fail(BO_ERR_INVALID_ARG, "bo_dispatch T=%lld differs from the last bo_route (T=%lld)",
+                                   static_cast<long long>(T), static_cast<long long>(h->route_T));
+  if (nrep < 1 || nrep > 8) return fail(BO_ERR_INVALID_ARG, "nrep %d outside [1, 8]", nrep);
+  if (T == 0) return BO_OK;
+  if (!row_base || !x || !rows_out || !w_out || !row_of) return fail(BO_ERR_INVALID_ARG, "null argument");
+  bo_ws_layout L;
+  bo_status st;
+  if ((st = check_ws(h, T, workspace, ws_bytes, &L)) != BO_OK) return st;
+  if (!aligned16(x) || !aligned16(rows_out)) return fail(BO_ERR_SHAPE, "x / rows_out must be 16-byte aligned");
+  const bo_config& c = h->cfg;
+  const int dt = c.dtype == BO_BF16 ? 0 : 1;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  BO_CUDA(bo::launch_permute(at<int32_t>(workspace, L.topk_id), at<float>(workspace, L.topk_w), static_cast<int>(T),
+                             c.top_k, c.num_experts, h->route_tile, at<int32_t>(workspace, L.tile_base), row_base,
+                             nrep, row_of, nullptr, w_out, s),
+          "dispatch permute");
+  BO_CUDA(bo::launch_gather(dt, x, static_cast<int>(T), c.hidden, c.top_k * nrep, row_of, rows_out, h->num_sms, s),
+          "dispatch gather");
+  return BO_OK;
+}
+
+bo_status bo_block_copy(bo_handle* h, const void* src, void* dst, int32_t row_bytes, const float* w_src,
+                        float* w_dst, int32_t n_blocks, const int32_t* src_off, const int32_t* dst_start,
+                        int64_t total_rows, void* stream) {
+  if (!h) return fail(BO_ERR_INVALID_ARG, "null handle");
+  if (total_rows == 0) return BO_OK;
+  if (!src || !dst || !src_off || !dst_start || n_blocks < 1 || (w_src && !w_dst))
+    return fail(BO_ERR_INVALID_ARG, "null argument");
+  if (row_bytes <= 0 || row_bytes % 16 || !aligned16(src) || !aligned16(dst))
+    return fail(BO_ERR_SHAPE, "rows must be 16-byte multiples and 16-byte aligned");
+  BO_CUDA(bo::launch_block_copy(src, dst, row_bytes, w_src, w_dst, n_blocks, src_off, dst_start, total_rows,
+                                h->num_sms, static_cast<cudaStream_t>(stream)),
+          "block_copy");
+  return BO_OK;
+}
+
+bo_status bo_expert_ffn(bo_handle* h, const void* rows, int64_t R, const float* row_w, const int32_t* exec_off,
+                        const int32_t* mtile_off, int32_t n_orig, int32_t n_united, int32_t f_united, const void* Wg,
+                        const void* Wu, const void* Wd, const void* UWg, const void* UWu, const void* UWd,
+                        void* h_buf, void* out, void* stream) {
+  if (!h) return fail(BO_ERR_INVALID_ARG, "null handle");
+  if (R == 0) return BO_OK;
+  const bo_config& c = h->cfg;
+  if (n_orig < 0 || n_united < 0 || n_orig + n_united > bo::kMaxExec)
+    return fail(BO_ERR_INVALID_ARG, "executor counts out of range");
+  if (n_united > 0 && (f_united <= 0 || f_united > c.ffn || f_united % 128))
+    return fail(BO_ERR_SHAPE, "f_united=%d must be a positive multiple of 128 and <= ffn", f_united);
+  if (!rows || !row_w || !exec_off || !mtile_off || !h_buf || !out) return fail(BO_ERR_INVALID_ARG, "null argument");
+  if ((n_orig > 0 && (!Wg || !Wu || !Wd)) || (n_united > 0 && (!UWg || !UWu || !UWd)))
+    return fail(BO_ERR_INVALID_ARG, "null weights");
+  const void* ptrs[] = {rows, h_buf, out, Wg ? Wg : rows, Wu ? Wu : rows, Wd ? Wd : rows,
+                        UWg ? UWg : rows, UWu ? UWu : rows, UWd ? UWd : rows};
+  for (const void* p : ptrs)
+    if (!aligned16(p)) return fail(BO_ERR_SHAPE, "tensor pointers must be 16-byte aligned");
+  if (!Wg) { Wg = UWg; Wu = UWu; Wd = UWd; }
+  if (!UWg) { UWg = Wg; UWu = Wu; UWd = Wd; }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Prof prof(h, s, 1 << 30);
+  int launches = 0;
+  return ffn_stage(h, rows, R, row_w, exec_off, mtile_off, n_orig, n_united, n_united > 0 ? f_united : c.ffn, Wg, Wu,
+                   Wd, UWg, UWu, UWd, n_united > 0 ? n_united : 1, h_buf, out, s, prof, launches);
+}
+
+bo_status bo_combine(bo_handle* h, int64_t T, const void* rows, const int32_t* row_of, int32_t nrep, const void* x,
+                     void* y, void* stream) {
+  if (!h) return fail(BO_ERR_INVALID_ARG, "null handle");
+  if (T == 0) return BO_OK;
+  if (!rows || !row_of || !y || (h->cfg.add_residual && !x) || nrep < 1)
+    return fail(BO_ERR_INVALID_ARG, "null argument");
+  const bo_config& c = h->cfg;
+  BO_CUDA(bo::launch_combine(c.dtype == BO_BF16 ? 0 : 1, rows, x, static_cast<int>(T), c.hidden, c.top_k * nrep,
+                             row_of, c.add_residual, y, h->num_sms, static_cast<cudaStream_t>(stream)),
+          "combine");
   return BO_OK;
 }
 

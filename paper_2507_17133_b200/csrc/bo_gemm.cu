@@ -154,23 +154,29 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int n_tiles = p.n_tiles;
-  const int total_work = s_mtile[nexec] * n_tiles;
-  const int num_kb = p.Kdim / C::BK;
+  // Two executor classes (originals x < m_orig, united x >= m_orig) may differ in
+  // n-tiles, reduction length and B rows (expert-parallel united f-slices).
+  const int mo = p.m_orig < nexec ? p.m_orig : nexec;
+  const int nt_o = p.n_tiles, nt_u = p.n_tiles_u;
+  auto start_of = [&](int x) {
+    return x <= mo ? nt_o * s_mtile[x] : nt_o * s_mtile[mo] + nt_u * (s_mtile[x] - s_mtile[mo]);
+  };
+  const int total_work = start_of(nexec);
 
-  // work item -> (executor, m-tile inside executor, n-tile)
+  // work item -> (executor, m-tile inside executor, n-tile); m-tile fastest
   auto decode = [&](int w, int& x, int& mi, int& n) {
     int lo = 0, hi = nexec;
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
-      if (s_mtile[mid] * n_tiles <= w) lo = mid; else hi = mid;
+      if (start_of(mid) <= w) lo = mid; else hi = mid;
     }
     x = lo;
     const int mt = s_mtile[x + 1] - s_mtile[x];
-    const int local = w - s_mtile[x] * n_tiles;
+    const int local = w - start_of(x);
     n = local / mt;
     mi = local - n * mt;
   };
+  auto kblocks = [&](int x) { return (x < mo ? p.Kdim : p.Kdim_u) / C::BK; };
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -186,7 +192,8 @@ __global__ void __launch_bounds__(192, 1)
         const bool orig = x < p.m_orig;
         const CUtensorMap* mb0 = orig ? &tmB0 : &tmB2;
         const CUtensorMap* mb1 = orig ? &tmB1 : &tmB3;
-        const int brow = (orig ? x : x - p.m_orig) * p.b_rows_per_exec;
+        const int brow = orig ? x * p.b_rows_per_exec : (x - p.m_orig) * p.b_rows_u;
+        const int num_kb = kblocks(x);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
@@ -211,6 +218,9 @@ __global__ void __launch_bounds__(192, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
+        int x, mi, n;
+        decode(w, x, mi, n);
+        const int num_kb = kblocks(x);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);

@@ -15,8 +15,11 @@ constexpr int kMaxExec = 512;   // m + G
 enum Epi : int { EPI_SWIGLU = 0, EPI_WEIGHTED = 1, EPI_ROUTER = 2 };
 
 struct GemmParams {
-  int Kdim;              // reduction length
-  int n_tiles;           // output tiles per executor along N
+  int Kdim;              // reduction length (executors < m_orig)
+  int n_tiles;           // output tiles per executor along N (executors < m_orig)
+  int Kdim_u;            // reduction length of executors >= m_orig
+  int n_tiles_u;         // output tiles of executors >= m_orig
+  int b_rows_u;          // rows of B per executor >= m_orig in its stacked view
   int ldo;               // leading dimension of the output (elements)
   int n_valid;           // valid output columns (router: m)
   int m_orig;            // executors < m_orig read B maps 0/1, others maps 2/3
@@ -57,15 +60,20 @@ cudaError_t launch_plan(const int32_t* tile_cnt, int ntiles, int m, int way, dou
                         int32_t* exec_off, int32_t* mtile_off, int64_t* stats, cudaStream_t s);
 
 cudaError_t launch_permute(const int32_t* topk_id, const float* topk_w, int T, int K, int m, int tile,
-                           const int32_t* tile_base, const int32_t* exec_of_expert,
-                           const int32_t* expert_row_off, int32_t* row_of, int32_t* row_tok, float* row_w,
-                           cudaStream_t s);
+                           const int32_t* tile_base, const int32_t* row_base, int nrep, int32_t* row_of,
+                           int32_t* row_tok, float* row_w, cudaStream_t s);
 
-cudaError_t launch_gather(int dtype, const void* x, int T, int d, int K, const int32_t* row_of, void* xp,
+cudaError_t launch_gather(int dtype, const void* x, int T, int d, int KR, const int32_t* row_of, void* xp,
                           int num_sms, cudaStream_t s);
 
-cudaError_t launch_combine(int dtype, const void* yp, const void* x, int T, int d, int K,
+cudaError_t launch_combine(int dtype, const void* yp, const void* x, int T, int d, int KR,
                            const int32_t* row_of, int add_residual, void* y, int num_sms, cudaStream_t s);
+
+// Row-block permutation: dst row i lies in block b (dst_start[b] <= i < dst_start[b+1]) and
+// copies src row src_off[b] + (i - dst_start[b]) (and its float weight if w_src != nullptr).
+cudaError_t launch_block_copy(const void* src, void* dst, int row_bytes, const float* w_src, float* w_dst,
+                              int n_blocks, const int32_t* src_off, const int32_t* dst_start, int64_t total_rows,
+                              int num_sms, cudaStream_t s);
 
 cudaError_t launch_build_united(int dtype, const void* W, int m, int way, int64_t per_expert, void* U,
                                 cudaStream_t s);

@@ -465,15 +465,18 @@ cudaError_t launch_plan(const int32_t* tile_cnt, int ntiles, int m, int way, dou
 }
 
 // ----------------------------------------------------------- permutation
-// One CTA per token tile (the tile of the histogram that produced tile_base).  Assignments a = t*K + s of the tile are split
-// into 8 contiguous warp ranges; pass 1 counts per (warp, expert), a prefix
-// over warps gives each warp's start, pass 2 assigns ranks in order.  Row of
-// assignment = expert_row_off[e] + tile_base[tile][e] + rank within the tile.
+// One CTA per token tile (the tile of the histogram that produced tile_base).
+// Assignments a = t*K + s of the tile are split into 8 contiguous warp ranges;
+// pass 1 counts per (warp, expert), a prefix over warps gives each warp's
+// start, pass 2 assigns ranks in order (stable: token ascending, D11).
+// Row of (assignment, rep) = row_base[e*nrep + rep] + tile_base[tile][e] + rank
+// (row_base < 0: no row, e.g. dropped in full brownout).  nrep = 1 on one GPU;
+// under expert parallelism an assignment delegated to an f-sliced united
+// expert has one row per slice.
 __global__ void __launch_bounds__(256) k_permute(const int32_t* __restrict__ topk_id,
                                                  const float* __restrict__ topk_w, int T, int K, int m, int tile,
                                                  const int32_t* __restrict__ tile_base,
-                                                 const int32_t* __restrict__ exec_of_expert,
-                                                 const int32_t* __restrict__ expert_row_off,
+                                                 const int32_t* __restrict__ row_base, int nrep,
                                                  int32_t* __restrict__ row_of, int32_t* __restrict__ row_tok,
                                                  float* __restrict__ row_w) {
   __shared__ int wcnt[8][kMaxExperts];
@@ -518,62 +521,69 @@ __global__ void __launch_bounds__(256) k_permute(const int32_t* __restrict__ top
     __syncwarp();
     if (e >= 0) {
       const int64_t a = a0 + i;
-      if (exec_of_expert[e] >= 0) {
-        const int r = expert_row_off[e] + tile_base[static_cast<int64_t>(blockIdx.x) * m + e] + start +
-                      __popc(peers & lt);
-        row_of[a] = r;
-        row_tok[r] = static_cast<int32_t>(a / K);
-        row_w[r] = topk_w[a];
-      } else {
-        row_of[a] = -1;   // dropped (full brownout)
+      const int rank = tile_base[static_cast<int64_t>(blockIdx.x) * m + e] + start + __popc(peers & lt);
+      const float w = topk_w[a];
+      for (int rep = 0; rep < nrep; ++rep) {
+        const int base_r = row_base[e * nrep + rep];
+        if (base_r >= 0) {
+          const int r = base_r + rank;
+          row_of[a * nrep + rep] = r;
+          if (row_tok) row_tok[r] = static_cast<int32_t>(a / K);
+          row_w[r] = w;
+        } else {
+          row_of[a * nrep + rep] = -1;
+        }
       }
     }
   }
 }
 
 cudaError_t launch_permute(const int32_t* topk_id, const float* topk_w, int T, int K, int m, int tile,
-                           const int32_t* tile_base, const int32_t* exec_of_expert,
-                           const int32_t* expert_row_off, int32_t* row_of, int32_t* row_tok, float* row_w,
-                           cudaStream_t s) {
+                           const int32_t* tile_base, const int32_t* row_base, int nrep, int32_t* row_of,
+                           int32_t* row_tok, float* row_w, cudaStream_t s) {
   const int ntiles = (T + tile - 1) / tile;
   if (ntiles == 0) return cudaSuccess;
-  k_permute<<<ntiles, 256, 0, s>>>(topk_id, topk_w, T, K, m, tile, tile_base, exec_of_expert, expert_row_off, row_of,
-                                   row_tok, row_w);
+  k_permute<<<ntiles, 256, 0, s>>>(topk_id, topk_w, T, K, m, tile, tile_base, row_base, nrep, row_of, row_tok,
+                                   row_w);
   return cudaGetLastError();
 }
 
 // ----------------------------------------------------------------- gather
-// Warp per token: each 16-byte chunk of x[t] is loaded once and stored to the
-// token's K rows.  Row indices live one per lane (K <= 16) and are broadcast.
-__global__ void __launch_bounds__(256) k_gather(const uint4* __restrict__ x, int T, int vec_per_row, int K,
+// Warp per token: each 16-byte chunk of x[t] is loaded once and stored to all
+// of the token's rows (KR = K * nrep row slots; row indices one per lane,
+// broadcast by shuffle).
+__global__ void __launch_bounds__(256) k_gather(const uint4* __restrict__ x, int T, int vec_per_row, int KR,
                                                 const int32_t* __restrict__ row_of, uint4* __restrict__ xp) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int t = gw; t < T; t += nw) {
-    const int my_row = lane < K ? row_of[static_cast<int64_t>(t) * K + lane] : -1;
     const uint4* src = x + static_cast<int64_t>(t) * vec_per_row;
-    for (int c0 = 0; c0 < vec_per_row; c0 += 32) {   // warp-uniform trip count (shuffles below)
-      const int c = c0 + lane;
-      const bool ok = c < vec_per_row;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (ok) v = __ldg(src + c);
-      for (int s = 0; s < K; ++s) {
-        const int r = __shfl_sync(0xffffffffu, my_row, s);
-        if (ok && r >= 0) xp[static_cast<int64_t>(r) * vec_per_row + c] = v;
+    for (int r0 = 0; r0 < KR; r0 += 32) {
+      const int nr = min(32, KR - r0);
+      const int my_row = lane < nr ? row_of[static_cast<int64_t>(t) * KR + r0 + lane] : -1;
+      for (int c0 = 0; c0 < vec_per_row; c0 += 32) {   // warp-uniform trip count (shuffles below)
+        const int c = c0 + lane;
+        const bool ok = c < vec_per_row;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (ok) v = __ldg(src + c);
+        for (int s = 0; s < nr; ++s) {
+          const int r = __shfl_sync(0xffffffffu, my_row, s);
+          if (ok && r >= 0) xp[static_cast<int64_t>(r) * vec_per_row + c] = v;
+        }
       }
     }
   }
 }
 
-cudaError_t launch_gather(int dtype, const void* x, int T, int d, int K, const int32_t* row_of, void* xp,
+cudaError_t launch_gather(int dtype, const void* x, int T, int d, int KR, const int32_t* row_of, void* xp,
                           int num_sms, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   const int vec = d * (dtype == 0 ? 2 : 4) / 16;
   int blocks = (T + 7) / 8;
   const int cap = num_sms * 8;
   if (blocks > cap) blocks = cap;
-  k_gather<<<blocks, 256, 0, s>>>(static_cast<const uint4*>(x), T, vec, K, row_of, static_cast<uint4*>(xp));
+  k_gather<<<blocks, 256, 0, s>>>(static_cast<const uint4*>(x), T, vec, KR, row_of, static_cast<uint4*>(xp));
   return cudaGetLastError();
 }
 
@@ -619,14 +629,13 @@ struct Vec8<float> {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_combine(const T* __restrict__ yp, const T* __restrict__ x, int Tn, int d,
-                                                 int K, const int32_t* __restrict__ row_of, int add_residual,
+                                                 int KR, const int32_t* __restrict__ row_of, int add_residual,
                                                  T* __restrict__ y) {
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   const int nvec = d / 8;
   for (int t = gw; t < Tn; t += nw) {
-    const int my_row = lane < K ? row_of[static_cast<int64_t>(t) * K + lane] : -1;
     for (int c0 = 0; c0 < nvec; c0 += 32) {   // warp-uniform trip count (shuffles below)
       const int c = c0 + lane;
       const bool ok = c < nvec;
@@ -637,13 +646,17 @@ __global__ void __launch_bounds__(256) k_combine(const T* __restrict__ yp, const
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
       }
-      for (int s = 0; s < K; ++s) {   // slot order (Eq. 5 sum)
-        const int r = __shfl_sync(0xffffffffu, my_row, s);
-        if (ok && r >= 0) {
-          float v[8];
-          Vec8<T>::load(yp + static_cast<int64_t>(r) * d + c * 8, v);
+      for (int r0 = 0; r0 < KR; r0 += 32) {
+        const int nr = min(32, KR - r0);
+        const int my_row = lane < nr ? row_of[static_cast<int64_t>(t) * KR + r0 + lane] : -1;
+        for (int s = 0; s < nr; ++s) {   // slot order, then slice order (Eq. 5 sum)
+          const int r = __shfl_sync(0xffffffffu, my_row, s);
+          if (ok && r >= 0) {
+            float v[8];
+            Vec8<T>::load(yp + static_cast<int64_t>(r) * d + c * 8, v);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) acc[i] += v[i];
+            for (int i = 0; i < 8; ++i) acc[i] += v[i];
+          }
         }
       }
       if (ok) Vec8<T>::store(y + static_cast<int64_t>(t) * d + c * 8, acc);
@@ -651,7 +664,7 @@ __global__ void __launch_bounds__(256) k_combine(const T* __restrict__ yp, const
   }
 }
 
-cudaError_t launch_combine(int dtype, const void* yp, const void* x, int T, int d, int K, const int32_t* row_of,
+cudaError_t launch_combine(int dtype, const void* yp, const void* x, int T, int d, int KR, const int32_t* row_of,
                            int add_residual, void* y, int num_sms, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   int blocks = (T + 7) / 8;
@@ -659,10 +672,10 @@ cudaError_t launch_combine(int dtype, const void* yp, const void* x, int T, int 
   if (blocks > cap) blocks = cap;
   if (dtype == 0)
     k_combine<__nv_bfloat16><<<blocks, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(yp),
-                                                    static_cast<const __nv_bfloat16*>(x), T, d, K, row_of,
+                                                    static_cast<const __nv_bfloat16*>(x), T, d, KR, row_of,
                                                     add_residual, static_cast<__nv_bfloat16*>(y));
   else
-    k_combine<float><<<blocks, 256, 0, s>>>(static_cast<const float*>(yp), static_cast<const float*>(x), T, d, K,
+    k_combine<float><<<blocks, 256, 0, s>>>(static_cast<const float*>(yp), static_cast<const float*>(x), T, d, KR,
                                             row_of, add_residual, static_cast<float*>(y));
   return cudaGetLastError();
 }
