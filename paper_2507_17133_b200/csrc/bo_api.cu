@@ -249,8 +249,13 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
   const int n_exec = n_orig + n_united;
   bo_status st;
   if (R == 0 || n_exec == 0) return BO_OK;
+  // Tile width: prefill (many rows per executor) is tensor-bound -> widest
+  // tile; decode (few rows) streams weights from HBM, where the number of
+  // equal-cost tiles decides the wave quantisation over 148 SMs -> narrower.
+  const int tier = R <= 1024 ? 64 : (R <= 4096 ? 128 : 256);
   {
-    const int bn = (f % 128 == 0 && f_u % 128 == 0) ? 256 : 128;   // gate + up columns per tile
+    int bn = tier;                                                  // gate + up columns per tile
+    while (bn > 64 && (f % (bn / 2) || f_u % (bn / 2))) bn >>= 1;
     CUtensorMap mA, mG, mU, mUG, mUU;
     if ((st = make_map(&mA, X, c.dtype, R, d, bo::kBM)) != BO_OK) return st;
     const uint64_t orows = static_cast<uint64_t>(n_orig > 0 ? n_orig : 1) * f;
@@ -281,7 +286,8 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     ++launches;
   }
   {
-    const int bn = gemm2_bn(d);
+    int bn = gemm2_bn(d);
+    if (bn > tier) bn = tier;
     CUtensorMap mA, mD, mUD;
     if ((st = make_map(&mA, Hbuf, c.dtype, R, f, bo::kBM)) != BO_OK) return st;
     const uint64_t orows = static_cast<uint64_t>(n_orig > 0 ? n_orig : 1) * d;

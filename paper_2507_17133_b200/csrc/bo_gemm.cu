@@ -378,6 +378,7 @@ static cudaError_t dispatch(int epi, int bn, const CUtensorMap& A, const CUtenso
   if (epi == EPI_SWIGLU) {
     if (bn == 256) return launch_t<T, 256, EPI_SWIGLU>(A, B0, B1, B2, B3, p, grid, s);
     if (bn == 128) return launch_t<T, 128, EPI_SWIGLU>(A, B0, B1, B2, B3, p, grid, s);
+    if (bn == 64) return launch_t<T, 64, EPI_SWIGLU>(A, B0, B1, B2, B3, p, grid, s);
   } else if (epi == EPI_WEIGHTED) {
     if (bn == 256) return launch_t<T, 256, EPI_WEIGHTED>(A, B0, B1, B2, B3, p, grid, s);
     if (bn == 128) return launch_t<T, 128, EPI_WEIGHTED>(A, B0, B1, B2, B3, p, grid, s);
