@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <cstdarg>
@@ -24,6 +25,7 @@ struct bo_handle {
   int32_t prof_n;
   int64_t route_T;     // token count / tile of the last route stage (bo_route, forward)
   int32_t route_tile;
+  int32_t cta_pairs;   // 1: prefill FFN GEMMs use cta_group::2 CTA pairs (env BO_GEMM_CG=1 disables)
 };
 
 namespace {
@@ -249,10 +251,9 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
   const int n_exec = n_orig + n_united;
   bo_status st;
   if (R == 0 || n_exec == 0) return BO_OK;
-  // Tile width: prefill (many rows per executor) is tensor-bound -> widest
-  // tile; decode (few rows) streams weights from HBM, where the number of
-  // equal-cost tiles decides the wave quantisation over 148 SMs -> narrower.
-  const int tier = R <= 1024 ? 64 : (R <= 4096 ? 128 : 256);
+  // Tile width: widest tile everywhere.  (Narrower decode tiles, tried to cut
+  // the wave quantisation of few-row steps, measured slower: r01 profiles.)
+  const int tier = 256;
   {
     int bn = tier;                                                  // gate + up columns per tile
     while (bn > 64 && (f % (bn / 2) || f_u % (bn / 2))) bn >>= 1;
@@ -279,10 +280,15 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.exec_off = exec_off;
     p.mtile_off = mtile_off;
     p.out = Hbuf;
-    const int64_t max_work = ((R + bo::kBM - 1) / bo::kBM + n_exec) * p.n_tiles;
-    const int grid = static_cast<int>(max_work < h->num_sms ? max_work : h->num_sms);
+    const bool pair = h->cta_pairs && dt == 0 && bn == 256;   // 256 x 256 tiles on CTA pairs
+    const int tile_m = pair ? 2 * bo::kBM : bo::kBM;
+    const int64_t max_work = ((R + tile_m - 1) / tile_m + n_exec) * p.n_tiles;
+    const int units = pair ? h->num_sms / 2 : h->num_sms;
+    const int grid = static_cast<int>(max_work < units ? max_work : units) * (pair ? 2 : 1);
     prof.mark(launches);
-    BO_CUDA(bo::launch_grouped_gemm(dt, bo::EPI_SWIGLU, bn, mA, mG, mU, mUG, mUU, p, grid, s), "gemm1");
+    BO_CUDA(bo::launch_grouped_gemm(dt, pair ? bo::EPI_SWIGLU_PAIR : bo::EPI_SWIGLU, bn, mA, mG, mU, mUG, mUU, p,
+                                    grid, s),
+            "gemm1");
     ++launches;
   }
   {
@@ -310,10 +316,15 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.mtile_off = mtile_off;
     p.out = Y;
     p.row_w = row_w;
-    const int64_t max_work = ((R + bo::kBM - 1) / bo::kBM + n_exec) * p.n_tiles;
-    const int grid = static_cast<int>(max_work < h->num_sms ? max_work : h->num_sms);
+    const bool pair = h->cta_pairs && dt == 0 && bn == 256;
+    const int tile_m = pair ? 2 * bo::kBM : bo::kBM;
+    const int64_t max_work = ((R + tile_m - 1) / tile_m + n_exec) * p.n_tiles;
+    const int units = pair ? h->num_sms / 2 : h->num_sms;
+    const int grid = static_cast<int>(max_work < units ? max_work : units) * (pair ? 2 : 1);
     prof.mark(launches);
-    BO_CUDA(bo::launch_grouped_gemm(dt, bo::EPI_WEIGHTED, bn, mA, mD, mD, mUD, mUD, p, grid, s), "gemm2");
+    BO_CUDA(bo::launch_grouped_gemm(dt, pair ? bo::EPI_WEIGHTED_PAIR : bo::EPI_WEIGHTED, bn, mA, mD, mD, mUD, mUD,
+                                    p, grid, s),
+            "gemm2");
     ++launches;
   }
   return BO_OK;
@@ -440,6 +451,8 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   h->prof_n = 0;
   h->route_T = -1;
   h->route_tile = 0;
+  const char* cg = getenv("BO_GEMM_CG");
+  h->cta_pairs = (cg && cg[0] == '1') ? 0 : 1;
   *out = h;
   return BO_OK;
 }

@@ -30,13 +30,13 @@ struct GemmShape {
                                                                           : 512;
 };
 
-template <typename T, int BN>
+template <typename T, int BN, int CG = 1>
 struct GemmCfg {
-  static constexpr int BM = kBM;
+  static constexpr int BM = kBM;                         // rows per CTA (the pair covers CG * 128)
   static constexpr int BK = 128 / (int)sizeof(T);       // one 128-byte swizzle row
   static constexpr int UK = 32 / (int)sizeof(T);        // MMA K per instruction
   static constexpr int A_BYTES = BM * 128;
-  static constexpr int B_BYTES = BN * 128;
+  static constexpr int B_BYTES = (BN / CG) * 128;       // each CTA of a pair holds half of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
@@ -89,15 +89,22 @@ __device__ __forceinline__ void topk_insert(float (&tv)[KMAX], int (&ti)[KMAX], 
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-template <typename T, int BN, int EPI, int KMAX>
+template <typename T, int BN, int EPI, int KMAX, int CG>
 __global__ void __launch_bounds__(192, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
                    const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmB2,
                    const __grid_constant__ CUtensorMap tmB3, const GemmParams p) {
-  using C = GemmCfg<T, BN>;
+  // CG = 1: one CTA computes a 128 x BN tile with tcgen05.mma.cta_group::1.
+  // CG = 2: a CTA pair (cluster of 2) computes a 256 x BN tile with
+  //         tcgen05.mma.cta_group::2 issued by the leader: each CTA stages its
+  //         128 rows of A and half of B (BN/2 rows), halving the shared-memory
+  //         and L2 traffic per MMA; each CTA's TMEM holds its 128 rows.
+  static_assert(CG == 1 || (CG == 2 && EPI != EPI_ROUTER && sizeof(T) == 2), "pair mode: bf16 FFN GEMMs");
+  using C = GemmCfg<T, BN, CG>;
   constexpr int STAGES = C::STAGES;
   constexpr int TMEM_COLS = GemmShape<BN, EPI>::kTmemCols;
-  constexpr uint32_t IDESC = idesc_f32acc<T>(128, BN);
+  constexpr uint32_t IDESC = idesc_f32acc<T>(128 * CG, BN);
+  constexpr int TILE_M = kBM * CG;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -112,15 +119,19 @@ __global__ void __launch_bounds__(192, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t crank = CG == 2 ? cluster_ctarank() : 0u;
+  const bool leader = crank == 0;
+  const int unit = CG == 2 ? (blockIdx.x >> 1) : blockIdx.x;       // work-unit (CTA or CTA pair) index
+  const int n_units = CG == 2 ? (gridDim.x >> 1) : gridDim.x;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full_bar[s], 1);
+      mbar_init(&full_bar[s], CG);         // pair: both producers arrive on the leader's barrier
       mbar_init(&empty_bar[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 4);
+      mbar_init(&tempty_bar[a], 4 * CG);   // pair: epilogue warps of both CTAs arrive on the leader's
     }
     fence_barrier_init();
   }
@@ -131,23 +142,42 @@ __global__ void __launch_bounds__(192, 1)
     tma_prefetch_desc(&tmB2);
     tma_prefetch_desc(&tmB3);
   }
+  if constexpr (CG == 2) cluster_sync();   // peer barriers initialised before any remote arrive / alloc
   if (warp == 1) {
-    tmem_alloc(tmem_slot, TMEM_COLS);
-    tmem_relinquish();
+    if constexpr (CG == 2) {
+      tmem_alloc_pair(tmem_slot, TMEM_COLS);
+      tmem_relinquish_pair();
+    } else {
+      tmem_alloc(tmem_slot, TMEM_COLS);
+      tmem_relinquish();
+    }
   }
+  // executor row offsets and the prefix of TILE_M-row m-tiles (warp 2, shuffle scan)
   const int nexec = p.single_rows >= 0 ? 1 : p.num_exec;
   if (p.single_rows >= 0) {
     if (threadIdx.x == 0) {
-      s_mtile[0] = 0;
-      s_mtile[1] = (p.single_rows + kBM - 1) / kBM;
       s_eoff[0] = 0;
       s_eoff[1] = p.single_rows;
     }
   } else {
-    for (int i = threadIdx.x; i <= nexec; i += blockDim.x) {
-      s_mtile[i] = p.mtile_off[i];
-      s_eoff[i] = p.exec_off[i];
+    for (int i = threadIdx.x; i <= nexec; i += blockDim.x) s_eoff[i] = p.exec_off[i];
+  }
+  __syncthreads();
+  if (warp == 2) {
+    int carry = 0;
+    for (int i0 = 0; i0 < nexec; i0 += 32) {
+      const int i = i0 + lane;
+      const int v = i < nexec ? (s_eoff[i + 1] - s_eoff[i] + TILE_M - 1) / TILE_M : 0;
+      int incl = v;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += o;
+      }
+      if (i < nexec) s_mtile[i] = carry + incl - v;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
     }
+    if (lane == 0) s_mtile[nexec] = carry;
   }
   tc_fence_before();
   __syncthreads();
@@ -185,10 +215,10 @@ __global__ void __launch_bounds__(192, 1)
       const uint64_t pol_b = policy_evict_normal(); // weight tile is re-read by the executor's other m-tiles
       int stage = 0;
       uint32_t phase = 0;
-      for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
+      for (int w = unit; w < total_work; w += n_units) {
         int x, mi, n;
         decode(w, x, mi, n);
-        const int arow = s_eoff[x] + mi * kBM;
+        const int arow = s_eoff[x] + mi * TILE_M + static_cast<int>(crank) * kBM;
         const bool orig = x < p.m_orig;
         const CUtensorMap* mb0 = orig ? &tmB0 : &tmB2;
         const CUtensorMap* mb1 = orig ? &tmB1 : &tmB3;
@@ -198,13 +228,27 @@ __global__ void __launch_bounds__(192, 1)
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           uint8_t* sb = sa + C::A_BYTES;
-          mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
-          tma_load_2d(sa, &tmA, &full_bar[stage], kb * C::BK, arow, pol_a);
-          if constexpr (EPI == EPI_SWIGLU) {
-            tma_load_2d(sb, mb0, &full_bar[stage], kb * C::BK, brow + n * (BN / 2), pol_b);
-            tma_load_2d(sb + (BN / 2) * 128, mb1, &full_bar[stage], kb * C::BK, brow + n * (BN / 2), pol_b);
+          if constexpr (CG == 1) {
+            mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
+            tma_load_2d(sa, &tmA, &full_bar[stage], kb * C::BK, arow, pol_a);
+            if constexpr (EPI == EPI_SWIGLU) {
+              tma_load_2d(sb, mb0, &full_bar[stage], kb * C::BK, brow + n * (BN / 2), pol_b);
+              tma_load_2d(sb + (BN / 2) * 128, mb1, &full_bar[stage], kb * C::BK, brow + n * (BN / 2), pol_b);
+            } else {
+              tma_load_2d(sb, mb0, &full_bar[stage], kb * C::BK, brow + n * BN, pol_b);
+            }
           } else {
-            tma_load_2d(sb, mb0, &full_bar[stage], kb * C::BK, brow + n * BN, pol_b);
+            // Both CTAs load their halves; completion is counted on the leader's barrier.
+            if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * C::STAGE_BYTES);
+            else mbar_arrive_remote(&full_bar[stage], 0);
+            tma_load_2d_pair(sa, &tmA, &full_bar[stage], kb * C::BK, arow, pol_a);
+            if constexpr (EPI == EPI_SWIGLU) {
+              // leader: gate rows, peer: up rows of the same 128 f-columns -> D[:, 0:128] = gate, D[:, 128:256] = up
+              tma_load_2d_pair(sb, leader ? mb0 : mb1, &full_bar[stage], kb * C::BK, brow + n * (BN / 2), pol_b);
+            } else {
+              tma_load_2d_pair(sb, mb0, &full_bar[stage], kb * C::BK,
+                               brow + n * BN + static_cast<int>(crank) * (BN / 2), pol_b);
+            }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -212,12 +256,12 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else if (warp == 1) {
     // --------------------------------------------------------- MMA issuer
-    if (lane == 0) {
+    if (lane == 0 && leader) {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
+      for (int w = unit; w < total_work; w += n_units) {
         int x, mi, n;
         decode(w, x, mi, n);
         const int num_kb = kblocks(x);
@@ -231,14 +275,28 @@ __global__ void __launch_bounds__(192, 1)
           const uint32_t b_addr = a_addr + C::A_BYTES;
 #pragma unroll
           for (int k = 0; k < C::BK / C::UK; ++k) {
-            mma_ss<T>(sdesc_k_sw128(a_addr + k * 32), sdesc_k_sw128(b_addr + k * 32), d_tmem, IDESC,
-                      (kb | k) != 0 ? 1u : 0u);
+            if constexpr (CG == 1)
+              mma_ss<T>(sdesc_k_sw128(a_addr + k * 32), sdesc_k_sw128(b_addr + k * 32), d_tmem, IDESC,
+                        (kb | k) != 0 ? 1u : 0u);
+            else
+              mma_ss_pair_bf16(sdesc_k_sw128(a_addr + k * 32), sdesc_k_sw128(b_addr + k * 32), d_tmem, IDESC,
+                               (kb | k) != 0 ? 1u : 0u);
           }
-          tc_commit(&empty_bar[stage]);
+          if constexpr (CG == 1) tc_commit(&empty_bar[stage]);
+          else tc_commit_pair(&empty_bar[stage]);   // frees the stage in both CTAs
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        tc_commit(&tfull_bar[acc]);
+        if constexpr (CG == 1) tc_commit(&tfull_bar[acc]);
+        else tc_commit_pair(&tfull_bar[acc]);       // both CTAs' epilogues
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+      if constexpr (CG == 2) {
+        // drain: the peer's last remote arrivals must land before the CTAs exit
+        const int iters = total_work > unit ? (total_work - unit + n_units - 1) / n_units : 0;
+        if (iters > 0) {
+          const int last = iters - 1;
+          mbar_wait(&tempty_bar[last & 1], (last >> 1) & 1);
+        }
       }
     }
   } else {
@@ -246,11 +304,11 @@ __global__ void __launch_bounds__(192, 1)
     const int q = warp & 3;   // TMEM lane quarter this warp may access
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int w = blockIdx.x; w < total_work; w += gridDim.x) {
+    for (int w = unit; w < total_work; w += n_units) {
       int x, mi, n;
       decode(w, x, mi, n);
       const int rows_x = s_eoff[x + 1] - s_eoff[x];
-      const int r_local = mi * kBM + q * 32 + lane;
+      const int r_local = mi * TILE_M + static_cast<int>(crank) * kBM + q * 32 + lane;
       const bool valid = r_local < rows_x;
       const int64_t grow = static_cast<int64_t>(s_eoff[x]) + r_local;
       mbar_wait(&tfull_bar[acc], acc_phase);
@@ -341,33 +399,55 @@ __global__ void __launch_bounds__(192, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+      if (lane == 0) {
+        if (CG == 1 || leader) mbar_arrive(&tempty_bar[acc]);
+        else mbar_arrive_remote(&tempty_bar[acc], 0);
+      }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  if constexpr (CG == 2) cluster_sync();
   if (warp == 1) {
     __syncwarp();
     tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
+    if constexpr (CG == 2) tmem_dealloc_pair(tmem_base, TMEM_COLS);
+    else tmem_dealloc(tmem_base, TMEM_COLS);
   }
 }
 
-template <typename T, int BN, int EPI, int KMAX = 0>
+template <typename T, int BN, int EPI, int KMAX = 0, int CG = 1>
 static cudaError_t launch_t(const CUtensorMap& A, const CUtensorMap& B0, const CUtensorMap& B1,
                             const CUtensorMap& B2, const CUtensorMap& B3, const GemmParams& p, int grid,
                             cudaStream_t s) {
-  using C = GemmCfg<T, BN>;
+  using C = GemmCfg<T, BN, CG>;
   static bool attr_set = false;
-  auto kern = k_grouped_gemm<T, BN, EPI, KMAX>;
+  auto kern = k_grouped_gemm<T, BN, EPI, KMAX, CG>;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  kern<<<grid, 192, C::SMEM, s>>>(A, B0, B1, B2, B3, p);
+  if constexpr (CG == 1) {
+    kern<<<grid, 192, C::SMEM, s>>>(A, B0, B1, B2, B3, p);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid & ~1));
+    cfg.blockDim = dim3(192);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, A, B0, B1, B2, B3, p);
+    if (e != cudaSuccess) return e;
+  }
   return cudaGetLastError();
 }
 
@@ -375,7 +455,13 @@ template <typename T>
 static cudaError_t dispatch(int epi, int bn, const CUtensorMap& A, const CUtensorMap& B0, const CUtensorMap& B1,
                             const CUtensorMap& B2, const CUtensorMap& B3, const GemmParams& p, int grid,
                             cudaStream_t s) {
-  if (epi == EPI_SWIGLU) {
+  if (epi == EPI_SWIGLU_PAIR) {
+    if constexpr (sizeof(T) == 2)
+      if (bn == 256) return launch_t<T, 256, EPI_SWIGLU, 0, 2>(A, B0, B1, B2, B3, p, grid, s);
+  } else if (epi == EPI_WEIGHTED_PAIR) {
+    if constexpr (sizeof(T) == 2)
+      if (bn == 256) return launch_t<T, 256, EPI_WEIGHTED, 0, 2>(A, B0, B1, B2, B3, p, grid, s);
+  } else if (epi == EPI_SWIGLU) {
     if (bn == 256) return launch_t<T, 256, EPI_SWIGLU>(A, B0, B1, B2, B3, p, grid, s);
     if (bn == 128) return launch_t<T, 128, EPI_SWIGLU>(A, B0, B1, B2, B3, p, grid, s);
     if (bn == 64) return launch_t<T, 64, EPI_SWIGLU>(A, B0, B1, B2, B3, p, grid, s);

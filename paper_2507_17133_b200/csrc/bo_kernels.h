@@ -12,7 +12,8 @@ constexpr int kBM = 128;        // rows per GEMM tile (TMEM lanes)
 constexpr int kMaxExperts = 256;
 constexpr int kMaxExec = 512;   // m + G
 
-enum Epi : int { EPI_SWIGLU = 0, EPI_WEIGHTED = 1, EPI_ROUTER = 2 };
+enum Epi : int { EPI_SWIGLU = 0, EPI_WEIGHTED = 1, EPI_ROUTER = 2,
+                 EPI_SWIGLU_PAIR = 3, EPI_WEIGHTED_PAIR = 4 };   // *_PAIR: cta_group::2, grid even
 
 struct GemmParams {
   int Kdim;              // reduction length (executors < m_orig)
