@@ -294,12 +294,14 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
   {
     int bn = gemm2_bn(d);
     if (bn > tier) bn = tier;
+    const bool pair = h->cta_pairs && dt == 0 && bn == 256;   // each CTA of a pair stages BN/2 rows of B
+    const uint32_t box_b = pair ? bn / 2 : bn;
     CUtensorMap mA, mD, mUD;
     if ((st = make_map(&mA, Hbuf, c.dtype, R, f, bo::kBM)) != BO_OK) return st;
     const uint64_t orows = static_cast<uint64_t>(n_orig > 0 ? n_orig : 1) * d;
     const uint64_t urows = static_cast<uint64_t>(united_stack > 0 ? united_stack : 1) * d;
-    if ((st = make_map(&mD, Wd, c.dtype, orows, f, bn)) != BO_OK) return st;
-    if ((st = make_map(&mUD, UWd, c.dtype, urows, f_u, bn)) != BO_OK) return st;
+    if ((st = make_map(&mD, Wd, c.dtype, orows, f, box_b)) != BO_OK) return st;
+    if ((st = make_map(&mUD, UWd, c.dtype, urows, f_u, box_b)) != BO_OK) return st;
     bo::GemmParams p{};
     p.Kdim = f;
     p.n_tiles = d / bn;
@@ -316,7 +318,6 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.mtile_off = mtile_off;
     p.out = Y;
     p.row_w = row_w;
-    const bool pair = h->cta_pairs && dt == 0 && bn == 256;
     const int tile_m = pair ? 2 * bo::kBM : bo::kBM;
     const int64_t max_work = ((R + tile_m - 1) / tile_m + n_exec) * p.n_tiles;
     const int units = pair ? h->num_sms / 2 : h->num_sms;
