@@ -38,14 +38,60 @@ struct GemmCfg {
   static constexpr int A_BYTES = BM * 128;
   static constexpr int B_BYTES = (BN / CG) * 128;       // each CTA of a pair holds half of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES_RAW = (200 * 1024) / STAGE_BYTES;
-  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int BAR_BYTES = 2048;                 // barriers + tmem slot (1 KB) + router histogram (1 KB)
   static constexpr int SCHED_BYTES = 2 * (kMaxExec + 1) * 4;
-  static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE_BYTES + BAR_BYTES + SCHED_BYTES;
+  static constexpr int EPI_ROW = 32 * (int)sizeof(T) + 16;   // staged 32-column row chunk + bank pad
+  static constexpr int EPI_BYTES = 4 * 32 * EPI_ROW;         // one staging tile per epilogue warp
+  static constexpr int OTHER = 1024 /*align slack*/ + BAR_BYTES + SCHED_BYTES + EPI_BYTES;
+  static constexpr int STAGES_RAW = (227 * 1024 - OTHER) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int SMEM = OTHER + STAGES * STAGE_BYTES;
 };
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+
+// Coalesced epilogue store of a 32-row x 32-column chunk owned by one warp
+// (thread = row, as tcgen05.ld 32x32b delivers it): rows are staged in the
+// warp's shared-memory tile (16-byte pad -> conflict-free), then written back
+// as whole 64/128-byte row segments, several rows per store instruction.
+template <typename T>
+__device__ __forceinline__ void stage_row32(uint8_t* stage, int lane, const float (&v)[32]) {
+  constexpr int ROW = 32 * (int)sizeof(T) + 16;
+  uint4* d = reinterpret_cast<uint4*>(stage + lane * ROW);
+  if constexpr (sizeof(T) == 2) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 u;
+      u.x = pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+      u.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+      u.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+      u.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+      d[q] = u;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      d[q] = make_uint4(__float_as_uint(v[4 * q]), __float_as_uint(v[4 * q + 1]), __float_as_uint(v[4 * q + 2]),
+                        __float_as_uint(v[4 * q + 3]));
+  }
+}
+// rows of the warp: global row index = row0 + r (r < nrows valid), column offset col0.
+template <typename T>
+__device__ __forceinline__ void flush_rows32(const uint8_t* stage, int lane, T* out, int64_t row0, int nrows,
+                                             int64_t ldo) {
+  constexpr int V16 = 32 * (int)sizeof(T) / 16;   // 16-byte pieces per row chunk
+  constexpr int ROW = 32 * (int)sizeof(T) + 16;
+  constexpr int RPI = 32 / V16;                    // rows per store instruction
+  const int piece = lane % V16;
+#pragma unroll
+  for (int i = 0; i < V16; ++i) {
+    const int r = i * RPI + lane / V16;
+    if (r < nrows) {
+      const uint4 v = *reinterpret_cast<const uint4*>(stage + r * ROW + piece * 16);
+      *reinterpret_cast<uint4*>(out + (row0 + r) * ldo + piece * (16 / (int)sizeof(T))) = v;
+    }
+  }
+}
 
 template <typename T>
 __device__ __forceinline__ void store_row32(T* dst, const float (&v)[32]);
@@ -116,6 +162,7 @@ __global__ void __launch_bounds__(192, 1)
   int* s_hist = reinterpret_cast<int*>(smem + STAGES * C::STAGE_BYTES + 1024);
   int* s_mtile = reinterpret_cast<int*>(smem + STAGES * C::STAGE_BYTES + C::BAR_BYTES);
   int* s_eoff = s_mtile + (kMaxExec + 1);
+  uint8_t* s_epi = smem + STAGES * C::STAGE_BYTES + C::BAR_BYTES + C::SCHED_BYTES;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -314,8 +361,13 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t t0 = tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(q * 32) << 16);
+      // rows of this warp's 32-row slab that belong to the executor
+      const int slab = mi * TILE_M + static_cast<int>(crank) * kBM + q * 32;
+      const int nrows = rows_x - slab < 0 ? 0 : (rows_x - slab > 32 ? 32 : rows_x - slab);
+      const int64_t row0 = static_cast<int64_t>(s_eoff[x]) + slab;
+      uint8_t* stage = s_epi + (warp - 2) * 32 * C::EPI_ROW;
       if constexpr (EPI == EPI_SWIGLU) {
-        T* out = reinterpret_cast<T*>(p.out) + grow * p.ldo + n * (BN / 2);
+        T* out = reinterpret_cast<T*>(p.out) + n * (BN / 2);
 #pragma unroll 1
         for (int c = 0; c < BN / 2; c += 32) {
           uint32_t g[32], u[32];
@@ -325,11 +377,14 @@ __global__ void __launch_bounds__(192, 1)
           float h[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) h[i] = silu_f(__uint_as_float(g[i])) * __uint_as_float(u[i]);
-          if (valid) store_row32<T>(out + c, h);
+          stage_row32<T>(stage, lane, h);
+          __syncwarp();
+          flush_rows32<T>(stage, lane, out + c, row0, nrows, p.ldo);
+          __syncwarp();
         }
       } else if constexpr (EPI == EPI_WEIGHTED) {
         const float wr = valid ? p.row_w[grow] : 0.0f;
-        T* out = reinterpret_cast<T*>(p.out) + grow * p.ldo + n * BN;
+        T* out = reinterpret_cast<T*>(p.out) + n * BN;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           uint32_t a[32];
@@ -338,7 +393,10 @@ __global__ void __launch_bounds__(192, 1)
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(a[i]) * wr;
-          if (valid) store_row32<T>(out + c, v);
+          stage_row32<T>(stage, lane, v);
+          __syncwarp();
+          flush_rows32<T>(stage, lane, out + c, row0, nrows, p.ldo);
+          __syncwarp();
         }
       } else {
         // Router (Eq. 8) with Eq. 7 fused: this thread owns token `grow`'s m logits.

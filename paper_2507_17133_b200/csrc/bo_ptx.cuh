@@ -191,7 +191,9 @@ __device__ __forceinline__ void cluster_sync() {
 __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(cta));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+  // default (.release.cta) semantics: no ordering of this thread's global writes is needed, and a
+  // .release.cluster arrive compiles to MEMBAR.ALL.GPU, which stalled the pair pipeline (r01 ncu).
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 // TMA load by either CTA of a pair whose completion is signalled on the LEADER
 // CTA's mbarrier (peer bit of the shared::cluster address cleared).
