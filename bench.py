@@ -118,7 +118,13 @@ def algorithmic(cfg, T, stats, d, f, m):
             "weight_bytes": w_bytes}
 
 
-KERNELS = ["router_topk", "plan", "permute", "gather", "gemm1_swiglu", "gemm2_weighted", "combine"]
+KERNELS_7 = ["router_topk", "plan", "permute", "gather", "gemm1_swiglu", "gemm2_weighted", "combine"]
+KERNELS_6 = ["router_topk", "plan", "permute", "gemm1_swiglu", "gemm2_weighted", "combine"]   # gather fused in GEMM1
+KERNELS = KERNELS_7
+
+
+def kernel_names(layer):
+    return KERNELS_6 if layer.moe.last_launch_count() == 6 else KERNELS_7
 
 
 class Layer:
@@ -163,9 +169,10 @@ def time_steps(layer, steps, warmup, dist_on, per_kernel=True, graph=True):
     for _ in range(warmup):
         layer.step()
     torch.cuda.synchronize()
+    names = kernel_names(layer)
     ev_sets = None
     if per_kernel:
-        ev_sets = [[torch.cuda.Event(enable_timing=True) for _ in range(len(KERNELS) + 1)] for _ in range(steps)]
+        ev_sets = [[torch.cuda.Event(enable_timing=True) for _ in range(len(KERNELS_7) + 1)] for _ in range(steps)]
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     g = None
@@ -209,7 +216,7 @@ def time_steps(layer, steps, warmup, dist_on, per_kernel=True, graph=True):
     kern = None
     if ev_sets:
         kern = {}
-        for j, name in enumerate(KERNELS):
+        for j, name in enumerate(names):
             kern[name] = sum(ev[j].elapsed_time(ev[j + 1]) for ev in ev_sets) / steps
     del g
     return ms, kern

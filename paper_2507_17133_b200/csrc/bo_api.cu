@@ -26,6 +26,7 @@ struct bo_handle {
   int64_t route_T;     // token count / tile of the last route stage (bo_route, forward)
   int32_t route_tile;
   int32_t cta_pairs;   // 1: prefill FFN GEMMs use cta_group::2 CTA pairs (env BO_GEMM_CG=1 disables)
+  int32_t fused_gather;  // 1: GEMM1 gathers x rows by TMA gather4 (env BO_GATHER=0 disables)
 };
 
 namespace {
@@ -244,7 +245,10 @@ bo_status route_stage(bo_handle* h, const void* x, int64_t T, const void* Wr, co
 bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, const int32_t* exec_off,
                     const int32_t* mtile_off, int n_orig, int n_united, int f_u, const void* Wg, const void* Wu,
                     const void* Wd, const void* UWg, const void* UWu, const void* UWd, int64_t united_stack,
-                    void* Hbuf, void* Y, cudaStream_t s, Prof& prof, int& launches) {
+                    void* Hbuf, void* Y, cudaStream_t s, Prof& prof, int& launches,
+                    const int32_t* gather_tok = nullptr, int64_t gather_T = 0) {
+  // gather_tok != nullptr: X is the token matrix x [gather_T, d] and GEMM1 gathers
+  // row r = x[gather_tok[r]] with TMA tile::gather4 (no packed Xp).
   const bo_config& c = h->cfg;
   const int dt = c.dtype == BO_BF16 ? 0 : 1;
   const int d = c.hidden, f = c.ffn;
@@ -258,7 +262,12 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     int bn = tier;                                                  // gate + up columns per tile
     while (bn > 64 && (f % (bn / 2) || f_u % (bn / 2))) bn >>= 1;
     CUtensorMap mA, mG, mU, mUG, mUU;
-    if ((st = make_map(&mA, X, c.dtype, R, d, bo::kBM)) != BO_OK) return st;
+    const bool gather = gather_tok != nullptr;
+    if (gather) {
+      if ((st = make_map(&mA, X, c.dtype, gather_T, d, 1)) != BO_OK) return st;   // box {64 cols, 1 row}
+    } else {
+      if ((st = make_map(&mA, X, c.dtype, R, d, bo::kBM)) != BO_OK) return st;
+    }
     const uint64_t orows = static_cast<uint64_t>(n_orig > 0 ? n_orig : 1) * f;
     const uint64_t urows = static_cast<uint64_t>(united_stack > 0 ? united_stack : 1) * f_u;
     if ((st = make_map(&mG, Wg, c.dtype, orows, d, bn / 2)) != BO_OK) return st;
@@ -280,15 +289,17 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.exec_off = exec_off;
     p.mtile_off = mtile_off;
     p.out = Hbuf;
+    p.row_tok = gather_tok;
+    p.rows_total = static_cast<int>(R);
     const bool pair = h->cta_pairs && dt == 0 && bn == 256;   // 256 x 256 tiles on CTA pairs
     const int tile_m = pair ? 2 * bo::kBM : bo::kBM;
     const int64_t max_work = ((R + tile_m - 1) / tile_m + n_exec) * p.n_tiles;
     const int units = pair ? h->num_sms / 2 : h->num_sms;
     const int grid = static_cast<int>(max_work < units ? max_work : units) * (pair ? 2 : 1);
     prof.mark(launches);
-    BO_CUDA(bo::launch_grouped_gemm(dt, pair ? bo::EPI_SWIGLU_PAIR : bo::EPI_SWIGLU, bn, mA, mG, mU, mUG, mUU, p,
-                                    grid, s),
-            "gemm1");
+    const int epi = gather ? (pair ? bo::EPI_SWIGLU_PAIR_GATHER : bo::EPI_SWIGLU_GATHER)
+                           : (pair ? bo::EPI_SWIGLU_PAIR : bo::EPI_SWIGLU);
+    BO_CUDA(bo::launch_grouped_gemm(dt, epi, bn, mA, mG, mU, mUG, mUU, p, grid, s), "gemm1");
     ++launches;
   }
   {
@@ -381,15 +392,25 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
                              at<int32_t>(ws, L.row_tok), row_w, s),
           "permute");
   ++launches;
-  void* xp = at<char>(ws, L.xp);
-  prof.mark(launches);
-  BO_CUDA(bo::launch_gather(dt, x, static_cast<int>(T), d, K, row_of, xp, h->num_sms, s), "gather");
-  ++launches;
-  // a6-a7: grouped SwiGLU FFN over the m original + G united executors
+  // a6-a7: grouped SwiGLU FFN over the m original + G united executors.  By
+  // default GEMM1 gathers its A rows straight from x (concat_tokens fused into
+  // the TMA operand load); BO_GATHER=0 materialises Xp with the gather kernel.
   void* yp = at<char>(ws, L.yp);
-  if ((st = ffn_stage(h, xp, R, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), m, G, f, Wg, Wu,
-                      Wd, UWg, UWu, UWd, have_united ? G : m, at<char>(ws, L.h), yp, s, prof, launches)) != BO_OK)
-    return st;
+  const int32_t* row_tok = at<int32_t>(ws, L.row_tok);
+  if (h->fused_gather) {
+    if ((st = ffn_stage(h, x, R, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), m, G, f, Wg, Wu,
+                        Wd, UWg, UWu, UWd, have_united ? G : m, at<char>(ws, L.h), yp, s, prof, launches, row_tok,
+                        T)) != BO_OK)
+      return st;
+  } else {
+    void* xp = at<char>(ws, L.xp);
+    prof.mark(launches);
+    BO_CUDA(bo::launch_gather(dt, x, static_cast<int>(T), d, K, row_of, xp, h->num_sms, s), "gather");
+    ++launches;
+    if ((st = ffn_stage(h, xp, R, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), m, G, f, Wg, Wu,
+                        Wd, UWg, UWu, UWd, have_united ? G : m, at<char>(ws, L.h), yp, s, prof, launches)) != BO_OK)
+      return st;
+  }
   // a8: combine (Eq. 5 sum over the token's K slots)
   prof.mark(launches);
   BO_CUDA(bo::launch_combine(dt, yp, x, static_cast<int>(T), d, K, row_of, c.add_residual, y, h->num_sms, s),
@@ -454,6 +475,8 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   h->route_tile = 0;
   const char* cg = getenv("BO_GEMM_CG");
   h->cta_pairs = (cg && cg[0] == '1') ? 0 : 1;
+  const char* ga = getenv("BO_GATHER");
+  h->fused_gather = (ga && ga[0] == '0') ? 0 : 1;
   *out = h;
   return BO_OK;
 }

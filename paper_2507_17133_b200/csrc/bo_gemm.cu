@@ -39,7 +39,7 @@ struct GemmCfg {
   static constexpr int B_BYTES = (BN / CG) * 128;       // each CTA of a pair holds half of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int BAR_BYTES = 2048;                 // barriers + tmem slot (1 KB) + router histogram (1 KB)
-  static constexpr int SCHED_BYTES = 2 * (kMaxExec + 1) * 4;
+  static constexpr int SCHED_BYTES = ((2 * (kMaxExec + 1) * 4) + 127) / 128 * 128;   // keeps the staging 16B-aligned
   static constexpr int EPI_ROW = 32 * (int)sizeof(T) + 16;   // staged 32-column row chunk + bank pad
   static constexpr int EPI_BYTES = 4 * 32 * EPI_ROW;         // one staging tile per epilogue warp
   static constexpr int OTHER = 1024 /*align slack*/ + BAR_BYTES + SCHED_BYTES + EPI_BYTES;
@@ -135,7 +135,7 @@ __device__ __forceinline__ void topk_insert(float (&tv)[KMAX], int (&ti)[KMAX], 
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-template <typename T, int BN, int EPI, int KMAX, int CG>
+template <typename T, int BN, int EPI, int KMAX, int CG, bool GATHER>
 __global__ void __launch_bounds__(192, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
                    const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmB2,
@@ -146,6 +146,10 @@ __global__ void __launch_bounds__(192, 1)
   //         128 rows of A and half of B (BN/2 rows), halving the shared-memory
   //         and L2 traffic per MMA; each CTA's TMEM holds its 128 rows.
   static_assert(CG == 1 || (CG == 2 && EPI != EPI_ROUTER && sizeof(T) == 2), "pair mode: bf16 FFN GEMMs");
+  // GATHER: the A rows are not read from a packed Xp but gathered from the token
+  // matrix x by TMA tile::gather4 (4 rows per instruction, row index = row_tok),
+  // i.e. concat_tokens fused into GEMM1's operand load.
+  static_assert(!GATHER || EPI == EPI_SWIGLU, "gather feeds GEMM1 only");
   using C = GemmCfg<T, BN, CG>;
   constexpr int STAGES = C::STAGES;
   constexpr int TMEM_COLS = GemmShape<BN, EPI>::kTmemCols;
@@ -257,7 +261,7 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
-    if (lane == 0) {
+    if (GATHER || lane == 0) {
       const uint64_t pol_a = policy_evict_last();   // activations are re-read per n-tile
       const uint64_t pol_b = policy_evict_normal(); // weight tile is re-read by the executor's other m-tiles
       int stage = 0;
@@ -271,31 +275,45 @@ __global__ void __launch_bounds__(192, 1)
         const CUtensorMap* mb1 = orig ? &tmB1 : &tmB3;
         const int brow = orig ? x * p.b_rows_per_exec : (x - p.m_orig) * p.b_rows_u;
         const int num_kb = kblocks(x);
+        int4 tok = make_int4(0, 0, 0, 0);
+        if constexpr (GATHER) {   // this lane gathers rows arow + 4*lane .. +3 (their tokens)
+          const int r = arow + 4 * lane;
+          tok.x = r + 0 < p.rows_total ? __ldg(p.row_tok + r + 0) : 0;
+          tok.y = r + 1 < p.rows_total ? __ldg(p.row_tok + r + 1) : 0;
+          tok.z = r + 2 < p.rows_total ? __ldg(p.row_tok + r + 2) : 0;
+          tok.w = r + 3 < p.rows_total ? __ldg(p.row_tok + r + 3) : 0;
+        }
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           uint8_t* sb = sa + C::A_BYTES;
-          if constexpr (CG == 1) {
-            mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
-            tma_load_2d(sa, &tmA, &full_bar[stage], kb * C::BK, arow, pol_a);
-            if constexpr (EPI == EPI_SWIGLU) {
-              tma_load_2d(sb, mb0, &full_bar[stage], kb * C::BK, brow + n * (BN / 2), pol_b);
-              tma_load_2d(sb + (BN / 2) * 128, mb1, &full_bar[stage], kb * C::BK, brow + n * (BN / 2), pol_b);
+          if (lane == 0) {
+            if constexpr (CG == 1) {
+              mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
+              if constexpr (!GATHER) tma_load_2d(sa, &tmA, &full_bar[stage], kb * C::BK, arow, pol_a);
+              if constexpr (EPI == EPI_SWIGLU) {
+                tma_load_2d(sb, mb0, &full_bar[stage], kb * C::BK, brow + n * (BN / 2), pol_b);
+                tma_load_2d(sb + (BN / 2) * 128, mb1, &full_bar[stage], kb * C::BK, brow + n * (BN / 2), pol_b);
+              } else {
+                tma_load_2d(sb, mb0, &full_bar[stage], kb * C::BK, brow + n * BN, pol_b);
+              }
             } else {
-              tma_load_2d(sb, mb0, &full_bar[stage], kb * C::BK, brow + n * BN, pol_b);
+              // Both CTAs load their halves; completion is counted on the leader's barrier.
+              if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * C::STAGE_BYTES);
+              else mbar_arrive_remote(&full_bar[stage], 0);
+              if constexpr (!GATHER) tma_load_2d_pair(sa, &tmA, &full_bar[stage], kb * C::BK, arow, pol_a);
+              if constexpr (EPI == EPI_SWIGLU) {
+                // leader: gate rows, peer: up rows of the same f-columns -> D[:, 0:BN/2] = gate, D[:, BN/2:] = up
+                tma_load_2d_pair(sb, leader ? mb0 : mb1, &full_bar[stage], kb * C::BK, brow + n * (BN / 2), pol_b);
+              } else {
+                tma_load_2d_pair(sb, mb0, &full_bar[stage], kb * C::BK,
+                                 brow + n * BN + static_cast<int>(crank) * (BN / 2), pol_b);
+              }
             }
-          } else {
-            // Both CTAs load their halves; completion is counted on the leader's barrier.
-            if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * C::STAGE_BYTES);
-            else mbar_arrive_remote(&full_bar[stage], 0);
-            tma_load_2d_pair(sa, &tmA, &full_bar[stage], kb * C::BK, arow, pol_a);
-            if constexpr (EPI == EPI_SWIGLU) {
-              // leader: gate rows, peer: up rows of the same 128 f-columns -> D[:, 0:128] = gate, D[:, 128:256] = up
-              tma_load_2d_pair(sb, leader ? mb0 : mb1, &full_bar[stage], kb * C::BK, brow + n * (BN / 2), pol_b);
-            } else {
-              tma_load_2d_pair(sb, mb0, &full_bar[stage], kb * C::BK,
-                               brow + n * BN + static_cast<int>(crank) * (BN / 2), pol_b);
-            }
+          }
+          if constexpr (GATHER) {
+            if constexpr (CG == 1) tma_gather4(sa + lane * 512, &tmA, &full_bar[stage], kb * C::BK, tok, pol_a);
+            else tma_gather4_pair(sa + lane * 512, &tmA, &full_bar[stage], kb * C::BK, tok, pol_a);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -476,13 +494,13 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
-template <typename T, int BN, int EPI, int KMAX = 0, int CG = 1>
+template <typename T, int BN, int EPI, int KMAX = 0, int CG = 1, bool GATHER = false>
 static cudaError_t launch_t(const CUtensorMap& A, const CUtensorMap& B0, const CUtensorMap& B1,
                             const CUtensorMap& B2, const CUtensorMap& B3, const GemmParams& p, int grid,
                             cudaStream_t s) {
   using C = GemmCfg<T, BN, CG>;
   static bool attr_set = false;
-  auto kern = k_grouped_gemm<T, BN, EPI, KMAX, CG>;
+  auto kern = k_grouped_gemm<T, BN, EPI, KMAX, CG, GATHER>;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return e;
@@ -513,7 +531,13 @@ template <typename T>
 static cudaError_t dispatch(int epi, int bn, const CUtensorMap& A, const CUtensorMap& B0, const CUtensorMap& B1,
                             const CUtensorMap& B2, const CUtensorMap& B3, const GemmParams& p, int grid,
                             cudaStream_t s) {
-  if (epi == EPI_SWIGLU_PAIR) {
+  if (epi == EPI_SWIGLU_GATHER) {
+    if (bn == 256) return launch_t<T, 256, EPI_SWIGLU, 0, 1, true>(A, B0, B1, B2, B3, p, grid, s);
+    if (bn == 128) return launch_t<T, 128, EPI_SWIGLU, 0, 1, true>(A, B0, B1, B2, B3, p, grid, s);
+  } else if (epi == EPI_SWIGLU_PAIR_GATHER) {
+    if constexpr (sizeof(T) == 2)
+      if (bn == 256) return launch_t<T, 256, EPI_SWIGLU, 0, 2, true>(A, B0, B1, B2, B3, p, grid, s);
+  } else if (epi == EPI_SWIGLU_PAIR) {
     if constexpr (sizeof(T) == 2)
       if (bn == 256) return launch_t<T, 256, EPI_SWIGLU, 0, 2>(A, B0, B1, B2, B3, p, grid, s);
   } else if (epi == EPI_WEIGHTED_PAIR) {

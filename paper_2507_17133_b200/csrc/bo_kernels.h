@@ -13,7 +13,8 @@ constexpr int kMaxExperts = 256;
 constexpr int kMaxExec = 512;   // m + G
 
 enum Epi : int { EPI_SWIGLU = 0, EPI_WEIGHTED = 1, EPI_ROUTER = 2,
-                 EPI_SWIGLU_PAIR = 3, EPI_WEIGHTED_PAIR = 4 };   // *_PAIR: cta_group::2, grid even
+                 EPI_SWIGLU_PAIR = 3, EPI_WEIGHTED_PAIR = 4,    // *_PAIR: cta_group::2, grid even
+                 EPI_SWIGLU_GATHER = 5, EPI_SWIGLU_PAIR_GATHER = 6 };   // A rows gathered from x (row_tok)
 
 struct GemmParams {
   int Kdim;              // reduction length (executors < m_orig)
@@ -35,6 +36,8 @@ struct GemmParams {
   int32_t* topk_id;      // EPI_ROUTER: [T, K]
   float* topk_w;         // EPI_ROUTER: [T, K]
   int32_t* tile_cnt;     // EPI_ROUTER: [ceil(T/128), m] histogram per 128-token tile
+  const int32_t* row_tok;  // *_GATHER: token of each row (A row r = x[row_tok[r]])
+  int rows_total;          // *_GATHER: R (rows >= R gather token 0, masked at the store)
 };
 
 // Grouped tcgen05 GEMM: for each executor x and each 128-row tile of its rows,

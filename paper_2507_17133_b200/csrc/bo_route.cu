@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
                                               int32_t* __restrict__ counts, int32_t* __restrict__ exec_of_expert,
                                               int32_t* __restrict__ expert_row_off, int32_t* __restrict__ exec_off,
                                               int32_t* __restrict__ mtile_off, int64_t* __restrict__ stats) {
-  __shared__ int s_tc[kPlanStage];
+  __shared__ __align__(16) int s_tc[kPlanStage];
   __shared__ int s_cnt[kMaxExperts];
   __shared__ int s_sorted[kMaxExperts];
   __shared__ long long s_excl[kMaxExperts];
@@ -338,8 +338,12 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
   // 1. cnt_i (Alg. 1 input) and the per-tile exclusive prefix used by
   //    the permutation.  Histograms are staged with coalesced loads, then a
   //    warp per expert scans over tiles (lanes over tiles, shuffle scan + carry).
-  if (staged)
-    for (int i = tid; i < n_tc; i += blockDim.x) s_tc[i] = __ldg(tile_cnt + i);
+  if (staged) {   // all loads in flight at once (cp.async), not one dependent load per iteration
+    const int n16 = n_tc / 4;
+    for (int i = tid; i < n16; i += blockDim.x) cp_async16(s_tc + 4 * i, tile_cnt + 4 * i);
+    for (int i = 4 * n16 + tid; i < n_tc; i += blockDim.x) s_tc[i] = __ldg(tile_cnt + i);
+    cp_async_wait_all();
+  }
   if (tid < m) s_gsize[tid] = 0;
   __syncthreads();
   for (int e = warp; e < m; e += 16) {
