@@ -26,7 +26,7 @@ struct bo_handle {
   int64_t route_T;     // token count / tile of the last route stage (bo_route, forward)
   int32_t route_tile;
   int32_t cta_pairs;   // 1: prefill FFN GEMMs use cta_group::2 CTA pairs (env BO_GEMM_CG=1 disables)
-  int32_t fused_gather;  // 1: GEMM1 gathers x rows by TMA gather4 (env BO_GATHER=0 disables)
+  int32_t fused_gather;  // 1: GEMM1 gathers x rows by TMA gather4 (env BO_GATHER=1; default off)
 };
 
 namespace {
@@ -392,9 +392,9 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
                              at<int32_t>(ws, L.row_tok), row_w, s),
           "permute");
   ++launches;
-  // a6-a7: grouped SwiGLU FFN over the m original + G united executors.  By
-  // default GEMM1 gathers its A rows straight from x (concat_tokens fused into
-  // the TMA operand load); BO_GATHER=0 materialises Xp with the gather kernel.
+  // a6-a7: grouped SwiGLU FFN over the m original + G united executors.  The
+  // gather kernel materialises Xp (concat_tokens); BO_GATHER=1 instead lets
+  // GEMM1 gather its A rows from x with TMA tile::gather4 (slower, see above).
   void* yp = at<char>(ws, L.yp);
   const int32_t* row_tok = at<int32_t>(ws, L.row_tok);
   if (h->fused_gather) {
@@ -475,8 +475,10 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   h->route_tile = 0;
   const char* cg = getenv("BO_GEMM_CG");
   h->cta_pairs = (cg && cg[0] == '1') ? 0 : 1;
+  // TMA gather4 (4 rows x 128 B per instruction, 32 per k-block) measured 2.8x slower
+  // than materialising Xp (r01 profiles): off unless BO_GATHER=1.
   const char* ga = getenv("BO_GATHER");
-  h->fused_gather = (ga && ga[0] == '0') ? 0 : 1;
+  h->fused_gather = (ga && ga[0] == '1') ? 1 : 0;
   *out = h;
   return BO_OK;
 }
