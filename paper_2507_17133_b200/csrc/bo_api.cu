@@ -291,7 +291,9 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.out = Hbuf;
     p.row_tok = gather_tok;
     p.rows_total = static_cast<int>(R);
-    const bool pair = h->cta_pairs && dt == 0 && bn == 256;   // 256 x 256 tiles on CTA pairs
+    // 256 x 256 tiles on CTA pairs when rows are plentiful (prefill); few-row
+    // (decode) steps keep 128-row tiles so that more tiles share the SMs.
+    const bool pair = h->cta_pairs && dt == 0 && bn == 256 && R >= 2048;
     const int tile_m = pair ? 2 * bo::kBM : bo::kBM;
     const int64_t max_work = ((R + tile_m - 1) / tile_m + n_exec) * p.n_tiles;
     const int units = pair ? h->num_sms / 2 : h->num_sms;
@@ -305,7 +307,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
   {
     int bn = gemm2_bn(d);
     if (bn > tier) bn = tier;
-    const bool pair = h->cta_pairs && dt == 0 && bn == 256;   // each CTA of a pair stages BN/2 rows of B
+    const bool pair = h->cta_pairs && dt == 0 && bn == 256 && R >= 2048;   // each CTA of a pair stages BN/2 of B
     const uint32_t box_b = pair ? bn / 2 : bn;
     CUtensorMap mA, mD, mUD;
     if ((st = make_map(&mA, Hbuf, c.dtype, R, f, bo::kBM)) != BO_OK) return st;

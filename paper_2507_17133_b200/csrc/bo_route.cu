@@ -553,27 +553,33 @@ cudaError_t launch_permute(const int32_t* topk_id, const float* topk_w, int T, i
 }
 
 // ----------------------------------------------------------------- gather
-// Warp per token: each 16-byte chunk of x[t] is loaded once and stored to all
-// of the token's rows (KR = K * nrep row slots; row indices one per lane,
-// broadcast by shuffle).
+// Flattened over (token, 16-byte vector): consecutive threads copy consecutive
+// vectors of the same token (coalesced), each x vector is loaded once and
+// stored to all of the token's rows (KR = K * nrep row slots).  UNROLL
+// independent items per thread keep several loads in flight; the flat index
+// space fills every SM even for a few hundred (decode) tokens.
+template <int UNROLL>
 __global__ void __launch_bounds__(256) k_gather(const uint4* __restrict__ x, int T, int vec_per_row, int KR,
                                                 const int32_t* __restrict__ row_of, uint4* __restrict__ xp) {
-  const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int t = gw; t < T; t += nw) {
-    const uint4* src = x + static_cast<int64_t>(t) * vec_per_row;
-    for (int r0 = 0; r0 < KR; r0 += 32) {
-      const int nr = min(32, KR - r0);
-      const int my_row = lane < nr ? row_of[static_cast<int64_t>(t) * KR + r0 + lane] : -1;
-      for (int c0 = 0; c0 < vec_per_row; c0 += 32) {   // warp-uniform trip count (shuffles below)
-        const int c = c0 + lane;
-        const bool ok = c < vec_per_row;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (ok) v = __ldg(src + c);
-        for (int s = 0; s < nr; ++s) {
-          const int r = __shfl_sync(0xffffffffu, my_row, s);
-          if (ok && r >= 0) xp[static_cast<int64_t>(r) * vec_per_row + c] = v;
+  const int64_t total = static_cast<int64_t>(T) * vec_per_row;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; base < total;
+       base += stride * UNROLL) {
+    uint4 v[UNROLL];
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const int64_t i = base + u * stride;
+      if (i < total) v[u] = __ldg(x + i);
+    }
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      const int64_t i = base + u * stride;
+      if (i < total) {
+        const int64_t t = i / vec_per_row;
+        const int c = static_cast<int>(i - t * vec_per_row);
+        for (int s = 0; s < KR; ++s) {
+          const int r = __ldg(row_of + t * KR + s);
+          if (r >= 0) xp[static_cast<int64_t>(r) * vec_per_row + c] = v[u];
         }
       }
     }
@@ -584,10 +590,11 @@ cudaError_t launch_gather(int dtype, const void* x, int T, int d, int KR, const 
                           int num_sms, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
   const int vec = d * (dtype == 0 ? 2 : 4) / 16;
-  int blocks = (T + 7) / 8;
-  const int cap = num_sms * 8;
-  if (blocks > cap) blocks = cap;
-  k_gather<<<blocks, 256, 0, s>>>(static_cast<const uint4*>(x), T, vec, KR, row_of, static_cast<uint4*>(xp));
+  const int64_t total = static_cast<int64_t>(T) * vec;
+  int64_t blocks = (total + 4 * 256 - 1) / (4 * 256);
+  if (blocks > num_sms * 8) blocks = num_sms * 8;
+  k_gather<4><<<static_cast<int>(blocks), 256, 0, s>>>(static_cast<const uint4*>(x), T, vec, KR, row_of,
+                                                      static_cast<uint4*>(xp));
   return cudaGetLastError();
 }
 
@@ -631,56 +638,52 @@ struct Vec8<float> {
   }
 };
 
+// Flattened over (token, 8-element vector) like the gather; fp32 sum of the
+// token's rows in slot order (then slice order), plus the residual if asked.
 template <typename T>
 __global__ void __launch_bounds__(256) k_combine(const T* __restrict__ yp, const T* __restrict__ x, int Tn, int d,
                                                  int KR, const int32_t* __restrict__ row_of, int add_residual,
                                                  T* __restrict__ y) {
-  const int lane = threadIdx.x & 31;
-  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
   const int nvec = d / 8;
-  for (int t = gw; t < Tn; t += nw) {
-    for (int c0 = 0; c0 < nvec; c0 += 32) {   // warp-uniform trip count (shuffles below)
-      const int c = c0 + lane;
-      const bool ok = c < nvec;
-      float acc[8];
-      if (add_residual && ok) {
-        Vec8<T>::load(x + static_cast<int64_t>(t) * d + c * 8, acc);
-      } else {
+  const int64_t total = static_cast<int64_t>(Tn) * nvec;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const int64_t t = i / nvec;
+    const int c = static_cast<int>(i - t * nvec);
+    float acc[8];
+    if (add_residual) {
+      Vec8<T>::load(x + t * d + c * 8, acc);
+    } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
-      }
-      for (int r0 = 0; r0 < KR; r0 += 32) {
-        const int nr = min(32, KR - r0);
-        const int my_row = lane < nr ? row_of[static_cast<int64_t>(t) * KR + r0 + lane] : -1;
-        for (int s = 0; s < nr; ++s) {   // slot order, then slice order (Eq. 5 sum)
-          const int r = __shfl_sync(0xffffffffu, my_row, s);
-          if (ok && r >= 0) {
-            float v[8];
-            Vec8<T>::load(yp + static_cast<int64_t>(r) * d + c * 8, v);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) acc[i] += v[i];
-          }
-        }
-      }
-      if (ok) Vec8<T>::store(y + static_cast<int64_t>(t) * d + c * 8, acc);
+      for (int k = 0; k < 8; ++k) acc[k] = 0.0f;
     }
+    for (int s = 0; s < KR; ++s) {   // slot order, then slice order (Eq. 5 sum)
+      const int r = __ldg(row_of + t * KR + s);
+      if (r >= 0) {
+        float v[8];
+        Vec8<T>::load(yp + static_cast<int64_t>(r) * d + c * 8, v);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] += v[k];
+      }
+    }
+    Vec8<T>::store(y + t * d + c * 8, acc);
   }
 }
 
 cudaError_t launch_combine(int dtype, const void* yp, const void* x, int T, int d, int KR, const int32_t* row_of,
                            int add_residual, void* y, int num_sms, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
-  int blocks = (T + 7) / 8;
-  const int cap = num_sms * 8;
-  if (blocks > cap) blocks = cap;
+  const int64_t total = static_cast<int64_t>(T) * (d / 8);
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > num_sms * 8) blocks = num_sms * 8;
   if (dtype == 0)
-    k_combine<__nv_bfloat16><<<blocks, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(yp),
-                                                    static_cast<const __nv_bfloat16*>(x), T, d, KR, row_of,
-                                                    add_residual, static_cast<__nv_bfloat16*>(y));
+    k_combine<__nv_bfloat16><<<static_cast<int>(blocks), 256, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(yp), static_cast<const __nv_bfloat16*>(x), T, d, KR, row_of, add_residual,
+        static_cast<__nv_bfloat16*>(y));
   else
-    k_combine<float><<<blocks, 256, 0, s>>>(static_cast<const float*>(yp), static_cast<const float*>(x), T, d, KR,
-                                            row_of, add_residual, static_cast<float*>(y));
+    k_combine<float><<<static_cast<int>(blocks), 256, 0, s>>>(static_cast<const float*>(yp),
+                                                              static_cast<const float*>(x), T, d, KR, row_of,
+                                                              add_residual, static_cast<float*>(y));
   return cudaGetLastError();
 }
 

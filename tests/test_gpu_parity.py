@@ -261,3 +261,15 @@ def test_plan_random_counts_bitexact():
         perm = O.permutation(ids, np.ones_like(ids, dtype=float), ref)
         assert np.array_equal(out["expert_row_off"].cpu().numpy(), perm.expert_row_off)
         assert np.array_equal(out["exec_off"].cpu().numpy(), perm.exec_off)
+
+
+@pytest.mark.parametrize("env", [{"BO_GATHER": "1"}, {"BO_GEMM_CG": "1"}], ids=["gather4_gemm1", "single_cta_gemm"])
+@pytest.mark.parametrize("cfg", [SMALL[0], SMALL[2]], ids=lambda c: c.name)
+def test_engine_variants_match_oracle(cfg, env, monkeypatch):
+    """The non-default engine variants stay correct: GEMM1 fed by TMA gather4
+    from x (BO_GATHER=1) and one-CTA tcgen05 tiles instead of CTA pairs."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _, y, dbg, ref = _run_injected(cfg, 0.5, seed=21)
+    _check_routing_and_plan(dbg, ref, cfg.T, cfg.K)
+    assert _rel_err(_np(y), ref.y) <= OUT_TOL
