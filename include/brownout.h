@@ -109,6 +109,8 @@ typedef struct {
   size_t xp;              /* dtype [T*K, d]     gathered rows (concat_tokens)     */
   size_t h;               /* dtype [T*K, f]     SwiGLU activations                      */
   size_t yp;              /* dtype [T*K, d]     weighted executor outputs               */
+  size_t partial;         /* float [8, T*K, d]  split-K partials of GEMM2 (T*K <= 1024 only, else 0 bytes) */
+  size_t ksplit;          /* int32 [1]          split count GEMM2 chose                 */
   int64_t T;              /* tokens the layout was computed for                          */
   int64_t ntiles;         /* histogram tiles the workspace is sized for (8 tokens each)  */
   int64_t num_executors;  /* E = m + G                                                   */

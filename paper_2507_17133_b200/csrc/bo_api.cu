@@ -27,6 +27,8 @@ struct bo_handle {
   int32_t route_tile;
   int32_t cta_pairs;   // 1: prefill FFN GEMMs use cta_group::2 CTA pairs (env BO_GEMM_CG=1 disables)
   int32_t fused_gather;  // 1: GEMM1 gathers x rows by TMA gather4 (env BO_GATHER=1; default off)
+  int32_t splitk;        // 1: GEMM2 split-K for decode-sized steps (env BO_SPLITK=0 disables)
+  int32_t decode_bn1;    // >0: GEMM1 tile width for decode-sized steps (env BO_DECODE_BN1, experiments)
 };
 
 namespace {
@@ -102,6 +104,9 @@ int router_bn(int m) {
   return bn;
 }
 
+constexpr int64_t kSplitRows = 1024;   // GEMM2 split-K (decode) only for R <= this
+constexpr int kSplitMax = 8;
+
 int gemm2_bn(int d) { return d % 256 == 0 ? 256 : d % 128 == 0 ? 128 : 64; }
 int gemm1_bn(int f) { return f % 128 == 0 ? 256 : 128; }   // gate + up columns
 
@@ -136,6 +141,8 @@ bo_status compute_layout(const bo_handle* h, int64_t T, bo_ws_layout* L) {
   L->xp = take(static_cast<size_t>(eb) * R * d);
   L->h = take(static_cast<size_t>(eb) * R * f);
   L->yp = take(static_cast<size_t>(eb) * R * d);
+  L->partial = take(R <= kSplitRows ? sizeof(float) * kSplitMax * R * d : 0);
+  L->ksplit = take(sizeof(int32_t));
   L->total_bytes = off;
   L->T = T;
   L->ntiles = ntiles;
@@ -246,7 +253,10 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
                     const int32_t* mtile_off, int n_orig, int n_united, int f_u, const void* Wg, const void* Wu,
                     const void* Wd, const void* UWg, const void* UWu, const void* UWd, int64_t united_stack,
                     void* Hbuf, void* Y, cudaStream_t s, Prof& prof, int& launches,
-                    const int32_t* gather_tok = nullptr, int64_t gather_T = 0) {
+                    const int32_t* gather_tok = nullptr, int64_t gather_T = 0, float* partial = nullptr,
+                    int* ks_dev = nullptr) {
+  // partial != nullptr: GEMM2 runs split-K into fp32 partials [<=8, R, d] (the
+  // caller combines them with launch_combine_partials); Y is then unused.
   // gather_tok != nullptr: X is the token matrix x [gather_T, d] and GEMM1 gathers
   // row r = x[gather_tok[r]] with TMA tile::gather4 (no packed Xp).
   const bo_config& c = h->cfg;
@@ -260,6 +270,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
   const int tier = 256;
   {
     int bn = tier;                                                  // gate + up columns per tile
+    if (R <= kSplitRows && h->decode_bn1 > 0) bn = h->decode_bn1;   // experiment knob (BO_DECODE_BN1)
     while (bn > 64 && (f % (bn / 2) || f_u % (bn / 2))) bn >>= 1;
     CUtensorMap mA, mG, mU, mUG, mUU;
     const bool gather = gather_tok != nullptr;
@@ -331,6 +342,12 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.mtile_off = mtile_off;
     p.out = Y;
     p.row_w = row_w;
+    p.rows_total = static_cast<int>(R);
+    if (partial) {
+      p.ksplit_max = kSplitMax;
+      p.partial = partial;
+      p.ks_out = ks_dev;
+    }
     const int tile_m = pair ? 2 * bo::kBM : bo::kBM;
     const int64_t max_work = ((R + tile_m - 1) / tile_m + n_exec) * p.n_tiles;
     const int units = pair ? h->num_sms / 2 : h->num_sms;
@@ -399,6 +416,9 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   // GEMM1 gather its A rows from x with TMA tile::gather4 (slower, see above).
   void* yp = at<char>(ws, L.yp);
   const int32_t* row_tok = at<int32_t>(ws, L.row_tok);
+  // decode-sized steps: GEMM2 split-K into fp32 partials (fills the SMs when
+  // few executor tiles exist); BO_SPLITK=0 disables
+  const bool split = h->splitk && R <= kSplitRows && !h->fused_gather;
   if (h->fused_gather) {
     if ((st = ffn_stage(h, x, R, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), m, G, f, Wg, Wu,
                         Wd, UWg, UWu, UWd, have_united ? G : m, at<char>(ws, L.h), yp, s, prof, launches, row_tok,
@@ -410,13 +430,20 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
     BO_CUDA(bo::launch_gather(dt, x, static_cast<int>(T), d, K, row_of, xp, h->num_sms, s), "gather");
     ++launches;
     if ((st = ffn_stage(h, xp, R, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), m, G, f, Wg, Wu,
-                        Wd, UWg, UWu, UWd, have_united ? G : m, at<char>(ws, L.h), yp, s, prof, launches)) != BO_OK)
+                        Wd, UWg, UWu, UWd, have_united ? G : m, at<char>(ws, L.h), yp, s, prof, launches, nullptr, 0,
+                        split ? at<float>(ws, L.partial) : nullptr, split ? at<int>(ws, L.ksplit) : nullptr)) !=
+        BO_OK)
       return st;
   }
-  // a8: combine (Eq. 5 sum over the token's K slots)
+  // a8: combine (Eq. 5 sum over the token's K slots; split-K partials summed first)
   prof.mark(launches);
-  BO_CUDA(bo::launch_combine(dt, yp, x, static_cast<int>(T), d, K, row_of, c.add_residual, y, h->num_sms, s),
-          "combine");
+  if (split)
+    BO_CUDA(bo::launch_combine_partials(dt, at<float>(ws, L.partial), at<int>(ws, L.ksplit), R, x, static_cast<int>(T),
+                                        d, K, row_of, c.add_residual, y, h->num_sms, s),
+            "combine");
+  else
+    BO_CUDA(bo::launch_combine(dt, yp, x, static_cast<int>(T), d, K, row_of, c.add_residual, y, h->num_sms, s),
+            "combine");
   ++launches;
   prof.mark(launches);
   if (prof.err != cudaSuccess) return cuda_fail(prof.err, "profile event record");
@@ -481,6 +508,11 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   // than materialising Xp (r01 profiles): off unless BO_GATHER=1.
   const char* ga = getenv("BO_GATHER");
   h->fused_gather = (ga && ga[0] == '1') ? 1 : 0;
+  const char* sk = getenv("BO_SPLITK");
+  h->splitk = (sk && sk[0] == '0') ? 0 : 1;
+  const char* bn1 = getenv("BO_DECODE_BN1");
+  h->decode_bn1 = bn1 ? atoi(bn1) : 0;
+  if (h->decode_bn1 != 0 && h->decode_bn1 != 64 && h->decode_bn1 != 128 && h->decode_bn1 != 256) h->decode_bn1 = 0;
   *out = h;
   return BO_OK;
 }

@@ -242,7 +242,23 @@ __global__ void __launch_bounds__(192, 1)
   auto start_of = [&](int x) {
     return x <= mo ? nt_o * s_mtile[x] : nt_o * s_mtile[mo] + nt_u * (s_mtile[x] - s_mtile[mo]);
   };
-  const int total_work = start_of(nexec);
+  const int base_work = start_of(nexec);
+  auto kblocks = [&](int x) { return (x < mo ? p.Kdim : p.Kdim_u) / C::BK; };
+  // Split-K (GEMM2, few rows): when the tiles would leave SMs idle, each tile's
+  // reduction is cut into ks contiguous k-block ranges written as fp32 partials
+  // (summed, in split order, by the combine).  ks is a function of the plan only.
+  int ks = 1;
+  if constexpr (EPI == EPI_WEIGHTED) {
+    if (p.ksplit_max > 1 && base_work > 0) {
+      const int want = (2 * n_units + base_work - 1) / base_work;
+      const int kmin = (p.Kdim < p.Kdim_u ? p.Kdim : p.Kdim_u) / C::BK;
+      ks = want < 1 ? 1 : want;
+      if (ks > p.ksplit_max) ks = p.ksplit_max;
+      if (ks > kmin) ks = kmin;
+    }
+    if (p.ksplit_max > 1 && blockIdx.x == 0 && threadIdx.x == 0) *p.ks_out = ks;
+  }
+  const int total_work = base_work * ks;
 
   // work item -> (executor, m-tile inside executor, n-tile); m-tile fastest
   auto decode = [&](int w, int& x, int& mi, int& n) {
@@ -257,7 +273,16 @@ __global__ void __launch_bounds__(192, 1)
     n = local / mt;
     mi = local - n * mt;
   };
-  auto kblocks = [&](int x) { return (x < mo ? p.Kdim : p.Kdim_u) / C::BK; };
+  // work item -> tile + k-block range [kb0, kb1) of split sp
+  auto decode_k = [&](int w, int& x, int& mi, int& n, int& sp, int& kb0, int& kb1) {
+    const int tw = w / ks;
+    sp = w - tw * ks;
+    decode(tw, x, mi, n);
+    const int nkb = kblocks(x);
+    const int per = (nkb + ks - 1) / ks;
+    kb0 = sp * per < nkb ? sp * per : nkb;
+    kb1 = kb0 + per < nkb ? kb0 + per : nkb;
+  };
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -267,14 +292,13 @@ __global__ void __launch_bounds__(192, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int w = unit; w < total_work; w += n_units) {
-        int x, mi, n;
-        decode(w, x, mi, n);
+        int x, mi, n, sp, kb0, kb1;
+        decode_k(w, x, mi, n, sp, kb0, kb1);
         const int arow = s_eoff[x] + mi * TILE_M + static_cast<int>(crank) * kBM;
         const bool orig = x < p.m_orig;
         const CUtensorMap* mb0 = orig ? &tmB0 : &tmB2;
         const CUtensorMap* mb1 = orig ? &tmB1 : &tmB3;
         const int brow = orig ? x * p.b_rows_per_exec : (x - p.m_orig) * p.b_rows_u;
-        const int num_kb = kblocks(x);
         int4 tok = make_int4(0, 0, 0, 0);
         if constexpr (GATHER) {   // this lane gathers rows arow + 4*lane .. +3 (their tokens)
           const int r = arow + 4 * lane;
@@ -283,7 +307,7 @@ __global__ void __launch_bounds__(192, 1)
           tok.z = r + 2 < p.rows_total ? __ldg(p.row_tok + r + 2) : 0;
           tok.w = r + 3 < p.rows_total ? __ldg(p.row_tok + r + 3) : 0;
         }
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           uint8_t* sb = sa + C::A_BYTES;
@@ -327,25 +351,23 @@ __global__ void __launch_bounds__(192, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int w = unit; w < total_work; w += n_units) {
-        int x, mi, n;
-        decode(w, x, mi, n);
-        const int num_kb = kblocks(x);
+        int x, mi, n, sp, kb0, kb1;
+        decode_k(w, x, mi, n, sp, kb0, kb1);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t b_addr = a_addr + C::A_BYTES;
 #pragma unroll
           for (int k = 0; k < C::BK / C::UK; ++k) {
+            const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
             if constexpr (CG == 1)
-              mma_ss<T>(sdesc_k_sw128(a_addr + k * 32), sdesc_k_sw128(b_addr + k * 32), d_tmem, IDESC,
-                        (kb | k) != 0 ? 1u : 0u);
+              mma_ss<T>(sdesc_k_sw128(a_addr + k * 32), sdesc_k_sw128(b_addr + k * 32), d_tmem, IDESC, accum);
             else
-              mma_ss_pair_bf16(sdesc_k_sw128(a_addr + k * 32), sdesc_k_sw128(b_addr + k * 32), d_tmem, IDESC,
-                               (kb | k) != 0 ? 1u : 0u);
+              mma_ss_pair_bf16(sdesc_k_sw128(a_addr + k * 32), sdesc_k_sw128(b_addr + k * 32), d_tmem, IDESC, accum);
           }
           if constexpr (CG == 1) tc_commit(&empty_bar[stage]);
           else tc_commit_pair(&empty_bar[stage]);   // frees the stage in both CTAs
@@ -370,8 +392,8 @@ __global__ void __launch_bounds__(192, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int w = unit; w < total_work; w += n_units) {
-      int x, mi, n;
-      decode(w, x, mi, n);
+      int x, mi, n, sp, kb0, kb1;
+      decode_k(w, x, mi, n, sp, kb0, kb1);
       const int rows_x = s_eoff[x + 1] - s_eoff[x];
       const int r_local = mi * TILE_M + static_cast<int>(crank) * kBM + q * 32 + lane;
       const bool valid = r_local < rows_x;
@@ -402,6 +424,27 @@ __global__ void __launch_bounds__(192, 1)
         }
       } else if constexpr (EPI == EPI_WEIGHTED) {
         const float wr = valid ? p.row_w[grow] : 0.0f;
+        if (p.ksplit_max > 1) {   // split-K: fp32 partial of split sp, row-scaled (Eq. 6)
+          float* outp = p.partial + (static_cast<int64_t>(sp) * p.rows_total + grow) * p.ldo + n * BN;
+#pragma unroll 1
+          for (int c = 0; c < BN; c += 32) {
+            uint32_t a[32];
+            tmem_ld32(t0 + c, a);
+            tmem_ld_wait();
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(a[i]) * wr;
+            if (valid) store_row32<float>(outp + c, v);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (CG == 1 || leader) mbar_arrive(&tempty_bar[acc]);
+            else mbar_arrive_remote(&tempty_bar[acc], 0);
+          }
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+          continue;
+        }
         T* out = reinterpret_cast<T*>(p.out) + n * BN;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {

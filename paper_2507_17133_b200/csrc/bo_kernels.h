@@ -37,8 +37,16 @@ struct GemmParams {
   float* topk_w;         // EPI_ROUTER: [T, K]
   int32_t* tile_cnt;     // EPI_ROUTER: [ceil(T/128), m] histogram per 128-token tile
   const int32_t* row_tok;  // *_GATHER: token of each row (A row r = x[row_tok[r]])
-  int rows_total;          // *_GATHER: R (rows >= R gather token 0, masked at the store)
+  int rows_total;          // *_GATHER: R (rows >= R gather token 0, masked at the store); split-K partial rows
+  int ksplit_max;          // EPI_WEIGHTED: > 1 enables split-K (fp32 partials [ks, R, ldo] into `partial`)
+  float* partial;          // EPI_WEIGHTED split-K output
+  int* ks_out;             // EPI_WEIGHTED split-K: the kernel publishes the split count it chose
 };
+
+// Combine of split-K fp32 partials: y[t] = [x_t] + sum_slots sum_splits P[sp][row].
+cudaError_t launch_combine_partials(int dtype, const float* partial, const int* ks, int64_t R, const void* x, int T,
+                                    int d, int KR, const int32_t* row_of, int add_residual, void* y, int num_sms,
+                                    cudaStream_t s);
 
 // Grouped tcgen05 GEMM: for each executor x and each 128-row tile of its rows,
 // D = A[rows] * B_x^T with an epilogue selected by `epi`.

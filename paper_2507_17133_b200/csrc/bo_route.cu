@@ -687,6 +687,65 @@ cudaError_t launch_combine(int dtype, const void* yp, const void* x, int T, int 
   return cudaGetLastError();
 }
 
+// Split-K combine: rows' fp32 partials (already gate-weighted) summed over the
+// splits in split order, then over the token's slots in slot order.
+template <typename T>
+__global__ void __launch_bounds__(256) k_combine_partials(const float* __restrict__ part,
+                                                          const int* __restrict__ ks_dev, int64_t R,
+                                                          const T* __restrict__ x, int Tn, int d, int KR,
+                                                          const int32_t* __restrict__ row_of, int add_residual,
+                                                          T* __restrict__ y) {
+  const int ks = *ks_dev;
+  const int nvec = d / 8;
+  const int64_t total = static_cast<int64_t>(Tn) * nvec;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const int64_t t = i / nvec;
+    const int c = static_cast<int>(i - t * nvec);
+    float acc[8];
+    if (add_residual) {
+      Vec8<T>::load(x + t * d + c * 8, acc);
+    } else {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] = 0.0f;
+    }
+    for (int s = 0; s < KR; ++s) {
+      const int r = __ldg(row_of + t * KR + s);
+      if (r < 0) continue;
+      float row[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) row[k] = 0.0f;
+      for (int sp = 0; sp < ks; ++sp) {
+        float v[8];
+        Vec8<float>::load(part + (sp * R + r) * d + c * 8, v);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) row[k] += v[k];
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] += row[k];
+    }
+    Vec8<T>::store(y + t * d + c * 8, acc);
+  }
+}
+
+cudaError_t launch_combine_partials(int dtype, const float* partial, const int* ks, int64_t R, const void* x, int T,
+                                    int d, int KR, const int32_t* row_of, int add_residual, void* y, int num_sms,
+                                    cudaStream_t s) {
+  if (T == 0) return cudaSuccess;
+  const int64_t total = static_cast<int64_t>(T) * (d / 8);
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > num_sms * 8) blocks = num_sms * 8;
+  if (dtype == 0)
+    k_combine_partials<__nv_bfloat16><<<static_cast<int>(blocks), 256, 0, s>>>(
+        partial, ks, R, static_cast<const __nv_bfloat16*>(x), T, d, KR, row_of, add_residual,
+        static_cast<__nv_bfloat16*>(y));
+  else
+    k_combine_partials<float><<<static_cast<int>(blocks), 256, 0, s>>>(partial, ks, R, static_cast<const float*>(x),
+                                                                        T, d, KR, row_of, add_residual,
+                                                                        static_cast<float*>(y));
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------ united init
 // Round an fp64 value to bf16, ties to even, directly from the fp64 bits.
 __device__ __forceinline__ uint16_t f64_to_bf16_rne(double v) {
