@@ -27,7 +27,7 @@ struct bo_handle {
   int32_t route_tile;
   int32_t cta_pairs;   // 1: prefill FFN GEMMs use cta_group::2 CTA pairs (env BO_GEMM_CG=1 disables)
   int32_t fused_gather;  // 1: GEMM1 gathers x rows by TMA gather4 (env BO_GATHER=1; default off)
-  int32_t splitk;        // 1: GEMM2 split-K for decode-sized steps (env BO_SPLITK=0 disables)
+  int32_t splitk;        // 1: GEMM2 split-K for decode-sized steps (env BO_SPLITK=1; default off, bf16 only)
   int32_t decode_bn1;    // >0: GEMM1 tile width for decode-sized steps (env BO_DECODE_BN1, experiments)
 };
 
@@ -416,9 +416,9 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   // GEMM1 gather its A rows from x with TMA tile::gather4 (slower, see above).
   void* yp = at<char>(ws, L.yp);
   const int32_t* row_tok = at<int32_t>(ws, L.row_tok);
-  // decode-sized steps: GEMM2 split-K into fp32 partials (fills the SMs when
-  // few executor tiles exist); BO_SPLITK=0 disables
-  const bool split = h->splitk && R <= kSplitRows && !h->fused_gather;
+  // decode-sized steps: optional GEMM2 split-K into fp32 partials (fills the SMs
+  // when few executor tiles exist); BO_SPLITK=1 enables
+  const bool split = h->splitk && R <= kSplitRows && !h->fused_gather && dt == 0;   // bf16 only
   if (h->fused_gather) {
     if ((st = ffn_stage(h, x, R, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), m, G, f, Wg, Wu,
                         Wd, UWg, UWu, UWd, have_united ? G : m, at<char>(ws, L.h), yp, s, prof, launches, row_tok,
@@ -508,8 +508,10 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   // than materialising Xp (r01 profiles): off unless BO_GATHER=1.
   const char* ga = getenv("BO_GATHER");
   h->fused_gather = (ga && ga[0] == '1') ? 1 : 0;
+  // GEMM2 split-K for decode-sized steps: measured mixed (-11 % GEMM2 at ratio 1,
+  // +2 % step at ratios 0 / 0.5, profiles/r01_bench_decode_splitk_*.json): off unless BO_SPLITK=1.
   const char* sk = getenv("BO_SPLITK");
-  h->splitk = (sk && sk[0] == '0') ? 0 : 1;
+  h->splitk = (sk && sk[0] == '1') ? 1 : 0;
   const char* bn1 = getenv("BO_DECODE_BN1");
   h->decode_bn1 = bn1 ? atoi(bn1) : 0;
   if (h->decode_bn1 != 0 && h->decode_bn1 != 64 && h->decode_bn1 != 128 && h->decode_bn1 != 256) h->decode_bn1 = 0;
