@@ -118,13 +118,12 @@ def algorithmic(cfg, T, stats, d, f, m):
             "weight_bytes": w_bytes}
 
 
-KERNELS_7 = ["router_topk", "plan", "permute", "gather", "gemm1_swiglu", "gemm2_weighted", "combine"]
-KERNELS_6 = ["router_topk", "plan", "permute", "gemm1_swiglu", "gemm2_weighted", "combine"]   # gather fused in GEMM1
-KERNELS = KERNELS_7
+KERNELS_6 = ["router_topk", "plan", "permute_gather", "gemm1_swiglu", "gemm2_weighted", "combine"]
+KERNELS_7 = KERNELS_6   # event slots allocated (launch count 6; one spare)
 
 
 def kernel_names(layer):
-    return KERNELS_6 if layer.moe.last_launch_count() == 6 else KERNELS_7
+    return KERNELS_6
 
 
 class Layer:

@@ -398,7 +398,7 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   const int G = (m + c.way - 1) / c.way;
   const int64_t R = T * K;
   int launches = 0;
-  Prof prof(h, s, 7);
+  Prof prof(h, s, 6);
   int tile = 0;
   // a1-a4: router, top-K, histogram, Alg. 1 plan
   if ((st = route_stage(h, x, T, Wr, logits_in, ws, L, s, prof, launches, tile)) != BO_OK) return st;
@@ -408,8 +408,9 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   prof.mark(launches);
   BO_CUDA(bo::launch_permute(at<int32_t>(ws, L.topk_id), at<float>(ws, L.topk_w), static_cast<int>(T), K, m, tile,
                              at<int32_t>(ws, L.tile_base), at<int32_t>(ws, L.expert_row_off), 1, row_of,
-                             at<int32_t>(ws, L.row_tok), row_w, s),
-          "permute");
+                             at<int32_t>(ws, L.row_tok), row_w, s, dt, x,
+                             h->fused_gather ? nullptr : at<char>(ws, L.xp), d),
+          "permute + gather");
   ++launches;
   // a6-a7: grouped SwiGLU FFN over the m original + G united executors.  The
   // gather kernel materialises Xp (concat_tokens); BO_GATHER=1 instead lets
@@ -425,10 +426,7 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
                         T)) != BO_OK)
       return st;
   } else {
-    void* xp = at<char>(ws, L.xp);
-    prof.mark(launches);
-    BO_CUDA(bo::launch_gather(dt, x, static_cast<int>(T), d, K, row_of, xp, h->num_sms, s), "gather");
-    ++launches;
+    void* xp = at<char>(ws, L.xp);   // filled by the permute kernel (fused gather)
     if ((st = ffn_stage(h, xp, R, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), m, G, f, Wg, Wu,
                         Wd, UWg, UWu, UWd, have_united ? G : m, at<char>(ws, L.h), yp, s, prof, launches, nullptr, 0,
                         split ? at<float>(ws, L.partial) : nullptr, split ? at<int>(ws, L.ksplit) : nullptr)) !=
@@ -646,10 +644,8 @@ bo_status bo_dispatch(bo_handle* h, int64_t T, void* workspace, size_t ws_bytes,
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   BO_CUDA(bo::launch_permute(at<int32_t>(workspace, L.topk_id), at<float>(workspace, L.topk_w), static_cast<int>(T),
                              c.top_k, c.num_experts, h->route_tile, at<int32_t>(workspace, L.tile_base), row_base,
-                             nrep, row_of, nullptr, w_out, s),
-          "dispatch permute");
-  BO_CUDA(bo::launch_gather(dt, x, static_cast<int>(T), c.hidden, c.top_k * nrep, row_of, rows_out, h->num_sms, s),
-          "dispatch gather");
+                             nrep, row_of, nullptr, w_out, s, dt, x, rows_out, c.hidden),
+          "dispatch permute + gather");
   return BO_OK;
 }
 

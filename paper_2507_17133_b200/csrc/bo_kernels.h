@@ -71,9 +71,11 @@ cudaError_t launch_plan(const int32_t* tile_cnt, int ntiles, int m, int way, dou
                         int32_t* tile_base, int32_t* counts, int32_t* exec_of_expert, int32_t* expert_row_off,
                         int32_t* exec_off, int32_t* mtile_off, int64_t* stats, cudaStream_t s);
 
+// xp != nullptr: the permute also copies each token's x row to its rows (fused gather).
 cudaError_t launch_permute(const int32_t* topk_id, const float* topk_w, int T, int K, int m, int tile,
                            const int32_t* tile_base, const int32_t* row_base, int nrep, int32_t* row_of,
-                           int32_t* row_tok, float* row_w, cudaStream_t s);
+                           int32_t* row_tok, float* row_w, cudaStream_t s, int dtype = 0, const void* x = nullptr,
+                           void* xp = nullptr, int d = 0);
 
 cudaError_t launch_gather(int dtype, const void* x, int T, int d, int KR, const int32_t* row_of, void* xp,
                           int num_sms, cudaStream_t s);

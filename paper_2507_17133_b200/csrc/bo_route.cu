@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(256) k_router_small(const T* __restrict__ x, c
   extern __shared__ uint4 s_wr[];
   __shared__ int hist[32];
   constexpr int EPV = 16 / sizeof(T);         // elements per 16-byte vector
-  constexpr int BATCH = TPW >= 4 ? 2 : 4;     // 16-byte loads per token in flight per lane
+  constexpr int BATCH = TPW >= 4 ? 2 : (TPW == 2 ? 4 : 16);   // 16-byte loads per token in flight per lane
   const int nvec = d / EPV;
   {
     const uint4* src = reinterpret_cast<const uint4*>(Wr);
@@ -482,7 +482,8 @@ __global__ void __launch_bounds__(256) k_permute(const int32_t* __restrict__ top
                                                  const int32_t* __restrict__ tile_base,
                                                  const int32_t* __restrict__ row_base, int nrep,
                                                  int32_t* __restrict__ row_of, int32_t* __restrict__ row_tok,
-                                                 float* __restrict__ row_w) {
+                                                 float* __restrict__ row_w, const uint4* __restrict__ x,
+                                                 uint4* __restrict__ xp, int vec_per_row) {
   __shared__ int wcnt[8][kMaxExperts];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < 8 * kMaxExperts; i += blockDim.x) (&wcnt[0][0])[i] = 0;
@@ -540,15 +541,37 @@ __global__ void __launch_bounds__(256) k_permute(const int32_t* __restrict__ top
       }
     }
   }
+  // concat_tokens for this tile: copy each token's x row to its rows,
+  // flattened over (token, 16-byte vector); row_of of the tile was written by
+  // this CTA and is visible after the barrier.
+  if (xp) {
+    __syncthreads();
+    const int t0 = blockIdx.x * tile;
+    const int nt = min(tile, T - t0);
+    const int KR = K * nrep;
+    const int total = nt * vec_per_row;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+      const int tt = i / vec_per_row;
+      const int c = i - tt * vec_per_row;
+      const int64_t t = t0 + tt;
+      const uint4 v = __ldg(x + t * vec_per_row + c);
+      for (int s = 0; s < KR; ++s) {
+        const int r = row_of[t * KR + s];
+        if (r >= 0) xp[static_cast<int64_t>(r) * vec_per_row + c] = v;
+      }
+    }
+  }
 }
 
 cudaError_t launch_permute(const int32_t* topk_id, const float* topk_w, int T, int K, int m, int tile,
                            const int32_t* tile_base, const int32_t* row_base, int nrep, int32_t* row_of,
-                           int32_t* row_tok, float* row_w, cudaStream_t s) {
+                           int32_t* row_tok, float* row_w, cudaStream_t s, int dtype, const void* x, void* xp,
+                           int d) {
   const int ntiles = (T + tile - 1) / tile;
   if (ntiles == 0) return cudaSuccess;
+  const int vec = xp ? d * (dtype == 0 ? 2 : 4) / 16 : 0;
   k_permute<<<ntiles, 256, 0, s>>>(topk_id, topk_w, T, K, m, tile, tile_base, row_base, nrep, row_of, row_tok,
-                                   row_w);
+                                   row_w, static_cast<const uint4*>(x), static_cast<uint4*>(xp), vec);
   return cudaGetLastError();
 }
 
