@@ -119,11 +119,12 @@ def algorithmic(cfg, T, stats, d, f, m):
 
 
 KERNELS_6 = ["router_topk", "plan", "permute_gather", "gemm1_swiglu", "gemm2_weighted", "combine"]
-KERNELS_7 = KERNELS_6   # event slots allocated (launch count 6; one spare)
+KERNELS_7 = ["router_topk", "plan", "permute", "gather", "gemm1_swiglu", "gemm2_weighted", "combine"]
 
 
 def kernel_names(layer):
-    return KERNELS_6
+    """Small batches fuse the gather into the permute (6 launches), large ones do not (7)."""
+    return KERNELS_6 if layer.moe.last_launch_count() == 6 else KERNELS_7
 
 
 class Layer:

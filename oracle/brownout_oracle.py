@@ -270,6 +270,67 @@ def permutation(ids: np.ndarray, g: np.ndarray, plan: Plan) -> Permutation:
                        row_exec=row_exec, row_w=row_w)
 
 
+def permutation_dedup(ids: np.ndarray, g: np.ndarray, plan: Plan) -> Permutation:
+    """Row de-duplication variant (reading D10'):
+    when several of a token's K slots are delegated to the SAME united expert
+    (their experts share a group and are all in S2), Eq. 5 adds
+    q_1 FFN_u(x_t) + q_2 FFN_u(x_t) + ... = (q_1 + q_2 + ...) FFN_u(x_t)
+    (Eq. 6): one row with the summed weight (fp64, slot order)
+    gives the same output.  Rows of original executors are unchanged.
+
+    Row order: executor ascending; inside an original executor, token ascending;
+    inside a united executor, token ascending (one row per token).  row_of of the
+    first slot of a merged group points at the row; the other merged slots get -1
+    (as dropped slots do: they have no row of their own).
+    """
+    ids = np.asarray(ids)
+    T, K = ids.shape
+    m, E = plan.m, plan.E
+    exec_of = plan.exec_of_expert
+    # unique (token, executor) pairs in token order, slots in slot order
+    first = {}                        # (t, x) -> first slot
+    wsum = {}
+    for t in range(T):
+        for s in range(K):
+            x = int(exec_of[int(ids[t, s])])
+            if x < 0:
+                continue
+            key = (t, x) if x >= m else (t, x, s)      # originals never merge (distinct experts)
+            if key not in first:
+                first[key] = s
+                wsum[key] = 0.0
+            wsum[key] += g[t, s]
+    rows_of_exec = np.zeros(E, dtype=np.int64)
+    for key in first:
+        rows_of_exec[key[1]] += 1
+    exec_off = np.zeros(E + 1, dtype=np.int64)
+    exec_off[1:] = np.cumsum(rows_of_exec)
+    R = int(exec_off[-1])
+    expert_row_off = np.full(m, -1, dtype=np.int64)
+    for e in range(m):
+        if 0 <= exec_of[e] < m:
+            expert_row_off[e] = exec_off[exec_of[e]]
+    row_of = np.full(T * K, -1, dtype=np.int64)
+    row_tok = np.empty(R, dtype=np.int64)
+    row_slot = np.empty(R, dtype=np.int64)
+    row_exec = np.empty(R, dtype=np.int64)
+    row_w = np.empty(R, dtype=np.float64)
+    nxt = exec_off[:-1].copy()
+    for key in sorted(first, key=lambda k: (k[1], k[0])):   # executor, then token
+        t, x = key[0], key[1]
+        s = first[key]
+        r = int(nxt[x])
+        nxt[x] += 1
+        row_of[t * K + s] = r
+        row_tok[r] = t
+        row_slot[r] = s
+        row_exec[r] = x
+        row_w[r] = wsum[key]
+    return Permutation(exec_off=exec_off, expert_row_off=expert_row_off,
+                       row_of=row_of, row_tok=row_tok, row_slot=row_slot,
+                       row_exec=row_exec, row_w=row_w)
+
+
 # --------------------------------------------------------------------------
 # Expert FFN and Eq. 5
 # --------------------------------------------------------------------------
@@ -311,20 +372,22 @@ class ForwardResult:
     rows_y: np.ndarray = None       # [R, d] weighted executor outputs (sampled forward: None)
 
 
-def route(x, Wr, K, way, ratio, mode=PARTIAL, logits=None):
+def route(x, Wr, K, way, ratio, mode=PARTIAL, logits=None, dedup=False):
     """Eq. 8 -> Eq. 7 -> Alg. 1 -> concat order.  If ``logits`` is given it is
-    used instead of Eq. 8 (parity entry: "given identical fp32 logits", B:5)."""
+    used instead of Eq. 8 (parity entry: "given identical fp32 logits", B:5).
+    dedup=True merges a token's slots delegated to the same united expert
+    (permutation_dedup)."""
     L = router_logits(x, Wr) if logits is None else np.asarray(logits, dtype=np.float64)
     m = L.shape[1]
     ids, g = topk_gate(L, K)
     cnt = expert_counts(ids, m)
     plan = brownout_plan(cnt, ratio, way, mode)
-    perm = permutation(ids, g, plan)
+    perm = permutation_dedup(ids, g, plan) if dedup else permutation(ids, g, plan)
     return L, ids, g, plan, perm
 
 
 def moe_forward(x, Wr, experts, united, K, way, ratio, mode=PARTIAL,
-                logits=None, add_residual=False, tokens=None) -> ForwardResult:
+                logits=None, add_residual=False, tokens=None, dedup=False) -> ForwardResult:
     """Eq. 5 evaluated the way Alg. 1 processes it (lines 16-30).
 
     For each executor, its concatenated rows are run through that executor's
@@ -338,7 +401,7 @@ def moe_forward(x, Wr, experts, united, K, way, ratio, mode=PARTIAL,
     listed token.
     """
     x64 = np.asarray(x, dtype=np.float64)
-    L, ids, g, plan, perm = route(x, Wr, K, way, ratio, mode, logits)
+    L, ids, g, plan, perm = route(x, Wr, K, way, ratio, mode, logits, dedup)
     T, d = x64.shape
     want = np.arange(T) if tokens is None else np.asarray(tokens, dtype=np.int64)
     R = int(perm.exec_off[-1])

@@ -27,7 +27,7 @@ struct bo_handle {
   int32_t route_tile;
   int32_t cta_pairs;   // 1: prefill FFN GEMMs use cta_group::2 CTA pairs (env BO_GEMM_CG=1 disables)
   int32_t fused_gather;  // 1: GEMM1 gathers x rows by TMA gather4 (env BO_GATHER=1; default off)
-  int32_t splitk;        // 1: GEMM2 split-K for decode-sized steps (env BO_SPLITK=1; default off, bf16 only)
+  int32_t splitk;        // 1: GEMM2 split-K for decode-sized steps (env BO_SPLITK=1; default off)
   int32_t decode_bn1;    // >0: GEMM1 tile width for decode-sized steps (env BO_DECODE_BN1, experiments)
 };
 
@@ -398,20 +398,29 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   const int G = (m + c.way - 1) / c.way;
   const int64_t R = T * K;
   int launches = 0;
-  Prof prof(h, s, 6);
+  Prof prof(h, s, 7);
   int tile = 0;
   // a1-a4: router, top-K, histogram, Alg. 1 plan
   if ((st = route_stage(h, x, T, Wr, logits_in, ws, L, s, prof, launches, tile)) != BO_OK) return st;
   // a5: permutation (rows in executor / expert / token order) and gather of Xp
   int32_t* row_of = at<int32_t>(ws, L.row_of);
   float* row_w = at<float>(ws, L.row_w);
+  // Small batches: the permute CTAs also copy the rows (one launch less).  Large
+  // batches: a separate grid-wide gather (the permute has too few CTAs to move
+  // R*d*2 bytes at HBM speed; measured r01).
+  const bool gather_in_permute = !h->fused_gather && R <= kSplitRows * 2;
   prof.mark(launches);
   BO_CUDA(bo::launch_permute(at<int32_t>(ws, L.topk_id), at<float>(ws, L.topk_w), static_cast<int>(T), K, m, tile,
                              at<int32_t>(ws, L.tile_base), at<int32_t>(ws, L.expert_row_off), 1, row_of,
                              at<int32_t>(ws, L.row_tok), row_w, s, dt, x,
-                             h->fused_gather ? nullptr : at<char>(ws, L.xp), d),
-          "permute + gather");
+                             gather_in_permute ? at<char>(ws, L.xp) : nullptr, d),
+          "permute");
   ++launches;
+  if (!h->fused_gather && !gather_in_permute) {
+    prof.mark(launches);
+    BO_CUDA(bo::launch_gather(dt, x, static_cast<int>(T), d, K, row_of, at<char>(ws, L.xp), h->num_sms, s), "gather");
+    ++launches;
+  }
   // a6-a7: grouped SwiGLU FFN over the m original + G united executors.  The
   // gather kernel materialises Xp (concat_tokens); BO_GATHER=1 instead lets
   // GEMM1 gather its A rows from x with TMA tile::gather4 (slower, see above).
@@ -419,14 +428,14 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   const int32_t* row_tok = at<int32_t>(ws, L.row_tok);
   // decode-sized steps: optional GEMM2 split-K into fp32 partials (fills the SMs
   // when few executor tiles exist); BO_SPLITK=1 enables
-  const bool split = h->splitk && R <= kSplitRows && !h->fused_gather && dt == 0;   // bf16 only
+  const bool split = h->splitk && R <= kSplitRows && !h->fused_gather;
   if (h->fused_gather) {
     if ((st = ffn_stage(h, x, R, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), m, G, f, Wg, Wu,
                         Wd, UWg, UWu, UWd, have_united ? G : m, at<char>(ws, L.h), yp, s, prof, launches, row_tok,
                         T)) != BO_OK)
       return st;
   } else {
-    void* xp = at<char>(ws, L.xp);   // filled by the permute kernel (fused gather)
+    void* xp = at<char>(ws, L.xp);   // filled by the permute (small batches) or the gather kernel
     if ((st = ffn_stage(h, xp, R, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), m, G, f, Wg, Wu,
                         Wd, UWg, UWu, UWd, have_united ? G : m, at<char>(ws, L.h), yp, s, prof, launches, nullptr, 0,
                         split ? at<float>(ws, L.partial) : nullptr, split ? at<int>(ws, L.ksplit) : nullptr)) !=

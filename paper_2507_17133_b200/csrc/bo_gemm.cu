@@ -427,13 +427,14 @@ __global__ void __launch_bounds__(192, 1)
         if (p.ksplit_max > 1) {   // split-K: fp32 partial of split sp, row-scaled (Eq. 6)
           float* outp = p.partial + (static_cast<int64_t>(sp) * p.rows_total + grow) * p.ldo + n * BN;
 #pragma unroll 1
+          const float scale = kb1 > kb0 ? wr : 0.0f;   // an empty k-range contributes 0 (stale TMEM)
           for (int c = 0; c < BN; c += 32) {
             uint32_t a[32];
             tmem_ld32(t0 + c, a);
             tmem_ld_wait();
             float v[32];
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(a[i]) * wr;
+            for (int i = 0; i < 32; ++i) v[i] = kb1 > kb0 ? __uint_as_float(a[i]) * scale : 0.0f;
             if (valid) store_row32<float>(outp + c, v);
           }
           tc_fence_before();

@@ -265,7 +265,7 @@ def test_plan_random_counts_bitexact():
 
 @pytest.mark.parametrize("env", [{"BO_GATHER": "1"}, {"BO_GEMM_CG": "1"}, {"BO_SPLITK": "1"}],
                          ids=["gather4_gemm1", "single_cta_gemm", "splitk_gemm2"])
-@pytest.mark.parametrize("cfg", [SMALL[0], SMALL[2]], ids=lambda c: c.name)
+@pytest.mark.parametrize("cfg", [SMALL[0], SMALL[2], SMALL[3]], ids=lambda c: c.name)
 def test_engine_variants_match_oracle(cfg, env, monkeypatch):
     """The non-default engine variants stay correct: GEMM1 fed by TMA gather4
     from x (BO_GATHER=1) and one-CTA tcgen05 tiles instead of CTA pairs."""

@@ -365,3 +365,40 @@ def test_build_united_mean_special_cases():
     # hand example: mean of 1, 2, 4 = 7/3 -> bf16 2.328125 (7/3 = 10.0101010...b)
     Wh = np.array([1.0, 2.0, 4.0]).reshape(3, 1, 1)
     assert O.build_united_mean(Wh, Wh, Wh, 3)[0].item() == 2.328125
+
+
+# --------------------------------------------- f3: united-row de-duplication
+@pytest.mark.parametrize("ratio", [0.0, 0.5, 1.0])
+def test_dedup_forward_equals_plain_forward(ratio):
+    """Merging a token's slots delegated to the same united expert into one
+    row with the summed weight is exact algebra on Eq. 5 (q1 F(x) + q2 F(x) =
+    (q1 + q2) F(x)): the outputs agree to rounding."""
+    cfg, x, Wr, ex, un = _tiny(12, T=60, K=3, way=4, m=8)
+    a = O.moe_forward(x, Wr, ex, un, cfg.K, cfg.way, ratio)
+    b = O.moe_forward(x, Wr, ex, un, cfg.K, cfg.way, ratio, dedup=True)
+    assert np.abs(a.y - b.y).max() <= 1e-12 * np.abs(a.y).max()
+    # rows: originals unchanged, united rows = unique (token, united executor) pairs
+    m = cfg.m
+    uniq = {(t, int(a.plan.exec_of_expert[e])) for t in range(cfg.T) for e in a.ids[t]
+            if a.plan.exec_of_expert[e] >= m}
+    assert int(b.perm.exec_off[-1] - b.perm.exec_off[m]) == len(uniq)
+    assert np.array_equal(a.perm.exec_off[:m + 1], b.perm.exec_off[:m + 1])
+    # weights of a token's united rows sum to its delegated gate mass
+    for t in range(cfg.T):
+        rows = [r for r in b.perm.row_of[t * cfg.K:(t + 1) * cfg.K] if r >= 0]
+        assert np.isclose(sum(b.perm.row_w[r] for r in rows), 1.0)
+
+
+def test_dedup_hand_example():
+    """Token 0 routed to experts 0 and 2 (same group of 4, both delegated at
+    ratio 1) -> one united row carrying g0 + g2."""
+    L = np.array([[3.0, 0.0, 2.0, -1.0, -5.0, -5.0, -5.0, -5.0],
+                  [-5.0, 4.0, -5.0, -5.0, 3.0, -5.0, -5.0, -5.0]])
+    ids, g = O.topk_gate(L, 2)
+    plan = O.brownout_plan(O.expert_counts(ids, 8), 1.0, 4)
+    # group 0 has experts {0, 1, 2} delegated (>= 2 members) -> UE0; group 1 has {4} -> singleton
+    assert plan.exec_of_expert[0] == 8 and plan.exec_of_expert[2] == 8 and plan.exec_of_expert[4] == 4
+    p = O.permutation_dedup(ids, g, plan)
+    r0 = p.row_of[0]
+    assert p.row_of[1] == -1 and p.row_w[r0] == pytest.approx(g[0, 0] + g[0, 1])
+    assert p.exec_off[-1] == 3          # token 0 -> UE0 (merged), token 1 -> UE0 and E4
