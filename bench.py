@@ -122,9 +122,16 @@ KERNELS_6 = ["router_topk", "plan", "permute_gather", "gemm1_swiglu", "gemm2_wei
 KERNELS_7 = ["router_topk", "plan", "permute", "gather", "gemm1_swiglu", "gemm2_weighted", "combine"]
 
 
+KERNELS_9 = ["router_topk", "plan", "dedup_count", "dedup_plan", "dedup_permute", "gather", "gemm1_swiglu",
+             "gemm2_weighted", "combine"]
+N_EVENTS = 10
+
+
 def kernel_names(layer):
-    """Small batches fuse the gather into the permute (6 launches), large ones do not (7)."""
-    return KERNELS_6 if layer.moe.last_launch_count() == 6 else KERNELS_7
+    """Small batches fuse the gather into the permute (6 launches), large ones do not (7);
+    united-row de-duplication adds its count / prefix / permute kernels (9)."""
+    n = layer.moe.last_launch_count()
+    return {6: KERNELS_6, 7: KERNELS_7, 9: KERNELS_9}[n]
 
 
 class Layer:
@@ -172,7 +179,7 @@ def time_steps(layer, steps, warmup, dist_on, per_kernel=True, graph=True):
     names = kernel_names(layer)
     ev_sets = None
     if per_kernel:
-        ev_sets = [[torch.cuda.Event(enable_timing=True) for _ in range(len(KERNELS_7) + 1)] for _ in range(steps)]
+        ev_sets = [[torch.cuda.Event(enable_timing=True) for _ in range(N_EVENTS)] for _ in range(steps)]
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     g = None
@@ -395,15 +402,26 @@ def main():
         except Exception as e:   # pragma: no cover
             out["e2e"] = {"error": str(e)}
     if not args.no_sweep:
+        from paper_2507_17133_b200 import BrownoutMoE
         sweep = {}
+        base_moe = layer.moe
+        dedup_moe = BrownoutMoE(cfg.d, cfg.f, cfg.m, cfg.K, cfg.way, dtype=cfg.dtype, max_tokens=cfg.T, dedup=True)
         for r in S.RATIO_SWEEP:
-            layer.moe.set_brownout(r)
-            layer.step()
-            s_r = layer.stats()
-            ms_r, k_r = time_steps(layer, args.steps, 3, dist_on, graph=not args.no_graph)
-            sweep[str(r)] = {"tokens_per_s": world * cfg.T / (ms_r / args.steps / 1e3), "ms": ms_r / args.steps,
-                             "executors": s_r["executors_accessed"], "gemm1_ms": k_r["gemm1_swiglu"],
-                             "gemm2_ms": k_r["gemm2_weighted"]}
+            entry = {}
+            for tag, moe in (("", base_moe), ("dedup_", dedup_moe)):   # f3: united-row de-duplication
+                layer.moe = moe
+                layer.ws = moe.workspace(cfg.T, "cuda")
+                moe.set_brownout(r)
+                layer.step()
+                s_r = layer.stats()
+                ms_r, k_r = time_steps(layer, args.steps, 3, dist_on, graph=not args.no_graph)
+                entry.update({tag + "tokens_per_s": world * cfg.T / (ms_r / args.steps / 1e3),
+                              tag + "ms": ms_r / args.steps, tag + "executors": s_r["executors_accessed"],
+                              tag + "rows": s_r["rows_original"] + s_r["rows_united"],
+                              tag + "gemm1_ms": k_r["gemm1_swiglu"], tag + "gemm2_ms": k_r["gemm2_weighted"]})
+            sweep[str(r)] = entry
+        layer.moe = base_moe
+        layer.ws = base_moe.workspace(cfg.T, "cuda")
         layer.moe.set_brownout(cfg.ratio)
         out["ratio_sweep"] = sweep
     if not args.no_extra and cfg.name == "mixtral_prefill":
@@ -560,7 +578,7 @@ def run_ep(args, cfg, rank, world, local, pk):
 def salc_demo(layer, S, iters=240, T=256):
     """Algorithm 2 (SALC) closing the loop on this layer in the decode
     regime (Mixtral, T = 256, weight streaming).  The middle third of the run adds
-    co-located interference (a 1 GiB HBM copy on a side stream overlapping every
+    co-located interference (a 256 MiB HBM copy on a side stream overlapping every
     forward, the paper's "interference from other services"); the per-layer
     SLO is 1.15x the undisturbed ratio-0 latency.  SALC (warning 0.8, shrink 0.8,
     increment 0.1) against a static threshold of 1 (zero brownout)."""
@@ -575,7 +593,7 @@ def salc_demo(layer, S, iters=240, T=256):
     ws = moe.workspace(T, "cuda")
     L = layer.lay
     side = torch.cuda.Stream()
-    hog_src = torch.empty(1 << 29, dtype=torch.bfloat16, device="cuda")
+    hog_src = torch.empty(1 << 27, dtype=torch.bfloat16, device="cuda")   # 256 MiB
     hog_dst = torch.empty_like(hog_src)
     main = torch.cuda.current_stream()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -620,7 +638,7 @@ def salc_demo(layer, S, iters=240, T=256):
                      "mean_threshold": float(np.mean(thrs))}
     del hog_src, hog_dst
     return {"slo_us": slo * 1e6, "T": T, "iters": iters, "ratio0_latency_us": lat0 * 1e6,
-            "interference": "1 GiB device copy on a side stream during the middle third", **res}
+            "interference": "256 MiB device copy on a side stream during the middle third", **res}
 
 
 def run_reference(args, cfg, rank, world):

@@ -72,7 +72,8 @@ typedef struct {
   int32_t way;           /* k of the paper: experts per united group, G = ceil(m / way) */
   int32_t dtype;         /* bo_dtype */
   int32_t add_residual;  /* 1: h_t = x_t + ... (Eq. 5 first term); 0: omit x_t (parity, reading D12) */
-  int32_t reserved;
+  int32_t dedup_united;  /* 1: a token's slots delegated to the same united expert share ONE row carrying
+                            the summed weight (Eq. 5-6 algebra; single-GPU forward only) */
   int64_t max_tokens;    /* largest T a forward will be called with */
 } bo_config;
 
@@ -110,6 +111,8 @@ typedef struct {
   size_t h;               /* dtype [T*K, f]     SwiGLU activations                      */
   size_t yp;              /* dtype [T*K, d]     weighted executor outputs               */
   size_t partial;         /* float [8, T*K, d]  split-K partials of GEMM2 (T*K <= 1024 only, else 0 bytes) */
+  size_t tile_xcnt;       /* int32 [ntiles, E]  rows per executor per tile (dedup_united)   */
+  size_t tile_xbase;      /* int32 [ntiles, E]  their exclusive prefix over tiles            */
   size_t ksplit;          /* int32 [1]          split count GEMM2 chose                 */
   int64_t T;              /* tokens the layout was computed for                          */
   int64_t ntiles;         /* histogram tiles the workspace is sized for (8 tokens each)  */

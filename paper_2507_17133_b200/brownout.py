@@ -30,7 +30,7 @@ EXPORTED = (
 
 class bo_config(C.Structure):
     _fields_ = [("hidden", C.c_int32), ("ffn", C.c_int32), ("num_experts", C.c_int32), ("top_k", C.c_int32),
-                ("way", C.c_int32), ("dtype", C.c_int32), ("add_residual", C.c_int32), ("reserved", C.c_int32),
+                ("way", C.c_int32), ("dtype", C.c_int32), ("add_residual", C.c_int32), ("dedup_united", C.c_int32),
                 ("max_tokens", C.c_int64)]
 
 
@@ -46,7 +46,7 @@ class bo_ws_layout(C.Structure):
     _fields_ = [(n, C.c_size_t) for n in ("total_bytes", "logits", "topk_id", "topk_w", "tile_cnt", "tile_base",
                                           "counts", "exec_of_expert", "expert_row_off", "exec_off", "mtile_off",
                                           "stats", "row_of", "row_tok", "row_w", "xp", "h", "yp", "partial",
-                                          "ksplit")] + \
+                                          "tile_xcnt", "tile_xbase", "ksplit")] + \
                [("T", C.c_int64), ("ntiles", C.c_int64), ("num_executors", C.c_int64)]
 
 
@@ -121,10 +121,11 @@ class BrownoutMoE:
     """One MoE layer handle: bo_create / bo_set_brownout / bo_moe_forward."""
 
     def __init__(self, hidden, ffn, num_experts, top_k, way, dtype="bf16", add_residual=False,
-                 max_tokens=16384):
+                 max_tokens=16384, dedup=False):
         self.cfg = bo_config(hidden=hidden, ffn=ffn, num_experts=num_experts, top_k=top_k, way=way,
                              dtype=BO_BF16 if dtype in ("bf16", torch.bfloat16) else BO_FP32,
-                             add_residual=1 if add_residual else 0, reserved=0, max_tokens=max_tokens)
+                             add_residual=1 if add_residual else 0, dedup_united=1 if dedup else 0,
+                             max_tokens=max_tokens)
         h = C.c_void_p()
         _check(_lib.bo_create(C.byref(self.cfg), C.byref(h)))
         self._h = h

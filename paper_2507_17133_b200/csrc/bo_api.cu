@@ -142,6 +142,8 @@ bo_status compute_layout(const bo_handle* h, int64_t T, bo_ws_layout* L) {
   L->h = take(static_cast<size_t>(eb) * R * f);
   L->yp = take(static_cast<size_t>(eb) * R * d);
   L->partial = take(R <= kSplitRows ? sizeof(float) * kSplitMax * R * d : 0);
+  L->tile_xcnt = take(c.dedup_united ? sizeof(int32_t) * ntiles * E : 0);
+  L->tile_xbase = take(c.dedup_united ? sizeof(int32_t) * ntiles * E : 0);
   L->ksplit = take(sizeof(int32_t));
   L->total_bytes = off;
   L->T = T;
@@ -395,10 +397,10 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int dt = c.dtype == BO_BF16 ? 0 : 1;
   const int m = c.num_experts, K = c.top_k, d = c.hidden, f = c.ffn;
-  const int G = (m + c.way - 1) / c.way;
+  const int G = (m + c.way - 1) / c.way, E = m + G;
   const int64_t R = T * K;
   int launches = 0;
-  Prof prof(h, s, 7);
+  Prof prof(h, s, 9);
   int tile = 0;
   // a1-a4: router, top-K, histogram, Alg. 1 plan
   if ((st = route_stage(h, x, T, Wr, logits_in, ws, L, s, prof, launches, tile)) != BO_OK) return st;
@@ -408,7 +410,20 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   // Small batches: the permute CTAs also copy the rows (one launch less).  Large
   // batches: a separate grid-wide gather (the permute has too few CTAs to move
   // R*d*2 bytes at HBM speed; measured r01).
-  const bool gather_in_permute = !h->fused_gather && R <= kSplitRows * 2;
+  const bool gather_in_permute = !h->fused_gather && R <= kSplitRows * 2 && !c.dedup_united;
+  if (c.dedup_united) {
+    // f3: one row per (token, united executor); Alg. 1 above is unchanged
+    for (int stage = 0; stage < 3; ++stage) {
+      prof.mark(launches);
+      BO_CUDA(bo::launch_dedup(stage, at<int32_t>(ws, L.topk_id), at<float>(ws, L.topk_w), static_cast<int>(T), K,
+                               tile, m, E, at<int32_t>(ws, L.exec_of_expert), at<int32_t>(ws, L.tile_xcnt),
+                               at<int32_t>(ws, L.tile_xbase), at<int32_t>(ws, L.exec_off),
+                               at<int32_t>(ws, L.mtile_off), at<int64_t>(ws, L.stats), row_of,
+                               at<int32_t>(ws, L.row_tok), row_w, s),
+              "dedup");
+      ++launches;
+    }
+  } else {
   prof.mark(launches);
   BO_CUDA(bo::launch_permute(at<int32_t>(ws, L.topk_id), at<float>(ws, L.topk_w), static_cast<int>(T), K, m, tile,
                              at<int32_t>(ws, L.tile_base), at<int32_t>(ws, L.expert_row_off), 1, row_of,
@@ -416,6 +431,7 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
                              gather_in_permute ? at<char>(ws, L.xp) : nullptr, d),
           "permute");
   ++launches;
+  }
   if (!h->fused_gather && !gather_in_permute) {
     prof.mark(launches);
     BO_CUDA(bo::launch_gather(dt, x, static_cast<int>(T), d, K, row_of, at<char>(ws, L.xp), h->num_sms, s), "gather");
@@ -642,6 +658,7 @@ bo_status bo_dispatch(bo_handle* h, int64_t T, void* workspace, size_t ws_bytes,
   if (T != h->route_T) return fail(BO_ERR_INVALID_ARG, "bo_dispatch T=%lld differs from the last bo_route (T=%lld)",
                                    static_cast<long long>(T), static_cast<long long>(h->route_T));
   if (nrep < 1 || nrep > 8) return fail(BO_ERR_INVALID_ARG, "nrep %d outside [1, 8]", nrep);
+  if (h->cfg.dedup_united) return fail(BO_ERR_UNSUPPORTED, "dedup_united is single-GPU only");
   if (T == 0) return BO_OK;
   if (!row_base || !x || !rows_out || !w_out || !row_of) return fail(BO_ERR_INVALID_ARG, "null argument");
   bo_ws_layout L;

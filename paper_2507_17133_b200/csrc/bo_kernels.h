@@ -89,6 +89,12 @@ cudaError_t launch_block_copy(const void* src, void* dst, int row_bytes, const f
                               int n_blocks, const int32_t* src_off, const int32_t* dst_start, int64_t total_rows,
                               int num_sms, cudaStream_t s);
 
+// United-row de-duplication, stage 0: count, 1: per-executor prefix, 2: permute.
+cudaError_t launch_dedup(int stage, const int32_t* topk_id, const float* topk_w, int T, int K, int tile, int m, int E,
+                         const int32_t* exec_of, int32_t* tile_xcnt, int32_t* tile_xbase, int32_t* exec_off,
+                         int32_t* mtile_off, int64_t* stats, int32_t* row_of, int32_t* row_tok, float* row_w,
+                         cudaStream_t s);
+
 cudaError_t launch_build_united(int dtype, const void* W, int m, int way, int64_t per_expert, void* U,
                                 cudaStream_t s);
 

@@ -274,3 +274,34 @@ def test_engine_variants_match_oracle(cfg, env, monkeypatch):
     _, y, dbg, ref = _run_injected(cfg, 0.5, seed=21)
     _check_routing_and_plan(dbg, ref, cfg.T, cfg.K)
     assert _rel_err(_np(y), ref.y) <= OUT_TOL
+
+
+@pytest.mark.parametrize("cfg", [SMALL[0], SMALL[1], SMALL[2], SMALL[3], SMALL[5]], ids=lambda c: c.name)
+@pytest.mark.parametrize("ratio", [0.0, 0.5, 1.0])
+def test_dedup_united_rows_match_oracle(cfg, ratio):
+    """f3: a token's slots delegated to the same united expert share one row
+    (summed weight): rows, offsets and permutation bit-exact vs the oracle's
+    permutation_dedup, weights within 1e-6, outputs within 2e-2."""
+    from paper_2507_17133_b200 import BrownoutMoE
+    lay = S.make_layer(cfg)
+    uni = S.make_united_random(cfg)
+    x = S.make_tokens(cfg, batch_index=5)
+    L = S.make_logits(cfg.T, cfg.m, seed=5, sigma=cfg.sigma)
+    moe = BrownoutMoE(cfg.d, cfg.f, cfg.m, cfg.K, cfg.way, dtype=cfg.dtype, max_tokens=cfg.T, dedup=True)
+    moe.set_brownout(ratio)
+    g = {k: v.cuda() for k, v in lay.items()}
+    u = {k: v.cuda() for k, v in uni.items()}
+    y = moe.forward(x.cuda(), g["Wr"], (g["Wg"], g["Wu"], g["Wd"]), (u["UWg"], u["UWu"], u["UWd"]), logits=L.cuda())
+    torch.cuda.synchronize()
+    dbg = moe.debug_arrays(cfg.T)
+    ex, un = _oracle_weights(lay, uni)
+    ref = O.moe_forward(_np(x), None, ex, un, cfg.K, cfg.way, ratio, logits=L.double().numpy(), dedup=True)
+    assert np.array_equal(dbg["exec_of_expert"].cpu().numpy(), ref.plan.exec_of_expert)
+    assert np.array_equal(dbg["exec_off"].cpu().numpy(), ref.perm.exec_off)
+    assert np.array_equal(dbg["row_of"].cpu().numpy(), ref.perm.row_of)
+    R = int(ref.perm.exec_off[-1])
+    assert np.array_equal(dbg["row_tok"][:R].cpu().numpy(), ref.perm.row_tok)
+    assert np.abs(dbg["row_w"][:R].cpu().double().numpy() - ref.perm.row_w).max() <= 1e-6
+    st = dbg["stats"].cpu().numpy()
+    assert st[4] == ref.perm.exec_off[cfg.m] and st[5] == R - ref.perm.exec_off[cfg.m]
+    assert _rel_err(_np(y), ref.y) <= OUT_TOL
