@@ -305,3 +305,57 @@ def test_dedup_united_rows_match_oracle(cfg, ratio):
     st = dbg["stats"].cpu().numpy()
     assert st[4] == ref.perm.exec_off[cfg.m] and st[5] == R - ref.perm.exec_off[cfg.m]
     assert _rel_err(_np(y), ref.y) <= OUT_TOL
+
+
+def _rand_cfgs(n=12, seed=123):
+    """Random shapes over the supported envelope: m up to 256, K up to 16,
+    way from 1 (every group a singleton) to m (one united expert), ragged
+    groups, d / f multiples of 64, both dtypes."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for i in range(n):
+        m = int(rng.choice([2, 5, 8, 16, 60, 128, 256]))
+        K = int(rng.integers(1, min(m, 16) + 1))
+        way = int(rng.choice([1, 2, 3, 4, 8, m]))
+        dt = "fp32" if rng.random() < 0.25 else "bf16"
+        d = int(rng.choice([64, 128, 192, 320]))
+        f = int(rng.choice([128, 192, 256, 384]))
+        T = int(rng.integers(1, 200))
+        out.append(S.LayerConfig(f"rand{i}_m{m}_K{K}_w{way}_{dt}", d=d, f=f, m=m, K=K, way=way, T=T, ratio=0.5,
+                                 dtype=dt, sigma=float(rng.choice([0.0, 0.5, 1.0])), config_id=100 + i))
+    return out
+
+
+@pytest.mark.parametrize("cfg", _rand_cfgs(), ids=lambda c: c.name)
+def test_random_shapes_match_oracle(cfg):
+    ratio = [0.0, 0.3, 0.5, 0.9, 1.0][cfg.config_id % 5]
+    mode = "full" if cfg.config_id % 7 == 0 else "partial"
+    _, y, dbg, ref = _run_injected(cfg, ratio, mode=mode, seed=cfg.config_id)
+    _check_routing_and_plan(dbg, ref, cfg.T, cfg.K)
+    if np.abs(ref.y).max() > 0:
+        assert _rel_err(_np(y), ref.y) <= OUT_TOL
+
+
+@pytest.mark.parametrize("cfg", _rand_cfgs(n=8, seed=7), ids=lambda c: c.name)
+def test_random_shapes_router_and_topk(cfg):
+    """Router (Eq. 8, CUDA-core or tcgen05 path by shape) vs fp64, and its fused
+    top-K: on tokens whose K-th / (K+1)-th fp64 gap is clear, the selected
+    experts equal the oracle's."""
+    lay = S.make_layer(cfg)
+    x = S.make_tokens(cfg, T=cfg.T, batch_index=3)
+    moe = _moe(cfg)
+    moe.set_brownout(0.0)
+    g = {k: v.cuda() for k, v in lay.items()}
+    moe.forward(x.cuda(), g["Wr"], (g["Wg"], g["Wu"], g["Wd"]), None)
+    torch.cuda.synchronize()
+    dbg = moe.debug_arrays(cfg.T)
+    Lg = dbg["logits"].cpu().double().numpy()
+    Lr = O.router_logits(_np(x), _np(lay["Wr"]))
+    tol = (2e-3 if cfg.dtype == "fp32" else 1e-3) * (1.0 + np.abs(Lr))
+    assert (np.abs(Lg - Lr) <= tol).all()
+    ids_ref, _ = O.topk_gate(Lr, cfg.K)
+    Ls = np.sort(Lr, axis=1)[:, ::-1]
+    gap = Ls[:, cfg.K - 1] - (Ls[:, cfg.K] if cfg.K < cfg.m else -np.inf)
+    clear = gap > 4 * 1e-3 * (1 + np.abs(Ls[:, cfg.K - 1]))
+    ids = dbg["topk_id"].cpu().numpy()
+    assert np.array_equal(np.sort(ids[clear], 1), np.sort(ids_ref[clear], 1))
