@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(256) k_router_small(const T* __restrict__ x, c
   extern __shared__ uint4 s_wr[];
   __shared__ int hist[32];
   constexpr int EPV = 16 / sizeof(T);         // elements per 16-byte vector
-  constexpr int BATCH = TPW >= 4 ? 2 : (TPW == 2 ? 4 : 16);   // 16-byte loads per token in flight per lane
+  constexpr int BATCH = TPW >= 4 ? 4 : (TPW == 2 ? 8 : 16);   // 16-byte loads per token in flight per lane
   const int nvec = d / EPV;
   {
     const uint4* src = reinterpret_cast<const uint4*>(Wr);
