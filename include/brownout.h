@@ -74,6 +74,9 @@ typedef struct {
   int32_t add_residual;  /* 1: h_t = x_t + ... (Eq. 5 first term); 0: omit x_t (parity, reading D12) */
   int32_t dedup_united;  /* 1: a token's slots delegated to the same united expert share ONE row carrying
                             the summed weight (Eq. 5-6 algebra; single-GPU forward only) */
+  int32_t num_shared;    /* N_s of Eq. 5: shared experts applied to every token with weight 1, shape
+                            of an original expert; weights via bo_set_shared_experts (single-GPU forward only) */
+  int32_t reserved;
   int64_t max_tokens;    /* largest T a forward will be called with */
 } bo_config;
 
@@ -101,15 +104,15 @@ typedef struct {
   size_t counts;          /* int32 [m]          cnt_i of Alg. 1                          */
   size_t exec_of_expert;  /* int32 [m]          executor of expert (-1 inactive, -2 dropped) */
   size_t expert_row_off;  /* int32 [m]          first row of expert's tokens (-1 if none) */
-  size_t exec_off;        /* int32 [E+1]        first row of each executor              */
-  size_t mtile_off;       /* int32 [E+1]        prefix of ceil(rows/128) per executor    */
+  size_t exec_off;        /* int32 [E+N_s+1]    first row of each executor (shared last) */
+  size_t mtile_off;       /* int32 [E+N_s+1]    prefix of ceil(rows/128) per executor    */
   size_t stats;           /* bo_plan_stats                                              */
-  size_t row_of;          /* int32 [T*K]        row of assignment (t,s), -1 if dropped  */
-  size_t row_tok;         /* int32 [T*K]        token of each row (first R entries)     */
-  size_t row_w;           /* float [T*K]        gate weight carried by each row (Eq. 6) */
-  size_t xp;              /* dtype [T*K, d]     gathered rows (concat_tokens)     */
-  size_t h;               /* dtype [T*K, f]     SwiGLU activations                      */
-  size_t yp;              /* dtype [T*K, d]     weighted executor outputs               */
+  size_t row_of;          /* int32 [T, K + N_s] row of (t, slot); slots K.. are the shared rows; -1: no row */
+  size_t row_tok;         /* int32 [R]          token of each row, R = T*K + N_s*T        */
+  size_t row_w;           /* float [R]          weight carried by each row (Eq. 6 p / q; 1 for shared) */
+  size_t xp;              /* dtype [R, d]       gathered rows (concat_tokens)     */
+  size_t h;               /* dtype [R, f]       SwiGLU activations                      */
+  size_t yp;              /* dtype [R, d]       weighted executor outputs               */
   size_t partial;         /* float [8, T*K, d]  split-K partials of GEMM2 (T*K <= 1024 only, else 0 bytes) */
   size_t tile_xcnt;       /* int32 [ntiles, E]  rows per executor per tile (dedup_united)   */
   size_t tile_xbase;      /* int32 [ntiles, E]  their exclusive prefix over tiles            */
@@ -137,6 +140,12 @@ BO_API bo_status bo_workspace_layout(const bo_handle* h, int64_t T, bo_ws_layout
  * Runs once per layer; not part of the timed forward. */
 BO_API bo_status bo_build_united(bo_handle* h, const void* Wg, const void* Wu, const void* Wd,
                           int32_t init, void* UWg, void* UWu, void* UWd, void* stream);
+
+/* Shared experts of Eq. 5 (second term): SWg, SWu [N_s, f, d], SWd [N_s, d, f]
+ * device pointers (caller-owned) used by every following forward; N_s is fixed
+ * by bo_config.num_shared.  A wider shared FFN (e.g. one of width 4f) is exactly
+ * N_s = 4 experts of width f holding its column slices (SwiGLU is elementwise in f). */
+BO_API bo_status bo_set_shared_experts(bo_handle* h, const void* SWg, const void* SWu, const void* SWd);
 
 /* The brownout knob: ratio = 1 - threshold, in [0, 1].
  * Host state only; snapshotted by the next forward (may change every

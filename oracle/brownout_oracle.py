@@ -387,13 +387,18 @@ def route(x, Wr, K, way, ratio, mode=PARTIAL, logits=None, dedup=False):
 
 
 def moe_forward(x, Wr, experts, united, K, way, ratio, mode=PARTIAL,
-                logits=None, add_residual=False, tokens=None, dedup=False) -> ForwardResult:
+                logits=None, add_residual=False, tokens=None, dedup=False, shared=None) -> ForwardResult:
     """Eq. 5 evaluated the way Alg. 1 processes it (lines 16-30).
 
     For each executor, its concatenated rows are run through that executor's
     FFN (process_tokens); each row's output is scaled by its gate
-    weight (p or q of Eq. 6) and added to the row's token.  N_s = 0 (no shared
-    experts, reading D12).
+    weight (p or q of Eq. 6) and added to the row's token.
+
+    ``shared``: optional (SWg [N_s, f, d], SWu [N_s, f, d], SWd [N_s, d, f]),
+    the N_s shared experts of Eq. 5's second term, sum_{i=1}^{N_s}
+    FFN_i^(s)(x_t): every token, weight 1, untouched by Alg. 1
+    (which only re-routes original experts).  Added after the routed
+    slots (reading D12).  None: N_s = 0.
 
     ``tokens``: optional list of token indices; when given, only those tokens'
     outputs are computed (routing and the plan still use the whole batch, since
@@ -428,6 +433,10 @@ def moe_forward(x, Wr, experts, united, K, way, ratio, mode=PARTIAL,
             r = int(perm.row_of[int(t) * K + s])
             if r >= 0:
                 y[i] += rows_y[r]
+    if shared is not None:               # Eq. 5 second term: sum_i FFN_i^(s)(x_t)
+        SWg, SWu, SWd = (np.asarray(a, dtype=np.float64) for a in shared)
+        for j in range(SWg.shape[0]):
+            y += swiglu_ffn(x64[want], SWg[j], SWu[j], SWd[j])
     return ForwardResult(y=y, logits=L, ids=ids, g=g, plan=plan, perm=perm,
                          rows_y=rows_y if tokens is None else None)
 

@@ -21,7 +21,7 @@ BO_PARTIAL, BO_FULL = 0, 1
 BO_UNITED_MEAN = 0
 
 EXPORTED = (
-    "bo_create", "bo_destroy", "bo_workspace_size", "bo_workspace_layout", "bo_build_united",
+    "bo_create", "bo_destroy", "bo_workspace_size", "bo_workspace_layout", "bo_build_united", "bo_set_shared_experts",
     "bo_set_brownout", "bo_get_brownout", "bo_moe_forward", "bo_moe_forward_ex", "bo_plan_from_counts",
     "bo_route", "bo_plan_counts", "bo_dispatch", "bo_block_copy", "bo_expert_ffn", "bo_combine",
     "bo_set_profile_events", "bo_last_launch_count", "bo_status_string", "bo_last_error", "bo_version",
@@ -31,7 +31,7 @@ EXPORTED = (
 class bo_config(C.Structure):
     _fields_ = [("hidden", C.c_int32), ("ffn", C.c_int32), ("num_experts", C.c_int32), ("top_k", C.c_int32),
                 ("way", C.c_int32), ("dtype", C.c_int32), ("add_residual", C.c_int32), ("dedup_united", C.c_int32),
-                ("max_tokens", C.c_int64)]
+                ("num_shared", C.c_int32), ("reserved", C.c_int32), ("max_tokens", C.c_int64)]
 
 
 class bo_plan_stats(C.Structure):
@@ -69,6 +69,7 @@ def _load():
         "bo_workspace_layout": ([vp, i64, C.POINTER(bo_ws_layout)], C.c_int),
         "bo_build_united": ([vp, vp, vp, vp, i32, vp, vp, vp, vp], C.c_int),
         "bo_set_brownout": ([vp, C.c_double, i32], C.c_int),
+        "bo_set_shared_experts": ([vp, vp, vp, vp], C.c_int),
         "bo_get_brownout": ([vp, C.POINTER(C.c_double), C.POINTER(i32)], C.c_int),
         "bo_moe_forward": ([vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp], C.c_int),
         "bo_moe_forward_ex": ([vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp, vp], C.c_int),
@@ -121,11 +122,11 @@ class BrownoutMoE:
     """One MoE layer handle: bo_create / bo_set_brownout / bo_moe_forward."""
 
     def __init__(self, hidden, ffn, num_experts, top_k, way, dtype="bf16", add_residual=False,
-                 max_tokens=16384, dedup=False):
+                 max_tokens=16384, dedup=False, num_shared=0):
         self.cfg = bo_config(hidden=hidden, ffn=ffn, num_experts=num_experts, top_k=top_k, way=way,
                              dtype=BO_BF16 if dtype in ("bf16", torch.bfloat16) else BO_FP32,
                              add_residual=1 if add_residual else 0, dedup_united=1 if dedup else 0,
-                             max_tokens=max_tokens)
+                             num_shared=num_shared, reserved=0, max_tokens=max_tokens)
         h = C.c_void_p()
         _check(_lib.bo_create(C.byref(self.cfg), C.byref(h)))
         self._h = h
@@ -167,6 +168,11 @@ class BrownoutMoE:
         return self._ws
 
     # -- calls -----------------------------------------------------------
+    def set_shared_experts(self, SWg, SWu, SWd):
+        """Eq. 5 shared experts [N_s, f, d] / [N_s, d, f] (device tensors kept alive here)."""
+        self._shared = (SWg, SWu, SWd)
+        _check(_lib.bo_set_shared_experts(self._h, _ptr(SWg), _ptr(SWu), _ptr(SWd)))
+
     def build_united(self, Wg, Wu, Wd, stream=None):
         m, f, d = Wg.shape
         G = self.G
@@ -177,8 +183,12 @@ class BrownoutMoE:
                                     _ptr(UWd), _stream(stream)))
         return UWg, UWu, UWd
 
-    def forward(self, x, Wr, experts, united, y=None, workspace=None, logits=None, stream=None):
-        """moe_forward(tokens, router, experts, united) -> y [T, d]."""
+    def forward(self, x, Wr, experts, united, y=None, workspace=None, logits=None, stream=None, shared=None):
+        """moe_forward(tokens, router, experts, united) -> y [T, d].
+        shared: optional (SWg, SWu, SWd) for a handle created with num_shared > 0
+        (same as calling set_shared_experts first)."""
+        if shared is not None:
+            self.set_shared_experts(*shared)
         T = x.shape[0]
         Wg, Wu, Wd = experts
         UWg, UWu, UWd = united if united is not None else (None, None, None)
@@ -217,8 +227,9 @@ class BrownoutMoE:
         L = self.workspace_layout(T)
         m, K = self.cfg.num_experts, self.cfg.top_k
         d, f = self.cfg.hidden, self.cfg.ffn
-        E = int(L.num_executors)
-        R = T * K
+        E = int(L.num_executors)            # m + G routed executors + N_s shared
+        Ns = self.cfg.num_shared
+        R = T * K + Ns * T
         eb = 2 if self.cfg.dtype == BO_BF16 else 4
 
         def view(off, n, dt):
@@ -227,15 +238,15 @@ class BrownoutMoE:
 
         out = {
             "logits": view(L.logits, T * m, torch.float32).view(T, m),
-            "topk_id": view(L.topk_id, R, torch.int32).view(T, K),
-            "topk_w": view(L.topk_w, R, torch.float32).view(T, K),
+            "topk_id": view(L.topk_id, T * K, torch.int32).view(T, K),
+            "topk_w": view(L.topk_w, T * K, torch.float32).view(T, K),
             "counts": view(L.counts, m, torch.int32),
             "exec_of_expert": view(L.exec_of_expert, m, torch.int32),
             "expert_row_off": view(L.expert_row_off, m, torch.int32),
             "exec_off": view(L.exec_off, E + 1, torch.int32),
             "mtile_off": view(L.mtile_off, E + 1, torch.int32),
             "stats": view(L.stats, 8, torch.int64),
-            "row_of": view(L.row_of, R, torch.int32),
+            "row_of": view(L.row_of, T * (K + Ns), torch.int32),   # [T, K + N_s]
             "row_tok": view(L.row_tok, R, torch.int32),
             "row_w": view(L.row_w, R, torch.float32),
             "xp": view(L.xp, R * d, self.torch_dtype).view(R, d),

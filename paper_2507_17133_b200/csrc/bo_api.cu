@@ -29,6 +29,9 @@ struct bo_handle {
   int32_t fused_gather;  // 1: GEMM1 gathers x rows by TMA gather4 (env BO_GATHER=1; default off)
   int32_t splitk;        // 1: GEMM2 split-K for decode-sized steps (env BO_SPLITK=1; default off)
   int32_t decode_bn1;    // >0: GEMM1 tile width for decode-sized steps (env BO_DECODE_BN1, experiments)
+  const void* SWg;       // shared experts (Eq. 5 second term): [N_s, f, d], [N_s, f, d], [N_s, d, f]
+  const void* SWu;
+  const void* SWd;
 };
 
 namespace {
@@ -113,9 +116,10 @@ int gemm1_bn(int f) { return f % 128 == 0 ? 256 : 128; }   // gate + up columns
 bo_status compute_layout(const bo_handle* h, int64_t T, bo_ws_layout* L) {
   const bo_config& c = h->cfg;
   const int64_t m = c.num_experts, K = c.top_k, d = c.hidden, f = c.ffn;
-  const int64_t G = (m + c.way - 1) / c.way, E = m + G;
+  const int64_t G = (m + c.way - 1) / c.way, Ns = c.num_shared, E = m + G + Ns;
   const int64_t ntiles = (T + bo::kTileMin - 1) / bo::kTileMin;   // upper bound over every tile size
-  const int64_t R = T * K;
+  const int64_t Rk = T * K;          // routed (token, slot) pairs
+  const int64_t R = Rk + Ns * T;     // expert rows incl. the shared experts' (every token)
   const int eb = elem_bytes(c.dtype);
   memset(L, 0, sizeof(*L));
   size_t off = 0;
@@ -125,8 +129,8 @@ bo_status compute_layout(const bo_handle* h, int64_t T, bo_ws_layout* L) {
     return o;
   };
   L->logits = take(sizeof(float) * T * m);
-  L->topk_id = take(sizeof(int32_t) * R);
-  L->topk_w = take(sizeof(float) * R);
+  L->topk_id = take(sizeof(int32_t) * Rk);
+  L->topk_w = take(sizeof(float) * Rk);
   L->tile_cnt = take(sizeof(int32_t) * ntiles * m);
   L->tile_base = take(sizeof(int32_t) * ntiles * m);
   L->counts = take(sizeof(int32_t) * m);
@@ -142,8 +146,8 @@ bo_status compute_layout(const bo_handle* h, int64_t T, bo_ws_layout* L) {
   L->h = take(static_cast<size_t>(eb) * R * f);
   L->yp = take(static_cast<size_t>(eb) * R * d);
   L->partial = take(R <= kSplitRows ? sizeof(float) * kSplitMax * R * d : 0);
-  L->tile_xcnt = take(c.dedup_united ? sizeof(int32_t) * ntiles * E : 0);
-  L->tile_xbase = take(c.dedup_united ? sizeof(int32_t) * ntiles * E : 0);
+  L->tile_xcnt = take(c.dedup_united ? sizeof(int32_t) * ntiles * (m + G) : 0);
+  L->tile_xbase = take(c.dedup_united ? sizeof(int32_t) * ntiles * (m + G) : 0);
   L->ksplit = take(sizeof(int32_t));
   L->total_bytes = off;
   L->T = T;
@@ -229,7 +233,9 @@ bo_status route_stage(bo_handle* h, const void* x, int64_t T, const void* Wr, co
     const int work = static_cast<int>((T + bo::kBM - 1) / bo::kBM);
     const int grid = work < h->num_sms ? work : h->num_sms;
     prof.mark(launches);
-    BO_CUDA(bo::launch_grouped_gemm(dt, bo::EPI_ROUTER, bn, mA, mB, mB, mB, mB, p, grid, s), "router gemm");
+    bo::BMaps mbs;
+    for (int i = 0; i < 6; ++i) mbs.m[i] = mB;
+    BO_CUDA(bo::launch_grouped_gemm(dt, bo::EPI_ROUTER, bn, mA, mbs, p, grid, s), "router gemm");
     ++launches;
   }
   const int ntiles = static_cast<int>((T + tile - 1) / tile);
@@ -239,7 +245,8 @@ bo_status route_stage(bo_handle* h, const void* x, int64_t T, const void* Wr, co
   BO_CUDA(bo::launch_plan(tile_cnt, ntiles, m, c.way, h->ratio, h->mode, at<int32_t>(ws, L.tile_base),
                           at<int32_t>(ws, L.counts), at<int32_t>(ws, L.exec_of_expert),
                           at<int32_t>(ws, L.expert_row_off), at<int32_t>(ws, L.exec_off),
-                          at<int32_t>(ws, L.mtile_off), at<int64_t>(ws, L.stats), s),
+                          at<int32_t>(ws, L.mtile_off), at<int64_t>(ws, L.stats), s, c.num_shared,
+                          static_cast<int>(T)),
           "plan");
   ++launches;
   h->route_T = T;
@@ -251,9 +258,21 @@ bo_status route_stage(bo_handle* h, const void* x, int64_t T, const void* Wr, co
 // row gate weight.  Executors [0, n_orig) read Wg/Wu/Wd stacks of width f,
 // executors [n_orig, n_orig + n_united) read UWg/UWu/UWd stacks of width f_u
 // (f_u < f: expert-parallel f-slices of united experts).
+// Weights of one executor class: stacked [n, f, d] gate / up and [n, d, f] down.
+struct FfnClass {
+  const void* Wg = nullptr;
+  const void* Wu = nullptr;
+  const void* Wd = nullptr;
+  int n = 0;        // executors of this class in the row layout
+  int f = 0;        // width (united: f-slice under expert parallelism)
+  int64_t stack = 0;  // experts in the weight stacks (>= n; tensor-map extent)
+};
+
+// Steps a6-a7 over rows already grouped by executor: GEMM1 + SwiGLU, GEMM2 x
+// row gate weight.  Executors are laid out originals, united, shared (Eq. 5
+// second term: every token, weight 1); the united class may have its own width.
 bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, const int32_t* exec_off,
-                    const int32_t* mtile_off, int n_orig, int n_united, int f_u, const void* Wg, const void* Wu,
-                    const void* Wd, const void* UWg, const void* UWu, const void* UWd, int64_t united_stack,
+                    const int32_t* mtile_off, const FfnClass& orig, const FfnClass& uni, const FfnClass& shr,
                     void* Hbuf, void* Y, cudaStream_t s, Prof& prof, int& launches,
                     const int32_t* gather_tok = nullptr, int64_t gather_T = 0, float* partial = nullptr,
                     int* ks_dev = nullptr) {
@@ -264,9 +283,20 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
   const bo_config& c = h->cfg;
   const int dt = c.dtype == BO_BF16 ? 0 : 1;
   const int d = c.hidden, f = c.ffn;
-  const int n_exec = n_orig + n_united;
+  const int f_u = uni.n > 0 ? uni.f : f;
+  const int n_exec = orig.n + uni.n + shr.n;
   bo_status st;
   if (R == 0 || n_exec == 0) return BO_OK;
+  // Any present class's pointers stand in for an empty class (its map is never used).
+  const FfnClass& any = orig.n ? orig : (uni.n ? uni : shr);
+  auto ptr = [&](const FfnClass& k, int which) {
+    const FfnClass& q = k.Wg ? k : any;
+    return which == 0 ? q.Wg : (which == 1 ? q.Wu : q.Wd);
+  };
+  auto rows_of = [&](const FfnClass& k, int width) {
+    const FfnClass& q = k.Wg ? k : any;
+    return static_cast<uint64_t>(q.stack > 0 ? q.stack : 1) * width;
+  };
   // Tile width: widest tile everywhere.  (Narrower decode tiles, tried to cut
   // the wave quantisation of few-row steps, measured slower: r01 profiles.)
   const int tier = 256;
@@ -274,19 +304,22 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     int bn = tier;                                                  // gate + up columns per tile
     if (R <= kSplitRows && h->decode_bn1 > 0) bn = h->decode_bn1;   // experiment knob (BO_DECODE_BN1)
     while (bn > 64 && (f % (bn / 2) || f_u % (bn / 2))) bn >>= 1;
-    CUtensorMap mA, mG, mU, mUG, mUU;
+    CUtensorMap mA;
+    bo::BMaps mb;
     const bool gather = gather_tok != nullptr;
     if (gather) {
       if ((st = make_map(&mA, X, c.dtype, gather_T, d, 1)) != BO_OK) return st;   // box {64 cols, 1 row}
     } else {
       if ((st = make_map(&mA, X, c.dtype, R, d, bo::kBM)) != BO_OK) return st;
     }
-    const uint64_t orows = static_cast<uint64_t>(n_orig > 0 ? n_orig : 1) * f;
-    const uint64_t urows = static_cast<uint64_t>(united_stack > 0 ? united_stack : 1) * f_u;
-    if ((st = make_map(&mG, Wg, c.dtype, orows, d, bn / 2)) != BO_OK) return st;
-    if ((st = make_map(&mU, Wu, c.dtype, orows, d, bn / 2)) != BO_OK) return st;
-    if ((st = make_map(&mUG, UWg, c.dtype, urows, d, bn / 2)) != BO_OK) return st;
-    if ((st = make_map(&mUU, UWu, c.dtype, urows, d, bn / 2)) != BO_OK) return st;
+    const FfnClass* cls[3] = {&orig, &uni, &shr};
+    for (int k = 0; k < 3; ++k) {
+      const int width = k == 1 ? f_u : f;
+      if ((st = make_map(&mb.m[2 * k], ptr(*cls[k], 0), c.dtype, rows_of(*cls[k], width), d, bn / 2)) != BO_OK)
+        return st;
+      if ((st = make_map(&mb.m[2 * k + 1], ptr(*cls[k], 1), c.dtype, rows_of(*cls[k], width), d, bn / 2)) != BO_OK)
+        return st;
+    }
     bo::GemmParams p{};
     p.Kdim = d;
     p.n_tiles = f / (bn / 2);
@@ -295,7 +328,8 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.b_rows_u = f_u;
     p.ldo = f;
     p.n_valid = f;
-    p.m_orig = n_orig;
+    p.m_orig = orig.n;
+    p.m_united = uni.n;
     p.b_rows_per_exec = f;
     p.num_exec = n_exec;
     p.single_rows = -1;
@@ -314,7 +348,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     prof.mark(launches);
     const int epi = gather ? (pair ? bo::EPI_SWIGLU_PAIR_GATHER : bo::EPI_SWIGLU_GATHER)
                            : (pair ? bo::EPI_SWIGLU_PAIR : bo::EPI_SWIGLU);
-    BO_CUDA(bo::launch_grouped_gemm(dt, epi, bn, mA, mG, mU, mUG, mUU, p, grid, s), "gemm1");
+    BO_CUDA(bo::launch_grouped_gemm(dt, epi, bn, mA, mb, p, grid, s), "gemm1");
     ++launches;
   }
   {
@@ -322,12 +356,17 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     if (bn > tier) bn = tier;
     const bool pair = h->cta_pairs && dt == 0 && bn == 256 && R >= 2048;   // each CTA of a pair stages BN/2 of B
     const uint32_t box_b = pair ? bn / 2 : bn;
-    CUtensorMap mA, mD, mUD;
+    CUtensorMap mA;
+    bo::BMaps mb;
     if ((st = make_map(&mA, Hbuf, c.dtype, R, f, bo::kBM)) != BO_OK) return st;
-    const uint64_t orows = static_cast<uint64_t>(n_orig > 0 ? n_orig : 1) * d;
-    const uint64_t urows = static_cast<uint64_t>(united_stack > 0 ? united_stack : 1) * d;
-    if ((st = make_map(&mD, Wd, c.dtype, orows, f, box_b)) != BO_OK) return st;
-    if ((st = make_map(&mUD, UWd, c.dtype, urows, f_u, box_b)) != BO_OK) return st;
+    const FfnClass* cls[3] = {&orig, &uni, &shr};
+    for (int k = 0; k < 3; ++k) {
+      const FfnClass& q = cls[k]->Wg ? *cls[k] : any;
+      const int kdim = k == 1 ? f_u : f;
+      const uint64_t rows = static_cast<uint64_t>(q.stack > 0 ? q.stack : 1) * d;
+      if ((st = make_map(&mb.m[2 * k], ptr(*cls[k], 2), c.dtype, rows, kdim, box_b)) != BO_OK) return st;
+      mb.m[2 * k + 1] = mb.m[2 * k];
+    }
     bo::GemmParams p{};
     p.Kdim = f;
     p.n_tiles = d / bn;
@@ -336,7 +375,8 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.b_rows_u = d;
     p.ldo = d;
     p.n_valid = d;
-    p.m_orig = n_orig;
+    p.m_orig = orig.n;
+    p.m_united = uni.n;
     p.b_rows_per_exec = d;
     p.num_exec = n_exec;
     p.single_rows = -1;
@@ -355,8 +395,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     const int units = pair ? h->num_sms / 2 : h->num_sms;
     const int grid = static_cast<int>(max_work < units ? max_work : units) * (pair ? 2 : 1);
     prof.mark(launches);
-    BO_CUDA(bo::launch_grouped_gemm(dt, pair ? bo::EPI_WEIGHTED_PAIR : bo::EPI_WEIGHTED, bn, mA, mD, mD, mUD, mUD,
-                                    p, grid, s),
+    BO_CUDA(bo::launch_grouped_gemm(dt, pair ? bo::EPI_WEIGHTED_PAIR : bo::EPI_WEIGHTED, bn, mA, mb, p, grid, s),
             "gemm2");
     ++launches;
   }
@@ -398,7 +437,12 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   const int dt = c.dtype == BO_BF16 ? 0 : 1;
   const int m = c.num_experts, K = c.top_k, d = c.hidden, f = c.ffn;
   const int G = (m + c.way - 1) / c.way, E = m + G;
+  const int Ns = c.num_shared;
+  const int KR = K + Ns;               // row_of slots per token: K routed, then the N_s shared experts
   const int64_t R = T * K;
+  const int64_t Rt = R + static_cast<int64_t>(Ns) * T;
+  if (Ns > 0 && (!h->SWg || !h->SWu || !h->SWd))
+    return fail(BO_ERR_INVALID_ARG, "num_shared=%d but bo_set_shared_experts was not called", Ns);
   int launches = 0;
   Prof prof(h, s, 9);
   int tile = 0;
@@ -410,7 +454,7 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   // Small batches: the permute CTAs also copy the rows (one launch less).  Large
   // batches: a separate grid-wide gather (the permute has too few CTAs to move
   // R*d*2 bytes at HBM speed; measured r01).
-  const bool gather_in_permute = !h->fused_gather && R <= kSplitRows * 2 && !c.dedup_united;
+  const bool gather_in_permute = !h->fused_gather && Rt <= kSplitRows * 2 && !c.dedup_united;
   if (c.dedup_united) {
     // f3: one row per (token, united executor); Alg. 1 above is unchanged
     for (int stage = 0; stage < 3; ++stage) {
@@ -428,13 +472,14 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   BO_CUDA(bo::launch_permute(at<int32_t>(ws, L.topk_id), at<float>(ws, L.topk_w), static_cast<int>(T), K, m, tile,
                              at<int32_t>(ws, L.tile_base), at<int32_t>(ws, L.expert_row_off), 1, row_of,
                              at<int32_t>(ws, L.row_tok), row_w, s, dt, x,
-                             gather_in_permute ? at<char>(ws, L.xp) : nullptr, d),
+                             gather_in_permute ? at<char>(ws, L.xp) : nullptr, d, Ns,
+                             at<int32_t>(ws, L.exec_off) + E),
           "permute");
   ++launches;
   }
   if (!h->fused_gather && !gather_in_permute) {
     prof.mark(launches);
-    BO_CUDA(bo::launch_gather(dt, x, static_cast<int>(T), d, K, row_of, at<char>(ws, L.xp), h->num_sms, s), "gather");
+    BO_CUDA(bo::launch_gather(dt, x, static_cast<int>(T), d, KR, row_of, at<char>(ws, L.xp), h->num_sms, s), "gather");
     ++launches;
   }
   // a6-a7: grouped SwiGLU FFN over the m original + G united executors.  The
@@ -444,16 +489,19 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   const int32_t* row_tok = at<int32_t>(ws, L.row_tok);
   // decode-sized steps: optional GEMM2 split-K into fp32 partials (fills the SMs
   // when few executor tiles exist); BO_SPLITK=1 enables
-  const bool split = h->splitk && R <= kSplitRows && !h->fused_gather;
+  const bool split = h->splitk && Rt <= kSplitRows && !h->fused_gather;
+  FfnClass orig, uni, shr;
+  orig.Wg = Wg; orig.Wu = Wu; orig.Wd = Wd; orig.n = m; orig.f = f; orig.stack = m;
+  uni.Wg = UWg; uni.Wu = UWu; uni.Wd = UWd; uni.n = G; uni.f = f; uni.stack = have_united ? G : m;
+  if (Ns > 0) { shr.Wg = h->SWg; shr.Wu = h->SWu; shr.Wd = h->SWd; shr.n = Ns; shr.f = f; shr.stack = Ns; }
   if (h->fused_gather) {
-    if ((st = ffn_stage(h, x, R, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), m, G, f, Wg, Wu,
-                        Wd, UWg, UWu, UWd, have_united ? G : m, at<char>(ws, L.h), yp, s, prof, launches, row_tok,
-                        T)) != BO_OK)
+    if ((st = ffn_stage(h, x, Rt, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), orig, uni, shr,
+                        at<char>(ws, L.h), yp, s, prof, launches, row_tok, T)) != BO_OK)
       return st;
   } else {
     void* xp = at<char>(ws, L.xp);   // filled by the permute (small batches) or the gather kernel
-    if ((st = ffn_stage(h, xp, R, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), m, G, f, Wg, Wu,
-                        Wd, UWg, UWu, UWd, have_united ? G : m, at<char>(ws, L.h), yp, s, prof, launches, nullptr, 0,
+    if ((st = ffn_stage(h, xp, Rt, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), orig, uni, shr,
+                        at<char>(ws, L.h), yp, s, prof, launches, nullptr, 0,
                         split ? at<float>(ws, L.partial) : nullptr, split ? at<int>(ws, L.ksplit) : nullptr)) !=
         BO_OK)
       return st;
@@ -461,11 +509,11 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   // a8: combine (Eq. 5 sum over the token's K slots; split-K partials summed first)
   prof.mark(launches);
   if (split)
-    BO_CUDA(bo::launch_combine_partials(dt, at<float>(ws, L.partial), at<int>(ws, L.ksplit), R, x, static_cast<int>(T),
-                                        d, K, row_of, c.add_residual, y, h->num_sms, s),
+    BO_CUDA(bo::launch_combine_partials(dt, at<float>(ws, L.partial), at<int>(ws, L.ksplit), Rt, x,
+                                        static_cast<int>(T), d, KR, row_of, c.add_residual, y, h->num_sms, s),
             "combine");
   else
-    BO_CUDA(bo::launch_combine(dt, yp, x, static_cast<int>(T), d, K, row_of, c.add_residual, y, h->num_sms, s),
+    BO_CUDA(bo::launch_combine(dt, yp, x, static_cast<int>(T), d, KR, row_of, c.add_residual, y, h->num_sms, s),
             "combine");
   ++launches;
   prof.mark(launches);
@@ -509,7 +557,12 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   if (c.hidden <= 0 || c.hidden % mult || c.ffn <= 0 || c.ffn % mult)
     return fail(BO_ERR_SHAPE, "hidden=%d / ffn=%d must be positive multiples of %d", c.hidden, c.ffn, mult);
   if (c.ffn % 64) return fail(BO_ERR_SHAPE, "ffn=%d must be a multiple of 64", c.ffn);
-  if (c.max_tokens < 0 || c.max_tokens * c.top_k > (int64_t(1) << 31) - 1)
+  const int G = (c.num_experts + c.way - 1) / c.way;
+  if (c.num_shared < 0 || c.num_experts + G + c.num_shared > bo::kMaxExec)
+    return fail(BO_ERR_INVALID_ARG, "num_shared=%d: m + G + N_s must be <= %d", c.num_shared, bo::kMaxExec);
+  if (c.num_shared > 0 && c.dedup_united)
+    return fail(BO_ERR_UNSUPPORTED, "dedup_united with shared experts is not built");
+  if (c.max_tokens < 0 || c.max_tokens * (c.top_k + c.num_shared) > (int64_t(1) << 31) - 1)
     return fail(BO_ERR_INVALID_ARG, "max_tokens=%lld out of range", static_cast<long long>(c.max_tokens));
   int dev = 0, sms = 0;
   BO_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
@@ -525,6 +578,7 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   h->prof_n = 0;
   h->route_T = -1;
   h->route_tile = 0;
+  h->SWg = h->SWu = h->SWd = nullptr;
   const char* cg = getenv("BO_GEMM_CG");
   h->cta_pairs = (cg && cg[0] == '1') ? 0 : 1;
   // TMA gather4 (4 rows x 128 B per instruction, 32 per k-block) measured 2.8x slower
@@ -588,6 +642,18 @@ bo_status bo_build_united(bo_handle* h, const void* Wg, const void* Wu, const vo
   BO_CUDA(bo::launch_build_united(dt, Wg, c.num_experts, c.way, per, UWg, s), "build_united Wg");
   BO_CUDA(bo::launch_build_united(dt, Wu, c.num_experts, c.way, per, UWu, s), "build_united Wu");
   BO_CUDA(bo::launch_build_united(dt, Wd, c.num_experts, c.way, per, UWd, s), "build_united Wd");
+  return BO_OK;
+}
+
+bo_status bo_set_shared_experts(bo_handle* h, const void* SWg, const void* SWu, const void* SWd) {
+  if (!h) return fail(BO_ERR_INVALID_ARG, "null handle");
+  if (h->cfg.num_shared == 0) return fail(BO_ERR_INVALID_ARG, "handle was created with num_shared = 0");
+  if (!SWg || !SWu || !SWd) return fail(BO_ERR_INVALID_ARG, "null shared-expert weights");
+  if (!aligned16(SWg) || !aligned16(SWu) || !aligned16(SWd))
+    return fail(BO_ERR_SHAPE, "tensor pointers must be 16-byte aligned");
+  h->SWg = SWg;
+  h->SWu = SWu;
+  h->SWd = SWd;
   return BO_OK;
 }
 
@@ -659,6 +725,7 @@ bo_status bo_dispatch(bo_handle* h, int64_t T, void* workspace, size_t ws_bytes,
                                    static_cast<long long>(T), static_cast<long long>(h->route_T));
   if (nrep < 1 || nrep > 8) return fail(BO_ERR_INVALID_ARG, "nrep %d outside [1, 8]", nrep);
   if (h->cfg.dedup_united) return fail(BO_ERR_UNSUPPORTED, "dedup_united is single-GPU only");
+  if (h->cfg.num_shared) return fail(BO_ERR_UNSUPPORTED, "shared experts are single-GPU only (bo_moe_forward)");
   if (T == 0) return BO_OK;
   if (!row_base || !x || !rows_out || !w_out || !row_of) return fail(BO_ERR_INVALID_ARG, "null argument");
   bo_ws_layout L;
@@ -708,13 +775,13 @@ bo_status bo_expert_ffn(bo_handle* h, const void* rows, int64_t R, const float* 
                         UWg ? UWg : rows, UWu ? UWu : rows, UWd ? UWd : rows};
   for (const void* p : ptrs)
     if (!aligned16(p)) return fail(BO_ERR_SHAPE, "tensor pointers must be 16-byte aligned");
-  if (!Wg) { Wg = UWg; Wu = UWu; Wd = UWd; }
-  if (!UWg) { UWg = Wg; UWu = Wu; UWd = Wd; }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   Prof prof(h, s, 1 << 30);
   int launches = 0;
-  return ffn_stage(h, rows, R, row_w, exec_off, mtile_off, n_orig, n_united, n_united > 0 ? f_united : c.ffn, Wg, Wu,
-                   Wd, UWg, UWu, UWd, n_united > 0 ? n_united : 1, h_buf, out, s, prof, launches);
+  FfnClass orig, uni, shr;
+  if (n_orig > 0) { orig.Wg = Wg; orig.Wu = Wu; orig.Wd = Wd; orig.n = n_orig; orig.f = c.ffn; orig.stack = n_orig; }
+  if (n_united > 0) { uni.Wg = UWg; uni.Wu = UWu; uni.Wd = UWd; uni.n = n_united; uni.f = f_united; uni.stack = n_united; }
+  return ffn_stage(h, rows, R, row_w, exec_off, mtile_off, orig, uni, shr, h_buf, out, s, prof, launches);
 }
 
 bo_status bo_combine(bo_handle* h, int64_t T, const void* rows, const int32_t* row_of, int32_t nrep, const void* x,

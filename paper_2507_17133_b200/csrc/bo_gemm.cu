@@ -137,9 +137,7 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: 
 
 template <typename T, int BN, int EPI, int KMAX, int CG, bool GATHER>
 __global__ void __launch_bounds__(192, 1)
-    k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB0,
-                   const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmB2,
-                   const __grid_constant__ CUtensorMap tmB3, const GemmParams p) {
+    k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ BMaps tmB, const GemmParams p) {
   // CG = 1: one CTA computes a 128 x BN tile with tcgen05.mma.cta_group::1.
   // CG = 2: a CTA pair (cluster of 2) computes a 256 x BN tile with
   //         tcgen05.mma.cta_group::2 issued by the leader: each CTA stages its
@@ -188,10 +186,7 @@ __global__ void __launch_bounds__(192, 1)
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
-    tma_prefetch_desc(&tmB0);
-    tma_prefetch_desc(&tmB1);
-    tma_prefetch_desc(&tmB2);
-    tma_prefetch_desc(&tmB3);
+    for (int i = 0; i < 6; ++i) tma_prefetch_desc(&tmB.m[i]);
   }
   if constexpr (CG == 2) cluster_sync();   // peer barriers initialised before any remote arrive / alloc
   if (warp == 1) {
@@ -235,15 +230,20 @@ __global__ void __launch_bounds__(192, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  // Two executor classes (originals x < m_orig, united x >= m_orig) may differ in
-  // n-tiles, reduction length and B rows (expert-parallel united f-slices).
+  // Executor classes: originals [0, mo), united [mo, mu), shared [mu, nexec).
+  // United experts may differ in n-tiles, reduction length and B rows
+  // (expert-parallel f-slices); shared experts have the originals' shape.
   const int mo = p.m_orig < nexec ? p.m_orig : nexec;
+  const int mu = mo + p.m_united < nexec ? mo + p.m_united : nexec;
   const int nt_o = p.n_tiles, nt_u = p.n_tiles_u;
   auto start_of = [&](int x) {
-    return x <= mo ? nt_o * s_mtile[x] : nt_o * s_mtile[mo] + nt_u * (s_mtile[x] - s_mtile[mo]);
+    const int a = x < mo ? x : mo;                      // min(x, mo)
+    const int b = x < mo ? mo : (x < mu ? x : mu);      // clamp(x, mo, mu)
+    const int c = x < mu ? mu : x;                      // max(x, mu)
+    return nt_o * s_mtile[a] + nt_u * (s_mtile[b] - s_mtile[mo]) + nt_o * (s_mtile[c] - s_mtile[mu]);
   };
   const int base_work = start_of(nexec);
-  auto kblocks = [&](int x) { return (x < mo ? p.Kdim : p.Kdim_u) / C::BK; };
+  auto kblocks = [&](int x) { return (x < mo || x >= mu ? p.Kdim : p.Kdim_u) / C::BK; };
   // Split-K (GEMM2, few rows): when the tiles would leave SMs idle, each tile's
   // reduction is cut into ks contiguous k-block ranges written as fp32 partials
   // (summed, in split order, by the combine).  ks is a function of the plan only.
@@ -295,10 +295,11 @@ __global__ void __launch_bounds__(192, 1)
         int x, mi, n, sp, kb0, kb1;
         decode_k(w, x, mi, n, sp, kb0, kb1);
         const int arow = s_eoff[x] + mi * TILE_M + static_cast<int>(crank) * kBM;
-        const bool orig = x < p.m_orig;
-        const CUtensorMap* mb0 = orig ? &tmB0 : &tmB2;
-        const CUtensorMap* mb1 = orig ? &tmB1 : &tmB3;
-        const int brow = orig ? x * p.b_rows_per_exec : (x - p.m_orig) * p.b_rows_u;
+        const int cls = x < mo ? 0 : (x < mu ? 1 : 2);      // original / united / shared
+        const CUtensorMap* mb0 = &tmB.m[2 * cls];
+        const CUtensorMap* mb1 = &tmB.m[2 * cls + 1];
+        const int brow = cls == 0 ? x * p.b_rows_per_exec
+                                  : (cls == 1 ? (x - mo) * p.b_rows_u : (x - mu) * p.b_rows_per_exec);
         int4 tok = make_int4(0, 0, 0, 0);
         if constexpr (GATHER) {   // this lane gathers rows arow + 4*lane .. +3 (their tokens)
           const int r = arow + 4 * lane;
@@ -539,9 +540,7 @@ __global__ void __launch_bounds__(192, 1)
 }
 
 template <typename T, int BN, int EPI, int KMAX = 0, int CG = 1, bool GATHER = false>
-static cudaError_t launch_t(const CUtensorMap& A, const CUtensorMap& B0, const CUtensorMap& B1,
-                            const CUtensorMap& B2, const CUtensorMap& B3, const GemmParams& p, int grid,
-                            cudaStream_t s) {
+static cudaError_t launch_t(const CUtensorMap& A, const BMaps& B, const GemmParams& p, int grid, cudaStream_t s) {
   using C = GemmCfg<T, BN, CG>;
   static bool attr_set = false;
   auto kern = k_grouped_gemm<T, BN, EPI, KMAX, CG, GATHER>;
@@ -551,7 +550,7 @@ static cudaError_t launch_t(const CUtensorMap& A, const CUtensorMap& B0, const C
     attr_set = true;
   }
   if constexpr (CG == 1) {
-    kern<<<grid, 192, C::SMEM, s>>>(A, B0, B1, B2, B3, p);
+    kern<<<grid, 192, C::SMEM, s>>>(A, B, p);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(grid & ~1));
@@ -565,53 +564,51 @@ static cudaError_t launch_t(const CUtensorMap& A, const CUtensorMap& B0, const C
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, A, B0, B1, B2, B3, p);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, A, B, p);
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }
 
 template <typename T>
-static cudaError_t dispatch(int epi, int bn, const CUtensorMap& A, const CUtensorMap& B0, const CUtensorMap& B1,
-                            const CUtensorMap& B2, const CUtensorMap& B3, const GemmParams& p, int grid,
+static cudaError_t dispatch(int epi, int bn, const CUtensorMap& A, const BMaps& B, const GemmParams& p, int grid,
                             cudaStream_t s) {
   if (epi == EPI_SWIGLU_GATHER) {
-    if (bn == 256) return launch_t<T, 256, EPI_SWIGLU, 0, 1, true>(A, B0, B1, B2, B3, p, grid, s);
-    if (bn == 128) return launch_t<T, 128, EPI_SWIGLU, 0, 1, true>(A, B0, B1, B2, B3, p, grid, s);
+    if (bn == 256) return launch_t<T, 256, EPI_SWIGLU, 0, 1, true>(A, B, p, grid, s);
+    if (bn == 128) return launch_t<T, 128, EPI_SWIGLU, 0, 1, true>(A, B, p, grid, s);
   } else if (epi == EPI_SWIGLU_PAIR_GATHER) {
     if constexpr (sizeof(T) == 2)
-      if (bn == 256) return launch_t<T, 256, EPI_SWIGLU, 0, 2, true>(A, B0, B1, B2, B3, p, grid, s);
+      if (bn == 256) return launch_t<T, 256, EPI_SWIGLU, 0, 2, true>(A, B, p, grid, s);
   } else if (epi == EPI_SWIGLU_PAIR) {
     if constexpr (sizeof(T) == 2)
-      if (bn == 256) return launch_t<T, 256, EPI_SWIGLU, 0, 2>(A, B0, B1, B2, B3, p, grid, s);
+      if (bn == 256) return launch_t<T, 256, EPI_SWIGLU, 0, 2>(A, B, p, grid, s);
   } else if (epi == EPI_WEIGHTED_PAIR) {
     if constexpr (sizeof(T) == 2)
-      if (bn == 256) return launch_t<T, 256, EPI_WEIGHTED, 0, 2>(A, B0, B1, B2, B3, p, grid, s);
+      if (bn == 256) return launch_t<T, 256, EPI_WEIGHTED, 0, 2>(A, B, p, grid, s);
   } else if (epi == EPI_SWIGLU) {
-    if (bn == 256) return launch_t<T, 256, EPI_SWIGLU>(A, B0, B1, B2, B3, p, grid, s);
-    if (bn == 128) return launch_t<T, 128, EPI_SWIGLU>(A, B0, B1, B2, B3, p, grid, s);
-    if (bn == 64) return launch_t<T, 64, EPI_SWIGLU>(A, B0, B1, B2, B3, p, grid, s);
+    if (bn == 256) return launch_t<T, 256, EPI_SWIGLU>(A, B, p, grid, s);
+    if (bn == 128) return launch_t<T, 128, EPI_SWIGLU>(A, B, p, grid, s);
+    if (bn == 64) return launch_t<T, 64, EPI_SWIGLU>(A, B, p, grid, s);
   } else if (epi == EPI_WEIGHTED) {
-    if (bn == 256) return launch_t<T, 256, EPI_WEIGHTED>(A, B0, B1, B2, B3, p, grid, s);
-    if (bn == 128) return launch_t<T, 128, EPI_WEIGHTED>(A, B0, B1, B2, B3, p, grid, s);
-    if (bn == 64) return launch_t<T, 64, EPI_WEIGHTED>(A, B0, B1, B2, B3, p, grid, s);
+    if (bn == 256) return launch_t<T, 256, EPI_WEIGHTED>(A, B, p, grid, s);
+    if (bn == 128) return launch_t<T, 128, EPI_WEIGHTED>(A, B, p, grid, s);
+    if (bn == 64) return launch_t<T, 64, EPI_WEIGHTED>(A, B, p, grid, s);
   } else if (epi == EPI_ROUTER) {
     const bool k8 = p.topk_k <= 8;
 #define BO_R(BNV)                                                                        \
-  if (bn == BNV) return k8 ? launch_t<T, BNV, EPI_ROUTER, 8>(A, B0, B1, B2, B3, p, grid, s) \
-                           : launch_t<T, BNV, EPI_ROUTER, 16>(A, B0, B1, B2, B3, p, grid, s);
+  if (bn == BNV) return k8 ? launch_t<T, BNV, EPI_ROUTER, 8>(A, B, p, grid, s) \
+                           : launch_t<T, BNV, EPI_ROUTER, 16>(A, B, p, grid, s);
     BO_R(256) BO_R(128) BO_R(64) BO_R(32) BO_R(16)
 #undef BO_R
   }
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_grouped_gemm(int dtype, int epi, int bn, const CUtensorMap& A, const CUtensorMap& B0,
-                                const CUtensorMap& B1, const CUtensorMap& B2, const CUtensorMap& B3,
+cudaError_t launch_grouped_gemm(int dtype, int epi, int bn, const CUtensorMap& A, const BMaps& B,
                                 const GemmParams& p, int grid, cudaStream_t s) {
   if (grid <= 0) return cudaSuccess;
-  if (dtype == 0) return dispatch<__nv_bfloat16>(epi, bn, A, B0, B1, B2, B3, p, grid, s);
-  return dispatch<float>(epi, bn, A, B0, B1, B2, B3, p, grid, s);
+  if (dtype == 0) return dispatch<__nv_bfloat16>(epi, bn, A, B, p, grid, s);
+  return dispatch<float>(epi, bn, A, B, p, grid, s);
 }
 
 int gemm_smem_bytes(int dtype, int epi, int bn) {

@@ -24,7 +24,8 @@ struct GemmParams {
   int b_rows_u;          // rows of B per executor >= m_orig in its stacked view
   int ldo;               // leading dimension of the output (elements)
   int n_valid;           // valid output columns (router: m)
-  int m_orig;            // executors < m_orig read B maps 0/1, others maps 2/3
+  int m_orig;            // executors < m_orig read B maps 0/1 (originals)
+  int m_united;          // next m_united executors read maps 2/3 (united); the rest maps 4/5 (shared)
   int b_rows_per_exec;   // rows of B per executor in the stacked [E*rows, K] view
   int num_exec;          // executors (1 for the router)
   int single_rows;       // >= 0: one executor with this many rows (no device schedule)
@@ -51,8 +52,12 @@ cudaError_t launch_combine_partials(int dtype, const float* partial, const int* 
 // Grouped tcgen05 GEMM: for each executor x and each 128-row tile of its rows,
 // D = A[rows] * B_x^T with an epilogue selected by `epi`.
 // dtype: 0 bf16, 1 fp32 (tf32 MMA).  bn: MMA N (SwiGLU: gate+up columns).
-cudaError_t launch_grouped_gemm(int dtype, int epi, int bn, const CUtensorMap& A, const CUtensorMap& B0,
-                                const CUtensorMap& B1, const CUtensorMap& B2, const CUtensorMap& B3,
+// B operand maps by executor class: [0]/[1] originals (gate or the only B / up),
+// [2]/[3] united experts, [4]/[5] shared experts (Eq. 5 second term).
+struct BMaps {
+  CUtensorMap m[6];
+};
+cudaError_t launch_grouped_gemm(int dtype, int epi, int bn, const CUtensorMap& A, const BMaps& B,
                                 const GemmParams& p, int grid, cudaStream_t s);
 int gemm_smem_bytes(int dtype, int epi, int bn);
 
@@ -67,15 +72,17 @@ int router_small_tile(int T, int num_sms);   // 8..32 tokens per CTA
 cudaError_t launch_router_small(int dtype, const void* x, const void* Wr, int T, int d, int m, int K, int tile,
                                 float* logits, int32_t* topk_id, float* topk_w, int32_t* tile_cnt, cudaStream_t s);
 
+// n_shared shared experts (Eq. 5) are appended after the m + G routed executors with shared_rows rows each.
 cudaError_t launch_plan(const int32_t* tile_cnt, int ntiles, int m, int way, double ratio, int mode,
                         int32_t* tile_base, int32_t* counts, int32_t* exec_of_expert, int32_t* expert_row_off,
-                        int32_t* exec_off, int32_t* mtile_off, int64_t* stats, cudaStream_t s);
+                        int32_t* exec_off, int32_t* mtile_off, int64_t* stats, cudaStream_t s, int n_shared = 0,
+                        int shared_rows = 0);
 
 // xp != nullptr: the permute also copies each token's x row to its rows (fused gather).
 cudaError_t launch_permute(const int32_t* topk_id, const float* topk_w, int T, int K, int m, int tile,
                            const int32_t* tile_base, const int32_t* row_base, int nrep, int32_t* row_of,
                            int32_t* row_tok, float* row_w, cudaStream_t s, int dtype = 0, const void* x = nullptr,
-                           void* xp = nullptr, int d = 0);
+                           void* xp = nullptr, int d = 0, int n_shared = 0, const int32_t* shared_off = nullptr);
 
 cudaError_t launch_gather(int dtype, const void* x, int T, int d, int KR, const int32_t* row_of, void* xp,
                           int num_sms, cudaStream_t s);

@@ -319,7 +319,8 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
                                               double ratio, int mode, int32_t* __restrict__ tile_base,
                                               int32_t* __restrict__ counts, int32_t* __restrict__ exec_of_expert,
                                               int32_t* __restrict__ expert_row_off, int32_t* __restrict__ exec_off,
-                                              int32_t* __restrict__ mtile_off, int64_t* __restrict__ stats) {
+                                              int32_t* __restrict__ mtile_off, int64_t* __restrict__ stats,
+                                              int n_shared, int shared_rows) {
   __shared__ __align__(16) int s_tc[kPlanStage];
   __shared__ int s_cnt[kMaxExperts];
   __shared__ int s_sorted[kMaxExperts];
@@ -404,8 +405,10 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
     exec_of_expert[tid] = x_me;
   }
   __syncthreads();
-  // 5. rows per executor, exec_off / mtile_off = exclusive scans over executors
+  // 5. rows per executor, exec_off / mtile_off = exclusive scans over executors;
+  //    the N_s shared experts of Eq. 5 follow the routed executors (all tokens each)
   int rows = 0;
+  if (tid >= E && tid < E + n_shared) rows = shared_rows;
   if (tid < E) {
     if (tid < m) {
       rows = s_exec[tid] == tid ? s_cnt[tid] : 0;
@@ -420,15 +423,17 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
   const long long xoff = block_excl_scan(rows, s_warp, &R_total);
   long long MT_total;
   const long long moff = block_excl_scan((rows + kBM - 1) / kBM, s_warp, &MT_total);
-  if (tid < E) {
+  const int Et = E + n_shared;
+  if (tid < Et) {
     exec_off[tid] = static_cast<int>(xoff);
     mtile_off[tid] = static_cast<int>(moff);
-    s_xoff[tid] = static_cast<int>(xoff);
   }
+  if (tid < E) s_xoff[tid] = static_cast<int>(xoff);
   if (tid == 0) {
-    exec_off[E] = static_cast<int>(R_total);
-    mtile_off[E] = static_cast<int>(MT_total);
+    exec_off[Et] = static_cast<int>(R_total);
+    mtile_off[Et] = static_cast<int>(MT_total);
   }
+  R_total -= static_cast<long long>(n_shared) * shared_rows;   // routed rows only, for the statistics
   __syncthreads();
   // 6. expert_row_off: executor start + earlier members of the same executor (D11)
   if (tid < m) {
@@ -462,9 +467,10 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
 
 cudaError_t launch_plan(const int32_t* tile_cnt, int ntiles, int m, int way, double ratio, int mode,
                         int32_t* tile_base, int32_t* counts, int32_t* exec_of_expert, int32_t* expert_row_off,
-                        int32_t* exec_off, int32_t* mtile_off, int64_t* stats, cudaStream_t s) {
+                        int32_t* exec_off, int32_t* mtile_off, int64_t* stats, cudaStream_t s, int n_shared,
+                        int shared_rows) {
   k_plan<<<1, kMaxExec, 0, s>>>(tile_cnt, ntiles, m, way, ratio, mode, tile_base, counts, exec_of_expert,
-                                expert_row_off, exec_off, mtile_off, stats);
+                                expert_row_off, exec_off, mtile_off, stats, n_shared, shared_rows);
   return cudaGetLastError();
 }
 
@@ -483,7 +489,11 @@ __global__ void __launch_bounds__(256) k_permute(const int32_t* __restrict__ top
                                                  const int32_t* __restrict__ row_base, int nrep,
                                                  int32_t* __restrict__ row_of, int32_t* __restrict__ row_tok,
                                                  float* __restrict__ row_w, const uint4* __restrict__ x,
-                                                 uint4* __restrict__ xp, int vec_per_row) {
+                                                 uint4* __restrict__ xp, int vec_per_row, int n_shared,
+                                                 const int32_t* __restrict__ shared_off) {
+  // row_of is [T, KR] with KR = K*nrep + n_shared: slot s replica rep at
+  // s*nrep + rep, the shared experts' rows (Eq. 5 second term) after them.
+  const int KR = K * nrep + n_shared;
   __shared__ int wcnt[8][kMaxExperts];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < 8 * kMaxExperts; i += blockDim.x) (&wcnt[0][0])[i] = 0;
@@ -528,17 +538,32 @@ __global__ void __launch_bounds__(256) k_permute(const int32_t* __restrict__ top
       const int64_t a = a0 + i;
       const int rank = tile_base[static_cast<int64_t>(blockIdx.x) * m + e] + start + __popc(peers & lt);
       const float w = topk_w[a];
+      const int64_t t = a / K;
+      const int64_t slot0 = t * KR + (a - t * K) * nrep;
       for (int rep = 0; rep < nrep; ++rep) {
         const int base_r = row_base[e * nrep + rep];
         if (base_r >= 0) {
           const int r = base_r + rank;
-          row_of[a * nrep + rep] = r;
-          if (row_tok) row_tok[r] = static_cast<int32_t>(a / K);
+          row_of[slot0 + rep] = r;
+          if (row_tok) row_tok[r] = static_cast<int32_t>(t);
           row_w[r] = w;
         } else {
-          row_of[a * nrep + rep] = -1;
+          row_of[slot0 + rep] = -1;
         }
       }
+    }
+  }
+  // shared-expert rows of this tile: token t -> row shared_off[i] + t, weight 1
+  if (n_shared > 0) {
+    const int t0 = blockIdx.x * tile;
+    const int nt = min(tile, T - t0);
+    for (int i = threadIdx.x; i < nt * n_shared; i += blockDim.x) {
+      const int tt = i / n_shared, j = i - tt * n_shared;
+      const int64_t t = t0 + tt;
+      const int r = shared_off[j] + static_cast<int>(t);
+      row_of[t * KR + K * nrep + j] = r;
+      if (row_tok) row_tok[r] = static_cast<int32_t>(t);
+      row_w[r] = 1.0f;
     }
   }
   // concat_tokens for this tile: copy each token's x row to its rows,
@@ -548,7 +573,6 @@ __global__ void __launch_bounds__(256) k_permute(const int32_t* __restrict__ top
     __syncthreads();
     const int t0 = blockIdx.x * tile;
     const int nt = min(tile, T - t0);
-    const int KR = K * nrep;
     const int total = nt * vec_per_row;
     for (int i = threadIdx.x; i < total; i += blockDim.x) {
       const int tt = i / vec_per_row;
@@ -566,12 +590,13 @@ __global__ void __launch_bounds__(256) k_permute(const int32_t* __restrict__ top
 cudaError_t launch_permute(const int32_t* topk_id, const float* topk_w, int T, int K, int m, int tile,
                            const int32_t* tile_base, const int32_t* row_base, int nrep, int32_t* row_of,
                            int32_t* row_tok, float* row_w, cudaStream_t s, int dtype, const void* x, void* xp,
-                           int d) {
+                           int d, int n_shared, const int32_t* shared_off) {
   const int ntiles = (T + tile - 1) / tile;
   if (ntiles == 0) return cudaSuccess;
   const int vec = xp ? d * (dtype == 0 ? 2 : 4) / 16 : 0;
   k_permute<<<ntiles, 256, 0, s>>>(topk_id, topk_w, T, K, m, tile, tile_base, row_base, nrep, row_of, row_tok,
-                                   row_w, static_cast<const uint4*>(x), static_cast<uint4*>(xp), vec);
+                                   row_w, static_cast<const uint4*>(x), static_cast<uint4*>(xp), vec, n_shared,
+                                   shared_off);
   return cudaGetLastError();
 }
 

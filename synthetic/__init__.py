@@ -40,6 +40,7 @@ class LayerConfig:
     dtype: str        # "bf16" | "fp32"
     sigma: float = 0.5
     config_id: int = 0
+    Ns: int = 0       # shared experts (Eq. 5 second term), each of width f
 
     @property
     def G(self) -> int:
@@ -57,7 +58,15 @@ C4 = LayerConfig("qwen3_30b_a3b_prefill", d=2048, f=768, m=128, K=8, way=4, T=81
                  ratio=0.5, dtype="bf16", sigma=0.5, config_id=4)
 C5 = LayerConfig("mixtral_ep", d=4096, f=14336, m=8, K=2, way=4, T=4096, ratio=0.5,
                  dtype="bf16", sigma=0.5, config_id=5)
-CONFIGS = {c.name: c for c in (C1, C2, C3, C4, C5)}
+# f2 (SURVEY.md §8 "next"): the paper's own model shape, Qwen1.5-MoE-A2.7B:
+# 60 experts top-4, hidden 2048, expert ffn 1408, shared-expert width 5632 =
+# 4 x 1408 (public model config) as N_s = 4 shared experts; the paper's
+# (way, threshold) configs (2, 0), (4, 0.2), (8, 0.4) -> way 4, ratio
+# 1 - 0.2 = 0.8 here (reading D2; way 8 gives the ragged 8th group of 4).
+PAPER_WAY_THRESHOLD = ((2, 0.0), (4, 0.2), (8, 0.4))
+F2 = LayerConfig("qwen15_moe_a27b_prefill", d=2048, f=1408, m=60, K=4, way=4, T=4096, ratio=0.8,
+                 dtype="bf16", sigma=0.5, config_id=6, Ns=4)
+CONFIGS = {c.name: c for c in (C1, C2, C3, C4, C5, F2)}
 RATIO_SWEEP = (0.0, 0.25, 0.5, 1.0)
 
 
@@ -87,6 +96,14 @@ def make_layer(cfg: LayerConfig, device="cpu", seed: int | None = None):
             w[e] = (torch.randn(shape[1:], generator=g, device=device, dtype=torch.float32)
                     * (1.0 / scale) ** 0.5).to(dt)
         out[name] = w
+    if cfg.Ns:   # shared experts: same scales, drawn after the routed ones
+        for name, shape, scale in (("SWg", (cfg.Ns, f, d), d), ("SWu", (cfg.Ns, f, d), d),
+                                   ("SWd", (cfg.Ns, d, f), f)):
+            w = torch.empty(shape, device=device, dtype=dt)
+            for e in range(cfg.Ns):
+                w[e] = (torch.randn(shape[1:], generator=g, device=device, dtype=torch.float32)
+                        * (1.0 / scale) ** 0.5).to(dt)
+            out[name] = w
     return out
 
 

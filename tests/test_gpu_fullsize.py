@@ -1,5 +1,6 @@
 """Full-size parity at BASELINE.json's configs (C2 Mixtral prefill, C3 Mixtral
-decode, C4 Qwen3-30B-A3B prefill) in the launch configuration bench.py times
+decode, C4 Qwen3-30B-A3B prefill; and f2, the paper's Qwen1.5-MoE-A2.7B shape
+with 4 shared experts) in the launch configuration bench.py times
 (same kernels, CTA pairs, fused gather, tile choices), on outputs the oracle
 can compute one token at a time:
 
@@ -31,13 +32,15 @@ def _f32np(t):
 
 
 @pytest.mark.parametrize("name,ratio", [("mixtral_prefill", 0.5), ("mixtral_decode", 1.0),
-                                        ("qwen3_30b_a3b_prefill", 0.5)])
+                                        ("qwen3_30b_a3b_prefill", 0.5), ("qwen15_moe_a27b_prefill", 0.8)])
 def test_fullsize_sampled_parity(name, ratio):
     from paper_2507_17133_b200 import BrownoutMoE
     cfg = S.with_(S.CONFIGS[name], ratio=ratio)
     lay = S.make_layer(cfg, device="cuda")
-    moe = BrownoutMoE(cfg.d, cfg.f, cfg.m, cfg.K, cfg.way, dtype=cfg.dtype, max_tokens=cfg.T)
+    moe = BrownoutMoE(cfg.d, cfg.f, cfg.m, cfg.K, cfg.way, dtype=cfg.dtype, max_tokens=cfg.T, num_shared=cfg.Ns)
     moe.set_brownout(ratio)
+    if cfg.Ns:
+        moe.set_shared_experts(lay["SWg"], lay["SWu"], lay["SWd"])
     U = moe.build_united(lay["Wg"], lay["Wu"], lay["Wd"])
     x = S.make_tokens(cfg, T=cfg.T, device="cuda")
     L = S.make_logits(cfg.T, cfg.m, seed=17, sigma=cfg.sigma)          # CPU draw, same bits on both sides
@@ -53,13 +56,17 @@ def test_fullsize_sampled_parity(name, ratio):
                               want.reshape(-1)[idx])
     toks = np.sort(np.random.default_rng(1).choice(cfg.T, size=N_SAMPLE, replace=False))
     xn = _f32np(x)
-    ref = O.moe_forward(xn, None, ex, un, cfg.K, cfg.way, ratio, logits=L.double().numpy(), tokens=toks)
+    sh = tuple(_f32np(lay[k]) for k in ("SWg", "SWu", "SWd")) if cfg.Ns else None
+    ref = O.moe_forward(xn, None, ex, un, cfg.K, cfg.way, ratio, logits=L.double().numpy(), tokens=toks,
+                        shared=sh)
     # routing, plan and permutation: every token, bit-exact
     assert np.array_equal(dbg["topk_id"].cpu().numpy(), ref.ids)
     assert np.abs(dbg["topk_w"].cpu().double().numpy() - ref.g).max() <= 1e-6
     assert np.array_equal(dbg["exec_of_expert"].cpu().numpy(), ref.plan.exec_of_expert)
-    assert np.array_equal(dbg["exec_off"].cpu().numpy(), ref.perm.exec_off)
-    assert np.array_equal(dbg["row_of"].cpu().numpy(), ref.perm.row_of)
+    E = cfg.m + cfg.G
+    assert np.array_equal(dbg["exec_off"].cpu().numpy()[:E + 1], ref.perm.exec_off)
+    ro = dbg["row_of"].cpu().numpy().reshape(cfg.T, cfg.K + cfg.Ns)
+    assert np.array_equal(ro[:, :cfg.K].reshape(-1), ref.perm.row_of)
     # outputs of the sampled tokens
     yg = y[torch.as_tensor(toks, device="cuda")].double().cpu().numpy()
     den = np.abs(ref.y).max(1, keepdims=True)

@@ -402,3 +402,54 @@ def test_dedup_hand_example():
     r0 = p.row_of[0]
     assert p.row_of[1] == -1 and p.row_w[r0] == pytest.approx(g[0, 0] + g[0, 1])
     assert p.exec_off[-1] == 3          # token 0 -> UE0 (merged), token 1 -> UE0 and E4
+
+
+# ------------------------------------------------------- shared experts (f2)
+def _shared_case(Ns=3, d=16, f=8, T=5, seed=4):
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((T, d))
+    SWg = rng.standard_normal((Ns, f, d)) / 4
+    SWu = rng.standard_normal((Ns, f, d)) / 4
+    SWd = rng.standard_normal((Ns, d, f)) / 3
+    return x, (SWg, SWu, SWd)
+
+
+def test_shared_experts_equal_one_wide_expert_with_gate_one():
+    """Eq. 5 second term: N_s shared SwiGLU experts of width f summed with
+    weight 1 equal ONE expert of width N_s f whose gate / up rows and down
+    columns are the blocks concatenated (the SwiGLU is row-separable in f).
+    The wide expert runs as the only routed expert of a top-1 layer, where Eq. 7's
+    softmax over a single logit gives gate 1; the shared side runs next to a
+    routed expert whose down-projection is zero."""
+    x, (SWg, SWu, SWd) = _shared_case()
+    T, d = x.shape
+    Ns, f, _ = SWg.shape
+    zero = (np.zeros((1, f, d)), np.zeros((1, f, d)), np.zeros((1, d, f)))
+    L = np.zeros((T, 1))
+    got = O.moe_forward(x, None, zero, zero, 1, 1, 0.0, logits=L, shared=(SWg, SWu, SWd)).y
+    wide = (SWg.reshape(1, Ns * f, d), SWu.reshape(1, Ns * f, d),
+            np.concatenate(list(SWd), axis=1)[None])
+    want = O.moe_forward(x, None, wide, wide, 1, 1, 0.0, logits=L).y
+    assert np.allclose(got, want, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("mode", [O.PARTIAL, O.FULL])
+def test_shared_term_is_independent_of_brownout(mode):
+    """Alg. 1 re-routes only original experts: the shared term of
+    Eq. 5 is the same at every ratio / mode, also for tokens whose routed slots
+    were all dropped (full brownout, ratio 1)."""
+    cfg = S.with_(S.C1, T=24)
+    lay = S.make_layer(cfg)
+    ex = tuple(lay[k].double().numpy() for k in ("Wg", "Wu", "Wd"))
+    un = O.build_united_mean(*ex, cfg.way)
+    x = S.make_tokens(cfg).double().numpy()
+    _, sh = _shared_case(Ns=2, d=cfg.d, f=cfg.f, T=cfg.T)
+    L = S.make_logits(cfg.T, cfg.m, seed=3).double().numpy()
+    deltas = []
+    for ratio in (0.0, 0.5, 1.0):
+        a = O.moe_forward(x, None, ex, un, cfg.K, cfg.way, ratio, mode, logits=L, shared=sh).y
+        b = O.moe_forward(x, None, ex, un, cfg.K, cfg.way, ratio, mode, logits=L).y
+        deltas.append(a - b)
+    for dl in deltas[1:]:
+        assert np.allclose(dl, deltas[0], rtol=1e-12, atol=1e-12)
+    assert np.abs(deltas[0]).max() > 0.1
