@@ -106,8 +106,11 @@ class ClockSampler:
 # --------------------------------------------------------------- workload
 def algorithmic(cfg, T, stats, d, f, m):
     """Method's own work: FLOPs = 2 T d m + 6 d f R_kept,
-    bytes = sum over accessed executors of 3 d f * 2 B + x and y (2 T d * 2 B) + Wr."""
-    R = stats["rows_original"] + stats["rows_united"]
+    bytes = sum over accessed executors of 3 d f * 2 B + x and y (2 T d * 2 B) + Wr.
+    Shared experts (Eq. 5, N_s = cfg.Ns) add N_s T rows and N_s always-accessed executors."""
+    Ns = getattr(cfg, "Ns", 0)
+    R = stats["rows_original"] + stats["rows_united"] + Ns * T
+    stats = dict(stats, executors_accessed=stats["executors_accessed"] + Ns)
     flops = 2.0 * T * d * m + 6.0 * d * f * R
     gemm1_flops = 4.0 * d * f * R
     gemm2_flops = 2.0 * d * f * R
@@ -142,8 +145,11 @@ class Layer:
         self.cfg = cfg
         self.T = cfg.T if T is None else T
         self.lay = S.make_layer(cfg, device=device)
-        self.moe = BrownoutMoE(cfg.d, cfg.f, cfg.m, cfg.K, cfg.way, dtype=cfg.dtype, max_tokens=self.T)
+        self.moe = BrownoutMoE(cfg.d, cfg.f, cfg.m, cfg.K, cfg.way, dtype=cfg.dtype, max_tokens=self.T,
+                               num_shared=cfg.Ns)
         L = self.lay
+        if cfg.Ns:
+            self.moe.set_shared_experts(L["SWg"], L["SWu"], L["SWd"])
         self.united = self.moe.build_united(L["Wg"], L["Wu"], L["Wd"])
         self.x = S.make_tokens(cfg, T=self.T, device=device)
         self.y = torch.empty_like(self.x)
@@ -267,11 +273,12 @@ def oracle_sample(layer_host, cfg, ratio, n_tok, seed=0):
     workload: full-batch Eq. 8 / Eq. 7 / Alg. 1, FFN rows of the sampled tokens."""
     import numpy as np
     from oracle import brownout_oracle as O
-    x, Wr, ex, un = layer_host
+    x, Wr, ex, un = layer_host[:4]
+    sh = layer_host[4] if len(layer_host) > 4 else None
     T = x.shape[0]
     toks = np.sort(np.random.default_rng(seed).choice(T, size=min(n_tok, T), replace=False))
     t0 = time.perf_counter()
-    O.moe_forward(x, Wr, ex, un, cfg.K, cfg.way, ratio, tokens=toks)
+    O.moe_forward(x, Wr, ex, un, cfg.K, cfg.way, ratio, tokens=toks, shared=sh)
     return time.perf_counter() - t0, len(toks)
 
 
@@ -281,7 +288,8 @@ def host_copy(layer):
     f32 = lambda t: t.float().cpu().numpy()   # exact widening of bf16
     ex = tuple(f32(L[k]) for k in ("Wg", "Wu", "Wd"))
     un = tuple(f32(u) for u in layer.united)
-    return f32(layer.x), f32(L["Wr"]), ex, un
+    sh = tuple(f32(L[k]) for k in ("SWg", "SWu", "SWd")) if layer.cfg.Ns else None
+    return f32(layer.x), f32(L["Wr"]), ex, un, sh
 
 
 def cpu_threads():
@@ -371,6 +379,7 @@ def main():
         roof = {"kernel": "gemm1_swiglu", "bound": "tensor", "achieved": ach, "peak": pk["bf16_tflops_sustained"],
                 "unit": "TFLOP/s", "frac": ach / pk["bf16_tflops_sustained"],
                 "peak_note": "sustained bf16 (kernel timed inside a long step); " + pk["source"],
+                "frac_of_burst": ach / pk["bf16_tflops"],
                 "algorithmic_per_launch": alg["gemm1_flops"]}
     else:
         ach = alg["gemm1_bytes"] / g1 / 1e9
@@ -386,7 +395,7 @@ def main():
         "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (seeded; random-init Mixtral-shaped weights)",
         "config": {"workload": cfg.name, "T": cfg.T, "d": cfg.d, "f": cfg.f, "m": cfg.m, "K": cfg.K,
-                   "way": cfg.way, "ratio": cfg.ratio, "mode": "partial", "sigma": cfg.sigma,
+                   "way": cfg.way, "ratio": cfg.ratio, "mode": "partial", "sigma": cfg.sigma, "num_shared": cfg.Ns,
                    "parallelism": f"replicas{world}" if world > 1 else "single",
                    "l2": "inputs larger than L2 (expert weights %.2f GB/step)" % (alg["weight_bytes"] / 1e9)},
         "roofline": roof,
@@ -459,6 +468,29 @@ def main():
                                "gemm1_frac_bf16": a2["gemm1_flops"] / (k2["gemm1_swiglu"] / 1e3) / 1e12
                                / pk["bf16_tflops_sustained"]}
             extra[name] = res
+        # f2: the paper's model shape (Qwen1.5-MoE-A2.7B, 60 experts top-4, 4 shared
+        # experts) at its three (way, threshold) configs, ratio = 1 - threshold
+        del lay2
+        torch.cuda.empty_cache()
+        res = {}
+        for way, thr in S.PAPER_WAY_THRESHOLD:
+            c2 = S.with_(S.F2, way=way, ratio=round(1.0 - thr, 6))
+            lay2 = Layer(c2, "cuda")
+            lay2.moe.set_brownout(c2.ratio)
+            lay2.step()
+            s2 = lay2.stats()
+            ms2, k2 = time_steps(lay2, args.steps, 3, dist_on, graph=not args.no_graph)
+            a2 = algorithmic(c2, c2.T, s2, c2.d, c2.f, c2.m)
+            t2 = ms2 / args.steps / 1e3
+            res[f"way{way}_threshold{thr}"] = {
+                "ratio": c2.ratio, "tokens_per_s": world * c2.T / t2, "ms": t2 * 1e3,
+                "executors": s2["executors_accessed"] + c2.Ns, "kernel_ms": k2,
+                "frac_bf16_step": a2["flops"] / t2 / 1e12 / pk["bf16_tflops_sustained"],
+                "gemm1_frac_bf16": a2["gemm1_flops"] / (k2["gemm1_swiglu"] / 1e3) / 1e12
+                / pk["bf16_tflops_sustained"]}
+            del lay2
+            torch.cuda.empty_cache()
+        extra[S.F2.name] = res
         out["other_workloads"] = extra
     if rank == 0 and not args.no_cpu:
         try:
@@ -659,7 +691,8 @@ def run_reference(args, cfg, rank, world):
     ex = tuple(f32(lay[k]) for k in ("Wg", "Wu", "Wd"))
     un = O.build_united_mean(*ex, cfg.way, out_dtype=cfg.dtype)
     x = f32(S.make_tokens(cfg, T=cfg.T))
-    hc = (x, f32(lay["Wr"]), ex, un)
+    sh = tuple(f32(lay[k]) for k in ("SWg", "SWu", "SWd")) if cfg.Ns else None
+    hc = (x, f32(lay["Wr"]), ex, un, sh)
     n_tok = max(1, args.cpu_tokens // 4)
     for _ in range(args.warmup):
         oracle_sample(hc, cfg, cfg.ratio, n_tok)
@@ -674,7 +707,7 @@ def run_reference(args, cfg, rank, world):
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (seeded)",
            "config": {"workload": cfg.name, "T": cfg.T, "d": cfg.d, "f": cfg.f, "m": cfg.m, "K": cfg.K,
-                      "way": cfg.way, "ratio": cfg.ratio},
+                      "way": cfg.way, "ratio": cfg.ratio, "num_shared": cfg.Ns},
            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cpu_threads(), "kind": "oracle",
                             "sample": f"{n_tok} of {cfg.T} tokens per step (full-batch routing + plan)",
                             "cpu": cpu_model()},
