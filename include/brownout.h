@@ -241,6 +241,67 @@ BO_API bo_status bo_expert_ffn(bo_handle* h, const void* rows, int64_t R, const 
 BO_API bo_status bo_combine(bo_handle* h, int64_t T, const void* rows, const int32_t* row_of, int32_t nrep,
                             const void* x, void* y, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * United-expert distillation (paper §4.2, Eq. 4 at P:152; SURVEY
+ * §8(f) row f4).  For every group j (experts [j*way, min((j+1)*way, m)))
+ * the united expert UE_j (student) is trained so that its hidden states match
+ * the group's original experts (teacher) under
+ *     L^j = (1/k) sum_i || H_u^j - H_o^{j*k+i} ||^2                  (Eq. 4)
+ * averaged over the N training tokens (reading D21; k = the group's size),
+ * with plain gradient descent on fp32 master weights (D22).  Every group
+ * trains on the same token matrix X [N, d] (D23).  Operands are bf16
+ * (fp32 accumulation); handles must be BO_BF16.  N must be a positive
+ * multiple of 64 (the weight-gradient GEMMs reduce over tokens in 64-token
+ * blocks).  Shapes and layouts: X [N, d]; originals Wg/Wu [m, f, d], Wd
+ * [m, d, f]; masters UWg_m/UWu_m [G, f, d] and UWd_m [G, d, f] fp32 (caller-
+ * owned, updated in place); bf16 copies UWg/UWu [G, f, d], UWd [G, d, f]
+ * (caller-owned; these are the united experts bo_moe_forward consumes).
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  size_t total_bytes;
+  size_t hbar;     /* f32 [G, N, d]: mean of the group's teacher outputs (the minimiser of Eq. 4) */
+  size_t floor_;   /* f64 [G]: variance floor (1/N)(1/k) sum_t sum_i ||Hbar - H_o^i||^2 */
+  size_t loss;     /* f64 [G]: Eq. 4 of the weights entering the last bo_distill_step */
+  size_t xt;       /* bf16 [d, N]: X^T (weight-gradient operand) */
+  size_t teach_h;  /* bf16 [m, N, f]: teacher SwiGLU activations */
+  size_t teach_y;  /* f32 [m, N, d]: teacher outputs H_o */
+  size_t p, q;     /* bf16 [G, N, f]: student pre-activations X UWg^T, X UWu^T */
+  size_t hs;       /* bf16 [G, N, f]: silu(P) * Q */
+  size_t hst;      /* bf16 [G, f, N] */
+  size_t y;        /* f32 [G, N, d]: student output H_u */
+  size_t dy;       /* bf16 [G, N, d]: dL/dH_u = (2/N)(H_u - Hbar) */
+  size_t dyt;      /* bf16 [G, d, N] */
+  size_t dhs;      /* bf16 [G, N, f] */
+  size_t dpt, dqt; /* bf16 [G, f, N]: dL/dP^T, dL/dQ^T */
+  size_t uwdt;     /* bf16 [G, f, d]: UWd^T (backward operand), refreshed with the bf16 copies */
+  size_t part;     /* f64 partial sums of the reductions */
+  size_t off_tok, off_teach, off_f, off_d; /* int32 executor row offsets of the four GEMM schedules */
+  int64_t N;
+} bo_distill_layout;
+
+BO_API bo_status bo_distill_workspace_layout(const bo_handle* h, int64_t N, bo_distill_layout* out);
+
+/* Once per token set: teacher outputs of all m originals on X (grouped tcgen05
+ * GEMMs), their per-group mean Hbar and variance floor, X^T. */
+BO_API bo_status bo_distill_prepare(bo_handle* h, const void* X, int64_t N, const void* Wg, const void* Wu,
+                                    const void* Wd, void* workspace, size_t ws_bytes, void* stream);
+
+/* Masters <- widen(bf16 united UWg/UWu/UWd) (e.g. the bo_build_united mean
+ * initialisation) and UWd^T into the workspace. */
+BO_API bo_status bo_distill_load_united(bo_handle* h, int64_t N, const void* UWg, const void* UWu, const void* UWd,
+                                        float* UWg_m, float* UWu_m, float* UWd_m, void* workspace, size_t ws_bytes,
+                                        void* stream);
+
+/* One gradient-descent step on every group: student forward, Eq. 4 loss
+ * (written to layout.loss, before the update), backward, W_m -= lr dL/dW_m
+ * (fused into the weight-gradient GEMM epilogue), then the bf16 copies and
+ * UWd^T are refreshed from the masters.  X must be the matrix given to
+ * bo_distill_prepare.  Requires bo_distill_prepare and bo_distill_load_united
+ * (or a previous step) on the same workspace.  No host synchronisation. */
+BO_API bo_status bo_distill_step(bo_handle* h, const void* X, int64_t N, float lr, float* UWg_m, float* UWu_m,
+                                 float* UWd_m, void* UWg, void* UWu, void* UWd, void* workspace, size_t ws_bytes,
+                                 void* stream);
+
 /* Optional per-kernel timing: when `events` (an array of n cudaEvent_t cast
  * to void*) is non-NULL, each following forward records events[i] on its
  * stream immediately before its i-th kernel launch and events[L] after the

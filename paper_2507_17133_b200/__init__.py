@@ -7,7 +7,7 @@ can (re)build the library first; loading it fails loudly if it is missing.
 """
 import importlib
 
-__all__ = ["BrownoutMoE", "BrownoutError", "LIB_PATH", "lib", "STATS_FIELDS"]
+__all__ = ["BrownoutMoE", "BrownoutError", "UnitedDistiller", "LIB_PATH", "lib", "STATS_FIELDS"]
 
 
 def __getattr__(name):

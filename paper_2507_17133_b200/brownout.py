@@ -25,6 +25,7 @@ EXPORTED = (
     "bo_set_brownout", "bo_get_brownout", "bo_moe_forward", "bo_moe_forward_ex", "bo_plan_from_counts",
     "bo_route", "bo_plan_counts", "bo_dispatch", "bo_block_copy", "bo_expert_ffn", "bo_combine",
     "bo_set_profile_events", "bo_last_launch_count", "bo_status_string", "bo_last_error", "bo_version",
+    "bo_distill_workspace_layout", "bo_distill_prepare", "bo_distill_load_united", "bo_distill_step",
 )
 
 
@@ -48,6 +49,12 @@ class bo_ws_layout(C.Structure):
                                           "stats", "row_of", "row_tok", "row_w", "xp", "h", "yp", "partial",
                                           "tile_xcnt", "tile_xbase", "ksplit")] + \
                [("T", C.c_int64), ("ntiles", C.c_int64), ("num_executors", C.c_int64)]
+
+
+class bo_distill_layout(C.Structure):
+    _fields_ = [(n, C.c_size_t) for n in ("total_bytes", "hbar", "floor_", "loss", "xt", "teach_h", "teach_y", "p",
+                                          "q", "hs", "hst", "y", "dy", "dyt", "dhs", "dpt", "dqt", "uwdt", "part",
+                                          "off_tok", "off_teach", "off_f", "off_d")] + [("N", C.c_int64)]
 
 
 class BrownoutError(RuntimeError):
@@ -81,6 +88,10 @@ def _load():
         "bo_expert_ffn": ([vp, vp, i64, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
         "bo_combine": ([vp, i64, vp, vp, i32, vp, vp, vp], C.c_int),
         "bo_set_profile_events": ([vp, C.POINTER(vp), i32], C.c_int),
+        "bo_distill_workspace_layout": ([vp, i64, C.POINTER(bo_distill_layout)], C.c_int),
+        "bo_distill_prepare": ([vp, vp, i64, vp, vp, vp, vp, C.c_size_t, vp], C.c_int),
+        "bo_distill_load_united": ([vp, i64, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp], C.c_int),
+        "bo_distill_step": ([vp, vp, i64, C.c_float, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp], C.c_int),
         "bo_last_launch_count": ([vp], i32),
         "bo_status_string": ([C.c_int], C.c_char_p),
         "bo_last_error": ([], C.c_char_p),
@@ -315,3 +326,59 @@ class BrownoutMoE:
         _check(_lib.bo_plan_from_counts(self._h, _ptr(counts), _ptr(exec_of), _ptr(erow), _ptr(eoff), _ptr(stats),
                                         _stream(stream)))
         return {"exec_of_expert": exec_of, "expert_row_off": erow, "exec_off": eoff[:self.E + 1], "stats": stats}
+
+
+class UnitedDistiller:
+    """United-expert distillation (paper §4.2, Eq. 4; include/brownout.h
+    bo_distill_*): trains the G united experts of `moe`'s layer against their
+    groups' original experts on the token matrix X [N, d] (N % 64 == 0) by
+    plain gradient descent on fp32 masters.  The bf16 united tensors returned
+    by `united` are what BrownoutMoE.forward consumes."""
+
+    def __init__(self, moe: BrownoutMoE, N: int, device="cuda"):
+        self.moe = moe
+        self.N = int(N)
+        self.L = bo_distill_layout()
+        _check(_lib.bo_distill_workspace_layout(moe._h, self.N, C.byref(self.L)))
+        self.ws = torch.empty(self.L.total_bytes, dtype=torch.uint8, device=device)
+        self.X = None
+        self.masters = None
+        self.united = None
+
+    def prepare(self, X, Wg, Wu, Wd, stream=None):
+        """Teacher outputs of every original expert on X, their group means and
+        variance floors (once per token set)."""
+        assert X.shape[0] == self.N
+        self.X = X
+        self._experts = (Wg, Wu, Wd)
+        _check(_lib.bo_distill_prepare(self.moe._h, _ptr(X), self.N, _ptr(Wg), _ptr(Wu), _ptr(Wd), _ptr(self.ws),
+                                       self.ws.numel(), _stream(stream)))
+
+    def load_united(self, UWg, UWu, UWd, stream=None):
+        """Initial student weights (bf16, e.g. BrownoutMoE.build_united); the
+        tensors are then updated in place by every step."""
+        self.united = (UWg, UWu, UWd)
+        self.masters = tuple(torch.empty(u.shape, dtype=torch.float32, device=u.device) for u in self.united)
+        _check(_lib.bo_distill_load_united(self.moe._h, self.N, *[_ptr(u) for u in self.united],
+                                           *[_ptr(w) for w in self.masters], _ptr(self.ws), self.ws.numel(),
+                                           _stream(stream)))
+
+    def step(self, lr: float, stream=None):
+        _check(_lib.bo_distill_step(self.moe._h, _ptr(self.X), self.N, float(lr), *[_ptr(w) for w in self.masters],
+                                    *[_ptr(u) for u in self.united], _ptr(self.ws), self.ws.numel(),
+                                    _stream(stream)))
+
+    def _view(self, off, n, dt):
+        nbytes = n * torch.tensor([], dtype=dt).element_size()
+        return self.ws[off:off + nbytes].view(dt)
+
+    def loss(self):
+        """Eq. 4 per group (fp64) of the weights that entered the last step."""
+        return self._view(self.L.loss, self.moe.G, torch.float64)
+
+    def floor(self):
+        return self._view(self.L.floor_, self.moe.G, torch.float64)
+
+    def hbar(self):
+        d = self.moe.cfg.hidden
+        return self._view(self.L.hbar, self.moe.G * self.N * d, torch.float32).view(self.moe.G, self.N, d)

@@ -522,9 +522,364 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   return BO_OK;
 }
 
+// ---------------------------------------------------------------- distillation
+// One ungrouped-epilogue GEMM on the grouped engine: for executor x,
+// out[rows of x] = alpha * A[rows of x (or 0.. when a_shared)] B_x^T, with
+// B_x = rows [x * b_rows_per_exec, +n_cols) of B.  f32_mode 0: bf16 out;
+// 1: fp32 out; 2: fp32 out += (the fused gradient-descent update).
+struct PlainGemm {
+  const void* A = nullptr;
+  int64_t a_rows = 0;
+  int Kdim = 0;
+  int a_shared = 0;
+  const void* B = nullptr;
+  int64_t b_rows = 0;
+  int b_rows_per_exec = 0;
+  const int32_t* exec_off = nullptr;
+  int num_exec = 0;
+  int64_t rows_total = 0;
+  int n_cols = 0;
+  void* out = nullptr;
+  int ldo = 0;
+  int f32_mode = 0;
+  float alpha = 1.0f;
+};
+
+bo_status plain_gemm(bo_handle* h, const PlainGemm& g, cudaStream_t s, Prof& prof, int& launches) {
+  if (g.rows_total == 0) return BO_OK;
+  bo_status st;
+  int bn = gemm2_bn(g.n_cols);
+  const bool pair = h->cta_pairs && bn == 256 && g.rows_total >= 2048;
+  CUtensorMap mA, mB;
+  if ((st = make_map(&mA, g.A, BO_BF16, g.a_rows, g.Kdim, bo::kBM)) != BO_OK) return st;
+  if ((st = make_map(&mB, g.B, BO_BF16, g.b_rows, g.Kdim, pair ? bn / 2 : bn)) != BO_OK) return st;
+  bo::BMaps mb;
+  for (int i = 0; i < 6; ++i) mb.m[i] = mB;
+  bo::GemmParams p{};
+  p.Kdim = g.Kdim;
+  p.n_tiles = g.n_cols / bn;
+  p.Kdim_u = g.Kdim;
+  p.n_tiles_u = p.n_tiles;
+  p.b_rows_u = g.b_rows_per_exec;
+  p.ldo = g.ldo;
+  p.n_valid = g.n_cols;
+  p.m_orig = g.num_exec;
+  p.m_united = 0;
+  p.b_rows_per_exec = g.b_rows_per_exec;
+  p.num_exec = g.num_exec;
+  p.single_rows = -1;
+  p.exec_off = g.exec_off;
+  p.rows_total = static_cast<int>(g.rows_total);
+  p.a_shared = g.a_shared;
+  p.alpha = g.alpha;
+  p.f32_mode = g.f32_mode;
+  if (g.f32_mode) p.partial = static_cast<float*>(g.out);
+  else p.out = g.out;
+  const int tile_m = pair ? 2 * bo::kBM : bo::kBM;
+  const int64_t max_work = ((g.rows_total + tile_m - 1) / tile_m + g.num_exec) * p.n_tiles;
+  const int units = pair ? h->num_sms / 2 : h->num_sms;
+  const int grid = static_cast<int>(max_work < units ? max_work : units) * (pair ? 2 : 1);
+  prof.mark(launches);
+  BO_CUDA(bo::launch_grouped_gemm(0, pair ? bo::EPI_WEIGHTED_PAIR : bo::EPI_WEIGHTED, bn, mA, mb, p, grid, s),
+          "distill gemm");
+  ++launches;
+  return BO_OK;
+}
+
+void distill_layout(const bo_handle* h, int64_t N, bo_distill_layout* L) {
+  const bo_config& c = h->cfg;
+  const int64_t m = c.num_experts, d = c.hidden, f = c.ffn, G = (m + c.way - 1) / c.way;
+  memset(L, 0, sizeof(*L));
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = align256(off + (bytes ? bytes : 1));
+    return o;
+  };
+  const int nb_mean = bo::group_mean_blocks(N, static_cast<int>(d), h->num_sms);
+  const int64_t nb_mse = bo::mse_grad_blocks(N, d);
+  L->hbar = take(4 * G * N * d);
+  L->floor_ = take(8 * G);
+  L->loss = take(8 * G);
+  L->xt = take(2 * d * N);
+  L->teach_h = take(2 * m * N * f);
+  L->teach_y = take(4 * m * N * d);
+  L->p = take(2 * G * N * f);
+  L->q = take(2 * G * N * f);
+  L->hs = take(2 * G * N * f);
+  L->hst = take(2 * G * f * N);
+  L->y = take(4 * G * N * d);
+  L->dy = take(2 * G * N * d);
+  L->dyt = take(2 * G * d * N);
+  L->dhs = take(2 * G * N * f);
+  L->dpt = take(2 * G * f * N);
+  L->dqt = take(2 * G * f * N);
+  L->uwdt = take(2 * G * f * d);
+  L->part = take(8 * G * (nb_mean > nb_mse ? nb_mean : nb_mse));
+  L->off_tok = take(4 * (G + 1));
+  L->off_teach = take(4 * (m + 1));
+  L->off_f = take(4 * (G + 1));
+  L->off_d = take(4 * (G + 1));
+  L->total_bytes = off;
+  L->N = N;
+}
+
+bo_status distill_check(const bo_handle* h, int64_t N, void* ws, size_t ws_bytes, bo_distill_layout* L) {
+  if (!h) return fail(BO_ERR_INVALID_ARG, "null handle");
+  if (h->cfg.dtype != BO_BF16) return fail(BO_ERR_UNSUPPORTED, "distillation is built for bf16 handles");
+  if (N <= 0 || N % 64 || N > (int64_t(1) << 24))
+    return fail(BO_ERR_SHAPE, "N=%lld must be a positive multiple of 64", static_cast<long long>(N));
+  const int64_t rows = N * h->cfg.num_experts;
+  if (rows > (int64_t(1) << 31) - 1) return fail(BO_ERR_SHAPE, "m * N too large");
+  distill_layout(h, N, L);
+  if (!ws || ws_bytes < L->total_bytes)
+    return fail(BO_ERR_WORKSPACE, "distill workspace %zu bytes < required %zu", ws_bytes, L->total_bytes);
+  if (!aligned16(ws)) return fail(BO_ERR_SHAPE, "workspace must be 16-byte aligned");
+  return BO_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+bo_status bo_distill_workspace_layout(const bo_handle* h, int64_t N, bo_distill_layout* out) {
+  if (!h || !out) return fail(BO_ERR_INVALID_ARG, "null argument");
+  if (N < 0) return fail(BO_ERR_INVALID_ARG, "N < 0");
+  distill_layout(h, N, out);
+  return BO_OK;
+}
+
+bo_status bo_distill_prepare(bo_handle* h, const void* X, int64_t N, const void* Wg, const void* Wu, const void* Wd,
+                             void* ws, size_t ws_bytes, void* stream) {
+  bo_distill_layout L;
+  bo_status st;
+  if ((st = distill_check(h, N, ws, ws_bytes, &L)) != BO_OK) return st;
+  if (!X || !Wg || !Wu || !Wd) return fail(BO_ERR_INVALID_ARG, "null tensor pointer");
+  const void* ptrs[] = {X, Wg, Wu, Wd};
+  for (const void* q : ptrs)
+    if (!aligned16(q)) return fail(BO_ERR_SHAPE, "tensor pointers must be 16-byte aligned");
+  const bo_config& c = h->cfg;
+  const int m = c.num_experts, d = c.hidden, f = c.ffn, G = (m + c.way - 1) / c.way;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Prof prof(h, s, 1 << 30);
+  int launches = 0;
+  int32_t* off_teach = at<int32_t>(ws, L.off_teach);
+  BO_CUDA(bo::launch_fill_offsets(off_teach, m, static_cast<int>(N), s), "offsets");
+  BO_CUDA(bo::launch_fill_offsets(at<int32_t>(ws, L.off_tok), G, static_cast<int>(N), s), "offsets");
+  BO_CUDA(bo::launch_fill_offsets(at<int32_t>(ws, L.off_f), G, f, s), "offsets");
+  BO_CUDA(bo::launch_fill_offsets(at<int32_t>(ws, L.off_d), G, d, s), "offsets");
+  // teacher: every original expert on every token, H_o = Wd (silu(Wg x) * Wu x)
+  {
+    // GEMM1 + SwiGLU with the shared token matrix as A
+    const int64_t R = N * m;
+    int bn = 256;
+    while (bn > 64 && f % (bn / 2)) bn >>= 1;
+    const bool pair = h->cta_pairs && bn == 256 && R >= 2048;
+    CUtensorMap mA;
+    bo::BMaps mb;
+    if ((st = make_map(&mA, X, BO_BF16, N, d, bo::kBM)) != BO_OK) return st;
+    if ((st = make_map(&mb.m[0], Wg, BO_BF16, static_cast<uint64_t>(m) * f, d, bn / 2)) != BO_OK) return st;
+    if ((st = make_map(&mb.m[1], Wu, BO_BF16, static_cast<uint64_t>(m) * f, d, bn / 2)) != BO_OK) return st;
+    for (int i = 2; i < 6; ++i) mb.m[i] = mb.m[i & 1];
+    bo::GemmParams p{};
+    p.Kdim = d;
+    p.n_tiles = f / (bn / 2);
+    p.Kdim_u = d;
+    p.n_tiles_u = p.n_tiles;
+    p.b_rows_u = f;
+    p.ldo = f;
+    p.n_valid = f;
+    p.m_orig = m;
+    p.b_rows_per_exec = f;
+    p.num_exec = m;
+    p.single_rows = -1;
+    p.exec_off = off_teach;
+    p.out = at<char>(ws, L.teach_h);
+    p.rows_total = static_cast<int>(R);
+    p.a_shared = 1;
+    const int tile_m = pair ? 2 * bo::kBM : bo::kBM;
+    const int64_t max_work = ((R + tile_m - 1) / tile_m + m) * p.n_tiles;
+    const int units = pair ? h->num_sms / 2 : h->num_sms;
+    const int grid = static_cast<int>(max_work < units ? max_work : units) * (pair ? 2 : 1);
+    BO_CUDA(bo::launch_grouped_gemm(0, pair ? bo::EPI_SWIGLU_PAIR : bo::EPI_SWIGLU, bn, mA, mb, p, grid, s),
+            "teacher gemm1");
+  }
+  PlainGemm g2;   // H_o = H Wd^T in fp32
+  g2.A = at<char>(ws, L.teach_h);
+  g2.a_rows = N * m;
+  g2.Kdim = f;
+  g2.B = Wd;
+  g2.b_rows = static_cast<int64_t>(m) * d;
+  g2.b_rows_per_exec = d;
+  g2.exec_off = off_teach;
+  g2.num_exec = m;
+  g2.rows_total = N * m;
+  g2.n_cols = d;
+  g2.out = at<char>(ws, L.teach_y);
+  g2.ldo = d;
+  g2.f32_mode = 1;
+  if ((st = plain_gemm(h, g2, s, prof, launches)) != BO_OK) return st;
+  BO_CUDA(bo::launch_group_mean(at<float>(ws, L.teach_y), m, c.way, N, d, at<float>(ws, L.hbar),
+                                at<double>(ws, L.part), at<double>(ws, L.floor_), h->num_sms, s),
+          "group mean");
+  // X^T for the weight gradients (a cast of bf16 through fp32 is exact)
+  BO_CUDA(bo::launch_widen(X, at<float>(ws, L.teach_y), N * d, h->num_sms, s), "widen X");
+  BO_CUDA(bo::launch_cast_master(at<float>(ws, L.teach_y), nullptr, at<char>(ws, L.xt), 1, N, d, s), "X^T");
+  return BO_OK;
+}
+
+bo_status bo_distill_load_united(bo_handle* h, int64_t N, const void* UWg, const void* UWu, const void* UWd,
+                                 float* UWg_m, float* UWu_m, float* UWd_m, void* ws, size_t ws_bytes, void* stream) {
+  bo_distill_layout L;
+  bo_status st;
+  if ((st = distill_check(h, N, ws, ws_bytes, &L)) != BO_OK) return st;
+  if (!UWg || !UWu || !UWd || !UWg_m || !UWu_m || !UWd_m) return fail(BO_ERR_INVALID_ARG, "null tensor pointer");
+  const bo_config& c = h->cfg;
+  const int64_t m = c.num_experts, d = c.hidden, f = c.ffn, G = (m + c.way - 1) / c.way;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  BO_CUDA(bo::launch_widen(UWg, UWg_m, G * f * d, h->num_sms, s), "widen");
+  BO_CUDA(bo::launch_widen(UWu, UWu_m, G * f * d, h->num_sms, s), "widen");
+  BO_CUDA(bo::launch_widen(UWd, UWd_m, G * d * f, h->num_sms, s), "widen");
+  BO_CUDA(bo::launch_cast_master(UWd_m, nullptr, at<char>(ws, L.uwdt), G, d, f, s), "UWd^T");
+  return BO_OK;
+}
+
+bo_status bo_distill_step(bo_handle* h, const void* X, int64_t N, float lr, float* UWg_m, float* UWu_m,
+                          float* UWd_m, void* UWg, void* UWu, void* UWd, void* ws, size_t ws_bytes, void* stream) {
+  bo_distill_layout L;
+  bo_status st;
+  if ((st = distill_check(h, N, ws, ws_bytes, &L)) != BO_OK) return st;
+  if (!X || !UWg_m || !UWu_m || !UWd_m || !UWg || !UWu || !UWd) return fail(BO_ERR_INVALID_ARG, "null tensor pointer");
+  const void* ptrs[] = {X, UWg_m, UWu_m, UWd_m, UWg, UWu, UWd};
+  for (const void* q : ptrs)
+    if (!aligned16(q)) return fail(BO_ERR_SHAPE, "tensor pointers must be 16-byte aligned");
+  if (!(lr >= 0.0f)) return fail(BO_ERR_INVALID_ARG, "lr must be >= 0");
+  const bo_config& c = h->cfg;
+  const int m = c.num_experts, d = c.hidden, f = c.ffn, G = (m + c.way - 1) / c.way;
+  const int64_t R = static_cast<int64_t>(G) * N;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Prof prof(h, s, 13);   // 13 marked launch regions (the loss region is 2 kernels)
+  int launches = 0;
+  const int32_t* off_tok = at<int32_t>(ws, L.off_tok);
+  // student forward: P = X UWg^T, Q = X UWu^T (shared A = X)
+  PlainGemm g;
+  g.A = X;
+  g.a_rows = N;
+  g.Kdim = d;
+  g.a_shared = 1;
+  g.b_rows = static_cast<int64_t>(G) * f;
+  g.b_rows_per_exec = f;
+  g.exec_off = off_tok;
+  g.num_exec = G;
+  g.rows_total = R;
+  g.n_cols = f;
+  g.ldo = f;
+  g.B = UWg;
+  g.out = at<char>(ws, L.p);
+  if ((st = plain_gemm(h, g, s, prof, launches)) != BO_OK) return st;
+  g.B = UWu;
+  g.out = at<char>(ws, L.q);
+  if ((st = plain_gemm(h, g, s, prof, launches)) != BO_OK) return st;
+  prof.mark(launches);
+  BO_CUDA(bo::launch_swiglu_fwd(at<char>(ws, L.p), at<char>(ws, L.q), at<char>(ws, L.hs), at<char>(ws, L.hst), G,
+                                N, f, s),
+          "swiglu fwd");
+  ++launches;
+  // H_u = Hs UWd^T (fp32)
+  PlainGemm gy;
+  gy.A = at<char>(ws, L.hs);
+  gy.a_rows = R;
+  gy.Kdim = f;
+  gy.B = UWd;
+  gy.b_rows = static_cast<int64_t>(G) * d;
+  gy.b_rows_per_exec = d;
+  gy.exec_off = off_tok;
+  gy.num_exec = G;
+  gy.rows_total = R;
+  gy.n_cols = d;
+  gy.out = at<char>(ws, L.y);
+  gy.ldo = d;
+  gy.f32_mode = 1;
+  if ((st = plain_gemm(h, gy, s, prof, launches)) != BO_OK) return st;
+  // Eq. 4 loss and dL/dH_u
+  prof.mark(launches);
+  BO_CUDA(bo::launch_mse_grad(at<float>(ws, L.y), at<float>(ws, L.hbar), at<char>(ws, L.dy), at<char>(ws, L.dyt), G,
+                              N, d, at<double>(ws, L.part), at<double>(ws, L.floor_), m, c.way,
+                              at<double>(ws, L.loss), s),
+          "mse grad");
+  ++launches;
+  // dHs = dY UWd  (B = UWd^T [G, f, d])
+  PlainGemm gh;
+  gh.A = at<char>(ws, L.dy);
+  gh.a_rows = R;
+  gh.Kdim = d;
+  gh.B = at<char>(ws, L.uwdt);
+  gh.b_rows = static_cast<int64_t>(G) * f;
+  gh.b_rows_per_exec = f;
+  gh.exec_off = off_tok;
+  gh.num_exec = G;
+  gh.rows_total = R;
+  gh.n_cols = f;
+  gh.out = at<char>(ws, L.dhs);
+  gh.ldo = f;
+  if ((st = plain_gemm(h, gh, s, prof, launches)) != BO_OK) return st;
+  prof.mark(launches);
+  BO_CUDA(bo::launch_swiglu_bwd(at<char>(ws, L.dhs), at<char>(ws, L.p), at<char>(ws, L.q), at<char>(ws, L.dpt),
+                                at<char>(ws, L.dqt), G, N, f, s),
+          "swiglu bwd");
+  ++launches;
+  // weight gradients with the fused update W_m += (-lr) dL/dW_m (reduction over tokens)
+  PlainGemm gw;
+  gw.Kdim = static_cast<int>(N);
+  gw.a_rows = static_cast<int64_t>(G) * f;
+  gw.B = at<char>(ws, L.xt);
+  gw.b_rows = d;
+  gw.b_rows_per_exec = 0;   // X^T shared by every group
+  gw.exec_off = at<int32_t>(ws, L.off_f);
+  gw.num_exec = G;
+  gw.rows_total = static_cast<int64_t>(G) * f;
+  gw.n_cols = d;
+  gw.ldo = d;
+  gw.f32_mode = 2;
+  gw.alpha = -lr;
+  gw.A = at<char>(ws, L.dpt);
+  gw.out = UWg_m;
+  if ((st = plain_gemm(h, gw, s, prof, launches)) != BO_OK) return st;
+  gw.A = at<char>(ws, L.dqt);
+  gw.out = UWu_m;
+  if ((st = plain_gemm(h, gw, s, prof, launches)) != BO_OK) return st;
+  PlainGemm gd;   // dL/dUWd = dY^T Hs: A = dY^T [G, d, N], B = Hs^T [G, f, N]
+  gd.A = at<char>(ws, L.dyt);
+  gd.a_rows = static_cast<int64_t>(G) * d;
+  gd.Kdim = static_cast<int>(N);
+  gd.B = at<char>(ws, L.hst);
+  gd.b_rows = static_cast<int64_t>(G) * f;
+  gd.b_rows_per_exec = f;
+  gd.exec_off = at<int32_t>(ws, L.off_d);
+  gd.num_exec = G;
+  gd.rows_total = static_cast<int64_t>(G) * d;
+  gd.n_cols = f;
+  gd.out = UWd_m;
+  gd.ldo = f;
+  gd.f32_mode = 2;
+  gd.alpha = -lr;
+  if ((st = plain_gemm(h, gd, s, prof, launches)) != BO_OK) return st;
+  // refresh the bf16 copies (and UWd^T) from the masters
+  prof.mark(launches);
+  BO_CUDA(bo::launch_cast_master(UWg_m, UWg, nullptr, 1, static_cast<int64_t>(G) * f, d, s), "cast");
+  ++launches;
+  prof.mark(launches);
+  BO_CUDA(bo::launch_cast_master(UWu_m, UWu, nullptr, 1, static_cast<int64_t>(G) * f, d, s), "cast");
+  ++launches;
+  prof.mark(launches);
+  BO_CUDA(bo::launch_cast_master(UWd_m, UWd, at<char>(ws, L.uwdt), G, d, f, s), "cast");
+  ++launches;
+  prof.mark(launches);
+  if (prof.err != cudaSuccess) return cuda_fail(prof.err, "profile event record");
+  h->last_launches = launches + 1;   // + the loss reduction kernel
+  return BO_OK;
+}
+
 
 const char* bo_version(void) { return "brownout-b200 0.1 (sm_100a)"; }
 

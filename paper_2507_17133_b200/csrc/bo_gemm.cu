@@ -116,6 +116,15 @@ __device__ __forceinline__ void store_row32<float>(float* dst, const float (&v)[
   for (int q = 0; q < 8; ++q) d[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
 }
 
+__device__ __forceinline__ void add_row32(float* dst, const float (&v)[32]) {
+  float4* d = reinterpret_cast<float4*>(dst);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float4 o = d[q];
+    d[q] = make_float4(o.x + v[4 * q], o.y + v[4 * q + 1], o.z + v[4 * q + 2], o.w + v[4 * q + 3]);
+  }
+}
+
 // Running top-K list, (value desc, id asc); ids arrive in ascending order so a
 // new element only overtakes strictly smaller values (reading D8).
 template <int KMAX>
@@ -294,7 +303,7 @@ __global__ void __launch_bounds__(192, 1)
       for (int w = unit; w < total_work; w += n_units) {
         int x, mi, n, sp, kb0, kb1;
         decode_k(w, x, mi, n, sp, kb0, kb1);
-        const int arow = s_eoff[x] + mi * TILE_M + static_cast<int>(crank) * kBM;
+        const int arow = (p.a_shared ? 0 : s_eoff[x]) + mi * TILE_M + static_cast<int>(crank) * kBM;
         const int cls = x < mo ? 0 : (x < mu ? 1 : 2);      // original / united / shared
         const CUtensorMap* mb0 = &tmB.m[2 * cls];
         const CUtensorMap* mb1 = &tmB.m[2 * cls + 1];
@@ -424,8 +433,8 @@ __global__ void __launch_bounds__(192, 1)
           __syncwarp();
         }
       } else if constexpr (EPI == EPI_WEIGHTED) {
-        const float wr = valid ? p.row_w[grow] : 0.0f;
-        if (p.ksplit_max > 1) {   // split-K: fp32 partial of split sp, row-scaled (Eq. 6)
+        const float wr = valid ? (p.row_w ? p.row_w[grow] : p.alpha) : 0.0f;
+        if (p.ksplit_max > 1 || p.f32_mode) {   // split-K: fp32 partial of split sp, row-scaled (Eq. 6)
           float* outp = p.partial + (static_cast<int64_t>(sp) * p.rows_total + grow) * p.ldo + n * BN;
 #pragma unroll 1
           const float scale = kb1 > kb0 ? wr : 0.0f;   // an empty k-range contributes 0 (stale TMEM)
@@ -436,7 +445,10 @@ __global__ void __launch_bounds__(192, 1)
             float v[32];
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = kb1 > kb0 ? __uint_as_float(a[i]) * scale : 0.0f;
-            if (valid) store_row32<float>(outp + c, v);
+            if (valid) {
+              if (p.f32_mode == 2) add_row32(outp + c, v);   // W += alpha * acc (distillation update)
+              else store_row32<float>(outp + c, v);
+            }
           }
           tc_fence_before();
           __syncwarp();

@@ -42,6 +42,9 @@ struct GemmParams {
   int ksplit_max;          // EPI_WEIGHTED: > 1 enables split-K (fp32 partials [ks, R, ldo] into `partial`)
   float* partial;          // EPI_WEIGHTED split-K output
   int* ks_out;             // EPI_WEIGHTED split-K: the kernel publishes the split count it chose
+  int a_shared;            // 1: every executor reads A rows from 0 (one shared A, e.g. distillation tokens)
+  int f32_mode;            // EPI_WEIGHTED: 1 = fp32 output to `partial`; 2 = fp32 accumulate (+=) into `partial`
+  float alpha;             // EPI_WEIGHTED: row scale when row_w == nullptr
 };
 
 // Combine of split-K fp32 partials: y[t] = [x_t] + sum_slots sum_splits P[sp][row].
@@ -104,5 +107,20 @@ cudaError_t launch_dedup(int stage, const int32_t* topk_id, const float* topk_w,
 
 cudaError_t launch_build_united(int dtype, const void* W, int m, int way, int64_t per_expert, void* U,
                                 cudaStream_t s);
+
+// ---- united-expert distillation (bo_distill.cu; Eq. 4)
+cudaError_t launch_fill_offsets(int32_t* off, int n, int stride, cudaStream_t s);
+int group_mean_blocks(int64_t N, int d, int num_sms);
+int mse_grad_blocks(int64_t N, int64_t d);
+cudaError_t launch_group_mean(const float* Yo, int m, int way, int64_t N, int d, float* Hbar, double* part,
+                              double* floor_out, int num_sms, cudaStream_t s);
+cudaError_t launch_swiglu_fwd(const void* P, const void* Q, void* Hs, void* HsT, int64_t G, int64_t N, int64_t f,
+                              cudaStream_t s);
+cudaError_t launch_mse_grad(const float* Y, const float* Hbar, void* dY, void* dYT, int64_t G, int64_t N, int64_t d,
+                            double* part, const double* floor_in, int m, int way, double* loss_out, cudaStream_t s);
+cudaError_t launch_swiglu_bwd(const void* dHs, const void* P, const void* Q, void* dPT, void* dQT, int64_t G,
+                              int64_t N, int64_t f, cudaStream_t s);
+cudaError_t launch_cast_master(const float* W, void* Wb, void* WbT, int64_t G, int64_t R, int64_t C, cudaStream_t s);
+cudaError_t launch_widen(const void* Wb, float* W, int64_t n, int num_sms, cudaStream_t s);
 
 }  // namespace bo
