@@ -127,14 +127,16 @@ KERNELS_7 = ["router_topk", "plan", "permute", "gather", "gemm1_swiglu", "gemm2_
 
 KERNELS_9 = ["router_topk", "plan", "dedup_count", "dedup_plan", "dedup_permute", "gather", "gemm1_swiglu",
              "gemm2_weighted", "combine"]
-N_EVENTS = 10
+# bo_distill_step: 11 marked regions (the loss region holds the mse kernel and its reduction)
+KERNELS_DISTILL = ["gemm_P", "gemm_Q", "swiglu_fwd", "gemm_Y", "mse_grad", "gemm_dHs", "swiglu_bwd",
+                   "gemm_dUWg_sgd", "gemm_dUWu_sgd", "gemm_dUWd_sgd", "cast_UWd_T"]
 
 
 def kernel_names(layer):
     """Small batches fuse the gather into the permute (6 launches), large ones do not (7);
     united-row de-duplication adds its count / prefix / permute kernels (9)."""
     n = layer.moe.last_launch_count()
-    return {6: KERNELS_6, 7: KERNELS_7, 9: KERNELS_9}[n]
+    return {6: KERNELS_6, 7: KERNELS_7, 9: KERNELS_9, 12: KERNELS_DISTILL}[n]
 
 
 class Layer:
@@ -185,7 +187,7 @@ def time_steps(layer, steps, warmup, dist_on, per_kernel=True, graph=True):
     names = kernel_names(layer)
     ev_sets = None
     if per_kernel:
-        ev_sets = [[torch.cuda.Event(enable_timing=True) for _ in range(N_EVENTS)] for _ in range(steps)]
+        ev_sets = [[torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)] for _ in range(steps)]
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     g = None
@@ -233,6 +235,55 @@ def time_steps(layer, steps, warmup, dist_on, per_kernel=True, graph=True):
             kern[name] = sum(ev[j].elapsed_time(ev[j + 1]) for ev in ev_sets) / steps
     del g
     return ms, kern
+
+
+class DistillLayer:
+    """f4: one gradient-descent step of united-expert distillation (Eq. 4) on
+    every group of a layer, teacher outputs prepared once (bench `distill`)."""
+
+    def __init__(self, cfg, N, lr=0.2):
+        import torch
+        import synthetic as S
+        from paper_2507_17133_b200 import BrownoutMoE, UnitedDistiller
+        self.cfg, self.N, self.lr = cfg, N, lr
+        lay = S.make_layer(cfg, device="cuda")
+        self.moe = BrownoutMoE(cfg.d, cfg.f, cfg.m, cfg.K, cfg.way, dtype="bf16", max_tokens=16)
+        U = self.moe.build_united(lay["Wg"], lay["Wu"], lay["Wd"])
+        self.dist = UnitedDistiller(self.moe, N)
+        X = S.make_tokens(cfg, T=N, batch_index=11, device="cuda")
+        self.dist.prepare(X, lay["Wg"], lay["Wu"], lay["Wd"])
+        del lay
+        torch.cuda.empty_cache()
+        self.dist.load_united(*U)
+
+    def step(self):
+        self.dist.step(self.lr)
+
+    def flops(self):
+        """14 N d f G: student forward 6, backward dHs 2, weight gradients 6 (no dX)."""
+        c = self.cfg
+        return 14.0 * self.N * c.d * c.f * c.G
+
+
+def distill_bench(S, pk, steps):
+    import torch
+    cfg = S.C2
+    lay = DistillLayer(cfg, N=4096)
+    loss0 = lay.dist.loss().clone()
+    lay.step()
+    loss0 = lay.dist.loss().cpu().tolist()
+    ms, kern = time_steps(lay, steps, 3, False)
+    t = ms / steps / 1e3
+    tf = lay.flops() / t / 1e12
+    loss1 = lay.dist.loss().cpu().tolist()
+    out = {"workload": "Mixtral-8x7B layer shape, way 4 (G = 2 united experts), N = 4096 training tokens, "
+                       "bf16 operands, fp32 masters, plain GD lr 0.2",
+           "ms_per_step": t * 1e3, "tflops": tf, "frac_bf16_sustained": tf / pk["bf16_tflops_sustained"],
+           "flops_per_step": lay.flops(), "kernel_ms": kern, "loss_first": loss0, "loss_after": loss1,
+           "floor": lay.dist.floor().cpu().tolist(), "gpu_launches_per_step": lay.moe.last_launch_count()}
+    del lay
+    torch.cuda.empty_cache()
+    return out
 
 
 def time_e2e(layer, steps, warmup):
@@ -435,6 +486,7 @@ def main():
         out["ratio_sweep"] = sweep
     if not args.no_extra and cfg.name == "mixtral_prefill":
         out["salc_closed_loop"] = salc_demo(layer, S)
+        out["distill"] = distill_bench(S, pk, max(3, args.steps // 4))
         extra = {}
         for name in ("mixtral_decode", "qwen3_30b_a3b_prefill"):
             c2 = S.CONFIGS[name]

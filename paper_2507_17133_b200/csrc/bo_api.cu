@@ -540,6 +540,7 @@ struct PlainGemm {
   int64_t rows_total = 0;
   int n_cols = 0;
   void* out = nullptr;
+  void* out_bf16 = nullptr;   // f32_mode 2: also write the updated values rounded to bf16 here
   int ldo = 0;
   int f32_mode = 0;
   float alpha = 1.0f;
@@ -573,8 +574,12 @@ bo_status plain_gemm(bo_handle* h, const PlainGemm& g, cudaStream_t s, Prof& pro
   p.a_shared = g.a_shared;
   p.alpha = g.alpha;
   p.f32_mode = g.f32_mode;
-  if (g.f32_mode) p.partial = static_cast<float*>(g.out);
-  else p.out = g.out;
+  if (g.f32_mode) {
+    p.partial = static_cast<float*>(g.out);
+    p.out = g.out_bf16;
+  } else {
+    p.out = g.out;
+  }
   const int tile_m = pair ? 2 * bo::kBM : bo::kBM;
   const int64_t max_work = ((g.rows_total + tile_m - 1) / tile_m + g.num_exec) * p.n_tiles;
   const int units = pair ? h->num_sms / 2 : h->num_sms;
@@ -758,7 +763,7 @@ bo_status bo_distill_step(bo_handle* h, const void* X, int64_t N, float lr, floa
   const int m = c.num_experts, d = c.hidden, f = c.ffn, G = (m + c.way - 1) / c.way;
   const int64_t R = static_cast<int64_t>(G) * N;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  Prof prof(h, s, 13);   // 13 marked launch regions (the loss region is 2 kernels)
+  Prof prof(h, s, 11);   // 11 marked launch regions (the loss region is 2 kernels)
   int launches = 0;
   const int32_t* off_tok = at<int32_t>(ws, L.off_tok);
   // student forward: P = X UWg^T, Q = X UWu^T (shared A = X)
@@ -844,9 +849,11 @@ bo_status bo_distill_step(bo_handle* h, const void* X, int64_t N, float lr, floa
   gw.alpha = -lr;
   gw.A = at<char>(ws, L.dpt);
   gw.out = UWg_m;
+  gw.out_bf16 = UWg;      // the bf16 copy is written by the same epilogue
   if ((st = plain_gemm(h, gw, s, prof, launches)) != BO_OK) return st;
   gw.A = at<char>(ws, L.dqt);
   gw.out = UWu_m;
+  gw.out_bf16 = UWu;
   if ((st = plain_gemm(h, gw, s, prof, launches)) != BO_OK) return st;
   PlainGemm gd;   // dL/dUWd = dY^T Hs: A = dY^T [G, d, N], B = Hs^T [G, f, N]
   gd.A = at<char>(ws, L.dyt);
@@ -864,13 +871,7 @@ bo_status bo_distill_step(bo_handle* h, const void* X, int64_t N, float lr, floa
   gd.f32_mode = 2;
   gd.alpha = -lr;
   if ((st = plain_gemm(h, gd, s, prof, launches)) != BO_OK) return st;
-  // refresh the bf16 copies (and UWd^T) from the masters
-  prof.mark(launches);
-  BO_CUDA(bo::launch_cast_master(UWg_m, UWg, nullptr, 1, static_cast<int64_t>(G) * f, d, s), "cast");
-  ++launches;
-  prof.mark(launches);
-  BO_CUDA(bo::launch_cast_master(UWu_m, UWu, nullptr, 1, static_cast<int64_t>(G) * f, d, s), "cast");
-  ++launches;
+  // refresh the bf16 UWd and UWd^T from the master (UWg / UWu: in the GEMM epilogues)
   prof.mark(launches);
   BO_CUDA(bo::launch_cast_master(UWd_m, UWd, at<char>(ws, L.uwdt), G, d, f, s), "cast");
   ++launches;

@@ -116,12 +116,17 @@ __device__ __forceinline__ void store_row32<float>(float* dst, const float (&v)[
   for (int q = 0; q < 8; ++q) d[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
 }
 
-__device__ __forceinline__ void add_row32(float* dst, const float (&v)[32]) {
+// dst += v; v <- the updated values
+__device__ __forceinline__ void add_row32(float* dst, float (&v)[32]) {
   float4* d = reinterpret_cast<float4*>(dst);
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const float4 o = d[q];
-    d[q] = make_float4(o.x + v[4 * q], o.y + v[4 * q + 1], o.z + v[4 * q + 2], o.w + v[4 * q + 3]);
+    v[4 * q] += o.x;
+    v[4 * q + 1] += o.y;
+    v[4 * q + 2] += o.z;
+    v[4 * q + 3] += o.w;
+    d[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
   }
 }
 
@@ -446,8 +451,12 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = kb1 > kb0 ? __uint_as_float(a[i]) * scale : 0.0f;
             if (valid) {
-              if (p.f32_mode == 2) add_row32(outp + c, v);   // W += alpha * acc (distillation update)
-              else store_row32<float>(outp + c, v);
+              if (p.f32_mode == 2) {   // W += alpha * acc (distillation update), optional bf16 copy in p.out
+                add_row32(outp + c, v);
+                if (p.out) store_row32<T>(reinterpret_cast<T*>(p.out) + grow * p.ldo + n * BN + c, v);
+              } else {
+                store_row32<float>(outp + c, v);
+              }
             }
           }
           tc_fence_before();
