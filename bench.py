@@ -187,7 +187,9 @@ def time_steps(layer, steps, warmup, dist_on, per_kernel=True, graph=True):
     names = kernel_names(layer)
     ev_sets = None
     if per_kernel:
-        ev_sets = [[torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)] for _ in range(steps)]
+        # the library records only when given >= (its marked launches + 1) events (forward: 10)
+        n_ev = max(10, len(names) + 1)
+        ev_sets = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(steps)]
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     g = None
@@ -233,6 +235,10 @@ def time_steps(layer, steps, warmup, dist_on, per_kernel=True, graph=True):
         kern = {}
         for j, name in enumerate(names):
             kern[name] = sum(ev[j].elapsed_time(ev[j + 1]) for ev in ev_sets) / steps
+        # the per-kernel events must tile the step (else they were not recorded by the library)
+        tot = sum(kern.values())
+        if not 0.7 * ms / steps <= tot <= 1.05 * ms / steps:
+            raise RuntimeError(f"per-kernel events ({tot:.4f} ms) do not match the step ({ms / steps:.4f} ms)")
     del g
     return ms, kern
 
