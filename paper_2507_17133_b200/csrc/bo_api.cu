@@ -29,6 +29,7 @@ struct bo_handle {
   int32_t fused_gather;  // 1: GEMM1 gathers x rows by TMA gather4 (env BO_GATHER=1; default off)
   int32_t splitk;        // 1: GEMM2 split-K for decode-sized steps (env BO_SPLITK=1; default off)
   int32_t decode_bn1;    // >0: GEMM1 tile width for decode-sized steps (env BO_DECODE_BN1, experiments)
+  int32_t router_split;  // 1: decode-sized batches use k_router_split (env BO_ROUTER_SPLIT=0 disables)
   const void* SWg;       // shared experts (Eq. 5 second term): [N_s, f, d], [N_s, f, d], [N_s, d, f]
   const void* SWu;
   const void* SWd;
@@ -117,7 +118,8 @@ bo_status compute_layout(const bo_handle* h, int64_t T, bo_ws_layout* L) {
   const bo_config& c = h->cfg;
   const int64_t m = c.num_experts, K = c.top_k, d = c.hidden, f = c.ffn;
   const int64_t G = (m + c.way - 1) / c.way, Ns = c.num_shared, E = m + G + Ns;
-  const int64_t ntiles = (T + bo::kTileMin - 1) / bo::kTileMin;   // upper bound over every tile size
+  // upper bound over every token tile the route stage may pick (the decode router: 1 token per tile)
+  const int64_t ntiles = T < 8 * h->num_sms ? T : (T + bo::kTileMin - 1) / bo::kTileMin;
   const int64_t Rk = T * K;          // routed (token, slot) pairs
   const int64_t R = Rk + Ns * T;     // expert rows incl. the shared experts' (every token)
   const int eb = elem_bytes(c.dtype);
@@ -201,11 +203,20 @@ bo_status route_stage(bo_handle* h, const void* x, int64_t T, const void* Wr, co
     BO_CUDA(bo::launch_topk_hist(logits_in, static_cast<int>(T), m, K, tile, topk_id, topk_w, tile_cnt, s), "topk");
     ++launches;
   } else if (bo::router_small_ok(dt, m, d)) {
-    tile = bo::router_small_tile(static_cast<int>(T), h->num_sms);   // m <= 32: CUDA-core router (HBM-bound)
+    // m <= 32: CUDA-core router (HBM-bound); decode-sized batches split each token over several warps
+    const int tpc = h->router_split ? bo::router_split_tpc(static_cast<int>(T), h->num_sms) : 0;
     prof.mark(launches);
-    BO_CUDA(bo::launch_router_small(dt, x, Wr, static_cast<int>(T), d, m, K, tile, logits, topk_id, topk_w,
-                                    tile_cnt, s),
-            "router");
+    if (tpc > 0) {
+      tile = tpc;
+      BO_CUDA(bo::launch_router_split(dt, x, Wr, static_cast<int>(T), d, m, K, tpc, logits, topk_id, topk_w,
+                                      tile_cnt, s),
+              "router");
+    } else {
+      tile = bo::router_small_tile(static_cast<int>(T), h->num_sms);
+      BO_CUDA(bo::launch_router_small(dt, x, Wr, static_cast<int>(T), d, m, K, tile, logits, topk_id, topk_w,
+                                      tile_cnt, s),
+              "router");
+    }
     ++launches;
   } else {
     tile = bo::kTileTok;     // tcgen05 router, top-K fused into the epilogue
@@ -945,6 +956,8 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   // +2 % step at ratios 0 / 0.5, profiles/r01_bench_decode_splitk_*.json): off unless BO_SPLITK=1.
   const char* sk = getenv("BO_SPLITK");
   h->splitk = (sk && sk[0] == '1') ? 1 : 0;
+  const char* rs = getenv("BO_ROUTER_SPLIT");
+  h->router_split = (rs && rs[0] == '0') ? 0 : 1;
   const char* bn1 = getenv("BO_DECODE_BN1");
   h->decode_bn1 = bn1 ? atoi(bn1) : 0;
   if (h->decode_bn1 != 0 && h->decode_bn1 != 64 && h->decode_bn1 != 128 && h->decode_bn1 != 256) h->decode_bn1 = 0;

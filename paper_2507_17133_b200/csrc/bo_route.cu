@@ -233,6 +233,119 @@ __global__ void __launch_bounds__(256) k_router_small(const T* __restrict__ x, c
   if (threadIdx.x < m) tile_cnt[static_cast<int64_t>(blockIdx.x) * m + threadIdx.x] = hist[threadIdx.x];
 }
 
+// Decode-sized batches (T < 8 * #SM): k_router_small would run one warp per
+// token on T/8 CTAs, latency-bound on the FMA chain of each warp.  Here the
+// hidden dimension of each token is split over 8/tpc warps of a CTA (tpc
+// tokens per CTA, >= #SM CTAs), centroids read through L1 (no shared-memory
+// staging), partial logits reduced in a fixed order through shared memory.
+template <typename T, int MAXM>
+__global__ void __launch_bounds__(256) k_router_split(const T* __restrict__ x, const T* __restrict__ Wr, int Tn,
+                                                      int d, int m, int K, int tpc, float* __restrict__ logits,
+                                                      int32_t* __restrict__ topk_id, float* __restrict__ topk_w,
+                                                      int32_t* __restrict__ tile_cnt) {
+  __shared__ float s_part[8][MAXM];
+  __shared__ int hist[32];
+  constexpr int EPV = 16 / sizeof(T);
+  constexpr int U = 4;   // 16-byte x loads per lane in flight
+  const int nvec = d / EPV;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wpt = 8 / tpc;
+  const int tl = warp / wpt, q = warp - tl * wpt;
+  const int t = blockIdx.x * tpc + tl;
+  const int nvw = nvec / wpt;
+  const int v0 = q * nvw, v1 = v0 + nvw;
+  if (threadIdx.x < 32) hist[threadIdx.x] = 0;
+  float acc[MAXM];
+#pragma unroll
+  for (int e = 0; e < MAXM; ++e) acc[e] = 0.0f;
+  if (t < Tn) {
+    const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(t) * d);
+    const uint4* wr = reinterpret_cast<const uint4*>(Wr);
+    for (int c0 = v0 + lane; c0 < v1; c0 += 32 * U) {
+      uint4 xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + 32 * u;
+        xv[u] = c < v1 ? __ldg(xr + c) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int e0 = 0; e0 < MAXM; e0 += 8) {
+        if (e0 < m) {
+          uint4 wv[U][8];
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int c = c0 + 32 * u;
+              wv[u][j] = (c < v1 && e0 + j < m) ? __ldg(wr + static_cast<int64_t>(e0 + j) * nvec + c)
+                                                : make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            float xf[EPV];
+            unpack8<T>(xv[u], xf);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float wf[EPV];
+              unpack8<T>(wv[u][j], wf);
+#pragma unroll
+              for (int k = 0; k < EPV; ++k) acc[e0 + j] = fmaf(xf[k], wf[k], acc[e0 + j]);
+            }
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < MAXM; ++e) {
+    if (e < m) {
+      float a = acc[e];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+      if (lane == 0) s_part[warp][e] = a;
+    }
+  }
+  __syncthreads();
+  if (q == 0 && t < Tn) {   // warp-uniform: the token's first warp finishes Eq. 8 and does Eq. 7
+    float v[1];
+    v[0] = 0.0f;
+    if (lane < m)
+      for (int qq = 0; qq < wpt; ++qq) v[0] += s_part[tl * wpt + qq][lane];
+    if (lane < m) logits[static_cast<int64_t>(t) * m + lane] = v[0];
+    int id;
+    float w;
+    warp_topk_softmax<1>(v, m, K, lane, id, w);
+    if (lane < K) {
+      topk_id[static_cast<int64_t>(t) * K + lane] = id;
+      topk_w[static_cast<int64_t>(t) * K + lane] = w;
+      atomicAdd(&hist[id], 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < m) tile_cnt[static_cast<int64_t>(blockIdx.x) * m + threadIdx.x] = hist[threadIdx.x];
+}
+
+int router_split_tpc(int T, int num_sms) {
+  if (T >= 8 * num_sms) return 0;   // k_router_small
+  return T >= 4 * num_sms ? 4 : (T >= 2 * num_sms ? 2 : 1);
+}
+
+cudaError_t launch_router_split(int dtype, const void* x, const void* Wr, int T, int d, int m, int K, int tpc,
+                                float* logits, int32_t* topk_id, float* topk_w, int32_t* tile_cnt, cudaStream_t s) {
+  const int ntiles = (T + tpc - 1) / tpc;
+  if (ntiles == 0) return cudaSuccess;
+#define BO_RS(TYPE, M)                                                                                       \
+  k_router_split<TYPE, M><<<ntiles, 256, 0, s>>>(static_cast<const TYPE*>(x), static_cast<const TYPE*>(Wr), T, \
+                                                 d, m, K, tpc, logits, topk_id, topk_w, tile_cnt)
+  if (dtype == 0) {
+    if (m <= 8) BO_RS(__nv_bfloat16, 8); else if (m <= 16) BO_RS(__nv_bfloat16, 16); else BO_RS(__nv_bfloat16, 32);
+  } else {
+    if (m <= 8) BO_RS(float, 8); else if (m <= 16) BO_RS(float, 16); else BO_RS(float, 32);
+  }
+#undef BO_RS
+  return cudaGetLastError();
+}
+
 bool router_small_ok(int dtype, int m, int d) {
   const int eb = dtype == 0 ? 2 : 4;
   return m <= 32 && static_cast<int64_t>(m) * d * eb <= 160 * 1024;
@@ -574,14 +687,29 @@ __global__ void __launch_bounds__(256) k_permute(const int32_t* __restrict__ top
     const int t0 = blockIdx.x * tile;
     const int nt = min(tile, T - t0);
     const int total = nt * vec_per_row;
-    for (int i = threadIdx.x; i < total; i += blockDim.x) {
-      const int tt = i / vec_per_row;
-      const int c = i - tt * vec_per_row;
-      const int64_t t = t0 + tt;
-      const uint4 v = __ldg(x + t * vec_per_row + c);
-      for (int s = 0; s < KR; ++s) {
-        const int r = row_of[t * KR + s];
-        if (r >= 0) xp[static_cast<int64_t>(r) * vec_per_row + c] = v;
+    constexpr int U = 4;   // loads in flight per thread before the stores (the copy is latency-bound)
+    for (int i0 = threadIdx.x; i0 < total; i0 += U * blockDim.x) {
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * blockDim.x;
+        if (i < total) {
+          const int tt = i / vec_per_row;
+          v[u] = __ldg(x + (t0 + tt) * static_cast<int64_t>(vec_per_row) + (i - tt * vec_per_row));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * blockDim.x;
+        if (i < total) {
+          const int tt = i / vec_per_row;
+          const int c = i - tt * vec_per_row;
+          const int64_t t = t0 + tt;
+          for (int s = 0; s < KR; ++s) {
+            const int r = row_of[t * KR + s];
+            if (r >= 0) xp[static_cast<int64_t>(r) * vec_per_row + c] = v[u];
+          }
+        }
       }
     }
   }

@@ -155,9 +155,16 @@ def test_zero_tokens_is_noop():
     assert y.shape == (0, cfg.d)
 
 
-@pytest.mark.parametrize("cfg", SMALL, ids=lambda c: c.name)
-def test_router_logits_vs_fp64(cfg):
-    """Eq. 8 on the tensor cores (fp32 accumulate) vs the fp64 oracle."""
+@pytest.mark.parametrize("cfg", SMALL + [S.LayerConfig("split_router_tpc4", d=512, f=128, m=8, K=2, way=4, T=700,
+                                                        ratio=0.5, dtype="bf16", sigma=0.5, config_id=17)],
+                         ids=lambda c: c.name)
+@pytest.mark.parametrize("router", ["default", "no_split"])
+def test_router_logits_vs_fp64(cfg, router, monkeypatch):
+    """Eq. 8 (tensor cores for m > 32; CUDA cores for m <= 32: the split-warp
+    decode router below 8 x #SM tokens, else the warp-per-token router;
+    BO_ROUTER_SPLIT=0 forces the latter) vs the fp64 oracle."""
+    if router == "no_split":
+        monkeypatch.setenv("BO_ROUTER_SPLIT", "0")
     lay = S.make_layer(cfg)
     x = S.make_tokens(cfg, T=cfg.T)
     moe = _moe(cfg)
