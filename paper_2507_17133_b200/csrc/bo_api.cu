@@ -30,6 +30,7 @@ struct bo_handle {
   int32_t splitk;        // 1: GEMM2 split-K for decode-sized steps (env BO_SPLITK=1; default off)
   int32_t decode_bn1;    // >0: GEMM1 tile width for decode-sized steps (env BO_DECODE_BN1, experiments)
   int32_t router_split;  // 1: decode-sized batches use k_router_split (env BO_ROUTER_SPLIT=0 disables)
+  int32_t tile_alt;      // 1: GEMM1 may pick a narrower SwiGLU tile on the device (env BO_TILE_ALT=0 disables)
   const void* SWg;       // shared experts (Eq. 5 second term): [N_s, f, d], [N_s, f, d], [N_s, d, f]
   const void* SWu;
   const void* SWd;
@@ -245,7 +246,7 @@ bo_status route_stage(bo_handle* h, const void* x, int64_t T, const void* Wr, co
     const int grid = work < h->num_sms ? work : h->num_sms;
     prof.mark(launches);
     bo::BMaps mbs;
-    for (int i = 0; i < 6; ++i) mbs.m[i] = mB;
+    for (int i = 0; i < 12; ++i) mbs.m[i] = mB;
     BO_CUDA(bo::launch_grouped_gemm(dt, bo::EPI_ROUTER, bn, mA, mbs, p, grid, s), "router gemm");
     ++launches;
   }
@@ -332,6 +333,24 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
         return st;
     }
     bo::GemmParams p{};
+    // alternative tile width for the device-side wave choice: the widest gate/up half
+    // below bn/2 (multiple of 16, >= 64) that divides both widths
+    int bh_alt = 0;
+    if (h->tile_alt && !gather)
+      for (int bh = bn / 2 - 16; bh >= 64 && !bh_alt; bh -= 16)
+        if (f % bh == 0 && f_u % bh == 0) bh_alt = bh;
+    if (bh_alt) {
+      for (int k = 0; k < 3; ++k) {
+        const int width = k == 1 ? f_u : f;
+        if ((st = make_map(&mb.m[6 + 2 * k], ptr(*cls[k], 0), c.dtype, rows_of(*cls[k], width), d, bh_alt)) != BO_OK)
+          return st;
+        if ((st = make_map(&mb.m[7 + 2 * k], ptr(*cls[k], 1), c.dtype, rows_of(*cls[k], width), d, bh_alt)) != BO_OK)
+          return st;
+      }
+      p.bh_alt = bh_alt;
+      p.nt_alt = f / bh_alt;
+      p.nt_alt_u = f_u / bh_alt;
+    }
     p.Kdim = d;
     p.n_tiles = f / (bn / 2);
     p.Kdim_u = d;
@@ -956,6 +975,8 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   // +2 % step at ratios 0 / 0.5, profiles/r01_bench_decode_splitk_*.json): off unless BO_SPLITK=1.
   const char* sk = getenv("BO_SPLITK");
   h->splitk = (sk && sk[0] == '1') ? 1 : 0;
+  const char* ta = getenv("BO_TILE_ALT");
+  h->tile_alt = (ta && ta[0] == '0') ? 0 : 1;
   const char* rs = getenv("BO_ROUTER_SPLIT");
   h->router_split = (rs && rs[0] == '0') ? 0 : 1;
   const char* bn1 = getenv("BO_DECODE_BN1");

@@ -78,7 +78,7 @@ __device__ __forceinline__ void stage_row32(uint8_t* stage, int lane, const floa
 // rows of the warp: global row index = row0 + r (r < nrows valid), column offset col0.
 template <typename T>
 __device__ __forceinline__ void flush_rows32(const uint8_t* stage, int lane, T* out, int64_t row0, int nrows,
-                                             int64_t ldo) {
+                                             int64_t ldo, int vmax = 32 * (int)sizeof(T) / 16) {
   constexpr int V16 = 32 * (int)sizeof(T) / 16;   // 16-byte pieces per row chunk
   constexpr int ROW = 32 * (int)sizeof(T) + 16;
   constexpr int RPI = 32 / V16;                    // rows per store instruction
@@ -86,7 +86,7 @@ __device__ __forceinline__ void flush_rows32(const uint8_t* stage, int lane, T* 
 #pragma unroll
   for (int i = 0; i < V16; ++i) {
     const int r = i * RPI + lane / V16;
-    if (r < nrows) {
+    if (r < nrows && piece < vmax) {
       const uint4 v = *reinterpret_cast<const uint4*>(stage + r * ROW + piece * 16);
       *reinterpret_cast<uint4*>(out + (row0 + r) * ldo + piece * (16 / (int)sizeof(T))) = v;
     }
@@ -201,6 +201,8 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     for (int i = 0; i < 6; ++i) tma_prefetch_desc(&tmB.m[i]);
+    if (p.bh_alt > 0)
+      for (int i = 6; i < 12; ++i) tma_prefetch_desc(&tmB.m[i]);
   }
   if constexpr (CG == 2) cluster_sync();   // peer barriers initialised before any remote arrive / alloc
   if (warp == 1) {
@@ -249,13 +251,37 @@ __global__ void __launch_bounds__(192, 1)
   // (expert-parallel f-slices); shared experts have the originals' shape.
   const int mo = p.m_orig < nexec ? p.m_orig : nexec;
   const int mu = mo + p.m_united < nexec ? mo + p.m_united : nexec;
-  const int nt_o = p.n_tiles, nt_u = p.n_tiles_u;
+  int nt_o = p.n_tiles, nt_u = p.n_tiles_u;
   auto start_of = [&](int x) {
     const int a = x < mo ? x : mo;                      // min(x, mo)
     const int b = x < mo ? mo : (x < mu ? x : mu);      // clamp(x, mo, mu)
     const int c = x < mu ? mu : x;                      // max(x, mu)
     return nt_o * s_mtile[a] + nt_u * (s_mtile[b] - s_mtile[mo]) + nt_o * (s_mtile[c] - s_mtile[mu]);
   };
+  // SwiGLU tile width: BN (gate + up columns) or the alternative 2 * bh_alt, whichever
+  // needs fewer tile-column waves over the persistent grid: decode-sized steps have
+  // few m-tiles, and the last partial wave of BN-wide tiles can idle most SMs.
+  int bh = BN / 2;
+  bool alt = false;
+  if constexpr (EPI == EPI_SWIGLU && !GATHER) {
+    if (p.bh_alt > 0) {
+      const int items_p = start_of(nexec);
+      nt_o = p.nt_alt;
+      nt_u = p.nt_alt_u;
+      const int items_a = start_of(nexec);
+      const long long cost_p = static_cast<long long>((items_p + n_units - 1) / n_units) * (BN + 32);
+      const long long cost_a = static_cast<long long>((items_a + n_units - 1) / n_units) * (2 * p.bh_alt + 32);
+      alt = cost_a < cost_p;
+      if (alt) {
+        bh = p.bh_alt;
+      } else {
+        nt_o = p.n_tiles;
+        nt_u = p.n_tiles_u;
+      }
+    }
+  }
+  const uint32_t idesc = alt ? idesc_f32acc<T>(128 * CG, 2 * bh) : IDESC;
+  const int stage_tx = C::A_BYTES + (EPI == EPI_SWIGLU ? 2 * bh : BN) * 128 / CG;   // bytes per CTA per stage
   const int base_work = start_of(nexec);
   auto kblocks = [&](int x) { return (x < mo || x >= mu ? p.Kdim : p.Kdim_u) / C::BK; };
   // Split-K (GEMM2, few rows): when the tiles would leave SMs idle, each tile's
@@ -310,8 +336,8 @@ __global__ void __launch_bounds__(192, 1)
         decode_k(w, x, mi, n, sp, kb0, kb1);
         const int arow = (p.a_shared ? 0 : s_eoff[x]) + mi * TILE_M + static_cast<int>(crank) * kBM;
         const int cls = x < mo ? 0 : (x < mu ? 1 : 2);      // original / united / shared
-        const CUtensorMap* mb0 = &tmB.m[2 * cls];
-        const CUtensorMap* mb1 = &tmB.m[2 * cls + 1];
+        const CUtensorMap* mb0 = &tmB.m[(alt ? 6 : 0) + 2 * cls];
+        const CUtensorMap* mb1 = &tmB.m[(alt ? 6 : 0) + 2 * cls + 1];
         const int brow = cls == 0 ? x * p.b_rows_per_exec
                                   : (cls == 1 ? (x - mo) * p.b_rows_u : (x - mu) * p.b_rows_per_exec);
         int4 tok = make_int4(0, 0, 0, 0);
@@ -328,22 +354,22 @@ __global__ void __launch_bounds__(192, 1)
           uint8_t* sb = sa + C::A_BYTES;
           if (lane == 0) {
             if constexpr (CG == 1) {
-              mbar_arrive_expect_tx(&full_bar[stage], C::STAGE_BYTES);
+              mbar_arrive_expect_tx(&full_bar[stage], stage_tx);
               if constexpr (!GATHER) tma_load_2d(sa, &tmA, &full_bar[stage], kb * C::BK, arow, pol_a);
               if constexpr (EPI == EPI_SWIGLU) {
-                tma_load_2d(sb, mb0, &full_bar[stage], kb * C::BK, brow + n * (BN / 2), pol_b);
-                tma_load_2d(sb + (BN / 2) * 128, mb1, &full_bar[stage], kb * C::BK, brow + n * (BN / 2), pol_b);
+                tma_load_2d(sb, mb0, &full_bar[stage], kb * C::BK, brow + n * bh, pol_b);
+                tma_load_2d(sb + bh * 128, mb1, &full_bar[stage], kb * C::BK, brow + n * bh, pol_b);
               } else {
                 tma_load_2d(sb, mb0, &full_bar[stage], kb * C::BK, brow + n * BN, pol_b);
               }
             } else {
               // Both CTAs load their halves; completion is counted on the leader's barrier.
-              if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * C::STAGE_BYTES);
+              if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * stage_tx);
               else mbar_arrive_remote(&full_bar[stage], 0);
               if constexpr (!GATHER) tma_load_2d_pair(sa, &tmA, &full_bar[stage], kb * C::BK, arow, pol_a);
               if constexpr (EPI == EPI_SWIGLU) {
                 // leader: gate rows, peer: up rows of the same f-columns -> D[:, 0:BN/2] = gate, D[:, BN/2:] = up
-                tma_load_2d_pair(sb, leader ? mb0 : mb1, &full_bar[stage], kb * C::BK, brow + n * (BN / 2), pol_b);
+                tma_load_2d_pair(sb, leader ? mb0 : mb1, &full_bar[stage], kb * C::BK, brow + n * bh, pol_b);
               } else {
                 tma_load_2d_pair(sb, mb0, &full_bar[stage], kb * C::BK,
                                  brow + n * BN + static_cast<int>(crank) * (BN / 2), pol_b);
@@ -380,9 +406,9 @@ __global__ void __launch_bounds__(192, 1)
           for (int k = 0; k < C::BK / C::UK; ++k) {
             const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
             if constexpr (CG == 1)
-              mma_ss<T>(sdesc_k_sw128(a_addr + k * 32), sdesc_k_sw128(b_addr + k * 32), d_tmem, IDESC, accum);
+              mma_ss<T>(sdesc_k_sw128(a_addr + k * 32), sdesc_k_sw128(b_addr + k * 32), d_tmem, idesc, accum);
             else
-              mma_ss_pair_bf16(sdesc_k_sw128(a_addr + k * 32), sdesc_k_sw128(b_addr + k * 32), d_tmem, IDESC, accum);
+              mma_ss_pair_bf16(sdesc_k_sw128(a_addr + k * 32), sdesc_k_sw128(b_addr + k * 32), d_tmem, idesc, accum);
           }
           if constexpr (CG == 1) tc_commit(&empty_bar[stage]);
           else tc_commit_pair(&empty_bar[stage]);   // frees the stage in both CTAs
@@ -422,27 +448,30 @@ __global__ void __launch_bounds__(192, 1)
       const int64_t row0 = static_cast<int64_t>(s_eoff[x]) + slab;
       uint8_t* stage = s_epi + (warp - 2) * 32 * C::EPI_ROW;
       if constexpr (EPI == EPI_SWIGLU) {
-        T* out = reinterpret_cast<T*>(p.out) + n * (BN / 2);
+        T* out = reinterpret_cast<T*>(p.out) + n * bh;
 #pragma unroll 1
-        for (int c = 0; c < BN / 2; c += 32) {
+        for (int c = 0; c < bh; c += 32) {
+          // a 16-column tail (bh % 32 == 16) reads 16 columns past each half (inside
+          // this accumulator's BN-column slot) and stores only the valid ones
           uint32_t g[32], u[32];
           tmem_ld32(t0 + c, g);
-          tmem_ld32(t0 + BN / 2 + c, u);
+          tmem_ld32(t0 + bh + c, u);
           tmem_ld_wait();
           float h[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) h[i] = silu_f(__uint_as_float(g[i])) * __uint_as_float(u[i]);
           stage_row32<T>(stage, lane, h);
           __syncwarp();
-          flush_rows32<T>(stage, lane, out + c, row0, nrows, p.ldo);
+          const int cols = bh - c < 32 ? bh - c : 32;
+          flush_rows32<T>(stage, lane, out + c, row0, nrows, p.ldo, cols * (int)sizeof(T) / 16);
           __syncwarp();
         }
       } else if constexpr (EPI == EPI_WEIGHTED) {
         const float wr = valid ? (p.row_w ? p.row_w[grow] : p.alpha) : 0.0f;
         if (p.ksplit_max > 1 || p.f32_mode) {   // split-K: fp32 partial of split sp, row-scaled (Eq. 6)
           float* outp = p.partial + (static_cast<int64_t>(sp) * p.rows_total + grow) * p.ldo + n * BN;
-#pragma unroll 1
           const float scale = kb1 > kb0 ? wr : 0.0f;   // an empty k-range contributes 0 (stale TMEM)
+#pragma unroll 1
           for (int c = 0; c < BN; c += 32) {
             uint32_t a[32];
             tmem_ld32(t0 + c, a);

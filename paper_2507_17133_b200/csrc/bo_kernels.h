@@ -45,6 +45,9 @@ struct GemmParams {
   int a_shared;            // 1: every executor reads A rows from 0 (one shared A, e.g. distillation tokens)
   int f32_mode;            // EPI_WEIGHTED: 1 = fp32 output to `partial`; 2 = fp32 accumulate (+=) into `partial`
   float alpha;             // EPI_WEIGHTED: row scale when row_w == nullptr
+  int bh_alt;              // EPI_SWIGLU: > 0 enables an alternative half-width (gate / up columns per tile)
+  int nt_alt, nt_alt_u;    // its n-tile counts (originals & shared / united); the kernel picks the width
+                           // with the fewer estimated tile-column waves over the device-side plan
 };
 
 // Combine of split-K fp32 partials: y[t] = [x_t] + sum_slots sum_splits P[sp][row].
@@ -57,8 +60,10 @@ cudaError_t launch_combine_partials(int dtype, const float* partial, const int* 
 // dtype: 0 bf16, 1 fp32 (tf32 MMA).  bn: MMA N (SwiGLU: gate+up columns).
 // B operand maps by executor class: [0]/[1] originals (gate or the only B / up),
 // [2]/[3] united experts, [4]/[5] shared experts (Eq. 5 second term).
+// [6..11]: the same three classes encoded for the alternative SwiGLU tile
+// width (GemmParams::bh_alt rows per gate / up half), when it is enabled.
 struct BMaps {
-  CUtensorMap m[6];
+  CUtensorMap m[12];
 };
 cudaError_t launch_grouped_gemm(int dtype, int epi, int bn, const CUtensorMap& A, const BMaps& B,
                                 const GemmParams& p, int grid, cudaStream_t s);

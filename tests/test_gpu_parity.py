@@ -106,6 +106,9 @@ SMALL = [
                   sigma=0.5, config_id=15),
     S.LayerConfig("fp32_m64", d=128, f=64, m=64, K=3, way=4, T=100, ratio=0.5, dtype="fp32", sigma=0.5,
                   config_id=16),
+    # f = 16 x 112: GEMM1's alternative tile (112 gate + 112 up columns, a 16-column epilogue tail)
+    S.LayerConfig("tile_alt_112", d=256, f=1792, m=8, K=2, way=4, T=100, ratio=0.5, dtype="bf16", sigma=0.5,
+                  config_id=18),
 ]
 
 
@@ -270,9 +273,9 @@ def test_plan_random_counts_bitexact():
         assert np.array_equal(out["exec_off"].cpu().numpy(), perm.exec_off)
 
 
-@pytest.mark.parametrize("env", [{"BO_GATHER": "1"}, {"BO_GEMM_CG": "1"}, {"BO_SPLITK": "1"}],
-                         ids=["gather4_gemm1", "single_cta_gemm", "splitk_gemm2"])
-@pytest.mark.parametrize("cfg", [SMALL[0], SMALL[2], SMALL[3]], ids=lambda c: c.name)
+@pytest.mark.parametrize("env", [{"BO_GATHER": "1"}, {"BO_GEMM_CG": "1"}, {"BO_SPLITK": "1"}, {"BO_TILE_ALT": "0"}],
+                         ids=["gather4_gemm1", "single_cta_gemm", "splitk_gemm2", "no_tile_alt"])
+@pytest.mark.parametrize("cfg", [SMALL[0], SMALL[2], SMALL[3], SMALL[7]], ids=lambda c: c.name)
 def test_engine_variants_match_oracle(cfg, env, monkeypatch):
     """The non-default engine variants stay correct: GEMM1 fed by TMA gather4
     from x (BO_GATHER=1) and one-CTA tcgen05 tiles instead of CTA pairs."""
