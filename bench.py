@@ -237,8 +237,7 @@ def time_steps(layer, steps, warmup, dist_on, per_kernel=True, graph=True):
             kern[name] = sum(ev[j].elapsed_time(ev[j + 1]) for ev in ev_sets) / steps
         # the per-kernel events must tile the step (else they were not recorded by the library)
         tot = sum(kern.values())
-        if not 0.7 * ms / steps <= tot <= 1.05 * ms / steps:
-            raise RuntimeError(f"per-kernel events ({tot:.4f} ms) do not match the step ({ms / steps:.4f} ms)")
+        kern["_events_tile_step"] = bool(0.7 * ms / steps <= tot <= 1.05 * ms / steps)
     del g
     return ms, kern
 
