@@ -31,6 +31,7 @@ struct bo_handle {
   int32_t decode_bn1;    // >0: GEMM1 tile width for decode-sized steps (env BO_DECODE_BN1, experiments)
   int32_t router_split;  // 1: decode-sized batches use k_router_split (env BO_ROUTER_SPLIT=0 disables)
   int32_t tile_alt;      // 1: GEMM1 may pick a narrower SwiGLU tile on the device (env BO_TILE_ALT=0 disables)
+  int32_t store_hint;    // 1: FFN GEMM epilogue stores hint L2 evict_first (env BO_STORE_HINT=0 disables)
   const void* SWg;       // shared experts (Eq. 5 second term): [N_s, f, d], [N_s, f, d], [N_s, d, f]
   const void* SWu;
   const void* SWd;
@@ -360,6 +361,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.n_valid = f;
     p.m_orig = orig.n;
     p.m_united = uni.n;
+    p.store_hint = h->store_hint;
     p.b_rows_per_exec = f;
     p.num_exec = n_exec;
     p.single_rows = -1;
@@ -407,6 +409,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.n_valid = d;
     p.m_orig = orig.n;
     p.m_united = uni.n;
+    p.store_hint = h->store_hint;
     p.b_rows_per_exec = d;
     p.num_exec = n_exec;
     p.single_rows = -1;
@@ -975,6 +978,10 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   // +2 % step at ratios 0 / 0.5, profiles/r01_bench_decode_splitk_*.json): off unless BO_SPLITK=1.
   const char* sk = getenv("BO_SPLITK");
   h->splitk = (sk && sk[0] == '1') ? 1 : 0;
+  const char* sh = getenv("BO_STORE_HINT");
+  // evict_first on the streaming H / Yp stores keeps weight tiles in L2: C2 GEMM1 DRAM reads
+  // 1.60 -> 1.47 GB, step -1.2 % (interleaved A/B, profiles/r01_ab_store_hint.json)
+  h->store_hint = (sh && sh[0] == '0') ? 0 : 1;
   const char* ta = getenv("BO_TILE_ALT");
   h->tile_alt = (ta && ta[0] == '0') ? 0 : 1;
   const char* rs = getenv("BO_ROUTER_SPLIT");

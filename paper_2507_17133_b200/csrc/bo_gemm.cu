@@ -78,7 +78,7 @@ __device__ __forceinline__ void stage_row32(uint8_t* stage, int lane, const floa
 // rows of the warp: global row index = row0 + r (r < nrows valid), column offset col0.
 template <typename T>
 __device__ __forceinline__ void flush_rows32(const uint8_t* stage, int lane, T* out, int64_t row0, int nrows,
-                                             int64_t ldo, int vmax = 32 * (int)sizeof(T) / 16) {
+                                             int64_t ldo, int vmax = 32 * (int)sizeof(T) / 16, uint64_t pol = 0) {
   constexpr int V16 = 32 * (int)sizeof(T) / 16;   // 16-byte pieces per row chunk
   constexpr int ROW = 32 * (int)sizeof(T) + 16;
   constexpr int RPI = 32 / V16;                    // rows per store instruction
@@ -88,7 +88,9 @@ __device__ __forceinline__ void flush_rows32(const uint8_t* stage, int lane, T* 
     const int r = i * RPI + lane / V16;
     if (r < nrows && piece < vmax) {
       const uint4 v = *reinterpret_cast<const uint4*>(stage + r * ROW + piece * 16);
-      *reinterpret_cast<uint4*>(out + (row0 + r) * ldo + piece * (16 / (int)sizeof(T))) = v;
+      T* dst = out + (row0 + r) * ldo + piece * (16 / (int)sizeof(T));
+      if (pol) st_global_hint(dst, v, pol);   // streaming output: keep the weight tiles in L2
+      else *reinterpret_cast<uint4*>(dst) = v;
     }
   }
 }
@@ -430,6 +432,7 @@ __global__ void __launch_bounds__(192, 1)
   } else {
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;   // TMEM lane quarter this warp may access
+    const uint64_t pol_out = p.store_hint ? policy_evict_first() : 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int w = unit; w < total_work; w += n_units) {
@@ -463,7 +466,7 @@ __global__ void __launch_bounds__(192, 1)
           stage_row32<T>(stage, lane, h);
           __syncwarp();
           const int cols = bh - c < 32 ? bh - c : 32;
-          flush_rows32<T>(stage, lane, out + c, row0, nrows, p.ldo, cols * (int)sizeof(T) / 16);
+          flush_rows32<T>(stage, lane, out + c, row0, nrows, p.ldo, cols * (int)sizeof(T) / 16, pol_out);
           __syncwarp();
         }
       } else if constexpr (EPI == EPI_WEIGHTED) {
@@ -508,7 +511,7 @@ __global__ void __launch_bounds__(192, 1)
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(a[i]) * wr;
           stage_row32<T>(stage, lane, v);
           __syncwarp();
-          flush_rows32<T>(stage, lane, out + c, row0, nrows, p.ldo);
+          flush_rows32<T>(stage, lane, out + c, row0, nrows, p.ldo, 32 * (int)sizeof(T) / 16, pol_out);
           __syncwarp();
         }
       } else {

@@ -46,6 +46,7 @@ struct GemmParams {
   int f32_mode;            // EPI_WEIGHTED: 1 = fp32 output to `partial`; 2 = fp32 accumulate (+=) into `partial`
   float alpha;             // EPI_WEIGHTED: row scale when row_w == nullptr
   int bh_alt;              // EPI_SWIGLU: > 0 enables an alternative half-width (gate / up columns per tile)
+  int store_hint;          // 1: epilogue stores carry an L2 evict_first hint (streaming H / Yp)
   int nt_alt, nt_alt_u;    // its n-tile counts (originals & shared / united); the kernel picks the width
                            // with the fewer estimated tile-column waves over the device-side plan
 };
