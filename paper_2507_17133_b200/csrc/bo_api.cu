@@ -30,6 +30,7 @@ struct bo_handle {
   int32_t splitk;        // 1: GEMM2 split-K for decode-sized steps (env BO_SPLITK=1; default off)
   int32_t decode_bn1;    // >0: GEMM1 tile width for decode-sized steps (env BO_DECODE_BN1, experiments)
   int32_t router_split;  // 1: decode-sized batches use k_router_split (env BO_ROUTER_SPLIT=0 disables)
+  int32_t router_mma;    // 1: prefill-sized bf16 batches with m <= 32 use k_router_mma (env BO_ROUTER_MMA=0 disables)
   int32_t tile_alt;      // 1: GEMM1 may pick a narrower SwiGLU tile on the device (env BO_TILE_ALT=0 disables)
   int32_t store_hint;    // 1: FFN GEMM epilogue stores hint L2 evict_first (env BO_STORE_HINT=0 disables)
   const void* SWg;       // shared experts (Eq. 5 second term): [N_s, f, d], [N_s, f, d], [N_s, d, f]
@@ -208,7 +209,11 @@ bo_status route_stage(bo_handle* h, const void* x, int64_t T, const void* Wr, co
     // m <= 32: CUDA-core router (HBM-bound); decode-sized batches split each token over several warps
     const int tpc = h->router_split ? bo::router_split_tpc(static_cast<int>(T), h->num_sms) : 0;
     prof.mark(launches);
-    if (tpc > 0) {
+    if (h->router_mma && bo::router_mma_ok(dt, m, d, static_cast<int>(T), h->num_sms)) {
+      tile = 16;
+      BO_CUDA(bo::launch_router_mma(x, Wr, static_cast<int>(T), d, m, K, logits, topk_id, topk_w, tile_cnt, s),
+              "router");
+    } else if (tpc > 0) {
       tile = tpc;
       BO_CUDA(bo::launch_router_split(dt, x, Wr, static_cast<int>(T), d, m, K, tpc, logits, topk_id, topk_w,
                                       tile_cnt, s),
@@ -984,6 +989,8 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   h->store_hint = (sh && sh[0] == '0') ? 0 : 1;
   const char* ta = getenv("BO_TILE_ALT");
   h->tile_alt = (ta && ta[0] == '0') ? 0 : 1;
+  const char* rm = getenv("BO_ROUTER_MMA");
+  h->router_mma = (rm && rm[0] == '0') ? 0 : 1;
   const char* rs = getenv("BO_ROUTER_SPLIT");
   h->router_split = (rs && rs[0] == '0') ? 0 : 1;
   const char* bn1 = getenv("BO_DECODE_BN1");

@@ -78,6 +78,10 @@ cudaError_t launch_topk_hist(const float* logits, int T, int m, int K, int tile,
 
 bool router_small_ok(int dtype, int m, int d);
 int router_small_tile(int T, int num_sms);   // 8..32 tokens per CTA
+// Prefill-sized batches, bf16, m <= 32, d % 128 == 0: mma.sync router over 16-token tiles.
+bool router_mma_ok(int dtype, int m, int d, int T, int num_sms);
+cudaError_t launch_router_mma(const void* x, const void* Wr, int T, int d, int m, int K, float* logits,
+                              int32_t* topk_id, float* topk_w, int32_t* tile_cnt, cudaStream_t s);
 // Decode-sized batches: tpc tokens per CTA (0: use k_router_small), hidden dim split over 8/tpc warps.
 int router_split_tpc(int T, int num_sms);
 cudaError_t launch_router_split(int dtype, const void* x, const void* Wr, int T, int d, int m, int K, int tpc,

@@ -325,6 +325,139 @@ __global__ void __launch_bounds__(256) k_router_split(const T* __restrict__ x, c
   if (threadIdx.x < m) tile_cnt[static_cast<int64_t>(blockIdx.x) * m + threadIdx.x] = hist[threadIdx.x];
 }
 
+// Prefill-sized batches, m <= 32, bf16: Eq. 8 on the tensor cores with
+// mma.sync m16n8k16 (bf16 x bf16 -> fp32).  N = m is far too narrow for a
+// tcgen05 tile, but one m16n8k16 per 8 experts x 16 tokens x 16 k replaces
+// 2 x 16 x 8 x 16 FMAs.  CTA = 16 tokens x 4 warps, warp w reduces over the
+// w-th quarter of d; operands come straight from global memory in 16-byte
+// loads: within every 32-wide k chunk, thread (r = lane/4, q = lane%4) holds
+// x[r][8q..8q+7], x[r+8][8q..8q+7] and Wr[n][8q..8q+7]; the two MMAs of the
+// chunk take elements {0,1},{2,3} and {4,5},{6,7} as their k-pairs (the same
+// k permutation on both operands, so the dot products are unchanged).  Partial
+// logits of the 4 warps are summed in a fixed order through shared memory,
+// then the warp top-K of Eq. 7.
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+template <int NB, int NW>
+__global__ void __launch_bounds__(32 * NW) k_router_mma(const __nv_bfloat16* __restrict__ x,
+                                                    const __nv_bfloat16* __restrict__ Wr, int Tn, int d, int m, int K,
+                                                    float* __restrict__ logits, int32_t* __restrict__ topk_id,
+                                                    float* __restrict__ topk_w, int32_t* __restrict__ tile_cnt) {
+  constexpr int U = 4;   // 32-wide k chunks in flight per thread
+  __shared__ float s_c[NW][16][NB * 8 + 1];
+  __shared__ int hist[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = lane >> 2, q = lane & 3;
+  const int t0 = blockIdx.x * 16;
+  const int nk = d / NW, k0 = warp * nk;
+  if (threadIdx.x < 32) hist[threadIdx.x] = 0;
+  const bool va = t0 + r < Tn, vb = t0 + r + 8 < Tn;
+  const uint4* xa = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(va ? t0 + r : 0) * d + k0 + 8 * q);
+  const uint4* xb = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(vb ? t0 + r + 8 : 0) * d + k0 + 8 * q);
+  const uint4* wp[NB];
+  bool vw[NB];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    vw[j] = 8 * j + r < m;
+    wp[j] = reinterpret_cast<const uint4*>(Wr + static_cast<int64_t>(vw[j] ? 8 * j + r : 0) * d + k0 + 8 * q);
+  }
+  float c[NB][4];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) c[j][0] = c[j][1] = c[j][2] = c[j][3] = 0.0f;
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  // register double buffer: the loads of chunk group i+1 are issued before the MMAs of group i
+  uint4 a[2][U], b[2][U], w[2][U][NB];
+  auto load = [&](int buf, int kc) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool in = kc + 32 * u < nk;
+      const int off = (kc + 32 * u) / 8;      // in 16-byte units
+      a[buf][u] = (in && va) ? __ldg(xa + off) : z;
+      b[buf][u] = (in && vb) ? __ldg(xb + off) : z;
+#pragma unroll
+      for (int j = 0; j < NB; ++j) w[buf][u][j] = (in && vw[j]) ? __ldg(wp[j] + off) : z;
+    }
+  };
+  auto compute = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        mma_bf16_16816(c[j], a[buf][u].x, b[buf][u].x, a[buf][u].y, b[buf][u].y, w[buf][u][j].x, w[buf][u][j].y);
+        mma_bf16_16816(c[j], a[buf][u].z, b[buf][u].z, a[buf][u].w, b[buf][u].w, w[buf][u][j].z, w[buf][u][j].w);
+      }
+  };
+  load(0, 0);
+  for (int kc = 0; kc < nk; kc += 64 * U) {   // nk is a multiple of 32 (d % 128 == 0)
+    load(1, kc + 32 * U);
+    compute(0);
+    if (kc + 32 * U >= nk) break;
+    load(0, kc + 64 * U);
+    compute(1);
+  }
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    s_c[warp][r][8 * j + 2 * q] = c[j][0];
+    s_c[warp][r][8 * j + 2 * q + 1] = c[j][1];
+    s_c[warp][r + 8][8 * j + 2 * q] = c[j][2];
+    s_c[warp][r + 8][8 * j + 2 * q + 1] = c[j][3];
+  }
+  __syncthreads();
+  // warp w finishes tokens (16 / NW) w ..: fixed-order sum over the K slices, Eq. 7, histogram
+  for (int i = 0; i < 16 / NW; ++i) {
+    const int tt = (16 / NW) * warp + i;
+    const int t = t0 + tt;
+    if (t >= Tn) break;   // warp-uniform
+    float v[1];
+    v[0] = 0.0f;
+    if (lane < m)
+      for (int ww = 0; ww < NW; ++ww) v[0] += s_c[ww][tt][lane];
+    if (lane < m) logits[static_cast<int64_t>(t) * m + lane] = v[0];
+    int id;
+    float wgt;
+    warp_topk_softmax<1>(v, m, K, lane, id, wgt);
+    if (lane < K) {
+      topk_id[static_cast<int64_t>(t) * K + lane] = id;
+      topk_w[static_cast<int64_t>(t) * K + lane] = wgt;
+      atomicAdd(&hist[id], 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < m) tile_cnt[static_cast<int64_t>(blockIdx.x) * m + threadIdx.x] = hist[threadIdx.x];
+}
+
+bool router_mma_ok(int dtype, int m, int d, int T, int num_sms) {
+  // decode-sized batches keep the split-warp router: its 1-token tiles give the
+  // permutation one CTA per token (mma router: 16-token tiles, permute 2.4x slower at T = 256)
+  return dtype == 0 && m <= 32 && d % 128 == 0 && T >= 8 * num_sms;
+}
+constexpr int kRouterMmaWarps = 8;   // K slices per 16-token tile (d % 256 == 0), else 4
+
+cudaError_t launch_router_mma(const void* x, const void* Wr, int T, int d, int m, int K, float* logits,
+                              int32_t* topk_id, float* topk_w, int32_t* tile_cnt, cudaStream_t s) {
+  const int ntiles = (T + 15) / 16;
+  if (ntiles == 0) return cudaSuccess;
+  const auto* xb = static_cast<const __nv_bfloat16*>(x);
+  const auto* wb = static_cast<const __nv_bfloat16*>(Wr);
+  const int nb = (m + 7) / 8;
+#define BO_RM(NB, NW) \
+  k_router_mma<NB, NW><<<ntiles, 32 * NW, 0, s>>>(xb, wb, T, d, m, K, logits, topk_id, topk_w, tile_cnt)
+  if (d % (32 * kRouterMmaWarps) == 0) {
+    if (nb == 1) BO_RM(1, kRouterMmaWarps); else if (nb == 2) BO_RM(2, kRouterMmaWarps); else BO_RM(4, kRouterMmaWarps);
+  } else {
+    if (nb == 1) BO_RM(1, 4); else if (nb == 2) BO_RM(2, 4); else BO_RM(4, 4);
+  }
+#undef BO_RM
+  return cudaGetLastError();
+}
+
 int router_split_tpc(int T, int num_sms) {
   if (T >= 8 * num_sms) return 0;   // k_router_small
   return T >= 4 * num_sms ? 4 : (T >= 2 * num_sms ? 2 : 1);

@@ -158,16 +158,28 @@ def test_zero_tokens_is_noop():
     assert y.shape == (0, cfg.d)
 
 
-@pytest.mark.parametrize("cfg", SMALL + [S.LayerConfig("split_router_tpc4", d=512, f=128, m=8, K=2, way=4, T=700,
-                                                        ratio=0.5, dtype="bf16", sigma=0.5, config_id=17)],
-                         ids=lambda c: c.name)
-@pytest.mark.parametrize("router", ["default", "no_split"])
+ROUTER_CFGS = SMALL + [
+    S.LayerConfig("split_router_tpc4", d=512, f=128, m=8, K=2, way=4, T=700, ratio=0.5, dtype="bf16", sigma=0.5,
+                  config_id=17),
+    # >= 8 x #SM tokens: the mma.sync router (16-token tiles, ragged last tile)
+    S.LayerConfig("mma_router_m8", d=512, f=128, m=8, K=2, way=4, T=1300, ratio=0.5, dtype="bf16", sigma=0.5,
+                  config_id=19),
+    S.LayerConfig("mma_router_m20_k5", d=256, f=128, m=20, K=5, way=4, T=2000, ratio=0.5, dtype="bf16", sigma=1.0,
+                  config_id=20),
+]
+
+
+@pytest.mark.parametrize("cfg", ROUTER_CFGS, ids=lambda c: c.name)
+@pytest.mark.parametrize("router", ["default", "no_split", "no_mma"])
 def test_router_logits_vs_fp64(cfg, router, monkeypatch):
-    """Eq. 8 (tensor cores for m > 32; CUDA cores for m <= 32: the split-warp
-    decode router below 8 x #SM tokens, else the warp-per-token router;
-    BO_ROUTER_SPLIT=0 forces the latter) vs the fp64 oracle."""
+    """Eq. 8 (tcgen05 for m > 32; for m <= 32: the split-warp decode router
+    below 8 x #SM tokens, the mma.sync router above (bf16), else the
+    warp-per-token CUDA-core router; BO_ROUTER_SPLIT=0 / BO_ROUTER_MMA=0 force
+    the latter) vs the fp64 oracle."""
     if router == "no_split":
         monkeypatch.setenv("BO_ROUTER_SPLIT", "0")
+    if router == "no_mma":
+        monkeypatch.setenv("BO_ROUTER_MMA", "0")
     lay = S.make_layer(cfg)
     x = S.make_tokens(cfg, T=cfg.T)
     moe = _moe(cfg)
@@ -181,7 +193,7 @@ def test_router_logits_vs_fp64(cfg, router, monkeypatch):
     assert (np.abs(Lg - Lr) <= tol).all()
 
 
-@pytest.mark.parametrize("cfg", SMALL, ids=lambda c: c.name)
+@pytest.mark.parametrize("cfg", SMALL + ROUTER_CFGS[-2:], ids=lambda c: c.name)
 def test_full_path_with_router_matches_oracle_when_margins_are_clear(cfg):
     """End to end with the GPU router: when every token's K-th / (K+1)-th fp64
     logit gap exceeds the router error bound, routing cannot differ, so the
