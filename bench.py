@@ -238,6 +238,10 @@ def time_steps(layer, steps, warmup, dist_on, per_kernel=True, graph=True):
         # the per-kernel events must tile the step (else they were not recorded by the library)
         tot = sum(kern.values())
         kern["_events_tile_step"] = bool(0.7 * ms / steps <= tot <= 1.05 * ms / steps)
+        # per-step spans (first to last library event of each step): distribution over the K steps
+        spans = sorted(ev[0].elapsed_time(ev[len(names)]) for ev in ev_sets)
+        q = lambda f: spans[min(len(spans) - 1, int(round(f * (len(spans) - 1))))]
+        kern["_step_ms_p10_p50_p90"] = [q(0.1), q(0.5), q(0.9)]
     del g
     return ms, kern
 

@@ -604,7 +604,10 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
         const int o = __shfl_up_sync(0xffffffffu, incl, off);
         if (lane >= off) incl += o;
       }
-      if (tile_base && t < ntiles) tile_base[static_cast<int64_t>(t) * m + e] = carry + incl - v;
+      if (tile_base && t < ntiles) {
+        if (staged) s_tc[t * m + e] = carry + incl - v;   // written back coalesced below
+        else tile_base[static_cast<int64_t>(t) * m + e] = carry + incl - v;
+      }
       carry += __shfl_sync(0xffffffffu, incl, 31);
     }
     if (lane == 0) {
@@ -613,11 +616,18 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
     }
   }
   __syncthreads();
+  if (tile_base && staged) {   // per-tile prefixes: 16-byte coalesced stores instead of m-strided ones
+    const int n16 = n_tc / 4;
+    for (int i = tid; i < n16; i += blockDim.x)
+      reinterpret_cast<int4*>(tile_base)[i] = reinterpret_cast<const int4*>(s_tc)[i];
+    for (int i = 4 * n16 + tid; i < n_tc; i += blockDim.x) tile_base[i] = s_tc[i];
+  }
   // 2. Alg. 1 line 5: order by (cnt desc, id asc) (D5) -- rank by counting
   const int c_me = tid < m ? s_cnt[tid] : 0;
   if (tid < m) {
     int pos = 0;
-    for (int j = 0; j < m; ++j) {
+#pragma unroll 8
+    for (int j = 0; j < m; ++j) {   // independent shared loads: unrolled so they overlap
       const int cj = s_cnt[j];
       pos += (cj > c_me) | ((cj == c_me) & (j < tid));
     }
