@@ -287,7 +287,9 @@ def test_plan_random_counts_bitexact():
 
 @pytest.mark.parametrize("env", [{"BO_GATHER": "1"}, {"BO_GEMM_CG": "1"}, {"BO_SPLITK": "1"}, {"BO_TILE_ALT": "0"}],
                          ids=["gather4_gemm1", "single_cta_gemm", "splitk_gemm2", "no_tile_alt"])
-@pytest.mark.parametrize("cfg", [SMALL[0], SMALL[2], SMALL[3], SMALL[7]], ids=lambda c: c.name)
+@pytest.mark.parametrize("cfg", [SMALL[0], SMALL[2], SMALL[3], SMALL[7],
+                                 S.LayerConfig("pairs_bf16", d=256, f=512, m=8, K=2, way=4, T=1500, ratio=0.5,
+                                               dtype="bf16", sigma=0.5, config_id=21)], ids=lambda c: c.name)
 def test_engine_variants_match_oracle(cfg, env, monkeypatch):
     """The non-default engine variants stay correct: GEMM1 fed by TMA gather4
     from x (BO_GATHER=1) and one-CTA tcgen05 tiles instead of CTA pairs."""
