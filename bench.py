@@ -121,22 +121,21 @@ def algorithmic(cfg, T, stats, d, f, m):
             "weight_bytes": w_bytes}
 
 
-KERNELS_6 = ["router_topk", "plan", "permute_gather", "gemm1_swiglu", "gemm2_weighted", "combine"]
-KERNELS_7 = ["router_topk", "plan", "permute", "gather", "gemm1_swiglu", "gemm2_weighted", "combine"]
-
-
-KERNELS_9 = ["router_topk", "plan", "dedup_count", "dedup_plan", "dedup_permute", "gather", "gemm1_swiglu",
-             "gemm2_weighted", "combine"]
 # bo_distill_step: 11 marked regions (the loss region holds the mse kernel and its reduction)
 KERNELS_DISTILL = ["gemm_P", "gemm_Q", "swiglu_fwd", "gemm_Y", "mse_grad", "gemm_dHs", "swiglu_bwd",
                    "gemm_dUWg_sgd", "gemm_dUWu_sgd", "gemm_dUWd_sgd", "cast_UWd_T"]
 
 
 def kernel_names(layer):
-    """Small batches fuse the gather into the permute (6 launches), large ones do not (7);
-    united-row de-duplication adds its count / prefix / permute kernels (9)."""
+    """The kernels of the last forward as the library reports them (small batches fuse the
+    gather into the permute, large ones do not; the combine runs in GEMM2's epilogue unless
+    split-K partials need it; de-duplication adds its count / prefix / permute kernels)."""
     n = layer.moe.last_launch_count()
-    return {6: KERNELS_6, 7: KERNELS_7, 9: KERNELS_9, 12: KERNELS_DISTILL}[n]
+    if n == 12:
+        return KERNELS_DISTILL
+    names = layer.moe.last_kernels()
+    assert len(names) == n, (names, n)
+    return names
 
 
 class Layer:
@@ -515,7 +514,7 @@ def main():
                 entry.update({tag + "tokens_per_s": world * cfg.T / (ms_r / args.steps / 1e3),
                               tag + "ms": ms_r / args.steps, tag + "executors": s_r["executors_accessed"],
                               tag + "rows": s_r["rows_original"] + s_r["rows_united"],
-                              tag + "gemm1_ms": k_r["gemm1_swiglu"], tag + "gemm2_ms": k_r["gemm2_weighted"]})
+                              tag + "gemm1_ms": k_r["gemm1_swiglu"], tag + "gemm2_ms": k_r.get("gemm2_weighted", k_r.get("gemm2_weighted_combine"))})
             sweep[str(r)] = entry
         layer.moe = base_moe
         layer.ws = base_moe.workspace(cfg.T, "cuda")

@@ -117,6 +117,7 @@ typedef struct {
   size_t tile_xcnt;       /* int32 [ntiles, E]  rows per executor per tile (dedup_united)   */
   size_t tile_xbase;      /* int32 [ntiles, E]  their exclusive prefix over tiles            */
   size_t ksplit;          /* int32 [1]          split count GEMM2 chose                 */
+  size_t comb_cnt;        /* int32 [T, d/BN2]   arrival counters of the combine fused into GEMM2 (a8; BN2 = 256/128/64, GEMM2 tile width) */
   int64_t T;              /* tokens the layout was computed for                          */
   int64_t ntiles;         /* histogram tiles the workspace is sized for (8 tokens each)  */
   int64_t num_executors;  /* E = m + G                                                   */
@@ -311,6 +312,11 @@ BO_API bo_status bo_set_profile_events(bo_handle* h, void** events, int32_t n);
 
 /* Number of GPU kernels the last forward on this handle enqueued. */
 BO_API int32_t bo_last_launch_count(const bo_handle* h);
+/* Names of those kernels in launch order, comma-separated (e.g.
+ * "router_topk,plan,permute,gather,gemm1_swiglu,gemm2_weighted_combine"; a
+ * "_combine" suffix marks GEMM2 with the combine, a8, fused into its epilogue).
+ * Owned by the handle, valid until its next forward / bo_route / bo_expert_ffn. */
+BO_API const char* bo_last_kernels(const bo_handle* h);
 
 BO_API const char* bo_status_string(bo_status s);
 BO_API const char* bo_last_error(void);

@@ -24,7 +24,7 @@ EXPORTED = (
     "bo_create", "bo_destroy", "bo_workspace_size", "bo_workspace_layout", "bo_build_united", "bo_set_shared_experts",
     "bo_set_brownout", "bo_get_brownout", "bo_moe_forward", "bo_moe_forward_ex", "bo_plan_from_counts",
     "bo_route", "bo_plan_counts", "bo_dispatch", "bo_block_copy", "bo_expert_ffn", "bo_combine",
-    "bo_set_profile_events", "bo_last_launch_count", "bo_status_string", "bo_last_error", "bo_version",
+    "bo_set_profile_events", "bo_last_launch_count", "bo_last_kernels", "bo_status_string", "bo_last_error", "bo_version",
     "bo_distill_workspace_layout", "bo_distill_prepare", "bo_distill_load_united", "bo_distill_step",
 )
 
@@ -47,7 +47,7 @@ class bo_ws_layout(C.Structure):
     _fields_ = [(n, C.c_size_t) for n in ("total_bytes", "logits", "topk_id", "topk_w", "tile_cnt", "tile_base",
                                           "counts", "exec_of_expert", "expert_row_off", "exec_off", "mtile_off",
                                           "stats", "row_of", "row_tok", "row_w", "xp", "h", "yp", "partial",
-                                          "tile_xcnt", "tile_xbase", "ksplit")] + \
+                                          "tile_xcnt", "tile_xbase", "ksplit", "comb_cnt")] + \
                [("T", C.c_int64), ("ntiles", C.c_int64), ("num_executors", C.c_int64)]
 
 
@@ -93,6 +93,7 @@ def _load():
         "bo_distill_load_united": ([vp, i64, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp], C.c_int),
         "bo_distill_step": ([vp, vp, i64, C.c_float, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp], C.c_int),
         "bo_last_launch_count": ([vp], i32),
+        "bo_last_kernels": ([vp], C.c_char_p),
         "bo_status_string": ([C.c_int], C.c_char_p),
         "bo_last_error": ([], C.c_char_p),
         "bo_version": ([], C.c_char_p),
@@ -231,6 +232,11 @@ class BrownoutMoE:
 
     def last_launch_count(self) -> int:
         return int(_lib.bo_last_launch_count(self._h))
+
+    def last_kernels(self) -> list:
+        """Names of the kernels the last forward launched, in launch order."""
+        names = _lib.bo_last_kernels(self._h).decode()
+        return names.split(",") if names else []
 
     def debug_arrays(self, T: int, workspace=None) -> dict:
         """Views of the workspace arrays of the last forward over T tokens."""

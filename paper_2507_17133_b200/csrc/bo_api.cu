@@ -33,6 +33,8 @@ struct bo_handle {
   int32_t router_mma;    // 1: prefill-sized bf16 batches with m <= 32 use k_router_mma (env BO_ROUTER_MMA=0 disables)
   int32_t tile_alt;      // 1: GEMM1 may pick a narrower SwiGLU tile on the device (env BO_TILE_ALT=0 disables)
   int32_t store_hint;    // 1: FFN GEMM epilogue stores hint L2 evict_first (env BO_STORE_HINT=0 disables)
+  int32_t fused_combine; // combine (a8) in GEMM2's epilogue: 0 never, 1 always, 2 auto (env BO_FUSED_COMBINE=0/1, default auto)
+  std::string last_kernels;   // comma-separated names of the kernels the last forward launched
   const void* SWg;       // shared experts (Eq. 5 second term): [N_s, f, d], [N_s, f, d], [N_s, d, f]
   const void* SWu;
   const void* SWd;
@@ -154,6 +156,7 @@ bo_status compute_layout(const bo_handle* h, int64_t T, bo_ws_layout* L) {
   L->tile_xcnt = take(c.dedup_united ? sizeof(int32_t) * ntiles * (m + G) : 0);
   L->tile_xbase = take(c.dedup_united ? sizeof(int32_t) * ntiles * (m + G) : 0);
   L->ksplit = take(sizeof(int32_t));
+  L->comb_cnt = take(sizeof(int32_t) * T * (d / gemm2_bn(static_cast<int>(d))));
   L->total_bytes = off;
   L->T = T;
   L->ntiles = ntiles;
@@ -182,7 +185,12 @@ struct Prof {
       flags = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
     }
   }
-  void mark(int i) {
+  // event i precedes launch i; `name` (forward path) is appended to the handle's kernel list
+  void mark(int i, const char* name = nullptr) {
+    if (name) {
+      if (!h->last_kernels.empty()) h->last_kernels += ",";
+      h->last_kernels += name;
+    }
     if (on && err == cudaSuccess) err = cudaEventRecordWithFlags(static_cast<cudaEvent_t>(h->prof_events[i]), s, flags);
   }
 };
@@ -202,13 +210,13 @@ bo_status route_stage(bo_handle* h, const void* x, int64_t T, const void* Wr, co
   bo_status st;
   if (logits_in) {
     tile = bo::kTileSmall;
-    prof.mark(launches);
+    prof.mark(launches, "router_topk");
     BO_CUDA(bo::launch_topk_hist(logits_in, static_cast<int>(T), m, K, tile, topk_id, topk_w, tile_cnt, s), "topk");
     ++launches;
   } else if (bo::router_small_ok(dt, m, d)) {
     // m <= 32: CUDA-core router (HBM-bound); decode-sized batches split each token over several warps
     const int tpc = h->router_split ? bo::router_split_tpc(static_cast<int>(T), h->num_sms) : 0;
-    prof.mark(launches);
+    prof.mark(launches, "router_topk");
     if (h->router_mma && bo::router_mma_ok(dt, m, d, static_cast<int>(T), h->num_sms)) {
       tile = 16;
       BO_CUDA(bo::launch_router_mma(x, Wr, static_cast<int>(T), d, m, K, logits, topk_id, topk_w, tile_cnt, s),
@@ -250,7 +258,7 @@ bo_status route_stage(bo_handle* h, const void* x, int64_t T, const void* Wr, co
     p.tile_cnt = tile_cnt;
     const int work = static_cast<int>((T + bo::kBM - 1) / bo::kBM);
     const int grid = work < h->num_sms ? work : h->num_sms;
-    prof.mark(launches);
+    prof.mark(launches, "router_topk");
     bo::BMaps mbs;
     for (int i = 0; i < 12; ++i) mbs.m[i] = mB;
     BO_CUDA(bo::launch_grouped_gemm(dt, bo::EPI_ROUTER, bn, mA, mbs, p, grid, s), "router gemm");
@@ -259,7 +267,7 @@ bo_status route_stage(bo_handle* h, const void* x, int64_t T, const void* Wr, co
   const int ntiles = static_cast<int>((T + tile - 1) / tile);
   // Alg. 1 over this batch (snapshot of the knob at enqueue time); also yields
   // cnt_i and the per-tile prefix the permutation needs.
-  prof.mark(launches);
+  prof.mark(launches, "plan");
   BO_CUDA(bo::launch_plan(tile_cnt, ntiles, m, c.way, h->ratio, h->mode, at<int32_t>(ws, L.tile_base),
                           at<int32_t>(ws, L.counts), at<int32_t>(ws, L.exec_of_expert),
                           at<int32_t>(ws, L.expert_row_off), at<int32_t>(ws, L.exec_off),
@@ -286,6 +294,30 @@ struct FfnClass {
   int64_t stack = 0;  // experts in the weight stacks (>= n; tensor-map extent)
 };
 
+// The combine (a8) fused into GEMM2's epilogue (bo::GemmParams::comb_cnt).
+struct CombFuse {
+  int32_t* cnt;            // [T, d / BN2] arrival counters (workspace)
+  const int32_t* row_of;   // [T, KR]
+  int KR;
+  int64_t T;
+  const void* x;
+  void* y;
+  int add_residual;
+};
+
+void set_comb(bo::GemmParams& p, const CombFuse* cf, int d, int nt2) {
+  if (!cf) return;
+  p.comb_cnt = cf->cnt;
+  p.row_of = cf->row_of;
+  p.comb_KR = cf->KR;
+  p.comb_T = static_cast<int>(cf->T);
+  p.comb_nt = nt2;
+  p.comb_d = d;
+  p.add_residual = cf->add_residual;
+  p.comb_x = cf->x;
+  p.comb_y = cf->y;
+}
+
 // Steps a6-a7 over rows already grouped by executor: GEMM1 + SwiGLU, GEMM2 x
 // row gate weight.  Executors are laid out originals, united, shared (Eq. 5
 // second term: every token, weight 1); the united class may have its own width.
@@ -293,7 +325,8 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
                     const int32_t* mtile_off, const FfnClass& orig, const FfnClass& uni, const FfnClass& shr,
                     void* Hbuf, void* Y, cudaStream_t s, Prof& prof, int& launches,
                     const int32_t* gather_tok = nullptr, int64_t gather_T = 0, float* partial = nullptr,
-                    int* ks_dev = nullptr) {
+                    int* ks_dev = nullptr, const CombFuse* comb = nullptr,
+                    const int32_t* comb_row_tok = nullptr) {
   // partial != nullptr: GEMM2 runs split-K into fp32 partials [<=8, R, d] (the
   // caller combines them with launch_combine_partials); Y is then unused.
   // gather_tok != nullptr: X is the token matrix x [gather_T, d] and GEMM1 gathers
@@ -375,6 +408,11 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.out = Hbuf;
     p.row_tok = gather_tok;
     p.rows_total = static_cast<int>(R);
+    {
+      int bn2 = gemm2_bn(d);
+      if (bn2 > tier) bn2 = tier;
+      set_comb(p, comb, d, d / bn2);   // GEMM1's prologue zeroes GEMM2's arrival counters
+    }
     // 256 x 256 tiles on CTA pairs when rows are plentiful (prefill); few-row
     // (decode) steps keep 128-row tiles so that more tiles share the SMs.
     const bool pair = h->cta_pairs && dt == 0 && bn == 256 && R >= 2048;
@@ -382,7 +420,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     const int64_t max_work = ((R + tile_m - 1) / tile_m + n_exec) * p.n_tiles;
     const int units = pair ? h->num_sms / 2 : h->num_sms;
     const int grid = static_cast<int>(max_work < units ? max_work : units) * (pair ? 2 : 1);
-    prof.mark(launches);
+    prof.mark(launches, "gemm1_swiglu");
     const int epi = gather ? (pair ? bo::EPI_SWIGLU_PAIR_GATHER : bo::EPI_SWIGLU_GATHER)
                            : (pair ? bo::EPI_SWIGLU_PAIR : bo::EPI_SWIGLU);
     BO_CUDA(bo::launch_grouped_gemm(dt, epi, bn, mA, mb, p, grid, s), "gemm1");
@@ -423,6 +461,11 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.out = Y;
     p.row_w = row_w;
     p.rows_total = static_cast<int>(R);
+    if (comb) {
+      set_comb(p, comb, d, d / bn);
+      p.row_tok = comb_row_tok;
+      p.store_hint = 0;   // the completing warp re-reads the token's other Yp rows: keep them in L2
+    }
     if (partial) {
       p.ksplit_max = kSplitMax;
       p.partial = partial;
@@ -432,7 +475,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     const int64_t max_work = ((R + tile_m - 1) / tile_m + n_exec) * p.n_tiles;
     const int units = pair ? h->num_sms / 2 : h->num_sms;
     const int grid = static_cast<int>(max_work < units ? max_work : units) * (pair ? 2 : 1);
-    prof.mark(launches);
+    prof.mark(launches, comb ? "gemm2_weighted_combine" : "gemm2_weighted");
     BO_CUDA(bo::launch_grouped_gemm(dt, pair ? bo::EPI_WEIGHTED_PAIR : bo::EPI_WEIGHTED, bn, mA, mb, p, grid, s),
             "gemm2");
     ++launches;
@@ -448,11 +491,14 @@ bo_status check_ws(const bo_handle* h, int64_t T, void* ws, size_t ws_bytes, bo_
   return BO_OK;
 }
 
+const char* const kDedupNames[3] = {"dedup_count", "dedup_plan", "dedup_permute"};
+
 bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, const void* Wg, const void* Wu,
                        const void* Wd, const void* UWg, const void* UWu, const void* UWd, void* y, void* ws,
                        size_t ws_bytes, const float* logits_in, void* stream) {
   if (!h) return fail(BO_ERR_INVALID_ARG, "null handle");
   h->last_launches = 0;
+  h->last_kernels.clear();
   const bo_config& c = h->cfg;
   if (T < 0 || T > c.max_tokens) return fail(BO_ERR_INVALID_ARG, "T=%lld outside [0, max_tokens=%lld]",
                                              static_cast<long long>(T), static_cast<long long>(c.max_tokens));
@@ -496,7 +542,7 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   if (c.dedup_united) {
     // f3: one row per (token, united executor); Alg. 1 above is unchanged
     for (int stage = 0; stage < 3; ++stage) {
-      prof.mark(launches);
+      prof.mark(launches, kDedupNames[stage]);
       BO_CUDA(bo::launch_dedup(stage, at<int32_t>(ws, L.topk_id), at<float>(ws, L.topk_w), static_cast<int>(T), K,
                                tile, m, E, at<int32_t>(ws, L.exec_of_expert), at<int32_t>(ws, L.tile_xcnt),
                                at<int32_t>(ws, L.tile_xbase), at<int32_t>(ws, L.exec_off),
@@ -506,7 +552,7 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
       ++launches;
     }
   } else {
-  prof.mark(launches);
+  prof.mark(launches, gather_in_permute ? "permute_gather" : "permute");
   BO_CUDA(bo::launch_permute(at<int32_t>(ws, L.topk_id), at<float>(ws, L.topk_w), static_cast<int>(T), K, m, tile,
                              at<int32_t>(ws, L.tile_base), at<int32_t>(ws, L.expert_row_off), 1, row_of,
                              at<int32_t>(ws, L.row_tok), row_w, s, dt, x,
@@ -516,7 +562,7 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   ++launches;
   }
   if (!h->fused_gather && !gather_in_permute) {
-    prof.mark(launches);
+    prof.mark(launches, "gather");
     BO_CUDA(bo::launch_gather(dt, x, static_cast<int>(T), d, KR, row_of, at<char>(ws, L.xp), h->num_sms, s), "gather");
     ++launches;
   }
@@ -528,24 +574,42 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   // decode-sized steps: optional GEMM2 split-K into fp32 partials (fills the SMs
   // when few executor tiles exist); BO_SPLITK=1 enables
   const bool split = h->splitk && Rt <= kSplitRows && !h->fused_gather;
+  // a8 fused into GEMM2's epilogue unless split-K partials need their own combine
+  // Auto: fused only where it measured faster (interleaved A/B, profiles/r01_ab_fused_combine.json):
+  // prefill-sized steps with <= 2 rows per token (C2: GEMM2 + combine -5 %); with K = 8 (C4) the
+  // completing warps' memory round trips (fence, count, 8 row loads) outrun GEMM2's short
+  // per-tile mainloop, and decode steps (< 1 wave of GEMM2 tiles) expose them at the end.
+  const bool fuse_comb = !split && KR <= 16 &&   // 16 = kCombSlots (bo_gemm.cu)
+                         (h->fused_combine == 1 || (h->fused_combine == 2 && KR <= 2 && Rt >= 2048));
+  CombFuse cf;
+  cf.cnt = at<int32_t>(ws, L.comb_cnt);
+  cf.row_of = row_of;
+  cf.KR = KR;
+  cf.T = T;
+  cf.x = x;
+  cf.y = y;
+  cf.add_residual = c.add_residual;
+  const CombFuse* cfp = fuse_comb ? &cf : nullptr;
   FfnClass orig, uni, shr;
   orig.Wg = Wg; orig.Wu = Wu; orig.Wd = Wd; orig.n = m; orig.f = f; orig.stack = m;
   uni.Wg = UWg; uni.Wu = UWu; uni.Wd = UWd; uni.n = G; uni.f = f; uni.stack = have_united ? G : m;
   if (Ns > 0) { shr.Wg = h->SWg; shr.Wu = h->SWu; shr.Wd = h->SWd; shr.n = Ns; shr.f = f; shr.stack = Ns; }
   if (h->fused_gather) {
     if ((st = ffn_stage(h, x, Rt, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), orig, uni, shr,
-                        at<char>(ws, L.h), yp, s, prof, launches, row_tok, T)) != BO_OK)
+                        at<char>(ws, L.h), yp, s, prof, launches, row_tok, T, nullptr, nullptr, cfp,
+                        row_tok)) != BO_OK)
       return st;
   } else {
     void* xp = at<char>(ws, L.xp);   // filled by the permute (small batches) or the gather kernel
     if ((st = ffn_stage(h, xp, Rt, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), orig, uni, shr,
                         at<char>(ws, L.h), yp, s, prof, launches, nullptr, 0,
-                        split ? at<float>(ws, L.partial) : nullptr, split ? at<int>(ws, L.ksplit) : nullptr)) !=
-        BO_OK)
+                        split ? at<float>(ws, L.partial) : nullptr, split ? at<int>(ws, L.ksplit) : nullptr, cfp,
+                        row_tok)) != BO_OK)
       return st;
   }
   // a8: combine (Eq. 5 sum over the token's K slots; split-K partials summed first)
-  prof.mark(launches);
+  if (!fuse_comb) {
+  prof.mark(launches, "combine");
   if (split)
     BO_CUDA(bo::launch_combine_partials(dt, at<float>(ws, L.partial), at<int>(ws, L.ksplit), Rt, x,
                                         static_cast<int>(T), d, KR, row_of, c.add_residual, y, h->num_sms, s),
@@ -554,6 +618,7 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
     BO_CUDA(bo::launch_combine(dt, yp, x, static_cast<int>(T), d, KR, row_of, c.add_residual, y, h->num_sms, s),
             "combine");
   ++launches;
+  }
   prof.mark(launches);
   if (prof.err != cudaSuccess) return cuda_fail(prof.err, "profile event record");
   h->last_launches = launches;
@@ -987,6 +1052,8 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   // evict_first on the streaming H / Yp stores keeps weight tiles in L2: C2 GEMM1 DRAM reads
   // 1.60 -> 1.47 GB, step -1.2 % (interleaved A/B, profiles/r01_ab_store_hint.json)
   h->store_hint = (sh && sh[0] == '0') ? 0 : 1;
+  const char* fc = getenv("BO_FUSED_COMBINE");
+  h->fused_combine = (fc && fc[0] == '0') ? 0 : ((fc && fc[0] == '1') ? 1 : 2);
   const char* ta = getenv("BO_TILE_ALT");
   h->tile_alt = (ta && ta[0] == '0') ? 0 : 1;
   const char* rm = getenv("BO_ROUTER_MMA");
@@ -1093,6 +1160,7 @@ bo_status bo_plan_from_counts(bo_handle* h, const int32_t* counts, int32_t* exec
 bo_status bo_route(bo_handle* h, const void* x, int64_t T, const void* Wr, const float* logits_in, void* workspace,
                    size_t ws_bytes, void* stream) {
   if (!h) return fail(BO_ERR_INVALID_ARG, "null handle");
+  h->last_kernels.clear();
   if (T < 0 || T > h->cfg.max_tokens) return fail(BO_ERR_INVALID_ARG, "T out of range");
   if (!x || (!Wr && !logits_in)) return fail(BO_ERR_INVALID_ARG, "null tensor pointer");
   bo_ws_layout L;
@@ -1166,6 +1234,7 @@ bo_status bo_expert_ffn(bo_handle* h, const void* rows, int64_t R, const float* 
                         const void* Wu, const void* Wd, const void* UWg, const void* UWu, const void* UWd,
                         void* h_buf, void* out, void* stream) {
   if (!h) return fail(BO_ERR_INVALID_ARG, "null handle");
+  h->last_kernels.clear();
   if (R == 0) return BO_OK;
   const bo_config& c = h->cfg;
   if (n_orig < 0 || n_united < 0 || n_orig + n_united > bo::kMaxExec)
@@ -1209,5 +1278,6 @@ bo_status bo_set_profile_events(bo_handle* h, void** events, int32_t n) {
 }
 
 int32_t bo_last_launch_count(const bo_handle* h) { return h ? h->last_launches : 0; }
+const char* bo_last_kernels(const bo_handle* h) { return h ? h->last_kernels.c_str() : ""; }
 
 }  // extern "C"

@@ -151,6 +151,147 @@ __device__ __forceinline__ void topk_insert(float (&tv)[KMAX], int (&ti)[KMAX], 
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
+// 16-byte vector <-> fp32 (8 bf16 or 4 fp32 elements); loads bypass L1 (rows
+// written by other CTAs of the same kernel).
+template <typename T>
+__device__ __forceinline__ void unpack16(const uint4& u, float (&f)[16 / sizeof(T)]) {
+  if constexpr (sizeof(T) == 2) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 t = __bfloat1622float2(h[i]);
+      f[2 * i] = t.x;
+      f[2 * i + 1] = t.y;
+    }
+  } else {
+    f[0] = __uint_as_float(u.x); f[1] = __uint_as_float(u.y);
+    f[2] = __uint_as_float(u.z); f[3] = __uint_as_float(u.w);
+  }
+}
+template <typename T>
+__device__ __forceinline__ void ld16_cg(const T* p, float (&f)[16 / sizeof(T)]) {
+  unpack16<T>(__ldcg(reinterpret_cast<const uint4*>(p)), f);
+}
+template <typename T>
+__device__ __forceinline__ void st16(T* p, const float (&f)[16 / sizeof(T)]) {
+  uint4 u;
+  if constexpr (sizeof(T) == 2) {
+    u.x = pack_bf16x2(f[0], f[1]); u.y = pack_bf16x2(f[2], f[3]);
+    u.z = pack_bf16x2(f[4], f[5]); u.w = pack_bf16x2(f[6], f[7]);
+  } else {
+    u = make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]), __float_as_uint(f[3]));
+  }
+  *reinterpret_cast<uint4*>(p) = u;
+}
+
+// Eq. 5 sum for token t over columns [c0, c0 + ncols) by one warp:
+// y[t] = [x[t]] + sum over the token's rows in slot order (rows < 0 skipped),
+// fp32 accumulation of the stored (rounded) Yp values - the order and
+// arithmetic of k_combine, so fused and separate combines agree bitwise.
+// The same Eq. 5 sum for every token of the warp's `done` mask over columns
+// [c0, c0 + ncols).  Lane i holds token t_lane and its row indices rr[] (slot
+// order) when bit i is set.  The warp's (token, 16-byte vector) items are
+// spread over the lanes, U items per lane at a time, the row indices arrive by
+// shuffle and all KRB row loads of the U items are issued before the in-order
+// accumulation, so a warp keeps U * KRB loads in flight (one round trip per
+// batch instead of one per token and slot).
+constexpr int kCombSlots = 16;   // max row slots per token on the fused path (host falls back above)
+template <typename T, int KRB, int U>
+__device__ __forceinline__ void combine_tokens_batched(const GemmParams& p, const T* yp, int64_t ldy, uint32_t done,
+                                                       int t_lane, const int (&rr)[kCombSlots], int c0, int ncols,
+                                                       int lane) {
+  constexpr int EV = 16 / (int)sizeof(T);
+  const int nv = ncols / EV;
+  const int nitems = __popc(done) * nv;
+  for (int base = 0; base < nitems; base += 32 * U) {
+    int src[U], vec[U], tok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int it = base + u * 32 + lane;
+      const int k = it < nitems ? it / nv : 0;
+      vec[u] = it < nitems ? it - k * nv : -1;
+      src[u] = __fns(done, 0, k + 1);
+      tok[u] = __shfl_sync(0xffffffffu, t_lane, src[u]);
+    }
+    float acc[U][EV];
+    uint4 xr[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (vec[u] >= 0 && p.add_residual)
+        xr[u] = __ldcg(reinterpret_cast<const uint4*>(reinterpret_cast<const T*>(p.comb_x) +
+                                                      static_cast<int64_t>(tok[u]) * p.comb_d + c0 + vec[u] * EV));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (vec[u] >= 0 && p.add_residual) {
+        unpack16<T>(xr[u], acc[u]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < EV; ++k) acc[u][k] = 0.0f;
+      }
+    }
+#pragma unroll
+    for (int s0 = 0; s0 < kCombSlots; s0 += KRB) {
+      if (s0 >= p.comb_KR) break;   // warp-uniform
+      int r[U][KRB];
+      uint4 raw[U][KRB];
+#pragma unroll
+      for (int j = 0; j < KRB; ++j)
+#pragma unroll
+        for (int u = 0; u < U; ++u) r[u][j] = __shfl_sync(0xffffffffu, rr[s0 + j], src[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < KRB; ++j)
+          if (vec[u] >= 0 && r[u][j] >= 0)
+            raw[u][j] = __ldcg(reinterpret_cast<const uint4*>(yp + static_cast<int64_t>(r[u][j]) * ldy + c0 +
+                                                              vec[u] * EV));
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < KRB; ++j)
+          if (vec[u] >= 0 && r[u][j] >= 0) {   // slot order (Eq. 5 sum), as k_combine
+            float f[EV];
+            unpack16<T>(raw[u][j], f);
+#pragma unroll
+            for (int k = 0; k < EV; ++k) acc[u][k] += f[k];
+          }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (vec[u] >= 0)
+        st16<T>(reinterpret_cast<T*>(p.comb_y) + static_cast<int64_t>(tok[u]) * p.comb_d + c0 + vec[u] * EV, acc[u]);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void combine_token_cols(const GemmParams& p, const T* yp, int64_t ldy, int t, int c0,
+                                                   int ncols, int lane) {
+  constexpr int EV = 16 / (int)sizeof(T);
+  const int nv = ncols / EV;
+  const int32_t* ro = p.row_of + static_cast<int64_t>(t) * p.comb_KR;
+  const T* xr = reinterpret_cast<const T*>(p.comb_x) + static_cast<int64_t>(t) * p.comb_d + c0;
+  T* yr = reinterpret_cast<T*>(p.comb_y) + static_cast<int64_t>(t) * p.comb_d + c0;
+  for (int v = lane; v < nv; v += 32) {
+    float acc[EV];
+    if (p.add_residual) {
+      ld16_cg<T>(xr + v * EV, acc);
+    } else {
+#pragma unroll
+      for (int k = 0; k < EV; ++k) acc[k] = 0.0f;
+    }
+    for (int sl = 0; sl < p.comb_KR; ++sl) {
+      const int r = __ldg(ro + sl);
+      if (r >= 0) {
+        float u[EV];
+        ld16_cg<T>(yp + static_cast<int64_t>(r) * ldy + c0 + v * EV, u);
+#pragma unroll
+        for (int k = 0; k < EV; ++k) acc[k] += u[k];
+      }
+    }
+    st16<T>(yr + v * EV, acc);
+  }
+}
+
 template <typename T, int BN, int EPI, int KMAX, int CG, bool GATHER>
 __global__ void __launch_bounds__(192, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ BMaps tmB, const GemmParams p) {
@@ -431,6 +572,25 @@ __global__ void __launch_bounds__(192, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue
+    if constexpr (EPI == EPI_SWIGLU) {
+      // Fused-combine bookkeeping for the GEMM2 that follows (while the first
+      // accumulator fills): zero the arrival counters; a token with no row
+      // (every slot dropped, full brownout) gets y = [x] here.
+      if (p.comb_cnt) {
+        const int et = threadIdx.x - 64;
+        const int64_t ncnt = static_cast<int64_t>(p.comb_T) * p.comb_nt;
+        for (int64_t i = static_cast<int64_t>(blockIdx.x) * 128 + et; i < ncnt;
+             i += static_cast<int64_t>(gridDim.x) * 128)
+          p.comb_cnt[i] = 0;
+        for (int t = blockIdx.x * 4 + (warp - 2); t < p.comb_T; t += gridDim.x * 4) {
+          bool mine = false;
+          for (int sl = lane; sl < p.comb_KR; sl += 32)
+            mine |= __ldg(p.row_of + static_cast<int64_t>(t) * p.comb_KR + sl) >= 0;
+          const bool has = __any_sync(0xffffffffu, mine);
+          if (!has) combine_token_cols<T>(p, reinterpret_cast<const T*>(p.out), 0, t, 0, p.comb_d, lane);
+        }
+      }
+    }
     const int q = warp & 3;   // TMEM lane quarter this warp may access
     const uint64_t pol_out = p.store_hint ? policy_evict_first() : 0;
     int acc = 0;
@@ -513,6 +673,42 @@ __global__ void __launch_bounds__(192, 1)
           __syncwarp();
           flush_rows32<T>(stage, lane, out + c, row0, nrows, p.ldo, 32 * (int)sizeof(T) / 16, pol_out);
           __syncwarp();
+        }
+        if (p.comb_cnt) {
+          // Fused combine (a8).  The accumulator is no longer needed: hand it back
+          // to the MMA warp first, so the count / combine below overlaps the next
+          // tile's mainloop.
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (CG == 1 || leader) mbar_arrive(&tempty_bar[acc]);
+            else mbar_arrive_remote(&tempty_bar[acc], 0);
+          }
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+          // Release this warp's Yp rows (every lane fences its own stores, then the
+          // warp barrier), count each row against its token; the warp whose
+          // arrival completes a token sums its rows for this n-tile.
+          int t = -1;
+          int need = 0;
+          int rr[kCombSlots];
+          if (valid) t = __ldg(p.row_tok + grow);
+#pragma unroll
+          for (int sl = 0; sl < kCombSlots; ++sl) {
+            rr[sl] = (valid && sl < p.comb_KR) ? __ldg(p.row_of + static_cast<int64_t>(t) * p.comb_KR + sl) : -1;
+            need += rr[sl] >= 0 ? 1 : 0;
+          }
+          __threadfence();
+          __syncwarp();
+          const bool last = valid && atomicAdd(p.comb_cnt + static_cast<int64_t>(t) * p.comb_nt + n, 1) == need - 1;
+          const uint32_t done = __ballot_sync(0xffffffffu, last);
+          if (done) {
+            __threadfence();   // acquire: the other rows' stores precede their counts
+            const T* yb = reinterpret_cast<const T*>(p.out);
+            if (p.comb_KR <= 2) combine_tokens_batched<T, 2, 4>(p, yb, p.ldo, done, t, rr, n * BN, BN, lane);
+            else if (p.comb_KR <= 4) combine_tokens_batched<T, 4, 2>(p, yb, p.ldo, done, t, rr, n * BN, BN, lane);
+            else combine_tokens_batched<T, 8, 2>(p, yb, p.ldo, done, t, rr, n * BN, BN, lane);
+          }
+          continue;
         }
       } else {
         // Router (Eq. 8) with Eq. 7 fused: this thread owns token `grow`'s m logits.

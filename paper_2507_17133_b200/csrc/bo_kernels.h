@@ -49,6 +49,21 @@ struct GemmParams {
   int store_hint;          // 1: epilogue stores carry an L2 evict_first hint (streaming H / Yp)
   int nt_alt, nt_alt_u;    // its n-tile counts (originals & shared / united); the kernel picks the width
                            // with the fewer estimated tile-column waves over the device-side plan
+  // Combine (a8, Eq. 5 sum over a token's rows) fused into GEMM2's epilogue:
+  // every GEMM2 epilogue warp that has stored its rows' Yp segment of n-tile n
+  // counts them in comb_cnt[t, n]; the warp whose arrival completes token t's
+  // rows sums them in slot order (fp32, same order as k_combine) and writes
+  // y[t, n-tile].  GEMM1 (always launched first) zeroes the counters in its
+  // prologue and writes y of tokens that have no row (full brownout).
+  int32_t* comb_cnt;        // [comb_T, comb_nt] arrival counters; nullptr: separate combine kernel
+  const int32_t* row_of;    // [comb_T, comb_KR] row of (token, slot), -1: none
+  int comb_KR;
+  int comb_T;
+  int comb_nt;              // GEMM2 n-tiles (counters per token)
+  int comb_d;               // hidden size (y / x leading dimension)
+  int add_residual;         // y = x + ... (Eq. 5 residual term)
+  const void* comb_x;       // [T, d]
+  void* comb_y;             // [T, d]
 };
 
 // Combine of split-K fp32 partials: y[t] = [x_t] + sum_slots sum_splits P[sp][row].

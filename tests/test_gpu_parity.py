@@ -383,3 +383,55 @@ def test_random_shapes_router_and_topk(cfg):
     clear = gap > 4 * 1e-3 * (1 + np.abs(Ls[:, cfg.K - 1]))
     ids = dbg["topk_id"].cpu().numpy()
     assert np.array_equal(np.sort(ids[clear], 1), np.sort(ids_ref[clear], 1))
+
+
+def _fwd_once(cfg, ratio, mode, add_residual, dedup, Ns=0, seed=7):
+    """One forward with injected logits; returns (y, kernel names)."""
+    from paper_2507_17133_b200 import BrownoutMoE
+    lay = S.make_layer(cfg)
+    uni = S.make_united_random(cfg)
+    x = S.make_tokens(cfg, batch_index=seed)
+    L = S.make_logits(cfg.T, cfg.m, seed=seed, sigma=cfg.sigma)
+    moe = BrownoutMoE(cfg.d, cfg.f, cfg.m, cfg.K, cfg.way, dtype=cfg.dtype, add_residual=add_residual,
+                      max_tokens=cfg.T, dedup=dedup, num_shared=Ns)
+    moe.set_brownout(ratio, mode)
+    g = {k: v.cuda() for k, v in lay.items()}
+    u = {k: v.cuda() for k, v in uni.items()}
+    shared = (g["SWg"], g["SWu"], g["SWd"]) if Ns else None
+    y = moe.forward(x.cuda(), g["Wr"], (g["Wg"], g["Wu"], g["Wd"]), (u["UWg"], u["UWu"], u["UWd"]),
+                    logits=L.cuda(), shared=shared)
+    torch.cuda.synchronize()
+    return y.cpu(), moe.last_kernels()
+
+
+@pytest.mark.parametrize("case", [
+    (SMALL[0], 0.5, "partial", False, False, 0),
+    (SMALL[0], 0.5, "partial", True, False, 0),
+    (SMALL[1], 1.0, "partial", True, False, 0),
+    (SMALL[2], 0.5, "partial", False, False, 0),
+    (SMALL[3], 0.5, "partial", True, False, 0),        # fp32 (tf32 MMA), 64-wide GEMM2 tiles
+    (SMALL[6], 0.5, "partial", False, False, 0),
+    (SMALL[5], 0.5, "partial", True, False, 0),         # K = 10: two 8-slot load batches
+    (SMALL[0], 0.6, "full", True, False, 0),            # dropped slots; tokens with no row at all
+    (SMALL[0], 1.0, "full", True, False, 0),            # every token dropped: y = x from GEMM1's prologue
+    (SMALL[0], 1.0, "full", False, False, 0),           # ... y = 0
+    (SMALL[2], 1.0, "partial", False, True, 0),         # de-duplicated united rows (row_of = -1 slots)
+    (S.LayerConfig("shared2", d=256, f=256, m=8, K=2, way=4, T=333, ratio=0.5, dtype="bf16", sigma=0.5,
+                   config_id=31, Ns=2), 0.5, "partial", True, False, 2),
+    (S.LayerConfig("pairs_fc", d=512, f=512, m=8, K=2, way=4, T=1500, ratio=0.5, dtype="bf16", sigma=0.5,
+                   config_id=32), 0.5, "partial", False, False, 0),   # CTA-pair GEMM2 (R >= 2048)
+], ids=lambda c: f"{c[0].name}_r{c[1]}_{c[2]}_res{int(c[3])}_dedup{int(c[4])}_ns{c[5]}")
+def test_fused_combine_bitwise_equals_separate_kernel(case, monkeypatch):
+    """a8 fused into GEMM2's epilogue (arrival counters, the completing warp sums
+    the token's rows in slot order) gives bitwise the y of the separate
+    k_combine kernel (BO_FUSED_COMBINE=0), including dropped tokens, the
+    residual, shared-expert rows and de-duplicated united rows."""
+    cfg, ratio, mode, res, dedup, Ns = case
+    monkeypatch.setenv("BO_FUSED_COMBINE", "1")
+    y_f, k_f = _fwd_once(cfg, ratio, mode, res, dedup, Ns)
+    monkeypatch.setenv("BO_FUSED_COMBINE", "0")
+    y_s, k_s = _fwd_once(cfg, ratio, mode, res, dedup, Ns)
+    assert k_f[-1] == "gemm2_weighted_combine" and "combine" not in k_f
+    assert k_s[-2:] == ["gemm2_weighted", "combine"]
+    assert torch.equal(y_f.view(torch.int16) if y_f.dtype == torch.bfloat16 else y_f.view(torch.int32),
+                       y_s.view(torch.int16) if y_s.dtype == torch.bfloat16 else y_s.view(torch.int32))
