@@ -47,7 +47,7 @@ class bo_ws_layout(C.Structure):
     _fields_ = [(n, C.c_size_t) for n in ("total_bytes", "logits", "topk_id", "topk_w", "tile_cnt", "tile_base",
                                           "counts", "exec_of_expert", "expert_row_off", "exec_off", "mtile_off",
                                           "stats", "row_of", "row_tok", "row_w", "xp", "h", "yp", "partial",
-                                          "tile_xcnt", "tile_xbase", "ksplit", "comb_cnt")] + \
+                                          "tile_xcnt", "tile_xbase", "ksplit", "comb_cnt", "sk_part", "sk_flag")] + \
                [("T", C.c_int64), ("ntiles", C.c_int64), ("num_executors", C.c_int64)]
 
 

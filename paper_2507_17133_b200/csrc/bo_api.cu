@@ -26,6 +26,13 @@ struct bo_handle {
   int64_t route_T;     // token count / tile of the last route stage (bo_route, forward)
   int32_t route_tile;
   int32_t cta_pairs;   // 1: prefill FFN GEMMs use cta_group::2 CTA pairs (env BO_GEMM_CG=1 disables)
+  int32_t stream_k;    // decode-sized FFN GEMMs (env BO_STREAMK): 0 classic tiles (default), 1 stream-K
+                       // hybrid, 2 lockstep split-K when < 1 wave of tiles.  Both options measured no faster
+                       // than the classic persistent schedule on C3 (profiles/r01_ab_stream_k.json): the
+                       // concurrently running CTAs of the classic order read the same weight / activation
+                       // tiles together, which the even k-range split gives up.
+  int32_t pair_rows1;  // GEMM1 uses CTA pairs from this many rows (env BO_PAIR_ROWS1, default 2048)
+  int32_t pair_rows2;  // GEMM2 likewise (env BO_PAIR_ROWS2, default 2048)
   int32_t fused_gather;  // 1: GEMM1 gathers x rows by TMA gather4 (env BO_GATHER=1; default off)
   int32_t splitk;        // 1: GEMM2 split-K for decode-sized steps (env BO_SPLITK=1; default off)
   int32_t decode_bn1;    // >0: GEMM1 tile width for decode-sized steps (env BO_DECODE_BN1, experiments)
@@ -157,6 +164,9 @@ bo_status compute_layout(const bo_handle* h, int64_t T, bo_ws_layout* L) {
   L->tile_xbase = take(c.dedup_united ? sizeof(int32_t) * ntiles * (m + G) : 0);
   L->ksplit = take(sizeof(int32_t));
   L->comb_cnt = take(sizeof(int32_t) * T * (d / gemm2_bn(static_cast<int>(d))));
+  const bool sk = R <= kSplitRows;   // stream-K is used for decode-sized steps only
+  L->sk_part = take(sk ? sizeof(float) * h->num_sms * bo::kBM * bo::kSkCols : 0);
+  L->sk_flag = take(sk ? sizeof(int32_t) * h->num_sms : 0);
   L->total_bytes = off;
   L->T = T;
   L->ntiles = ntiles;
@@ -326,7 +336,8 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
                     void* Hbuf, void* Y, cudaStream_t s, Prof& prof, int& launches,
                     const int32_t* gather_tok = nullptr, int64_t gather_T = 0, float* partial = nullptr,
                     int* ks_dev = nullptr, const CombFuse* comb = nullptr,
-                    const int32_t* comb_row_tok = nullptr) {
+                    const int32_t* comb_row_tok = nullptr, float* sk_part = nullptr, int* sk_flag = nullptr) {
+  // sk_part != nullptr: stream-K for the single-CTA (non-pair) GEMMs (flags zeroed by the caller)
   // partial != nullptr: GEMM2 runs split-K into fp32 partials [<=8, R, d] (the
   // caller combines them with launch_combine_partials); Y is then unused.
   // gather_tok != nullptr: X is the token matrix x [gather_T, d] and GEMM1 gathers
@@ -415,11 +426,17 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     }
     // 256 x 256 tiles on CTA pairs when rows are plentiful (prefill); few-row
     // (decode) steps keep 128-row tiles so that more tiles share the SMs.
-    const bool pair = h->cta_pairs && dt == 0 && bn == 256 && R >= 2048;
+    const bool pair = h->cta_pairs && dt == 0 && bn == 256 && R >= h->pair_rows1;
     const int tile_m = pair ? 2 * bo::kBM : bo::kBM;
     const int64_t max_work = ((R + tile_m - 1) / tile_m + n_exec) * p.n_tiles;
     const int units = pair ? h->num_sms / 2 : h->num_sms;
-    const int grid = static_cast<int>(max_work < units ? max_work : units) * (pair ? 2 : 1);
+    const bool skm = sk_part && !pair && !gather;
+    if (skm) {
+      p.stream_k = h->stream_k;
+      p.sk_part = sk_part;
+      p.sk_flag = sk_flag;
+    }
+    const int grid = skm ? h->num_sms : static_cast<int>(max_work < units ? max_work : units) * (pair ? 2 : 1);
     prof.mark(launches, "gemm1_swiglu");
     const int epi = gather ? (pair ? bo::EPI_SWIGLU_PAIR_GATHER : bo::EPI_SWIGLU_GATHER)
                            : (pair ? bo::EPI_SWIGLU_PAIR : bo::EPI_SWIGLU);
@@ -429,7 +446,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
   {
     int bn = gemm2_bn(d);
     if (bn > tier) bn = tier;
-    const bool pair = h->cta_pairs && dt == 0 && bn == 256 && R >= 2048;   // each CTA of a pair stages BN/2 of B
+    const bool pair = h->cta_pairs && dt == 0 && bn == 256 && R >= h->pair_rows2;   // each CTA of a pair stages BN/2 of B
     const uint32_t box_b = pair ? bn / 2 : bn;
     CUtensorMap mA;
     bo::BMaps mb;
@@ -474,7 +491,13 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     const int tile_m = pair ? 2 * bo::kBM : bo::kBM;
     const int64_t max_work = ((R + tile_m - 1) / tile_m + n_exec) * p.n_tiles;
     const int units = pair ? h->num_sms / 2 : h->num_sms;
-    const int grid = static_cast<int>(max_work < units ? max_work : units) * (pair ? 2 : 1);
+    const bool skm = sk_part && !pair && !partial && f_u == f;
+    if (skm) {
+      p.stream_k = h->stream_k;
+      p.sk_part = sk_part;
+      p.sk_flag = sk_flag;
+    }
+    const int grid = skm ? h->num_sms : static_cast<int>(max_work < units ? max_work : units) * (pair ? 2 : 1);
     prof.mark(launches, comb ? "gemm2_weighted_combine" : "gemm2_weighted");
     BO_CUDA(bo::launch_grouped_gemm(dt, pair ? bo::EPI_WEIGHTED_PAIR : bo::EPI_WEIGHTED, bn, mA, mb, p, grid, s),
             "gemm2");
@@ -590,6 +613,11 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   cf.y = y;
   cf.add_residual = c.add_residual;
   const CombFuse* cfp = fuse_comb ? &cf : nullptr;
+  // stream-K for decode-sized steps (the workspace holds its partial tiles then)
+  const bool use_sk = h->stream_k != 0 && Rt <= kSplitRows && !h->fused_gather;
+  float* sk_part = use_sk ? at<float>(ws, L.sk_part) : nullptr;
+  int* sk_flag = use_sk ? at<int>(ws, L.sk_flag) : nullptr;
+  if (use_sk) BO_CUDA(cudaMemsetAsync(sk_flag, 0, sizeof(int) * h->num_sms, s), "stream-K flags");
   FfnClass orig, uni, shr;
   orig.Wg = Wg; orig.Wu = Wu; orig.Wd = Wd; orig.n = m; orig.f = f; orig.stack = m;
   uni.Wg = UWg; uni.Wu = UWu; uni.Wd = UWd; uni.n = G; uni.f = f; uni.stack = have_united ? G : m;
@@ -604,7 +632,7 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
     if ((st = ffn_stage(h, xp, Rt, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), orig, uni, shr,
                         at<char>(ws, L.h), yp, s, prof, launches, nullptr, 0,
                         split ? at<float>(ws, L.partial) : nullptr, split ? at<int>(ws, L.ksplit) : nullptr, cfp,
-                        row_tok)) != BO_OK)
+                        row_tok, sk_part, sk_flag)) != BO_OK)
       return st;
   }
   // a8: combine (Eq. 5 sum over the token's K slots; split-K partials summed first)
@@ -1040,6 +1068,13 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   h->SWg = h->SWu = h->SWd = nullptr;
   const char* cg = getenv("BO_GEMM_CG");
   h->cta_pairs = (cg && cg[0] == '1') ? 0 : 1;
+  const char* skk = getenv("BO_STREAMK");
+  h->stream_k = skk ? atoi(skk) : 0;
+  if (h->stream_k < 0 || h->stream_k > 2) h->stream_k = 0;
+  const char* pr1 = getenv("BO_PAIR_ROWS1");
+  const char* pr2 = getenv("BO_PAIR_ROWS2");
+  h->pair_rows1 = pr1 ? atoi(pr1) : 2048;
+  h->pair_rows2 = pr2 ? atoi(pr2) : 2048;
   // TMA gather4 (4 rows x 128 B per instruction, 32 per k-block) measured 2.8x slower
   // than materialising Xp (r01 profiles): off unless BO_GATHER=1.
   const char* ga = getenv("BO_GATHER");

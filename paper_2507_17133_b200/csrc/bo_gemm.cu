@@ -151,6 +151,15 @@ __device__ __forceinline__ void topk_insert(float (&tv)[KMAX], int (&ti)[KMAX], 
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
+__device__ __forceinline__ void st_release_gpu(int* ptr, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(ptr), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_gpu(const int* ptr) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+  return v;
+}
+
 // 16-byte vector <-> fp32 (8 bf16 or 4 fp32 elements); loads bypass L1 (rows
 // written by other CTAs of the same kernel).
 template <typename T>
@@ -412,8 +421,11 @@ __global__ void __launch_bounds__(192, 1)
       nt_o = p.nt_alt;
       nt_u = p.nt_alt_u;
       const int items_a = start_of(nexec);
-      const long long cost_p = static_cast<long long>((items_p + n_units - 1) / n_units) * (BN + 32);
-      const long long cost_a = static_cast<long long>((items_a + n_units - 1) / n_units) * (2 * p.bh_alt + 32);
+      // stream-K spreads the k-blocks evenly: cost ~ items * width (no wave rounding)
+      const long long cost_p = static_cast<long long>(p.stream_k ? items_p : (items_p + n_units - 1) / n_units) *
+                               (BN + 32);
+      const long long cost_a = static_cast<long long>(p.stream_k ? items_a : (items_a + n_units - 1) / n_units) *
+                               (2 * p.bh_alt + 32);
       alt = cost_a < cost_p;
       if (alt) {
         bh = p.bh_alt;
@@ -433,11 +445,15 @@ __global__ void __launch_bounds__(192, 1)
   int ks = 1;
   if constexpr (EPI == EPI_WEIGHTED) {
     if (p.ksplit_max > 1 && base_work > 0) {
-      const int want = (2 * n_units + base_work - 1) / base_work;
+      // the split count with the least time per unit of work, ceil(items * ks / units) / ks
+      // (fewest splits on ties: each split adds an fp32 partial of the tile)
       const int kmin = (p.Kdim < p.Kdim_u ? p.Kdim : p.Kdim_u) / C::BK;
-      ks = want < 1 ? 1 : want;
-      if (ks > p.ksplit_max) ks = p.ksplit_max;
-      if (ks > kmin) ks = kmin;
+      const int kmax = p.ksplit_max < kmin ? p.ksplit_max : kmin;
+      long long best_num = (base_work + n_units - 1) / n_units, best_den = 1;
+      for (int k = 2; k <= kmax; ++k) {
+        const long long w = (static_cast<long long>(base_work) * k + n_units - 1) / n_units;
+        if (w * best_den < best_num * k) { best_num = w; best_den = k; ks = k; }
+      }
     }
     if (p.ksplit_max > 1 && blockIdx.x == 0 && threadIdx.x == 0) *p.ks_out = ks;
   }
@@ -466,6 +482,72 @@ __global__ void __launch_bounds__(192, 1)
     kb0 = sp * per < nkb ? sp * per : nkb;
     kb1 = kb0 + per < nkb ? kb0 + per : nkb;
   };
+  // Segments this CTA (unit) processes, in order.  Classic: work items
+  // unit, unit + n_units, ... (whole tiles or split-K ranges).  Stream-K
+  // (decode-sized steps, CG = 1, uniform reduction length), the "data-parallel +
+  // two-tile stream-K" hybrid: all but the last two waves of tiles run whole
+  // (tile w on unit w % n_units, so concurrently running CTAs still share weight
+  // and activation tiles in L2); the remaining (<= 2 waves of) tiles are cut into
+  // n_units equal contiguous ranges of their (tile, k-block) space, so every SM
+  // streams the same number of k-blocks.  A tile cut between CTAs is finished by
+  // the CTA holding its k-block 0 (the owner), which adds the fp32 partials the
+  // later CTAs left in sk_part (slot = their unit).
+  const bool stream = CG == 1 && p.stream_k == 1 && EPI != EPI_ROUTER;
+  const int kb_u = kblocks(0);
+  // Lockstep split-K (p.stream_k == 2): when the tiles fill less than one wave, each
+  // tile's reduction is cut into ks_l equal k-ranges run side by side on units
+  // tile * ks_l + sp (one item per CTA, every split of every tile concurrently,
+  // so CTAs reading the same weight / activation tile do it together); split 0
+  // owns the tile and adds the other splits' fp32 partials (slot = their unit).
+  int ks_l = 1;
+  if (CG == 1 && p.stream_k == 2 && EPI != EPI_ROUTER && ks == 1 && base_work > 0)
+    for (int k = 2; k <= 8 && k <= kb_u && base_work * k <= n_units; ++k) ks_l = k;
+  const bool lock = ks_l > 1;
+  const int waves = (base_work + n_units - 1) / n_units;
+  const int dp_tiles = stream ? (waves > 2 ? (waves - 2) * n_units : 0) : 0;
+  const long long dp_cnt = stream ? (dp_tiles > unit ? (dp_tiles - unit + n_units - 1) / n_units : 0) : 0;
+  const long long tu = stream ? static_cast<long long>(base_work - dp_tiles) * kb_u : 0;   // stream-K units
+  const long long su_lo = stream ? tu * unit / n_units : 0;
+  const long long su_hi = stream ? tu * (unit + 1) / n_units : 0;
+  long long sk_pos = 0;   // stream-K position of the current segment (set by seg_at)
+  auto seg_at = [&](long long cur, int& x, int& mi, int& n, int& sp, int& kb0, int& kb1) -> bool {
+    if (lock) {
+      if (cur != 0 || unit >= base_work * ks_l) return false;
+      decode(unit / ks_l, x, mi, n);
+      sp = unit % ks_l;
+      kb0 = sp * kb_u / ks_l;
+      kb1 = (sp + 1) * kb_u / ks_l;
+      return true;
+    }
+    if (!stream) {
+      if (cur >= total_work) return false;
+      decode_k(static_cast<int>(cur), x, mi, n, sp, kb0, kb1);
+      return true;
+    }
+    sp = 0;
+    if (cur < dp_cnt) {   // whole tile of the data-parallel waves
+      decode(static_cast<int>(unit + cur * n_units), x, mi, n);
+      kb0 = 0;
+      kb1 = kb_u;
+      return true;
+    }
+    sk_pos = su_lo + (cur - dp_cnt);
+    if (sk_pos >= su_hi) return false;
+    const long long tile = sk_pos / kb_u;
+    kb0 = static_cast<int>(sk_pos - tile * kb_u);
+    const long long end = su_hi < (tile + 1) * kb_u ? su_hi : (tile + 1) * kb_u;
+    kb1 = static_cast<int>(end - tile * kb_u);
+    decode(dp_tiles + static_cast<int>(tile), x, mi, n);
+    return true;
+  };
+  auto seg_next = [&](long long cur, int kb0, int kb1) -> long long {
+    return lock ? cur + 1 : (stream ? (cur < dp_cnt ? cur + 1 : cur + (kb1 - kb0)) : cur + n_units);
+  };
+  const long long seg0 = (stream || lock) ? 0 : unit;
+  // stream-K: the unit whose range holds stream-K position u, and whether unit c
+  // holds any position (empty ranges when the stream-K tiles * k-blocks < grid)
+  auto unit_of = [&](long long u) -> int { return static_cast<int>(((u + 1) * n_units - 1) / tu); };
+  auto unit_busy = [&](int c) -> bool { return lock || tu * c / n_units != tu * (c + 1) / n_units; };
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -474,9 +556,8 @@ __global__ void __launch_bounds__(192, 1)
       const uint64_t pol_b = policy_evict_normal(); // weight tile is re-read by the executor's other m-tiles
       int stage = 0;
       uint32_t phase = 0;
-      for (int w = unit; w < total_work; w += n_units) {
-        int x, mi, n, sp, kb0, kb1;
-        decode_k(w, x, mi, n, sp, kb0, kb1);
+      int x, mi, n, sp, kb0, kb1;
+      for (long long cur = seg0; seg_at(cur, x, mi, n, sp, kb0, kb1); cur = seg_next(cur, kb0, kb1)) {
         const int arow = (p.a_shared ? 0 : s_eoff[x]) + mi * TILE_M + static_cast<int>(crank) * kBM;
         const int cls = x < mo ? 0 : (x < mu ? 1 : 2);      // original / united / shared
         const CUtensorMap* mb0 = &tmB.m[(alt ? 6 : 0) + 2 * cls];
@@ -534,9 +615,8 @@ __global__ void __launch_bounds__(192, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int w = unit; w < total_work; w += n_units) {
-        int x, mi, n, sp, kb0, kb1;
-        decode_k(w, x, mi, n, sp, kb0, kb1);
+      int x, mi, n, sp, kb0, kb1;
+      for (long long cur = seg0; seg_at(cur, x, mi, n, sp, kb0, kb1); cur = seg_next(cur, kb0, kb1)) {
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
@@ -595,9 +675,8 @@ __global__ void __launch_bounds__(192, 1)
     const uint64_t pol_out = p.store_hint ? policy_evict_first() : 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int w = unit; w < total_work; w += n_units) {
-      int x, mi, n, sp, kb0, kb1;
-      decode_k(w, x, mi, n, sp, kb0, kb1);
+    int x, mi, n, sp, kb0, kb1;
+    for (long long cur = seg0; seg_at(cur, x, mi, n, sp, kb0, kb1); cur = seg_next(cur, kb0, kb1)) {
       const int rows_x = s_eoff[x + 1] - s_eoff[x];
       const int r_local = mi * TILE_M + static_cast<int>(crank) * kBM + q * 32 + lane;
       const bool valid = r_local < rows_x;
@@ -605,6 +684,63 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t t0 = tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(q * 32) << 16);
+      if ((stream || lock) && kb0 > 0) {
+        // stream-K contributor: this tile's k-blocks [kb0, kb1) as an fp32 partial in
+        // slot `unit` (TMEM column order), then publish it (every thread fences its
+        // stores, the epilogue barrier, one release store of the flag)
+        float* dst = p.sk_part + (static_cast<int64_t>(unit) * kBM + q * 32 + lane) * kSkCols;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t a[32];
+          tmem_ld32(t0 + c, a);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            __stcg(reinterpret_cast<float4*>(dst + c) + j,
+                   make_float4(__uint_as_float(a[4 * j]), __uint_as_float(a[4 * j + 1]),
+                               __uint_as_float(a[4 * j + 2]), __uint_as_float(a[4 * j + 3])));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty_bar[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        __threadfence();
+        epi_bar();
+        if (threadIdx.x == 64) st_release_gpu(p.sk_flag + unit, 1);
+        continue;
+      }
+      // stream-K owner of a tile cut between CTAs: wait for the partials of units
+      // c_first..c_last (the later CTAs whose ranges hold the rest of its k-blocks)
+      int c_first = 0, c_last = -1;
+      if ((stream || lock) && kb1 < kb_u) {   // (only stream-K segments are cut: sk_pos is this segment's)
+        c_first = unit + 1;
+        c_last = lock ? unit + ks_l - 1 : unit_of((sk_pos / kb_u + 1) * kb_u - 1);
+        for (int cc = c_first; cc <= c_last; ++cc)
+          if (unit_busy(cc))
+            while (ld_acquire_gpu(p.sk_flag + cc) == 0) {
+            }
+        epi_bar();   // every epilogue warp has seen the flags: reset them for the next launch
+        if (threadIdx.x == 64)
+          for (int cc = c_first; cc <= c_last; ++cc) p.sk_flag[cc] = 0;
+      }
+      // accumulator columns [col, col + 32) of this thread's row += the partials, in unit order
+      auto add_part = [&](uint32_t (&v)[32], int col) {
+        for (int cc = c_first; cc <= c_last; ++cc) {
+          if (!unit_busy(cc)) continue;
+          const float4* src = reinterpret_cast<const float4*>(
+              p.sk_part + (static_cast<int64_t>(cc) * kBM + q * 32 + lane) * kSkCols + col);
+          float4 f[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) f[j] = __ldcg(src + j);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            v[4 * j] = __float_as_uint(__uint_as_float(v[4 * j]) + f[j].x);
+            v[4 * j + 1] = __float_as_uint(__uint_as_float(v[4 * j + 1]) + f[j].y);
+            v[4 * j + 2] = __float_as_uint(__uint_as_float(v[4 * j + 2]) + f[j].z);
+            v[4 * j + 3] = __float_as_uint(__uint_as_float(v[4 * j + 3]) + f[j].w);
+          }
+        }
+      };
       // rows of this warp's 32-row slab that belong to the executor
       const int slab = mi * TILE_M + static_cast<int>(crank) * kBM + q * 32;
       const int nrows = rows_x - slab < 0 ? 0 : (rows_x - slab > 32 ? 32 : rows_x - slab);
@@ -620,6 +756,10 @@ __global__ void __launch_bounds__(192, 1)
           tmem_ld32(t0 + c, g);
           tmem_ld32(t0 + bh + c, u);
           tmem_ld_wait();
+          if (c_last >= c_first) {
+            add_part(g, c);
+            add_part(u, bh + c);
+          }
           float h[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) h[i] = silu_f(__uint_as_float(g[i])) * __uint_as_float(u[i]);
@@ -666,6 +806,7 @@ __global__ void __launch_bounds__(192, 1)
           uint32_t a[32];
           tmem_ld32(t0 + c, a);
           tmem_ld_wait();
+          if (c_last >= c_first) add_part(a, c);
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(a[i]) * wr;

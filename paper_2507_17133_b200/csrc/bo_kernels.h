@@ -11,6 +11,7 @@ constexpr int kTileTok = 128;   // token tile of the tcgen05 router (= GEMM BM)
 constexpr int kBM = 128;        // rows per GEMM tile (TMEM lanes)
 constexpr int kMaxExperts = 256;
 constexpr int kMaxExec = 512;   // m + G
+constexpr int kSkCols = 256;    // stream-K partial tile row stride (fp32 columns >= any BN)
 
 enum Epi : int { EPI_SWIGLU = 0, EPI_WEIGHTED = 1, EPI_ROUTER = 2,
                  EPI_SWIGLU_PAIR = 3, EPI_WEIGHTED_PAIR = 4,    // *_PAIR: cta_group::2, grid even
@@ -64,6 +65,11 @@ struct GemmParams {
   int add_residual;         // y = x + ... (Eq. 5 residual term)
   const void* comb_x;       // [T, d]
   void* comb_y;             // [T, d]
+  // Stream-K (CG = 1): the (tile, k-block) space split evenly over the grid; tiles cut
+  // between CTAs are finished by their k-block-0 owner from fp32 partials.
+  int stream_k;             // 1: enabled (grid must be resident: <= #SM, 1 CTA / SM)
+  float* sk_part;           // [grid, 128, kSkCols] partial of each contributing CTA
+  int* sk_flag;             // [grid] 1 = partial published (reset to 0 by the owner; zero before first use)
 };
 
 // Combine of split-K fp32 partials: y[t] = [x_t] + sum_slots sum_splits P[sp][row].

@@ -285,8 +285,11 @@ def test_plan_random_counts_bitexact():
         assert np.array_equal(out["exec_off"].cpu().numpy(), perm.exec_off)
 
 
-@pytest.mark.parametrize("env", [{"BO_GATHER": "1"}, {"BO_GEMM_CG": "1"}, {"BO_SPLITK": "1"}, {"BO_TILE_ALT": "0"}],
-                         ids=["gather4_gemm1", "single_cta_gemm", "splitk_gemm2", "no_tile_alt"])
+@pytest.mark.parametrize("env", [{"BO_GATHER": "1"}, {"BO_GEMM_CG": "1"}, {"BO_SPLITK": "1"}, {"BO_TILE_ALT": "0"},
+                                 {"BO_STREAMK": "2"}, {"BO_STREAMK": "1"}, {"BO_PAIR_ROWS1": "1", "BO_PAIR_ROWS2": "1"},
+                                 {"BO_PAIR_ROWS2": "1", "BO_SPLITK": "1"}],
+                         ids=["gather4_gemm1", "single_cta_gemm", "splitk_gemm2", "no_tile_alt", "lockstep_splitk", "stream_k_hybrid",
+                              "pairs_always", "pairs_splitk_gemm2"])
 @pytest.mark.parametrize("cfg", [SMALL[0], SMALL[2], SMALL[3], SMALL[7],
                                  S.LayerConfig("pairs_bf16", d=256, f=512, m=8, K=2, way=4, T=1500, ratio=0.5,
                                                dtype="bf16", sigma=0.5, config_id=21)], ids=lambda c: c.name)
