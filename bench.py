@@ -412,7 +412,7 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-tokens", type=int, default=32)
+    ap.add_argument("--cpu-tokens", type=int, default=256)
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of one CUDA-graph replay")
     args = ap.parse_args()
 
