@@ -31,6 +31,7 @@ struct bo_handle {
                        // than the classic persistent schedule on C3 (profiles/r01_ab_stream_k.json): the
                        // concurrently running CTAs of the classic order read the same weight / activation
                        // tiles together, which the even k-range split gives up.
+  int32_t decode_pair2; // 1: decode steps with >= 256 rows per executor: GEMM2 pairs + split-K (env BO_DECODE_PAIR2=0 disables)
   int32_t pair_rows1;  // GEMM1 uses CTA pairs from this many rows (env BO_PAIR_ROWS1, default 2048)
   int32_t pair_rows2;  // GEMM2 likewise (env BO_PAIR_ROWS2, default 2048)
   int32_t fused_gather;  // 1: GEMM1 gathers x rows by TMA gather4 (env BO_GATHER=1; default off)
@@ -336,7 +337,8 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
                     void* Hbuf, void* Y, cudaStream_t s, Prof& prof, int& launches,
                     const int32_t* gather_tok = nullptr, int64_t gather_T = 0, float* partial = nullptr,
                     int* ks_dev = nullptr, const CombFuse* comb = nullptr,
-                    const int32_t* comb_row_tok = nullptr, float* sk_part = nullptr, int* sk_flag = nullptr) {
+                    const int32_t* comb_row_tok = nullptr, float* sk_part = nullptr, int* sk_flag = nullptr,
+                    bool force_pair2 = false) {
   // sk_part != nullptr: stream-K for the single-CTA (non-pair) GEMMs (flags zeroed by the caller)
   // partial != nullptr: GEMM2 runs split-K into fp32 partials [<=8, R, d] (the
   // caller combines them with launch_combine_partials); Y is then unused.
@@ -446,7 +448,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
   {
     int bn = gemm2_bn(d);
     if (bn > tier) bn = tier;
-    const bool pair = h->cta_pairs && dt == 0 && bn == 256 && R >= h->pair_rows2;   // each CTA of a pair stages BN/2 of B
+    const bool pair = h->cta_pairs && dt == 0 && bn == 256 && (R >= h->pair_rows2 || force_pair2);   // each CTA of a pair stages BN/2 of B
     const uint32_t box_b = pair ? bn / 2 : bn;
     CUtensorMap mA;
     bo::BMaps mb;
@@ -596,7 +598,16 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   const int32_t* row_tok = at<int32_t>(ws, L.row_tok);
   // decode-sized steps: optional GEMM2 split-K into fp32 partials (fills the SMs
   // when few executor tiles exist); BO_SPLITK=1 enables
-  const bool split = h->splitk && Rt <= kSplitRows && !h->fused_gather;
+  // Decode-sized steps whose executors hold >= 256 rows each (brownout ratio near 1: the
+  // G united experts take almost every row; estimate (1 - ratio) m + ratio G executors):
+  // GEMM2 on CTA pairs (one 256-row tile per executor instead of two 128-row tiles reading
+  // the same weights) with split-K partials to fill the SMs.  C3 ratio 1: GEMM2
+  // 0.101 -> 0.071 ms (profiles/r01_ab_decode_pairs_splitk.json); a loss at ratios 0 / 0.5.
+  const double est_exec = (1.0 - h->ratio) * m + h->ratio * G;
+  const bool decode_pair2 = h->decode_pair2 && h->cta_pairs && dt == 0 && Rt <= kSplitRows &&
+                            !h->fused_gather && h->mode == BO_PARTIAL && Ns == 0 &&
+                            static_cast<double>(Rt) >= 256.0 * (est_exec < 1.0 ? 1.0 : est_exec);
+  const bool split = (h->splitk || decode_pair2) && Rt <= kSplitRows && !h->fused_gather;
   // a8 fused into GEMM2's epilogue unless split-K partials need their own combine
   // Auto: fused only where it measured faster (interleaved A/B, profiles/r01_ab_fused_combine.json):
   // prefill-sized steps with <= 2 rows per token (C2: GEMM2 + combine -5 %); with K = 8 (C4) the
@@ -632,7 +643,7 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
     if ((st = ffn_stage(h, xp, Rt, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), orig, uni, shr,
                         at<char>(ws, L.h), yp, s, prof, launches, nullptr, 0,
                         split ? at<float>(ws, L.partial) : nullptr, split ? at<int>(ws, L.ksplit) : nullptr, cfp,
-                        row_tok, sk_part, sk_flag)) != BO_OK)
+                        row_tok, sk_part, sk_flag, decode_pair2)) != BO_OK)
       return st;
   }
   // a8: combine (Eq. 5 sum over the token's K slots; split-K partials summed first)
@@ -1071,6 +1082,8 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   const char* skk = getenv("BO_STREAMK");
   h->stream_k = skk ? atoi(skk) : 0;
   if (h->stream_k < 0 || h->stream_k > 2) h->stream_k = 0;
+  const char* dp2 = getenv("BO_DECODE_PAIR2");
+  h->decode_pair2 = (dp2 && dp2[0] == '0') ? 0 : 1;
   const char* pr1 = getenv("BO_PAIR_ROWS1");
   const char* pr2 = getenv("BO_PAIR_ROWS2");
   h->pair_rows1 = pr1 ? atoi(pr1) : 2048;

@@ -321,7 +321,10 @@ __global__ void __launch_bounds__(192, 1)
   constexpr int TILE_M = kBM * CG;
 
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned (SWIZZLE_128B atoms); offset arithmetic on the __shared__
+  // array keeps the shared address space visible to the compiler (LDS/STS for the
+  // epilogue staging instead of generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE_BYTES);
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* tfull_bar = empty_bar + STAGES;
