@@ -329,7 +329,8 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* tfull_bar = empty_bar + STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* fix_bar = tempty_bar + 2;   // split-tile fix-up: contributor partial landed in shared memory
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 3);
   int* s_hist = reinterpret_cast<int*>(smem + STAGES * C::STAGE_BYTES + 1024);
   int* s_mtile = reinterpret_cast<int*>(smem + STAGES * C::STAGE_BYTES + C::BAR_BYTES);
   int* s_eoff = s_mtile + (kMaxExec + 1);
@@ -351,6 +352,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], 4 * CG);   // pair: epilogue warps of both CTAs arrive on the leader's
     }
+    mbar_init(fix_bar, 1);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -424,11 +426,21 @@ __global__ void __launch_bounds__(192, 1)
       nt_o = p.nt_alt;
       nt_u = p.nt_alt_u;
       const int items_a = start_of(nexec);
-      // stream-K spreads the k-blocks evenly: cost ~ items * width (no wave rounding)
-      const long long cost_p = static_cast<long long>(p.stream_k ? items_p : (items_p + n_units - 1) / n_units) *
-                               (BN + 32);
-      const long long cost_a = static_cast<long long>(p.stream_k ? items_a : (items_a + n_units - 1) / n_units) *
-                               (2 * p.bh_alt + 32);
+      // waves x width; stream-K spreads the k-blocks evenly (no wave rounding), the
+      // lockstep tail split shortens the last partial wave by its split count
+      auto wave_cost = [&](int items) -> long long {
+        if (p.stream_k == 1) return 8LL * items;
+        const int full = items / n_units, r = items - full * n_units;
+        if (r == 0) return 8LL * full;
+        if (p.stream_k != 2) return 8LL * (full + 1);
+        int k = n_units / r;
+        k = k > 4 ? 4 : k;
+        const int kbm = p.Kdim / C::BK;
+        k = k > kbm ? kbm : k;
+        return 8LL * full + 8 / (k < 1 ? 1 : k);
+      };
+      const long long cost_p = wave_cost(items_p) * (BN + 32);
+      const long long cost_a = wave_cost(items_a) * (2 * p.bh_alt + 32);
       alt = cost_a < cost_p;
       if (alt) {
         bh = p.bh_alt;
@@ -497,15 +509,20 @@ __global__ void __launch_bounds__(192, 1)
   // later CTAs left in sk_part (slot = their unit).
   const bool stream = CG == 1 && p.stream_k == 1 && EPI != EPI_ROUTER;
   const int kb_u = kblocks(0);
-  // Lockstep split-K (p.stream_k == 2): when the tiles fill less than one wave, each
-  // tile's reduction is cut into ks_l equal k-ranges run side by side on units
-  // tile * ks_l + sp (one item per CTA, every split of every tile concurrently,
-  // so CTAs reading the same weight / activation tile do it together); split 0
-  // owns the tile and adds the other splits' fp32 partials (slot = their unit).
+  // Lockstep tail split-K (p.stream_k == 2): the complete waves of tiles run whole
+  // (tile w on unit w % n_units); the r tiles of the last, partial wave have their
+  // reduction cut into ks_l equal k-ranges run side by side on units
+  // tile * ks_l + sp (every split of every tail tile concurrently, so CTAs reading
+  // the same weight / activation tile do it together); split 0 owns the tile and
+  // adds the other splits' fp32 partials (slot = their unit: a CTA contributes at
+  // most once, in the tail).
+  const int full_tiles = (base_work / n_units) * n_units;
+  const int tail = base_work - full_tiles;
   int ks_l = 1;
-  if (CG == 1 && p.stream_k == 2 && EPI != EPI_ROUTER && ks == 1 && base_work > 0)
-    for (int k = 2; k <= 8 && k <= kb_u && base_work * k <= n_units; ++k) ks_l = k;
+  if (CG == 1 && p.stream_k == 2 && EPI != EPI_ROUTER && ks == 1 && tail > 0)
+    for (int k = 2; k <= 4 && k <= kb_u && tail * k <= n_units; ++k) ks_l = k;
   const bool lock = ks_l > 1;
+  const long long dpl = lock ? full_tiles / n_units : 0;   // whole tiles per unit before the tail
   const int waves = (base_work + n_units - 1) / n_units;
   const int dp_tiles = stream ? (waves > 2 ? (waves - 2) * n_units : 0) : 0;
   const long long dp_cnt = stream ? (dp_tiles > unit ? (dp_tiles - unit + n_units - 1) / n_units : 0) : 0;
@@ -515,8 +532,15 @@ __global__ void __launch_bounds__(192, 1)
   long long sk_pos = 0;   // stream-K position of the current segment (set by seg_at)
   auto seg_at = [&](long long cur, int& x, int& mi, int& n, int& sp, int& kb0, int& kb1) -> bool {
     if (lock) {
-      if (cur != 0 || unit >= base_work * ks_l) return false;
-      decode(unit / ks_l, x, mi, n);
+      if (cur < dpl) {   // whole tile of a complete wave
+        decode(static_cast<int>(unit + cur * n_units), x, mi, n);
+        sp = 0;
+        kb0 = 0;
+        kb1 = kb_u;
+        return true;
+      }
+      if (cur != dpl || unit >= tail * ks_l) return false;
+      decode(full_tiles + unit / ks_l, x, mi, n);
       sp = unit % ks_l;
       kb0 = sp * kb_u / ks_l;
       kb1 = (sp + 1) * kb_u / ks_l;
@@ -679,6 +703,7 @@ __global__ void __launch_bounds__(192, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     int x, mi, n, sp, kb0, kb1;
+    uint32_t fix_phase = 0;
     for (long long cur = seg0; seg_at(cur, x, mi, n, sp, kb0, kb1); cur = seg_next(cur, kb0, kb1)) {
       const int rows_x = s_eoff[x + 1] - s_eoff[x];
       const int r_local = mi * TILE_M + static_cast<int>(crank) * kBM + q * 32 + lane;
@@ -691,7 +716,10 @@ __global__ void __launch_bounds__(192, 1)
         // stream-K contributor: this tile's k-blocks [kb0, kb1) as an fp32 partial in
         // slot `unit` (TMEM column order), then publish it (every thread fences its
         // stores, the epilogue barrier, one release store of the flag)
-        float* dst = p.sk_part + (static_cast<int64_t>(unit) * kBM + q * 32 + lane) * kSkCols;
+        // layout [column quad][128 rows] of float4: a warp's stores are 512 contiguous
+        // bytes, and the owner's fix-up reads it back from shared memory conflict-free
+        float4* dst = reinterpret_cast<float4*>(p.sk_part + static_cast<int64_t>(unit) * kBM * kSkCols) +
+                      (q * 32 + lane);
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           uint32_t a[32];
@@ -699,7 +727,7 @@ __global__ void __launch_bounds__(192, 1)
           tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < 8; ++j)
-            __stcg(reinterpret_cast<float4*>(dst + c) + j,
+            __stcg(dst + (c / 4 + j) * kBM,
                    make_float4(__uint_as_float(a[4 * j]), __uint_as_float(a[4 * j + 1]),
                                __uint_as_float(a[4 * j + 2]), __uint_as_float(a[4 * j + 3])));
         }
@@ -712,38 +740,48 @@ __global__ void __launch_bounds__(192, 1)
         if (threadIdx.x == 64) st_release_gpu(p.sk_flag + unit, 1);
         continue;
       }
-      // stream-K owner of a tile cut between CTAs: wait for the partials of units
-      // c_first..c_last (the later CTAs whose ranges hold the rest of its k-blocks)
-      int c_first = 0, c_last = -1;
+      // Owner of a tile cut between CTAs (stream-K / lockstep split): this is the CTA's
+      // last segment, so its MMAs are done and the stage ring is free.  For each
+      // contributing unit in order: wait for its flag, bulk-copy its partial tile into
+      // the ring (one TMA transfer), TMEM accumulator += partial, then the epilogue
+      // below reads the finished sum.
       if ((stream || lock) && kb1 < kb_u) {   // (only stream-K segments are cut: sk_pos is this segment's)
-        c_first = unit + 1;
-        c_last = lock ? unit + ks_l - 1 : unit_of((sk_pos / kb_u + 1) * kb_u - 1);
-        for (int cc = c_first; cc <= c_last; ++cc)
-          if (unit_busy(cc))
-            while (ld_acquire_gpu(p.sk_flag + cc) == 0) {
-            }
-        epi_bar();   // every epilogue warp has seen the flags: reset them for the next launch
-        if (threadIdx.x == 64)
-          for (int cc = c_first; cc <= c_last; ++cc) p.sk_flag[cc] = 0;
-      }
-      // accumulator columns [col, col + 32) of this thread's row += the partials, in unit order
-      auto add_part = [&](uint32_t (&v)[32], int col) {
+        const int c_first = unit + 1;
+        const int c_last = lock ? unit + ks_l - 1 : unit_of((sk_pos / kb_u + 1) * kb_u - 1);
+        const uint32_t bytes = static_cast<uint32_t>(kBM) * BN * 4;
+        const float4* fbuf = reinterpret_cast<const float4*>(smem) + (q * 32 + lane);
         for (int cc = c_first; cc <= c_last; ++cc) {
           if (!unit_busy(cc)) continue;
-          const float4* src = reinterpret_cast<const float4*>(
-              p.sk_part + (static_cast<int64_t>(cc) * kBM + q * 32 + lane) * kSkCols + col);
-          float4 f[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) f[j] = __ldcg(src + j);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            v[4 * j] = __float_as_uint(__uint_as_float(v[4 * j]) + f[j].x);
-            v[4 * j + 1] = __float_as_uint(__uint_as_float(v[4 * j + 1]) + f[j].y);
-            v[4 * j + 2] = __float_as_uint(__uint_as_float(v[4 * j + 2]) + f[j].z);
-            v[4 * j + 3] = __float_as_uint(__uint_as_float(v[4 * j + 3]) + f[j].w);
+          if (threadIdx.x == 64) {
+            while (ld_acquire_gpu(p.sk_flag + cc) == 0) {
+            }
+            p.sk_flag[cc] = 0;   // consumed (the next launch starts from zero)
+            fence_proxy_async_global();   // generic-proxy partial -> async-proxy bulk read
+            fence_proxy_async_smem();     // earlier generic reads of the ring -> async-proxy write
+            mbar_arrive_expect_tx(fix_bar, bytes);
+            bulk_g2s(smem, p.sk_part + static_cast<int64_t>(cc) * kBM * kSkCols, bytes, fix_bar);
           }
+          mbar_wait(fix_bar, fix_phase);
+          fix_phase ^= 1;
+#pragma unroll 1
+          for (int c = 0; c < BN; c += 32) {
+            uint32_t a[32];
+            tmem_ld32(t0 + c, a);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 f = fbuf[(c / 4 + j) * kBM];
+              a[4 * j] = __float_as_uint(__uint_as_float(a[4 * j]) + f.x);
+              a[4 * j + 1] = __float_as_uint(__uint_as_float(a[4 * j + 1]) + f.y);
+              a[4 * j + 2] = __float_as_uint(__uint_as_float(a[4 * j + 2]) + f.z);
+              a[4 * j + 3] = __float_as_uint(__uint_as_float(a[4 * j + 3]) + f.w);
+            }
+            tmem_st32(t0 + c, a);
+          }
+          tmem_st_wait();
+          epi_bar();   // the ring is read by every epilogue thread before the next copy lands
         }
-      };
+      }
       // rows of this warp's 32-row slab that belong to the executor
       const int slab = mi * TILE_M + static_cast<int>(crank) * kBM + q * 32;
       const int nrows = rows_x - slab < 0 ? 0 : (rows_x - slab > 32 ? 32 : rows_x - slab);
@@ -759,10 +797,6 @@ __global__ void __launch_bounds__(192, 1)
           tmem_ld32(t0 + c, g);
           tmem_ld32(t0 + bh + c, u);
           tmem_ld_wait();
-          if (c_last >= c_first) {
-            add_part(g, c);
-            add_part(u, bh + c);
-          }
           float h[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) h[i] = silu_f(__uint_as_float(g[i])) * __uint_as_float(u[i]);
@@ -809,7 +843,6 @@ __global__ void __launch_bounds__(192, 1)
           uint32_t a[32];
           tmem_ld32(t0 + c, a);
           tmem_ld_wait();
-          if (c_last >= c_first) add_part(a, c);
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(a[i]) * wr;
