@@ -32,6 +32,7 @@ struct bo_handle {
                        // concurrently running CTAs of the classic order read the same weight / activation
                        // tiles together, which the even k-range split gives up.
   int32_t decode_pair2; // 1: decode steps with >= 256 rows per executor: GEMM2 pairs + split-K (env BO_DECODE_PAIR2=0 disables)
+  int32_t pf_dist;      // L2 prefetch distance (k-blocks) of the FFN GEMMs' B tiles (env BO_PF_DIST)
   int32_t pair_rows1;  // GEMM1 uses CTA pairs from this many rows (env BO_PAIR_ROWS1, default 2048)
   int32_t pair_rows2;  // GEMM2 likewise (env BO_PAIR_ROWS2, default 2048)
   int32_t fused_gather;  // 1: GEMM1 gathers x rows by TMA gather4 (env BO_GATHER=1; default off)
@@ -413,6 +414,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.m_orig = orig.n;
     p.m_united = uni.n;
     p.store_hint = h->store_hint;
+    p.pf_dist = h->pf_dist;
     p.b_rows_per_exec = f;
     p.num_exec = n_exec;
     p.single_rows = -1;
@@ -472,6 +474,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.m_orig = orig.n;
     p.m_united = uni.n;
     p.store_hint = h->store_hint;
+    p.pf_dist = h->pf_dist;
     p.b_rows_per_exec = d;
     p.num_exec = n_exec;
     p.single_rows = -1;
@@ -1084,6 +1087,8 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   if (h->stream_k < 0 || h->stream_k > 2) h->stream_k = 0;
   const char* dp2 = getenv("BO_DECODE_PAIR2");
   h->decode_pair2 = (dp2 && dp2[0] == '0') ? 0 : 1;
+  const char* pfd = getenv("BO_PF_DIST");
+  h->pf_dist = pfd ? atoi(pfd) : 0;
   const char* pr1 = getenv("BO_PAIR_ROWS1");
   const char* pr2 = getenv("BO_PAIR_ROWS2");
   h->pair_rows1 = pr1 ? atoi(pr1) : 2048;

@@ -576,6 +576,21 @@ __global__ void __launch_bounds__(192, 1)
   auto unit_of = [&](long long u) -> int { return static_cast<int>(((u + 1) * n_units - 1) / tu); };
   auto unit_busy = [&](int c) -> bool { return lock || tu * c / n_units != tu * (c + 1) / n_units; };
 
+  // L2 prefetch of k-block kq of the B tile(s) the producer will load (CTA-pair
+  // mode: this CTA's half)
+  auto prefetch_b = [&](const CUtensorMap* mb0, const CUtensorMap* mb1, int kq, int brow, int n) {
+    if constexpr (EPI == EPI_SWIGLU) {
+      if constexpr (CG == 1) {
+        tma_prefetch_l2_2d(mb0, kq * C::BK, brow + n * bh);
+        tma_prefetch_l2_2d(mb1, kq * C::BK, brow + n * bh);
+      } else {
+        tma_prefetch_l2_2d(crank == 0 ? mb0 : mb1, kq * C::BK, brow + n * bh);
+      }
+    } else {
+      tma_prefetch_l2_2d(mb0, kq * C::BK, brow + n * BN + (CG == 2 ? static_cast<int>(crank) * (BN / 2) : 0));
+    }
+  };
+
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (GATHER || lane == 0) {
@@ -599,7 +614,14 @@ __global__ void __launch_bounds__(192, 1)
           tok.z = r + 2 < p.rows_total ? __ldg(p.row_tok + r + 2) : 0;
           tok.w = r + 3 < p.rows_total ? __ldg(p.row_tok + r + 3) : 0;
         }
+        // L2 prefetch of the first pf_dist k-blocks' B tiles of this segment (weight
+        // streaming: more DRAM requests in flight than the stage ring holds)
+        if (p.pf_dist > 0 && lane == 0) {
+          const int kpf = kb0 + p.pf_dist < kb1 ? kb0 + p.pf_dist : kb1;
+          for (int kq = kb0; kq < kpf; ++kq) prefetch_b(mb0, mb1, kq, brow, n);
+        }
         for (int kb = kb0; kb < kb1; ++kb) {
+          if (p.pf_dist > 0 && lane == 0 && kb + p.pf_dist < kb1) prefetch_b(mb0, mb1, kb + p.pf_dist, brow, n);
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           uint8_t* sb = sa + C::A_BYTES;
