@@ -186,8 +186,8 @@ def time_steps(layer, steps, warmup, dist_on, per_kernel=True, graph=True):
     names = kernel_names(layer)
     ev_sets = None
     if per_kernel:
-        # the library records only when given >= (its marked launches + 1) events (forward: 10)
-        n_ev = max(10, len(names) + 1)
+        # the library records only when given >= (its marked launches + 1) events (forward: 11)
+        n_ev = max(11, len(names) + 1)
         ev_sets = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(steps)]
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)

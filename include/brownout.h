@@ -118,8 +118,8 @@ typedef struct {
   size_t tile_xbase;      /* int32 [ntiles, E]  their exclusive prefix over tiles            */
   size_t ksplit;          /* int32 [1]          split count GEMM2 chose                 */
   size_t comb_cnt;        /* int32 [T, d/BN2]   arrival counters of the combine fused into GEMM2 (a8; BN2 = 256/128/64, GEMM2 tile width) */
-  size_t sk_part;         /* float [#SM, 128, 256] stream-K partial tiles (T*K <= 1024 only, else 0 bytes) */
-  size_t sk_flag;         /* int32 [#SM]        stream-K partial-published flags (zeroed by each forward) */
+  size_t sk_part;         /* float [#SM, 256/4, 128, 4] partial tiles of split GEMM tiles (router, decode FFN) */
+  size_t sk_flag;         /* int32 [#SM]        their published flags (zeroed by each forward that splits) */
   int64_t T;              /* tokens the layout was computed for                          */
   int64_t ntiles;         /* histogram tiles the workspace is sized for (8 tokens each)  */
   int64_t num_executors;  /* E = m + G                                                   */

@@ -32,6 +32,8 @@ struct bo_handle {
                        // concurrently running CTAs of the classic order read the same weight / activation
                        // tiles together, which the even k-range split gives up.
   int32_t decode_pair2; // 1: decode steps with >= 256 rows per executor: GEMM2 pairs + split-K (env BO_DECODE_PAIR2=0 disables)
+  int32_t router_splitk;  // 1: tcgen05 router with < #SM/2 token tiles splits K in lockstep (env BO_ROUTER_SPLITK=1;
+                          // off: no gain on C4, whose router time is its top-K epilogue, profiles/r01_ab_router_variants.json)
   int32_t pf_dist;      // L2 prefetch distance (k-blocks) of the FFN GEMMs' B tiles (env BO_PF_DIST)
   int32_t pair_rows1;  // GEMM1 uses CTA pairs from this many rows (env BO_PAIR_ROWS1, default 2048)
   int32_t pair_rows2;  // GEMM2 likewise (env BO_PAIR_ROWS2, default 2048)
@@ -166,9 +168,9 @@ bo_status compute_layout(const bo_handle* h, int64_t T, bo_ws_layout* L) {
   L->tile_xbase = take(c.dedup_united ? sizeof(int32_t) * ntiles * (m + G) : 0);
   L->ksplit = take(sizeof(int32_t));
   L->comb_cnt = take(sizeof(int32_t) * T * (d / gemm2_bn(static_cast<int>(d))));
-  const bool sk = R <= kSplitRows;   // stream-K is used for decode-sized steps only
-  L->sk_part = take(sk ? sizeof(float) * h->num_sms * bo::kBM * bo::kSkCols : 0);
-  L->sk_flag = take(sk ? sizeof(int32_t) * h->num_sms : 0);
+  // split-tile partials (lockstep split of the tcgen05 router, decode FFN schedules)
+  L->sk_part = take(sizeof(float) * h->num_sms * bo::kBM * bo::kSkCols);
+  L->sk_flag = take(sizeof(int32_t) * h->num_sms);
   L->total_bytes = off;
   L->T = T;
   L->ntiles = ntiles;
@@ -269,7 +271,16 @@ bo_status route_stage(bo_handle* h, const void* x, int64_t T, const void* Wr, co
     p.topk_w = topk_w;
     p.tile_cnt = tile_cnt;
     const int work = static_cast<int>((T + bo::kBM - 1) / bo::kBM);
-    const int grid = work < h->num_sms ? work : h->num_sms;
+    int grid = work < h->num_sms ? work : h->num_sms;
+    // fewer 128-token tiles than SMs: split each tile's reduction over 2-4 CTAs in
+    // lockstep (the owner adds the partials before its top-K epilogue)
+    if (h->router_splitk && work * 2 <= h->num_sms) {
+      p.stream_k = 2;
+      p.sk_part = at<float>(ws, L.sk_part);
+      p.sk_flag = at<int>(ws, L.sk_flag);
+      grid = h->num_sms;
+      BO_CUDA(cudaMemsetAsync(p.sk_flag, 0, sizeof(int) * h->num_sms, s), "split flags");
+    }
     prof.mark(launches, "router_topk");
     bo::BMaps mbs;
     for (int i = 0; i < 12; ++i) mbs.m[i] = mB;
@@ -556,7 +567,7 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   if (Ns > 0 && (!h->SWg || !h->SWu || !h->SWd))
     return fail(BO_ERR_INVALID_ARG, "num_shared=%d but bo_set_shared_experts was not called", Ns);
   int launches = 0;
-  Prof prof(h, s, 9);
+  Prof prof(h, s, 10);
   int tile = 0;
   // a1-a4: router, top-K, histogram, Alg. 1 plan
   if ((st = route_stage(h, x, T, Wr, logits_in, ws, L, s, prof, launches, tile)) != BO_OK) return st;
@@ -628,7 +639,7 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   cf.add_residual = c.add_residual;
   const CombFuse* cfp = fuse_comb ? &cf : nullptr;
   // stream-K for decode-sized steps (the workspace holds its partial tiles then)
-  const bool use_sk = h->stream_k != 0 && Rt <= kSplitRows && !h->fused_gather;
+  const bool use_sk = h->stream_k != 0 && Rt <= kSplitRows && !h->fused_gather;   // (flags are clean after a split router)
   float* sk_part = use_sk ? at<float>(ws, L.sk_part) : nullptr;
   int* sk_flag = use_sk ? at<int>(ws, L.sk_flag) : nullptr;
   if (use_sk) BO_CUDA(cudaMemsetAsync(sk_flag, 0, sizeof(int) * h->num_sms, s), "stream-K flags");
@@ -1087,6 +1098,8 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   if (h->stream_k < 0 || h->stream_k > 2) h->stream_k = 0;
   const char* dp2 = getenv("BO_DECODE_PAIR2");
   h->decode_pair2 = (dp2 && dp2[0] == '0') ? 0 : 1;
+  const char* rsk = getenv("BO_ROUTER_SPLITK");
+  h->router_splitk = (rsk && rsk[0] == '1') ? 1 : 0;
   const char* pfd = getenv("BO_PF_DIST");
   h->pf_dist = pfd ? atoi(pfd) : 0;
   const char* pr1 = getenv("BO_PAIR_ROWS1");

@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(192, 1)
   const int full_tiles = (base_work / n_units) * n_units;
   const int tail = base_work - full_tiles;
   int ks_l = 1;
-  if (CG == 1 && p.stream_k == 2 && EPI != EPI_ROUTER && ks == 1 && tail > 0)
+  if (CG == 1 && p.stream_k == 2 && ks == 1 && tail > 0)
     for (int k = 2; k <= 4 && k <= kb_u && tail * k <= n_units; ++k) ks_l = k;
   const bool lock = ks_l > 1;
   const long long dpl = lock ? full_tiles / n_units : 0;   // whole tiles per unit before the tail

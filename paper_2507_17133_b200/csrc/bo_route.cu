@@ -62,7 +62,7 @@ __device__ __forceinline__ void warp_topk_softmax(const float (&v)[VPL], int m, 
 
 // Top-K of given fp32 logits (parity entry / injected logits) + per-tile histogram.
 template <int VPL>
-__global__ void __launch_bounds__(256) k_topk_hist(const float* __restrict__ logits, int T, int m, int K, int tile,
+__global__ void __launch_bounds__(512) k_topk_hist(const float* __restrict__ logits, int T, int m, int K, int tile,
                                                    int32_t* __restrict__ topk_id, float* __restrict__ topk_w,
                                                    int32_t* __restrict__ tile_cnt) {
   __shared__ int hist[kMaxExperts];
@@ -71,7 +71,8 @@ __global__ void __launch_bounds__(256) k_topk_hist(const float* __restrict__ log
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t0 = blockIdx.x * tile;
   const int t1 = min(t0 + tile, T);
-  for (int t = t0 + warp; t < t1; t += 8) {
+  const int nw = blockDim.x >> 5;
+  for (int t = t0 + warp; t < t1; t += nw) {
     float v[VPL];
 #pragma unroll
     for (int j = 0; j < VPL; ++j) {
@@ -96,9 +97,10 @@ cudaError_t launch_topk_hist(const float* logits, int T, int m, int K, int tile,
   const int ntiles = (T + tile - 1) / tile;
   if (ntiles == 0) return cudaSuccess;
   const int vpl = (m + 31) / 32;
+  const int threads = tile >= 128 ? 512 : 256;   // a warp per token, tokens of the tile over 8-16 warps
   switch (vpl) {
 #define BO_TOPK_CASE(N) \
-  case N: k_topk_hist<N><<<ntiles, 256, 0, s>>>(logits, T, m, K, tile, topk_id, topk_w, tile_cnt); break;
+  case N: k_topk_hist<N><<<ntiles, threads, 0, s>>>(logits, T, m, K, tile, topk_id, topk_w, tile_cnt); break;
     BO_TOPK_CASE(1) BO_TOPK_CASE(2) BO_TOPK_CASE(3) BO_TOPK_CASE(4)
     BO_TOPK_CASE(5) BO_TOPK_CASE(6) BO_TOPK_CASE(7) BO_TOPK_CASE(8)
 #undef BO_TOPK_CASE

@@ -170,7 +170,7 @@ ROUTER_CFGS = SMALL + [
 
 
 @pytest.mark.parametrize("cfg", ROUTER_CFGS, ids=lambda c: c.name)
-@pytest.mark.parametrize("router", ["default", "no_split", "no_mma"])
+@pytest.mark.parametrize("router", ["default", "no_split", "no_mma", "splitk"])
 def test_router_logits_vs_fp64(cfg, router, monkeypatch):
     """Eq. 8 (tcgen05 for m > 32; for m <= 32: the split-warp decode router
     below 8 x #SM tokens, the mma.sync router above (bf16), else the
@@ -180,6 +180,8 @@ def test_router_logits_vs_fp64(cfg, router, monkeypatch):
         monkeypatch.setenv("BO_ROUTER_SPLIT", "0")
     if router == "no_mma":
         monkeypatch.setenv("BO_ROUTER_MMA", "0")
+    if router == "splitk":       # m > 32: lockstep K split of the router tiles (option)
+        monkeypatch.setenv("BO_ROUTER_SPLITK", "1")
     lay = S.make_layer(cfg)
     x = S.make_tokens(cfg, T=cfg.T)
     moe = _moe(cfg)
