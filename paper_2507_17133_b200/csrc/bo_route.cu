@@ -595,6 +595,37 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
   }
   if (tid < m) s_gsize[tid] = 0;
   __syncthreads();
+  if (staged && m >= 32) {
+    // many experts: thread (chunk c, expert e) walks its chunk of tiles sequentially
+    // (consecutive threads read consecutive experts: no shared-memory bank conflicts;
+    // the lane-over-tiles scan below strides by m, a 32-way conflict for m = 128)
+    __shared__ int s_chunk[kMaxExec];
+    const int nch = blockDim.x / m;                      // >= 1 (m <= 256 < 512)
+    const int e = tid % m, ch = tid / m;
+    const int per = (ntiles + nch - 1) / nch;
+    const int t0 = ch * per, t1 = min(ntiles, t0 + per);
+    int sum = 0;
+    if (ch < nch)
+      for (int t = t0; t < t1; ++t) sum += s_tc[t * m + e];
+    if (ch < nch) s_chunk[ch * m + e] = sum;
+    __syncthreads();
+    if (ch < nch) {
+      int carry = 0;
+      for (int c2 = 0; c2 < ch; ++c2) carry += s_chunk[c2 * m + e];
+      if (tile_base)
+        for (int t = t0; t < t1; ++t) {
+          const int v = s_tc[t * m + e];
+          s_tc[t * m + e] = carry;
+          carry += v;
+        }
+      if (ch == nch - 1) {
+        int tot = 0;
+        for (int c2 = 0; c2 < nch; ++c2) tot += s_chunk[c2 * m + e];
+        s_cnt[e] = tot;
+        counts[e] = tot;
+      }
+    }
+  } else
   for (int e = warp; e < m; e += 16) {
     int carry = 0;
     for (int t0 = 0; t0 < ntiles; t0 += 32) {
