@@ -412,7 +412,7 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-tokens", type=int, default=256)
+    ap.add_argument("--cpu-tokens", type=int, default=4096, help="oracle sample (whole C2 batch: ~6 s on 16 host threads)")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of one CUDA-graph replay")
     args = ap.parse_args()
 
@@ -463,10 +463,16 @@ def main():
     prefill_like = alg["gemm1_flops"] / max(alg["gemm1_bytes"], 1) > 300
     if prefill_like:
         ach = alg["gemm1_flops"] / g1 / 1e12
-        roof = {"kernel": "gemm1_swiglu", "bound": "tensor", "achieved": ach, "peak": pk["bf16_tflops_sustained"],
-                "unit": "TFLOP/s", "frac": ach / pk["bf16_tflops_sustained"],
-                "peak_note": "sustained bf16 (kernel timed inside a long step); " + pk["source"],
+        # the timed region (K steps) lasts well under the 4 s over which the sustained
+        # figure was measured, so the burst peak is the denominator; both are reported
+        long_region = ms / 1e3 >= 1.0
+        pk_use = pk["bf16_tflops_sustained"] if long_region else pk["bf16_tflops"]
+        roof = {"kernel": "gemm1_swiglu", "bound": "tensor", "achieved": ach, "peak": pk_use,
+                "unit": "TFLOP/s", "frac": ach / pk_use,
+                "peak_note": ("sustained" if long_region else "burst") + f" bf16 (timed region {ms:.0f} ms); "
+                             + pk["source"],
                 "frac_of_burst": ach / pk["bf16_tflops"],
+                "frac_of_sustained": ach / pk["bf16_tflops_sustained"],
                 "algorithmic_per_launch": alg["gemm1_flops"]}
     else:
         ach = alg["gemm1_bytes"] / g1 / 1e9
