@@ -704,7 +704,7 @@ def run_ep(args, cfg, rank, world, local, pk):
 def salc_demo(layer, S, iters=240, T=256):
     """Algorithm 2 (SALC) closing the loop on this layer in the decode
     regime (Mixtral, T = 256, weight streaming).  The middle third of the run adds
-    co-located interference (a 256 MiB HBM copy on a side stream overlapping every
+    co-located interference (a 512 MiB HBM copy on a side stream overlapping every
     forward, the paper's "interference from other services"); the per-layer
     SLO is 1.15x the undisturbed ratio-0 latency.  SALC (warning 0.8, shrink 0.8,
     increment 0.1) against a static threshold of 1 (zero brownout)."""
@@ -719,7 +719,7 @@ def salc_demo(layer, S, iters=240, T=256):
     ws = moe.workspace(T, "cuda")
     L = layer.lay
     side = torch.cuda.Stream()
-    hog_src = torch.empty(1 << 27, dtype=torch.bfloat16, device="cuda")   # 256 MiB
+    hog_src = torch.empty(1 << 28, dtype=torch.bfloat16, device="cuda")   # 512 MiB
     hog_dst = torch.empty_like(hog_src)
     main = torch.cuda.current_stream()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -764,7 +764,7 @@ def salc_demo(layer, S, iters=240, T=256):
                      "mean_threshold": float(np.mean(thrs))}
     del hog_src, hog_dst
     return {"slo_us": slo * 1e6, "T": T, "iters": iters, "ratio0_latency_us": lat0 * 1e6,
-            "interference": "256 MiB device copy on a side stream during the middle third", **res}
+            "interference": "512 MiB device copy on a side stream during the middle third", **res}
 
 
 def run_reference(args, cfg, rank, world):
