@@ -440,3 +440,23 @@ def test_fused_combine_bitwise_equals_separate_kernel(case, monkeypatch):
     assert k_s[-2:] == ["gemm2_weighted", "combine"]
     assert torch.equal(y_f.view(torch.int16) if y_f.dtype == torch.bfloat16 else y_f.view(torch.int32),
                        y_s.view(torch.int16) if y_s.dtype == torch.bfloat16 else y_s.view(torch.int32))
+
+
+@pytest.mark.parametrize("cfg", [
+    S.LayerConfig("decode_many_rows", d=256, f=512, m=8, K=2, way=4, T=500, ratio=1.0, dtype="bf16", sigma=0.5,
+                  config_id=51),
+    S.LayerConfig("decode_many_rows_alt112", d=256, f=1792, m=8, K=2, way=4, T=450, ratio=1.0, dtype="bf16",
+                  sigma=0.5, config_id=52),
+    S.LayerConfig("decode_many_rows_ragged", d=192, f=256, m=6, K=2, way=3, T=333, ratio=1.0, dtype="bf16",
+                  sigma=1.0, config_id=53),
+], ids=lambda c: c.name)
+@pytest.mark.parametrize("env", [{}, {"BO_DECODE_PAIR2": "0"}], ids=["pair2", "classic"])
+def test_decode_many_rows_per_executor_match_oracle(cfg, env, monkeypatch):
+    """Decode-sized steps at brownout ratio 1 (executors hold >= 256 rows): GEMM2 on CTA
+    pairs with split-K partials (BO_DECODE_PAIR2), against the oracle, and the classic
+    schedule."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _, y, dbg, ref = _run_injected(cfg, cfg.ratio, seed=3)
+    _check_routing_and_plan(dbg, ref, cfg.T, cfg.K)
+    assert _rel_err(_np(y), ref.y) <= OUT_TOL
