@@ -34,6 +34,9 @@ struct bo_handle {
   int32_t decode_pair2; // 1: decode steps with >= 256 rows per executor: GEMM2 pairs + split-K (env BO_DECODE_PAIR2=0 disables)
   int32_t router_splitk;  // 1: tcgen05 router with < #SM/2 token tiles splits K in lockstep (env BO_ROUTER_SPLITK=1;
                           // off: no gain on C4, whose router time is its top-K epilogue, profiles/r01_ab_router_variants.json)
+  int32_t b_policy;     // L2 policy of the FFN GEMMs' weight loads (env BO_B_POLICY): 0 evict_normal, 1 evict_first,
+                        // -1 auto = evict_first for decode-sized steps (C3 -2..-4 %, prefill neutral:
+                        // profiles/r01_ab_weight_evict_first.json)
   int32_t pf_dist;      // L2 prefetch distance (k-blocks) of the FFN GEMMs' B tiles (env BO_PF_DIST)
   int32_t pair_rows1;  // GEMM1 uses CTA pairs from this many rows (env BO_PAIR_ROWS1, default 2048)
   int32_t pair_rows2;  // GEMM2 likewise (env BO_PAIR_ROWS2, default 2048)
@@ -317,6 +320,13 @@ struct FfnClass {
   int64_t stack = 0;  // experts in the weight stacks (>= n; tensor-map extent)
 };
 
+// L2 policy of the weight (B) tile loads: decode-sized steps stream every weight tile
+// once per concurrent m-tile pair, so evict_first keeps the re-read activations in L2.
+int b_policy_for(const bo_handle* h, int64_t R) {
+  if (h->b_policy >= 0) return h->b_policy;
+  return R <= kSplitRows ? 1 : 0;
+}
+
 // The combine (a8) fused into GEMM2's epilogue (bo::GemmParams::comb_cnt).
 struct CombFuse {
   int32_t* cnt;            // [T, d / BN2] arrival counters (workspace)
@@ -426,6 +436,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.m_united = uni.n;
     p.store_hint = h->store_hint;
     p.pf_dist = h->pf_dist;
+    p.b_policy = b_policy_for(h, R);
     p.b_rows_per_exec = f;
     p.num_exec = n_exec;
     p.single_rows = -1;
@@ -486,6 +497,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.m_united = uni.n;
     p.store_hint = h->store_hint;
     p.pf_dist = h->pf_dist;
+    p.b_policy = b_policy_for(h, R);
     p.b_rows_per_exec = d;
     p.num_exec = n_exec;
     p.single_rows = -1;
@@ -1100,6 +1112,8 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   h->decode_pair2 = (dp2 && dp2[0] == '0') ? 0 : 1;
   const char* rsk = getenv("BO_ROUTER_SPLITK");
   h->router_splitk = (rsk && rsk[0] == '1') ? 1 : 0;
+  const char* bpo = getenv("BO_B_POLICY");
+  h->b_policy = bpo ? atoi(bpo) : -1;
   const char* pfd = getenv("BO_PF_DIST");
   h->pf_dist = pfd ? atoi(pfd) : 0;
   const char* pr1 = getenv("BO_PAIR_ROWS1");

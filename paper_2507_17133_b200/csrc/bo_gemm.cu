@@ -595,7 +595,9 @@ __global__ void __launch_bounds__(192, 1)
     // ------------------------------------------------------------ producer
     if (GATHER || lane == 0) {
       const uint64_t pol_a = policy_evict_last();   // activations are re-read per n-tile
-      const uint64_t pol_b = policy_evict_normal(); // weight tile is re-read by the executor's other m-tiles
+      // weight tile is re-read by the executor's other m-tiles (running alongside);
+      // b_policy 1: evict_first (streamed weights make way for the re-read activations)
+      const uint64_t pol_b = p.b_policy == 1 ? policy_evict_first() : policy_evict_normal();
       int stage = 0;
       uint32_t phase = 0;
       int x, mi, n, sp, kb0, kb1;

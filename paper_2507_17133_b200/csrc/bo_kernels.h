@@ -68,6 +68,7 @@ struct GemmParams {
   // Stream-K (CG = 1): the (tile, k-block) space split evenly over the grid; tiles cut
   // between CTAs are finished by their k-block-0 owner from fp32 partials.
   int pf_dist;              // > 0: the producer prefetches B tiles this many k-blocks ahead into L2
+  int b_policy;             // L2 policy of the B (weight) tile loads: 0 evict_normal, 1 evict_first
   int stream_k;             // 1: enabled (grid must be resident: <= #SM, 1 CTA / SM)
   float* sk_part;           // [grid, 128, kSkCols] partial of each contributing CTA
   int* sk_flag;             // [grid] 1 = partial published (reset to 0 by the owner; zero before first use)
