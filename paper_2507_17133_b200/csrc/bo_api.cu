@@ -434,7 +434,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.n_valid = f;
     p.m_orig = orig.n;
     p.m_united = uni.n;
-    p.store_hint = h->store_hint;
+    p.store_hint = h->store_hint && R > kSplitRows;   // decode: H / Yp (a few MB) stay in L2 for the next kernel
     p.pf_dist = h->pf_dist;
     p.b_policy = b_policy_for(h, R);
     p.b_rows_per_exec = f;
@@ -495,7 +495,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.n_valid = d;
     p.m_orig = orig.n;
     p.m_united = uni.n;
-    p.store_hint = h->store_hint;
+    p.store_hint = h->store_hint && R > kSplitRows;   // decode: H / Yp (a few MB) stay in L2 for the next kernel
     p.pf_dist = h->pf_dist;
     p.b_policy = b_policy_for(h, R);
     p.b_rows_per_exec = d;
