@@ -64,6 +64,16 @@ typedef enum { BO_PARTIAL = 0, BO_FULL = 1 } bo_mode;
  * the group's member weights, computed in fp64 and rounded once (RNE). */
 typedef enum { BO_UNITED_MEAN = 0 } bo_united_init;
 
+/* Memory layout of the expert weight stacks.  ROWMAJOR: nn.Linear [out, in]
+ * row-major matrices.  TILED: the same matrices re-laid out by bo_pack_weights
+ * into 128-row x 128-byte blocks, [n][rows/128][K/kc][128][kc] (kc = 128 bytes of
+ * K), so that each TMA box the GEMMs load is one contiguous 16 KB block —
+ * streamed from HBM at ~7.1 TB/s instead of ~5.7 TB/s for 128-byte row pieces at
+ * the row stride (decode steps are weight-streaming).  TILED needs hidden and
+ * ffn to be multiples of 128; it is a single-GPU forward layout (bo_expert_ffn
+ * takes ROWMAJOR).  bo_build_united works on either (element-wise). */
+typedef enum { BO_WEIGHTS_ROWMAJOR = 0, BO_WEIGHTS_TILED = 1 } bo_weight_layout;
+
 typedef struct {
   int32_t hidden;        /* d   */
   int32_t ffn;           /* f   */
@@ -76,7 +86,7 @@ typedef struct {
                             the summed weight (Eq. 5-6 algebra; single-GPU forward only) */
   int32_t num_shared;    /* N_s of Eq. 5: shared experts applied to every token with weight 1, shape
                             of an original expert; weights via bo_set_shared_experts (single-GPU forward only) */
-  int32_t reserved;
+  int32_t weight_layout; /* bo_weight_layout of every expert weight stack (originals, united, shared) */
   int64_t max_tokens;    /* largest T a forward will be called with */
 } bo_config;
 
@@ -143,6 +153,13 @@ BO_API bo_status bo_workspace_layout(const bo_handle* h, int64_t T, bo_ws_layout
  * Runs once per layer; not part of the timed forward. */
 BO_API bo_status bo_build_united(bo_handle* h, const void* Wg, const void* Wu, const void* Wd,
                           int32_t init, void* UWg, void* UWu, void* UWd, void* stream);
+
+/* Re-lay n row-major [rows, K] matrices W (device) into the TILED layout in P
+ * (device, same byte size, caller-owned, must not alias W): which = 0 for
+ * gate / up stacks ([n, f, d]: rows = ffn, K = hidden), 1 for down stacks
+ * ([n, d, f]: rows = hidden, K = ffn).  Runs once per weight load (the paper's
+ * Experts Loader); enqueued on `stream`. */
+BO_API bo_status bo_pack_weights(const bo_handle* h, const void* W, int64_t n, int32_t which, void* P, void* stream);
 
 /* Shared experts of Eq. 5 (second term): SWg, SWu [N_s, f, d], SWd [N_s, d, f]
  * device pointers (caller-owned) used by every following forward; N_s is fixed

@@ -22,6 +22,7 @@ BO_UNITED_MEAN = 0
 
 EXPORTED = (
     "bo_create", "bo_destroy", "bo_workspace_size", "bo_workspace_layout", "bo_build_united", "bo_set_shared_experts",
+    "bo_pack_weights",
     "bo_set_brownout", "bo_get_brownout", "bo_moe_forward", "bo_moe_forward_ex", "bo_plan_from_counts",
     "bo_route", "bo_plan_counts", "bo_dispatch", "bo_block_copy", "bo_expert_ffn", "bo_combine",
     "bo_set_profile_events", "bo_last_launch_count", "bo_last_kernels", "bo_status_string", "bo_last_error", "bo_version",
@@ -32,7 +33,7 @@ EXPORTED = (
 class bo_config(C.Structure):
     _fields_ = [("hidden", C.c_int32), ("ffn", C.c_int32), ("num_experts", C.c_int32), ("top_k", C.c_int32),
                 ("way", C.c_int32), ("dtype", C.c_int32), ("add_residual", C.c_int32), ("dedup_united", C.c_int32),
-                ("num_shared", C.c_int32), ("reserved", C.c_int32), ("max_tokens", C.c_int64)]
+                ("num_shared", C.c_int32), ("weight_layout", C.c_int32), ("max_tokens", C.c_int64)]
 
 
 class bo_plan_stats(C.Structure):
@@ -75,6 +76,7 @@ def _load():
         "bo_workspace_size": ([vp, i64, C.POINTER(C.c_size_t)], C.c_int),
         "bo_workspace_layout": ([vp, i64, C.POINTER(bo_ws_layout)], C.c_int),
         "bo_build_united": ([vp, vp, vp, vp, i32, vp, vp, vp, vp], C.c_int),
+        "bo_pack_weights": ([vp, vp, i64, i32, vp, vp], C.c_int),
         "bo_set_brownout": ([vp, C.c_double, i32], C.c_int),
         "bo_set_shared_experts": ([vp, vp, vp, vp], C.c_int),
         "bo_get_brownout": ([vp, C.POINTER(C.c_double), C.POINTER(i32)], C.c_int),
@@ -134,11 +136,12 @@ class BrownoutMoE:
     """One MoE layer handle: bo_create / bo_set_brownout / bo_moe_forward."""
 
     def __init__(self, hidden, ffn, num_experts, top_k, way, dtype="bf16", add_residual=False,
-                 max_tokens=16384, dedup=False, num_shared=0):
+                 max_tokens=16384, dedup=False, num_shared=0, tiled=False):
         self.cfg = bo_config(hidden=hidden, ffn=ffn, num_experts=num_experts, top_k=top_k, way=way,
                              dtype=BO_BF16 if dtype in ("bf16", torch.bfloat16) else BO_FP32,
                              add_residual=1 if add_residual else 0, dedup_united=1 if dedup else 0,
-                             num_shared=num_shared, reserved=0, max_tokens=max_tokens)
+                             num_shared=num_shared, weight_layout=1 if tiled else 0,
+                             max_tokens=max_tokens)
         h = C.c_void_p()
         _check(_lib.bo_create(C.byref(self.cfg), C.byref(h)))
         self._h = h
@@ -194,6 +197,17 @@ class BrownoutMoE:
         _check(_lib.bo_build_united(self._h, _ptr(Wg), _ptr(Wu), _ptr(Wd), BO_UNITED_MEAN, _ptr(UWg), _ptr(UWu),
                                     _ptr(UWd), _stream(stream)))
         return UWg, UWu, UWd
+
+    def pack(self, W, which, stream=None):
+        """bo_pack_weights: a TILED-layout copy of the weight stack W ([n, f, d] gate / up:
+        which=0; [n, d, f] down: which=1).  Same shape and dtype; only the memory layout
+        differs (pass it to a handle created with tiled=True)."""
+        P = torch.empty_like(W)
+        _check(_lib.bo_pack_weights(self._h, _ptr(W), W.shape[0], int(which), _ptr(P), _stream(stream)))
+        return P
+
+    def pack_all(self, Wg, Wu, Wd, stream=None):
+        return self.pack(Wg, 0, stream), self.pack(Wu, 0, stream), self.pack(Wd, 1, stream)
 
     def forward(self, x, Wr, experts, united, y=None, workspace=None, logits=None, stream=None, shared=None):
         """moe_forward(tokens, router, experts, united) -> y [T, d].

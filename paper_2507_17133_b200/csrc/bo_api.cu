@@ -119,6 +119,39 @@ bo_status make_map(CUtensorMap* m, const void* base, int32_t dtype, uint64_t row
   return BO_OK;
 }
 
+// Tile-packed weight stack (bo_pack_weights) of `rows` rows (all matrices stacked)
+// and K columns: a 3-D view {kc elements, 128 rows of a band, band * K/kc + k-chunk}
+// whose boxes {kc, box_rows <= 128, 1} are contiguous 16 KB blocks.
+bo_status make_map_packed(CUtensorMap* m, const void* base, int32_t dtype, uint64_t rows, uint64_t k,
+                          uint32_t box_rows) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return fail(BO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const int eb = elem_bytes(dtype);
+  const uint64_t kc = 128 / eb;
+  if (rows % bo::kPackRows || k % kc) return fail(BO_ERR_SHAPE, "packed map: rows=%llu k=%llu",
+                                                   static_cast<unsigned long long>(rows),
+                                                   static_cast<unsigned long long>(k));
+  cuuint64_t dims[3] = {kc, static_cast<cuuint64_t>(bo::kPackRows), (rows / bo::kPackRows) * (k / kc)};
+  cuuint64_t strides[2] = {128, static_cast<cuuint64_t>(bo::kPackRows) * 128};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(kc), box_rows > 128 ? 128u : box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, dtype == BO_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(BO_ERR_CUDA, "cuTensorMapEncodeTiled (packed) failed (%d) rows=%llu k=%llu", static_cast<int>(r),
+                static_cast<unsigned long long>(rows), static_cast<unsigned long long>(k));
+  return BO_OK;
+}
+
+// B operand map of a weight stack in the handle's layout.
+bo_status make_map_w(const bo_handle* h, CUtensorMap* m, const void* base, uint64_t rows, uint64_t k,
+                     uint32_t box_rows) {
+  if (h->cfg.weight_layout == BO_WEIGHTS_TILED) return make_map_packed(m, base, h->cfg.dtype, rows, k, box_rows);
+  return make_map(m, base, h->cfg.dtype, rows, k, box_rows);
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 int router_bn(int m) {
@@ -388,7 +421,8 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
   const int tier = 256;
   {
     int bn = tier;                                                  // gate + up columns per tile
-    if (R <= kSplitRows && h->decode_bn1 > 0) bn = h->decode_bn1;   // experiment knob (BO_DECODE_BN1)
+    if (R <= kSplitRows && h->decode_bn1 > 0 && c.weight_layout != BO_WEIGHTS_TILED)
+      bn = h->decode_bn1;   // experiment knob (BO_DECODE_BN1)
     while (bn > 64 && (f % (bn / 2) || f_u % (bn / 2))) bn >>= 1;
     CUtensorMap mA;
     bo::BMaps mb;
@@ -401,16 +435,16 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     const FfnClass* cls[3] = {&orig, &uni, &shr};
     for (int k = 0; k < 3; ++k) {
       const int width = k == 1 ? f_u : f;
-      if ((st = make_map(&mb.m[2 * k], ptr(*cls[k], 0), c.dtype, rows_of(*cls[k], width), d, bn / 2)) != BO_OK)
+      if ((st = make_map_w(h, &mb.m[2 * k], ptr(*cls[k], 0), rows_of(*cls[k], width), d, bn / 2)) != BO_OK)
         return st;
-      if ((st = make_map(&mb.m[2 * k + 1], ptr(*cls[k], 1), c.dtype, rows_of(*cls[k], width), d, bn / 2)) != BO_OK)
+      if ((st = make_map_w(h, &mb.m[2 * k + 1], ptr(*cls[k], 1), rows_of(*cls[k], width), d, bn / 2)) != BO_OK)
         return st;
     }
     bo::GemmParams p{};
     // alternative tile width for the device-side wave choice: the widest gate/up half
     // below bn/2 (multiple of 16, >= 64) that divides both widths
     int bh_alt = 0;
-    if (h->tile_alt && !gather)
+    if (h->tile_alt && !gather && c.weight_layout != BO_WEIGHTS_TILED)   // packed bands are 128 rows
       for (int bh = bn / 2 - 16; bh >= 64 && !bh_alt; bh -= 16)
         if (f % bh == 0 && f_u % bh == 0) bh_alt = bh;
     if (bh_alt) {
@@ -437,6 +471,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.store_hint = h->store_hint && R > kSplitRows;   // decode: H / Yp (a few MB) stay in L2 for the next kernel
     p.pf_dist = h->pf_dist;
     p.b_policy = b_policy_for(h, R);
+    p.b_packed = c.weight_layout == BO_WEIGHTS_TILED ? 1 : 0;
     p.b_rows_per_exec = f;
     p.num_exec = n_exec;
     p.single_rows = -1;
@@ -482,7 +517,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
       const FfnClass& q = cls[k]->Wg ? *cls[k] : any;
       const int kdim = k == 1 ? f_u : f;
       const uint64_t rows = static_cast<uint64_t>(q.stack > 0 ? q.stack : 1) * d;
-      if ((st = make_map(&mb.m[2 * k], ptr(*cls[k], 2), c.dtype, rows, kdim, box_b)) != BO_OK) return st;
+      if ((st = make_map_w(h, &mb.m[2 * k], ptr(*cls[k], 2), rows, kdim, box_b)) != BO_OK) return st;
       mb.m[2 * k + 1] = mb.m[2 * k];
     }
     bo::GemmParams p{};
@@ -498,6 +533,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.store_hint = h->store_hint && R > kSplitRows;   // decode: H / Yp (a few MB) stay in L2 for the next kernel
     p.pf_dist = h->pf_dist;
     p.b_policy = b_policy_for(h, R);
+    p.b_packed = c.weight_layout == BO_WEIGHTS_TILED ? 1 : 0;
     p.b_rows_per_exec = d;
     p.num_exec = n_exec;
     p.single_rows = -1;
@@ -1081,6 +1117,11 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   if (c.hidden <= 0 || c.hidden % mult || c.ffn <= 0 || c.ffn % mult)
     return fail(BO_ERR_SHAPE, "hidden=%d / ffn=%d must be positive multiples of %d", c.hidden, c.ffn, mult);
   if (c.ffn % 64) return fail(BO_ERR_SHAPE, "ffn=%d must be a multiple of 64", c.ffn);
+  if (c.weight_layout != BO_WEIGHTS_ROWMAJOR && c.weight_layout != BO_WEIGHTS_TILED)
+    return fail(BO_ERR_UNSUPPORTED, "weight_layout %d not built", c.weight_layout);
+  if (c.weight_layout == BO_WEIGHTS_TILED && (c.hidden % bo::kPackRows || c.ffn % bo::kPackRows))
+    return fail(BO_ERR_SHAPE, "TILED weights need hidden=%d and ffn=%d to be multiples of %d", c.hidden, c.ffn,
+                bo::kPackRows);
   const int G = (c.num_experts + c.way - 1) / c.way;
   if (c.num_shared < 0 || c.num_experts + G + c.num_shared > bo::kMaxExec)
     return fail(BO_ERR_INVALID_ARG, "num_shared=%d: m + G + N_s must be <= %d", c.num_shared, bo::kMaxExec);
@@ -1193,6 +1234,21 @@ bo_status bo_build_united(bo_handle* h, const void* Wg, const void* Wu, const vo
   BO_CUDA(bo::launch_build_united(dt, Wg, c.num_experts, c.way, per, UWg, s), "build_united Wg");
   BO_CUDA(bo::launch_build_united(dt, Wu, c.num_experts, c.way, per, UWu, s), "build_united Wu");
   BO_CUDA(bo::launch_build_united(dt, Wd, c.num_experts, c.way, per, UWd, s), "build_united Wd");
+  return BO_OK;
+}
+
+bo_status bo_pack_weights(const bo_handle* h, const void* W, int64_t n, int32_t which, void* P, void* stream) {
+  if (!h) return fail(BO_ERR_INVALID_ARG, "null handle");
+  if (n < 0 || (which != 0 && which != 1)) return fail(BO_ERR_INVALID_ARG, "n=%lld which=%d", (long long)n, which);
+  if (n == 0) return BO_OK;
+  if (!W || !P || W == P) return fail(BO_ERR_INVALID_ARG, "null or aliased weight pointers");
+  if (!aligned16(W) || !aligned16(P)) return fail(BO_ERR_SHAPE, "weight pointers must be 16-byte aligned");
+  const bo_config& c = h->cfg;
+  const int rows = which == 0 ? c.ffn : c.hidden, K = which == 0 ? c.hidden : c.ffn;
+  if (rows % bo::kPackRows || K % 64)
+    return fail(BO_ERR_SHAPE, "packing needs rows=%d to be a multiple of %d", rows, bo::kPackRows);
+  BO_CUDA(bo::launch_pack(c.dtype == BO_BF16 ? 0 : 1, W, n, rows, K, P, h->num_sms, static_cast<cudaStream_t>(stream)),
+          "pack");
   return BO_OK;
 }
 
@@ -1315,6 +1371,8 @@ bo_status bo_expert_ffn(bo_handle* h, const void* rows, int64_t R, const float* 
                         void* h_buf, void* out, void* stream) {
   if (!h) return fail(BO_ERR_INVALID_ARG, "null handle");
   h->last_kernels.clear();
+  if (h->cfg.weight_layout != BO_WEIGHTS_ROWMAJOR)
+    return fail(BO_ERR_UNSUPPORTED, "bo_expert_ffn takes ROWMAJOR weights (f-sliced united experts)");
   if (R == 0) return BO_OK;
   const bo_config& c = h->cfg;
   if (n_orig < 0 || n_united < 0 || n_orig + n_united > bo::kMaxExec)

@@ -618,24 +618,43 @@ __global__ void __launch_bounds__(192, 1)
         }
         // L2 prefetch of the first pf_dist k-blocks' B tiles of this segment (weight
         // streaming: more DRAM requests in flight than the stage ring holds)
-        if (p.pf_dist > 0 && lane == 0) {
+        if (p.pf_dist > 0 && !p.b_packed && lane == 0) {
           const int kpf = kb0 + p.pf_dist < kb1 ? kb0 + p.pf_dist : kb1;
           for (int kq = kb0; kq < kpf; ++kq) prefetch_b(mb0, mb1, kq, brow, n);
         }
         for (int kb = kb0; kb < kb1; ++kb) {
-          if (p.pf_dist > 0 && lane == 0 && kb + p.pf_dist < kb1) prefetch_b(mb0, mb1, kb + p.pf_dist, brow, n);
+          if (p.pf_dist > 0 && !p.b_packed && lane == 0 && kb + p.pf_dist < kb1)
+            prefetch_b(mb0, mb1, kb + p.pf_dist, brow, n);
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           uint8_t* sb = sa + C::A_BYTES;
           if (lane == 0) {
+            // B rows [grow, grow + nr) of k-block kb: one 2-D box, or (tile-packed weights)
+            // one 3-D box per 128-row band, each a contiguous block in memory
+            const int kbs = kblocks(x);
+            auto load_b = [&](uint8_t* dst, const CUtensorMap* mb, int grow, int nr) {
+              if (!p.b_packed) {
+                if constexpr (CG == 1) tma_load_2d(dst, mb, &full_bar[stage], kb * C::BK, grow, pol_b);
+                else tma_load_2d_pair(dst, mb, &full_bar[stage], kb * C::BK, grow, pol_b);
+                return;
+              }
+              for (int r0 = 0; r0 < nr; r0 += kPackRows) {
+                const int gr = grow + r0;
+                const int c2 = (gr / kPackRows) * kbs + kb;
+                if constexpr (CG == 1)
+                  tma_load_3d(dst + r0 * 128, mb, &full_bar[stage], 0, gr % kPackRows, c2, pol_b);
+                else
+                  tma_load_3d_pair(dst + r0 * 128, mb, &full_bar[stage], 0, gr % kPackRows, c2, pol_b);
+              }
+            };
             if constexpr (CG == 1) {
               mbar_arrive_expect_tx(&full_bar[stage], stage_tx);
               if constexpr (!GATHER) tma_load_2d(sa, &tmA, &full_bar[stage], kb * C::BK, arow, pol_a);
               if constexpr (EPI == EPI_SWIGLU) {
-                tma_load_2d(sb, mb0, &full_bar[stage], kb * C::BK, brow + n * bh, pol_b);
-                tma_load_2d(sb + bh * 128, mb1, &full_bar[stage], kb * C::BK, brow + n * bh, pol_b);
+                load_b(sb, mb0, brow + n * bh, bh);
+                load_b(sb + bh * 128, mb1, brow + n * bh, bh);
               } else {
-                tma_load_2d(sb, mb0, &full_bar[stage], kb * C::BK, brow + n * BN, pol_b);
+                load_b(sb, mb0, brow + n * BN, BN);
               }
             } else {
               // Both CTAs load their halves; completion is counted on the leader's barrier.
@@ -644,10 +663,9 @@ __global__ void __launch_bounds__(192, 1)
               if constexpr (!GATHER) tma_load_2d_pair(sa, &tmA, &full_bar[stage], kb * C::BK, arow, pol_a);
               if constexpr (EPI == EPI_SWIGLU) {
                 // leader: gate rows, peer: up rows of the same f-columns -> D[:, 0:BN/2] = gate, D[:, BN/2:] = up
-                tma_load_2d_pair(sb, leader ? mb0 : mb1, &full_bar[stage], kb * C::BK, brow + n * bh, pol_b);
+                load_b(sb, leader ? mb0 : mb1, brow + n * bh, bh);
               } else {
-                tma_load_2d_pair(sb, mb0, &full_bar[stage], kb * C::BK,
-                                 brow + n * BN + static_cast<int>(crank) * (BN / 2), pol_b);
+                load_b(sb, mb0, brow + n * BN + static_cast<int>(crank) * (BN / 2), BN / 2);
               }
             }
           }

@@ -11,6 +11,7 @@ constexpr int kTileTok = 128;   // token tile of the tcgen05 router (= GEMM BM)
 constexpr int kBM = 128;        // rows per GEMM tile (TMEM lanes)
 constexpr int kMaxExperts = 256;
 constexpr int kMaxExec = 512;   // m + G
+constexpr int kPackRows = 128;  // rows per band of the tile-packed weight layout
 constexpr int kSkCols = 256;    // stream-K partial tile row stride (fp32 columns >= any BN)
 
 enum Epi : int { EPI_SWIGLU = 0, EPI_WEIGHTED = 1, EPI_ROUTER = 2,
@@ -69,6 +70,7 @@ struct GemmParams {
   // between CTAs are finished by their k-block-0 owner from fp32 partials.
   int pf_dist;              // > 0: the producer prefetches B tiles this many k-blocks ahead into L2
   int b_policy;             // L2 policy of the B (weight) tile loads: 0 evict_normal, 1 evict_first
+  int b_packed;             // 1: B maps are 3-D over tile-packed weights (kPackRows-row bands, see launch_pack)
   int stream_k;             // 1: enabled (grid must be resident: <= #SM, 1 CTA / SM)
   float* sk_part;           // [grid, 128, kSkCols] partial of each contributing CTA
   int* sk_flag;             // [grid] 1 = partial published (reset to 0 by the owner; zero before first use)
@@ -141,6 +143,11 @@ cudaError_t launch_dedup(int stage, const int32_t* topk_id, const float* topk_w,
                          const int32_t* exec_of, int32_t* tile_xcnt, int32_t* tile_xbase, int32_t* exec_off,
                          int32_t* mtile_off, int64_t* stats, int32_t* row_of, int32_t* row_tok, float* row_w,
                          cudaStream_t s);
+
+// Tile-packed weights: n row-major matrices [rows, K] -> [n][rows/128][K/kc][128][kc]
+// (kc = 128 bytes of K): every 128-row x 128-byte TMA box of the GEMMs is one
+// contiguous 16 KB block, read at full DRAM streaming bandwidth.
+cudaError_t launch_pack(int dtype, const void* W, int64_t n, int rows, int K, void* P, int num_sms, cudaStream_t s);
 
 cudaError_t launch_build_united(int dtype, const void* W, int m, int way, int64_t per_expert, void* U,
                                 cudaStream_t s);

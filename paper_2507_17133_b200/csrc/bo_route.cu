@@ -1149,6 +1149,40 @@ __global__ void k_united_mean(const T* __restrict__ W, int m, int way, int64_t p
   }
 }
 
+// ------------------------------------------------------ tile-packed weights
+// One 16-byte vector per thread step; source index decomposed from the packed
+// (destination) order so the writes are fully sequential.
+__global__ void __launch_bounds__(256) k_pack(const uint4* __restrict__ W, int64_t n, int rows, int kv,
+                                              uint4* __restrict__ P) {
+  // kv = K in 16-byte vectors; a k-chunk is 8 vectors (128 bytes)
+  const int64_t total = n * rows * static_cast<int64_t>(kv);
+  const int kch = kv / 8, bands = rows / kPackRows;
+  for (int64_t o = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; o < total;
+       o += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    // o = (((e * bands + band) * kch + kc) * 128 + r) * 8 + v
+    const int v = static_cast<int>(o & 7);
+    int64_t q = o >> 3;
+    const int r = static_cast<int>(q % kPackRows);
+    q /= kPackRows;
+    const int kc = static_cast<int>(q % kch);
+    q /= kch;
+    const int band = static_cast<int>(q % bands);
+    const int64_t e = q / bands;
+    const int64_t src = ((e * rows) + static_cast<int64_t>(band) * kPackRows + r) * kv + kc * 8 + v;
+    P[o] = __ldg(W + src);
+  }
+}
+
+cudaError_t launch_pack(int dtype, const void* W, int64_t n, int rows, int K, void* P, int num_sms, cudaStream_t s) {
+  const int kv = K * (dtype == 0 ? 2 : 4) / 16;
+  const int64_t total = n * rows * static_cast<int64_t>(kv);
+  if (total == 0) return cudaSuccess;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > num_sms * 16) blocks = num_sms * 16;
+  k_pack<<<static_cast<int>(blocks), 256, 0, s>>>(static_cast<const uint4*>(W), n, rows, kv, static_cast<uint4*>(P));
+  return cudaGetLastError();
+}
+
 cudaError_t launch_build_united(int dtype, const void* W, int m, int way, int64_t per_expert, void* U,
                                 cudaStream_t s) {
   const int G = (m + way - 1) / way;

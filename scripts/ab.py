@@ -44,17 +44,30 @@ def main():
             torch.cuda.empty_cache()
             cache[wname] = bench.Layer(cfg, "cuda")
         layer = cache[wname]
-        moes = {}
+        moes, weights = {}, {}
+        base_w = (layer.lay, layer.united)
         for arm, env in arms.items():
             if arm == "A":
                 moes[arm] = layer.moe
+                weights[arm] = base_w
                 continue
+            env = dict(env)
+            tiled = env.pop("TILED", "0") == "1"   # pseudo-knob: TILED weight layout (packed copies)
             old = {k: os.environ.get(k) for k in env}
             os.environ.update(env)
             moe = BrownoutMoE(cfg.d, cfg.f, cfg.m, cfg.K, cfg.way, dtype=cfg.dtype, max_tokens=layer.T,
-                              num_shared=cfg.Ns)
+                              num_shared=cfg.Ns, tiled=tiled)
+            lay = layer.lay
+            uni = layer.united
+            if tiled:
+                lay = dict(layer.lay)
+                lay["Wg"], lay["Wu"], lay["Wd"] = moe.pack_all(layer.lay["Wg"], layer.lay["Wu"], layer.lay["Wd"])
+                uni = moe.pack_all(*layer.united)
+                if cfg.Ns:
+                    lay["SWg"], lay["SWu"], lay["SWd"] = moe.pack_all(lay["SWg"], lay["SWu"], lay["SWd"])
+            weights[arm] = (lay, uni)
             if cfg.Ns:
-                moe.set_shared_experts(layer.lay["SWg"], layer.lay["SWu"], layer.lay["SWd"])
+                moe.set_shared_experts(lay["SWg"], lay["SWu"], lay["SWd"])
             for k, v in old.items():
                 if v is None:
                     del os.environ[k]
@@ -68,11 +81,13 @@ def main():
             order = names[rep % len(names):] + names[:rep % len(names)]
             for arm in order:
                 layer.moe = moes[arm]
+                layer.lay, layer.united = weights[arm]
                 layer.moe.set_brownout(float(ratio))
                 ms, kern = bench.time_steps(layer, args.steps, 3, False)
                 res[arm]["ms"].append(ms / args.steps)
                 res[arm]["k"].append(kern)
         layer.moe = moe_a
+        layer.lay, layer.united = base_w
         summ = {}
         for arm in names:
             ks = {}
