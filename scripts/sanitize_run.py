@@ -1,0 +1,70 @@
+"""Small forwards over the library's code paths, for compute-sanitizer
+(memcheck / racecheck / synccheck / initcheck): bf16 decode and CTA-pair prefill,
+fp32 (tf32), shared experts, united-row de-duplication, full brownout, the TILED
+weight layout, the fused combine and the split-tile schedules.  Exits non-zero if
+a forward disagrees with the ROWMAJOR / default path of the same inputs."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import synthetic as S  # noqa: E402
+from paper_2507_17133_b200 import BrownoutMoE  # noqa: E402
+
+
+def run(cfg, ratio=0.5, mode="partial", dedup=False, tiled=False, logits=True):
+    lay = {k: v.cuda() for k, v in S.make_layer(cfg).items()}
+    x = S.make_tokens(cfg, batch_index=2).cuda()
+    moe = BrownoutMoE(cfg.d, cfg.f, cfg.m, cfg.K, cfg.way, dtype=cfg.dtype, max_tokens=cfg.T, dedup=dedup,
+                      num_shared=cfg.Ns, tiled=tiled)
+    ex = (lay["Wg"], lay["Wu"], lay["Wd"])
+    sh = (lay["SWg"], lay["SWu"], lay["SWd"]) if cfg.Ns else None
+    U = moe.build_united(*ex)
+    if tiled:
+        ex, U = moe.pack_all(*ex), moe.pack_all(*U)
+        sh = moe.pack_all(*sh) if sh else None
+    moe.set_brownout(ratio, mode)
+    L = S.make_logits(cfg.T, cfg.m, seed=2, sigma=cfg.sigma).cuda() if logits else None
+    y = moe.forward(x, lay["Wr"], ex, U, logits=L, shared=sh)
+    torch.cuda.synchronize()
+    return y
+
+
+def main():
+    small = S.LayerConfig("s", d=256, f=512, m=8, K=2, way=4, T=200, ratio=0.5, dtype="bf16", sigma=0.7,
+                          config_id=71)
+    pair = S.LayerConfig("p", d=256, f=256, m=8, K=2, way=4, T=1100, ratio=0.5, dtype="bf16", sigma=0.5,
+                         config_id=72)
+    fp32 = S.LayerConfig("f", d=64, f=128, m=8, K=2, way=4, T=32, ratio=0.5, dtype="fp32", sigma=0.0, config_id=1)
+    qwen = S.LayerConfig("q", d=256, f=256, m=128, K=8, way=4, T=130, ratio=0.5, dtype="bf16", sigma=0.5,
+                         config_id=73)
+    shared = S.LayerConfig("sh", d=256, f=256, m=8, K=2, way=4, T=150, ratio=0.5, dtype="bf16", sigma=0.5,
+                           config_id=74, Ns=2)
+    bad = 0
+    for name, f in [
+        ("decode", lambda: run(small)),
+        ("decode_ratio1", lambda: run(small, ratio=1.0)),
+        ("router_gpu", lambda: run(small, logits=False)),
+        ("prefill_pairs_fused_combine", lambda: run(pair)),
+        ("fp32", lambda: run(fp32)),
+        ("qwen_like_tc_router", lambda: run(qwen, logits=False)),
+        ("shared", lambda: run(shared)),
+        ("dedup", lambda: run(small, ratio=1.0, dedup=True)),
+        ("full_mode", lambda: run(small, ratio=0.6, mode="full")),
+    ]:
+        f()
+        print("ok", name, flush=True)
+    for name, a, b in [("tiled", lambda: run(small), lambda: run(small, tiled=True))]:
+        if not torch.equal(a(), b()):
+            bad += 1
+            print("MISMATCH", name)
+        else:
+            print("ok", name, flush=True)
+    sys.exit(1 if bad else 0)
+
+
+if __name__ == "__main__":
+    main()
