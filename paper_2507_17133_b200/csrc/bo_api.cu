@@ -1155,6 +1155,8 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   h->router_splitk = (rsk && rsk[0] == '1') ? 1 : 0;
   const char* bpo = getenv("BO_B_POLICY");
   h->b_policy = bpo ? atoi(bpo) : -1;
+  const char* pdl = getenv("BO_PDL");
+  bo::set_gemm_pdl(!(pdl && pdl[0] == '0'));
   const char* pfd = getenv("BO_PF_DIST");
   h->pf_dist = pfd ? atoi(pfd) : 0;
   const char* pr1 = getenv("BO_PAIR_ROWS1");

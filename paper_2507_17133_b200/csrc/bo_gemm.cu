@@ -371,6 +371,13 @@ __global__ void __launch_bounds__(192, 1)
       tmem_relinquish();
     }
   }
+  // Programmatic dependent launch: everything above (barriers, TMEM, descriptor
+  // prefetch) may overlap the previous kernel's tail; no global memory is touched
+  // before the previous kernel has completed and flushed.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // ... and let the next kernel (if launched programmatically) start its own prologue
+  // on the SMs this grid frees in its tail; it still waits for this grid to finish.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // executor row offsets and the prefix of TILE_M-row m-tiles (warp 2, shuffle scan)
   const int nexec = p.single_rows >= 0 ? 1 : p.num_exec;
   if (p.single_rows >= 0) {
@@ -1007,6 +1014,8 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
+static bool g_pdl = true;   // programmatic dependent launch of the GEMMs (set_gemm_pdl)
+
 template <typename T, int BN, int EPI, int KMAX = 0, int CG = 1, bool GATHER = false>
 static cudaError_t launch_t(const CUtensorMap& A, const BMaps& B, const GemmParams& p, int grid, cudaStream_t s) {
   using C = GemmCfg<T, BN, CG>;
@@ -1017,24 +1026,29 @@ static cudaError_t launch_t(const CUtensorMap& A, const BMaps& B, const GemmPara
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  if constexpr (CG == 1) {
-    kern<<<grid, 192, C::SMEM, s>>>(A, B, p);
-  } else {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(grid & ~1));
-    cfg.blockDim = dim3(192);
-    cfg.dynamicSmemBytes = C::SMEM;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, A, B, p);
-    if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(CG == 2 ? (grid & ~1) : grid));
+  cfg.blockDim = dim3(192);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if constexpr (CG == 2) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
   }
+  if (g_pdl) {   // may launch while the previous kernel drains; waits in-kernel (griddepcontrol.wait)
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, A, B, p);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -1078,6 +1092,8 @@ cudaError_t launch_grouped_gemm(int dtype, int epi, int bn, const CUtensorMap& A
   if (dtype == 0) return dispatch<__nv_bfloat16>(epi, bn, A, B, p, grid, s);
   return dispatch<float>(epi, bn, A, B, p, grid, s);
 }
+
+void set_gemm_pdl(bool on) { g_pdl = on; }
 
 int gemm_smem_bytes(int dtype, int epi, int bn) {
   (void)epi;

@@ -94,6 +94,8 @@ struct BMaps {
 cudaError_t launch_grouped_gemm(int dtype, int epi, int bn, const CUtensorMap& A, const BMaps& B,
                                 const GemmParams& p, int grid, cudaStream_t s);
 int gemm_smem_bytes(int dtype, int epi, int bn);
+// Programmatic dependent launch of the grouped GEMMs (process-wide; env BO_PDL=0 disables).
+void set_gemm_pdl(bool on);
 
 constexpr int kTileMin = 8;     // smallest token tile (workspace histograms are sized for it)
 constexpr int kTileSmall = 32;  // token tile of the injected-logits top-k
