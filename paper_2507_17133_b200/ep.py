@@ -112,8 +112,10 @@ class EPPlanner:
                     fd[self.v_of_slice[(j, s)]].append(e)
         return fd
 
-    def tables(self, C, exec_of_expert):
-        """C [R, m] per-rank expert counts; exec_of_expert [m] of the global plan."""
+    def tables(self, C, exec_of_expert, rank=None):
+        """C [R, m] per-rank expert counts; exec_of_expert [m] of the global plan.
+        Returns the per-rank tables of every rank, or only rank `rank`'s (the
+        forward path: each rank builds just its own)."""
         C = np.asarray(C, dtype=np.int64)
         R, m, V = self.R, self.m, self.V
         fd = self.feeds(exec_of_expert)
@@ -137,7 +139,7 @@ class EPPlanner:
                 row_base[:, e, rep] = vstart[:, v] + acc
                 acc += C[:, e]
         per_rank = []
-        for q in range(R):
+        for q in (range(R) if rank is None else (rank,)):
             lv = self.local_v[q]
             # receive buffer: source-major, then local executor order
             recv_seg = np.concatenate([[0], np.cumsum(send[:, q])])
@@ -172,7 +174,7 @@ class EPPlanner:
                 fwd_src_off=fwd_src_off, fwd_dst_start=fwd_dst_start,
                 inv_src_off=inv_src_off, inv_dst_start=inv_dst_start,
                 exec_off=exec_off, mtile_off=mtile_off, n_orig=n_orig, n_united=len(lv) - n_orig))
-        return per_rank
+        return per_rank if rank is None else per_rank[0]
 
 
 class TorchComm:
@@ -221,10 +223,35 @@ class EPMoE:
     (route / local_counts / plan_counts / dispatch / block_copy / expert_ffn /
     combine) to exercise this orchestration with gloo."""
 
+    TABLE_KEYS = ("row_base", "fwd_src_off", "fwd_dst_start", "inv_src_off", "inv_dst_start", "exec_off",
+                  "mtile_off")
+
     def __init__(self, ops, planner: EPPlanner, rank: int, experts, united, d: int, K: int, dtype):
         self.ops, self.pl, self.rank = ops, planner, rank
         self.d, self.K, self.dtype = d, K, dtype
         self.ex, self.un = planner.local_weights(rank, experts, united)
+        self._h_tab = None   # persistent (pinned on GPUs) host staging of the per-forward int32 tables
+        self._d_tab = None
+
+    def _upload_tables(self, tabs, dev):
+        """All int32 tables of this forward in ONE host-to-device copy (one staging
+        buffer reused every forward; the D2H of the next forward's counts orders it)."""
+        parts = [np.asarray(tabs[k], dtype=np.int32).reshape(-1) for k in self.TABLE_KEYS]
+        n = sum(a.size for a in parts)
+        if self._h_tab is None or self._h_tab.numel() < n:
+            cap = max(n, 1024) * 2
+            self._h_tab = torch.empty(cap, dtype=torch.int32)
+            if dev.type == "cuda":
+                self._h_tab = self._h_tab.pin_memory()
+            self._d_tab = torch.empty(cap, dtype=torch.int32, device=dev)
+        hv = self._h_tab.numpy()
+        views, o = {}, 0
+        for k, a in zip(self.TABLE_KEYS, parts):
+            hv[o:o + a.size] = a
+            views[k] = (o, a.size)
+            o += a.size
+        self._d_tab[:n].copy_(self._h_tab[:n], non_blocking=True)
+        return {k: self._d_tab[o0:o0 + sz] for k, (o0, sz) in views.items()}
 
     # phase 1 --------------------------------------------------------------
     def route(self, x, Wr, logits=None):
@@ -236,13 +263,18 @@ class EPMoE:
     def plan_and_dispatch(self, C_all: torch.Tensor):
         """C_all [R, m] gathered counts (device).  Returns send buffers + splits."""
         plan = self.ops.plan_counts(C_all)
-        C_host = C_all.to("cpu", torch.int64).numpy()
-        exec_host = plan["exec_of_expert"].to("cpu").numpy()
-        tabs = self.pl.tables(C_host, exec_host)[self.rank]
+        # one device-to-host copy (the forward's only synchronisation): counts + executor map
+        m = self.pl.m
+        both = torch.cat([C_all.reshape(-1).to(torch.int64), plan["exec_of_expert"].reshape(-1).to(torch.int64)])
+        both = both.cpu().numpy()
+        C_host = both[:-m].reshape(self.pl.R, m)
+        exec_host = both[-m:]
+        tabs = self.pl.tables(C_host, exec_host, rank=self.rank)
         dev = self.x.device
         T = self.x.shape[0]
         nrep = self.pl.nrep
-        row_base = torch.as_tensor(tabs["row_base"], dtype=torch.int32).to(dev)
+        self.dtabs = self._upload_tables(tabs, dev)
+        row_base = self.dtabs["row_base"]
         send_x = torch.empty(tabs["R_send"], self.d, dtype=self.dtype, device=dev)
         send_w = torch.empty(tabs["R_send"], dtype=torch.float32, device=dev)
         row_of = torch.empty(T * self.K * nrep, dtype=torch.int32, device=dev)
@@ -260,21 +292,21 @@ class EPMoE:
         rows = np.diff(eo)
         n_o = tb["n_orig"]
         self.last_ffn_flops = 6.0 * self.d * (self.pl.f * rows[:n_o].sum() + self.pl.f_u * rows[n_o:].sum())
-        i32 = lambda a: torch.as_tensor(np.asarray(a), dtype=torch.int32).to(dev)
+        dt = self.dtabs   # device copies of this forward's tables (one upload in plan_and_dispatch)
         Rr = recv_x.shape[0]
         gx = torch.empty_like(recv_x)
         gw = torch.empty_like(recv_w)
-        self.ops.block_copy(recv_x, gx, i32(tb["fwd_src_off"]), i32(tb["fwd_dst_start"]), recv_w, gw)
+        self.ops.block_copy(recv_x, gx, dt["fwd_src_off"], dt["fwd_dst_start"], recv_w, gw)
         h_buf = torch.empty(Rr, self.pl.f, dtype=self.dtype, device=dev)
         gy = torch.empty(Rr, self.d, dtype=self.dtype, device=dev)
         if self.timers is not None:
             self.timers[0].record()
-        self.ops.expert_ffn(gx, gw, i32(tb["exec_off"]), i32(tb["mtile_off"]), tb["n_orig"], tb["n_united"],
+        self.ops.expert_ffn(gx, gw, dt["exec_off"], dt["mtile_off"], tb["n_orig"], tb["n_united"],
                             self.pl.f_u, self.ex, self.un, h_buf, gy)
         if self.timers is not None:
             self.timers[1].record()
         ry = torch.empty_like(gy)
-        self.ops.block_copy(gy, ry, i32(tb["inv_src_off"]), i32(tb["inv_dst_start"]))
+        self.ops.block_copy(gy, ry, dt["inv_src_off"], dt["inv_dst_start"])
         return ry
 
     # phase 4 --------------------------------------------------------------
