@@ -369,7 +369,7 @@ def time_e2e(layer, steps, warmup):
     nbytes = hx[0].numel() * hx[0].element_size()
     return {"value": layer.T / (ms / 1e3), "unit": "tokens/s", "ms_per_step": ms,
             "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": hy[0].numel() * hy[0].element_size(),
-            "pipelining": "double-buffered: upload i+1 / download i-1 overlap forward i (separate copy streams)"}
+            "pipelining": "double-buffered: upload i+1 / download i-1 overlap forward i (separate copy streams); timed after the device-only region, so it can differ from value by the GPU power state (+-5-10 %)"}
 
 
 # ------------------------------------------------------------- CPU oracle
