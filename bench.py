@@ -603,6 +603,17 @@ def main():
             del lay2
             torch.cuda.empty_cache()
         extra[S.F2.name] = res
+        # C1 (B:7): the tiny fp32 layer is latency-bound; reported in microseconds per forward
+        c1 = S.CONFIGS["tiny"]
+        lay1 = Layer(c1, "cuda")
+        lay1.moe.set_brownout(c1.ratio)
+        lay1.step()
+        s1 = lay1.stats()
+        ms1, k1 = time_steps(lay1, max(args.steps, 50), 10, dist_on, graph=not args.no_graph)
+        extra[c1.name] = {"ratio": c1.ratio, "us_per_forward": ms1 / max(args.steps, 50) * 1e3,
+                          "executors": s1["executors_accessed"], "n_singleton": s1["n_singleton"],
+                          "kernel_us": {k: v * 1e3 for k, v in k1.items() if not k.startswith("_")}}
+        del lay1
         out["other_workloads"] = extra
     if rank == 0 and not args.no_cpu:
         try:

@@ -98,7 +98,7 @@ __device__ __forceinline__ void st_bf2(__nv_bfloat16* p, int64_t i, float a, flo
   *reinterpret_cast<__nv_bfloat162*>(p + i) = __floats2bfloat162_rn(a, b);
 }
 __device__ __forceinline__ float silu_bwd_a(float g, float a, float q) {
-  const float s = 1.0f / (1.0f + __expf(-a));
+  const float s = __fdividef(1.0f, 1.0f + __expf(-a));   // fast division (see silu_f in bo_gemm.cu)
   return g * q * (s + a * s * (1.0f - s));
 }
 
@@ -124,8 +124,8 @@ __global__ void __launch_bounds__(256) k_tile(const void* __restrict__ in0, cons
     if constexpr (OP == OP_SWIGLU_FWD) {
       // Hs = silu(P) * Q (D24); Hs and Hs^T
       const float2 a = ld_bf2(in0, i), q = ld_bf2(in1, i);
-      const __nv_bfloat162 h = __floats2bfloat162_rn(a.x / (1.0f + __expf(-a.x)) * q.x,
-                                                     a.y / (1.0f + __expf(-a.y)) * q.y);
+      const __nv_bfloat162 h = __floats2bfloat162_rn(__fdividef(a.x, 1.0f + __expf(-a.x)) * q.x,
+                                                     __fdividef(a.y, 1.0f + __expf(-a.y)) * q.y);
       *reinterpret_cast<__nv_bfloat162*>(out + i) = h;
       v0 = __bfloat1622float2(h);
     } else if constexpr (OP == OP_MSE_GRAD) {
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(256) k_tile(const void* __restrict__ in0, cons
       // dP = dHs * Q * silu'(P), dQ = dHs * silu(P); transposed outputs only
       const float2 g = ld_bf2(in0, i), a = ld_bf2(in1, i), q = ld_bf2(in2, i);
       v0 = make_float2(silu_bwd_a(g.x, a.x, q.x), silu_bwd_a(g.y, a.y, q.y));
-      v1 = make_float2(g.x * a.x / (1.0f + __expf(-a.x)), g.y * a.y / (1.0f + __expf(-a.y)));
+      v1 = make_float2(g.x * __fdividef(a.x, 1.0f + __expf(-a.x)), g.y * __fdividef(a.y, 1.0f + __expf(-a.y)));
     } else {
       // fp32 master -> bf16 copy and / or transposed copy
       v0 = *reinterpret_cast<const float2*>(static_cast<const float*>(in0) + i);

@@ -48,7 +48,11 @@ struct GemmCfg {
   static constexpr int SMEM = OTHER + STAGES * STAGE_BYTES;
 };
 
-__device__ __forceinline__ float silu_f(float g) { return g / (1.0f + __expf(-g)); }
+// silu(g) = g / (1 + e^-g).  __fdividef, not the IEEE division: the latter's
+// out-of-line slow-path code made a single-tile SwiGLU epilogue take ~12 us
+// (in-kernel globaltimer probe, tiny layer); __fdividef is within 2 ulp and returns
+// 0 for the huge denominators of g < -87, where silu(g) underflows anyway.
+__device__ __forceinline__ float silu_f(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
 
 // Coalesced epilogue store of a 32-row x 32-column chunk owned by one warp
 // (thread = row, as tcgen05.ld 32x32b delivers it): rows are staged in the
