@@ -978,7 +978,7 @@ __global__ void __launch_bounds__(192, 1)
           for (int j = 0; j < KMAX; ++j) {
             if (j < p.topk_k) {
               p.topk_id[grow * p.topk_k + j] = ti[j];
-              p.topk_w[grow * p.topk_k + j] = ex[j] / sum;
+              p.topk_w[grow * p.topk_k + j] = __fdividef(ex[j], sum);   // sum >= 1 (see silu_f)
             }
           }
         }
