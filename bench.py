@@ -187,34 +187,49 @@ def _capture(layer, steps, ev_sets):
     return g
 
 
-def time_steps(layer, steps, warmup, dist_on, per_kernel=True, graph=True):
+def g1t(kern):
+    """GEMM1 duration as timed inside the timed region (falls back to the instrumented replay)."""
+    return kern.get("_gemm1_swiglu_timed_region_ms", kern["gemm1_swiglu"])
+
+
+def time_steps(layer, steps, warmup, dist_on, per_kernel=True, graph=True, focus="gemm1_swiglu"):
     """W warm-up steps, then K timed steps between barrier + synchronize; device
     time with CUDA events on the launching stream; max over ranks.
 
     graph=True: the K steps are captured once into a CUDA graph and the timed
     region is one replay of it, so host launch overhead does not leak into the
-    device time of small (decode) steps.  per_kernel: the per-kernel breakdown
-    comes from a SEPARATE replay of a second graph in which the library records
-    an event before every kernel (those event nodes cost 25-45 us per decode
-    step, profiles/r01b_event_node_cost.json, so they stay out of the timed
-    region); the breakdown's own step time is reported as _instrumented_step_ms."""
+    device time of small (decode) steps.  per_kernel: inside the timed region the
+    library records only the two events around the `focus` kernel (the roofline's
+    dominant kernel, timed live over the timed region); the full per-kernel
+    breakdown comes from a separate replay of a graph with an event before every
+    kernel (those event nodes cost 25-45 us per decode step,
+    profiles/r01b_event_node_cost.json), reported with its own step time as
+    _instrumented_step_ms."""
     import torch
     for _ in range(warmup):
         layer.step()
     torch.cuda.synchronize()
     names = kernel_names(layer)
-    ev_sets = None
+    ev_sets = focus_sets = None
+    n_ev = max(11, len(names) + 1)   # the library records only when given >= (its launches + 1) slots
     if per_kernel:
-        # the library records only when given >= (its marked launches + 1) events (forward: 11)
-        n_ev = max(11, len(names) + 1)
         ev_sets = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(steps)]
         for ev in ev_sets:          # instantiate torch's lazily created events outside the capture
             for e in ev:
                 e.record()
+        if focus in names:
+            j = names.index(focus)
+            focus_sets = []
+            for _ in range(steps):
+                fs = [None] * n_ev
+                fs[j], fs[j + 1] = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                fs[j].record()
+                fs[j + 1].record()
+                focus_sets.append(fs)
         torch.cuda.synchronize()
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
-    g = _capture(layer, steps, None) if graph else None
+    g = _capture(layer, steps, focus_sets) if graph else None
     if dist_on:
         torch.distributed.barrier()
     torch.cuda.synchronize()
@@ -223,8 +238,12 @@ def time_steps(layer, steps, warmup, dist_on, per_kernel=True, graph=True):
     if g is not None:
         g.replay()
     else:
-        for _ in range(steps):
+        for i in range(steps):
+            if focus_sets:
+                layer.moe.set_profile_events(focus_sets[i])
             layer.step()
+        if focus_sets:
+            layer.moe.set_profile_events(None)
     end.record(stream)
     torch.cuda.synchronize()
     ms = start.elapsed_time(end)
@@ -258,6 +277,9 @@ def time_steps(layer, steps, warmup, dist_on, per_kernel=True, graph=True):
         spans = sorted(ev[0].elapsed_time(ev[len(names)]) for ev in ev_sets)
         q = lambda f: spans[min(len(spans) - 1, int(round(f * (len(spans) - 1))))]
         kern["_step_ms_p10_p50_p90"] = [q(0.1), q(0.5), q(0.9)]
+        if focus_sets:   # the focus kernel as timed inside the timed region (the roofline's duration)
+            j = names.index(focus)
+            kern["_" + focus + "_timed_region_ms"] = sum(fs[j].elapsed_time(fs[j + 1]) for fs in focus_sets) / steps
         del gi
     del g
     return ms, kern
@@ -477,7 +499,7 @@ def main():
     alg = algorithmic(cfg, cfg.T, st, cfg.d, cfg.f, cfg.m)
 
     # dominant kernel roofline: GEMM1 (SwiGLU), tensor-bound for prefill, HBM-bound for decode
-    g1 = kern["gemm1_swiglu"] / 1e3
+    g1 = kern.get("_gemm1_swiglu_timed_region_ms", kern["gemm1_swiglu"]) / 1e3   # live, in the timed region
     prefill_like = alg["gemm1_flops"] / max(alg["gemm1_bytes"], 1) > 300
     if prefill_like:
         ach = alg["gemm1_flops"] / g1 / 1e12
@@ -576,8 +598,8 @@ def main():
                                "frac_hbm_step": a2["bytes"] / t2 / 1e9 / pk["hbm_gbs"],
                                "frac_bf16_step": a2["flops"] / t2 / 1e12 / pk["bf16_tflops_sustained"],
                                "kernel_ms": k2,
-                               "gemm1_frac_hbm": a2["gemm1_bytes"] / (k2["gemm1_swiglu"] / 1e3) / 1e9 / pk["hbm_gbs"],
-                               "gemm1_frac_bf16": a2["gemm1_flops"] / (k2["gemm1_swiglu"] / 1e3) / 1e12
+                               "gemm1_frac_hbm": a2["gemm1_bytes"] / (g1t(k2) / 1e3) / 1e9 / pk["hbm_gbs"],
+                               "gemm1_frac_bf16": a2["gemm1_flops"] / (g1t(k2) / 1e3) / 1e12
                                / pk["bf16_tflops_sustained"]}
             extra[name] = res
         # f2: the paper's model shape (Qwen1.5-MoE-A2.7B, 60 experts top-4, 4 shared
@@ -598,7 +620,7 @@ def main():
                 "ratio": c2.ratio, "tokens_per_s": world * c2.T / t2, "ms": t2 * 1e3,
                 "executors": s2["executors_accessed"] + c2.Ns, "kernel_ms": k2,
                 "frac_bf16_step": a2["flops"] / t2 / 1e12 / pk["bf16_tflops_sustained"],
-                "gemm1_frac_bf16": a2["gemm1_flops"] / (k2["gemm1_swiglu"] / 1e3) / 1e12
+                "gemm1_frac_bf16": a2["gemm1_flops"] / (g1t(k2) / 1e3) / 1e12
                 / pk["bf16_tflops_sustained"]}
             del lay2
             torch.cuda.empty_cache()

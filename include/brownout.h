@@ -326,7 +326,8 @@ BO_API bo_status bo_distill_step(bo_handle* h, const void* X, int64_t N, float l
  * to void*) is non-NULL, each following forward records events[i] on its
  * stream immediately before its i-th kernel launch and events[L] after the
  * last one (L = launch count; requires n >= L + 1, else the events are not
- * recorded).  Pass NULL to disable.  The events stay owned by the caller. */
+ * recorded); a NULL entry skips that boundary (e.g. only the two events around
+ * one kernel).  Pass NULL to disable.  The events stay owned by the caller. */
 BO_API bo_status bo_set_profile_events(bo_handle* h, void** events, int32_t n);
 
 /* Number of GPU kernels the last forward on this handle enqueued. */

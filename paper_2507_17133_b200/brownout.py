@@ -232,15 +232,16 @@ class BrownoutMoE:
 
     def set_profile_events(self, events):
         """events: list of torch.cuda.Event(enable_timing=True) (>= launches + 1),
-        recorded around every kernel of the following forwards; None disables."""
+        recorded around every kernel of the following forwards (None entries skip
+        that boundary); events=None disables."""
         if events is None:
             self._prof = None
             _check(_lib.bo_set_profile_events(self._h, None, 0))
             return
         for e in events:      # torch creates the underlying cudaEvent_t lazily, on first record
-            if not e.cuda_event:
+            if e is not None and not e.cuda_event:
                 e.record()
-        arr = (C.c_void_p * len(events))(*[C.c_void_p(e.cuda_event) for e in events])
+        arr = (C.c_void_p * len(events))(*[C.c_void_p(e.cuda_event if e is not None else None) for e in events])
         self._prof = (events, arr)
         _check(_lib.bo_set_profile_events(self._h, arr, len(events)))
 

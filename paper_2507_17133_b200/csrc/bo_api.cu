@@ -241,7 +241,8 @@ struct Prof {
       if (!h->last_kernels.empty()) h->last_kernels += ",";
       h->last_kernels += name;
     }
-    if (on && err == cudaSuccess) err = cudaEventRecordWithFlags(static_cast<cudaEvent_t>(h->prof_events[i]), s, flags);
+    if (on && err == cudaSuccess && h->prof_events[i])   // NULL entries: no event at that boundary
+      err = cudaEventRecordWithFlags(static_cast<cudaEvent_t>(h->prof_events[i]), s, flags);
   }
 };
 
