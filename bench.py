@@ -192,15 +192,15 @@ def g1t(kern):
     return kern.get("_gemm1_swiglu_timed_region_ms", kern["gemm1_swiglu"])
 
 
-def time_steps(layer, steps, warmup, dist_on, per_kernel=True, graph=True, focus="gemm1_swiglu"):
+def time_steps(layer, steps, warmup, dist_on, per_kernel=True, graph=True, focus=None):
     """W warm-up steps, then K timed steps between barrier + synchronize; device
     time with CUDA events on the launching stream; max over ranks.
 
     graph=True: the K steps are captured once into a CUDA graph and the timed
     region is one replay of it, so host launch overhead does not leak into the
-    device time of small (decode) steps.  per_kernel: inside the timed region the
-    library records only the two events around the `focus` kernel (the roofline's
-    dominant kernel, timed live over the timed region); the full per-kernel
+    device time of small (decode) steps.  per_kernel: with `focus` (the headline's
+    roofline kernel) the library records only the two events around that kernel
+    inside the timed region (timed live there); the full per-kernel
     breakdown comes from a separate replay of a graph with an event before every
     kernel (those event nodes cost 25-45 us per decode step,
     profiles/r01b_event_node_cost.json), reported with its own step time as
@@ -492,7 +492,8 @@ def main():
     launches = layer.moe.last_launch_count()
 
     with ClockSampler(local) as clk:
-        ms, kern = time_steps(layer, args.steps, max(args.warmup, 3), dist_on, graph=not args.no_graph)
+        ms, kern = time_steps(layer, args.steps, max(args.warmup, 3), dist_on, graph=not args.no_graph,
+                              focus="gemm1_swiglu")   # the roofline kernel, timed live in the timed region
     clocks = clk.summary()
     ms_step = ms / args.steps
     value = world * cfg.T / (ms_step / 1e3)
