@@ -46,6 +46,8 @@ struct bo_handle {
   int32_t router_split;  // 1: decode-sized batches use k_router_split (env BO_ROUTER_SPLIT=0 disables)
   int32_t router_mma;    // 1: prefill-sized bf16 batches with m <= 32 use k_router_mma (env BO_ROUTER_MMA=0 disables)
   int32_t tile_alt;      // 1: GEMM1 may pick a narrower SwiGLU tile on the device (env BO_TILE_ALT=0 disables)
+  int32_t swap_tail;     // bit 0: CTA-pair GEMM1 runs each executor's ragged last m-tile with swapped
+                         // operands (default on); bit 1: GEMM2 likewise (off: measured slower).  env BO_SWAP_TAIL
   int32_t store_hint;    // 1: FFN GEMM epilogue stores hint L2 evict_first (env BO_STORE_HINT=0 disables)
   int32_t fused_combine; // combine (a8) in GEMM2's epilogue: 0 never, 1 always, 2 auto (env BO_FUSED_COMBINE=0/1, default auto)
   std::string last_kernels;   // comma-separated names of the kernels the last forward launched
@@ -442,10 +444,28 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
         return st;
     }
     bo::GemmParams p{};
+    // 256 x 256 tiles on CTA pairs when rows are plentiful (prefill); few-row
+    // (decode) steps keep 128-row tiles so that more tiles share the SMs.
+    const bool pair = h->cta_pairs && dt == 0 && bn == 256 && R >= h->pair_rows1;
+    // swapped-operand tail tiles (pairs): maps [6..11] = 64-row gate / up boxes,
+    // [12..14] = Xp in 16 / 32 / 64-row boxes
+    const bool swap = pair && !gather && (h->swap_tail & 1) && c.weight_layout != BO_WEIGHTS_TILED;
+    if (swap) {
+      for (int k = 0; k < 3; ++k) {
+        const int width = k == 1 ? f_u : f;
+        if ((st = make_map(&mb.m[6 + 2 * k], ptr(*cls[k], 0), c.dtype, rows_of(*cls[k], width), d, 64)) != BO_OK)
+          return st;
+        if ((st = make_map(&mb.m[7 + 2 * k], ptr(*cls[k], 1), c.dtype, rows_of(*cls[k], width), d, 64)) != BO_OK)
+          return st;
+      }
+      for (int i = 0; i < 3; ++i)
+        if ((st = make_map(&mb.m[12 + i], X, c.dtype, R, d, 16u << i)) != BO_OK) return st;
+      p.swap_tail = 1;
+    }
     // alternative tile width for the device-side wave choice: the widest gate/up half
     // below bn/2 (multiple of 16, >= 64) that divides both widths
     int bh_alt = 0;
-    if (h->tile_alt && !gather && c.weight_layout != BO_WEIGHTS_TILED)   // packed bands are 128 rows
+    if (h->tile_alt && !gather && !swap && c.weight_layout != BO_WEIGHTS_TILED)   // packed bands are 128 rows
       for (int bh = bn / 2 - 16; bh >= 64 && !bh_alt; bh -= 16)
         if (f % bh == 0 && f_u % bh == 0) bh_alt = bh;
     if (bh_alt) {
@@ -486,9 +506,6 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
       if (bn2 > tier) bn2 = tier;
       set_comb(p, comb, d, d / bn2);   // GEMM1's prologue zeroes GEMM2's arrival counters
     }
-    // 256 x 256 tiles on CTA pairs when rows are plentiful (prefill); few-row
-    // (decode) steps keep 128-row tiles so that more tiles share the SMs.
-    const bool pair = h->cta_pairs && dt == 0 && bn == 256 && R >= h->pair_rows1;
     const int tile_m = pair ? 2 * bo::kBM : bo::kBM;
     const int64_t max_work = ((R + tile_m - 1) / tile_m + n_exec) * p.n_tiles;
     const int units = pair ? h->num_sms / 2 : h->num_sms;
@@ -513,6 +530,11 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     CUtensorMap mA;
     bo::BMaps mb;
     if ((st = make_map(&mA, Hbuf, c.dtype, R, f, bo::kBM)) != BO_OK) return st;
+    // swapped-operand tail tiles (pairs, no split-K): [12..14] = H in 16 / 32 / 64-row boxes
+    if (pair && (h->swap_tail & 2) && !partial && c.weight_layout != BO_WEIGHTS_TILED) {
+      for (int i = 0; i < 3; ++i)
+        if ((st = make_map(&mb.m[12 + i], Hbuf, c.dtype, R, f, 16u << i)) != BO_OK) return st;
+    }
     const FfnClass* cls[3] = {&orig, &uni, &shr};
     for (int k = 0; k < 3; ++k) {
       const FfnClass& q = cls[k]->Wg ? *cls[k] : any;
@@ -522,6 +544,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
       mb.m[2 * k + 1] = mb.m[2 * k];
     }
     bo::GemmParams p{};
+    p.swap_tail = (pair && (h->swap_tail & 2) && !partial && c.weight_layout != BO_WEIGHTS_TILED) ? 1 : 0;
     p.Kdim = f;
     p.n_tiles = d / bn;
     p.Kdim_u = f_u;
@@ -1180,6 +1203,10 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   h->fused_combine = (fc && fc[0] == '0') ? 0 : ((fc && fc[0] == '1') ? 1 : 2);
   const char* ta = getenv("BO_TILE_ALT");
   h->tile_alt = (ta && ta[0] == '0') ? 0 : 1;
+  // Swapped-operand tail tiles: GEMM1 C2 1.495 -> 1.423 ms (ratio 0.5), 1.532 -> 1.476 (ratio 0);
+  // GEMM2 + fused combine 0.814 -> 0.866 ms, so GEMM1 only (profiles/r01_ab_swap_tail.json)
+  const char* swt = getenv("BO_SWAP_TAIL");
+  h->swap_tail = swt ? (atoi(swt) & 3) : 1;
   const char* rm = getenv("BO_ROUTER_MMA");
   h->router_mma = (rm && rm[0] == '0') ? 0 : 1;
   const char* rs = getenv("BO_ROUTER_SPLIT");

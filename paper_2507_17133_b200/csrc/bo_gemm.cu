@@ -154,6 +154,8 @@ __device__ __forceinline__ void topk_insert(float (&tv)[KMAX], int (&ti)[KMAX], 
 }
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+// two epilogue warps (swapped tail tiles: the gate warp and the up warp of the same columns)
+__device__ __forceinline__ void pair_bar(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 
 __device__ __forceinline__ void st_release_gpu(int* ptr, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(ptr), "r"(v) : "memory");
@@ -362,8 +364,8 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     for (int i = 0; i < 6; ++i) tma_prefetch_desc(&tmB.m[i]);
-    if (p.bh_alt > 0)
-      for (int i = 6; i < 12; ++i) tma_prefetch_desc(&tmB.m[i]);
+    if (p.bh_alt > 0 || p.swap_tail)
+      for (int i = 6; i < (p.swap_tail ? 15 : 12); ++i) tma_prefetch_desc(&tmB.m[i]);
   }
   if constexpr (CG == 2) cluster_sync();   // peer barriers initialised before any remote arrive / alloc
   if (warp == 1) {
@@ -462,6 +464,23 @@ __global__ void __launch_bounds__(192, 1)
     }
   }
   const uint32_t idesc = alt ? idesc_f32acc<T>(128 * CG, 2 * bh) : IDESC;
+  // Swapped-operand tail tile (CTA pairs, SwiGLU): an executor's last m-tile holding
+  // rin < 256 rows computes D^T = [Wg; Wu] Xp^T instead, with this CTA's 64 gate and
+  // 64 up weight rows on the MMA's M side (TMEM lanes 0-63 gate, 64-127 up of the same
+  // columns) and the tile's rows, rounded up to 32, on N (each CTA stages half of
+  // them).  The MMA and the shared-memory traffic then scale with rin instead of a
+  // full 256-row tile.  Three TMA boxes per k-block (gate, up, rows): the TMA issue
+  // cost of 16-row boxes (8-12 per k-block) made such a tile slower than a full one.
+  // GEMM2 (EPI_WEIGHTED) likewise: this CTA's 128 Wd rows (output columns) on M, the
+  // tile's H rows on N; the epilogue writes Yp column-sliced and counts columns for
+  // the fused combine.
+  constexpr bool kSwap = CG == 2 && (EPI == EPI_SWIGLU || EPI == EPI_WEIGHTED) && !GATHER;
+  const bool swap_ok = kSwap && p.swap_tail && !alt && !p.a_shared && !p.b_packed &&
+                       (EPI != EPI_WEIGHTED || (p.ksplit_max <= 1 && !p.f32_mode));
+  auto tile_rows = [&](int x, int mi) {   // rows of executor x in m-tile mi
+    const int r = s_eoff[x + 1] - s_eoff[x] - mi * TILE_M;
+    return r < TILE_M ? r : TILE_M;
+  };
   const int stage_tx = C::A_BYTES + (EPI == EPI_SWIGLU ? 2 * bh : BN) * 128 / CG;   // bytes per CTA per stage
   const int base_work = start_of(nexec);
   auto kblocks = [&](int x) { return (x < mo || x >= mu ? p.Kdim : p.Kdim_u) / C::BK; };
@@ -627,6 +646,35 @@ __global__ void __launch_bounds__(192, 1)
           tok.z = r + 2 < p.rows_total ? __ldg(p.row_tok + r + 2) : 0;
           tok.w = r + 3 < p.rows_total ? __ldg(p.row_tok + r + 3) : 0;
         }
+        if constexpr (kSwap) {
+          const int rin = tile_rows(x, mi);
+          if (swap_ok && rin < TILE_M) {
+            const int nsh = ((rin + 31) & ~31) / 2;   // token rows staged by this CTA (N / 2)
+            const int wrow = brow + n * 128 + static_cast<int>(crank) * 64;
+            const int trow = s_eoff[x] + mi * TILE_M + static_cast<int>(crank) * nsh;
+            // one box of >= nsh rows (16 / 32 / 64 / 128; rows past nsh land unused)
+            const int tbox = nsh <= 16 ? 16 : (nsh <= 32 ? 32 : (nsh <= 64 ? 64 : 128));
+            const CUtensorMap* mt = tbox == 128 ? &tmA : &tmB.m[tbox == 16 ? 12 : (tbox == 32 ? 13 : 14)];
+            for (int kb = kb0; kb < kb1; ++kb) {
+              mbar_wait(&empty_bar[stage], phase ^ 1);
+              uint8_t* sa = smem + stage * C::STAGE_BYTES;
+              if (lane == 0) {
+                if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * (C::A_BYTES + tbox * 128));
+                else mbar_arrive_remote(&full_bar[stage], 0);
+                if constexpr (EPI == EPI_SWIGLU) {
+                  tma_load_2d_pair(sa, &tmB.m[6 + 2 * cls], &full_bar[stage], kb * C::BK, wrow, pol_b);
+                  tma_load_2d_pair(sa + 64 * 128, &tmB.m[7 + 2 * cls], &full_bar[stage], kb * C::BK, wrow, pol_b);
+                } else {   // Wd rows n * BN + crank * 128 .. + 127 (the pair's usual B half box)
+                  tma_load_2d_pair(sa, &tmB.m[2 * cls], &full_bar[stage], kb * C::BK,
+                                   brow + n * BN + static_cast<int>(crank) * 128, pol_b);
+                }
+                tma_load_2d_pair(sa + C::A_BYTES, mt, &full_bar[stage], kb * C::BK, trow, pol_a);
+              }
+              if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+            continue;
+          }
+        }
         // L2 prefetch of the first pf_dist k-blocks' B tiles of this segment (weight
         // streaming: more DRAM requests in flight than the stage ring holds)
         if (p.pf_dist > 0 && !p.b_packed && lane == 0) {
@@ -700,6 +748,11 @@ __global__ void __launch_bounds__(192, 1)
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+        uint32_t idesc_t = idesc;
+        if constexpr (kSwap) {
+          const int rin = tile_rows(x, mi);
+          if (swap_ok && rin < TILE_M) idesc_t = idesc_f32acc<T>(256, (rin + 31) & ~31);
+        }
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
@@ -711,7 +764,7 @@ __global__ void __launch_bounds__(192, 1)
             if constexpr (CG == 1)
               mma_ss<T>(sdesc_k_sw128(a_addr + k * 32), sdesc_k_sw128(b_addr + k * 32), d_tmem, idesc, accum);
             else
-              mma_ss_pair_bf16(sdesc_k_sw128(a_addr + k * 32), sdesc_k_sw128(b_addr + k * 32), d_tmem, idesc, accum);
+              mma_ss_pair_bf16(sdesc_k_sw128(a_addr + k * 32), sdesc_k_sw128(b_addr + k * 32), d_tmem, idesc_t, accum);
           }
           if constexpr (CG == 1) tc_commit(&empty_bar[stage]);
           else tc_commit_pair(&empty_bar[stage]);   // frees the stage in both CTAs
@@ -840,10 +893,101 @@ __global__ void __launch_bounds__(192, 1)
       const int nrows = rows_x - slab < 0 ? 0 : (rows_x - slab > 32 ? 32 : rows_x - slab);
       const int64_t row0 = static_cast<int64_t>(s_eoff[x]) + slab;
       uint8_t* stage = s_epi + (warp - 2) * 32 * C::EPI_ROW;
+      bool swapped = false;
+      // swapped GEMM2 tail tile: Yp stores here, the shared release / count / combine below
+      int sw_rin = 0;
+      if constexpr (kSwap && EPI == EPI_WEIGHTED) {
+        const int rin = tile_rows(x, mi);
+        if (swap_ok && rin < TILE_M) {
+          // D^T tile: lane = output column col0 + lane, TMEM column = the tile's row:
+          // Yp[row, cols] = row_w[row] * acc, staged [32 rows][32 columns] per warp.
+          sw_rin = rin;
+          const int ns = (rin + 31) & ~31;
+          T* out = reinterpret_cast<T*>(p.out) + n * BN + static_cast<int>(crank) * 128 + q * 32;
+          const int64_t tok0 = static_cast<int64_t>(s_eoff[x]) + mi * TILE_M;
+#pragma unroll 1
+          for (int c = 0; c < ns; c += 32) {
+            uint32_t v[32];
+            tmem_ld32(t0 + c, v);
+            tmem_ld_wait();
+            const float wl = c + lane < rin ? (p.row_w ? p.row_w[tok0 + c + lane] : p.alpha) : 0.0f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              *reinterpret_cast<T*>(stage + j * C::EPI_ROW + lane * (int)sizeof(T)) =
+                  static_cast<T>(__uint_as_float(v[j]) * __shfl_sync(0xffffffffu, wl, j));
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int pc = i * 32 + lane, tk = pc >> 2, part = pc & 3;
+              if (c + tk < rin) {
+                const uint4 val = *reinterpret_cast<const uint4*>(stage + tk * C::EPI_ROW + part * 16);
+                T* dst = out + (tok0 + c + tk) * p.ldo + part * (16 / (int)sizeof(T));
+                if (pol_out) st_global_hint(dst, val, pol_out);
+                else *reinterpret_cast<uint4*>(dst) = val;
+              }
+            }
+            __syncwarp();
+          }
+        }
+      }
+      if constexpr (kSwap && EPI == EPI_SWIGLU) {
+        const int rin = tile_rows(x, mi);
+        if (swap_ok && rin < TILE_M) {
+          // D^T tile: lane = weight row, TMEM column = the tile's row.  Warp q < 2 holds
+          // the gate rows of columns colb..colb+31, warp q + 2 their up rows: the up warp
+          // hands its values over through its staging tile, 16 rows at a time; the gate
+          // warp computes H, stages [32 rows][32 columns] and writes it back.
+          swapped = true;
+          const int ns = (rin + 31) & ~31;
+          const bool up_w = q >= 2;
+          const int bid = 2 + (q & 1);
+          float* xch = reinterpret_cast<float*>(s_epi + (q & 1) * 32 * C::EPI_ROW);   // the up warp's tile
+          T* out = reinterpret_cast<T*>(p.out) + n * 128 + static_cast<int>(crank) * 64 + (q & 1) * 32;
+          const int64_t tok0 = static_cast<int64_t>(s_eoff[x]) + mi * TILE_M;
+#pragma unroll 1
+          for (int c = 0; c < ns; c += 32) {
+            uint32_t v[32];
+            tmem_ld32(t0 + c, v);
+            tmem_ld_wait();
+            float hv[32];
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+              pair_bar(bid);   // the previous half has been read
+              if (up_w) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) xch[j * 32 + lane] = __uint_as_float(v[hf * 16 + j]);
+              }
+              pair_bar(bid);
+              if (!up_w) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                  hv[hf * 16 + j] = silu_f(__uint_as_float(v[hf * 16 + j])) * xch[j * 32 + lane];
+              }
+            }
+            if (!up_w) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                *reinterpret_cast<T*>(stage + j * C::EPI_ROW + lane * (int)sizeof(T)) = static_cast<T>(hv[j]);
+              __syncwarp();
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int pc = i * 32 + lane, tk = pc >> 2, part = pc & 3;
+                if (c + tk < rin) {
+                  const uint4 val = *reinterpret_cast<const uint4*>(stage + tk * C::EPI_ROW + part * 16);
+                  T* dst = out + (tok0 + c + tk) * p.ldo + part * (16 / (int)sizeof(T));
+                  if (pol_out) st_global_hint(dst, val, pol_out);
+                  else *reinterpret_cast<uint4*>(dst) = val;
+                }
+              }
+              __syncwarp();
+            }
+          }
+        }
+      }
       if constexpr (EPI == EPI_SWIGLU) {
         T* out = reinterpret_cast<T*>(p.out) + n * bh;
 #pragma unroll 1
-        for (int c = 0; c < bh; c += 32) {
+        for (int c = 0; c < (swapped ? 0 : bh); c += 32) {
           // a 16-column tail (bh % 32 == 16) reads 16 columns past each half (inside
           // this accumulator's BN-column slot) and stores only the valid ones
           uint32_t g[32], u[32];
@@ -892,7 +1036,7 @@ __global__ void __launch_bounds__(192, 1)
         }
         T* out = reinterpret_cast<T*>(p.out) + n * BN;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
+        for (int c = 0; c < (sw_rin ? 0 : BN); c += 32) {
           uint32_t a[32];
           tmem_ld32(t0 + c, a);
           tmem_ld_wait();
@@ -916,27 +1060,38 @@ __global__ void __launch_bounds__(192, 1)
           }
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
           // Release this warp's Yp rows (every lane fences its own stores, then the
-          // warp barrier), count each row against its token; the warp whose
-          // arrival completes a token sums its rows for this n-tile.
-          int t = -1;
-          int need = 0;
-          int rr[kCombSlots];
-          if (valid) t = __ldg(p.row_tok + grow);
-#pragma unroll
-          for (int sl = 0; sl < kCombSlots; ++sl) {
-            rr[sl] = (valid && sl < p.comb_KR) ? __ldg(p.row_of + static_cast<int64_t>(t) * p.comb_KR + sl) : -1;
-            need += rr[sl] >= 0 ? 1 : 0;
-          }
+          // warp barrier), count each row against its token; the warp whose arrival
+          // completes a token sums its rows for this n-tile.  Arrivals are counted in
+          // columns: a row is complete when all BN columns of every slot have landed (a
+          // swapped tail tile's warps each deliver 32 columns of 32 rows per chunk).
           __threadfence();
           __syncwarp();
-          const bool last = valid && atomicAdd(p.comb_cnt + static_cast<int64_t>(t) * p.comb_nt + n, 1) == need - 1;
-          const uint32_t done = __ballot_sync(0xffffffffu, last);
-          if (done) {
-            __threadfence();   // acquire: the other rows' stores precede their counts
-            const T* yb = reinterpret_cast<const T*>(p.out);
-            if (p.comb_KR <= 2) combine_tokens_batched<T, 2, 4>(p, yb, p.ldo, done, t, rr, n * BN, BN, lane);
-            else if (p.comb_KR <= 4) combine_tokens_batched<T, 4, 2>(p, yb, p.ldo, done, t, rr, n * BN, BN, lane);
-            else combine_tokens_batched<T, 8, 2>(p, yb, p.ldo, done, t, rr, n * BN, BN, lane);
+          const int iters = sw_rin ? (sw_rin + 31) >> 5 : 1;
+          const int add = sw_rin ? 32 : BN;
+          const int64_t tok0 = static_cast<int64_t>(s_eoff[x]) + mi * TILE_M;
+#pragma unroll 1
+          for (int it = 0; it < iters; ++it) {
+            const bool rv = sw_rin ? it * 32 + lane < sw_rin : valid;
+            const int64_t gr = sw_rin ? tok0 + it * 32 + lane : grow;
+            int t = -1;
+            int need = 0;
+            int rr[kCombSlots];
+            if (rv) t = __ldg(p.row_tok + gr);
+#pragma unroll
+            for (int sl = 0; sl < kCombSlots; ++sl) {
+              rr[sl] = (rv && sl < p.comb_KR) ? __ldg(p.row_of + static_cast<int64_t>(t) * p.comb_KR + sl) : -1;
+              need += rr[sl] >= 0 ? 1 : 0;
+            }
+            const bool last =
+                rv && atomicAdd(p.comb_cnt + static_cast<int64_t>(t) * p.comb_nt + n, add) == need * BN - add;
+            const uint32_t done = __ballot_sync(0xffffffffu, last);
+            if (done) {
+              __threadfence();   // acquire: the other rows' stores precede their counts
+              const T* yb = reinterpret_cast<const T*>(p.out);
+              if (p.comb_KR <= 2) combine_tokens_batched<T, 2, 4>(p, yb, p.ldo, done, t, rr, n * BN, BN, lane);
+              else if (p.comb_KR <= 4) combine_tokens_batched<T, 4, 2>(p, yb, p.ldo, done, t, rr, n * BN, BN, lane);
+              else combine_tokens_batched<T, 8, 2>(p, yb, p.ldo, done, t, rr, n * BN, BN, lane);
+            }
           }
           continue;
         }

@@ -74,6 +74,11 @@ struct GemmParams {
   int stream_k;             // 1: enabled (grid must be resident: <= #SM, 1 CTA / SM)
   float* sk_part;           // [grid, 128, kSkCols] partial of each contributing CTA
   int* sk_flag;             // [grid] 1 = partial published (reset to 0 by the owner; zero before first use)
+  // Swapped-operand tail tiles (CG = 2 SwiGLU, BN = 256): an executor's last m-tile with
+  // fewer than 256 rows runs as D^T = W X^T, the 256 gate / up weight rows on the MMA's
+  // M side and its rows (rounded up to 32) on N, so a ragged tile costs its rows, not 256.
+  // Maps [6..11] then hold 64-row gate / up boxes and [12..14] 16 / 32 / 64-row boxes of A (Xp).
+  int swap_tail;
 };
 
 // Combine of split-K fp32 partials: y[t] = [x_t] + sum_slots sum_splits P[sp][row].
@@ -87,9 +92,10 @@ cudaError_t launch_combine_partials(int dtype, const float* partial, const int* 
 // B operand maps by executor class: [0]/[1] originals (gate or the only B / up),
 // [2]/[3] united experts, [4]/[5] shared experts (Eq. 5 second term).
 // [6..11]: the same three classes encoded for the alternative SwiGLU tile
-// width (GemmParams::bh_alt rows per gate / up half), when it is enabled.
+// width (GemmParams::bh_alt rows per gate / up half), when it is enabled, or the
+// 64-row gate / up boxes of the swapped tail tiles (GemmParams::swap_tail; [12..14] = A).
 struct BMaps {
-  CUtensorMap m[12];
+  CUtensorMap m[15];
 };
 cudaError_t launch_grouped_gemm(int dtype, int epi, int bn, const CUtensorMap& A, const BMaps& B,
                                 const GemmParams& p, int grid, cudaStream_t s);
