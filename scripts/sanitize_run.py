@@ -1,7 +1,8 @@
 """Small forwards over the library's code paths, for compute-sanitizer
 (memcheck / racecheck / synccheck / initcheck): bf16 decode and CTA-pair prefill,
 fp32 (tf32), shared experts, united-row de-duplication, full brownout, the TILED
-weight layout, the fused combine and the split-tile schedules.  Exits non-zero if
+weight layout, the fused combine, the split-tile schedules and the swapped
+tail tiles (GEMM1 default, GEMM2 with BO_SWAP_TAIL=3).  Exits non-zero if
 a forward disagrees with the ROWMAJOR / default path of the same inputs."""
 import os
 import sys
@@ -33,6 +34,19 @@ def run(cfg, ratio=0.5, mode="partial", dedup=False, tiled=False, logits=True):
     return y
 
 
+def run_env(env, *a, **k):
+    old = {n: os.environ.get(n) for n in env}
+    os.environ.update(env)
+    try:
+        return run(*a, **k)
+    finally:
+        for n, v in old.items():
+            if v is None:
+                os.environ.pop(n, None)
+            else:
+                os.environ[n] = v
+
+
 def main():
     small = S.LayerConfig("s", d=256, f=512, m=8, K=2, way=4, T=200, ratio=0.5, dtype="bf16", sigma=0.7,
                           config_id=71)
@@ -48,7 +62,8 @@ def main():
         ("decode", lambda: run(small)),
         ("decode_ratio1", lambda: run(small, ratio=1.0)),
         ("router_gpu", lambda: run(small, logits=False)),
-        ("prefill_pairs_fused_combine", lambda: run(pair)),
+        ("prefill_pairs_fused_combine", lambda: run(pair)),   # GEMM1 swapped tail tiles (default)
+        ("prefill_pairs_swap_gemm2", lambda: run_env({"BO_SWAP_TAIL": "3"}, pair)),
         ("fp32", lambda: run(fp32)),
         ("qwen_like_tc_router", lambda: run(qwen, logits=False)),
         ("shared", lambda: run(shared)),
