@@ -47,7 +47,7 @@ struct bo_handle {
   int32_t router_mma;    // 1: prefill-sized bf16 batches with m <= 32 use k_router_mma (env BO_ROUTER_MMA=0 disables)
   int32_t tile_alt;      // 1: GEMM1 may pick a narrower SwiGLU tile on the device (env BO_TILE_ALT=0 disables)
   int32_t swap_tail;     // bit 0: CTA-pair GEMM1 runs each executor's ragged last m-tile with swapped
-                         // operands (default on); bit 1: GEMM2 likewise (off: measured slower).  env BO_SWAP_TAIL
+                         // operands (default on); bit 1: GEMM2 likewise (off: neutral).  env BO_SWAP_TAIL
   int32_t store_hint;    // 1: FFN GEMM epilogue stores hint L2 evict_first (env BO_STORE_HINT=0 disables)
   int32_t fused_combine; // combine (a8) in GEMM2's epilogue: 0 never, 1 always, 2 auto (env BO_FUSED_COMBINE=0/1, default auto)
   std::string last_kernels;   // comma-separated names of the kernels the last forward launched
@@ -1203,8 +1203,8 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   h->fused_combine = (fc && fc[0] == '0') ? 0 : ((fc && fc[0] == '1') ? 1 : 2);
   const char* ta = getenv("BO_TILE_ALT");
   h->tile_alt = (ta && ta[0] == '0') ? 0 : 1;
-  // Swapped-operand tail tiles: GEMM1 C2 1.495 -> 1.423 ms (ratio 0.5), 1.532 -> 1.476 (ratio 0);
-  // GEMM2 + fused combine 0.814 -> 0.866 ms, so GEMM1 only (profiles/r01_ab_swap_tail.json)
+  // Swapped-operand tail tiles: GEMM1 C2 1.329 -> 1.305 ms (ratio 0.5), 1.393 -> 1.352 (ratio 0)
+  // (profiles/r01_ncu_ab_swap_tail.txt); GEMM2 neutral (-1.5 .. +0.5 %), so GEMM1 only by default
   const char* swt = getenv("BO_SWAP_TAIL");
   h->swap_tail = swt ? (atoi(swt) & 3) : 1;
   const char* rm = getenv("BO_ROUTER_MMA");

@@ -1063,14 +1063,19 @@ __global__ void __launch_bounds__(192, 1)
           // warp barrier), count each row against its token; the warp whose arrival
           // completes a token sums its rows for this n-tile.  Arrivals are counted in
           // columns: a row is complete when all BN columns of every slot have landed (a
-          // swapped tail tile's warps each deliver 32 columns of 32 rows per chunk).
+          // swapped tail tile's CTAs each deliver BN / 2 columns of its rows).
+          // A swapped tile's four warps first meet at the epilogue barrier (each lane's
+          // stores fenced before it), so each row is counted once per CTA with the CTA's
+          // BN / 2 columns; the warps split the row chunks.  (One arrival per warp and
+          // row made 8 atomics per row on the same counter and cost ~30 us per wave.)
           __threadfence();
-          __syncwarp();
+          if (sw_rin) epi_bar();
+          else __syncwarp();
           const int iters = sw_rin ? (sw_rin + 31) >> 5 : 1;
-          const int add = sw_rin ? 32 : BN;
+          const int add = sw_rin ? BN / 2 : BN;
           const int64_t tok0 = static_cast<int64_t>(s_eoff[x]) + mi * TILE_M;
 #pragma unroll 1
-          for (int it = 0; it < iters; ++it) {
+          for (int it = sw_rin ? q : 0; it < iters; it += sw_rin ? 4 : 1) {
             const bool rv = sw_rin ? it * 32 + lane < sw_rin : valid;
             const int64_t gr = sw_rin ? tok0 + it * 32 + lane : grow;
             int t = -1;
