@@ -130,9 +130,16 @@ def test_ep_gloo_matches_single_process_oracle(world, ratio):
 
 # ------------------------------------------------------------ one-GPU virtual EP
 @pytest.mark.gpu
+@pytest.mark.parametrize("env", [{}, {"BO_PAIR_ROWS1": "1", "BO_PAIR_ROWS2": "1", "BO_SWAP_TAIL": "3"}],
+                         ids=["default", "pairs_swapped_tails"])
 @pytest.mark.parametrize("R", [1, 2, 4, 8])
 @pytest.mark.parametrize("ratio", [0.0, 0.5, 1.0])
-def test_virtual_ep_on_gpu_matches_oracle(R, ratio):
+def test_virtual_ep_on_gpu_matches_oracle(R, ratio, env, monkeypatch):
+    """Expert parallelism on one GPU (R virtual ranks, f-sliced united experts);
+    the second variant runs the FFN GEMMs on CTA pairs with swapped tail tiles,
+    whose united class then has its own width f / R."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     from paper_2507_17133_b200 import BrownoutMoE
     from paper_2507_17133_b200.ep import EPMoE, virtual_ep_forward
     cfg = S.LayerConfig("ep_gpu", d=256, f=512, m=8, K=2, way=4, T=96, ratio=ratio, dtype="bf16", sigma=0.7,
