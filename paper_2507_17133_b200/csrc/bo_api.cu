@@ -48,6 +48,7 @@ struct bo_handle {
   int32_t tile_alt;      // 1: GEMM1 may pick a narrower SwiGLU tile on the device (env BO_TILE_ALT=0 disables)
   int32_t swap_tail;     // bit 0: CTA-pair GEMM1 runs each executor's ragged last m-tile with swapped
                          // operands (default on); bit 1: GEMM2 likewise (off: neutral).  env BO_SWAP_TAIL
+  int32_t swap_max;      // largest tail (rows) that runs swapped; 0 = any (env BO_SWAP_MAX)
   int32_t store_hint;    // 1: FFN GEMM epilogue stores hint L2 evict_first (env BO_STORE_HINT=0 disables)
   int32_t fused_combine; // combine (a8) in GEMM2's epilogue: 0 never, 1 always, 2 auto (env BO_FUSED_COMBINE=0/1, default auto)
   std::string last_kernels;   // comma-separated names of the kernels the last forward launched
@@ -461,6 +462,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
       for (int i = 0; i < 3; ++i)
         if ((st = make_map(&mb.m[12 + i], X, c.dtype, R, d, 16u << i)) != BO_OK) return st;
       p.swap_tail = 1;
+      p.swap_max = h->swap_max;
     }
     // alternative tile width for the device-side wave choice: the widest gate/up half
     // below bn/2 (multiple of 16, >= 64) that divides both widths
@@ -545,6 +547,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     }
     bo::GemmParams p{};
     p.swap_tail = (pair && (h->swap_tail & 2) && !partial && c.weight_layout != BO_WEIGHTS_TILED) ? 1 : 0;
+    p.swap_max = h->swap_max;
     p.Kdim = f;
     p.n_tiles = d / bn;
     p.Kdim_u = f_u;
@@ -1205,6 +1208,8 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   h->tile_alt = (ta && ta[0] == '0') ? 0 : 1;
   // Swapped-operand tail tiles: GEMM1 C2 1.329 -> 1.305 ms (ratio 0.5), 1.393 -> 1.352 (ratio 0)
   // (profiles/r01_ncu_ab_swap_tail.txt); GEMM2 neutral (-1.5 .. +0.5 %), so GEMM1 only by default
+  const char* swm = getenv("BO_SWAP_MAX");
+  h->swap_max = swm ? atoi(swm) : 0;
   const char* swt = getenv("BO_SWAP_TAIL");
   h->swap_tail = swt ? (atoi(swt) & 3) : 1;
   const char* rm = getenv("BO_ROUTER_MMA");

@@ -477,6 +477,8 @@ __global__ void __launch_bounds__(192, 1)
   constexpr bool kSwap = CG == 2 && (EPI == EPI_SWIGLU || EPI == EPI_WEIGHTED) && !GATHER;
   const bool swap_ok = kSwap && p.swap_tail && !alt && !p.a_shared && !p.b_packed &&
                        (EPI != EPI_WEIGHTED || (p.ksplit_max <= 1 && !p.f32_mode));
+  // largest tail swapped: a tail near 256 rows gains no MMA work and loses pipelining
+  const int swap_lim = p.swap_max > 0 && p.swap_max < TILE_M ? p.swap_max : TILE_M - 1;
   auto tile_rows = [&](int x, int mi) {   // rows of executor x in m-tile mi
     const int r = s_eoff[x + 1] - s_eoff[x] - mi * TILE_M;
     return r < TILE_M ? r : TILE_M;
@@ -648,7 +650,7 @@ __global__ void __launch_bounds__(192, 1)
         }
         if constexpr (kSwap) {
           const int rin = tile_rows(x, mi);
-          if (swap_ok && rin < TILE_M) {
+          if (swap_ok && rin <= swap_lim) {
             const int nsh = ((rin + 31) & ~31) / 2;   // token rows staged by this CTA (N / 2)
             const int wrow = brow + n * 128 + static_cast<int>(crank) * 64;
             const int trow = s_eoff[x] + mi * TILE_M + static_cast<int>(crank) * nsh;
@@ -751,7 +753,7 @@ __global__ void __launch_bounds__(192, 1)
         uint32_t idesc_t = idesc;
         if constexpr (kSwap) {
           const int rin = tile_rows(x, mi);
-          if (swap_ok && rin < TILE_M) idesc_t = idesc_f32acc<T>(256, (rin + 31) & ~31);
+          if (swap_ok && rin <= swap_lim) idesc_t = idesc_f32acc<T>(256, (rin + 31) & ~31);
         }
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
@@ -898,7 +900,7 @@ __global__ void __launch_bounds__(192, 1)
       int sw_rin = 0;
       if constexpr (kSwap && EPI == EPI_WEIGHTED) {
         const int rin = tile_rows(x, mi);
-        if (swap_ok && rin < TILE_M) {
+        if (swap_ok && rin <= swap_lim) {
           // D^T tile: lane = output column col0 + lane, TMEM column = the tile's row:
           // Yp[row, cols] = row_w[row] * acc, staged [32 rows][32 columns] per warp.
           sw_rin = rin;
@@ -932,7 +934,7 @@ __global__ void __launch_bounds__(192, 1)
       }
       if constexpr (kSwap && EPI == EPI_SWIGLU) {
         const int rin = tile_rows(x, mi);
-        if (swap_ok && rin < TILE_M) {
+        if (swap_ok && rin <= swap_lim) {
           // D^T tile: lane = weight row, TMEM column = the tile's row.  Warp q < 2 holds
           // the gate rows of columns colb..colb+31, warp q + 2 their up rows: the up warp
           // hands its values over through its staging tile, 16 rows at a time; the gate

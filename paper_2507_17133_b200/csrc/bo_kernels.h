@@ -79,6 +79,7 @@ struct GemmParams {
   // M side and its rows (rounded up to 32) on N, so a ragged tile costs its rows, not 256.
   // Maps [6..11] then hold 64-row gate / up boxes and [12..14] 16 / 32 / 64-row boxes of A (Xp).
   int swap_tail;
+  int swap_max;             // largest tail (rows) run swapped (<= 0: any tail < 256)
 };
 
 // Combine of split-K fp32 partials: y[t] = [x_t] + sum_slots sum_splits P[sp][row].
