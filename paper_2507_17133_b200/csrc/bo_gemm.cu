@@ -478,7 +478,8 @@ __global__ void __launch_bounds__(192, 1)
   const bool swap_ok = kSwap && p.swap_tail && !alt && !p.a_shared && !p.b_packed &&
                        (EPI != EPI_WEIGHTED || (p.ksplit_max <= 1 && !p.f32_mode));
   // largest tail swapped: a tail near 256 rows gains no MMA work and loses pipelining
-  const int swap_lim = p.swap_max > 0 && p.swap_max < TILE_M ? p.swap_max : TILE_M - 1;
+  // (swap_max >= TILE_M swaps full tiles too: an experiment knob)
+  const int swap_lim = p.swap_max > 0 ? (p.swap_max < TILE_M ? p.swap_max : TILE_M) : TILE_M - 1;
   auto tile_rows = [&](int x, int mi) {   // rows of executor x in m-tile mi
     const int r = s_eoff[x + 1] - s_eoff[x] - mi * TILE_M;
     return r < TILE_M ? r : TILE_M;
