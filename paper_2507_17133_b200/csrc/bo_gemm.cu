@@ -80,21 +80,26 @@ __device__ __forceinline__ void stage_row32(uint8_t* stage, int lane, const floa
   }
 }
 // rows of the warp: global row index = row0 + r (r < nrows valid), column offset col0.
+// The lane's first row address is formed once; later rows add a uniform stride, and
+// every store carries the L2 policy `pol` (evict_normal when no hint is wanted), so
+// the loop holds no 64-bit row multiply and no per-store policy branch (the C4 GEMM2
+// epilogue, 12 k-blocks per tile, was bound by these instructions: ncu source page).
 template <typename T>
 __device__ __forceinline__ void flush_rows32(const uint8_t* stage, int lane, T* out, int64_t row0, int nrows,
-                                             int64_t ldo, int vmax = 32 * (int)sizeof(T) / 16, uint64_t pol = 0) {
+                                             int64_t ldo, int vmax, uint64_t pol) {
   constexpr int V16 = 32 * (int)sizeof(T) / 16;   // 16-byte pieces per row chunk
   constexpr int ROW = 32 * (int)sizeof(T) + 16;
   constexpr int RPI = 32 / V16;                    // rows per store instruction
   const int piece = lane % V16;
+  const int rf = lane / V16;
+  T* base = out + (row0 + rf) * ldo + piece * (16 / (int)sizeof(T));
+  const int64_t step = static_cast<int64_t>(RPI) * ldo;
 #pragma unroll
   for (int i = 0; i < V16; ++i) {
-    const int r = i * RPI + lane / V16;
+    const int r = i * RPI + rf;
     if (r < nrows && piece < vmax) {
       const uint4 v = *reinterpret_cast<const uint4*>(stage + r * ROW + piece * 16);
-      T* dst = out + (row0 + r) * ldo + piece * (16 / (int)sizeof(T));
-      if (pol) st_global_hint(dst, v, pol);   // streaming output: keep the weight tiles in L2
-      else *reinterpret_cast<uint4*>(dst) = v;
+      st_global_hint(base + i * step, v, pol);
     }
   }
 }
@@ -808,7 +813,7 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
     const int q = warp & 3;   // TMEM lane quarter this warp may access
-    const uint64_t pol_out = p.store_hint ? policy_evict_first() : 0;
+    const uint64_t pol_out = p.store_hint ? policy_evict_first() : policy_evict_normal();
     int acc = 0;
     uint32_t acc_phase = 0;
     int x, mi, n, sp, kb0, kb1;
@@ -925,8 +930,7 @@ __global__ void __launch_bounds__(192, 1)
               if (c + tk < rin) {
                 const uint4 val = *reinterpret_cast<const uint4*>(stage + tk * C::EPI_ROW + part * 16);
                 T* dst = out + (tok0 + c + tk) * p.ldo + part * (16 / (int)sizeof(T));
-                if (pol_out) st_global_hint(dst, val, pol_out);
-                else *reinterpret_cast<uint4*>(dst) = val;
+                st_global_hint(dst, val, pol_out);
               }
             }
             __syncwarp();
@@ -978,8 +982,7 @@ __global__ void __launch_bounds__(192, 1)
                 if (c + tk < rin) {
                   const uint4 val = *reinterpret_cast<const uint4*>(stage + tk * C::EPI_ROW + part * 16);
                   T* dst = out + (tok0 + c + tk) * p.ldo + part * (16 / (int)sizeof(T));
-                  if (pol_out) st_global_hint(dst, val, pol_out);
-                  else *reinterpret_cast<uint4*>(dst) = val;
+                  st_global_hint(dst, val, pol_out);
                 }
               }
               __syncwarp();
