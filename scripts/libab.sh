@@ -1,6 +1,6 @@
 L=paper_2507_17133_b200
 cp $L/libbrownout.so /tmp/new.so
-for wl in "qwen3_30b_a3b_prefill 0.5" "qwen15_moe_a27b_prefill 0.8" "mixtral_prefill 0.5"; do
+for wl in ${WLS:-"qwen3_30b_a3b_prefill 0.5" "qwen15_moe_a27b_prefill 0.8" "mixtral_prefill 0.5"}; do
  for r in 1 2 3; do
   for arm in prev new; do
    if [ $arm = prev ]; then cp $L/libbrownout_prev.so.bak $L/libbrownout.so; else cp /tmp/new.so $L/libbrownout.so; fi
