@@ -49,6 +49,7 @@ struct bo_handle {
   int32_t swap_tail;     // bit 0: CTA-pair GEMM1 runs each executor's ragged last m-tile with swapped
                          // operands (default on); bit 1: GEMM2 likewise (off: neutral).  env BO_SWAP_TAIL
   int32_t swap_max;      // largest tail (rows) that runs swapped; 0 = any (env BO_SWAP_MAX)
+  int32_t tma_store;     // 1 (default): GEMM2 writes full 32-row slabs of Yp with TMA bulk stores (env BO_TMA_STORE=0: off)
   int32_t store_hint;    // 1: FFN GEMM epilogue stores hint L2 evict_first (env BO_STORE_HINT=0 disables)
   int32_t fused_combine; // combine (a8) in GEMM2's epilogue: 0 never, 1 always, 2 auto (env BO_FUSED_COMBINE=0/1, default auto)
   std::string last_kernels;   // comma-separated names of the kernels the last forward launched
@@ -119,6 +120,21 @@ bo_status make_map(CUtensorMap* m, const void* base, int32_t dtype, uint64_t row
   if (r != CUDA_SUCCESS)
     return fail(BO_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) rows=%llu k=%llu box_rows=%u", static_cast<int>(r),
                 static_cast<unsigned long long>(rows), static_cast<unsigned long long>(k), box_rows);
+  return BO_OK;
+}
+
+// Output box map for TMA bulk stores: [rows, cols] bf16 row-major, box 32 x 32, SWIZZLE_64B.
+bo_status make_map_store32(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return fail(BO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(BO_ERR_CUDA, "cuTensorMapEncodeTiled (store box) failed (%d)", static_cast<int>(r));
   return BO_OK;
 }
 
@@ -567,6 +583,10 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.exec_off = exec_off;
     p.mtile_off = mtile_off;
     p.out = Y;
+    if (h->tma_store && dt == 0 && !partial) {
+      if ((st = make_map_store32(&mb.m[6], Y, static_cast<uint64_t>(R), static_cast<uint64_t>(d))) != BO_OK) return st;
+      p.tma_store = 1;
+    }
     p.row_w = row_w;
     p.rows_total = static_cast<int>(R);
     if (comb) {
@@ -1208,6 +1228,10 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   h->tile_alt = (ta && ta[0] == '0') ? 0 : 1;
   // Swapped-operand tail tiles: GEMM1 C2 1.329 -> 1.305 ms (ratio 0.5), 1.393 -> 1.352 (ratio 0)
   // (profiles/r01_ncu_ab_swap_tail.txt); GEMM2 neutral (-1.5 .. +0.5 %), so GEMM1 only by default
+  // TMA bulk stores of GEMM2's full Yp slabs: C4 GEMM2 190.2 -> 183.2 us, f2 149.6 -> 146.4 us,
+  // C2 / C3 neutral (profiles/r01_ncu_ab_tma_store.txt)
+  const char* tst = getenv("BO_TMA_STORE");
+  h->tma_store = (tst && tst[0] == '0') ? 0 : 1;
   const char* swm = getenv("BO_SWAP_MAX");
   h->swap_max = swm ? atoi(swm) : 0;
   const char* swt = getenv("BO_SWAP_TAIL");

@@ -41,7 +41,8 @@ struct GemmCfg {
   static constexpr int BAR_BYTES = 2048;                 // barriers + tmem slot (1 KB) + router histogram (1 KB)
   static constexpr int SCHED_BYTES = ((2 * (kMaxExec + 1) * 4) + 127) / 128 * 128;   // keeps the staging 16B-aligned
   static constexpr int EPI_ROW = 32 * (int)sizeof(T) + 16;   // staged 32-column row chunk + bank pad
-  static constexpr int EPI_BYTES = 4 * 32 * EPI_ROW;         // one staging tile per epilogue warp
+  static constexpr int EPI_BYTES = 4 * 32 * EPI_ROW          // one staging tile per epilogue warp
+                                   + 1024 + 4 * 4096;          // + two dense 2 KB TMA-store boxes per warp (1 KB aligned)
   static constexpr int OTHER = 1024 /*align slack*/ + BAR_BYTES + SCHED_BYTES + EPI_BYTES;
   static constexpr int STAGES_RAW = (227 * 1024 - OTHER) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
@@ -1041,6 +1042,14 @@ __global__ void __launch_bounds__(192, 1)
           continue;
         }
         T* out = reinterpret_cast<T*>(p.out) + n * BN;
+        // TMA bulk stores for full slabs (no fused combine, which re-reads the rows at once):
+        // thread = row writes its 64 bytes into a dense 32 x 32 box (64B swizzle: 16-byte
+        // chunk q of row r at q ^ ((r >> 1) & 3), conflict-free), one elected lane stores
+        // the box; two boxes per warp alternate.
+        const bool tma_out = sizeof(T) == 2 && p.tma_store && nrows == 32 && !p.comb_cnt && !sw_rin;
+        uint8_t* tbox0 = smem +
+                         ((STAGES * C::STAGE_BYTES + C::BAR_BYTES + C::SCHED_BYTES + 4 * 32 * C::EPI_ROW + 1023) & ~1023) +
+                         (warp - 2) * 4096;   // 1 KB aligned (smem is): the swizzle follows address bits 7-8
 #pragma unroll 1
         for (int c = 0; c < (sw_rin ? 0 : BN); c += 32) {
           uint32_t a[32];
@@ -1049,6 +1058,27 @@ __global__ void __launch_bounds__(192, 1)
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(a[i]) * wr;
+          if (tma_out) {
+            uint8_t* tb = tbox0 + ((c >> 5) & 1) * 2048;
+            if (lane == 0) bulk_wait_read<1>();   // this box's store from two chunks ago has read it
+            __syncwarp();
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              uint4 u;
+              u.x = pack_bf16x2(v[8 * q4 + 0], v[8 * q4 + 1]);
+              u.y = pack_bf16x2(v[8 * q4 + 2], v[8 * q4 + 3]);
+              u.z = pack_bf16x2(v[8 * q4 + 4], v[8 * q4 + 5]);
+              u.w = pack_bf16x2(v[8 * q4 + 6], v[8 * q4 + 7]);
+              *reinterpret_cast<uint4*>(tb + lane * 64 + ((q4 ^ ((lane >> 1) & 3)) << 4)) = u;
+            }
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_2d(&tmB.m[6], tb, n * BN + c, static_cast<int>(row0));
+              bulk_commit();
+            }
+            continue;
+          }
           stage_row32<T>(stage, lane, v);
           __syncwarp();
           flush_rows32<T>(stage, lane, out + c, row0, nrows, p.ldo, 32 * (int)sizeof(T) / 16, pol_out);
@@ -1173,6 +1203,9 @@ __global__ void __launch_bounds__(192, 1)
     }
   }
 
+  if constexpr (EPI == EPI_WEIGHTED) {
+    if (warp >= 2 && lane == 0) bulk_wait_all();   // TMA-stored Yp boxes complete before exit
+  }
   tc_fence_before();
   __syncthreads();
   if constexpr (CG == 2) cluster_sync();
