@@ -49,6 +49,7 @@ struct bo_handle {
   int32_t swap_tail;     // bit 0: CTA-pair GEMM1 runs each executor's ragged last m-tile with swapped
                          // operands (default on); bit 1: GEMM2 likewise (off: neutral).  env BO_SWAP_TAIL
   int32_t swap_max;      // largest tail (rows) that runs swapped; 0 = any (env BO_SWAP_MAX)
+  int32_t a_policy;      // L2 policy of activation loads in the FFN GEMMs: 0 evict_last (default), 1 normal, 2 first
   int32_t tma_store;     // 1 (default): GEMM2 writes full 32-row slabs of Yp with TMA bulk stores (env BO_TMA_STORE=0: off)
   int32_t store_hint;    // 1: FFN GEMM epilogue stores hint L2 evict_first (env BO_STORE_HINT=0 disables)
   int32_t fused_combine; // combine (a8) in GEMM2's epilogue: 0 never, 1 always, 2 auto (env BO_FUSED_COMBINE=0/1, default auto)
@@ -510,6 +511,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.store_hint = h->store_hint && R > kSplitRows;   // decode: H / Yp (a few MB) stay in L2 for the next kernel
     p.pf_dist = h->pf_dist;
     p.b_policy = b_policy_for(h, R);
+    p.a_policy = h->a_policy;
     p.b_packed = c.weight_layout == BO_WEIGHTS_TILED ? 1 : 0;
     p.b_rows_per_exec = f;
     p.num_exec = n_exec;
@@ -576,6 +578,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.store_hint = h->store_hint && R > kSplitRows;   // decode: H / Yp (a few MB) stay in L2 for the next kernel
     p.pf_dist = h->pf_dist;
     p.b_policy = b_policy_for(h, R);
+    p.a_policy = h->a_policy;
     p.b_packed = c.weight_layout == BO_WEIGHTS_TILED ? 1 : 0;
     p.b_rows_per_exec = d;
     p.num_exec = n_exec;
@@ -1230,6 +1233,8 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   // (profiles/r01_ncu_ab_swap_tail.txt); GEMM2 neutral (-1.5 .. +0.5 %), so GEMM1 only by default
   // TMA bulk stores of GEMM2's full Yp slabs: C4 GEMM2 190.2 -> 183.2 us, f2 149.6 -> 146.4 us,
   // C2 / C3 neutral (profiles/r01_ncu_ab_tma_store.txt)
+  const char* apo = getenv("BO_A_POLICY");
+  h->a_policy = apo ? atoi(apo) : 0;
   const char* tst = getenv("BO_TMA_STORE");
   h->tma_store = (tst && tst[0] == '0') ? 0 : 1;
   const char* swm = getenv("BO_SWAP_MAX");

@@ -633,7 +633,9 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0) {
     // ------------------------------------------------------------ producer
     if (GATHER || lane == 0) {
-      const uint64_t pol_a = policy_evict_last();   // activations are re-read per n-tile
+      // activations are re-read per n-tile: evict_last (a_policy 0), or normal / first (1 / 2)
+      const uint64_t pol_a =
+          p.a_policy == 1 ? policy_evict_normal() : (p.a_policy == 2 ? policy_evict_first() : policy_evict_last());
       // weight tile is re-read by the executor's other m-tiles (running alongside);
       // b_policy 1: evict_first (streamed weights make way for the re-read activations)
       const uint64_t pol_b = p.b_policy == 1 ? policy_evict_first() : policy_evict_normal();

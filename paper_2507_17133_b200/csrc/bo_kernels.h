@@ -80,6 +80,7 @@ struct GemmParams {
   // Maps [6..11] then hold 64-row gate / up boxes and [12..14] 16 / 32 / 64-row boxes of A (Xp).
   int swap_tail;
   int swap_max;             // largest tail (rows) run swapped (<= 0: any tail < 256)
+  int a_policy;             // L2 policy of the A (activation) loads: 0 evict_last, 1 evict_normal, 2 evict_first
   int tma_store;            // EPI_WEIGHTED: full 32-row slabs leave through TMA bulk stores (map B[6], 32 x 32 box, 64B swizzle)
 };
 
