@@ -64,15 +64,29 @@ typedef enum { BO_PARTIAL = 0, BO_FULL = 1 } bo_mode;
  * the group's member weights, computed in fp64 and rounded once (RNE). */
 typedef enum { BO_UNITED_MEAN = 0 } bo_united_init;
 
-/* Memory layout of the expert weight stacks.  ROWMAJOR: nn.Linear [out, in]
- * row-major matrices.  TILED: the same matrices re-laid out by bo_pack_weights
- * into 128-row x 128-byte blocks, [n][rows/128][K/kc][128][kc] (kc = 128 bytes of
- * K), so that each TMA box the GEMMs load is one contiguous 16 KB block —
- * streamed from HBM at ~7.1 TB/s instead of ~5.7 TB/s for 128-byte row pieces at
- * the row stride (decode steps are weight-streaming).  TILED needs hidden and
- * ffn to be multiples of 128; it is a single-GPU forward layout (bo_expert_ffn
- * takes ROWMAJOR).  bo_build_united works on either (element-wise). */
-typedef enum { BO_WEIGHTS_ROWMAJOR = 0, BO_WEIGHTS_TILED = 1 } bo_weight_layout;
+/* Engine options (bo_set_engine_option): how the kernels of the forward are
+ * scheduled, never what they compute — every setting gives the same routing,
+ * plan and permutation and outputs within the parity tolerance (the tests run
+ * each).  bo_create sets the defaults (the measured-best configuration,
+ * DESIGN.md §5), overridable from the environment as BO_<NAME>=<int> (e.g.
+ * BO_CTA_PAIRS=0) for A/B runs. */
+typedef enum {
+  BO_OPT_CTA_PAIRS = 0,      /* 1: prefill-sized FFN GEMMs on cta_group::2 CTA pairs (256-row tiles)   [1]    */
+  BO_OPT_PAIR_ROWS1 = 1,     /* GEMM1 uses CTA pairs from this many rows                            [2048] */
+  BO_OPT_PAIR_ROWS2 = 2,     /* GEMM2 likewise                                                      [2048] */
+  BO_OPT_TILE_ALT = 3,       /* 1: GEMM1 may pick a narrower SwiGLU tile on the device (fewer waves)  [1]    */
+  BO_OPT_SWAP_TAIL = 4,      /* 1: CTA-pair GEMM1 runs ragged last m-tiles with swapped operands     [1]    */
+  BO_OPT_DECODE_PAIR2 = 5,   /* 1: decode GEMM2 on pairs + split-K when executors hold >= 256 rows   [1]    */
+  BO_OPT_GEMM2_SPLITK = 6,   /* 1: GEMM2 split-K (fp32 partials) for every decode-sized step         [0]    */
+  BO_OPT_FUSED_COMBINE = 7,  /* a8 in GEMM2's epilogue: 0 never, 1 always, 2 auto                    [2]    */
+  BO_OPT_TMA_STORE = 8,      /* 1: GEMM2 writes full Yp slabs with TMA bulk stores                   [1]    */
+  BO_OPT_STORE_HINT = 9,     /* 1: prefill H / Yp stores carry an L2 evict_first hint                [1]    */
+  BO_OPT_B_POLICY = 10,      /* weight loads: 0 evict_normal, 1 evict_first, -1 auto (decode: first) [-1]   */
+  BO_OPT_ROUTER_MMA = 11,    /* 1: prefill-sized bf16 batches with m <= 32 use the mma.sync router    [1]    */
+  BO_OPT_ROUTER_SPLIT = 12,  /* 1: decode-sized batches with m <= 32 use the split-warp router        [1]    */
+  BO_OPT_PDL = 13,           /* 1: GEMMs launch with programmatic dependent launch                   [1]    */
+  BO_OPT_COUNT = 14
+} bo_engine_option;
 
 typedef struct {
   int32_t hidden;        /* d   */
@@ -86,7 +100,6 @@ typedef struct {
                             the summed weight (Eq. 5-6 algebra; single-GPU forward only) */
   int32_t num_shared;    /* N_s of Eq. 5: shared experts applied to every token with weight 1, shape
                             of an original expert; weights via bo_set_shared_experts (single-GPU forward only) */
-  int32_t weight_layout; /* bo_weight_layout of every expert weight stack (originals, united, shared) */
   int64_t max_tokens;    /* largest T a forward will be called with */
 } bo_config;
 
@@ -128,8 +141,6 @@ typedef struct {
   size_t tile_xbase;      /* int32 [ntiles, E]  their exclusive prefix over tiles            */
   size_t ksplit;          /* int32 [1]          split count GEMM2 chose                 */
   size_t comb_cnt;        /* int32 [T, d/BN2]   arrival counters of the combine fused into GEMM2 (a8; BN2 = 256/128/64, GEMM2 tile width) */
-  size_t sk_part;         /* float [#SM, 256/4, 128, 4] partial tiles of split GEMM tiles (router, decode FFN) */
-  size_t sk_flag;         /* int32 [#SM]        their published flags (zeroed by each forward that splits) */
   int64_t T;              /* tokens the layout was computed for                          */
   int64_t ntiles;         /* histogram tiles the workspace is sized for (8 tokens each)  */
   int64_t num_executors;  /* E = m + G                                                   */
@@ -154,18 +165,16 @@ BO_API bo_status bo_workspace_layout(const bo_handle* h, int64_t T, bo_ws_layout
 BO_API bo_status bo_build_united(bo_handle* h, const void* Wg, const void* Wu, const void* Wd,
                           int32_t init, void* UWg, void* UWu, void* UWd, void* stream);
 
-/* Re-lay n row-major [rows, K] matrices W (device) into the TILED layout in P
- * (device, same byte size, caller-owned, must not alias W): which = 0 for
- * gate / up stacks ([n, f, d]: rows = ffn, K = hidden), 1 for down stacks
- * ([n, d, f]: rows = hidden, K = ffn).  Runs once per weight load (the paper's
- * Experts Loader); enqueued on `stream`. */
-BO_API bo_status bo_pack_weights(const bo_handle* h, const void* W, int64_t n, int32_t which, void* P, void* stream);
-
 /* Shared experts of Eq. 5 (second term): SWg, SWu [N_s, f, d], SWd [N_s, d, f]
  * device pointers (caller-owned) used by every following forward; N_s is fixed
  * by bo_config.num_shared.  A wider shared FFN (e.g. one of width 4f) is exactly
  * N_s = 4 experts of width f holding its column slices (SwiGLU is elementwise in f). */
 BO_API bo_status bo_set_shared_experts(bo_handle* h, const void* SWg, const void* SWu, const void* SWd);
+
+/* Engine options (bo_engine_option): BO_ERR_INVALID_ARG for an unknown option or a
+ * value outside its range.  Host state, read by the next forward. */
+BO_API bo_status bo_set_engine_option(bo_handle* h, int32_t option, int32_t value);
+BO_API bo_status bo_get_engine_option(const bo_handle* h, int32_t option, int32_t* value);
 
 /* The brownout knob: ratio = 1 - threshold, in [0, 1].
  * Host state only; snapshotted by the next forward (may change every
@@ -197,7 +206,8 @@ BO_API bo_status bo_moe_forward_ex(bo_handle* h, const void* x, int64_t T, const
                             void* y, void* workspace, size_t ws_bytes,
                             const float* logits_in, void* stream);
 
-/* Alg. 1 alone on given per-expert counts (device int32 [m]) with the
+/* Alg. 1 alone on given per-expert counts (device int32 [m], any 4-byte-aligned
+ * pointer) with the
  * handle's ratio/mode/way (parity entry for the plan).  Outputs (device):
  * exec_of_expert [m], expert_row_off [m], stats (bo_plan_stats, device) and
  * exec_off, a buffer of at least 2*(E+1) + m int32 whose first E+1 entries
@@ -221,7 +231,7 @@ BO_API bo_status bo_route(bo_handle* h, const void* x, int64_t T, const void* Wr
                           void* workspace, size_t ws_bytes, void* stream);
 
 /* Alg. 1 on the column sums of counts [nrows, m] (int32; one row per
- * rank under expert parallelism, D18: one global plan).  Outputs as
+ * rank under expert parallelism, D18: one global plan; any 4-byte-aligned pointer).  Outputs as
  * bo_plan_from_counts (exec_off: >= 2*(E+1) + m int32, first E+1 meaningful). */
 BO_API bo_status bo_plan_counts(bo_handle* h, const int32_t* counts, int32_t nrows, int32_t* exec_of_expert,
                                 int32_t* expert_row_off, int32_t* exec_off, void* stats, void* stream);

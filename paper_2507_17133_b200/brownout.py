@@ -19,10 +19,14 @@ BO_OK, BO_ERR_INVALID_ARG, BO_ERR_SHAPE, BO_ERR_UNSUPPORTED, BO_ERR_CUDA, BO_ERR
 BO_BF16, BO_FP32 = 0, 1
 BO_PARTIAL, BO_FULL = 0, 1
 BO_UNITED_MEAN = 0
+# bo_engine_option (include/brownout.h): name -> id
+ENGINE_OPTIONS = {n: i for i, n in enumerate((
+    "cta_pairs", "pair_rows1", "pair_rows2", "tile_alt", "swap_tail", "decode_pair2", "gemm2_splitk",
+    "fused_combine", "tma_store", "store_hint", "b_policy", "router_mma", "router_split", "pdl"))}
 
 EXPORTED = (
     "bo_create", "bo_destroy", "bo_workspace_size", "bo_workspace_layout", "bo_build_united", "bo_set_shared_experts",
-    "bo_pack_weights",
+    "bo_set_engine_option", "bo_get_engine_option",
     "bo_set_brownout", "bo_get_brownout", "bo_moe_forward", "bo_moe_forward_ex", "bo_plan_from_counts",
     "bo_route", "bo_plan_counts", "bo_dispatch", "bo_block_copy", "bo_expert_ffn", "bo_combine",
     "bo_set_profile_events", "bo_last_launch_count", "bo_last_kernels", "bo_status_string", "bo_last_error", "bo_version",
@@ -33,7 +37,7 @@ EXPORTED = (
 class bo_config(C.Structure):
     _fields_ = [("hidden", C.c_int32), ("ffn", C.c_int32), ("num_experts", C.c_int32), ("top_k", C.c_int32),
                 ("way", C.c_int32), ("dtype", C.c_int32), ("add_residual", C.c_int32), ("dedup_united", C.c_int32),
-                ("num_shared", C.c_int32), ("weight_layout", C.c_int32), ("max_tokens", C.c_int64)]
+                ("num_shared", C.c_int32), ("max_tokens", C.c_int64)]
 
 
 class bo_plan_stats(C.Structure):
@@ -48,7 +52,7 @@ class bo_ws_layout(C.Structure):
     _fields_ = [(n, C.c_size_t) for n in ("total_bytes", "logits", "topk_id", "topk_w", "tile_cnt", "tile_base",
                                           "counts", "exec_of_expert", "expert_row_off", "exec_off", "mtile_off",
                                           "stats", "row_of", "row_tok", "row_w", "xp", "h", "yp", "partial",
-                                          "tile_xcnt", "tile_xbase", "ksplit", "comb_cnt", "sk_part", "sk_flag")] + \
+                                          "tile_xcnt", "tile_xbase", "ksplit", "comb_cnt")] + \
                [("T", C.c_int64), ("ntiles", C.c_int64), ("num_executors", C.c_int64)]
 
 
@@ -76,7 +80,8 @@ def _load():
         "bo_workspace_size": ([vp, i64, C.POINTER(C.c_size_t)], C.c_int),
         "bo_workspace_layout": ([vp, i64, C.POINTER(bo_ws_layout)], C.c_int),
         "bo_build_united": ([vp, vp, vp, vp, i32, vp, vp, vp, vp], C.c_int),
-        "bo_pack_weights": ([vp, vp, i64, i32, vp, vp], C.c_int),
+        "bo_set_engine_option": ([vp, i32, i32], C.c_int),
+        "bo_get_engine_option": ([vp, i32, C.POINTER(i32)], C.c_int),
         "bo_set_brownout": ([vp, C.c_double, i32], C.c_int),
         "bo_set_shared_experts": ([vp, vp, vp, vp], C.c_int),
         "bo_get_brownout": ([vp, C.POINTER(C.c_double), C.POINTER(i32)], C.c_int),
@@ -123,6 +128,25 @@ def _ptr(t):
     return None if t is None else C.c_void_p(t.data_ptr())
 
 
+def _req(t, name, dtype, shape, device=None):
+    """Argument check before a raw pointer crosses the ABI (the C side can only
+    check alignment): dtype, contiguity, CUDA residency and shape."""
+    if t is None:
+        return
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name}: expected a torch.Tensor, got {type(t).__name__}")
+    if not t.is_cuda:
+        raise ValueError(f"{name}: must be a CUDA tensor")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name}: on {t.device}, expected {device}")
+    if t.dtype != dtype:
+        raise TypeError(f"{name}: dtype {t.dtype}, expected {dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: must be contiguous")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+
+
 def _stream(stream):
     if stream is None:
         stream = torch.cuda.current_stream()
@@ -136,12 +160,11 @@ class BrownoutMoE:
     """One MoE layer handle: bo_create / bo_set_brownout / bo_moe_forward."""
 
     def __init__(self, hidden, ffn, num_experts, top_k, way, dtype="bf16", add_residual=False,
-                 max_tokens=16384, dedup=False, num_shared=0, tiled=False):
+                 max_tokens=16384, dedup=False, num_shared=0, **engine_options):
         self.cfg = bo_config(hidden=hidden, ffn=ffn, num_experts=num_experts, top_k=top_k, way=way,
                              dtype=BO_BF16 if dtype in ("bf16", torch.bfloat16) else BO_FP32,
                              add_residual=1 if add_residual else 0, dedup_united=1 if dedup else 0,
-                             num_shared=num_shared, weight_layout=1 if tiled else 0,
-                             max_tokens=max_tokens)
+                             num_shared=num_shared, max_tokens=max_tokens)
         h = C.c_void_p()
         _check(_lib.bo_create(C.byref(self.cfg), C.byref(h)))
         self._h = h
@@ -149,6 +172,8 @@ class BrownoutMoE:
         self.G = -(-num_experts // way)
         self.E = num_experts + self.G
         self._ws = None
+        for k, v in engine_options.items():
+            self.set_option(k, v)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -189,6 +214,8 @@ class BrownoutMoE:
         _check(_lib.bo_set_shared_experts(self._h, _ptr(SWg), _ptr(SWu), _ptr(SWd)))
 
     def build_united(self, Wg, Wu, Wd, stream=None):
+        self._check_layer(torch.empty(0, self.cfg.hidden, dtype=self.torch_dtype, device=Wg.device),
+                          None, (Wg, Wu, Wd), None)
         m, f, d = Wg.shape
         G = self.G
         UWg = torch.empty(G, f, d, dtype=Wg.dtype, device=Wg.device)
@@ -198,16 +225,14 @@ class BrownoutMoE:
                                     _ptr(UWd), _stream(stream)))
         return UWg, UWu, UWd
 
-    def pack(self, W, which, stream=None):
-        """bo_pack_weights: a TILED-layout copy of the weight stack W ([n, f, d] gate / up:
-        which=0; [n, d, f] down: which=1).  Same shape and dtype; only the memory layout
-        differs (pass it to a handle created with tiled=True)."""
-        P = torch.empty_like(W)
-        _check(_lib.bo_pack_weights(self._h, _ptr(W), W.shape[0], int(which), _ptr(P), _stream(stream)))
-        return P
+    def set_option(self, name: str, value: int):
+        """bo_set_engine_option: scheduling choice of the kernels (ENGINE_OPTIONS), never the result."""
+        _check(_lib.bo_set_engine_option(self._h, ENGINE_OPTIONS[name], int(value)))
 
-    def pack_all(self, Wg, Wu, Wd, stream=None):
-        return self.pack(Wg, 0, stream), self.pack(Wu, 0, stream), self.pack(Wd, 1, stream)
+    def get_option(self, name: str) -> int:
+        v = C.c_int32()
+        _check(_lib.bo_get_engine_option(self._h, ENGINE_OPTIONS[name], C.byref(v)))
+        return v.value
 
     def forward(self, x, Wr, experts, united, y=None, workspace=None, logits=None, stream=None, shared=None):
         """moe_forward(tokens, router, experts, united) -> y [T, d].
@@ -218,8 +243,10 @@ class BrownoutMoE:
         T = x.shape[0]
         Wg, Wu, Wd = experts
         UWg, UWu, UWd = united if united is not None else (None, None, None)
+        self._check_layer(x, Wr, experts, united, logits)
         if y is None:
             y = torch.empty_like(x)
+        _req(y, "y", self.torch_dtype, x.shape, x.device)
         ws = workspace if workspace is not None else self.workspace(T, x.device)
         if logits is None:
             _check(_lib.bo_moe_forward(self._h, _ptr(x), T, _ptr(Wr), _ptr(Wg), _ptr(Wu), _ptr(Wd), _ptr(UWg),
@@ -229,6 +256,21 @@ class BrownoutMoE:
                                           _ptr(UWu), _ptr(UWd), _ptr(y), _ptr(ws), ws.numel(), _ptr(logits),
                                           _stream(stream)))
         return y
+
+    def _check_layer(self, x, Wr, experts, united, logits=None):
+        c, dt = self.cfg, self.torch_dtype
+        d, f, m = c.hidden, c.ffn, c.num_experts
+        _req(x, "x", dt, (x.shape[0], d))
+        dev = x.device
+        _req(Wr, "Wr", dt, (m, d), dev)
+        if logits is not None:
+            _req(logits, "logits", torch.float32, (x.shape[0], m), dev)
+        if experts is not None:
+            for name, t, shp in zip(("Wg", "Wu", "Wd"), experts, ((m, f, d), (m, f, d), (m, d, f))):
+                _req(t, name, dt, shp, dev)
+        if united is not None:
+            for name, t, shp in zip(("UWg", "UWu", "UWd"), united, ((self.G, f, d), (self.G, f, d), (self.G, d, f))):
+                _req(t, name, dt, shp, dev)
 
     def set_profile_events(self, events):
         """events: list of torch.cuda.Event(enable_timing=True) (>= launches + 1),
@@ -292,6 +334,7 @@ class BrownoutMoE:
     def route(self, x, Wr, logits=None, workspace=None, stream=None):
         """a1-a4 on a local batch; returns the workspace (counts etc. inside)."""
         T = x.shape[0]
+        self._check_layer(x, Wr if logits is None else None, None, None, logits)
         ws = workspace if workspace is not None else self.workspace(T, x.device)
         _check(_lib.bo_route(self._h, _ptr(x), T, _ptr(Wr), _ptr(logits), _ptr(ws), ws.numel(), _stream(stream)))
         return ws

@@ -12,54 +12,12 @@
 #include <string>
 
 #include "../../include/brownout.h"
+#include "bo_internal.h"
 #include "bo_kernels.h"
 
-struct bo_handle {
-  bo_config cfg;
-  double ratio;
-  int32_t mode;
-  int num_sms;
-  int device;
-  int32_t last_launches;
-  void** prof_events;
-  int32_t prof_n;
-  int64_t route_T;     // token count / tile of the last route stage (bo_route, forward)
-  int32_t route_tile;
-  int32_t cta_pairs;   // 1: prefill FFN GEMMs use cta_group::2 CTA pairs (env BO_GEMM_CG=1 disables)
-  int32_t stream_k;    // decode-sized FFN GEMMs (env BO_STREAMK): 0 classic tiles (default), 1 stream-K
-                       // hybrid, 2 lockstep split-K when < 1 wave of tiles.  Both options measured no faster
-                       // than the classic persistent schedule on C3 (profiles/r01_ab_stream_k.json): the
-                       // concurrently running CTAs of the classic order read the same weight / activation
-                       // tiles together, which the even k-range split gives up.
-  int32_t decode_pair2; // 1: decode steps with >= 256 rows per executor: GEMM2 pairs + split-K (env BO_DECODE_PAIR2=0 disables)
-  int32_t router_splitk;  // 1: tcgen05 router with < #SM/2 token tiles splits K in lockstep (env BO_ROUTER_SPLITK=1;
-                          // off: no gain on C4, whose router time is its top-K epilogue, profiles/r01_ab_router_variants.json)
-  int32_t b_policy;     // L2 policy of the FFN GEMMs' weight loads (env BO_B_POLICY): 0 evict_normal, 1 evict_first,
-                        // -1 auto = evict_first for decode-sized steps (C3 -2..-4 %, prefill neutral:
-                        // profiles/r01_ab_weight_evict_first.json)
-  int32_t pf_dist;      // L2 prefetch distance (k-blocks) of the FFN GEMMs' B tiles (env BO_PF_DIST)
-  int32_t pair_rows1;  // GEMM1 uses CTA pairs from this many rows (env BO_PAIR_ROWS1, default 2048)
-  int32_t pair_rows2;  // GEMM2 likewise (env BO_PAIR_ROWS2, default 2048)
-  int32_t fused_gather;  // 1: GEMM1 gathers x rows by TMA gather4 (env BO_GATHER=1; default off)
-  int32_t splitk;        // 1: GEMM2 split-K for decode-sized steps (env BO_SPLITK=1; default off)
-  int32_t decode_bn1;    // >0: GEMM1 tile width for decode-sized steps (env BO_DECODE_BN1, experiments)
-  int32_t router_split;  // 1: decode-sized batches use k_router_split (env BO_ROUTER_SPLIT=0 disables)
-  int32_t router_mma;    // 1: prefill-sized bf16 batches with m <= 32 use k_router_mma (env BO_ROUTER_MMA=0 disables)
-  int32_t tile_alt;      // 1: GEMM1 may pick a narrower SwiGLU tile on the device (env BO_TILE_ALT=0 disables)
-  int32_t swap_tail;     // bit 0: CTA-pair GEMM1 runs each executor's ragged last m-tile with swapped
-                         // operands (default on); bit 1: GEMM2 likewise (off: neutral).  env BO_SWAP_TAIL
-  int32_t swap_max;      // largest tail (rows) that runs swapped; 0 = any (env BO_SWAP_MAX)
-  int32_t a_policy;      // L2 policy of activation loads in the FFN GEMMs: 0 evict_last (default), 1 normal, 2 first
-  int32_t tma_store;     // 1 (default): GEMM2 writes full 32-row slabs of Yp with TMA bulk stores (env BO_TMA_STORE=0: off)
-  int32_t store_hint;    // 1: FFN GEMM epilogue stores hint L2 evict_first (env BO_STORE_HINT=0 disables)
-  int32_t fused_combine; // combine (a8) in GEMM2's epilogue: 0 never, 1 always, 2 auto (env BO_FUSED_COMBINE=0/1, default auto)
-  std::string last_kernels;   // comma-separated names of the kernels the last forward launched
-  const void* SWg;       // shared experts (Eq. 5 second term): [N_s, f, d], [N_s, f, d], [N_s, d, f]
-  const void* SWu;
-  const void* SWd;
-};
 
-namespace {
+
+namespace bo_impl {
 
 thread_local std::string g_last_error;
 
@@ -77,11 +35,6 @@ bo_status cuda_fail(cudaError_t e, const char* what) {
   return fail(BO_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
 }
 
-#define BO_CUDA(call, what)                 \
-  do {                                      \
-    cudaError_t e_ = (call);                \
-    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
-  } while (0)
 
 size_t align256(size_t v) { return (v + 255) & ~size_t(255); }
 
@@ -139,39 +92,6 @@ bo_status make_map_store32(CUtensorMap* m, const void* base, uint64_t rows, uint
   return BO_OK;
 }
 
-// Tile-packed weight stack (bo_pack_weights) of `rows` rows (all matrices stacked)
-// and K columns: a 3-D view {kc elements, 128 rows of a band, band * K/kc + k-chunk}
-// whose boxes {kc, box_rows <= 128, 1} are contiguous 16 KB blocks.
-bo_status make_map_packed(CUtensorMap* m, const void* base, int32_t dtype, uint64_t rows, uint64_t k,
-                          uint32_t box_rows) {
-  PFN_encodeTiled enc = get_encode();
-  if (!enc) return fail(BO_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  const int eb = elem_bytes(dtype);
-  const uint64_t kc = 128 / eb;
-  if (rows % bo::kPackRows || k % kc) return fail(BO_ERR_SHAPE, "packed map: rows=%llu k=%llu",
-                                                   static_cast<unsigned long long>(rows),
-                                                   static_cast<unsigned long long>(k));
-  cuuint64_t dims[3] = {kc, static_cast<cuuint64_t>(bo::kPackRows), (rows / bo::kPackRows) * (k / kc)};
-  cuuint64_t strides[2] = {128, static_cast<cuuint64_t>(bo::kPackRows) * 128};
-  cuuint32_t box[3] = {static_cast<cuuint32_t>(kc), box_rows > 128 ? 128u : box_rows, 1};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(m, dtype == BO_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
-                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS)
-    return fail(BO_ERR_CUDA, "cuTensorMapEncodeTiled (packed) failed (%d) rows=%llu k=%llu", static_cast<int>(r),
-                static_cast<unsigned long long>(rows), static_cast<unsigned long long>(k));
-  return BO_OK;
-}
-
-// B operand map of a weight stack in the handle's layout.
-bo_status make_map_w(const bo_handle* h, CUtensorMap* m, const void* base, uint64_t rows, uint64_t k,
-                     uint32_t box_rows) {
-  if (h->cfg.weight_layout == BO_WEIGHTS_TILED) return make_map_packed(m, base, h->cfg.dtype, rows, k, box_rows);
-  return make_map(m, base, h->cfg.dtype, rows, k, box_rows);
-}
-
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 int router_bn(int m) {
@@ -180,8 +100,6 @@ int router_bn(int m) {
   return bn;
 }
 
-constexpr int64_t kSplitRows = 1024;   // GEMM2 split-K (decode) only for R <= this
-constexpr int kSplitMax = 8;
 
 int gemm2_bn(int d) { return d % 256 == 0 ? 256 : d % 128 == 0 ? 128 : 64; }
 int gemm1_bn(int f) { return f % 128 == 0 ? 256 : 128; }   // gate + up columns
@@ -224,9 +142,6 @@ bo_status compute_layout(const bo_handle* h, int64_t T, bo_ws_layout* L) {
   L->tile_xbase = take(c.dedup_united ? sizeof(int32_t) * ntiles * (m + G) : 0);
   L->ksplit = take(sizeof(int32_t));
   L->comb_cnt = take(sizeof(int32_t) * T * (d / gemm2_bn(static_cast<int>(d))));
-  // split-tile partials (lockstep split of the tcgen05 router, decode FFN schedules)
-  L->sk_part = take(sizeof(float) * h->num_sms * bo::kBM * bo::kSkCols);
-  L->sk_flag = take(sizeof(int32_t) * h->num_sms);
   L->total_bytes = off;
   L->T = T;
   L->ntiles = ntiles;
@@ -234,43 +149,13 @@ bo_status compute_layout(const bo_handle* h, int64_t T, bo_ws_layout* L) {
   return BO_OK;
 }
 
-template <typename P>
-P* at(void* ws, size_t off) {
-  return reinterpret_cast<P*>(static_cast<char*>(ws) + off);
-}
 
-// Per-kernel profiling events (bo_set_profile_events); graph-capture aware.
-struct Prof {
-  bo_handle* h;
-  cudaStream_t s;
-  bool on = false;
-  unsigned flags = 0;
-  cudaError_t err = cudaSuccess;
-  Prof(bo_handle* h_, cudaStream_t s_, int max_launches) : h(h_), s(s_) {
-    on = h->prof_events && h->prof_n >= max_launches + 1;
-    if (on) {
-      cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-      err = cudaStreamIsCapturing(s, &cap);
-      // under stream capture the events must become graph event-record nodes (external)
-      flags = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
-    }
-  }
-  // event i precedes launch i; `name` (forward path) is appended to the handle's kernel list
-  void mark(int i, const char* name = nullptr) {
-    if (name) {
-      if (!h->last_kernels.empty()) h->last_kernels += ",";
-      h->last_kernels += name;
-    }
-    if (on && err == cudaSuccess && h->prof_events[i])   // NULL entries: no event at that boundary
-      err = cudaEventRecordWithFlags(static_cast<cudaEvent_t>(h->prof_events[i]), s, flags);
-  }
-};
 
 // Steps a1-a3: router logits (Eq. 8), top-K softmax (Eq. 7), per-tile expert
 // histogram; then the local counts / per-tile prefix (and Alg. 1 on the local
 // counts) via the plan kernel.  Returns the token tile used.
 bo_status route_stage(bo_handle* h, const void* x, int64_t T, const void* Wr, const float* logits_in, void* ws,
-                      const bo_ws_layout& L, cudaStream_t s, Prof& prof, int& launches, int& tile) {
+                      const bo_ws_layout& L, cudaStream_t s, Prof& prof, int& launches, int& tile, int32_t* ep_row) {
   const bo_config& c = h->cfg;
   const int dt = c.dtype == BO_BF16 ? 0 : 1;
   const int m = c.num_experts, K = c.top_k, d = c.hidden;
@@ -286,9 +171,9 @@ bo_status route_stage(bo_handle* h, const void* x, int64_t T, const void* Wr, co
     ++launches;
   } else if (bo::router_small_ok(dt, m, d)) {
     // m <= 32: CUDA-core router (HBM-bound); decode-sized batches split each token over several warps
-    const int tpc = h->router_split ? bo::router_split_tpc(static_cast<int>(T), h->num_sms) : 0;
+    const int tpc = h->opt.router_split ? bo::router_split_tpc(static_cast<int>(T), h->num_sms) : 0;
     prof.mark(launches, "router_topk");
-    if (h->router_mma && bo::router_mma_ok(dt, m, d, static_cast<int>(T), h->num_sms)) {
+    if (h->opt.router_mma && bo::router_mma_ok(dt, m, d, static_cast<int>(T), h->num_sms)) {
       tile = 16;
       BO_CUDA(bo::launch_router_mma(x, Wr, static_cast<int>(T), d, m, K, logits, topk_id, topk_w, tile_cnt, s),
               "router");
@@ -328,31 +213,27 @@ bo_status route_stage(bo_handle* h, const void* x, int64_t T, const void* Wr, co
     p.topk_w = topk_w;
     p.tile_cnt = tile_cnt;
     const int work = static_cast<int>((T + bo::kBM - 1) / bo::kBM);
-    int grid = work < h->num_sms ? work : h->num_sms;
-    // fewer 128-token tiles than SMs: split each tile's reduction over 2-4 CTAs in
-    // lockstep (the owner adds the partials before its top-K epilogue)
-    if (h->router_splitk && work * 2 <= h->num_sms) {
-      p.stream_k = 2;
-      p.sk_part = at<float>(ws, L.sk_part);
-      p.sk_flag = at<int>(ws, L.sk_flag);
-      grid = h->num_sms;
-      BO_CUDA(cudaMemsetAsync(p.sk_flag, 0, sizeof(int) * h->num_sms, s), "split flags");
-    }
+    const int grid = work < h->num_sms ? work : h->num_sms;
     prof.mark(launches, "router_topk");
     bo::BMaps mbs;
     for (int i = 0; i < 12; ++i) mbs.m[i] = mB;
-    BO_CUDA(bo::launch_grouped_gemm(dt, bo::EPI_ROUTER, bn, mA, mbs, p, grid, s), "router gemm");
+    BO_CUDA(bo::launch_grouped_gemm(dt, bo::EPI_ROUTER, bn, mA, mbs, p, grid, s, h->opt.pdl), "router gemm");
     ++launches;
   }
   const int ntiles = static_cast<int>((T + tile - 1) / tile);
   // Alg. 1 over this batch (snapshot of the knob at enqueue time); also yields
   // cnt_i and the per-tile prefix the permutation needs.
   prof.mark(launches, "plan");
+  bo::PlanExt ext;
+  if (ep_row) {   // expert parallelism: this rank's counts row [m] + knob tail [4] (the all-gather input)
+    ext.row_tail = ep_row + m;
+    ext.row_T = static_cast<int>(T);
+  }
   BO_CUDA(bo::launch_plan(tile_cnt, ntiles, m, c.way, h->ratio, h->mode, at<int32_t>(ws, L.tile_base),
-                          at<int32_t>(ws, L.counts), at<int32_t>(ws, L.exec_of_expert),
+                          ep_row ? ep_row : at<int32_t>(ws, L.counts), at<int32_t>(ws, L.exec_of_expert),
                           at<int32_t>(ws, L.expert_row_off), at<int32_t>(ws, L.exec_off),
                           at<int32_t>(ws, L.mtile_off), at<int64_t>(ws, L.stats), s, c.num_shared,
-                          static_cast<int>(T)),
+                          static_cast<int>(T), ext),
           "plan");
   ++launches;
   h->route_T = T;
@@ -364,33 +245,14 @@ bo_status route_stage(bo_handle* h, const void* x, int64_t T, const void* Wr, co
 // row gate weight.  Executors [0, n_orig) read Wg/Wu/Wd stacks of width f,
 // executors [n_orig, n_orig + n_united) read UWg/UWu/UWd stacks of width f_u
 // (f_u < f: expert-parallel f-slices of united experts).
-// Weights of one executor class: stacked [n, f, d] gate / up and [n, d, f] down.
-struct FfnClass {
-  const void* Wg = nullptr;
-  const void* Wu = nullptr;
-  const void* Wd = nullptr;
-  int n = 0;        // executors of this class in the row layout
-  int f = 0;        // width (united: f-slice under expert parallelism)
-  int64_t stack = 0;  // experts in the weight stacks (>= n; tensor-map extent)
-};
 
 // L2 policy of the weight (B) tile loads: decode-sized steps stream every weight tile
 // once per concurrent m-tile pair, so evict_first keeps the re-read activations in L2.
 int b_policy_for(const bo_handle* h, int64_t R) {
-  if (h->b_policy >= 0) return h->b_policy;
+  if (h->opt.b_policy >= 0) return h->opt.b_policy;
   return R <= kSplitRows ? 1 : 0;
 }
 
-// The combine (a8) fused into GEMM2's epilogue (bo::GemmParams::comb_cnt).
-struct CombFuse {
-  int32_t* cnt;            // [T, d / BN2] arrival counters (workspace)
-  const int32_t* row_of;   // [T, KR]
-  int KR;
-  int64_t T;
-  const void* x;
-  void* y;
-  int add_residual;
-};
 
 void set_comb(bo::GemmParams& p, const CombFuse* cf, int d, int nt2) {
   if (!cf) return;
@@ -410,17 +272,12 @@ void set_comb(bo::GemmParams& p, const CombFuse* cf, int d, int nt2) {
 // second term: every token, weight 1); the united class may have its own width.
 bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, const int32_t* exec_off,
                     const int32_t* mtile_off, const FfnClass& orig, const FfnClass& uni, const FfnClass& shr,
-                    void* Hbuf, void* Y, cudaStream_t s, Prof& prof, int& launches,
-                    const int32_t* gather_tok = nullptr, int64_t gather_T = 0, float* partial = nullptr,
-                    int* ks_dev = nullptr, const CombFuse* comb = nullptr,
-                    const int32_t* comb_row_tok = nullptr, float* sk_part = nullptr, int* sk_flag = nullptr,
-                    bool force_pair2 = false) {
-  // sk_part != nullptr: stream-K for the single-CTA (non-pair) GEMMs (flags zeroed by the caller)
+                    void* Hbuf, void* Y, cudaStream_t s, Prof& prof, int& launches, float* partial,
+                    int* ks_dev, const CombFuse* comb, const int32_t* comb_row_tok, bool force_pair2) {
   // partial != nullptr: GEMM2 runs split-K into fp32 partials [<=8, R, d] (the
   // caller combines them with launch_combine_partials); Y is then unused.
-  // gather_tok != nullptr: X is the token matrix x [gather_T, d] and GEMM1 gathers
-  // row r = x[gather_tok[r]] with TMA tile::gather4 (no packed Xp).
   const bo_config& c = h->cfg;
+  const EngineOptions& o = h->opt;
   const int dt = c.dtype == BO_BF16 ? 0 : 1;
   const int d = c.hidden, f = c.ffn;
   const int f_u = uni.n > 0 ? uni.f : f;
@@ -437,37 +294,30 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     const FfnClass& q = k.Wg ? k : any;
     return static_cast<uint64_t>(q.stack > 0 ? q.stack : 1) * width;
   };
-  // Tile width: widest tile everywhere.  (Narrower decode tiles, tried to cut
-  // the wave quantisation of few-row steps, measured slower: r01 profiles.)
-  const int tier = 256;
+  const FfnClass* cls[3] = {&orig, &uni, &shr};
   {
-    int bn = tier;                                                  // gate + up columns per tile
-    if (R <= kSplitRows && h->decode_bn1 > 0 && c.weight_layout != BO_WEIGHTS_TILED)
-      bn = h->decode_bn1;   // experiment knob (BO_DECODE_BN1)
+    // Widest tile everywhere (narrower decode tiles, tried to cut the wave quantisation
+    // of few-row steps, measured slower: r01 profiles); the device may still pick the
+    // alternative width below.
+    int bn = 256;                                                   // gate + up columns per tile
     while (bn > 64 && (f % (bn / 2) || f_u % (bn / 2))) bn >>= 1;
     CUtensorMap mA;
     bo::BMaps mb;
-    const bool gather = gather_tok != nullptr;
-    if (gather) {
-      if ((st = make_map(&mA, X, c.dtype, gather_T, d, 1)) != BO_OK) return st;   // box {64 cols, 1 row}
-    } else {
-      if ((st = make_map(&mA, X, c.dtype, R, d, bo::kBM)) != BO_OK) return st;
-    }
-    const FfnClass* cls[3] = {&orig, &uni, &shr};
+    if ((st = make_map(&mA, X, c.dtype, R, d, bo::kBM)) != BO_OK) return st;
     for (int k = 0; k < 3; ++k) {
       const int width = k == 1 ? f_u : f;
-      if ((st = make_map_w(h, &mb.m[2 * k], ptr(*cls[k], 0), rows_of(*cls[k], width), d, bn / 2)) != BO_OK)
+      if ((st = make_map(&mb.m[2 * k], ptr(*cls[k], 0), c.dtype, rows_of(*cls[k], width), d, bn / 2)) != BO_OK)
         return st;
-      if ((st = make_map_w(h, &mb.m[2 * k + 1], ptr(*cls[k], 1), rows_of(*cls[k], width), d, bn / 2)) != BO_OK)
+      if ((st = make_map(&mb.m[2 * k + 1], ptr(*cls[k], 1), c.dtype, rows_of(*cls[k], width), d, bn / 2)) != BO_OK)
         return st;
     }
     bo::GemmParams p{};
     // 256 x 256 tiles on CTA pairs when rows are plentiful (prefill); few-row
     // (decode) steps keep 128-row tiles so that more tiles share the SMs.
-    const bool pair = h->cta_pairs && dt == 0 && bn == 256 && R >= h->pair_rows1;
+    const bool pair = o.cta_pairs && dt == 0 && bn == 256 && R >= o.pair_rows1;
     // swapped-operand tail tiles (pairs): maps [6..11] = 64-row gate / up boxes,
     // [12..14] = Xp in 16 / 32 / 64-row boxes
-    const bool swap = pair && !gather && (h->swap_tail & 1) && c.weight_layout != BO_WEIGHTS_TILED;
+    const bool swap = pair && o.swap_tail;
     if (swap) {
       for (int k = 0; k < 3; ++k) {
         const int width = k == 1 ? f_u : f;
@@ -479,12 +329,11 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
       for (int i = 0; i < 3; ++i)
         if ((st = make_map(&mb.m[12 + i], X, c.dtype, R, d, 16u << i)) != BO_OK) return st;
       p.swap_tail = 1;
-      p.swap_max = h->swap_max;
     }
     // alternative tile width for the device-side wave choice: the widest gate/up half
     // below bn/2 (multiple of 16, >= 64) that divides both widths
     int bh_alt = 0;
-    if (h->tile_alt && !gather && !swap && c.weight_layout != BO_WEIGHTS_TILED)   // packed bands are 128 rows
+    if (o.tile_alt && !swap)
       for (int bh = bn / 2 - 16; bh >= 64 && !bh_alt; bh -= 16)
         if (f % bh == 0 && f_u % bh == 0) bh_alt = bh;
     if (bh_alt) {
@@ -508,64 +357,40 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.n_valid = f;
     p.m_orig = orig.n;
     p.m_united = uni.n;
-    p.store_hint = h->store_hint && R > kSplitRows;   // decode: H / Yp (a few MB) stay in L2 for the next kernel
-    p.pf_dist = h->pf_dist;
+    p.store_hint = o.store_hint && R > kSplitRows;   // decode: H / Yp (a few MB) stay in L2 for the next kernel
     p.b_policy = b_policy_for(h, R);
-    p.a_policy = h->a_policy;
-    p.b_packed = c.weight_layout == BO_WEIGHTS_TILED ? 1 : 0;
     p.b_rows_per_exec = f;
     p.num_exec = n_exec;
     p.single_rows = -1;
     p.exec_off = exec_off;
     p.mtile_off = mtile_off;
     p.out = Hbuf;
-    p.row_tok = gather_tok;
     p.rows_total = static_cast<int>(R);
-    {
-      int bn2 = gemm2_bn(d);
-      if (bn2 > tier) bn2 = tier;
-      set_comb(p, comb, d, d / bn2);   // GEMM1's prologue zeroes GEMM2's arrival counters
-    }
+    set_comb(p, comb, d, d / gemm2_bn(d));   // GEMM1's prologue zeroes GEMM2's arrival counters
     const int tile_m = pair ? 2 * bo::kBM : bo::kBM;
     const int64_t max_work = ((R + tile_m - 1) / tile_m + n_exec) * p.n_tiles;
     const int units = pair ? h->num_sms / 2 : h->num_sms;
-    const bool skm = sk_part && !pair && !gather;
-    if (skm) {
-      p.stream_k = h->stream_k;
-      p.sk_part = sk_part;
-      p.sk_flag = sk_flag;
-    }
-    const int grid = skm ? h->num_sms : static_cast<int>(max_work < units ? max_work : units) * (pair ? 2 : 1);
+    const int grid = static_cast<int>(max_work < units ? max_work : units) * (pair ? 2 : 1);
     prof.mark(launches, "gemm1_swiglu");
-    const int epi = gather ? (pair ? bo::EPI_SWIGLU_PAIR_GATHER : bo::EPI_SWIGLU_GATHER)
-                           : (pair ? bo::EPI_SWIGLU_PAIR : bo::EPI_SWIGLU);
-    BO_CUDA(bo::launch_grouped_gemm(dt, epi, bn, mA, mb, p, grid, s), "gemm1");
+    BO_CUDA(bo::launch_grouped_gemm(dt, pair ? bo::EPI_SWIGLU_PAIR : bo::EPI_SWIGLU, bn, mA, mb, p, grid, s, o.pdl),
+            "gemm1");
     ++launches;
   }
   {
-    int bn = gemm2_bn(d);
-    if (bn > tier) bn = tier;
-    const bool pair = h->cta_pairs && dt == 0 && bn == 256 && (R >= h->pair_rows2 || force_pair2);   // each CTA of a pair stages BN/2 of B
+    const int bn = gemm2_bn(d);
+    const bool pair = o.cta_pairs && dt == 0 && bn == 256 && (R >= o.pair_rows2 || force_pair2);   // each CTA of a pair stages BN/2 of B
     const uint32_t box_b = pair ? bn / 2 : bn;
     CUtensorMap mA;
     bo::BMaps mb;
     if ((st = make_map(&mA, Hbuf, c.dtype, R, f, bo::kBM)) != BO_OK) return st;
-    // swapped-operand tail tiles (pairs, no split-K): [12..14] = H in 16 / 32 / 64-row boxes
-    if (pair && (h->swap_tail & 2) && !partial && c.weight_layout != BO_WEIGHTS_TILED) {
-      for (int i = 0; i < 3; ++i)
-        if ((st = make_map(&mb.m[12 + i], Hbuf, c.dtype, R, f, 16u << i)) != BO_OK) return st;
-    }
-    const FfnClass* cls[3] = {&orig, &uni, &shr};
     for (int k = 0; k < 3; ++k) {
       const FfnClass& q = cls[k]->Wg ? *cls[k] : any;
       const int kdim = k == 1 ? f_u : f;
       const uint64_t rows = static_cast<uint64_t>(q.stack > 0 ? q.stack : 1) * d;
-      if ((st = make_map_w(h, &mb.m[2 * k], ptr(*cls[k], 2), rows, kdim, box_b)) != BO_OK) return st;
+      if ((st = make_map(&mb.m[2 * k], ptr(*cls[k], 2), c.dtype, rows, kdim, box_b)) != BO_OK) return st;
       mb.m[2 * k + 1] = mb.m[2 * k];
     }
     bo::GemmParams p{};
-    p.swap_tail = (pair && (h->swap_tail & 2) && !partial && c.weight_layout != BO_WEIGHTS_TILED) ? 1 : 0;
-    p.swap_max = h->swap_max;
     p.Kdim = f;
     p.n_tiles = d / bn;
     p.Kdim_u = f_u;
@@ -575,18 +400,15 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.n_valid = d;
     p.m_orig = orig.n;
     p.m_united = uni.n;
-    p.store_hint = h->store_hint && R > kSplitRows;   // decode: H / Yp (a few MB) stay in L2 for the next kernel
-    p.pf_dist = h->pf_dist;
+    p.store_hint = o.store_hint && R > kSplitRows;   // decode: H / Yp (a few MB) stay in L2 for the next kernel
     p.b_policy = b_policy_for(h, R);
-    p.a_policy = h->a_policy;
-    p.b_packed = c.weight_layout == BO_WEIGHTS_TILED ? 1 : 0;
     p.b_rows_per_exec = d;
     p.num_exec = n_exec;
     p.single_rows = -1;
     p.exec_off = exec_off;
     p.mtile_off = mtile_off;
     p.out = Y;
-    if (h->tma_store && dt == 0 && !partial) {
+    if (o.tma_store && dt == 0 && !partial) {
       if ((st = make_map_store32(&mb.m[6], Y, static_cast<uint64_t>(R), static_cast<uint64_t>(d))) != BO_OK) return st;
       p.tma_store = 1;
     }
@@ -605,19 +427,48 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     const int tile_m = pair ? 2 * bo::kBM : bo::kBM;
     const int64_t max_work = ((R + tile_m - 1) / tile_m + n_exec) * p.n_tiles;
     const int units = pair ? h->num_sms / 2 : h->num_sms;
-    const bool skm = sk_part && !pair && !partial && f_u == f;
-    if (skm) {
-      p.stream_k = h->stream_k;
-      p.sk_part = sk_part;
-      p.sk_flag = sk_flag;
-    }
-    const int grid = skm ? h->num_sms : static_cast<int>(max_work < units ? max_work : units) * (pair ? 2 : 1);
+    const int grid = static_cast<int>(max_work < units ? max_work : units) * (pair ? 2 : 1);
     prof.mark(launches, comb ? "gemm2_weighted_combine" : "gemm2_weighted");
-    BO_CUDA(bo::launch_grouped_gemm(dt, pair ? bo::EPI_WEIGHTED_PAIR : bo::EPI_WEIGHTED, bn, mA, mb, p, grid, s),
+    BO_CUDA(bo::launch_grouped_gemm(dt, pair ? bo::EPI_WEIGHTED_PAIR : bo::EPI_WEIGHTED, bn, mA, mb, p, grid, s,
+                                    o.pdl),
             "gemm2");
     ++launches;
   }
   return BO_OK;
+}
+
+// Engine options by bo_engine_option id (include/brownout.h): field, environment name,
+// allowed range.
+struct OptionSpec {
+  int32_t EngineOptions::*field;
+  const char* env;
+  int32_t lo, hi;
+};
+const OptionSpec kOptions[BO_OPT_COUNT] = {
+    {&EngineOptions::cta_pairs, "BO_CTA_PAIRS", 0, 1},
+    {&EngineOptions::pair_rows1, "BO_PAIR_ROWS1", 1, 1 << 30},
+    {&EngineOptions::pair_rows2, "BO_PAIR_ROWS2", 1, 1 << 30},
+    {&EngineOptions::tile_alt, "BO_TILE_ALT", 0, 1},
+    {&EngineOptions::swap_tail, "BO_SWAP_TAIL", 0, 1},
+    {&EngineOptions::decode_pair2, "BO_DECODE_PAIR2", 0, 1},
+    {&EngineOptions::gemm2_splitk, "BO_GEMM2_SPLITK", 0, 1},
+    {&EngineOptions::fused_combine, "BO_FUSED_COMBINE", 0, 2},
+    {&EngineOptions::tma_store, "BO_TMA_STORE", 0, 1},
+    {&EngineOptions::store_hint, "BO_STORE_HINT", 0, 1},
+    {&EngineOptions::b_policy, "BO_B_POLICY", -1, 1},
+    {&EngineOptions::router_mma, "BO_ROUTER_MMA", 0, 1},
+    {&EngineOptions::router_split, "BO_ROUTER_SPLIT", 0, 1},
+    {&EngineOptions::pdl, "BO_PDL", 0, 1},
+};
+
+void options_from_env(EngineOptions* o) {
+  for (const OptionSpec& sp : kOptions) {
+    const char* v = getenv(sp.env);
+    if (!v || !*v) continue;
+    char* end = nullptr;
+    const long x = strtol(v, &end, 10);
+    if (end && *end == 0 && x >= sp.lo && x <= sp.hi) o->*sp.field = static_cast<int32_t>(x);
+  }
 }
 
 bo_status check_ws(const bo_handle* h, int64_t T, void* ws, size_t ws_bytes, bo_ws_layout* L) {
@@ -675,7 +526,7 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   // Small batches: the permute CTAs also copy the rows (one launch less).  Large
   // batches: a separate grid-wide gather (the permute has too few CTAs to move
   // R*d*2 bytes at HBM speed; measured r01).
-  const bool gather_in_permute = !h->fused_gather && Rt <= kSplitRows * 2 && !c.dedup_united;
+  const bool gather_in_permute = Rt <= kSplitRows * 2 && !c.dedup_united;
   if (c.dedup_united) {
     // f3: one row per (token, united executor); Alg. 1 above is unchanged
     for (int stage = 0; stage < 3; ++stage) {
@@ -689,44 +540,42 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
       ++launches;
     }
   } else {
-  prof.mark(launches, gather_in_permute ? "permute_gather" : "permute");
-  BO_CUDA(bo::launch_permute(at<int32_t>(ws, L.topk_id), at<float>(ws, L.topk_w), static_cast<int>(T), K, m, tile,
-                             at<int32_t>(ws, L.tile_base), at<int32_t>(ws, L.expert_row_off), 1, row_of,
-                             at<int32_t>(ws, L.row_tok), row_w, s, dt, x,
-                             gather_in_permute ? at<char>(ws, L.xp) : nullptr, d, Ns,
-                             at<int32_t>(ws, L.exec_off) + E),
-          "permute");
-  ++launches;
+    prof.mark(launches, gather_in_permute ? "permute_gather" : "permute");
+    BO_CUDA(bo::launch_permute(at<int32_t>(ws, L.topk_id), at<float>(ws, L.topk_w), static_cast<int>(T), K, m, tile,
+                               at<int32_t>(ws, L.tile_base), at<int32_t>(ws, L.expert_row_off), 1, row_of,
+                               at<int32_t>(ws, L.row_tok), row_w, s, dt, x,
+                               gather_in_permute ? at<char>(ws, L.xp) : nullptr, d, Ns,
+                               at<int32_t>(ws, L.exec_off) + E),
+            "permute");
+    ++launches;
   }
-  if (!h->fused_gather && !gather_in_permute) {
+  if (!gather_in_permute) {
     prof.mark(launches, "gather");
     BO_CUDA(bo::launch_gather(dt, x, static_cast<int>(T), d, KR, row_of, at<char>(ws, L.xp), h->num_sms, s), "gather");
     ++launches;
   }
-  // a6-a7: grouped SwiGLU FFN over the m original + G united executors.  The
-  // gather kernel materialises Xp (concat_tokens); BO_GATHER=1 instead lets
-  // GEMM1 gather its A rows from x with TMA tile::gather4 (slower, see above).
+  // a6-a7: grouped SwiGLU FFN over the m original + G united (+ N_s shared) executors
+  // on the materialised Xp (concat_tokens).
   void* yp = at<char>(ws, L.yp);
   const int32_t* row_tok = at<int32_t>(ws, L.row_tok);
-  // decode-sized steps: optional GEMM2 split-K into fp32 partials (fills the SMs
-  // when few executor tiles exist); BO_SPLITK=1 enables
   // Decode-sized steps whose executors hold >= 256 rows each (brownout ratio near 1: the
   // G united experts take almost every row; estimate (1 - ratio) m + ratio G executors):
   // GEMM2 on CTA pairs (one 256-row tile per executor instead of two 128-row tiles reading
   // the same weights) with split-K partials to fill the SMs.  C3 ratio 1: GEMM2
   // 0.101 -> 0.071 ms (profiles/r01_ab_decode_pairs_splitk.json); a loss at ratios 0 / 0.5.
+  const EngineOptions& o = h->opt;
   const double est_exec = (1.0 - h->ratio) * m + h->ratio * G;
-  const bool decode_pair2 = h->decode_pair2 && h->cta_pairs && dt == 0 && Rt <= kSplitRows &&
-                            !h->fused_gather && h->mode == BO_PARTIAL && Ns == 0 &&
+  const bool decode_pair2 = o.decode_pair2 && o.cta_pairs && dt == 0 && Rt <= kSplitRows &&
+                            h->mode == BO_PARTIAL && Ns == 0 &&
                             static_cast<double>(Rt) >= 256.0 * (est_exec < 1.0 ? 1.0 : est_exec);
-  const bool split = (h->splitk || decode_pair2) && Rt <= kSplitRows && !h->fused_gather;
+  const bool split = (o.gemm2_splitk || decode_pair2) && Rt <= kSplitRows;
   // a8 fused into GEMM2's epilogue unless split-K partials need their own combine
   // Auto: fused only where it measured faster (interleaved A/B, profiles/r01_ab_fused_combine.json):
   // prefill-sized steps with <= 2 rows per token (C2: GEMM2 + combine -5 %); with K = 8 (C4) the
   // completing warps' memory round trips (fence, count, 8 row loads) outrun GEMM2's short
   // per-tile mainloop, and decode steps (< 1 wave of GEMM2 tiles) expose them at the end.
   const bool fuse_comb = !split && KR <= 16 &&   // 16 = kCombSlots (bo_gemm.cu)
-                         (h->fused_combine == 1 || (h->fused_combine == 2 && KR <= 2 && Rt >= 2048));
+                         (o.fused_combine == 1 || (o.fused_combine == 2 && KR <= 2 && Rt >= 2048));
   CombFuse cf;
   cf.cnt = at<int32_t>(ws, L.comb_cnt);
   cf.row_of = row_of;
@@ -736,39 +585,26 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   cf.y = y;
   cf.add_residual = c.add_residual;
   const CombFuse* cfp = fuse_comb ? &cf : nullptr;
-  // stream-K for decode-sized steps (the workspace holds its partial tiles then)
-  const bool use_sk = h->stream_k != 0 && Rt <= kSplitRows && !h->fused_gather;   // (flags are clean after a split router)
-  float* sk_part = use_sk ? at<float>(ws, L.sk_part) : nullptr;
-  int* sk_flag = use_sk ? at<int>(ws, L.sk_flag) : nullptr;
-  if (use_sk) BO_CUDA(cudaMemsetAsync(sk_flag, 0, sizeof(int) * h->num_sms, s), "stream-K flags");
   FfnClass orig, uni, shr;
   orig.Wg = Wg; orig.Wu = Wu; orig.Wd = Wd; orig.n = m; orig.f = f; orig.stack = m;
   uni.Wg = UWg; uni.Wu = UWu; uni.Wd = UWd; uni.n = G; uni.f = f; uni.stack = have_united ? G : m;
   if (Ns > 0) { shr.Wg = h->SWg; shr.Wu = h->SWu; shr.Wd = h->SWd; shr.n = Ns; shr.f = f; shr.stack = Ns; }
-  if (h->fused_gather) {
-    if ((st = ffn_stage(h, x, Rt, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), orig, uni, shr,
-                        at<char>(ws, L.h), yp, s, prof, launches, row_tok, T, nullptr, nullptr, cfp,
-                        row_tok)) != BO_OK)
-      return st;
-  } else {
-    void* xp = at<char>(ws, L.xp);   // filled by the permute (small batches) or the gather kernel
-    if ((st = ffn_stage(h, xp, Rt, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), orig, uni, shr,
-                        at<char>(ws, L.h), yp, s, prof, launches, nullptr, 0,
-                        split ? at<float>(ws, L.partial) : nullptr, split ? at<int>(ws, L.ksplit) : nullptr, cfp,
-                        row_tok, sk_part, sk_flag, decode_pair2)) != BO_OK)
-      return st;
-  }
+  void* xp = at<char>(ws, L.xp);   // filled by the permute (small batches) or the gather kernel
+  if ((st = ffn_stage(h, xp, Rt, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), orig, uni, shr,
+                      at<char>(ws, L.h), yp, s, prof, launches, split ? at<float>(ws, L.partial) : nullptr,
+                      split ? at<int>(ws, L.ksplit) : nullptr, cfp, row_tok, decode_pair2)) != BO_OK)
+    return st;
   // a8: combine (Eq. 5 sum over the token's K slots; split-K partials summed first)
   if (!fuse_comb) {
-  prof.mark(launches, "combine");
-  if (split)
-    BO_CUDA(bo::launch_combine_partials(dt, at<float>(ws, L.partial), at<int>(ws, L.ksplit), Rt, x,
-                                        static_cast<int>(T), d, KR, row_of, c.add_residual, y, h->num_sms, s),
-            "combine");
-  else
-    BO_CUDA(bo::launch_combine(dt, yp, x, static_cast<int>(T), d, KR, row_of, c.add_residual, y, h->num_sms, s),
-            "combine");
-  ++launches;
+    prof.mark(launches, "combine");
+    if (split)
+      BO_CUDA(bo::launch_combine_partials(dt, at<float>(ws, L.partial), at<int>(ws, L.ksplit), Rt, x,
+                                          static_cast<int>(T), d, KR, row_of, c.add_residual, y, h->num_sms, s),
+              "combine");
+    else
+      BO_CUDA(bo::launch_combine(dt, yp, x, static_cast<int>(T), d, KR, row_of, c.add_residual, y, h->num_sms, s),
+              "combine");
+    ++launches;
   }
   prof.mark(launches);
   if (prof.err != cudaSuccess) return cuda_fail(prof.err, "profile event record");
@@ -804,7 +640,7 @@ bo_status plain_gemm(bo_handle* h, const PlainGemm& g, cudaStream_t s, Prof& pro
   if (g.rows_total == 0) return BO_OK;
   bo_status st;
   int bn = gemm2_bn(g.n_cols);
-  const bool pair = h->cta_pairs && bn == 256 && g.rows_total >= 2048;
+  const bool pair = h->opt.cta_pairs && bn == 256 && g.rows_total >= 2048;
   CUtensorMap mA, mB;
   if ((st = make_map(&mA, g.A, BO_BF16, g.a_rows, g.Kdim, bo::kBM)) != BO_OK) return st;
   if ((st = make_map(&mB, g.B, BO_BF16, g.b_rows, g.Kdim, pair ? bn / 2 : bn)) != BO_OK) return st;
@@ -839,7 +675,8 @@ bo_status plain_gemm(bo_handle* h, const PlainGemm& g, cudaStream_t s, Prof& pro
   const int units = pair ? h->num_sms / 2 : h->num_sms;
   const int grid = static_cast<int>(max_work < units ? max_work : units) * (pair ? 2 : 1);
   prof.mark(launches);
-  BO_CUDA(bo::launch_grouped_gemm(0, pair ? bo::EPI_WEIGHTED_PAIR : bo::EPI_WEIGHTED, bn, mA, mb, p, grid, s),
+  BO_CUDA(bo::launch_grouped_gemm(0, pair ? bo::EPI_WEIGHTED_PAIR : bo::EPI_WEIGHTED, bn, mA, mb, p, grid, s,
+                                  h->opt.pdl),
           "distill gemm");
   ++launches;
   return BO_OK;
@@ -897,7 +734,9 @@ bo_status distill_check(const bo_handle* h, int64_t N, void* ws, size_t ws_bytes
   return BO_OK;
 }
 
-}  // namespace
+}  // namespace bo_impl
+
+using namespace bo_impl;
 
 extern "C" {
 
@@ -933,7 +772,7 @@ bo_status bo_distill_prepare(bo_handle* h, const void* X, int64_t N, const void*
     const int64_t R = N * m;
     int bn = 256;
     while (bn > 64 && f % (bn / 2)) bn >>= 1;
-    const bool pair = h->cta_pairs && bn == 256 && R >= 2048;
+    const bool pair = h->opt.cta_pairs && bn == 256 && R >= 2048;
     CUtensorMap mA;
     bo::BMaps mb;
     if ((st = make_map(&mA, X, BO_BF16, N, d, bo::kBM)) != BO_OK) return st;
@@ -960,7 +799,8 @@ bo_status bo_distill_prepare(bo_handle* h, const void* X, int64_t N, const void*
     const int64_t max_work = ((R + tile_m - 1) / tile_m + m) * p.n_tiles;
     const int units = pair ? h->num_sms / 2 : h->num_sms;
     const int grid = static_cast<int>(max_work < units ? max_work : units) * (pair ? 2 : 1);
-    BO_CUDA(bo::launch_grouped_gemm(0, pair ? bo::EPI_SWIGLU_PAIR : bo::EPI_SWIGLU, bn, mA, mb, p, grid, s),
+    BO_CUDA(bo::launch_grouped_gemm(0, pair ? bo::EPI_SWIGLU_PAIR : bo::EPI_SWIGLU, bn, mA, mb, p, grid, s,
+                                    h->opt.pdl),
             "teacher gemm1");
   }
   PlainGemm g2;   // H_o = H Wd^T in fp32
@@ -1167,11 +1007,6 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   if (c.hidden <= 0 || c.hidden % mult || c.ffn <= 0 || c.ffn % mult)
     return fail(BO_ERR_SHAPE, "hidden=%d / ffn=%d must be positive multiples of %d", c.hidden, c.ffn, mult);
   if (c.ffn % 64) return fail(BO_ERR_SHAPE, "ffn=%d must be a multiple of 64", c.ffn);
-  if (c.weight_layout != BO_WEIGHTS_ROWMAJOR && c.weight_layout != BO_WEIGHTS_TILED)
-    return fail(BO_ERR_UNSUPPORTED, "weight_layout %d not built", c.weight_layout);
-  if (c.weight_layout == BO_WEIGHTS_TILED && (c.hidden % bo::kPackRows || c.ffn % bo::kPackRows))
-    return fail(BO_ERR_SHAPE, "TILED weights need hidden=%d and ffn=%d to be multiples of %d", c.hidden, c.ffn,
-                bo::kPackRows);
   const int G = (c.num_experts + c.way - 1) / c.way;
   if (c.num_shared < 0 || c.num_experts + G + c.num_shared > bo::kMaxExec)
     return fail(BO_ERR_INVALID_ARG, "num_shared=%d: m + G + N_s must be <= %d", c.num_shared, bo::kMaxExec);
@@ -1194,61 +1029,25 @@ bo_status bo_create(const bo_config* cfg, bo_handle** out) {
   h->route_T = -1;
   h->route_tile = 0;
   h->SWg = h->SWu = h->SWd = nullptr;
-  const char* cg = getenv("BO_GEMM_CG");
-  h->cta_pairs = (cg && cg[0] == '1') ? 0 : 1;
-  const char* skk = getenv("BO_STREAMK");
-  h->stream_k = skk ? atoi(skk) : 0;
-  if (h->stream_k < 0 || h->stream_k > 2) h->stream_k = 0;
-  const char* dp2 = getenv("BO_DECODE_PAIR2");
-  h->decode_pair2 = (dp2 && dp2[0] == '0') ? 0 : 1;
-  const char* rsk = getenv("BO_ROUTER_SPLITK");
-  h->router_splitk = (rsk && rsk[0] == '1') ? 1 : 0;
-  const char* bpo = getenv("BO_B_POLICY");
-  h->b_policy = bpo ? atoi(bpo) : -1;
-  const char* pdl = getenv("BO_PDL");
-  bo::set_gemm_pdl(!(pdl && pdl[0] == '0'));
-  const char* pfd = getenv("BO_PF_DIST");
-  h->pf_dist = pfd ? atoi(pfd) : 0;
-  const char* pr1 = getenv("BO_PAIR_ROWS1");
-  const char* pr2 = getenv("BO_PAIR_ROWS2");
-  h->pair_rows1 = pr1 ? atoi(pr1) : 2048;
-  h->pair_rows2 = pr2 ? atoi(pr2) : 2048;
-  // TMA gather4 (4 rows x 128 B per instruction, 32 per k-block) measured 2.8x slower
-  // than materialising Xp (r01 profiles): off unless BO_GATHER=1.
-  const char* ga = getenv("BO_GATHER");
-  h->fused_gather = (ga && ga[0] == '1') ? 1 : 0;
-  // GEMM2 split-K for decode-sized steps: measured mixed (-11 % GEMM2 at ratio 1,
-  // +2 % step at ratios 0 / 0.5, profiles/r01_bench_decode_splitk_*.json): off unless BO_SPLITK=1.
-  const char* sk = getenv("BO_SPLITK");
-  h->splitk = (sk && sk[0] == '1') ? 1 : 0;
-  const char* sh = getenv("BO_STORE_HINT");
-  // evict_first on the streaming H / Yp stores keeps weight tiles in L2: C2 GEMM1 DRAM reads
-  // 1.60 -> 1.47 GB, step -1.2 % (interleaved A/B, profiles/r01_ab_store_hint.json)
-  h->store_hint = (sh && sh[0] == '0') ? 0 : 1;
-  const char* fc = getenv("BO_FUSED_COMBINE");
-  h->fused_combine = (fc && fc[0] == '0') ? 0 : ((fc && fc[0] == '1') ? 1 : 2);
-  const char* ta = getenv("BO_TILE_ALT");
-  h->tile_alt = (ta && ta[0] == '0') ? 0 : 1;
-  // Swapped-operand tail tiles: GEMM1 C2 1.329 -> 1.305 ms (ratio 0.5), 1.393 -> 1.352 (ratio 0)
-  // (profiles/r01_ncu_ab_swap_tail.txt); GEMM2 neutral (-1.5 .. +0.5 %), so GEMM1 only by default
-  // TMA bulk stores of GEMM2's full Yp slabs: C4 GEMM2 190.2 -> 183.2 us, f2 149.6 -> 146.4 us,
-  // C2 / C3 neutral (profiles/r01_ncu_ab_tma_store.txt)
-  const char* apo = getenv("BO_A_POLICY");
-  h->a_policy = apo ? atoi(apo) : 0;
-  const char* tst = getenv("BO_TMA_STORE");
-  h->tma_store = (tst && tst[0] == '0') ? 0 : 1;
-  const char* swm = getenv("BO_SWAP_MAX");
-  h->swap_max = swm ? atoi(swm) : 0;
-  const char* swt = getenv("BO_SWAP_TAIL");
-  h->swap_tail = swt ? (atoi(swt) & 3) : 1;
-  const char* rm = getenv("BO_ROUTER_MMA");
-  h->router_mma = (rm && rm[0] == '0') ? 0 : 1;
-  const char* rs = getenv("BO_ROUTER_SPLIT");
-  h->router_split = (rs && rs[0] == '0') ? 0 : 1;
-  const char* bn1 = getenv("BO_DECODE_BN1");
-  h->decode_bn1 = bn1 ? atoi(bn1) : 0;
-  if (h->decode_bn1 != 0 && h->decode_bn1 != 64 && h->decode_bn1 != 128 && h->decode_bn1 != 256) h->decode_bn1 = 0;
+  options_from_env(&h->opt);
   *out = h;
+  return BO_OK;
+}
+
+bo_status bo_set_engine_option(bo_handle* h, int32_t option, int32_t value) {
+  if (!h) return fail(BO_ERR_INVALID_ARG, "null handle");
+  if (option < 0 || option >= BO_OPT_COUNT) return fail(BO_ERR_INVALID_ARG, "engine option %d unknown", option);
+  const OptionSpec& sp = kOptions[option];
+  if (value < sp.lo || value > sp.hi)
+    return fail(BO_ERR_INVALID_ARG, "%s=%d outside [%d, %d]", sp.env, value, sp.lo, sp.hi);
+  h->opt.*sp.field = value;
+  return BO_OK;
+}
+
+bo_status bo_get_engine_option(const bo_handle* h, int32_t option, int32_t* value) {
+  if (!h || !value) return fail(BO_ERR_INVALID_ARG, "null argument");
+  if (option < 0 || option >= BO_OPT_COUNT) return fail(BO_ERR_INVALID_ARG, "engine option %d unknown", option);
+  *value = h->opt.*kOptions[option].field;
   return BO_OK;
 }
 
@@ -1298,21 +1097,6 @@ bo_status bo_build_united(bo_handle* h, const void* Wg, const void* Wu, const vo
   BO_CUDA(bo::launch_build_united(dt, Wg, c.num_experts, c.way, per, UWg, s), "build_united Wg");
   BO_CUDA(bo::launch_build_united(dt, Wu, c.num_experts, c.way, per, UWu, s), "build_united Wu");
   BO_CUDA(bo::launch_build_united(dt, Wd, c.num_experts, c.way, per, UWd, s), "build_united Wd");
-  return BO_OK;
-}
-
-bo_status bo_pack_weights(const bo_handle* h, const void* W, int64_t n, int32_t which, void* P, void* stream) {
-  if (!h) return fail(BO_ERR_INVALID_ARG, "null handle");
-  if (n < 0 || (which != 0 && which != 1)) return fail(BO_ERR_INVALID_ARG, "n=%lld which=%d", (long long)n, which);
-  if (n == 0) return BO_OK;
-  if (!W || !P || W == P) return fail(BO_ERR_INVALID_ARG, "null or aliased weight pointers");
-  if (!aligned16(W) || !aligned16(P)) return fail(BO_ERR_SHAPE, "weight pointers must be 16-byte aligned");
-  const bo_config& c = h->cfg;
-  const int rows = which == 0 ? c.ffn : c.hidden, K = which == 0 ? c.hidden : c.ffn;
-  if (rows % bo::kPackRows || K % 64)
-    return fail(BO_ERR_SHAPE, "packing needs rows=%d to be a multiple of %d", rows, bo::kPackRows);
-  BO_CUDA(bo::launch_pack(c.dtype == BO_BF16 ? 0 : 1, W, n, rows, K, P, h->num_sms, static_cast<cudaStream_t>(stream)),
-          "pack");
   return BO_OK;
 }
 
@@ -1435,8 +1219,6 @@ bo_status bo_expert_ffn(bo_handle* h, const void* rows, int64_t R, const float* 
                         void* h_buf, void* out, void* stream) {
   if (!h) return fail(BO_ERR_INVALID_ARG, "null handle");
   h->last_kernels.clear();
-  if (h->cfg.weight_layout != BO_WEIGHTS_ROWMAJOR)
-    return fail(BO_ERR_UNSUPPORTED, "bo_expert_ffn takes ROWMAJOR weights (f-sliced united experts)");
   if (R == 0) return BO_OK;
   const bo_config& c = h->cfg;
   if (n_orig < 0 || n_united < 0 || n_orig + n_united > bo::kMaxExec)

@@ -9,13 +9,15 @@
 // (exec_off / mtile_off), so no host synchronisation is needed.
 //
 // CTA layout (192 threads, 1 CTA per SM, persistent over a static round-robin
-// work list):
+// work list; split-K for decode-sized GEMM2 steps):
 //   warp 0      TMA producer: A tile [128 x BK] + B tile [BN x BK] per stage
 //   warp 1      MMA issuer: tcgen05.mma.cta_group::1 M=128 N=BN K=16(bf16)/8(tf32)
 //               into a double-buffered TMEM accumulator (2 x BN fp32 columns)
 //   warps 2-5   epilogue: tcgen05.ld 32x32b -> registers -> fused op -> global
 // Work item w -> (executor x, n-tile, m-tile) with the m-tile fastest, so
 // concurrently running CTAs share the same weight tile (B) through L2.
+#include <atomic>
+
 #include "bo_kernels.h"
 #include "bo_ptx.cuh"
 
@@ -38,7 +40,7 @@ struct GemmCfg {
   static constexpr int A_BYTES = BM * 128;
   static constexpr int B_BYTES = (BN / CG) * 128;       // each CTA of a pair holds half of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int BAR_BYTES = 2048;                 // barriers + tmem slot (1 KB) + router histogram (1 KB)
+  static constexpr int BAR_BYTES = 1024;                 // mbarriers + TMEM slot
   static constexpr int SCHED_BYTES = ((2 * (kMaxExec + 1) * 4) + 127) / 128 * 128;   // keeps the staging 16B-aligned
   static constexpr int EPI_ROW = 32 * (int)sizeof(T) + 16;   // staged 32-column row chunk + bank pad
   static constexpr int EPI_BYTES = 4 * 32 * EPI_ROW          // one staging tile per epilogue warp
@@ -162,15 +164,6 @@ __device__ __forceinline__ void topk_insert(float (&tv)[KMAX], int (&ti)[KMAX], 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 // two epilogue warps (swapped tail tiles: the gate warp and the up warp of the same columns)
 __device__ __forceinline__ void pair_bar(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
-
-__device__ __forceinline__ void st_release_gpu(int* ptr, int v) {
-  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(ptr), "r"(v) : "memory");
-}
-__device__ __forceinline__ int ld_acquire_gpu(const int* ptr) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
-  return v;
-}
 
 // 16-byte vector <-> fp32 (8 bf16 or 4 fp32 elements); loads bypass L1 (rows
 // written by other CTAs of the same kernel).
@@ -313,7 +306,7 @@ __device__ __forceinline__ void combine_token_cols(const GemmParams& p, const T*
   }
 }
 
-template <typename T, int BN, int EPI, int KMAX, int CG, bool GATHER>
+template <typename T, int BN, int EPI, int KMAX, int CG>
 __global__ void __launch_bounds__(192, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ BMaps tmB, const GemmParams p) {
   // CG = 1: one CTA computes a 128 x BN tile with tcgen05.mma.cta_group::1.
@@ -322,10 +315,6 @@ __global__ void __launch_bounds__(192, 1)
   //         128 rows of A and half of B (BN/2 rows), halving the shared-memory
   //         and L2 traffic per MMA; each CTA's TMEM holds its 128 rows.
   static_assert(CG == 1 || (CG == 2 && EPI != EPI_ROUTER && sizeof(T) == 2), "pair mode: bf16 FFN GEMMs");
-  // GATHER: the A rows are not read from a packed Xp but gathered from the token
-  // matrix x by TMA tile::gather4 (4 rows per instruction, row index = row_tok),
-  // i.e. concat_tokens fused into GEMM1's operand load.
-  static_assert(!GATHER || EPI == EPI_SWIGLU, "gather feeds GEMM1 only");
   using C = GemmCfg<T, BN, CG>;
   constexpr int STAGES = C::STAGES;
   constexpr int TMEM_COLS = GemmShape<BN, EPI>::kTmemCols;
@@ -341,12 +330,12 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* empty_bar = full_bar + STAGES;
   uint64_t* tfull_bar = empty_bar + STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint64_t* fix_bar = tempty_bar + 2;   // split-tile fix-up: contributor partial landed in shared memory
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 3);
-  int* s_hist = reinterpret_cast<int*>(smem + STAGES * C::STAGE_BYTES + 1024);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   int* s_mtile = reinterpret_cast<int*>(smem + STAGES * C::STAGE_BYTES + C::BAR_BYTES);
   int* s_eoff = s_mtile + (kMaxExec + 1);
   uint8_t* s_epi = smem + STAGES * C::STAGE_BYTES + C::BAR_BYTES + C::SCHED_BYTES;
+  // per-warp 4 KB region (1 KB aligned): TMA-store boxes (GEMM2), swizzled logits staging (router)
+  uint8_t* s_box = smem + ((STAGES * C::STAGE_BYTES + C::BAR_BYTES + C::SCHED_BYTES + 4 * 32 * C::EPI_ROW + 1023) & ~1023);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -364,7 +353,6 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], 4 * CG);   // pair: epilogue warps of both CTAs arrive on the leader's
     }
-    mbar_init(fix_bar, 1);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -439,28 +427,14 @@ __global__ void __launch_bounds__(192, 1)
   // few m-tiles, and the last partial wave of BN-wide tiles can idle most SMs.
   int bh = BN / 2;
   bool alt = false;
-  if constexpr (EPI == EPI_SWIGLU && !GATHER) {
+  if constexpr (EPI == EPI_SWIGLU) {
     if (p.bh_alt > 0) {
       const int items_p = start_of(nexec);
       nt_o = p.nt_alt;
       nt_u = p.nt_alt_u;
       const int items_a = start_of(nexec);
-      // waves x width; stream-K spreads the k-blocks evenly (no wave rounding), the
-      // lockstep tail split shortens the last partial wave by its split count
-      auto wave_cost = [&](int items) -> long long {
-        if (p.stream_k == 1) return 8LL * items;
-        const int full = items / n_units, r = items - full * n_units;
-        if (r == 0) return 8LL * full;
-        if (p.stream_k != 2) return 8LL * (full + 1);
-        int k = n_units / r;
-        k = k > 4 ? 4 : k;
-        const int kbm = p.Kdim / C::BK;
-        k = k > kbm ? kbm : k;
-        return 8LL * full + 8 / (k < 1 ? 1 : k);
-      };
-      const long long cost_p = wave_cost(items_p) * (BN + 32);
-      const long long cost_a = wave_cost(items_a) * (2 * p.bh_alt + 32);
-      alt = cost_a < cost_p;
+      auto waves = [&](int items) -> long long { return (items + n_units - 1) / n_units; };
+      alt = waves(items_a) * (2 * p.bh_alt + 32) < waves(items_p) * (BN + 32);
       if (alt) {
         bh = p.bh_alt;
       } else {
@@ -477,19 +451,13 @@ __global__ void __launch_bounds__(192, 1)
   // them).  The MMA and the shared-memory traffic then scale with rin instead of a
   // full 256-row tile.  Three TMA boxes per k-block (gate, up, rows): the TMA issue
   // cost of 16-row boxes (8-12 per k-block) made such a tile slower than a full one.
-  // GEMM2 (EPI_WEIGHTED) likewise: this CTA's 128 Wd rows (output columns) on M, the
-  // tile's H rows on N; the epilogue writes Yp column-sliced and counts columns for
-  // the fused combine.
-  constexpr bool kSwap = CG == 2 && (EPI == EPI_SWIGLU || EPI == EPI_WEIGHTED) && !GATHER;
-  const bool swap_ok = kSwap && p.swap_tail && !alt && !p.a_shared && !p.b_packed &&
-                       (EPI != EPI_WEIGHTED || (p.ksplit_max <= 1 && !p.f32_mode));
-  // largest tail swapped: a tail near 256 rows gains no MMA work and loses pipelining
-  // (swap_max >= TILE_M swaps full tiles too: an experiment knob)
-  const int swap_lim = p.swap_max > 0 ? (p.swap_max < TILE_M ? p.swap_max : TILE_M) : TILE_M - 1;
+  constexpr bool kSwap = CG == 2 && EPI == EPI_SWIGLU;
+  const bool swap_ok = kSwap && p.swap_tail && !alt && !p.a_shared;
   auto tile_rows = [&](int x, int mi) {   // rows of executor x in m-tile mi
     const int r = s_eoff[x + 1] - s_eoff[x] - mi * TILE_M;
     return r < TILE_M ? r : TILE_M;
   };
+  auto swapped_tile = [&](int x, int mi) { return swap_ok && tile_rows(x, mi) < TILE_M; };
   const int stage_tx = C::A_BYTES + (EPI == EPI_SWIGLU ? 2 * bh : BN) * 128 / CG;   // bytes per CTA per stage
   const int base_work = start_of(nexec);
   auto kblocks = [&](int x) { return (x < mo || x >= mu ? p.Kdim : p.Kdim_u) / C::BK; };
@@ -513,153 +481,50 @@ __global__ void __launch_bounds__(192, 1)
   }
   const int total_work = base_work * ks;
 
-  // work item -> (executor, m-tile inside executor, n-tile); m-tile fastest
-  auto decode = [&](int w, int& x, int& mi, int& n) {
+  // work item -> tile (executor x, m-tile mi fastest, n-tile n) + k-block range
+  // [kb0, kb1) of split sp; units take items unit, unit + n_units, ... (the
+  // concurrently running CTAs share each weight tile through L2)
+  auto decode = [&](int w, int& x, int& mi, int& n, int& sp, int& kb0, int& kb1) {
+    const int tw = w / ks;
+    sp = w - tw * ks;
     int lo = 0, hi = nexec;
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
-      if (start_of(mid) <= w) lo = mid; else hi = mid;
+      if (start_of(mid) <= tw) lo = mid; else hi = mid;
     }
     x = lo;
     const int mt = s_mtile[x + 1] - s_mtile[x];
-    const int local = w - start_of(x);
+    const int local = tw - start_of(x);
     n = local / mt;
     mi = local - n * mt;
-  };
-  // work item -> tile + k-block range [kb0, kb1) of split sp
-  auto decode_k = [&](int w, int& x, int& mi, int& n, int& sp, int& kb0, int& kb1) {
-    const int tw = w / ks;
-    sp = w - tw * ks;
-    decode(tw, x, mi, n);
     const int nkb = kblocks(x);
     const int per = (nkb + ks - 1) / ks;
     kb0 = sp * per < nkb ? sp * per : nkb;
     kb1 = kb0 + per < nkb ? kb0 + per : nkb;
   };
-  // Segments this CTA (unit) processes, in order.  Classic: work items
-  // unit, unit + n_units, ... (whole tiles or split-K ranges).  Stream-K
-  // (decode-sized steps, CG = 1, uniform reduction length), the "data-parallel +
-  // two-tile stream-K" hybrid: all but the last two waves of tiles run whole
-  // (tile w on unit w % n_units, so concurrently running CTAs still share weight
-  // and activation tiles in L2); the remaining (<= 2 waves of) tiles are cut into
-  // n_units equal contiguous ranges of their (tile, k-block) space, so every SM
-  // streams the same number of k-blocks.  A tile cut between CTAs is finished by
-  // the CTA holding its k-block 0 (the owner), which adds the fp32 partials the
-  // later CTAs left in sk_part (slot = their unit).
-  const bool stream = CG == 1 && p.stream_k == 1 && EPI != EPI_ROUTER;
-  const int kb_u = kblocks(0);
-  // Lockstep tail split-K (p.stream_k == 2): the complete waves of tiles run whole
-  // (tile w on unit w % n_units); the r tiles of the last, partial wave have their
-  // reduction cut into ks_l equal k-ranges run side by side on units
-  // tile * ks_l + sp (every split of every tail tile concurrently, so CTAs reading
-  // the same weight / activation tile do it together); split 0 owns the tile and
-  // adds the other splits' fp32 partials (slot = their unit: a CTA contributes at
-  // most once, in the tail).
-  const int full_tiles = (base_work / n_units) * n_units;
-  const int tail = base_work - full_tiles;
-  int ks_l = 1;
-  if (CG == 1 && p.stream_k == 2 && ks == 1 && tail > 0)
-    for (int k = 2; k <= 4 && k <= kb_u && tail * k <= n_units; ++k) ks_l = k;
-  const bool lock = ks_l > 1;
-  const long long dpl = lock ? full_tiles / n_units : 0;   // whole tiles per unit before the tail
-  const int waves = (base_work + n_units - 1) / n_units;
-  const int dp_tiles = stream ? (waves > 2 ? (waves - 2) * n_units : 0) : 0;
-  const long long dp_cnt = stream ? (dp_tiles > unit ? (dp_tiles - unit + n_units - 1) / n_units : 0) : 0;
-  const long long tu = stream ? static_cast<long long>(base_work - dp_tiles) * kb_u : 0;   // stream-K units
-  const long long su_lo = stream ? tu * unit / n_units : 0;
-  const long long su_hi = stream ? tu * (unit + 1) / n_units : 0;
-  long long sk_pos = 0;   // stream-K position of the current segment (set by seg_at)
-  auto seg_at = [&](long long cur, int& x, int& mi, int& n, int& sp, int& kb0, int& kb1) -> bool {
-    if (lock) {
-      if (cur < dpl) {   // whole tile of a complete wave
-        decode(static_cast<int>(unit + cur * n_units), x, mi, n);
-        sp = 0;
-        kb0 = 0;
-        kb1 = kb_u;
-        return true;
-      }
-      if (cur != dpl || unit >= tail * ks_l) return false;
-      decode(full_tiles + unit / ks_l, x, mi, n);
-      sp = unit % ks_l;
-      kb0 = sp * kb_u / ks_l;
-      kb1 = (sp + 1) * kb_u / ks_l;
-      return true;
-    }
-    if (!stream) {
-      if (cur >= total_work) return false;
-      decode_k(static_cast<int>(cur), x, mi, n, sp, kb0, kb1);
-      return true;
-    }
-    sp = 0;
-    if (cur < dp_cnt) {   // whole tile of the data-parallel waves
-      decode(static_cast<int>(unit + cur * n_units), x, mi, n);
-      kb0 = 0;
-      kb1 = kb_u;
-      return true;
-    }
-    sk_pos = su_lo + (cur - dp_cnt);
-    if (sk_pos >= su_hi) return false;
-    const long long tile = sk_pos / kb_u;
-    kb0 = static_cast<int>(sk_pos - tile * kb_u);
-    const long long end = su_hi < (tile + 1) * kb_u ? su_hi : (tile + 1) * kb_u;
-    kb1 = static_cast<int>(end - tile * kb_u);
-    decode(dp_tiles + static_cast<int>(tile), x, mi, n);
-    return true;
-  };
-  auto seg_next = [&](long long cur, int kb0, int kb1) -> long long {
-    return lock ? cur + 1 : (stream ? (cur < dp_cnt ? cur + 1 : cur + (kb1 - kb0)) : cur + n_units);
-  };
-  const long long seg0 = (stream || lock) ? 0 : unit;
-  // stream-K: the unit whose range holds stream-K position u, and whether unit c
-  // holds any position (empty ranges when the stream-K tiles * k-blocks < grid)
-  auto unit_of = [&](long long u) -> int { return static_cast<int>(((u + 1) * n_units - 1) / tu); };
-  auto unit_busy = [&](int c) -> bool { return lock || tu * c / n_units != tu * (c + 1) / n_units; };
-
-  // L2 prefetch of k-block kq of the B tile(s) the producer will load (CTA-pair
-  // mode: this CTA's half)
-  auto prefetch_b = [&](const CUtensorMap* mb0, const CUtensorMap* mb1, int kq, int brow, int n) {
-    if constexpr (EPI == EPI_SWIGLU) {
-      if constexpr (CG == 1) {
-        tma_prefetch_l2_2d(mb0, kq * C::BK, brow + n * bh);
-        tma_prefetch_l2_2d(mb1, kq * C::BK, brow + n * bh);
-      } else {
-        tma_prefetch_l2_2d(crank == 0 ? mb0 : mb1, kq * C::BK, brow + n * bh);
-      }
-    } else {
-      tma_prefetch_l2_2d(mb0, kq * C::BK, brow + n * BN + (CG == 2 ? static_cast<int>(crank) * (BN / 2) : 0));
-    }
-  };
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
-    if (GATHER || lane == 0) {
-      // activations are re-read per n-tile: evict_last (a_policy 0), or normal / first (1 / 2)
-      const uint64_t pol_a =
-          p.a_policy == 1 ? policy_evict_normal() : (p.a_policy == 2 ? policy_evict_first() : policy_evict_last());
-      // weight tile is re-read by the executor's other m-tiles (running alongside);
-      // b_policy 1: evict_first (streamed weights make way for the re-read activations)
+    if (lane == 0) {
+      // activations are re-read per n-tile (evict_last); the weight tile is re-read by the
+      // executor's other m-tiles running alongside (b_policy 1: evict_first for decode-sized
+      // steps, where the streamed weights should make way for the re-read activations)
+      const uint64_t pol_a = policy_evict_last();
       const uint64_t pol_b = p.b_policy == 1 ? policy_evict_first() : policy_evict_normal();
       int stage = 0;
       uint32_t phase = 0;
       int x, mi, n, sp, kb0, kb1;
-      for (long long cur = seg0; seg_at(cur, x, mi, n, sp, kb0, kb1); cur = seg_next(cur, kb0, kb1)) {
+      for (int w = unit; w < total_work; w += n_units) {
+        decode(w, x, mi, n, sp, kb0, kb1);
         const int arow = (p.a_shared ? 0 : s_eoff[x]) + mi * TILE_M + static_cast<int>(crank) * kBM;
         const int cls = x < mo ? 0 : (x < mu ? 1 : 2);      // original / united / shared
         const CUtensorMap* mb0 = &tmB.m[(alt ? 6 : 0) + 2 * cls];
         const CUtensorMap* mb1 = &tmB.m[(alt ? 6 : 0) + 2 * cls + 1];
         const int brow = cls == 0 ? x * p.b_rows_per_exec
                                   : (cls == 1 ? (x - mo) * p.b_rows_u : (x - mu) * p.b_rows_per_exec);
-        int4 tok = make_int4(0, 0, 0, 0);
-        if constexpr (GATHER) {   // this lane gathers rows arow + 4*lane .. +3 (their tokens)
-          const int r = arow + 4 * lane;
-          tok.x = r + 0 < p.rows_total ? __ldg(p.row_tok + r + 0) : 0;
-          tok.y = r + 1 < p.rows_total ? __ldg(p.row_tok + r + 1) : 0;
-          tok.z = r + 2 < p.rows_total ? __ldg(p.row_tok + r + 2) : 0;
-          tok.w = r + 3 < p.rows_total ? __ldg(p.row_tok + r + 3) : 0;
-        }
         if constexpr (kSwap) {
-          const int rin = tile_rows(x, mi);
-          if (swap_ok && rin <= swap_lim) {
+          if (swapped_tile(x, mi)) {
+            const int rin = tile_rows(x, mi);
             const int nsh = ((rin + 31) & ~31) / 2;   // token rows staged by this CTA (N / 2)
             const int wrow = brow + n * 128 + static_cast<int>(crank) * 64;
             const int trow = s_eoff[x] + mi * TILE_M + static_cast<int>(crank) * nsh;
@@ -669,79 +534,41 @@ __global__ void __launch_bounds__(192, 1)
             for (int kb = kb0; kb < kb1; ++kb) {
               mbar_wait(&empty_bar[stage], phase ^ 1);
               uint8_t* sa = smem + stage * C::STAGE_BYTES;
-              if (lane == 0) {
-                if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * (C::A_BYTES + tbox * 128));
-                else mbar_arrive_remote(&full_bar[stage], 0);
-                if constexpr (EPI == EPI_SWIGLU) {
-                  tma_load_2d_pair(sa, &tmB.m[6 + 2 * cls], &full_bar[stage], kb * C::BK, wrow, pol_b);
-                  tma_load_2d_pair(sa + 64 * 128, &tmB.m[7 + 2 * cls], &full_bar[stage], kb * C::BK, wrow, pol_b);
-                } else {   // Wd rows n * BN + crank * 128 .. + 127 (the pair's usual B half box)
-                  tma_load_2d_pair(sa, &tmB.m[2 * cls], &full_bar[stage], kb * C::BK,
-                                   brow + n * BN + static_cast<int>(crank) * 128, pol_b);
-                }
-                tma_load_2d_pair(sa + C::A_BYTES, mt, &full_bar[stage], kb * C::BK, trow, pol_a);
-              }
+              if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * (C::A_BYTES + tbox * 128));
+              else mbar_arrive_remote(&full_bar[stage], 0);
+              tma_load_2d_pair(sa, &tmB.m[6 + 2 * cls], &full_bar[stage], kb * C::BK, wrow, pol_b);
+              tma_load_2d_pair(sa + 64 * 128, &tmB.m[7 + 2 * cls], &full_bar[stage], kb * C::BK, wrow, pol_b);
+              tma_load_2d_pair(sa + C::A_BYTES, mt, &full_bar[stage], kb * C::BK, trow, pol_a);
               if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
             continue;
           }
         }
-        // L2 prefetch of the first pf_dist k-blocks' B tiles of this segment (weight
-        // streaming: more DRAM requests in flight than the stage ring holds)
-        if (p.pf_dist > 0 && !p.b_packed && lane == 0) {
-          const int kpf = kb0 + p.pf_dist < kb1 ? kb0 + p.pf_dist : kb1;
-          for (int kq = kb0; kq < kpf; ++kq) prefetch_b(mb0, mb1, kq, brow, n);
-        }
         for (int kb = kb0; kb < kb1; ++kb) {
-          if (p.pf_dist > 0 && !p.b_packed && lane == 0 && kb + p.pf_dist < kb1)
-            prefetch_b(mb0, mb1, kb + p.pf_dist, brow, n);
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           uint8_t* sb = sa + C::A_BYTES;
-          if (lane == 0) {
-            // B rows [grow, grow + nr) of k-block kb: one 2-D box, or (tile-packed weights)
-            // one 3-D box per 128-row band, each a contiguous block in memory
-            const int kbs = kblocks(x);
-            auto load_b = [&](uint8_t* dst, const CUtensorMap* mb, int grow, int nr) {
-              if (!p.b_packed) {
-                if constexpr (CG == 1) tma_load_2d(dst, mb, &full_bar[stage], kb * C::BK, grow, pol_b);
-                else tma_load_2d_pair(dst, mb, &full_bar[stage], kb * C::BK, grow, pol_b);
-                return;
-              }
-              for (int r0 = 0; r0 < nr; r0 += kPackRows) {
-                const int gr = grow + r0;
-                const int c2 = (gr / kPackRows) * kbs + kb;
-                if constexpr (CG == 1)
-                  tma_load_3d(dst + r0 * 128, mb, &full_bar[stage], 0, gr % kPackRows, c2, pol_b);
-                else
-                  tma_load_3d_pair(dst + r0 * 128, mb, &full_bar[stage], 0, gr % kPackRows, c2, pol_b);
-              }
-            };
-            if constexpr (CG == 1) {
-              mbar_arrive_expect_tx(&full_bar[stage], stage_tx);
-              if constexpr (!GATHER) tma_load_2d(sa, &tmA, &full_bar[stage], kb * C::BK, arow, pol_a);
-              if constexpr (EPI == EPI_SWIGLU) {
-                load_b(sb, mb0, brow + n * bh, bh);
-                load_b(sb + bh * 128, mb1, brow + n * bh, bh);
-              } else {
-                load_b(sb, mb0, brow + n * BN, BN);
-              }
+          if constexpr (CG == 1) {
+            mbar_arrive_expect_tx(&full_bar[stage], stage_tx);
+            tma_load_2d(sa, &tmA, &full_bar[stage], kb * C::BK, arow, pol_a);
+            if constexpr (EPI == EPI_SWIGLU) {
+              tma_load_2d(sb, mb0, &full_bar[stage], kb * C::BK, brow + n * bh, pol_b);
+              tma_load_2d(sb + bh * 128, mb1, &full_bar[stage], kb * C::BK, brow + n * bh, pol_b);
             } else {
-              // Both CTAs load their halves; completion is counted on the leader's barrier.
-              if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * stage_tx);
-              else mbar_arrive_remote(&full_bar[stage], 0);
-              if constexpr (!GATHER) tma_load_2d_pair(sa, &tmA, &full_bar[stage], kb * C::BK, arow, pol_a);
-              if constexpr (EPI == EPI_SWIGLU) {
-                // leader: gate rows, peer: up rows of the same f-columns -> D[:, 0:BN/2] = gate, D[:, BN/2:] = up
-                load_b(sb, leader ? mb0 : mb1, brow + n * bh, bh);
-              } else {
-                load_b(sb, mb0, brow + n * BN + static_cast<int>(crank) * (BN / 2), BN / 2);
-              }
+              tma_load_2d(sb, mb0, &full_bar[stage], kb * C::BK, brow + n * BN, pol_b);
             }
-          }
-          if constexpr (GATHER) {
-            if constexpr (CG == 1) tma_gather4(sa + lane * 512, &tmA, &full_bar[stage], kb * C::BK, tok, pol_a);
-            else tma_gather4_pair(sa + lane * 512, &tmA, &full_bar[stage], kb * C::BK, tok, pol_a);
+          } else {
+            // Both CTAs load their halves; completion is counted on the leader's barrier.
+            if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * stage_tx);
+            else mbar_arrive_remote(&full_bar[stage], 0);
+            tma_load_2d_pair(sa, &tmA, &full_bar[stage], kb * C::BK, arow, pol_a);
+            if constexpr (EPI == EPI_SWIGLU) {
+              // leader: gate rows, peer: up rows of the same f-columns -> D[:, 0:BN/2] = gate, D[:, BN/2:] = up
+              tma_load_2d_pair(sb, leader ? mb0 : mb1, &full_bar[stage], kb * C::BK, brow + n * bh, pol_b);
+            } else {
+              tma_load_2d_pair(sb, mb0, &full_bar[stage], kb * C::BK,
+                               brow + n * BN + static_cast<int>(crank) * (BN / 2), pol_b);
+            }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -755,14 +582,14 @@ __global__ void __launch_bounds__(192, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       int x, mi, n, sp, kb0, kb1;
-      for (long long cur = seg0; seg_at(cur, x, mi, n, sp, kb0, kb1); cur = seg_next(cur, kb0, kb1)) {
+      for (int w = unit; w < total_work; w += n_units) {
+        decode(w, x, mi, n, sp, kb0, kb1);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
         uint32_t idesc_t = idesc;
         if constexpr (kSwap) {
-          const int rin = tile_rows(x, mi);
-          if (swap_ok && rin <= swap_lim) idesc_t = idesc_f32acc<T>(256, (rin + 31) & ~31);
+          if (swapped_tile(x, mi)) idesc_t = idesc_f32acc<T>(256, (tile_rows(x, mi) + 31) & ~31);
         }
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
@@ -817,11 +644,13 @@ __global__ void __launch_bounds__(192, 1)
     }
     const int q = warp & 3;   // TMEM lane quarter this warp may access
     const uint64_t pol_out = p.store_hint ? policy_evict_first() : policy_evict_normal();
+    uint8_t* stage = s_epi + (warp - 2) * 32 * C::EPI_ROW;
+    uint8_t* box = s_box + (warp - 2) * 4096;   // 1 KB aligned (smem is): swizzles follow address bits 4-9
     int acc = 0;
     uint32_t acc_phase = 0;
     int x, mi, n, sp, kb0, kb1;
-    uint32_t fix_phase = 0;
-    for (long long cur = seg0; seg_at(cur, x, mi, n, sp, kb0, kb1); cur = seg_next(cur, kb0, kb1)) {
+    for (int w = unit; w < total_work; w += n_units) {
+      decode(w, x, mi, n, sp, kb0, kb1);
       const int rows_x = s_eoff[x + 1] - s_eoff[x];
       const int r_local = mi * TILE_M + static_cast<int>(crank) * kBM + q * 32 + lane;
       const bool valid = r_local < rows_x;
@@ -829,125 +658,19 @@ __global__ void __launch_bounds__(192, 1)
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t t0 = tmem_base + static_cast<uint32_t>(acc * BN) + (static_cast<uint32_t>(q * 32) << 16);
-      if ((stream || lock) && kb0 > 0) {
-        // stream-K contributor: this tile's k-blocks [kb0, kb1) as an fp32 partial in
-        // slot `unit` (TMEM column order), then publish it (every thread fences its
-        // stores, the epilogue barrier, one release store of the flag)
-        // layout [column quad][128 rows] of float4: a warp's stores are 512 contiguous
-        // bytes, and the owner's fix-up reads it back from shared memory conflict-free
-        float4* dst = reinterpret_cast<float4*>(p.sk_part + static_cast<int64_t>(unit) * kBM * kSkCols) +
-                      (q * 32 + lane);
-#pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t a[32];
-          tmem_ld32(t0 + c, a);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            __stcg(dst + (c / 4 + j) * kBM,
-                   make_float4(__uint_as_float(a[4 * j]), __uint_as_float(a[4 * j + 1]),
-                               __uint_as_float(a[4 * j + 2]), __uint_as_float(a[4 * j + 3])));
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty_bar[acc]);
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-        __threadfence();
-        epi_bar();
-        if (threadIdx.x == 64) st_release_gpu(p.sk_flag + unit, 1);
-        continue;
-      }
-      // Owner of a tile cut between CTAs (stream-K / lockstep split): this is the CTA's
-      // last segment, so its MMAs are done and the stage ring is free.  For each
-      // contributing unit in order: wait for its flag, bulk-copy its partial tile into
-      // the ring (one TMA transfer), TMEM accumulator += partial, then the epilogue
-      // below reads the finished sum.
-      if ((stream || lock) && kb1 < kb_u) {   // (only stream-K segments are cut: sk_pos is this segment's)
-        const int c_first = unit + 1;
-        const int c_last = lock ? unit + ks_l - 1 : unit_of((sk_pos / kb_u + 1) * kb_u - 1);
-        const uint32_t bytes = static_cast<uint32_t>(kBM) * BN * 4;
-        const float4* fbuf = reinterpret_cast<const float4*>(smem) + (q * 32 + lane);
-        for (int cc = c_first; cc <= c_last; ++cc) {
-          if (!unit_busy(cc)) continue;
-          if (threadIdx.x == 64) {
-            while (ld_acquire_gpu(p.sk_flag + cc) == 0) {
-            }
-            p.sk_flag[cc] = 0;   // consumed (the next launch starts from zero)
-            fence_proxy_async_global();   // generic-proxy partial -> async-proxy bulk read
-            fence_proxy_async_smem();     // earlier generic reads of the ring -> async-proxy write
-            mbar_arrive_expect_tx(fix_bar, bytes);
-            bulk_g2s(smem, p.sk_part + static_cast<int64_t>(cc) * kBM * kSkCols, bytes, fix_bar);
-          }
-          mbar_wait(fix_bar, fix_phase);
-          fix_phase ^= 1;
-#pragma unroll 1
-          for (int c = 0; c < BN; c += 32) {
-            uint32_t a[32];
-            tmem_ld32(t0 + c, a);
-            tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float4 f = fbuf[(c / 4 + j) * kBM];
-              a[4 * j] = __float_as_uint(__uint_as_float(a[4 * j]) + f.x);
-              a[4 * j + 1] = __float_as_uint(__uint_as_float(a[4 * j + 1]) + f.y);
-              a[4 * j + 2] = __float_as_uint(__uint_as_float(a[4 * j + 2]) + f.z);
-              a[4 * j + 3] = __float_as_uint(__uint_as_float(a[4 * j + 3]) + f.w);
-            }
-            tmem_st32(t0 + c, a);
-          }
-          tmem_st_wait();
-          epi_bar();   // the ring is read by every epilogue thread before the next copy lands
-        }
-      }
       // rows of this warp's 32-row slab that belong to the executor
       const int slab = mi * TILE_M + static_cast<int>(crank) * kBM + q * 32;
       const int nrows = rows_x - slab < 0 ? 0 : (rows_x - slab > 32 ? 32 : rows_x - slab);
       const int64_t row0 = static_cast<int64_t>(s_eoff[x]) + slab;
-      uint8_t* stage = s_epi + (warp - 2) * 32 * C::EPI_ROW;
       bool swapped = false;
-      // swapped GEMM2 tail tile: Yp stores here, the shared release / count / combine below
-      int sw_rin = 0;
-      if constexpr (kSwap && EPI == EPI_WEIGHTED) {
-        const int rin = tile_rows(x, mi);
-        if (swap_ok && rin <= swap_lim) {
-          // D^T tile: lane = output column col0 + lane, TMEM column = the tile's row:
-          // Yp[row, cols] = row_w[row] * acc, staged [32 rows][32 columns] per warp.
-          sw_rin = rin;
-          const int ns = (rin + 31) & ~31;
-          T* out = reinterpret_cast<T*>(p.out) + n * BN + static_cast<int>(crank) * 128 + q * 32;
-          const int64_t tok0 = static_cast<int64_t>(s_eoff[x]) + mi * TILE_M;
-#pragma unroll 1
-          for (int c = 0; c < ns; c += 32) {
-            uint32_t v[32];
-            tmem_ld32(t0 + c, v);
-            tmem_ld_wait();
-            const float wl = c + lane < rin ? (p.row_w ? p.row_w[tok0 + c + lane] : p.alpha) : 0.0f;
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              *reinterpret_cast<T*>(stage + j * C::EPI_ROW + lane * (int)sizeof(T)) =
-                  static_cast<T>(__uint_as_float(v[j]) * __shfl_sync(0xffffffffu, wl, j));
-            __syncwarp();
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int pc = i * 32 + lane, tk = pc >> 2, part = pc & 3;
-              if (c + tk < rin) {
-                const uint4 val = *reinterpret_cast<const uint4*>(stage + tk * C::EPI_ROW + part * 16);
-                T* dst = out + (tok0 + c + tk) * p.ldo + part * (16 / (int)sizeof(T));
-                st_global_hint(dst, val, pol_out);
-              }
-            }
-            __syncwarp();
-          }
-        }
-      }
-      if constexpr (kSwap && EPI == EPI_SWIGLU) {
-        const int rin = tile_rows(x, mi);
-        if (swap_ok && rin <= swap_lim) {
+      if constexpr (kSwap) {
+        if (swapped_tile(x, mi)) {
           // D^T tile: lane = weight row, TMEM column = the tile's row.  Warp q < 2 holds
           // the gate rows of columns colb..colb+31, warp q + 2 their up rows: the up warp
           // hands its values over through its staging tile, 16 rows at a time; the gate
           // warp computes H, stages [32 rows][32 columns] and writes it back.
           swapped = true;
+          const int rin = tile_rows(x, mi);
           const int ns = (rin + 31) & ~31;
           const bool up_w = q >= 2;
           const int bid = 2 + (q & 1);
@@ -1048,12 +771,9 @@ __global__ void __launch_bounds__(192, 1)
         // thread = row writes its 64 bytes into a dense 32 x 32 box (64B swizzle: 16-byte
         // chunk q of row r at q ^ ((r >> 1) & 3), conflict-free), one elected lane stores
         // the box; two boxes per warp alternate.
-        const bool tma_out = sizeof(T) == 2 && p.tma_store && nrows == 32 && !p.comb_cnt && !sw_rin;
-        uint8_t* tbox0 = smem +
-                         ((STAGES * C::STAGE_BYTES + C::BAR_BYTES + C::SCHED_BYTES + 4 * 32 * C::EPI_ROW + 1023) & ~1023) +
-                         (warp - 2) * 4096;   // 1 KB aligned (smem is): the swizzle follows address bits 7-8
+        const bool tma_out = sizeof(T) == 2 && p.tma_store && nrows == 32 && !p.comb_cnt;
 #pragma unroll 1
-        for (int c = 0; c < (sw_rin ? 0 : BN); c += 32) {
+        for (int c = 0; c < BN; c += 32) {
           uint32_t a[32];
           tmem_ld32(t0 + c, a);
           tmem_ld_wait();
@@ -1061,7 +781,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(a[i]) * wr;
           if (tma_out) {
-            uint8_t* tb = tbox0 + ((c >> 5) & 1) * 2048;
+            uint8_t* tb = box + ((c >> 5) & 1) * 2048;
             if (lane == 0) bulk_wait_read<1>();   // this box's store from two chunks ago has read it
             __syncwarp();
 #pragma unroll
@@ -1098,53 +818,43 @@ __global__ void __launch_bounds__(192, 1)
           }
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
           // Release this warp's Yp rows (every lane fences its own stores, then the
-          // warp barrier), count each row against its token; the warp whose arrival
-          // completes a token sums its rows for this n-tile.  Arrivals are counted in
-          // columns: a row is complete when all BN columns of every slot have landed (a
-          // swapped tail tile's CTAs each deliver BN / 2 columns of its rows).
-          // A swapped tile's four warps first meet at the epilogue barrier (each lane's
-          // stores fenced before it), so each row is counted once per CTA with the CTA's
-          // BN / 2 columns; the warps split the row chunks.  (One arrival per warp and
-          // row made 8 atomics per row on the same counter and cost ~30 us per wave.)
+          // warp barrier), count each row's BN columns against its token; the warp
+          // whose arrival completes a token (all BN columns of every slot landed)
+          // sums its rows for this n-tile.
           __threadfence();
-          if (sw_rin) epi_bar();
-          else __syncwarp();
-          const int iters = sw_rin ? (sw_rin + 31) >> 5 : 1;
-          const int add = sw_rin ? BN / 2 : BN;
-          const int64_t tok0 = static_cast<int64_t>(s_eoff[x]) + mi * TILE_M;
-#pragma unroll 1
-          for (int it = sw_rin ? q : 0; it < iters; it += sw_rin ? 4 : 1) {
-            const bool rv = sw_rin ? it * 32 + lane < sw_rin : valid;
-            const int64_t gr = sw_rin ? tok0 + it * 32 + lane : grow;
-            int t = -1;
-            int need = 0;
-            int rr[kCombSlots];
-            if (rv) t = __ldg(p.row_tok + gr);
+          __syncwarp();
+          int t = -1;
+          int need = 0;
+          int rr[kCombSlots];
+          if (valid) t = __ldg(p.row_tok + grow);
 #pragma unroll
-            for (int sl = 0; sl < kCombSlots; ++sl) {
-              rr[sl] = (rv && sl < p.comb_KR) ? __ldg(p.row_of + static_cast<int64_t>(t) * p.comb_KR + sl) : -1;
-              need += rr[sl] >= 0 ? 1 : 0;
-            }
-            const bool last =
-                rv && atomicAdd(p.comb_cnt + static_cast<int64_t>(t) * p.comb_nt + n, add) == need * BN - add;
-            const uint32_t done = __ballot_sync(0xffffffffu, last);
-            if (done) {
-              __threadfence();   // acquire: the other rows' stores precede their counts
-              const T* yb = reinterpret_cast<const T*>(p.out);
-              if (p.comb_KR <= 2) combine_tokens_batched<T, 2, 4>(p, yb, p.ldo, done, t, rr, n * BN, BN, lane);
-              else if (p.comb_KR <= 4) combine_tokens_batched<T, 4, 2>(p, yb, p.ldo, done, t, rr, n * BN, BN, lane);
-              else combine_tokens_batched<T, 8, 2>(p, yb, p.ldo, done, t, rr, n * BN, BN, lane);
-            }
+          for (int sl = 0; sl < kCombSlots; ++sl) {
+            rr[sl] = (valid && sl < p.comb_KR) ? __ldg(p.row_of + static_cast<int64_t>(t) * p.comb_KR + sl) : -1;
+            need += rr[sl] >= 0 ? 1 : 0;
+          }
+          const bool last =
+              valid && atomicAdd(p.comb_cnt + static_cast<int64_t>(t) * p.comb_nt + n, BN) == need * BN - BN;
+          const uint32_t done = __ballot_sync(0xffffffffu, last);
+          if (done) {
+            __threadfence();   // acquire: the other rows' stores precede their counts
+            const T* yb = reinterpret_cast<const T*>(p.out);
+            if (p.comb_KR <= 2) combine_tokens_batched<T, 2, 4>(p, yb, p.ldo, done, t, rr, n * BN, BN, lane);
+            else if (p.comb_KR <= 4) combine_tokens_batched<T, 4, 2>(p, yb, p.ldo, done, t, rr, n * BN, BN, lane);
+            else combine_tokens_batched<T, 8, 2>(p, yb, p.ldo, done, t, rr, n * BN, BN, lane);
           }
           continue;
         }
       } else {
         // Router (Eq. 8) with Eq. 7 fused: this thread owns token `grow`'s m logits.
+        // The logits leave through a swizzled 32 x 32 fp32 staging box per warp
+        // (16-byte chunk c of row r at c ^ (r & 7): conflict-free both ways) as whole
+        // 128-byte row segments, not as 32 scattered 4-byte stores per instruction.
         float tv[KMAX];
         int ti[KMAX];
 #pragma unroll
         for (int j = 0; j < KMAX; ++j) { tv[j] = 0.0f; ti[j] = -1; }
-        float* lrow = reinterpret_cast<float*>(p.out) + grow * p.ldo;
+        float* lbase = reinterpret_cast<float*>(p.out) + row0 * p.ldo;
+        const bool vec_ok = (p.ldo & 3) == 0;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           uint32_t a[32];
@@ -1153,12 +863,31 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const int col = c + i;
-            if (col < p.n_valid) {
-              const float v = __uint_as_float(a[i]);
-              if (valid) lrow[col] = v;
-              topk_insert<KMAX>(tv, ti, p.topk_k, v, col);
+            if (col < p.n_valid) topk_insert<KMAX>(tv, ti, p.topk_k, __uint_as_float(a[i]), col);
+          }
+          const int ncol = p.n_valid - c < 32 ? p.n_valid - c : 32;
+          if (ncol <= 0) continue;
+#pragma unroll
+          for (int c4 = 0; c4 < 8; ++c4)
+            *reinterpret_cast<uint4*>(box + lane * 128 + ((c4 ^ (lane & 7)) << 4)) =
+                make_uint4(a[4 * c4], a[4 * c4 + 1], a[4 * c4 + 2], a[4 * c4 + 3]);
+          __syncwarp();
+          if (vec_ok && ncol == 32) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {   // 4 rows x 8 chunks per instruction
+              const int r = i * 4 + (lane >> 3), c4 = lane & 7;
+              if (r < nrows)
+                *reinterpret_cast<uint4*>(lbase + r * p.ldo + c + 4 * c4) =
+                    *reinterpret_cast<const uint4*>(box + r * 128 + ((c4 ^ (r & 7)) << 4));
+            }
+          } else {
+            for (int i = lane; i < nrows * ncol; i += 32) {   // row-major element order: coalesced
+              const int r = i / ncol, cc = i - r * ncol;
+              lbase[r * p.ldo + c + cc] =
+                  *reinterpret_cast<const float*>(box + r * 128 + (((cc >> 2) ^ (r & 7)) << 4) + (cc & 3) * 4);
             }
           }
+          __syncwarp();
         }
         tc_fence_before();
         __syncwarp();
@@ -1172,26 +901,50 @@ __global__ void __launch_bounds__(192, 1)
           sum += ex[j];
         }
         if (valid) {
+          int32_t* idr = p.topk_id + grow * p.topk_k;
+          float* wr = p.topk_w + grow * p.topk_k;
+          if ((p.topk_k & 3) == 0) {   // 16-byte rows pieces
 #pragma unroll
-          for (int j = 0; j < KMAX; ++j) {
-            if (j < p.topk_k) {
-              p.topk_id[grow * p.topk_k + j] = ti[j];
-              p.topk_w[grow * p.topk_k + j] = __fdividef(ex[j], sum);   // sum >= 1 (see silu_f)
-            }
+            for (int j = 0; j < KMAX; j += 4)
+              if (j < p.topk_k) {
+                *reinterpret_cast<int4*>(idr + j) = make_int4(ti[j], ti[j + 1], ti[j + 2], ti[j + 3]);
+                *reinterpret_cast<float4*>(wr + j) =
+                    make_float4(__fdividef(ex[j], sum), __fdividef(ex[j + 1], sum), __fdividef(ex[j + 2], sum),
+                                __fdividef(ex[j + 3], sum));
+              }
+          } else {
+#pragma unroll
+            for (int j = 0; j < KMAX; ++j)
+              if (j < p.topk_k) {
+                idr[j] = ti[j];
+                wr[j] = __fdividef(ex[j], sum);   // sum >= 1 (see silu_f)
+              }
           }
         }
-        // per-tile expert histogram (tile = this 128-token m-tile)
-        const int et = threadIdx.x - 64;
-        epi_bar();
-        for (int e = et; e < p.n_valid; e += 128) s_hist[e] = 0;
-        epi_bar();
-        if (valid) {
+        // Per-tile expert histogram (Alg. 1 cnt_i input, tile = this 128-token m-tile),
+        // atomics-free: each warp counts its 32 tokens' choices per expert with
+        // __match_any_sync (the lowest lane of each equal-id group adds the group's
+        // size to the warp's own row), then the 4 warp rows are summed in order.
+        int* whist = reinterpret_cast<int*>(stage);   // this warp's row (m <= 256 ints <= its staging tile)
+        for (int e = lane; e < p.n_valid; e += 32) whist[e] = 0;
+        __syncwarp();
 #pragma unroll
-          for (int j = 0; j < KMAX; ++j)
-            if (j < p.topk_k) atomicAdd(&s_hist[ti[j]], 1);
+        for (int j = 0; j < KMAX; ++j) {
+          if (j < p.topk_k) {
+            const int e = valid ? ti[j] : -1;
+            const uint32_t peers = __match_any_sync(0xffffffffu, e);
+            if (e >= 0 && lane == __ffs(peers) - 1) whist[e] += __popc(peers);
+            __syncwarp();
+          }
         }
         epi_bar();
-        for (int e = et; e < p.n_valid; e += 128) p.tile_cnt[static_cast<int64_t>(mi) * p.n_valid + e] = s_hist[e];
+        for (int e = threadIdx.x - 64; e < p.n_valid; e += 128) {
+          int cnt = 0;
+#pragma unroll
+          for (int w4 = 0; w4 < 4; ++w4) cnt += reinterpret_cast<const int*>(s_epi + w4 * 32 * C::EPI_ROW)[e];
+          p.tile_cnt[static_cast<int64_t>(mi) * p.n_valid + e] = cnt;
+        }
+        epi_bar();   // the staging rows are reused by the next tile
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         continue;
       }
@@ -1219,18 +972,28 @@ __global__ void __launch_bounds__(192, 1)
   }
 }
 
-static bool g_pdl = true;   // programmatic dependent launch of the GEMMs (set_gemm_pdl)
+// cudaFuncSetAttribute applies to the current device's context: remember it per
+// device (bit per device ordinal; a process driving several GPUs sets it on each).
+template <typename K>
+static cudaError_t ensure_smem_attr(K kern, int bytes, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = dev < 64 ? (uint64_t(1) << dev) : 0;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && bit) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
-template <typename T, int BN, int EPI, int KMAX = 0, int CG = 1, bool GATHER = false>
-static cudaError_t launch_t(const CUtensorMap& A, const BMaps& B, const GemmParams& p, int grid, cudaStream_t s) {
+template <typename T, int BN, int EPI, int KMAX = 0, int CG = 1>
+static cudaError_t launch_t(const CUtensorMap& A, const BMaps& B, const GemmParams& p, int grid, cudaStream_t s,
+                            bool pdl) {
   using C = GemmCfg<T, BN, CG>;
-  static bool attr_set = false;
-  auto kern = k_grouped_gemm<T, BN, EPI, KMAX, CG, GATHER>;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  auto kern = k_grouped_gemm<T, BN, EPI, KMAX, CG>;
+  cudaError_t e = ensure_smem_attr(kern, C::SMEM, attr_done);
+  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(CG == 2 ? (grid & ~1) : grid));
   cfg.blockDim = dim3(192);
@@ -1245,46 +1008,40 @@ static cudaError_t launch_t(const CUtensorMap& A, const BMaps& B, const GemmPara
     attr[na].val.clusterDim.z = 1;
     ++na;
   }
-  if (g_pdl) {   // may launch while the previous kernel drains; waits in-kernel (griddepcontrol.wait)
+  if (pdl) {   // may launch while the previous kernel drains; waits in-kernel (griddepcontrol.wait)
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[na].val.programmaticStreamSerializationAllowed = 1;
     ++na;
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, A, B, p);
+  e = cudaLaunchKernelEx(&cfg, kern, A, B, p);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 template <typename T>
 static cudaError_t dispatch(int epi, int bn, const CUtensorMap& A, const BMaps& B, const GemmParams& p, int grid,
-                            cudaStream_t s) {
-  if (epi == EPI_SWIGLU_GATHER) {
-    if (bn == 256) return launch_t<T, 256, EPI_SWIGLU, 0, 1, true>(A, B, p, grid, s);
-    if (bn == 128) return launch_t<T, 128, EPI_SWIGLU, 0, 1, true>(A, B, p, grid, s);
-  } else if (epi == EPI_SWIGLU_PAIR_GATHER) {
+                            cudaStream_t s, bool pdl) {
+  if (epi == EPI_SWIGLU_PAIR) {
     if constexpr (sizeof(T) == 2)
-      if (bn == 256) return launch_t<T, 256, EPI_SWIGLU, 0, 2, true>(A, B, p, grid, s);
-  } else if (epi == EPI_SWIGLU_PAIR) {
-    if constexpr (sizeof(T) == 2)
-      if (bn == 256) return launch_t<T, 256, EPI_SWIGLU, 0, 2>(A, B, p, grid, s);
+      if (bn == 256) return launch_t<T, 256, EPI_SWIGLU, 0, 2>(A, B, p, grid, s, pdl);
   } else if (epi == EPI_WEIGHTED_PAIR) {
     if constexpr (sizeof(T) == 2)
-      if (bn == 256) return launch_t<T, 256, EPI_WEIGHTED, 0, 2>(A, B, p, grid, s);
+      if (bn == 256) return launch_t<T, 256, EPI_WEIGHTED, 0, 2>(A, B, p, grid, s, pdl);
   } else if (epi == EPI_SWIGLU) {
-    if (bn == 256) return launch_t<T, 256, EPI_SWIGLU>(A, B, p, grid, s);
-    if (bn == 128) return launch_t<T, 128, EPI_SWIGLU>(A, B, p, grid, s);
-    if (bn == 64) return launch_t<T, 64, EPI_SWIGLU>(A, B, p, grid, s);
+    if (bn == 256) return launch_t<T, 256, EPI_SWIGLU>(A, B, p, grid, s, pdl);
+    if (bn == 128) return launch_t<T, 128, EPI_SWIGLU>(A, B, p, grid, s, pdl);
+    if (bn == 64) return launch_t<T, 64, EPI_SWIGLU>(A, B, p, grid, s, pdl);
   } else if (epi == EPI_WEIGHTED) {
-    if (bn == 256) return launch_t<T, 256, EPI_WEIGHTED>(A, B, p, grid, s);
-    if (bn == 128) return launch_t<T, 128, EPI_WEIGHTED>(A, B, p, grid, s);
-    if (bn == 64) return launch_t<T, 64, EPI_WEIGHTED>(A, B, p, grid, s);
+    if (bn == 256) return launch_t<T, 256, EPI_WEIGHTED>(A, B, p, grid, s, pdl);
+    if (bn == 128) return launch_t<T, 128, EPI_WEIGHTED>(A, B, p, grid, s, pdl);
+    if (bn == 64) return launch_t<T, 64, EPI_WEIGHTED>(A, B, p, grid, s, pdl);
   } else if (epi == EPI_ROUTER) {
     const bool k8 = p.topk_k <= 8;
 #define BO_R(BNV)                                                                        \
-  if (bn == BNV) return k8 ? launch_t<T, BNV, EPI_ROUTER, 8>(A, B, p, grid, s) \
-                           : launch_t<T, BNV, EPI_ROUTER, 16>(A, B, p, grid, s);
+  if (bn == BNV) return k8 ? launch_t<T, BNV, EPI_ROUTER, 8>(A, B, p, grid, s, pdl) \
+                           : launch_t<T, BNV, EPI_ROUTER, 16>(A, B, p, grid, s, pdl);
     BO_R(256) BO_R(128) BO_R(64) BO_R(32) BO_R(16)
 #undef BO_R
   }
@@ -1292,13 +1049,11 @@ static cudaError_t dispatch(int epi, int bn, const CUtensorMap& A, const BMaps& 
 }
 
 cudaError_t launch_grouped_gemm(int dtype, int epi, int bn, const CUtensorMap& A, const BMaps& B,
-                                const GemmParams& p, int grid, cudaStream_t s) {
+                                const GemmParams& p, int grid, cudaStream_t s, bool pdl) {
   if (grid <= 0) return cudaSuccess;
-  if (dtype == 0) return dispatch<__nv_bfloat16>(epi, bn, A, B, p, grid, s);
-  return dispatch<float>(epi, bn, A, B, p, grid, s);
+  if (dtype == 0) return dispatch<__nv_bfloat16>(epi, bn, A, B, p, grid, s, pdl);
+  return dispatch<float>(epi, bn, A, B, p, grid, s, pdl);
 }
-
-void set_gemm_pdl(bool on) { g_pdl = on; }
 
 int gemm_smem_bytes(int dtype, int epi, int bn) {
   (void)epi;

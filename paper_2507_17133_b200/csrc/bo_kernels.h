@@ -11,12 +11,9 @@ constexpr int kTileTok = 128;   // token tile of the tcgen05 router (= GEMM BM)
 constexpr int kBM = 128;        // rows per GEMM tile (TMEM lanes)
 constexpr int kMaxExperts = 256;
 constexpr int kMaxExec = 512;   // m + G
-constexpr int kPackRows = 128;  // rows per band of the tile-packed weight layout
-constexpr int kSkCols = 256;    // stream-K partial tile row stride (fp32 columns >= any BN)
 
 enum Epi : int { EPI_SWIGLU = 0, EPI_WEIGHTED = 1, EPI_ROUTER = 2,
-                 EPI_SWIGLU_PAIR = 3, EPI_WEIGHTED_PAIR = 4,    // *_PAIR: cta_group::2, grid even
-                 EPI_SWIGLU_GATHER = 5, EPI_SWIGLU_PAIR_GATHER = 6 };   // A rows gathered from x (row_tok)
+                 EPI_SWIGLU_PAIR = 3, EPI_WEIGHTED_PAIR = 4 };   // *_PAIR: cta_group::2, grid even
 
 struct GemmParams {
   int Kdim;              // reduction length (executors < m_orig)
@@ -39,8 +36,8 @@ struct GemmParams {
   int32_t* topk_id;      // EPI_ROUTER: [T, K]
   float* topk_w;         // EPI_ROUTER: [T, K]
   int32_t* tile_cnt;     // EPI_ROUTER: [ceil(T/128), m] histogram per 128-token tile
-  const int32_t* row_tok;  // *_GATHER: token of each row (A row r = x[row_tok[r]])
-  int rows_total;          // *_GATHER: R (rows >= R gather token 0, masked at the store); split-K partial rows
+  const int32_t* row_tok;  // fused combine: token of each row
+  int rows_total;          // split-K partial rows (R)
   int ksplit_max;          // EPI_WEIGHTED: > 1 enables split-K (fp32 partials [ks, R, ldo] into `partial`)
   float* partial;          // EPI_WEIGHTED split-K output
   int* ks_out;             // EPI_WEIGHTED split-K: the kernel publishes the split count it chose
@@ -66,21 +63,12 @@ struct GemmParams {
   int add_residual;         // y = x + ... (Eq. 5 residual term)
   const void* comb_x;       // [T, d]
   void* comb_y;             // [T, d]
-  // Stream-K (CG = 1): the (tile, k-block) space split evenly over the grid; tiles cut
-  // between CTAs are finished by their k-block-0 owner from fp32 partials.
-  int pf_dist;              // > 0: the producer prefetches B tiles this many k-blocks ahead into L2
   int b_policy;             // L2 policy of the B (weight) tile loads: 0 evict_normal, 1 evict_first
-  int b_packed;             // 1: B maps are 3-D over tile-packed weights (kPackRows-row bands, see launch_pack)
-  int stream_k;             // 1: enabled (grid must be resident: <= #SM, 1 CTA / SM)
-  float* sk_part;           // [grid, 128, kSkCols] partial of each contributing CTA
-  int* sk_flag;             // [grid] 1 = partial published (reset to 0 by the owner; zero before first use)
   // Swapped-operand tail tiles (CG = 2 SwiGLU, BN = 256): an executor's last m-tile with
   // fewer than 256 rows runs as D^T = W X^T, the 256 gate / up weight rows on the MMA's
   // M side and its rows (rounded up to 32) on N, so a ragged tile costs its rows, not 256.
   // Maps [6..11] then hold 64-row gate / up boxes and [12..14] 16 / 32 / 64-row boxes of A (Xp).
   int swap_tail;
-  int swap_max;             // largest tail (rows) run swapped (<= 0: any tail < 256)
-  int a_policy;             // L2 policy of the A (activation) loads: 0 evict_last, 1 evict_normal, 2 evict_first
   int tma_store;            // EPI_WEIGHTED: full 32-row slabs leave through TMA bulk stores (map B[6], 32 x 32 box, 64B swizzle)
 };
 
@@ -100,11 +88,10 @@ cudaError_t launch_combine_partials(int dtype, const float* partial, const int* 
 struct BMaps {
   CUtensorMap m[15];
 };
+// pdl: programmatic dependent launch (the GEMM's prologue may overlap the previous kernel's tail).
 cudaError_t launch_grouped_gemm(int dtype, int epi, int bn, const CUtensorMap& A, const BMaps& B,
-                                const GemmParams& p, int grid, cudaStream_t s);
+                                const GemmParams& p, int grid, cudaStream_t s, bool pdl);
 int gemm_smem_bytes(int dtype, int epi, int bn);
-// Programmatic dependent launch of the grouped GEMMs (process-wide; env BO_PDL=0 disables).
-void set_gemm_pdl(bool on);
 
 constexpr int kTileMin = 8;     // smallest token tile (workspace histograms are sized for it)
 constexpr int kTileSmall = 32;  // token tile of the injected-logits top-k
@@ -125,11 +112,20 @@ cudaError_t launch_router_split(int dtype, const void* x, const void* Wr, int T,
 cudaError_t launch_router_small(int dtype, const void* x, const void* Wr, int T, int d, int m, int K, int tile,
                                 float* logits, int32_t* topk_id, float* topk_w, int32_t* tile_cnt, cudaStream_t s);
 
+// Expert-parallel extensions of the plan kernel: ld = row stride of the count rows (0: m);
+// knob_in (nullable, device int32[4] = [T, mode, ratio lo, ratio hi]) overrides ratio / mode;
+// row_tail (nullable, device int32[4]) receives [row_T, mode, ratio lo, ratio hi] of the knob used.
+struct PlanExt {
+  int ld = 0;
+  const int32_t* knob_in = nullptr;
+  int32_t* row_tail = nullptr;
+  int row_T = 0;
+};
 // n_shared shared experts (Eq. 5) are appended after the m + G routed executors with shared_rows rows each.
 cudaError_t launch_plan(const int32_t* tile_cnt, int ntiles, int m, int way, double ratio, int mode,
                         int32_t* tile_base, int32_t* counts, int32_t* exec_of_expert, int32_t* expert_row_off,
                         int32_t* exec_off, int32_t* mtile_off, int64_t* stats, cudaStream_t s, int n_shared = 0,
-                        int shared_rows = 0);
+                        int shared_rows = 0, PlanExt ext = PlanExt());
 
 // xp != nullptr: the permute also copies each token's x row to its rows (fused gather).
 cudaError_t launch_permute(const int32_t* topk_id, const float* topk_w, int T, int K, int m, int tile,
@@ -154,11 +150,6 @@ cudaError_t launch_dedup(int stage, const int32_t* topk_id, const float* topk_w,
                          const int32_t* exec_of, int32_t* tile_xcnt, int32_t* tile_xbase, int32_t* exec_off,
                          int32_t* mtile_off, int64_t* stats, int32_t* row_of, int32_t* row_tok, float* row_w,
                          cudaStream_t s);
-
-// Tile-packed weights: n row-major matrices [rows, K] -> [n][rows/128][K/kc][128][kc]
-// (kc = 128 bytes of K): every 128-row x 128-byte TMA box of the GEMMs is one
-// contiguous 16 KB block, read at full DRAM streaming bandwidth.
-cudaError_t launch_pack(int dtype, const void* W, int64_t n, int rows, int K, void* P, int num_sms, cudaStream_t s);
 
 cudaError_t launch_build_united(int dtype, const void* W, int m, int way, int64_t per_expert, void* U,
                                 cudaStream_t s);

@@ -568,7 +568,21 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
                                               int32_t* __restrict__ counts, int32_t* __restrict__ exec_of_expert,
                                               int32_t* __restrict__ expert_row_off, int32_t* __restrict__ exec_off,
                                               int32_t* __restrict__ mtile_off, int64_t* __restrict__ stats,
-                                              int n_shared, int shared_rows) {
+                                              int n_shared, int shared_rows, PlanExt ext) {
+  // Expert parallelism (ext.knob_in): the knob travels with the all-gathered count rows
+  // [R, m + 4] (tail [T, mode, ratio lo, ratio hi]); every rank plans with rank 0's, so
+  // ranks whose host knobs differ (a per-rank SALC loop) still agree on the global plan.
+  if (ext.knob_in) {
+    mode = ext.knob_in[1];
+    ratio = __hiloint2double(ext.knob_in[3], ext.knob_in[2]);
+  }
+  if (ext.row_tail && threadIdx.x == 0) {   // this rank's gather row tail
+    ext.row_tail[0] = ext.row_T;
+    ext.row_tail[1] = mode;
+    ext.row_tail[2] = __double2loint(ratio);
+    ext.row_tail[3] = __double2hiint(ratio);
+  }
+  const int ld = ext.ld > 0 ? ext.ld : m;   // row stride of tile_cnt
   __shared__ __align__(16) int s_tc[kPlanStage];
   __shared__ int s_cnt[kMaxExperts];
   __shared__ int s_sorted[kMaxExperts];
@@ -583,14 +597,17 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
   const int E = m + G;
   const int n_tc = ntiles * m;
   const bool staged = n_tc <= kPlanStage;
+  // 16-byte cp.async needs a 16-byte-aligned source; a caller's counts row (bo_plan_counts /
+  // bo_plan_from_counts take any int32 pointer) may be only 4-byte aligned
+  const bool vec16 = (reinterpret_cast<uintptr_t>(tile_cnt) & 15u) == 0 && ld == m;
 
   // 1. cnt_i (Alg. 1 input) and the per-tile exclusive prefix used by
   //    the permutation.  Histograms are staged with coalesced loads, then a
   //    warp per expert scans over tiles (lanes over tiles, shuffle scan + carry).
   if (staged) {   // all loads in flight at once (cp.async), not one dependent load per iteration
-    const int n16 = n_tc / 4;
+    const int n16 = vec16 ? n_tc / 4 : 0;
     for (int i = tid; i < n16; i += blockDim.x) cp_async16(s_tc + 4 * i, tile_cnt + 4 * i);
-    for (int i = 4 * n16 + tid; i < n_tc; i += blockDim.x) s_tc[i] = __ldg(tile_cnt + i);
+    for (int i = 4 * n16 + tid; i < n_tc; i += blockDim.x) s_tc[i] = __ldg(tile_cnt + (i / m) * ld + i % m);
     cp_async_wait_all();
   }
   if (tid < m) s_gsize[tid] = 0;
@@ -630,7 +647,7 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
     int carry = 0;
     for (int t0 = 0; t0 < ntiles; t0 += 32) {
       const int t = t0 + lane;
-      const int v = t < ntiles ? (staged ? s_tc[t * m + e] : __ldg(tile_cnt + static_cast<int64_t>(t) * m + e)) : 0;
+      const int v = t < ntiles ? (staged ? s_tc[t * m + e] : __ldg(tile_cnt + static_cast<int64_t>(t) * ld + e)) : 0;
       int incl = v;
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
@@ -757,9 +774,9 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
 cudaError_t launch_plan(const int32_t* tile_cnt, int ntiles, int m, int way, double ratio, int mode,
                         int32_t* tile_base, int32_t* counts, int32_t* exec_of_expert, int32_t* expert_row_off,
                         int32_t* exec_off, int32_t* mtile_off, int64_t* stats, cudaStream_t s, int n_shared,
-                        int shared_rows) {
+                        int shared_rows, PlanExt ext) {
   k_plan<<<1, kMaxExec, 0, s>>>(tile_cnt, ntiles, m, way, ratio, mode, tile_base, counts, exec_of_expert,
-                                expert_row_off, exec_off, mtile_off, stats, n_shared, shared_rows);
+                                expert_row_off, exec_off, mtile_off, stats, n_shared, shared_rows, ext);
   return cudaGetLastError();
 }
 
@@ -1147,40 +1164,6 @@ __global__ void k_united_mean(const T* __restrict__ W, int m, int way, int64_t p
       U[i] = __double2float_rn(mean);
     }
   }
-}
-
-// ------------------------------------------------------ tile-packed weights
-// One 16-byte vector per thread step; source index decomposed from the packed
-// (destination) order so the writes are fully sequential.
-__global__ void __launch_bounds__(256) k_pack(const uint4* __restrict__ W, int64_t n, int rows, int kv,
-                                              uint4* __restrict__ P) {
-  // kv = K in 16-byte vectors; a k-chunk is 8 vectors (128 bytes)
-  const int64_t total = n * rows * static_cast<int64_t>(kv);
-  const int kch = kv / 8, bands = rows / kPackRows;
-  for (int64_t o = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; o < total;
-       o += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    // o = (((e * bands + band) * kch + kc) * 128 + r) * 8 + v
-    const int v = static_cast<int>(o & 7);
-    int64_t q = o >> 3;
-    const int r = static_cast<int>(q % kPackRows);
-    q /= kPackRows;
-    const int kc = static_cast<int>(q % kch);
-    q /= kch;
-    const int band = static_cast<int>(q % bands);
-    const int64_t e = q / bands;
-    const int64_t src = ((e * rows) + static_cast<int64_t>(band) * kPackRows + r) * kv + kc * 8 + v;
-    P[o] = __ldg(W + src);
-  }
-}
-
-cudaError_t launch_pack(int dtype, const void* W, int64_t n, int rows, int K, void* P, int num_sms, cudaStream_t s) {
-  const int kv = K * (dtype == 0 ? 2 : 4) / 16;
-  const int64_t total = n * rows * static_cast<int64_t>(kv);
-  if (total == 0) return cudaSuccess;
-  int64_t blocks = (total + 255) / 256;
-  if (blocks > num_sms * 16) blocks = num_sms * 16;
-  k_pack<<<static_cast<int>(blocks), 256, 0, s>>>(static_cast<const uint4*>(W), n, rows, kv, static_cast<uint4*>(P));
-  return cudaGetLastError();
 }
 
 cudaError_t launch_build_united(int dtype, const void* W, int m, int way, int64_t per_expert, void* U,

@@ -52,19 +52,12 @@ def main():
                 weights[arm] = base_w
                 continue
             env = dict(env)
-            tiled = env.pop("TILED", "0") == "1"   # pseudo-knob: TILED weight layout (packed copies)
             old = {k: os.environ.get(k) for k in env}
             os.environ.update(env)
             moe = BrownoutMoE(cfg.d, cfg.f, cfg.m, cfg.K, cfg.way, dtype=cfg.dtype, max_tokens=layer.T,
-                              num_shared=cfg.Ns, tiled=tiled)
+                              num_shared=cfg.Ns)
             lay = layer.lay
             uni = layer.united
-            if tiled:
-                lay = dict(layer.lay)
-                lay["Wg"], lay["Wu"], lay["Wd"] = moe.pack_all(layer.lay["Wg"], layer.lay["Wu"], layer.lay["Wd"])
-                uni = moe.pack_all(*layer.united)
-                if cfg.Ns:
-                    lay["SWg"], lay["SWu"], lay["SWd"] = moe.pack_all(lay["SWg"], lay["SWu"], lay["SWd"])
             weights[arm] = (lay, uni)
             if cfg.Ns:
                 moe.set_shared_experts(lay["SWg"], lay["SWu"], lay["SWd"])

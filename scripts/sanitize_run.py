@@ -1,9 +1,8 @@
 """Small forwards over the library's code paths, for compute-sanitizer
 (memcheck / racecheck / synccheck / initcheck): bf16 decode and CTA-pair prefill,
-fp32 (tf32), shared experts, united-row de-duplication, full brownout, the TILED
-weight layout, the fused combine, the split-tile schedules and the swapped
-tail tiles (GEMM1 default, GEMM2 with BO_SWAP_TAIL=3).  Exits non-zero if
-a forward disagrees with the ROWMAJOR / default path of the same inputs."""
+fp32 (tf32), shared experts, united-row de-duplication, full brownout, the fused
+combine, the decode split-K GEMM2 and the swapped GEMM1 tail tiles.  Exits
+non-zero if the fused combine disagrees bitwise with the separate kernel."""
 import os
 import sys
 
@@ -16,17 +15,14 @@ import synthetic as S  # noqa: E402
 from paper_2507_17133_b200 import BrownoutMoE  # noqa: E402
 
 
-def run(cfg, ratio=0.5, mode="partial", dedup=False, tiled=False, logits=True):
+def run(cfg, ratio=0.5, mode="partial", dedup=False, logits=True):
     lay = {k: v.cuda() for k, v in S.make_layer(cfg).items()}
     x = S.make_tokens(cfg, batch_index=2).cuda()
     moe = BrownoutMoE(cfg.d, cfg.f, cfg.m, cfg.K, cfg.way, dtype=cfg.dtype, max_tokens=cfg.T, dedup=dedup,
-                      num_shared=cfg.Ns, tiled=tiled)
+                      num_shared=cfg.Ns)
     ex = (lay["Wg"], lay["Wu"], lay["Wd"])
     sh = (lay["SWg"], lay["SWu"], lay["SWd"]) if cfg.Ns else None
     U = moe.build_united(*ex)
-    if tiled:
-        ex, U = moe.pack_all(*ex), moe.pack_all(*U)
-        sh = moe.pack_all(*sh) if sh else None
     moe.set_brownout(ratio, mode)
     L = S.make_logits(cfg.T, cfg.m, seed=2, sigma=cfg.sigma).cuda() if logits else None
     y = moe.forward(x, lay["Wr"], ex, U, logits=L, shared=sh)
@@ -63,7 +59,7 @@ def main():
         ("decode_ratio1", lambda: run(small, ratio=1.0)),
         ("router_gpu", lambda: run(small, logits=False)),
         ("prefill_pairs_fused_combine", lambda: run(pair)),   # GEMM1 swapped tail tiles (default)
-        ("prefill_pairs_swap_gemm2", lambda: run_env({"BO_SWAP_TAIL": "3"}, pair)),
+        ("decode_gemm2_splitk", lambda: run_env({"BO_GEMM2_SPLITK": "1"}, small)),
         ("fp32", lambda: run(fp32)),
         ("qwen_like_tc_router", lambda: run(qwen, logits=False)),
         ("shared", lambda: run(shared)),
@@ -72,7 +68,8 @@ def main():
     ]:
         f()
         print("ok", name, flush=True)
-    for name, a, b in [("tiled", lambda: run(small), lambda: run(small, tiled=True))]:
+    for name, a, b in [("fused_combine", lambda: run_env({"BO_FUSED_COMBINE": "0"}, pair),
+                        lambda: run_env({"BO_FUSED_COMBINE": "1"}, pair))]:
         if not torch.equal(a(), b()):
             bad += 1
             print("MISMATCH", name)

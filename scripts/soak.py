@@ -20,11 +20,10 @@ import torch  # noqa: E402
 import synthetic as S  # noqa: E402
 from oracle import brownout_oracle as O  # noqa: E402
 
-KNOBS = [{}, {"BO_FUSED_COMBINE": "1"}, {"BO_FUSED_COMBINE": "0"}, {"BO_GEMM_CG": "1"}, {"BO_SPLITK": "1"},
-         {"BO_STREAMK": "1"}, {"BO_STREAMK": "2"}, {"BO_TILE_ALT": "0"}, {"BO_DECODE_PAIR2": "0"},
+KNOBS = [{}, {"BO_FUSED_COMBINE": "1"}, {"BO_FUSED_COMBINE": "0"}, {"BO_CTA_PAIRS": "0"}, {"BO_GEMM2_SPLITK": "1"},
+         {"BO_TILE_ALT": "0"}, {"BO_DECODE_PAIR2": "0"},
          {"BO_PAIR_ROWS1": "1", "BO_PAIR_ROWS2": "1"}, {"BO_B_POLICY": "1"},
-         {"BO_PAIR_ROWS1": "1", "BO_PAIR_ROWS2": "1", "BO_SWAP_TAIL": "3"},
-         {"BO_PAIR_ROWS1": "1", "BO_SWAP_TAIL": "0"}]
+         {"BO_PAIR_ROWS1": "1", "BO_SWAP_TAIL": "0"}, {"BO_TMA_STORE": "0", "BO_PDL": "0"}]
 
 
 def case(rng, i):

@@ -165,3 +165,47 @@ def make_logits(T: int, m: int, seed: int = 0, sigma: float = 0.5, device="cpu",
         return L
     bias = torch.randn(m, generator=g, device=device) * sigma
     return torch.randn(T, m, generator=g, device=device) + bias
+
+
+def make_exact_router_inputs(cfg: LayerConfig, T: int | None = None, batch_index: int = 0, device="cpu",
+                             ties: bool = False):
+    """Tokens x [T, d] and router centroids Wr [m, d] whose Eq. 8 dot products
+    are EXACT in fp32 (and tf32) accumulation in any order, so that the GPU
+    router's logits equal the fp64 ones bit for bit and routing parity needs no
+    clear-margin filter.
+
+    ties=False ("dyadic"): x ~ N(0, 1) rounded to multiples of 1/8 in
+    [-4, 4), x[:, 0] = 1; Wr ~ N(0, 1/d) rounded to multiples of 2^-10 in
+    (-1/4, 1/4), bias channel Wr[:, 0] ~ N(0, sigma^2) on the same grid.  Every
+    product is a multiple of 2^-13; the caller checks the partial-sum bound
+    sum_j |x_tj||Wr_ej| < 2^11 (exactness_bound) so every partial sum has at
+    most 24 significant bits.
+
+    ties=True ("integer"): x in {-1, 0, 1} (x[:, 0] = 1), Wr in {-1, 0, 1} on
+    16 channels plus an integer bias in [-2, 2]: logits are small integers and
+    exact ties between experts are frequent (Eq. 7 tie rule, reading D8).
+    """
+    T = cfg.T if T is None else T
+    g = _gen(5000 + 97 * cfg.config_id + batch_index, device)
+    dt = torch_dtype(cfg.dtype)
+    d, m = cfg.d, cfg.m
+    if ties:
+        x = torch.randint(-1, 2, (T, d), generator=g, device=device).to(torch.float32)
+        x[:, 0] = 1.0
+        Wr = torch.zeros(m, d, device=device)
+        nz = min(16, d - 1)
+        Wr[:, 1:1 + nz] = torch.randint(-1, 2, (m, nz), generator=g, device=device).to(torch.float32)
+        Wr[:, 0] = torch.randint(-2, 3, (m,), generator=g, device=device).to(torch.float32)
+    else:
+        x = (torch.randn(T, d, generator=g, device=device) * 8.0).round().clamp(-32, 31) / 8.0
+        x[:, 0] = 1.0
+        Wr = (torch.randn(m, d, generator=g, device=device) * (1.0 / d) ** 0.5 * 1024.0).round().clamp(-255, 255)
+        Wr[:, 0] = (torch.randn(m, generator=g, device=device) * cfg.sigma * 1024.0).round().clamp(-2047, 2047)
+        Wr = Wr / 1024.0
+    return x.to(dt), Wr.to(dt)
+
+
+def exactness_bound(x: torch.Tensor, Wr: torch.Tensor) -> float:
+    """max over (t, e) of sum_j |x_tj| |Wr_ej| (fp64) - with products on the
+    2^-13 grid, partial sums below 2^11 carry at most 24 significant bits."""
+    return float((x.double().abs() @ Wr.double().abs().T).max()) if x.numel() else 0.0

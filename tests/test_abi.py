@@ -56,7 +56,7 @@ def test_bad_configs_are_rejected_before_device_use(built):
 
     def create(**kw):
         base = dict(hidden=256, ffn=512, num_experts=8, top_k=2, way=4, dtype=0, add_residual=0, dedup_united=0,
-                    num_shared=0, weight_layout=0, max_tokens=128)
+                    num_shared=0, max_tokens=128)
         base.update(kw)
         return lib.bo_create(C.byref(bo_config(**base)), C.byref(h))
 

@@ -64,7 +64,12 @@ def test_tables_partition_every_row_exactly_once(R, ratio):
         eo = tabs[q]["exec_off"]
         assert eo[-1] == tabs[q]["R_recv"] and (np.diff(eo) >= 0).all()
         assert len(eo) - 1 == tabs[q]["n_orig"] + tabs[q]["n_united"]
-    assert all(len(f) > 0 for f in fd) or ratio < 1 or True
+    # a virtual executor is fed exactly when the plan uses its executor: an original
+    # expert that executes as itself, or a united expert some member is delegated to
+    ex = plan.exec_of_expert
+    for v, (q, kind, idx, _s) in enumerate(pl.vexec):
+        used = (ex[idx] == idx) if kind == "o" else bool((ex == 8 + idx).any())
+        assert (len(fd[v]) > 0) == used, (v, kind, idx)
 
 
 # ------------------------------------------------------------------ gloo path
@@ -130,7 +135,7 @@ def test_ep_gloo_matches_single_process_oracle(world, ratio):
 
 # ------------------------------------------------------------ one-GPU virtual EP
 @pytest.mark.gpu
-@pytest.mark.parametrize("env", [{}, {"BO_PAIR_ROWS1": "1", "BO_PAIR_ROWS2": "1", "BO_SWAP_TAIL": "3"}],
+@pytest.mark.parametrize("env", [{}, {"BO_PAIR_ROWS1": "1", "BO_PAIR_ROWS2": "1", "BO_SWAP_TAIL": "1"}],
                          ids=["default", "pairs_swapped_tails"])
 @pytest.mark.parametrize("R", [1, 2, 4, 8])
 @pytest.mark.parametrize("ratio", [0.0, 0.5, 1.0])

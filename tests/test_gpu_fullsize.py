@@ -6,8 +6,13 @@ can compute one token at a time:
 
   * routing / Alg. 1 plan / permutation: bit-exact for ALL tokens, given the
     same injected fp32 logits (seeded generator, not the CUDA path);
-  * outputs: 48 seeded sampled tokens within 2e-2 of the fp64 oracle;
-  * router GEMM (Eq. 8) on the sampled tokens within 1e-3 (1 + |s|) of fp64.
+  * outputs: 512 seeded sampled tokens (C3's 256: all) within 2e-2 of the fp64
+    oracle, at every ratio of the sweep (C2: 0 / 0.25 / 0.5 / 1, C3: 0 / 0.5 / 1);
+  * router GEMM (Eq. 8) on the sampled tokens within 1e-3 (1 + |s|) of fp64;
+  * the production router end to end (no injected logits) on exactly
+    representable inputs (synthetic.make_exact_router_inputs): logits of ALL
+    tokens equal fp64, ordered top-K ids / plan / permutation bit-exact against
+    the oracle's own Eq. 8 -> Eq. 7 -> Alg. 1, sampled outputs within 2e-2.
 """
 import numpy as np
 import pytest
@@ -18,7 +23,7 @@ from oracle import brownout_oracle as O
 
 pytestmark = pytest.mark.gpu
 
-N_SAMPLE = 48
+N_SAMPLE = 512
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -31,8 +36,12 @@ def _f32np(t):
     return t.float().cpu().numpy()
 
 
-@pytest.mark.parametrize("name,ratio", [("mixtral_prefill", 0.5), ("mixtral_decode", 1.0),
-                                        ("qwen3_30b_a3b_prefill", 0.5), ("qwen15_moe_a27b_prefill", 0.8)])
+FULL_CASES = ([("mixtral_prefill", r) for r in (0.0, 0.25, 0.5, 1.0)] +
+              [("mixtral_decode", r) for r in (0.0, 0.5, 1.0)] +
+              [("qwen3_30b_a3b_prefill", 0.5), ("qwen15_moe_a27b_prefill", 0.8)])
+
+
+@pytest.mark.parametrize("name,ratio", FULL_CASES)
 def test_fullsize_sampled_parity(name, ratio):
     from paper_2507_17133_b200 import BrownoutMoE
     cfg = S.with_(S.CONFIGS[name], ratio=ratio)
@@ -54,7 +63,7 @@ def test_fullsize_sampled_parity(name, ratio):
         idx = np.random.default_rng(0).integers(0, got.numel(), size=4096)
         assert np.array_equal(got.reshape(-1)[torch.as_tensor(idx, device="cuda")].double().cpu().numpy(),
                               want.reshape(-1)[idx])
-    toks = np.sort(np.random.default_rng(1).choice(cfg.T, size=N_SAMPLE, replace=False))
+    toks = np.sort(np.random.default_rng(1).choice(cfg.T, size=min(N_SAMPLE, cfg.T), replace=False))
     xn = _f32np(x)
     sh = tuple(_f32np(lay[k]) for k in ("SWg", "SWu", "SWd")) if cfg.Ns else None
     ref = O.moe_forward(xn, None, ex, un, cfg.K, cfg.way, ratio, logits=L.double().numpy(), tokens=toks,
@@ -77,3 +86,41 @@ def test_fullsize_sampled_parity(name, ratio):
     Lg = moe.debug_arrays(cfg.T)["logits"][torch.as_tensor(toks, device="cuda")].double().cpu().numpy()
     Lr = O.router_logits(xn[toks], _f32np(lay["Wr"]))
     assert (np.abs(Lg - Lr) <= 1e-3 * (1 + np.abs(Lr))).all()
+
+
+@pytest.mark.parametrize("name,ratio", [("mixtral_prefill", 0.5), ("mixtral_decode", 1.0),
+                                        ("qwen3_30b_a3b_prefill", 0.5), ("qwen15_moe_a27b_prefill", 0.8)])
+def test_fullsize_production_router_exact(name, ratio):
+    """The bench's launch configuration including its router (mma.sync for C2,
+    the split-warp router for C3, tcgen05 with the fused top-K for C4 / f2), on
+    exactly representable router inputs: no clear-margin filter anywhere."""
+    from paper_2507_17133_b200 import BrownoutMoE
+    cfg = S.with_(S.CONFIGS[name], ratio=ratio)
+    lay = S.make_layer(cfg, device="cuda")
+    moe = BrownoutMoE(cfg.d, cfg.f, cfg.m, cfg.K, cfg.way, dtype=cfg.dtype, max_tokens=cfg.T, num_shared=cfg.Ns)
+    moe.set_brownout(ratio)
+    if cfg.Ns:
+        moe.set_shared_experts(lay["SWg"], lay["SWu"], lay["SWd"])
+    U = moe.build_united(lay["Wg"], lay["Wu"], lay["Wd"])
+    x, Wr = S.make_exact_router_inputs(cfg, T=cfg.T)
+    assert S.exactness_bound(x, Wr) < 2.0 ** 11
+    y = moe.forward(x.cuda(), Wr.cuda(), (lay["Wg"], lay["Wu"], lay["Wd"]), U)
+    torch.cuda.synchronize()
+    dbg = moe.debug_arrays(cfg.T)
+    ex = tuple(_f32np(lay[k]) for k in ("Wg", "Wu", "Wd"))
+    un = O.build_united_mean(*ex, cfg.way)   # the oracle's own united init (GPU's is checked bit-exact above)
+    toks = np.sort(np.random.default_rng(2).choice(cfg.T, size=min(N_SAMPLE, cfg.T), replace=False))
+    sh = tuple(_f32np(lay[k]) for k in ("SWg", "SWu", "SWd")) if cfg.Ns else None
+    ref = O.moe_forward(_f32np(x), _f32np(Wr), ex, un, cfg.K, cfg.way, ratio, tokens=toks, shared=sh)
+    assert np.array_equal(dbg["logits"].cpu().double().numpy(), ref.logits)
+    assert np.array_equal(dbg["topk_id"].cpu().numpy(), ref.ids)
+    assert np.abs(dbg["topk_w"].cpu().double().numpy() - ref.g).max() <= 1e-6
+    assert np.array_equal(dbg["counts"].cpu().numpy(), ref.plan.counts)
+    assert np.array_equal(dbg["exec_of_expert"].cpu().numpy(), ref.plan.exec_of_expert)
+    E = cfg.m + cfg.G
+    assert np.array_equal(dbg["exec_off"].cpu().numpy()[:E + 1], ref.perm.exec_off)
+    ro = dbg["row_of"].cpu().numpy().reshape(cfg.T, cfg.K + cfg.Ns)
+    assert np.array_equal(ro[:, :cfg.K].reshape(-1), ref.perm.row_of)
+    yg = y[torch.as_tensor(toks, device="cuda")].double().cpu().numpy()
+    den = np.abs(ref.y).max(1, keepdims=True)
+    assert (np.abs(yg - ref.y) / den).max() <= 2e-2

@@ -170,7 +170,7 @@ ROUTER_CFGS = SMALL + [
 
 
 @pytest.mark.parametrize("cfg", ROUTER_CFGS, ids=lambda c: c.name)
-@pytest.mark.parametrize("router", ["default", "no_split", "no_mma", "splitk"])
+@pytest.mark.parametrize("router", ["default", "no_split", "no_mma"])
 def test_router_logits_vs_fp64(cfg, router, monkeypatch):
     """Eq. 8 (tcgen05 for m > 32; for m <= 32: the split-warp decode router
     below 8 x #SM tokens, the mma.sync router above (bf16), else the
@@ -180,8 +180,6 @@ def test_router_logits_vs_fp64(cfg, router, monkeypatch):
         monkeypatch.setenv("BO_ROUTER_SPLIT", "0")
     if router == "no_mma":
         monkeypatch.setenv("BO_ROUTER_MMA", "0")
-    if router == "splitk":       # m > 32: lockstep K split of the router tiles (option)
-        monkeypatch.setenv("BO_ROUTER_SPLITK", "1")
     lay = S.make_layer(cfg)
     x = S.make_tokens(cfg, T=cfg.T)
     moe = _moe(cfg)
@@ -195,31 +193,40 @@ def test_router_logits_vs_fp64(cfg, router, monkeypatch):
     assert (np.abs(Lg - Lr) <= tol).all()
 
 
+def _ordered_clear(Lr, K, rel=1e-3):
+    """Tokens whose top-(K+1) fp64 logits are separated by more than the router
+    error bound at EVERY consecutive gap: for them the GPU's ordered top-K ids
+    cannot differ from the oracle's (no sorting of the ids needed)."""
+    Ls = np.sort(Lr, axis=1)[:, ::-1]
+    k1 = min(K + 1, Lr.shape[1])
+    gaps = Ls[:, :k1 - 1] - Ls[:, 1:k1]
+    bound = rel * (1 + np.abs(Ls[:, :k1 - 1]))
+    return (gaps > bound).all(axis=1) if k1 > 1 else np.ones(Lr.shape[0], dtype=bool)
+
+
 @pytest.mark.parametrize("cfg", SMALL + ROUTER_CFGS[-2:], ids=lambda c: c.name)
-def test_full_path_with_router_matches_oracle_when_margins_are_clear(cfg):
-    """End to end with the GPU router: when every token's K-th / (K+1)-th fp64
-    logit gap exceeds the router error bound, routing cannot differ, so the
-    whole forward must match the oracle's own fp64 path."""
+def test_full_path_with_router_ordered_ids_on_random_inputs(cfg):
+    """End to end with the GPU router on the seeded N(0, 1) inputs: on tokens
+    whose top-(K+1) fp64 logits are clearly separated the ORDERED ids equal the
+    oracle's.  (Routing and outputs with no margin filter at all are checked on
+    exactly representable inputs, tests/test_gpu_router_exact.py.)"""
     lay = S.make_layer(cfg)
     uni = S.make_united_random(cfg)
     x = S.make_tokens(cfg, T=cfg.T, batch_index=7)
-    ex, un = _oracle_weights(lay, uni)
-    ref = O.moe_forward(_np(x), _np(lay["Wr"]), ex, un, cfg.K, cfg.way, 0.5)
-    Ls = np.sort(ref.logits, axis=1)[:, ::-1]
-    margin = (Ls[:, cfg.K - 1] - Ls[:, cfg.K]) if cfg.K < cfg.m else np.full(cfg.T, np.inf)
-    clear = margin > 1e-3 * (1 + np.abs(Ls[:, cfg.K - 1]))
+    Lr = O.router_logits(_np(x), _np(lay["Wr"]))
+    ids_ref, g_ref = O.topk_gate(Lr, cfg.K)
+    clear = _ordered_clear(Lr, cfg.K, 4e-3 if cfg.dtype == "fp32" else 1e-3)
+    assert clear.mean() > 0.5
     moe = _moe(cfg)
     moe.set_brownout(0.5)
     g = {k: v.cuda() for k, v in lay.items()}
     u = {k: v.cuda() for k, v in uni.items()}
-    y = moe.forward(x.cuda(), g["Wr"], (g["Wg"], g["Wu"], g["Wd"]), (u["UWg"], u["UWu"], u["UWd"]))
+    moe.forward(x.cuda(), g["Wr"], (g["Wg"], g["Wu"], g["Wd"]), (u["UWg"], u["UWu"], u["UWd"]))
     torch.cuda.synchronize()
     dbg = moe.debug_arrays(cfg.T)
     ids = dbg["topk_id"].cpu().numpy()
-    assert np.array_equal(ids[clear], ref.ids[clear])
-    if clear.all():
-        _check_routing_and_plan(dbg, ref, cfg.T, cfg.K)
-        assert _rel_err(_np(y), ref.y) <= OUT_TOL
+    assert np.array_equal(ids[clear], ids_ref[clear])
+    assert np.abs(dbg["topk_w"].cpu().double().numpy()[clear] - g_ref[clear]).max() <= 1e-2
 
 
 def test_deterministic_bitwise():
@@ -287,17 +294,19 @@ def test_plan_random_counts_bitexact():
         assert np.array_equal(out["exec_off"].cpu().numpy(), perm.exec_off)
 
 
-@pytest.mark.parametrize("env", [{"BO_GATHER": "1"}, {"BO_GEMM_CG": "1"}, {"BO_SPLITK": "1"}, {"BO_TILE_ALT": "0"},
-                                 {"BO_STREAMK": "2"}, {"BO_STREAMK": "1"}, {"BO_PAIR_ROWS1": "1", "BO_PAIR_ROWS2": "1"},
-                                 {"BO_PAIR_ROWS2": "1", "BO_SPLITK": "1"}],
-                         ids=["gather4_gemm1", "single_cta_gemm", "splitk_gemm2", "no_tile_alt", "lockstep_splitk", "stream_k_hybrid",
-                              "pairs_always", "pairs_splitk_gemm2"])
+@pytest.mark.parametrize("env", [{"BO_CTA_PAIRS": "0"}, {"BO_GEMM2_SPLITK": "1"}, {"BO_TILE_ALT": "0"},
+                                 {"BO_PAIR_ROWS1": "1", "BO_PAIR_ROWS2": "1"},
+                                 {"BO_PAIR_ROWS2": "1", "BO_GEMM2_SPLITK": "1"},
+                                 {"BO_PAIR_ROWS1": "1", "BO_SWAP_TAIL": "0"}, {"BO_TMA_STORE": "0", "BO_PDL": "0"},
+                                 {"BO_STORE_HINT": "0", "BO_B_POLICY": "1"}],
+                         ids=["single_cta_gemm", "splitk_gemm2", "no_tile_alt", "pairs_always", "pairs_splitk_gemm2",
+                              "pairs_no_swap", "no_tma_store_no_pdl", "hints"])
 @pytest.mark.parametrize("cfg", [SMALL[0], SMALL[2], SMALL[3], SMALL[7],
                                  S.LayerConfig("pairs_bf16", d=256, f=512, m=8, K=2, way=4, T=1500, ratio=0.5,
                                                dtype="bf16", sigma=0.5, config_id=21)], ids=lambda c: c.name)
 def test_engine_variants_match_oracle(cfg, env, monkeypatch):
-    """The non-default engine variants stay correct: GEMM1 fed by TMA gather4
-    from x (BO_GATHER=1) and one-CTA tcgen05 tiles instead of CTA pairs."""
+    """The non-default engine options (bo_engine_option, set here through the
+    BO_<NAME> environment defaults) stay correct."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     _, y, dbg, ref = _run_injected(cfg, 0.5, seed=21)
@@ -368,8 +377,8 @@ def test_random_shapes_match_oracle(cfg):
 @pytest.mark.parametrize("cfg", _rand_cfgs(n=8, seed=7), ids=lambda c: c.name)
 def test_random_shapes_router_and_topk(cfg):
     """Router (Eq. 8, CUDA-core or tcgen05 path by shape) vs fp64, and its fused
-    top-K: on tokens whose K-th / (K+1)-th fp64 gap is clear, the selected
-    experts equal the oracle's."""
+    top-K: on tokens whose top-(K+1) fp64 logits are clearly separated, the
+    ordered ids equal the oracle's."""
     lay = S.make_layer(cfg)
     x = S.make_tokens(cfg, T=cfg.T, batch_index=3)
     moe = _moe(cfg)
@@ -383,11 +392,9 @@ def test_random_shapes_router_and_topk(cfg):
     tol = (2e-3 if cfg.dtype == "fp32" else 1e-3) * (1.0 + np.abs(Lr))
     assert (np.abs(Lg - Lr) <= tol).all()
     ids_ref, _ = O.topk_gate(Lr, cfg.K)
-    Ls = np.sort(Lr, axis=1)[:, ::-1]
-    gap = Ls[:, cfg.K - 1] - (Ls[:, cfg.K] if cfg.K < cfg.m else -np.inf)
-    clear = gap > 4 * 1e-3 * (1 + np.abs(Ls[:, cfg.K - 1]))
+    clear = _ordered_clear(Lr, cfg.K, 4e-3)
     ids = dbg["topk_id"].cpu().numpy()
-    assert np.array_equal(np.sort(ids[clear], 1), np.sort(ids_ref[clear], 1))
+    assert np.array_equal(ids[clear], ids_ref[clear])
 
 
 def _fwd_once(cfg, ratio, mode, add_residual, dedup, Ns=0, seed=7):

@@ -1,6 +1,6 @@
 """compute-sanitizer over the library's code paths (scripts/sanitize_run.py: decode,
 CTA-pair prefill with the fused combine, fp32, tcgen05 router, shared experts,
-de-duplication, full brownout, TILED weights): no memory errors, no shared-memory
+de-duplication, full brownout, swapped tail tiles): no memory errors, no shared-memory
 races, no barrier misuse.  Logs of the round's runs: profiles/sanitizer_r01/."""
 import os
 import shutil

@@ -124,8 +124,8 @@ def test_shared_experts_ragged_T(T):
     assert _rel_err(_np(y), ref.y) <= OUT_TOL
 
 
-@pytest.mark.parametrize("env", [{"BO_GATHER": "1"}, {"BO_GEMM_CG": "1"}, {"BO_SPLITK": "1"}],
-                         ids=["gather4_gemm1", "single_cta_gemm", "splitk_gemm2"])
+@pytest.mark.parametrize("env", [{"BO_CTA_PAIRS": "0"}, {"BO_GEMM2_SPLITK": "1"}, {"BO_TILE_ALT": "0"}],
+                         ids=["single_cta_gemm", "splitk_gemm2", "no_tile_alt"])
 @pytest.mark.parametrize("cfg", [CFGS[0], CFGS[3]], ids=lambda c: c.name)
 def test_shared_experts_engine_variants(cfg, env, monkeypatch):
     for k, v in env.items():
