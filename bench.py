@@ -11,8 +11,8 @@ combine) over one batch of synthetic tokens already resident in HBM.  At N=1
 the workload is BASELINE.json configs[1]: the Mixtral-8x7B MoE layer (d 4096,
 f 14336, 8 experts, top-2, united groups of 4), prefill T = 4096, bf16, at
 brownout ratio 0.5 (the other ratios of the sweep are reported in
-"ratio_sweep").  For N > 1 (torchrun) every rank runs the same step on its own
-batch (weak scaling, replicas).
+"ratio_sweep").  For N > 1 (torchrun) the layer runs expert-parallel over the N
+ranks, each rank holding its own batch of T tokens (weak scaling).
 
 Rank 0 prints ONE JSON line.  --impl reference times the fp64 CPU oracle (the
 reference arm of this tier) on a bounded token sample of the same workload.
@@ -530,7 +530,7 @@ def main():
         "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (seeded; random-init Mixtral-shaped weights)",
         "config": {"workload": cfg.name, "T": cfg.T, "d": cfg.d, "f": cfg.f, "m": cfg.m, "K": cfg.K,
                    "way": cfg.way, "ratio": cfg.ratio, "mode": "partial", "sigma": cfg.sigma, "num_shared": cfg.Ns,
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "parallelism": "single",
                    "l2": "inputs larger than L2 (expert weights %.2f GB/step)" % (alg["weight_bytes"] / 1e9)},
         "roofline": roof,
         "step_roofline": {"tflops": step_tflops, "frac_bf16_sustained": step_tflops / pk["bf16_tflops_sustained"],
@@ -655,14 +655,20 @@ def main():
 
 
 def run_ep(args, cfg, rank, world, local, pk):
-    """N > 1: expert-parallel forward (paper_2507_17133_b200.ep) over NCCL.  Weak
-    scaling: every rank owns cfg.T tokens of the global batch (N x T tokens);
-    experts are sharded, united experts f-sliced over their group's ranks."""
+    """N > 1: expert-parallel forward (include/brownout.h bo_ep_*).
+    Weak scaling: every rank owns cfg.T tokens of the global batch (N x T tokens);
+    experts are sharded, united experts f-sliced over their group's ranks.  Over
+    NCCL the library owns the communicator and runs the whole forward in one call
+    (bo_ep_forward); with BO_DIST_BACKEND=gloo (test rigs: 2 ranks on 1 GPU) the
+    exchanges go through torch.distributed between the library's stage calls.
+    Batches of <= 2048 tokens per rank use fixed-capacity (padded) messages - no
+    host synchronisation, one CUDA graph per timed region; larger ones exact-size
+    messages (one device-to-host read of the 2R row counts per forward)."""
     import torch
     import torch.distributed as dist
     import synthetic as S
     from paper_2507_17133_b200 import BrownoutMoE
-    from paper_2507_17133_b200.ep import EPMoE, EPPlanner, TorchComm
+    from paper_2507_17133_b200.ep import EPContext, TorchComm, ep_forward_staged
 
     sizes = [64, 256, 1024, 4096, 16384] if not args.no_sweep else []
     tmax = max([cfg.T] + sizes)
@@ -670,54 +676,91 @@ def run_ep(args, cfg, rank, world, local, pk):
     moe = BrownoutMoE(cfg.d, cfg.f, cfg.m, cfg.K, cfg.way, dtype=cfg.dtype, max_tokens=tmax)
     moe.set_brownout(cfg.ratio)
     united = moe.build_united(lay["Wg"], lay["Wu"], lay["Wd"])
-    pl = EPPlanner(cfg.m, cfg.way, cfg.f, world)
-    ep = EPMoE(moe, pl, rank, (lay["Wg"], lay["Wu"], lay["Wd"]), united, cfg.d, cfg.K, S.torch_dtype(cfg.dtype))
+    nccl = dist.get_backend() == "nccl"
+    small_T = min(tmax, 4096 // cfg.K)
+    ctx_small = EPContext(moe, world, rank, small_T, padded=1)
+    ctx_big = EPContext(moe, world, rank, tmax, padded=0)
+    ex, un = ctx_big.local_weights((lay["Wg"], lay["Wu"], lay["Wd"]), united)
+    if nccl:   # the library's own communicators: rank 0's NCCL id shared over the process group
+        for c in (ctx_small, ctx_big):
+            uid = [EPContext.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            c.init_nccl(uid[0])
     comm = TorchComm()
     xg = S.make_tokens(cfg, T=tmax * world, device="cuda")
 
-    def timed(T, steps, warmup, timers=False):
+    def ctx_for(T):
+        return ctx_small if T <= small_T else ctx_big
+
+    def fwd(T, x, y=None):
+        c = ctx_for(T)
+        if nccl:
+            return c.forward(x, lay["Wr"], ex, un, y=y)
+        return ep_forward_staged(c, x, lay["Wr"], ex, un, comm)
+
+    def timed(T, steps, warmup, ffn_events=False):
         x = xg[rank * T:(rank + 1) * T].contiguous()
+        y = torch.empty_like(x)
         for _ in range(warmup):
-            ep.forward(x, lay["Wr"], comm)
+            fwd(T, x, y)
         torch.cuda.synchronize()
-        ffn = []
-        if timers:
-            ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(steps)]
+        graph = None
+        if nccl and ctx_for(T).padded:   # sync-free: K steps in one graph
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                for _ in range(steps):
+                    fwd(T, x, y)
+        ev = None
+        if ffn_events:   # the library records GEMM1 / GEMM2 boundaries of the rank-local grouped FFN
+            ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+            for e3 in ev:
+                for e in e3:
+                    e.record()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         dist.barrier()
         torch.cuda.synchronize()
         a.record()
-        for i in range(steps):
-            if timers:
-                ep.timers = ev[i]
-            ep.forward(x, lay["Wr"], comm)
+        if graph is not None:
+            graph.replay()
+        else:
+            for i in range(steps):
+                if ev:
+                    moe.set_profile_events(ev[i])
+                fwd(T, x, y)
         b.record()
         torch.cuda.synchronize()
-        ep.timers = None
+        moe.set_profile_events(None)
         ms = a.elapsed_time(b)
-        if timers:
-            ffn = [e[0].elapsed_time(e[1]) for e in ev]
+        ffn = [e3[0].elapsed_time(e3[2]) for e3 in ev] if ev else []
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item()) / steps, (sum(ffn) / len(ffn) if ffn else None)
 
     with ClockSampler(local) as clk:
-        ms_step, ffn_ms = timed(cfg.T, args.steps, max(args.warmup, 3), timers=True)
+        ms_step, ffn_ms = timed(cfg.T, args.steps, max(args.warmup, 3), ffn_events=True)
     clocks = clk.summary()
+    launches = moe.last_launch_count()
     value = world * cfg.T / (ms_step / 1e3)
-    ach = ep.last_ffn_flops / (ffn_ms / 1e3) / 1e12
-    roof = {"kernel": "expert_ffn (gemm1_swiglu + gemm2_weighted, rank-local executors)", "bound": "tensor",
-            "achieved": ach, "peak": pk["bf16_tflops_sustained"], "unit": "TFLOP/s",
-            "frac": ach / pk["bf16_tflops_sustained"], "peak_note": "sustained bf16; " + pk["source"],
-            "algorithmic_per_launch": ep.last_ffn_flops, "traffic": None}
+    c = ctx_for(cfg.T)
+    rows = c.local_rows()
+    n_o = c.info["e1"] - c.info["e0"]
+    ffn_flops = 6.0 * cfg.d * (cfg.f * sum(rows[:n_o]) + c.info["f_united"] * sum(rows[n_o:]))
+    ach = ffn_flops / (ffn_ms / 1e3) / 1e12 if ffn_ms else None
+    roof = {"kernel": "gemm1_swiglu + gemm2_weighted (rank-local executors)", "bound": "tensor",
+            "achieved": ach, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+            "frac": ach / pk["bf16_tflops"] if ach else None, "peak_note": "burst bf16; " + pk["source"],
+            "algorithmic_per_launch": ffn_flops, "traffic": None}
     out = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (seeded; random-init Mixtral-shaped weights)",
            "config": {"workload": cfg.name, "T_per_rank": cfg.T, "global_batch": cfg.T * world, "d": cfg.d,
                       "f": cfg.f, "m": cfg.m, "K": cfg.K, "way": cfg.way, "ratio": cfg.ratio,
-                      "parallelism": f"ep{world}", "united_f_slices": pl.n_slices,
+                      "parallelism": f"ep{world}", "united_f_slices": c.info["nrep"],
+                      "exchange": ("nccl (library-owned)" if nccl else "torch.distributed " + dist.get_backend())
+                                  + (", padded messages" if c.padded else ", exact-size messages"),
                       "l2": "inputs larger than L2 (expert weights)"},
-           "roofline": roof, "gpu_launches": 10 * args.steps, "clocks": clocks}
+           "roofline": roof, "gpu_launches": launches * args.steps,
+           "gpu_launch_names": moe.last_kernels(), "clocks": clocks}
     # e2e through the public API: pinned host tokens in, pinned host output back, every step
     x = xg[rank * cfg.T:(rank + 1) * cfg.T]
     hx = x.cpu().pin_memory()
@@ -725,7 +768,7 @@ def run_ep(args, cfg, rank, world, local, pk):
     dx = torch.empty_like(x)
     for _ in range(2):
         dx.copy_(hx, non_blocking=True)
-        hy.copy_(ep.forward(dx, lay["Wr"], comm), non_blocking=True)
+        hy.copy_(fwd(cfg.T, dx), non_blocking=True)
     torch.cuda.synchronize()
     dist.barrier()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -733,7 +776,7 @@ def run_ep(args, cfg, rank, world, local, pk):
     a.record()
     for _ in range(n_e2e):
         dx.copy_(hx, non_blocking=True)
-        hy.copy_(ep.forward(dx, lay["Wr"], comm), non_blocking=True)
+        hy.copy_(fwd(cfg.T, dx), non_blocking=True)
     b.record()
     torch.cuda.synchronize()
     t = torch.tensor([a.elapsed_time(b) / n_e2e], device="cuda", dtype=torch.float64)
@@ -746,7 +789,8 @@ def run_ep(args, cfg, rank, world, local, pk):
         sw = {}
         for T in sizes:
             ms, _ = timed(T, max(3, args.steps // 2), 2)
-            sw[str(T)] = {"tokens_per_s": world * T / (ms / 1e3), "ms": ms}
+            sw[str(T)] = {"tokens_per_s": world * T / (ms / 1e3), "ms": ms,
+                          "messages": "padded" if ctx_for(T).padded else "exact"}
         out["batch_sweep"] = sw
     if rank == 0:
         print(json.dumps(out), flush=True)

@@ -49,7 +49,7 @@ typedef enum {
   BO_ERR_SHAPE = 2,        /* hidden or ffn not a multiple of 64 (bf16) / 32 (fp32), m > 256, misaligned pointer */
   BO_ERR_UNSUPPORTED = 3,  /* dtype / mode / init not built */
   BO_ERR_CUDA = 4,         /* a CUDA runtime / driver call failed (message in bo_last_error) */
-  BO_ERR_NCCL = 5,         /* reserved for the expert-parallel path */
+  BO_ERR_NCCL = 5,         /* NCCL missing or a NCCL call failed (expert-parallel forward) */
   BO_ERR_WORKSPACE = 6     /* workspace null or smaller than bo_workspace_size() */
 } bo_status;
 
@@ -217,10 +217,9 @@ BO_API bo_status bo_plan_from_counts(bo_handle* h, const int32_t* counts, int32_
                               void* stream);
 
 /* ---------------------------------------------------------------------------
- * Building blocks of the expert-parallel forward:
- * the same stages as bo_moe_forward, exposed so that the exchange between
- * ranks (count all-gather, dispatch / combine all-to-all over NVLink) can sit
- * between them.  All pointers are device pointers; all calls are stream-ordered.
+ * Stage entry points of the forward (used by the expert-parallel forward below
+ * and available to callers that run the layer in pieces).  Device pointers,
+ * stream-ordered.
  * ------------------------------------------------------------------------- */
 
 /* a1-a4 on a local batch: router (Eq. 8), top-K (Eq. 7), per-tile histogram,
@@ -229,30 +228,6 @@ BO_API bo_status bo_plan_from_counts(bo_handle* h, const int32_t* counts, int32_
  * topk_id/topk_w, ...).  logits_in as in bo_moe_forward_ex. */
 BO_API bo_status bo_route(bo_handle* h, const void* x, int64_t T, const void* Wr, const float* logits_in,
                           void* workspace, size_t ws_bytes, void* stream);
-
-/* Alg. 1 on the column sums of counts [nrows, m] (int32; one row per
- * rank under expert parallelism, D18: one global plan; any 4-byte-aligned pointer).  Outputs as
- * bo_plan_from_counts (exec_off: >= 2*(E+1) + m int32, first E+1 meaningful). */
-BO_API bo_status bo_plan_counts(bo_handle* h, const int32_t* counts, int32_t nrows, int32_t* exec_of_expert,
-                                int32_t* expert_row_off, int32_t* exec_off, void* stats, void* stream);
-
-/* a5 with a caller-chosen row layout, for the batch of the last bo_route on this
- * handle (same T and workspace): the row of (token t, slot s, replica r), routed
- * to expert e, is row_base[e*nrep + r] + (stable rank of t among the batch's
- * tokens routed to e); row_base < 0 means "no row".  Writes rows_out[row] = x[t]
- * (d elements), w_out[row] = g[t,s] (Eq. 6 p/q) and row_of[(t*K + s)*nrep + r]
- * (-1 where no row).  nrep in [1, 8]. */
-BO_API bo_status bo_dispatch(bo_handle* h, int64_t T, void* workspace, size_t ws_bytes, const int32_t* row_base,
-                             int32_t nrep, const void* x, void* rows_out, float* w_out, int32_t* row_of,
-                             void* stream);
-
-/* Row-block permutation: for every dst row i with dst_start[b] <= i < dst_start[b+1]
- * (b < n_blocks, dst_start has n_blocks + 1 entries, dst_start[n_blocks] = total_rows)
- * dst[i] = src[src_off[b] + i - dst_start[b]] (row_bytes, multiple of 16) and,
- * if w_src != NULL, w_dst[i] = w_src[...]. */
-BO_API bo_status bo_block_copy(bo_handle* h, const void* src, void* dst, int32_t row_bytes, const float* w_src,
-                               float* w_dst, int32_t n_blocks, const int32_t* src_off, const int32_t* dst_start,
-                               int64_t total_rows, void* stream);
 
 /* a6-a7 on rows already grouped by executor: rows [R, d], row_w [R];
  * exec_off / mtile_off [n_orig + n_united + 1] (row offsets and prefix of
@@ -270,6 +245,129 @@ BO_API bo_status bo_expert_ffn(bo_handle* h, const void* rows, int64_t R, const 
  * in fp32, slot order then replica order (Eq. 5). */
 BO_API bo_status bo_combine(bo_handle* h, int64_t T, const void* rows, const int32_t* row_of, int32_t nrep,
                             const void* x, void* y, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Expert parallelism (the paper is silent on
+ * communication, its testbed is 4 x A100-PCIe).  One process per GPU,
+ * R ranks (1 <= R <= 8, one node).  Tokens are data-parallel: rank r holds its
+ * own batch of T_r <= max_tokens tokens (uneven, bursty sizes allowed).  Experts
+ * are sharded: original expert e lives on rank floor(e R / m); united expert j
+ * (group j) is f-sliced over the distinct owner ranks of its members when
+ * every group has the same number of them (SwiGLU is elementwise in f, so the
+ * slices' partial outputs add in the combine), else it lives whole on its first
+ * member's rank.
+ *
+ * The brownout plan is global (reading D18): every rank all-gathers the count
+ * rows [m + 4] of all ranks (cnt_i of its batch, then T_r, mode and the fp64
+ * ratio as two int32 halves), runs Alg. 1 on their sum with RANK 0's knob (so a
+ * per-rank SALC loop cannot make ranks disagree), and derives every exchange
+ * table on the device.  EP over R ranks therefore computes the single-GPU forward
+ * of the rank-order concatenated batch, bit for bit in routing and plan.
+ *
+ * Exchange buffers (rows of d elements, dtype of the handle, plus one float gate
+ * weight per row), all inside the caller's EP workspace:
+ *   send    this rank's rows ordered (destination rank, executor, expert, token)
+ *   recv    rows of every source, source-major
+ *   ret     (aliases recv) weighted FFN outputs in recv's layout, going back
+ *   back    (aliases send) outputs returned to this rank, in send's layout
+ * Padded mode: the message between every (source, destination) pair is `cap` =
+ * max_tokens * K rows at offset q * cap, whatever the plan - no host
+ * synchronisation and CUDA-graph capturable (the SURVEY's small-T mode).  Exact
+ * mode: messages carry only their rows, contiguous in rank order; the row counts
+ * (2R int64) are read by the host once per forward.
+ * ------------------------------------------------------------------------- */
+typedef struct bo_ep bo_ep;
+
+typedef struct {
+  int32_t world;         /* R, 1..8 */
+  int32_t rank;          /* this process's rank */
+  int32_t padded;        /* 1 padded, 0 exact, -1 auto: padded iff max_tokens * K <= 4096 */
+  int64_t max_tokens;    /* largest local batch (<= the handle's max_tokens) */
+} bo_ep_config;
+
+typedef struct {
+  int32_t world, rank, padded;
+  int32_t e0, e1;            /* local original experts [e0, e1) */
+  int32_t n_united_local;    /* united f-slices executed here (bo_ep_local_slices) */
+  int32_t f_united;          /* their width: ffn / slices per group */
+  int32_t nrep;              /* rows per delegated assignment (= slices per united expert) */
+  int32_t sliced;            /* 1: united experts f-sliced over their owner ranks */
+  int32_t n_exec;            /* virtual executors over all ranks (originals + united slices) */
+  int32_t n_local;           /* this rank's executors: (e1 - e0) originals, then n_united_local slices */
+  int64_t cap;               /* rows per (source, destination) message in padded mode: max_tokens * K */
+  int64_t rows_max;          /* rows of each exchange buffer: R * cap */
+} bo_ep_info;
+
+typedef struct {
+  size_t total_bytes;
+  size_t route;        /* the local route stage's bo_ws_layout workspace (its offsets are relative to here) */
+  size_t count_row;    /* int32 [m + 4]     this rank's all-gather input */
+  size_t gathered;     /* int32 [R, m + 4]  the all-gather output (every rank's row, rank order) */
+  size_t exec_of_expert, expert_row_off, plan_scratch, stats, counts;   /* global plan (Alg. 1) */
+  size_t tables;       /* int32 exchange tables (row_base, splits, block tables, exec_off, mtile_off) */
+  size_t splits;       /* int64 [2R]        rows sent to / received from each rank */
+  size_t send, send_w; /* [rows_max, d], float [rows_max]   (back aliases send) */
+  size_t recv, recv_w; /* [rows_max, d], float [rows_max]   (ret aliases recv) */
+  size_t grouped, grouped_w;   /* executor-major rows; the GEMM2 output overwrites grouped */
+  size_t h;            /* [rows_max, ffn] SwiGLU activations */
+  size_t row_of;       /* int32 [max_tokens, K, nrep] send / back row of (token, slot, replica), -1 none */
+  int64_t rows_max;
+} bo_ep_ws_layout;
+
+/* Static placement alone (host only, no GPU needed): the bo_ep_info fields of
+ * rank `rank` (cap / rows_max / padded zero).  BO_ERR_INVALID_ARG for world
+ * outside [1, 8] or rank outside [0, world); BO_ERR_SHAPE when the executors
+ * exceed the table limits (m <= 256, 512 virtual executors). */
+BO_API bo_status bo_ep_placement(int32_t num_experts, int32_t way, int32_t ffn, int32_t world, int32_t rank,
+                                 bo_ep_info* out);
+/* The (group, slice) of each local united slice, in executor order (n >= n_united_local). */
+BO_API bo_status bo_ep_placement_slices(int32_t num_experts, int32_t way, int32_t ffn, int32_t world, int32_t rank,
+                                        int32_t* group, int32_t* slice, int32_t n);
+
+/* An EP context on a layer handle (host state only; no device memory). */
+BO_API bo_status bo_ep_create(bo_handle* h, const bo_ep_config* cfg, bo_ep** out);
+BO_API bo_status bo_ep_destroy(bo_ep* ep);   /* also destroys the NCCL communicator of bo_ep_init */
+BO_API bo_status bo_ep_get_info(const bo_ep* ep, bo_ep_info* out);
+BO_API bo_status bo_ep_workspace_layout(const bo_ep* ep, bo_ep_ws_layout* out);
+
+/* Library-owned communicator: rank 0 calls bo_ep_nccl_unique_id and shares the
+ * 128 bytes with every rank (any side channel), then every rank calls bo_ep_init
+ * (collective, blocking until all R ranks have joined).  NCCL is loaded at run
+ * time (libnccl.so.2); BO_ERR_NCCL if it is missing or a call fails. */
+BO_API bo_status bo_ep_nccl_unique_id(unsigned char id[128]);
+BO_API bo_status bo_ep_init(bo_ep* ep, const unsigned char nccl_unique_id[128]);
+
+/* The whole EP forward over the library's communicator (after bo_ep_init):
+ * x [T, d] local tokens (T <= max_tokens), Wr [m, d]; local weights: originals
+ * Wg/Wu [e1-e0, f, d], Wd [e1-e0, d, f]; united slices (bo_ep_placement_slices
+ * order) UWg/UWu [n_united_local, f_united, d], UWd [n_united_local, d, f_united]
+ * (NULL when n_united_local == 0); y [T, d].  Padded mode: no host
+ * synchronisation, graph capturable.  Exact mode: one stream synchronisation. */
+BO_API bo_status bo_ep_forward(bo_ep* ep, const void* x, int64_t T, const void* Wr, const void* Wg, const void* Wu,
+                               const void* Wd, const void* UWg, const void* UWu, const void* UWd, void* y,
+                               void* workspace, size_t ws_bytes, void* stream);
+
+/* The same forward in stages, for callers that run the three exchanges
+ * themselves (e.g. torch.distributed):
+ *   bo_ep_route     a1-a3 on the local batch -> count_row
+ *   (all-gather count_row of every rank into gathered)
+ *   bo_ep_dispatch  global Alg. 1, exchange tables, permutation + gather of the
+ *                   local rows into send / send_w (a5)
+ *   bo_ep_splits    rows per (this rank -> q) and (r -> this rank): exact mode
+ *                   reads them (stream synchronisation), padded mode returns cap
+ *   (all-to-all send -> recv, send_w -> recv_w with those splits)
+ *   bo_ep_compute   regroup, grouped SwiGLU GEMMs x gate weight (a6-a7), back to
+ *                   recv's layout in ret
+ *   (all-to-all ret -> back, splits swapped)
+ *   bo_ep_combine   y_t = [x_t] + sum over slots and slices (a8, Eq. 5) */
+BO_API bo_status bo_ep_route(bo_ep* ep, const void* x, int64_t T, const void* Wr, const float* logits_in,
+                             void* workspace, size_t ws_bytes, void* stream);
+BO_API bo_status bo_ep_dispatch(bo_ep* ep, const void* x, void* workspace, size_t ws_bytes, void* stream);
+BO_API bo_status bo_ep_splits(bo_ep* ep, void* workspace, size_t ws_bytes, int64_t* send_rows, int64_t* recv_rows,
+                              void* stream);
+BO_API bo_status bo_ep_compute(bo_ep* ep, const void* Wg, const void* Wu, const void* Wd, const void* UWg,
+                               const void* UWu, const void* UWd, void* workspace, size_t ws_bytes, void* stream);
+BO_API bo_status bo_ep_combine(bo_ep* ep, const void* x, void* y, void* workspace, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------
  * United-expert distillation (paper §4.2, Eq. 4 at P:152; SURVEY

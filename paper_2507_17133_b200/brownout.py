@@ -28,7 +28,10 @@ EXPORTED = (
     "bo_create", "bo_destroy", "bo_workspace_size", "bo_workspace_layout", "bo_build_united", "bo_set_shared_experts",
     "bo_set_engine_option", "bo_get_engine_option",
     "bo_set_brownout", "bo_get_brownout", "bo_moe_forward", "bo_moe_forward_ex", "bo_plan_from_counts",
-    "bo_route", "bo_plan_counts", "bo_dispatch", "bo_block_copy", "bo_expert_ffn", "bo_combine",
+    "bo_route", "bo_expert_ffn", "bo_combine",
+    "bo_ep_placement", "bo_ep_placement_slices", "bo_ep_create", "bo_ep_destroy", "bo_ep_get_info",
+    "bo_ep_workspace_layout", "bo_ep_nccl_unique_id", "bo_ep_init", "bo_ep_forward", "bo_ep_route",
+    "bo_ep_dispatch", "bo_ep_splits", "bo_ep_compute", "bo_ep_combine",
     "bo_set_profile_events", "bo_last_launch_count", "bo_last_kernels", "bo_status_string", "bo_last_error", "bo_version",
     "bo_distill_workspace_layout", "bo_distill_prepare", "bo_distill_load_united", "bo_distill_step",
 )
@@ -62,6 +65,22 @@ class bo_distill_layout(C.Structure):
                                           "off_tok", "off_teach", "off_f", "off_d")] + [("N", C.c_int64)]
 
 
+class bo_ep_config(C.Structure):
+    _fields_ = [("world", C.c_int32), ("rank", C.c_int32), ("padded", C.c_int32), ("max_tokens", C.c_int64)]
+
+
+class bo_ep_info(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("world", "rank", "padded", "e0", "e1", "n_united_local", "f_united", "nrep",
+                                         "sliced", "n_exec", "n_local")] + [("cap", C.c_int64), ("rows_max", C.c_int64)]
+
+
+class bo_ep_ws_layout(C.Structure):
+    _fields_ = [(n, C.c_size_t) for n in ("total_bytes", "route", "count_row", "gathered", "exec_of_expert",
+                                          "expert_row_off", "plan_scratch", "stats", "counts", "tables", "splits",
+                                          "send", "send_w", "recv", "recv_w", "grouped", "grouped_w", "h",
+                                          "row_of")] + [("rows_max", C.c_int64)]
+
+
 class BrownoutError(RuntimeError):
     def __init__(self, status: int, msg: str):
         super().__init__(f"{msg} (status {status})")
@@ -89,9 +108,20 @@ def _load():
         "bo_moe_forward_ex": ([vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp, vp], C.c_int),
         "bo_plan_from_counts": ([vp, vp, vp, vp, vp, vp, vp], C.c_int),
         "bo_route": ([vp, vp, i64, vp, vp, vp, C.c_size_t, vp], C.c_int),
-        "bo_plan_counts": ([vp, vp, i32, vp, vp, vp, vp, vp], C.c_int),
-        "bo_dispatch": ([vp, i64, vp, C.c_size_t, vp, i32, vp, vp, vp, vp, vp], C.c_int),
-        "bo_block_copy": ([vp, vp, vp, i32, vp, vp, i32, vp, vp, i64, vp], C.c_int),
+        "bo_ep_placement": ([i32, i32, i32, i32, i32, C.POINTER(bo_ep_info)], C.c_int),
+        "bo_ep_placement_slices": ([i32, i32, i32, i32, i32, vp, vp, i32], C.c_int),
+        "bo_ep_create": ([vp, C.POINTER(bo_ep_config), C.POINTER(vp)], C.c_int),
+        "bo_ep_destroy": ([vp], C.c_int),
+        "bo_ep_get_info": ([vp, C.POINTER(bo_ep_info)], C.c_int),
+        "bo_ep_workspace_layout": ([vp, C.POINTER(bo_ep_ws_layout)], C.c_int),
+        "bo_ep_nccl_unique_id": ([vp], C.c_int),
+        "bo_ep_init": ([vp, vp], C.c_int),
+        "bo_ep_forward": ([vp, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp], C.c_int),
+        "bo_ep_route": ([vp, vp, i64, vp, vp, vp, C.c_size_t, vp], C.c_int),
+        "bo_ep_dispatch": ([vp, vp, vp, C.c_size_t, vp], C.c_int),
+        "bo_ep_splits": ([vp, vp, C.c_size_t, vp, vp, vp], C.c_int),
+        "bo_ep_compute": ([vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp], C.c_int),
+        "bo_ep_combine": ([vp, vp, vp, vp, C.c_size_t, vp], C.c_int),
         "bo_expert_ffn": ([vp, vp, i64, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
         "bo_combine": ([vp, i64, vp, vp, i32, vp, vp, vp], C.c_int),
         "bo_set_profile_events": ([vp, C.POINTER(vp), i32], C.c_int),
@@ -338,35 +368,6 @@ class BrownoutMoE:
         ws = workspace if workspace is not None else self.workspace(T, x.device)
         _check(_lib.bo_route(self._h, _ptr(x), T, _ptr(Wr), _ptr(logits), _ptr(ws), ws.numel(), _stream(stream)))
         return ws
-
-    def local_counts(self, T, workspace=None):
-        return self.debug_arrays(T, workspace)["counts"]
-
-    def plan_counts(self, counts: torch.Tensor, stream=None):
-        """Alg. 1 on the column sums of counts [nrows, m] (int32, device)."""
-        m = self.cfg.num_experts
-        dev = counts.device
-        counts = counts.reshape(-1, m).contiguous()
-        exec_of = torch.empty(m, dtype=torch.int32, device=dev)
-        erow = torch.empty(m, dtype=torch.int32, device=dev)
-        eoff = torch.empty(2 * (self.E + 1) + m, dtype=torch.int32, device=dev)
-        stats = torch.empty(8, dtype=torch.int64, device=dev)
-        _check(_lib.bo_plan_counts(self._h, _ptr(counts), counts.shape[0], _ptr(exec_of), _ptr(erow), _ptr(eoff),
-                                   _ptr(stats), _stream(stream)))
-        return {"exec_of_expert": exec_of, "expert_row_off": erow, "exec_off": eoff[:self.E + 1], "stats": stats}
-
-    def dispatch(self, T, row_base, nrep, x, rows_out, w_out, row_of, workspace=None, stream=None):
-        ws = self._ws if workspace is None else workspace
-        _check(_lib.bo_dispatch(self._h, T, _ptr(ws), ws.numel(), _ptr(row_base), nrep, _ptr(x), _ptr(rows_out),
-                                _ptr(w_out), _ptr(row_of), _stream(stream)))
-
-    def block_copy(self, src, dst, src_off, dst_start, w_src=None, w_dst=None, stream=None):
-        rows = dst.shape[0]
-        if rows == 0:
-            return
-        row_bytes = dst[0].numel() * dst.element_size()
-        _check(_lib.bo_block_copy(self._h, _ptr(src), _ptr(dst), row_bytes, _ptr(w_src), _ptr(w_dst),
-                                  src_off.numel(), _ptr(src_off), _ptr(dst_start), rows, _stream(stream)))
 
     def expert_ffn(self, rows, row_w, exec_off, mtile_off, n_orig, n_united, f_united, experts, united, h_buf, out,
                    stream=None):

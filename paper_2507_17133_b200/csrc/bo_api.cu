@@ -104,7 +104,7 @@ int router_bn(int m) {
 int gemm2_bn(int d) { return d % 256 == 0 ? 256 : d % 128 == 0 ? 128 : 64; }
 int gemm1_bn(int f) { return f % 128 == 0 ? 256 : 128; }   // gate + up columns
 
-bo_status compute_layout(const bo_handle* h, int64_t T, bo_ws_layout* L) {
+bo_status compute_layout(const bo_handle* h, int64_t T, bo_ws_layout* L, bool route_only) {
   const bo_config& c = h->cfg;
   const int64_t m = c.num_experts, K = c.top_k, d = c.hidden, f = c.ffn;
   const int64_t G = (m + c.way - 1) / c.way, Ns = c.num_shared, E = m + G + Ns;
@@ -134,14 +134,15 @@ bo_status compute_layout(const bo_handle* h, int64_t T, bo_ws_layout* L) {
   L->row_of = take(sizeof(int32_t) * R);
   L->row_tok = take(sizeof(int32_t) * R);
   L->row_w = take(sizeof(float) * R);
-  L->xp = take(static_cast<size_t>(eb) * R * d);
-  L->h = take(static_cast<size_t>(eb) * R * f);
-  L->yp = take(static_cast<size_t>(eb) * R * d);
-  L->partial = take(R <= kSplitRows ? sizeof(float) * kSplitMax * R * d : 0);
-  L->tile_xcnt = take(c.dedup_united ? sizeof(int32_t) * ntiles * (m + G) : 0);
-  L->tile_xbase = take(c.dedup_united ? sizeof(int32_t) * ntiles * (m + G) : 0);
+  const int64_t Rf = route_only ? 0 : R;   // route-only (expert parallelism): no FFN buffers
+  L->xp = take(static_cast<size_t>(eb) * Rf * d);
+  L->h = take(static_cast<size_t>(eb) * Rf * f);
+  L->yp = take(static_cast<size_t>(eb) * Rf * d);
+  L->partial = take(Rf > 0 && Rf <= kSplitRows ? sizeof(float) * kSplitMax * Rf * d : 0);
+  L->tile_xcnt = take(c.dedup_united && !route_only ? sizeof(int32_t) * ntiles * (m + G) : 0);
+  L->tile_xbase = take(c.dedup_united && !route_only ? sizeof(int32_t) * ntiles * (m + G) : 0);
   L->ksplit = take(sizeof(int32_t));
-  L->comb_cnt = take(sizeof(int32_t) * T * (d / gemm2_bn(static_cast<int>(d))));
+  L->comb_cnt = take(route_only ? 0 : sizeof(int32_t) * T * (d / gemm2_bn(static_cast<int>(d))));
   L->total_bytes = off;
   L->T = T;
   L->ntiles = ntiles;
@@ -1156,61 +1157,6 @@ bo_status bo_route(bo_handle* h, const void* x, int64_t T, const void* Wr, const
   Prof prof(h, s, 1 << 30);
   int launches = 0, tile = 0;
   return route_stage(h, x, T, Wr, logits_in, workspace, L, s, prof, launches, tile);
-}
-
-bo_status bo_plan_counts(bo_handle* h, const int32_t* counts, int32_t nrows, int32_t* exec_of_expert,
-                         int32_t* expert_row_off, int32_t* exec_off, void* stats, void* stream) {
-  if (!h || !counts || !exec_of_expert || !expert_row_off || !exec_off || !stats || nrows < 1)
-    return fail(BO_ERR_INVALID_ARG, "null argument or nrows < 1");
-  const bo_config& c = h->cfg;
-  const int m = c.num_experts;
-  const int E = m + (m + c.way - 1) / c.way;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  int32_t* mtile_scratch = exec_off + (E + 1);   // exec_off holds 2*(E+1) + m ints (brownout.h)
-  int32_t* counts_out = mtile_scratch + (E + 1);
-  BO_CUDA(bo::launch_plan(counts, nrows, m, c.way, h->ratio, h->mode, nullptr, counts_out, exec_of_expert,
-                          expert_row_off, exec_off, mtile_scratch, static_cast<int64_t*>(stats), s),
-          "plan_counts");
-  return BO_OK;
-}
-
-bo_status bo_dispatch(bo_handle* h, int64_t T, void* workspace, size_t ws_bytes, const int32_t* row_base,
-                      int32_t nrep, const void* x, void* rows_out, float* w_out, int32_t* row_of, void* stream) {
-  if (!h) return fail(BO_ERR_INVALID_ARG, "null handle");
-  if (T != h->route_T) return fail(BO_ERR_INVALID_ARG, "bo_dispatch T=%lld differs from the last bo_route (T=%lld)",
-                                   static_cast<long long>(T), static_cast<long long>(h->route_T));
-  if (nrep < 1 || nrep > 8) return fail(BO_ERR_INVALID_ARG, "nrep %d outside [1, 8]", nrep);
-  if (h->cfg.dedup_united) return fail(BO_ERR_UNSUPPORTED, "dedup_united is single-GPU only");
-  if (h->cfg.num_shared) return fail(BO_ERR_UNSUPPORTED, "shared experts are single-GPU only (bo_moe_forward)");
-  if (T == 0) return BO_OK;
-  if (!row_base || !x || !rows_out || !w_out || !row_of) return fail(BO_ERR_INVALID_ARG, "null argument");
-  bo_ws_layout L;
-  bo_status st;
-  if ((st = check_ws(h, T, workspace, ws_bytes, &L)) != BO_OK) return st;
-  if (!aligned16(x) || !aligned16(rows_out)) return fail(BO_ERR_SHAPE, "x / rows_out must be 16-byte aligned");
-  const bo_config& c = h->cfg;
-  const int dt = c.dtype == BO_BF16 ? 0 : 1;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  BO_CUDA(bo::launch_permute(at<int32_t>(workspace, L.topk_id), at<float>(workspace, L.topk_w), static_cast<int>(T),
-                             c.top_k, c.num_experts, h->route_tile, at<int32_t>(workspace, L.tile_base), row_base,
-                             nrep, row_of, nullptr, w_out, s, dt, x, rows_out, c.hidden),
-          "dispatch permute + gather");
-  return BO_OK;
-}
-
-bo_status bo_block_copy(bo_handle* h, const void* src, void* dst, int32_t row_bytes, const float* w_src,
-                        float* w_dst, int32_t n_blocks, const int32_t* src_off, const int32_t* dst_start,
-                        int64_t total_rows, void* stream) {
-  if (!h) return fail(BO_ERR_INVALID_ARG, "null handle");
-  if (total_rows == 0) return BO_OK;
-  if (!src || !dst || !src_off || !dst_start || n_blocks < 1 || (w_src && !w_dst))
-    return fail(BO_ERR_INVALID_ARG, "null argument");
-  if (row_bytes <= 0 || row_bytes % 16 || !aligned16(src) || !aligned16(dst))
-    return fail(BO_ERR_SHAPE, "rows must be 16-byte multiples and 16-byte aligned");
-  BO_CUDA(bo::launch_block_copy(src, dst, row_bytes, w_src, w_dst, n_blocks, src_off, dst_start, total_rows,
-                                h->num_sms, static_cast<cudaStream_t>(stream)),
-          "block_copy");
-  return BO_OK;
 }
 
 bo_status bo_expert_ffn(bo_handle* h, const void* rows, int64_t R, const float* row_w, const int32_t* exec_off,

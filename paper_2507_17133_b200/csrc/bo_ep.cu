@@ -1,31 +1,215 @@
-// bo_ep.cu - row-block permutation used by the expert-parallel exchange.
-//
-// Under expert parallelism rows arrive from every source rank
-// ordered (source, executor, expert, token); the grouped GEMMs need them
-// ordered (executor, source, expert, token), and the results go back the
-// other way.  Both are block permutations whose block tables the host derives
-// from the all-gathered counts; this kernel moves the rows (16-byte vectors,
-// warp per row) and the per-row gate weight that travels with them.
+// bo_ep.cu - device side of the expert-parallel exchange:
+// the per-forward exchange tables computed from the all-gathered counts (no host
+// round trip), and the row-block permutation between the exchange layout
+// (source, executor, expert, token) and the grouped GEMMs' layout (executor,
+// source, expert, token).
 #include "bo_kernels.h"
 #include "bo_ptx.cuh"
 
 namespace bo {
 
+// Exclusive scan of in[0, n) into out[0, n) by one warp (chunks of 32, shuffle scan
+// plus carry); returns the total.  in / out may alias.
+__device__ int warp_excl_scan(const int* in, int* out, int n, int lane) {
+  int carry = 0;
+  for (int i0 = 0; i0 < n; i0 += 32) {
+    const int i = i0 + lane;
+    const int v = i < n ? in[i] : 0;
+    int incl = v;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int o = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += o;
+    }
+    __syncwarp();
+    if (i < n) out[i] = carry + incl - v;
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+    __syncwarp();
+  }
+  return carry;
+}
+
+// One CTA.  gathered [R, ld] count rows (this forward's counts of every rank, D18),
+// exec_of_expert [m] of the global plan.  Writes the tables of EpTables (bo_kernels.h).
+__global__ void __launch_bounds__(512) k_ep_tables(const __grid_constant__ EpStatic st,
+                                                   const int32_t* __restrict__ gathered, int ld,
+                                                   const int32_t* __restrict__ exec_of, EpTables tb) {
+  __shared__ int s_exec[kMaxExperts];
+  __shared__ int s_rows[kEpMaxRanks * kEpMaxV];   // rows[r][v]
+  __shared__ int s_pre[kEpMaxV];                  // send prefix over v (this rank as source)
+  __shared__ int s_base[kEpMaxV];
+  __shared__ int s_flat[kEpMaxRanks * kEpMaxV];   // scratch for (i, r) / (r, i) scans
+  const int R = st.R, m = st.m, V = st.V, nl = st.nl, me = st.rank;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < m; e += blockDim.x) s_exec[e] = exec_of[e];
+  __syncthreads();
+  // rows[r][v]: assignments of source r's batch that virtual executor v processes
+  for (int i = tid; i < R * V; i += blockDim.x) {
+    const int r = i / V, v = i - r * V;
+    const int code = st.vexec[v];
+    const int idx = code & 0xffff;
+    int rows = 0;
+    if (((code >> 23) & 1) == 0) {   // original expert idx: its own rows when it executes as itself
+      rows = s_exec[idx] == idx ? gathered[r * ld + idx] : 0;
+    } else {                          // slice of united expert idx: every member delegated to it
+      const int e1 = min((idx + 1) * st.way, m);
+      for (int e = idx * st.way; e < e1; ++e)
+        if (s_exec[e] == m + idx) rows += gathered[r * ld + e];
+    }
+    s_rows[i] = rows;
+  }
+  __syncthreads();
+  // source side (r = me): segment of each v in the send buffer
+  if (warp == 0) {
+    warp_excl_scan(s_rows + me * V, s_pre, V, lane);
+    for (int v = lane; v < V; v += 32) {
+      const int q = (st.vexec[v] >> 24) & 0xff;
+      s_base[v] = st.padded ? static_cast<int>(q * st.cap) + s_pre[v] - s_pre[st.vfirst[q]] : s_pre[v];
+    }
+  }
+  if (warp == 1) {   // rows this rank sends to q
+    for (int q = lane; q < R; q += 32) {
+      int n = 0;
+      for (int v = st.vfirst[q]; v < st.vfirst[q + 1]; ++v) n += s_rows[me * V + v];
+      tb.send_rows[q] = n;
+      tb.splits[q] = n;
+    }
+  }
+  if (warp == 2) {   // rows q receives from each source r (this rank as destination)
+    for (int r = lane; r < R; r += 32) {
+      int n = 0;
+      for (int i = 0; i < nl; ++i) n += s_rows[r * V + st.local_v[i]];
+      tb.recv_rows[r] = n;
+      tb.splits[R + r] = n;
+    }
+  }
+  __syncthreads();
+  // row_base[e * nrep + rep] (dispatch of this rank's assignments)
+  for (int e = tid; e < m; e += blockDim.x) {
+    const int x = s_exec[e];
+    for (int rep = 0; rep < st.nrep; ++rep) tb.row_base[e * st.nrep + rep] = -1;
+    if (x >= 0 && x < m) {
+      tb.row_base[e * st.nrep] = s_base[st.v_of_orig[e]];
+    } else if (x >= m) {
+      const int j = x - m;
+      int acc = 0;   // earlier members of the same united executor (member order, D11)
+      for (int e2 = j * st.way; e2 < e; ++e2)
+        if (s_exec[e2] == x) acc += gathered[me * ld + e2];
+      for (int sl = 0; sl < st.nslices; ++sl) tb.row_base[e * st.nrep + sl] = s_base[st.v_of_slice[j * st.nrep + sl]] + acc;
+    }
+  }
+  // destination side: receive offsets recv_blk[r][i] (r, i order) and grouped offsets (i, r order)
+  __shared__ int s_rbase[kEpMaxRanks + 1];
+  if (warp == 0) {
+    // source segment starts: exact = prefix of recv_rows, padded = r * cap
+    int run = 0;
+    for (int r = 0; r < R; ++r) {
+      if (lane == 0) s_rbase[r] = st.padded ? static_cast<int>(r * st.cap) : run;
+      int n = 0;
+      for (int i = lane; i < nl; i += 32) n += s_rows[r * V + st.local_v[i]];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) n += __shfl_xor_sync(0xffffffffu, n, off);
+      run += n;
+    }
+    if (lane == 0) s_rbase[R] = st.padded ? static_cast<int>(R * st.cap) : run;
+  }
+  __syncthreads();
+  // (r, i) order: inverse-table destinations = receive layout
+  for (int k = tid; k < R * nl; k += blockDim.x) {
+    const int r = k / nl, i = k - r * nl;
+    s_flat[k] = s_rows[r * V + st.local_v[i]];
+  }
+  __syncthreads();
+  if (warp == 0) {
+    for (int r = 0; r < R; ++r) warp_excl_scan(s_flat + r * nl, s_flat + r * nl, nl, lane);
+  }
+  __syncthreads();
+  for (int k = tid; k < R * nl; k += blockDim.x) {
+    const int r = k / nl, i = k - r * nl;
+    tb.inv_dst[k] = s_rbase[r] + s_flat[k];       // recv_blk[r][i]
+    tb.fwd_src[i * R + r] = s_rbase[r] + s_flat[k];
+    const int len = s_rows[r * V + st.local_v[i]];
+    tb.inv_len[k] = len;
+    tb.fwd_len[i * R + r] = len;
+  }
+  __syncthreads();
+  // (i, r) order: grouped layout (executor-major, then source)
+  for (int k = tid; k < R * nl; k += blockDim.x) {
+    const int i = k / R, r = k - i * R;
+    s_flat[k] = s_rows[r * V + st.local_v[i]];
+  }
+  __syncthreads();
+  int total = 0;
+  if (warp == 0) total = warp_excl_scan(s_flat, s_flat, R * nl, lane);
+  __syncthreads();
+  for (int k = tid; k < R * nl; k += blockDim.x) {
+    const int i = k / R, r = k - i * R;
+    tb.fwd_dst[k] = s_flat[k];
+    tb.inv_src[r * nl + i] = s_flat[k];
+  }
+  if (warp == 0) {
+    // executor row offsets and the m-tile prefix of the local grouped GEMMs
+    int carry = 0, mcarry = 0;
+    for (int i0 = 0; i0 < nl; i0 += 32) {
+      const int i = i0 + lane;
+      int rows = 0;
+      if (i < nl)
+        for (int r = 0; r < R; ++r) rows += s_rows[r * V + st.local_v[i]];
+      int a = rows, b = (rows + kBM - 1) / kBM;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int oa = __shfl_up_sync(0xffffffffu, a, off), ob = __shfl_up_sync(0xffffffffu, b, off);
+        if (lane >= off) { a += oa; b += ob; }
+      }
+      if (i < nl) {
+        tb.exec_off[i] = carry + a - rows;
+        tb.mtile_off[i] = mcarry + b - (rows + kBM - 1) / kBM;
+      }
+      carry += __shfl_sync(0xffffffffu, a, 31);
+      mcarry += __shfl_sync(0xffffffffu, b, 31);
+    }
+    if (lane == 0) {
+      tb.exec_off[nl] = carry;
+      tb.mtile_off[nl] = mcarry;
+      tb.fwd_dst[R * nl] = total;
+      tb.inv_dst[R * nl] = s_rbase[R];
+      tb.totals[0] = total;         // grouped rows
+      tb.totals[1] = s_rbase[R];    // receive-layout extent
+    }
+  }
+}
+
+cudaError_t launch_ep_tables(const EpStatic& st, const int32_t* gathered, int ld, const int32_t* exec_of,
+                             const EpTables& tb, cudaStream_t s) {
+  k_ep_tables<<<1, 512, 0, s>>>(st, gathered, ld, exec_of, tb);
+  return cudaGetLastError();
+}
+
+// Row-block copy: block b moves len[b] rows src_off[b] + k -> dst_start[b] + k
+// (dst_start ascending; rows of the destination no block covers are left alone),
+// with the float weight that travels with each row when w_src != nullptr.  The
+// destination extent is read on the device (*extent, capped at extent_max).
 __global__ void __launch_bounds__(256) k_block_copy(const uint4* __restrict__ src, uint4* __restrict__ dst,
                                                     int vec_per_row, const float* __restrict__ w_src,
                                                     float* __restrict__ w_dst, int n_blocks,
+                                                    const int32_t* __restrict__ dst_start,
+                                                    const int32_t* __restrict__ len,
                                                     const int32_t* __restrict__ src_off,
-                                                    const int32_t* __restrict__ dst_start, int64_t total_rows) {
+                                                    const int32_t* __restrict__ extent, int64_t extent_max) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t i = gw; i < total_rows; i += nw) {
-    int lo = 0, hi = n_blocks;   // dst_start[lo] <= i < dst_start[hi]
+  int64_t total = extent ? static_cast<int64_t>(*extent) : extent_max;
+  total = total < extent_max ? total : extent_max;
+  for (int64_t i = gw; i < total; i += nw) {
+    int lo = 0, hi = n_blocks;   // last block with dst_start[lo] <= i
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
       if (dst_start[mid] <= i) lo = mid; else hi = mid;
     }
-    const int64_t srow = static_cast<int64_t>(src_off[lo]) + (i - dst_start[lo]);
+    const int64_t k = i - dst_start[lo];
+    if (k < 0 || k >= len[lo]) continue;
+    const int64_t srow = static_cast<int64_t>(src_off[lo]) + k;
     const uint4* sp = src + srow * vec_per_row;
     uint4* dp = dst + i * vec_per_row;
     for (int c = lane; c < vec_per_row; c += 32) dp[c] = __ldg(sp + c);
@@ -34,14 +218,14 @@ __global__ void __launch_bounds__(256) k_block_copy(const uint4* __restrict__ sr
 }
 
 cudaError_t launch_block_copy(const void* src, void* dst, int row_bytes, const float* w_src, float* w_dst,
-                              int n_blocks, const int32_t* src_off, const int32_t* dst_start, int64_t total_rows,
-                              int num_sms, cudaStream_t s) {
-  if (total_rows <= 0 || n_blocks <= 0) return cudaSuccess;
-  int64_t blocks = (total_rows + 7) / 8;
+                              int n_blocks, const int32_t* dst_start, const int32_t* len, const int32_t* src_off,
+                              const int32_t* extent, int64_t extent_max, int num_sms, cudaStream_t s) {
+  if (extent_max <= 0 || n_blocks <= 0) return cudaSuccess;
+  int64_t blocks = (extent_max + 7) / 8;
   if (blocks > num_sms * 8) blocks = num_sms * 8;
   k_block_copy<<<static_cast<int>(blocks), 256, 0, s>>>(static_cast<const uint4*>(src), static_cast<uint4*>(dst),
-                                                        row_bytes / 16, w_src, w_dst, n_blocks, src_off, dst_start,
-                                                        total_rows);
+                                                        row_bytes / 16, w_src, w_dst, n_blocks, dst_start, len,
+                                                        src_off, extent, extent_max);
   return cudaGetLastError();
 }
 
@@ -60,23 +244,34 @@ namespace bo {
 __global__ void __launch_bounds__(256) k_dedup_count(const int32_t* __restrict__ topk_id, int T, int K, int tile,
                                                      int E, const int32_t* __restrict__ exec_of,
                                                      int32_t* __restrict__ tile_xcnt) {
-  __shared__ int hist[kMaxExec];
-  for (int i = threadIdx.x; i < E; i += blockDim.x) hist[i] = 0;
+  // per-warp counts without atomics: the lanes holding the same executor meet in
+  // __match_any_sync and the lowest of them adds the group's size to its warp's row
+  __shared__ int hist[8][kMaxExec];
+  for (int i = threadIdx.x; i < 8 * kMaxExec; i += blockDim.x) (&hist[0][0])[i] = 0;
   __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t0 = blockIdx.x * tile;
   const int t1 = min(t0 + tile, T);
-  for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+  for (int tb = t0; tb < t1; tb += blockDim.x) {   // warp-uniform trip count
+    const int t = tb + threadIdx.x;
     int xs[16];
     for (int s = 0; s < K; ++s) {
-      const int x = exec_of[__ldg(topk_id + static_cast<int64_t>(t) * K + s)];
+      const int x = t < t1 ? exec_of[__ldg(topk_id + static_cast<int64_t>(t) * K + s)] : -1;
       xs[s] = x;
       bool dup = false;
       for (int q = 0; q < s; ++q) dup |= xs[q] == x;
-      if (x >= 0 && !dup) atomicAdd(&hist[x], 1);   // integer count: order-independent
+      const int key = (x >= 0 && !dup) ? x : -1;
+      const uint32_t peers = __match_any_sync(0xffffffffu, key);
+      if (key >= 0 && lane == __ffs(peers) - 1) hist[warp][key] += __popc(peers);
+      __syncwarp();
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < E; i += blockDim.x) tile_xcnt[static_cast<int64_t>(blockIdx.x) * E + i] = hist[i];
+  for (int i = threadIdx.x; i < E; i += blockDim.x) {
+    int c = 0;
+    for (int w = 0; w < 8; ++w) c += hist[w][i];
+    tile_xcnt[static_cast<int64_t>(blockIdx.x) * E + i] = c;
+  }
 }
 
 // One CTA: per-executor prefix over tiles, executor row offsets, m-tile prefix,

@@ -121,7 +121,7 @@ struct CombFuse {
 };
 
 // Workspace layout of a forward over T tokens (bo_ws_layout) and its check.
-bo_status compute_layout(const bo_handle* h, int64_t T, bo_ws_layout* L);
+bo_status compute_layout(const bo_handle* h, int64_t T, bo_ws_layout* L, bool route_only = false);
 bo_status check_ws(const bo_handle* h, int64_t T, void* ws, size_t ws_bytes, bo_ws_layout* L);
 // a1-a4 (router, top-K, histogram, Alg. 1 on the local counts); `tile` = token tile used.
 bo_status route_stage(bo_handle* h, const void* x, int64_t T, const void* Wr, const float* logits_in, void* ws,

@@ -139,11 +139,45 @@ cudaError_t launch_gather(int dtype, const void* x, int T, int d, int KR, const 
 cudaError_t launch_combine(int dtype, const void* yp, const void* x, int T, int d, int KR,
                            const int32_t* row_of, int add_residual, void* y, int num_sms, cudaStream_t s);
 
-// Row-block permutation: dst row i lies in block b (dst_start[b] <= i < dst_start[b+1]) and
-// copies src row src_off[b] + (i - dst_start[b]) (and its float weight if w_src != nullptr).
+// ---- expert parallelism (bo_ep.cu)
+constexpr int kEpMaxRanks = 8;     // one node
+constexpr int kEpMaxV = 512;       // virtual executors (originals + united f-slices, all ranks)
+// Static placement of one rank (kernel parameter image).  vexec[v] packs rank (bits
+// 24-31), kind (bit 23: 1 = united slice), idx (bits 0-15: expert or group); virtual
+// executors are rank-major, vfirst[q] the first of rank q.
+struct EpStatic {
+  int R, rank, m, way, nrep, nslices, V, nl, padded;
+  int64_t cap;                      // rows per (source, destination) message in padded mode
+  int32_t vexec[kEpMaxV];
+  int32_t vfirst[kEpMaxRanks + 1];
+  int32_t v_of_orig[kMaxExperts];
+  int32_t v_of_slice[kEpMaxV];      // [group * nrep + slice]
+  int32_t local_v[kEpMaxV];         // this rank's executors in GEMM order (originals, then slices)
+};
+// Per-forward tables (device int32 arrays in the EP workspace).
+struct EpTables {
+  int32_t* row_base;    // [m * nrep]   send position of expert e's first row (replica rep), -1 none
+  int32_t* send_rows;   // [R]          rows this rank sends to each rank
+  int32_t* recv_rows;   // [R]          rows this rank receives from each rank
+  int32_t* fwd_dst;     // [nl*R + 1]   receive -> grouped blocks, (executor, source) order
+  int32_t* fwd_len;     // [nl*R]
+  int32_t* fwd_src;     // [nl*R]
+  int32_t* inv_dst;     // [R*nl + 1]   grouped -> receive layout, (source, executor) order
+  int32_t* inv_len;     // [R*nl]
+  int32_t* inv_src;     // [R*nl]
+  int32_t* exec_off;    // [nl + 1]     grouped rows per local executor
+  int32_t* mtile_off;   // [nl + 1]
+  int32_t* totals;      // [2]          grouped rows, receive-layout extent
+  int64_t* splits;      // [2R]         send_rows, recv_rows (for the host in exact-size mode)
+};
+cudaError_t launch_ep_tables(const EpStatic& st, const int32_t* gathered, int ld, const int32_t* exec_of,
+                             const EpTables& tb, cudaStream_t s);
+// Row-block permutation: block b moves len[b] rows src_off[b] + k -> dst_start[b] + k
+// (dst_start ascending, n_blocks + 1 entries); destination extent read from `extent`
+// (device, nullable) capped at extent_max.
 cudaError_t launch_block_copy(const void* src, void* dst, int row_bytes, const float* w_src, float* w_dst,
-                              int n_blocks, const int32_t* src_off, const int32_t* dst_start, int64_t total_rows,
-                              int num_sms, cudaStream_t s);
+                              int n_blocks, const int32_t* dst_start, const int32_t* len, const int32_t* src_off,
+                              const int32_t* extent, int64_t extent_max, int num_sms, cudaStream_t s);
 
 // United-row de-duplication, stage 0: count, 1: per-executor prefix, 2: permute.
 cudaError_t launch_dedup(int stage, const int32_t* topk_id, const float* topk_w, int T, int K, int tile, int m, int E,

@@ -65,8 +65,10 @@ template <int VPL>
 __global__ void __launch_bounds__(512) k_topk_hist(const float* __restrict__ logits, int T, int m, int K, int tile,
                                                    int32_t* __restrict__ topk_id, float* __restrict__ topk_w,
                                                    int32_t* __restrict__ tile_cnt) {
-  __shared__ int hist[kMaxExperts];
-  for (int i = threadIdx.x; i < m; i += blockDim.x) hist[i] = 0;
+  // per-warp expert counts (a token's K ids are distinct, so lane writes never collide;
+  // no atomics), summed over the warps in a fixed order at the end
+  __shared__ int hist[16][kMaxExperts];
+  for (int i = threadIdx.x; i < 16 * kMaxExperts; i += blockDim.x) (&hist[0][0])[i] = 0;
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t0 = blockIdx.x * tile;
@@ -85,11 +87,16 @@ __global__ void __launch_bounds__(512) k_topk_hist(const float* __restrict__ log
     if (lane < K) {
       topk_id[static_cast<int64_t>(t) * K + lane] = id;
       topk_w[static_cast<int64_t>(t) * K + lane] = w;
-      atomicAdd(&hist[id], 1);   // integer count in shared memory: order-independent
+      hist[warp][id] += 1;
     }
+    __syncwarp();
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < m; i += blockDim.x) tile_cnt[static_cast<int64_t>(blockIdx.x) * m + i] = hist[i];
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    int c = 0;
+    for (int w = 0; w < nw; ++w) c += hist[w][i];
+    tile_cnt[static_cast<int64_t>(blockIdx.x) * m + i] = c;
+  }
 }
 
 cudaError_t launch_topk_hist(const float* logits, int T, int m, int K, int tile, int32_t* topk_id, float* topk_w,
@@ -146,7 +153,7 @@ __global__ void __launch_bounds__(256) k_router_small(const T* __restrict__ x, c
                                                       int32_t* __restrict__ topk_id, float* __restrict__ topk_w,
                                                       int32_t* __restrict__ tile_cnt) {
   extern __shared__ uint4 s_wr[];
-  __shared__ int hist[32];
+  __shared__ int hist[8][32];   // per-warp expert counts (no atomics), summed in warp order
   constexpr int EPV = 16 / sizeof(T);         // elements per 16-byte vector
   constexpr int BATCH = TPW >= 4 ? 4 : (TPW == 2 ? 8 : 16);   // 16-byte loads per token in flight per lane
   const int nvec = d / EPV;
@@ -154,8 +161,8 @@ __global__ void __launch_bounds__(256) k_router_small(const T* __restrict__ x, c
     const uint4* src = reinterpret_cast<const uint4*>(Wr);
     for (int i = threadIdx.x; i < m * nvec; i += blockDim.x) cp_async16(s_wr + i, src + i);
   }
-  if (threadIdx.x < 32) hist[threadIdx.x] = 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  hist[warp][lane] = 0;
   const int tbase = blockIdx.x * (8 * TPW) + warp * TPW;   // this warp's TPW consecutive tokens
   float acc[TPW][MAXM];
 #pragma unroll
@@ -227,12 +234,17 @@ __global__ void __launch_bounds__(256) k_router_small(const T* __restrict__ x, c
       if (lane < K) {
         topk_id[static_cast<int64_t>(t) * K + lane] = id;
         topk_w[static_cast<int64_t>(t) * K + lane] = w;
-        atomicAdd(&hist[id], 1);
+        hist[warp][id] += 1;   // a token's K ids are distinct
       }
+      __syncwarp();
     }
   }
   __syncthreads();
-  if (threadIdx.x < m) tile_cnt[static_cast<int64_t>(blockIdx.x) * m + threadIdx.x] = hist[threadIdx.x];
+  if (threadIdx.x < m) {
+    int c = 0;
+    for (int w = 0; w < 8; ++w) c += hist[w][threadIdx.x];
+    tile_cnt[static_cast<int64_t>(blockIdx.x) * m + threadIdx.x] = c;
+  }
 }
 
 // Decode-sized batches (T < 8 * #SM): k_router_small would run one warp per
@@ -246,7 +258,7 @@ __global__ void __launch_bounds__(256) k_router_split(const T* __restrict__ x, c
                                                       int32_t* __restrict__ topk_id, float* __restrict__ topk_w,
                                                       int32_t* __restrict__ tile_cnt) {
   __shared__ float s_part[8][MAXM];
-  __shared__ int hist[32];
+  __shared__ int hist[8][32];   // per-warp expert counts (no atomics)
   constexpr int EPV = 16 / sizeof(T);
   constexpr int U = 4;   // 16-byte x loads per lane in flight
   const int nvec = d / EPV;
@@ -256,7 +268,7 @@ __global__ void __launch_bounds__(256) k_router_split(const T* __restrict__ x, c
   const int t = blockIdx.x * tpc + tl;
   const int nvw = nvec / wpt;
   const int v0 = q * nvw, v1 = v0 + nvw;
-  if (threadIdx.x < 32) hist[threadIdx.x] = 0;
+  hist[warp][lane] = 0;
   float acc[MAXM];
 #pragma unroll
   for (int e = 0; e < MAXM; ++e) acc[e] = 0.0f;
@@ -320,11 +332,15 @@ __global__ void __launch_bounds__(256) k_router_split(const T* __restrict__ x, c
     if (lane < K) {
       topk_id[static_cast<int64_t>(t) * K + lane] = id;
       topk_w[static_cast<int64_t>(t) * K + lane] = w;
-      atomicAdd(&hist[id], 1);
+      hist[warp][id] += 1;   // one token per warp here: its K ids are distinct
     }
   }
   __syncthreads();
-  if (threadIdx.x < m) tile_cnt[static_cast<int64_t>(blockIdx.x) * m + threadIdx.x] = hist[threadIdx.x];
+  if (threadIdx.x < m) {
+    int c = 0;
+    for (int w = 0; w < 8; ++w) c += hist[w][threadIdx.x];
+    tile_cnt[static_cast<int64_t>(blockIdx.x) * m + threadIdx.x] = c;
+  }
 }
 
 // Prefill-sized batches, m <= 32, bf16: Eq. 8 on the tensor cores with
@@ -354,12 +370,12 @@ __global__ void __launch_bounds__(32 * NW) k_router_mma(const __nv_bfloat16* __r
                                                     float* __restrict__ topk_w, int32_t* __restrict__ tile_cnt) {
   constexpr int U = 4;   // 32-wide k chunks in flight per thread
   __shared__ float s_c[NW][16][NB * 8 + 1];
-  __shared__ int hist[32];
+  __shared__ int hist[NW][32];   // per-warp expert counts (no atomics)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = lane >> 2, q = lane & 3;
   const int t0 = blockIdx.x * 16;
   const int nk = d / NW, k0 = warp * nk;
-  if (threadIdx.x < 32) hist[threadIdx.x] = 0;
+  hist[warp][lane] = 0;
   const bool va = t0 + r < Tn, vb = t0 + r + 8 < Tn;
   const uint4* xa = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(va ? t0 + r : 0) * d + k0 + 8 * q);
   const uint4* xb = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(vb ? t0 + r + 8 : 0) * d + k0 + 8 * q);
@@ -428,11 +444,16 @@ __global__ void __launch_bounds__(32 * NW) k_router_mma(const __nv_bfloat16* __r
     if (lane < K) {
       topk_id[static_cast<int64_t>(t) * K + lane] = id;
       topk_w[static_cast<int64_t>(t) * K + lane] = wgt;
-      atomicAdd(&hist[id], 1);
+      hist[warp][id] += 1;   // a token's K ids are distinct
     }
+    __syncwarp();
   }
   __syncthreads();
-  if (threadIdx.x < m) tile_cnt[static_cast<int64_t>(blockIdx.x) * m + threadIdx.x] = hist[threadIdx.x];
+  if (threadIdx.x < m) {
+    int c = 0;
+    for (int w = 0; w < NW; ++w) c += hist[w][threadIdx.x];
+    tile_cnt[static_cast<int64_t>(blockIdx.x) * m + threadIdx.x] = c;
+  }
 }
 
 bool router_mma_ok(int dtype, int m, int d, int T, int num_sms) {
@@ -610,7 +631,6 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
     for (int i = 4 * n16 + tid; i < n_tc; i += blockDim.x) s_tc[i] = __ldg(tile_cnt + (i / m) * ld + i % m);
     cp_async_wait_all();
   }
-  if (tid < m) s_gsize[tid] = 0;
   __syncthreads();
   if (staged && m >= 32) {
     // many experts: thread (chunk c, expert e) walks its chunk of tiles sequentially
@@ -696,7 +716,13 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
     const bool active = c_me > 0;                                 // D6
     in_s1 = active && static_cast<double>(s_excl[tid]) < Tcov;    // D1
     in_s2 = active && !in_s1;
-    if (in_s2) atomicAdd(&s_gsize[tid / way], 1);     // group_experts (line 23); integer count
+    s_exec[tid] = in_s2 ? 1 : 0;                                  // S2 flags (s_exec reused below)
+  }
+  __syncthreads();
+  if (tid < G) {   // group_experts (line 23): |M_j| = S2 members of group j, counted by its own thread
+    int n = 0;
+    for (int e = tid * way; e < min((tid + 1) * way, m); ++e) n += s_exec[e];
+    s_gsize[tid] = n;
   }
   __syncthreads();
   // 4. executor of each expert (lines 16-30)
