@@ -107,7 +107,11 @@ class ClockSampler:
 def algorithmic(cfg, T, stats, d, f, m):
     """Method's own work: FLOPs = 2 T d m + 6 d f R_kept,
     bytes = sum over accessed executors of 3 d f * 2 B + x and y (2 T d * 2 B) + Wr.
-    Shared experts (Eq. 5, N_s = cfg.Ns) add N_s T rows and N_s always-accessed executors."""
+    Shared experts (Eq. 5, N_s = cfg.Ns) add N_s T rows and N_s always-accessed executors.
+    `stats` may be a list (one entry per rotated batch): the work is then their mean."""
+    if isinstance(stats, list):
+        parts = [algorithmic(cfg, T, s, d, f, m) for s in stats]
+        return {k: sum(p[k] for p in parts) / len(parts) for k in parts[0]}
     Ns = getattr(cfg, "Ns", 0)
     R = stats["rows_original"] + stats["rows_united"] + Ns * T
     stats = dict(stats, executors_accessed=stats["executors_accessed"] + Ns)
@@ -152,23 +156,35 @@ class Layer:
         if cfg.Ns:
             self.moe.set_shared_experts(L["SWg"], L["SWu"], L["SWd"])
         self.united = self.moe.build_united(L["Wg"], L["Wu"], L["Wd"])
-        self.x = S.make_tokens(cfg, T=self.T, device=device)
+        # two token batches (seeds 2000 and 2001) alternate step by step, so no step
+        # re-reads the previous step's tokens / permuted rows from L2
+        self.xs = [S.make_tokens(cfg, batch_index=b, T=self.T, device=device) for b in range(2)]
+        self.x = self.xs[0]
+        self.i = 0
         self.y = torch.empty_like(self.x)
         self.ws = self.moe.workspace(self.T, device)
         self.stream = torch.cuda.current_stream()
 
-    def step(self):
-        """One forward on the current stream (the capture stream under a CUDA graph)."""
+    def step(self, batch=None):
+        """One forward on the current stream (the capture stream under a CUDA graph),
+        on the next of the two token batches (or on `batch`)."""
         L = self.lay
-        self.moe.forward(self.x, L["Wr"], (L["Wg"], L["Wu"], L["Wd"]), self.united, y=self.y,
+        b = self.i % len(self.xs) if batch is None else batch
+        self.i += 1
+        self.moe.forward(self.xs[b], L["Wr"], (L["Wg"], L["Wu"], L["Wd"]), self.united, y=self.y,
                          workspace=self.ws, stream=None)
 
     def stats(self):
+        """Plan statistics of every batch (one forward each)."""
         import torch
-        torch.cuda.synchronize()
         from paper_2507_17133_b200 import STATS_FIELDS
-        st = self.moe.debug_arrays(self.T, self.ws)["stats"].cpu().tolist()
-        return dict(zip(STATS_FIELDS, st))
+        out = []
+        for b in range(len(self.xs)):
+            self.step(batch=b)
+            torch.cuda.synchronize()
+            st = self.moe.debug_arrays(self.T, self.ws)["stats"].cpu().tolist()
+            out.append(dict(zip(STATS_FIELDS, st)))
+        return out
 
 
 def _capture(layer, steps, ev_sets):
@@ -343,7 +359,7 @@ def time_e2e(layer, steps, warmup):
     overlap step i's forward.  Timed from the first upload to the last download."""
     import torch
     nb = 2
-    hx = [layer.x.cpu().pin_memory() for _ in range(nb)]
+    hx = [layer.xs[b % len(layer.xs)].cpu().pin_memory() for b in range(nb)]   # the two token batches
     hy = [torch.empty(layer.y.shape, dtype=layer.y.dtype, pin_memory=True) for _ in range(nb)]
     dx = [torch.empty_like(layer.x) for _ in range(nb)]
     dy = [torch.empty_like(layer.y) for _ in range(nb)]
@@ -384,7 +400,7 @@ def time_e2e(layer, steps, warmup):
     run(max(warmup, 2))
     ms = run(steps) / steps
     # the downloaded result is the forward of the uploaded tokens (bitwise: the path is deterministic)
-    layer.step()
+    layer.step(batch=((steps - 1) % nb) % len(layer.xs))
     torch.cuda.synchronize()
     if not torch.equal(hy[(steps - 1) % nb], layer.y.cpu()):
         raise RuntimeError("e2e pipeline result differs from the device-resident forward")
@@ -431,6 +447,15 @@ def cpu_threads():
 
 
 def cpu_model():
+    """`lscpu` model name (falls back to /proc/cpuinfo)."""
+    import subprocess
+    try:
+        r = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10)
+        for line in r.stdout.splitlines():
+            if line.strip().startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
     try:
         for line in open("/proc/cpuinfo"):
             if line.startswith("model name"):
@@ -438,6 +463,14 @@ def cpu_model():
     except Exception:
         pass
     return None
+
+
+def nproc():
+    import subprocess
+    try:
+        return int(subprocess.run(["nproc"], capture_output=True, text=True, timeout=10).stdout.strip())
+    except Exception:
+        return os.cpu_count()
 
 
 # -------------------------------------------------------------------- main
@@ -531,9 +564,11 @@ def main():
         "config": {"workload": cfg.name, "T": cfg.T, "d": cfg.d, "f": cfg.f, "m": cfg.m, "K": cfg.K,
                    "way": cfg.way, "ratio": cfg.ratio, "mode": "partial", "sigma": cfg.sigma, "num_shared": cfg.Ns,
                    "parallelism": "single",
-                   "l2": "inputs larger than L2 (expert weights %.2f GB/step)" % (alg["weight_bytes"] / 1e9)},
+                   "l2": "inputs larger than L2 (expert weights %.2f GB/step); two token batches alternate step by step"
+                         % (alg["weight_bytes"] / 1e9)},
         "roofline": roof,
-        "step_roofline": {"tflops": step_tflops, "frac_bf16_sustained": step_tflops / pk["bf16_tflops_sustained"],
+        "step_roofline": {"tflops": step_tflops, "frac_bf16": step_tflops / pk["bf16_tflops"],
+                          "frac_bf16_sustained": step_tflops / pk["bf16_tflops_sustained"],
                           "alg_gbs": step_gbs, "frac_hbm": step_gbs / pk["hbm_gbs"]},
         "kernel_ms": kern, "plan_stats": st, "gpu_launches": launches * args.steps,
         "clocks": clocks,
@@ -559,8 +594,8 @@ def main():
                 s_r = layer.stats()
                 ms_r, k_r = time_steps(layer, args.steps, 3, dist_on, graph=not args.no_graph)
                 entry.update({tag + "tokens_per_s": world * cfg.T / (ms_r / args.steps / 1e3),
-                              tag + "ms": ms_r / args.steps, tag + "executors": s_r["executors_accessed"],
-                              tag + "rows": s_r["rows_original"] + s_r["rows_united"],
+                              tag + "ms": ms_r / args.steps, tag + "executors": [q["executors_accessed"] for q in s_r],
+                              tag + "rows": [q["rows_original"] + q["rows_united"] for q in s_r],
                               tag + "gemm1_ms": k_r["gemm1_swiglu"], tag + "gemm2_ms": k_r.get("gemm2_weighted", k_r.get("gemm2_weighted_combine"))})
             sweep[str(r)] = entry
         layer.moe = base_moe
@@ -578,7 +613,8 @@ def main():
                 lay2.cfg, lay2.T, lay2.lay, lay2.united, lay2.stream = c2, c2.T, layer.lay, layer.united, layer.stream
                 from paper_2507_17133_b200 import BrownoutMoE
                 lay2.moe = BrownoutMoE(c2.d, c2.f, c2.m, c2.K, c2.way, dtype=c2.dtype, max_tokens=c2.T)
-                lay2.x = S.make_tokens(c2, T=c2.T, device="cuda")
+                lay2.xs = [S.make_tokens(c2, batch_index=b, T=c2.T, device="cuda") for b in range(2)]
+                lay2.x, lay2.i = lay2.xs[0], 0
                 lay2.y = torch.empty_like(lay2.x)
                 lay2.ws = lay2.moe.workspace(c2.T, "cuda")
             else:
@@ -595,12 +631,13 @@ def main():
                 a2 = algorithmic(c2, c2.T, s2, c2.d, c2.f, c2.m)
                 t2 = ms2 / args.steps / 1e3
                 res[str(r)] = {"tokens_per_s": world * c2.T / t2, "ms": t2 * 1e3,
-                               "executors": s2["executors_accessed"],
+                               "executors": [q["executors_accessed"] for q in s2],
                                "frac_hbm_step": a2["bytes"] / t2 / 1e9 / pk["hbm_gbs"],
-                               "frac_bf16_step": a2["flops"] / t2 / 1e12 / pk["bf16_tflops_sustained"],
+                               "frac_bf16_step": a2["flops"] / t2 / 1e12 / pk["bf16_tflops"],
                                "kernel_ms": k2,
                                "gemm1_frac_hbm": a2["gemm1_bytes"] / (g1t(k2) / 1e3) / 1e9 / pk["hbm_gbs"],
-                               "gemm1_frac_bf16": a2["gemm1_flops"] / (g1t(k2) / 1e3) / 1e12
+                               "gemm1_frac_bf16": a2["gemm1_flops"] / (g1t(k2) / 1e3) / 1e12 / pk["bf16_tflops"],
+                               "gemm1_frac_bf16_sustained": a2["gemm1_flops"] / (g1t(k2) / 1e3) / 1e12
                                / pk["bf16_tflops_sustained"]}
             extra[name] = res
         # f2: the paper's model shape (Qwen1.5-MoE-A2.7B, 60 experts top-4, 4 shared
@@ -619,9 +656,10 @@ def main():
             t2 = ms2 / args.steps / 1e3
             res[f"way{way}_threshold{thr}"] = {
                 "ratio": c2.ratio, "tokens_per_s": world * c2.T / t2, "ms": t2 * 1e3,
-                "executors": s2["executors_accessed"] + c2.Ns, "kernel_ms": k2,
-                "frac_bf16_step": a2["flops"] / t2 / 1e12 / pk["bf16_tflops_sustained"],
-                "gemm1_frac_bf16": a2["gemm1_flops"] / (g1t(k2) / 1e3) / 1e12
+                "executors": [q["executors_accessed"] + c2.Ns for q in s2], "kernel_ms": k2,
+                "frac_bf16_step": a2["flops"] / t2 / 1e12 / pk["bf16_tflops"],
+                "gemm1_frac_bf16": a2["gemm1_flops"] / (g1t(k2) / 1e3) / 1e12 / pk["bf16_tflops"],
+                "gemm1_frac_bf16_sustained": a2["gemm1_flops"] / (g1t(k2) / 1e3) / 1e12
                 / pk["bf16_tflops_sustained"]}
             del lay2
             torch.cuda.empty_cache()
@@ -634,7 +672,7 @@ def main():
         s1 = lay1.stats()
         ms1, k1 = time_steps(lay1, max(args.steps, 50), 10, dist_on, graph=not args.no_graph)
         extra[c1.name] = {"ratio": c1.ratio, "us_per_forward": ms1 / max(args.steps, 50) * 1e3,
-                          "executors": s1["executors_accessed"], "n_singleton": s1["n_singleton"],
+                          "executors": [q["executors_accessed"] for q in s1], "n_singleton": [q["n_singleton"] for q in s1],
                           "kernel_us": {k: v * 1e3 for k, v in k1.items() if not k.startswith("_")}}
         del lay1
         out["other_workloads"] = extra
@@ -642,8 +680,8 @@ def main():
         try:
             hc = host_copy(layer if layer.lay is not None else Layer(cfg, "cuda"))
             secs, n = oracle_sample(hc, cfg, cfg.ratio, args.cpu_tokens)
-            out["cpu_baseline"] = {"value": n / secs, "unit": "tokens/s", "cores": cpu_threads(), "kind": "oracle",
-                                   "sample": f"{n} of {cfg.T} tokens (full-batch routing + plan, FFN rows of the "
+            out["cpu_baseline"] = {"value": n / secs, "unit": "tokens/s", "cores": cpu_threads(), "nproc": nproc(),
+                                   "kind": "oracle", "sample": f"{n} of {cfg.T} tokens (full-batch routing + plan, FFN rows of the "
                                              f"sampled tokens), fp64 numpy, {secs:.1f} s",
                                    "cpu": cpu_model()}
         except Exception as e:   # pragma: no cover
@@ -898,7 +936,8 @@ def run_reference(args, cfg, rank, world):
            "data": "synthetic (seeded)",
            "config": {"workload": cfg.name, "T": cfg.T, "d": cfg.d, "f": cfg.f, "m": cfg.m, "K": cfg.K,
                       "way": cfg.way, "ratio": cfg.ratio, "num_shared": cfg.Ns},
-           "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cpu_threads(), "kind": "oracle",
+           "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cpu_threads(), "nproc": nproc(),
+                            "kind": "oracle",
                             "sample": f"{n_tok} of {cfg.T} tokens per step (full-batch routing + plan)",
                             "cpu": cpu_model()},
            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
