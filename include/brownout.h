@@ -85,7 +85,9 @@ typedef enum {
   BO_OPT_ROUTER_MMA = 11,    /* 1: prefill-sized bf16 batches with m <= 32 use the mma.sync router    [1]    */
   BO_OPT_ROUTER_SPLIT = 12,  /* 1: decode-sized batches with m <= 32 use the split-warp router        [1]    */
   BO_OPT_PDL = 13,           /* 1: GEMMs launch with programmatic dependent launch                   [1]    */
-  BO_OPT_COUNT = 14
+  BO_OPT_ROUTE_FUSED = 14,   /* 1: decode-sized m <= 32 steps run router + top-K + Alg. 1 + permute +
+                                   gather as one cooperative launch                                   [1]    */
+  BO_OPT_COUNT = 15
 } bo_engine_option;
 
 typedef struct {
@@ -326,7 +328,10 @@ BO_API bo_status bo_ep_placement_slices(int32_t num_experts, int32_t way, int32_
 
 /* An EP context on a layer handle (host state only; no device memory). */
 BO_API bo_status bo_ep_create(bo_handle* h, const bo_ep_config* cfg, bo_ep** out);
-BO_API bo_status bo_ep_destroy(bo_ep* ep);   /* also destroys the NCCL communicator of bo_ep_init */
+/* Also destroys the NCCL communicator of bo_ep_init.  Destroy every CUDA graph that captured
+   bo_ep_forward on this context first: such a graph holds the communicator's persistent NCCL
+   resources, and ncclCommDestroy under a live graph blocks (observed on the B200 box). */
+BO_API bo_status bo_ep_destroy(bo_ep* ep);
 BO_API bo_status bo_ep_get_info(const bo_ep* ep, bo_ep_info* out);
 BO_API bo_status bo_ep_workspace_layout(const bo_ep* ep, bo_ep_ws_layout* out);
 

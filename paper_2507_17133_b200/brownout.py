@@ -13,7 +13,10 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbrownout.so")
+# BO_LIB=probe loads the instrumentation build (build.py --variant probe); the product
+# library otherwise.  Either way there is no fallback.
+LIB_PATH = os.path.join(_HERE, "libbrownout.so" if os.environ.get("BO_LIB", "") != "probe"
+                        else "libbrownout_probe.so")
 
 BO_OK, BO_ERR_INVALID_ARG, BO_ERR_SHAPE, BO_ERR_UNSUPPORTED, BO_ERR_CUDA, BO_ERR_NCCL, BO_ERR_WORKSPACE = range(7)
 BO_BF16, BO_FP32 = 0, 1
@@ -22,7 +25,7 @@ BO_UNITED_MEAN = 0
 # bo_engine_option (include/brownout.h): name -> id
 ENGINE_OPTIONS = {n: i for i, n in enumerate((
     "cta_pairs", "pair_rows1", "pair_rows2", "tile_alt", "swap_tail", "decode_pair2", "gemm2_splitk",
-    "fused_combine", "tma_store", "store_hint", "b_policy", "router_mma", "router_split", "pdl"))}
+    "fused_combine", "tma_store", "store_hint", "b_policy", "router_mma", "router_split", "pdl", "route_fused"))}
 
 EXPORTED = (
     "bo_create", "bo_destroy", "bo_workspace_size", "bo_workspace_layout", "bo_build_united", "bo_set_shared_experts",

@@ -18,6 +18,10 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(ROOT, "build", "brownout")
 LIB = os.path.join(PKG, "libbrownout.so")
+# Instrumentation variant (python -m paper_2507_17133_b200.build --variant probe):
+# -DBO_PROBE adds per-tile globaltimer stamps to the grouped GEMM (bo_probe_copy);
+# loaded instead of the product library with BO_LIB=probe.  Never the default.
+VARIANTS = {"probe": ["-DBO_PROBE"]}
 INCLUDE = os.path.join(ROOT, "include")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -42,12 +46,14 @@ def _headers():
     return hs
 
 
-def _compile(src: str, force: bool, verbose_ptxas: bool) -> str:
-    obj = os.path.join(BUILD, os.path.basename(src)[:-3] + ".o")
+def _compile(src: str, force: bool, verbose_ptxas: bool, variant: str | None = None) -> str:
+    bdir = BUILD + ("_" + variant if variant else "")
+    obj = os.path.join(bdir, os.path.basename(src)[:-3] + ".o")
     newest_dep = max(os.path.getmtime(p) for p in [src] + _headers())
     if not force and os.path.exists(obj) and os.path.getmtime(obj) >= newest_dep:
         return obj
-    cmd = [nvcc()] + ARCH + CFLAGS + (["-Xptxas", "-v"] if verbose_ptxas else []) + ["-c", src, "-o", obj]
+    cmd = [nvcc()] + ARCH + CFLAGS + VARIANTS.get(variant, []) + (["-Xptxas", "-v"] if verbose_ptxas else []) + \
+        ["-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
@@ -56,20 +62,24 @@ def _compile(src: str, force: bool, verbose_ptxas: bool) -> str:
     return obj
 
 
-def build(force: bool = False, verbose_ptxas: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose_ptxas: bool = False, variant: str | None = None) -> str:
+    if variant is not None and variant not in VARIANTS:
+        raise ValueError(f"unknown build variant {variant!r}")
+    lib = LIB if variant is None else os.path.join(PKG, f"libbrownout_{variant}.so")
+    os.makedirs(BUILD + ("_" + variant if variant else ""), exist_ok=True)
     srcs = _sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        objs = list(ex.map(lambda s: _compile(s, force, verbose_ptxas), srcs))
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        tmp = LIB + ".tmp"
+        objs = list(ex.map(lambda s: _compile(s, force, verbose_ptxas, variant), srcs))
+    if force or not os.path.exists(lib) or os.path.getmtime(lib) < max(os.path.getmtime(o) for o in objs):
+        tmp = lib + ".tmp"
         cmd = [nvcc()] + ARCH + ["-shared", "-cudart", "shared", "-o", tmp] + objs
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-        os.replace(tmp, LIB)
-    return LIB
+        os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose_ptxas="-v" in sys.argv))
+    var = sys.argv[sys.argv.index("--variant") + 1] if "--variant" in sys.argv else None
+    print(build(force="--force" in sys.argv, verbose_ptxas="-v" in sys.argv, variant=var))

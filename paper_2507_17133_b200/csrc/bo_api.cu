@@ -460,6 +460,7 @@ const OptionSpec kOptions[BO_OPT_COUNT] = {
     {&EngineOptions::router_mma, "BO_ROUTER_MMA", 0, 1},
     {&EngineOptions::router_split, "BO_ROUTER_SPLIT", 0, 1},
     {&EngineOptions::pdl, "BO_PDL", 0, 1},
+    {&EngineOptions::route_fused, "BO_ROUTE_FUSED", 0, 1},
 };
 
 void options_from_env(EngineOptions* o) {
@@ -519,16 +520,39 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   int launches = 0;
   Prof prof(h, s, 10);
   int tile = 0;
-  // a1-a4: router, top-K, histogram, Alg. 1 plan
-  if ((st = route_stage(h, x, T, Wr, logits_in, ws, L, s, prof, launches, tile)) != BO_OK) return st;
-  // a5: permutation (rows in executor / expert / token order) and gather of Xp
   int32_t* row_of = at<int32_t>(ws, L.row_of);
   float* row_w = at<float>(ws, L.row_w);
   // Small batches: the permute CTAs also copy the rows (one launch less).  Large
   // batches: a separate grid-wide gather (the permute has too few CTAs to move
   // R*d*2 bytes at HBM speed; measured r01).
   const bool gather_in_permute = Rt <= kSplitRows * 2 && !c.dedup_united;
-  if (c.dedup_united) {
+  // Decode-sized steps on the split-warp router: a1-a5 in one cooperative launch
+  const int tpc = h->opt.router_split ? bo::router_split_tpc(static_cast<int>(T), h->num_sms) : 0;
+  const bool route_fused = h->opt.route_fused && !logits_in && gather_in_permute && Wr != nullptr &&
+                           bo::router_small_ok(dt, m, d) && tpc > 0 &&
+                           !(h->opt.router_mma && bo::router_mma_ok(dt, m, d, static_cast<int>(T), h->num_sms)) &&
+                           bo::route_fused_ok(dt, m, c.way, static_cast<int>(T), tpc, Ns, h->num_sms);
+  if (route_fused) {
+    tile = tpc;
+    prof.mark(launches, "route_fused");
+    BO_CUDA(bo::launch_route_fused(dt, x, Wr, static_cast<int>(T), d, m, K, tpc, at<float>(ws, L.logits),
+                                   at<int32_t>(ws, L.topk_id), at<float>(ws, L.topk_w), at<int32_t>(ws, L.tile_cnt),
+                                   c.way, h->ratio, h->mode, at<int32_t>(ws, L.tile_base),
+                                   at<int32_t>(ws, L.counts), at<int32_t>(ws, L.exec_of_expert),
+                                   at<int32_t>(ws, L.expert_row_off), at<int32_t>(ws, L.exec_off),
+                                   at<int32_t>(ws, L.mtile_off), at<int64_t>(ws, L.stats), Ns, row_of,
+                                   at<int32_t>(ws, L.row_tok), row_w, at<char>(ws, L.xp), s),
+            "route_fused");
+    ++launches;
+    h->route_T = T;
+    h->route_tile = tile;
+  } else {
+    // a1-a4: router, top-K, histogram, Alg. 1 plan
+    if ((st = route_stage(h, x, T, Wr, logits_in, ws, L, s, prof, launches, tile)) != BO_OK) return st;
+  }
+  // a5: permutation (rows in executor / expert / token order) and gather of Xp
+  if (route_fused) {
+  } else if (c.dedup_united) {
     // f3: one row per (token, united executor); Alg. 1 above is unchanged
     for (int stage = 0; stage < 3; ++stage) {
       prof.mark(launches, kDedupNames[stage]);

@@ -306,6 +306,24 @@ __device__ __forceinline__ void combine_token_cols(const GemmParams& p, const T*
   }
 }
 
+#ifdef BO_PROBE
+// Instrumentation build only (build.py --variant probe): per (launch class, CTA, work item)
+// globaltimer stamps [producer starts the tile, MMA has its first stage, MMA committed the
+// last k-block, epilogue done] and the tile id (x | mi << 10 | n << 16).
+constexpr int kProbeCtas = 160, kProbeItems = 48;
+__device__ unsigned long long g_probe[2][kProbeCtas][kProbeItems][4];
+__device__ int g_probe_id[2][kProbeCtas][kProbeItems];
+#define BO_STAMP(j, k)                                                                      \
+  do {                                                                                      \
+    if (blockIdx.x < kProbeCtas && (j) < kProbeItems)                                       \
+      g_probe[EPI == EPI_SWIGLU ? 0 : 1][blockIdx.x][(j)][(k)] = globaltimer_ns();          \
+  } while (0)
+#else
+#define BO_STAMP(j, k) \
+  do {                 \
+  } while (0)
+#endif
+
 template <typename T, int BN, int EPI, int KMAX, int CG>
 __global__ void __launch_bounds__(192, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ BMaps tmB, const GemmParams p) {
@@ -514,8 +532,14 @@ __global__ void __launch_bounds__(192, 1)
       int stage = 0;
       uint32_t phase = 0;
       int x, mi, n, sp, kb0, kb1;
-      for (int w = unit; w < total_work; w += n_units) {
+      int item = 0;
+      for (int w = unit; w < total_work; w += n_units, ++item) {
         decode(w, x, mi, n, sp, kb0, kb1);
+        BO_STAMP(item, 0);
+#ifdef BO_PROBE
+        if (blockIdx.x < kProbeCtas && item < kProbeItems)
+          g_probe_id[EPI == EPI_SWIGLU ? 0 : 1][blockIdx.x][item] = x | (mi << 10) | (n << 16);
+#endif
         const int arow = (p.a_shared ? 0 : s_eoff[x]) + mi * TILE_M + static_cast<int>(crank) * kBM;
         const int cls = x < mo ? 0 : (x < mu ? 1 : 2);      // original / united / shared
         const CUtensorMap* mb0 = &tmB.m[(alt ? 6 : 0) + 2 * cls];
@@ -582,7 +606,8 @@ __global__ void __launch_bounds__(192, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       int x, mi, n, sp, kb0, kb1;
-      for (int w = unit; w < total_work; w += n_units) {
+      int item = 0;
+      for (int w = unit; w < total_work; w += n_units, ++item) {
         decode(w, x, mi, n, sp, kb0, kb1);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -594,6 +619,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
+          if (kb == kb0) BO_STAMP(item, 1);
           const uint32_t a_addr = smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t b_addr = a_addr + C::A_BYTES;
 #pragma unroll
@@ -610,6 +636,7 @@ __global__ void __launch_bounds__(192, 1)
         }
         if constexpr (CG == 1) tc_commit(&tfull_bar[acc]);
         else tc_commit_pair(&tfull_bar[acc]);       // both CTAs' epilogues
+        BO_STAMP(item, 2);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
       if constexpr (CG == 2) {
@@ -649,7 +676,10 @@ __global__ void __launch_bounds__(192, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     int x, mi, n, sp, kb0, kb1;
+    int item = -1;
     for (int w = unit; w < total_work; w += n_units) {
+      if (item >= 0 && warp == 2 && lane == 0) BO_STAMP(item, 3);   // the previous tile's epilogue is done
+      ++item;
       decode(w, x, mi, n, sp, kb0, kb1);
       const int rows_x = s_eoff[x + 1] - s_eoff[x];
       const int r_local = mi * TILE_M + static_cast<int>(crank) * kBM + q * 32 + lane;
@@ -958,6 +988,12 @@ __global__ void __launch_bounds__(192, 1)
     }
   }
 
+#ifdef BO_PROBE
+  if (warp == 2 && lane == 0) {
+    const int last = total_work > unit ? (total_work - unit + n_units - 1) / n_units - 1 : -1;
+    if (last >= 0) BO_STAMP(last, 3);
+  }
+#endif
   if constexpr (EPI == EPI_WEIGHTED) {
     if (warp >= 2 && lane == 0) bulk_wait_all();   // TMA-stored Yp boxes complete before exit
   }
@@ -1054,6 +1090,14 @@ cudaError_t launch_grouped_gemm(int dtype, int epi, int bn, const CUtensorMap& A
   if (dtype == 0) return dispatch<__nv_bfloat16>(epi, bn, A, B, p, grid, s, pdl);
   return dispatch<float>(epi, bn, A, B, p, grid, s, pdl);
 }
+
+#ifdef BO_PROBE
+extern "C" __attribute__((visibility("default"))) int bo_probe_copy(void* stamps, void* ids) {
+  if (cudaMemcpyFromSymbol(stamps, g_probe, sizeof(g_probe)) != cudaSuccess) return 1;
+  if (cudaMemcpyFromSymbol(ids, g_probe_id, sizeof(g_probe_id)) != cudaSuccess) return 1;
+  return 0;
+}
+#endif
 
 int gemm_smem_bytes(int dtype, int epi, int bn) {
   (void)epi;

@@ -29,6 +29,7 @@ struct EngineOptions {
   int32_t router_mma = 1;      // prefill-sized bf16 m <= 32 batches: mma.sync router
   int32_t router_split = 1;    // decode-sized m <= 32 batches: split-warp router
   int32_t pdl = 1;             // programmatic dependent launch of the GEMMs
+  int32_t route_fused = 1;     // decode-sized m <= 32: routing, Alg. 1, permute + gather in one launch
 };
 
 struct bo_handle {

@@ -133,6 +133,18 @@ cudaError_t launch_permute(const int32_t* topk_id, const float* topk_w, int T, i
                            int32_t* row_tok, float* row_w, cudaStream_t s, int dtype = 0, const void* x = nullptr,
                            void* xp = nullptr, int d = 0, int n_shared = 0, const int32_t* shared_off = nullptr);
 
+// Decode-sized steps on one GPU: router (split-warp, m <= 32) + Eq. 7 + histogram, Alg. 1
+// and the permutation + gather in one cooperative launch (every plan output written as by
+// launch_plan / launch_permute).  route_fused_ok: the shapes fit and the grid is co-resident.
+constexpr int kRouteFusedMaxExec = 160;   // m + G + N_s executors the fused kernel's plan copy holds
+bool route_fused_ok(int dtype, int m, int way, int T, int tpc, int n_shared, int num_sms);
+cudaError_t launch_route_fused(int dtype, const void* x, const void* Wr, int T, int d, int m, int K, int tpc,
+                               float* logits, int32_t* topk_id, float* topk_w, int32_t* tile_cnt, int way,
+                               double ratio, int mode, int32_t* tile_base, int32_t* counts, int32_t* exec_of_expert,
+                               int32_t* expert_row_off, int32_t* exec_off, int32_t* mtile_off, int64_t* stats,
+                               int n_shared, int32_t* row_of, int32_t* row_tok, float* row_w, void* xp,
+                               cudaStream_t s);
+
 cudaError_t launch_gather(int dtype, const void* x, int T, int d, int KR, const int32_t* row_of, void* xp,
                           int num_sms, cudaStream_t s);
 

@@ -18,10 +18,16 @@
 //   k_united_mean united-expert init (D14): fp64 group mean, one RNE rounding.
 #include <float.h>
 
+#include <atomic>
+
+#include <cooperative_groups.h>
+
 #include "bo_kernels.h"
 #include "bo_ptx.cuh"
 
 namespace bo {
+
+namespace cg = cooperative_groups;
 
 // ----------------------------------------------------------------- top-k
 // Warp-cooperative Eq. 7 for one token whose m logits are spread over the
@@ -252,11 +258,13 @@ __global__ void __launch_bounds__(256) k_router_small(const T* __restrict__ x, c
 // hidden dimension of each token is split over 8/tpc warps of a CTA (tpc
 // tokens per CTA, >= #SM CTAs), centroids read through L1 (no shared-memory
 // staging), partial logits reduced in a fixed order through shared memory.
+// One token tile (tpc tokens, 256 threads) of the split-warp router; also the
+// first phase of the fused decode routing kernel (k_route_fused).
 template <typename T, int MAXM>
-__global__ void __launch_bounds__(256) k_router_split(const T* __restrict__ x, const T* __restrict__ Wr, int Tn,
-                                                      int d, int m, int K, int tpc, float* __restrict__ logits,
-                                                      int32_t* __restrict__ topk_id, float* __restrict__ topk_w,
-                                                      int32_t* __restrict__ tile_cnt) {
+__device__ __forceinline__ void router_split_tile(const T* __restrict__ x, const T* __restrict__ Wr, int Tn, int d,
+                                                  int m, int K, int tpc, float* __restrict__ logits,
+                                                  int32_t* __restrict__ topk_id, float* __restrict__ topk_w,
+                                                  int32_t* __restrict__ tile_cnt, int tile_idx) {
   __shared__ float s_part[8][MAXM];
   __shared__ int hist[8][32];   // per-warp expert counts (no atomics)
   constexpr int EPV = 16 / sizeof(T);
@@ -265,7 +273,7 @@ __global__ void __launch_bounds__(256) k_router_split(const T* __restrict__ x, c
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wpt = 8 / tpc;
   const int tl = warp / wpt, q = warp - tl * wpt;
-  const int t = blockIdx.x * tpc + tl;
+  const int t = tile_idx * tpc + tl;
   const int nvw = nvec / wpt;
   const int v0 = q * nvw, v1 = v0 + nvw;
   hist[warp][lane] = 0;
@@ -339,8 +347,16 @@ __global__ void __launch_bounds__(256) k_router_split(const T* __restrict__ x, c
   if (threadIdx.x < m) {
     int c = 0;
     for (int w = 0; w < 8; ++w) c += hist[w][threadIdx.x];
-    tile_cnt[static_cast<int64_t>(blockIdx.x) * m + threadIdx.x] = c;
+    tile_cnt[static_cast<int64_t>(tile_idx) * m + threadIdx.x] = c;
   }
+}
+
+template <typename T, int MAXM>
+__global__ void __launch_bounds__(256) k_router_split(const T* __restrict__ x, const T* __restrict__ Wr, int Tn,
+                                                      int d, int m, int K, int tpc, float* __restrict__ logits,
+                                                      int32_t* __restrict__ topk_id, float* __restrict__ topk_w,
+                                                      int32_t* __restrict__ tile_cnt) {
+  router_split_tile<T, MAXM>(x, Wr, Tn, d, m, K, tpc, logits, topk_id, topk_w, tile_cnt, blockIdx.x);
 }
 
 // Prefill-sized batches, m <= 32, bf16: Eq. 8 on the tensor cores with
@@ -512,6 +528,19 @@ int router_small_tile(int T, int num_sms) {
   return 8 * tpw;
 }
 
+// cudaFuncSetAttribute applies to the current device's context: set it once per device
+template <typename K>
+static cudaError_t smem_attr_once(K kern, int bytes, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = dev < 64 ? (uint64_t(1) << dev) : 0;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && bit) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
+
 cudaError_t launch_router_small(int dtype, const void* x, const void* Wr, int T, int d, int m, int K, int tile,
                                 float* logits, int32_t* topk_id, float* topk_w, int32_t* tile_cnt, cudaStream_t s) {
   const int ntiles = (T + tile - 1) / tile;
@@ -522,12 +551,9 @@ cudaError_t launch_router_small(int dtype, const void* x, const void* Wr, int T,
 #define BO_ROUTER_CASE(TYPE, M, TPW)                                                                           \
   {                                                                                                            \
     auto k = k_router_small<TYPE, M, TPW>;                                                                     \
-    static bool set = false;                                                                                   \
-    if (!set) {                                                                                                \
-      e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);                    \
-      if (e != cudaSuccess) return e;                                                                          \
-      set = true;                                                                                              \
-    }                                                                                                          \
+    static std::atomic<uint64_t> done{0};   /* per device ordinal (the attribute is per context) */            \
+    e = smem_attr_once(k, 160 * 1024, done);                                                                   \
+    if (e != cudaSuccess) return e;                                                                            \
     k<<<ntiles, 256, smem, s>>>(static_cast<const TYPE*>(x), static_cast<const TYPE*>(Wr), T, d, m, K, logits,  \
                                 topk_id, topk_w, tile_cnt);                                                    \
   }
@@ -582,14 +608,30 @@ __device__ __forceinline__ long long block_excl_scan(long long v, long long* s_w
   return r;
 }
 
-constexpr int kPlanStage = 8192;    // tile histograms staged in shared memory when ntiles*m fits
+constexpr int kPlanStage = 8192;       // tile histograms staged in shared memory when ntiles*m fits
+constexpr int kPlanStageFused = 4096;  // the fused decode routing kernel's stage (static smem budget)
 
-__global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_cnt, int ntiles, int m, int way,
-                                              double ratio, int mode, int32_t* __restrict__ tile_base,
-                                              int32_t* __restrict__ counts, int32_t* __restrict__ exec_of_expert,
-                                              int32_t* __restrict__ expert_row_off, int32_t* __restrict__ exec_off,
-                                              int32_t* __restrict__ mtile_off, int64_t* __restrict__ stats,
-                                              int n_shared, int shared_rows, PlanExt ext) {
+// What one CTA of the fused decode routing kernel keeps from the plan it computes
+// itself (every CTA plans redundantly from the same counts: no second grid barrier).
+struct PlanLocal {
+  bool write_global;    // this CTA also writes the plan's global outputs
+  int my_tile;          // token tile whose exclusive per-expert prefix is wanted
+  int32_t* row_off;     // [m]        expert_row_off (shared memory)
+  int32_t* exec_off;    // [Et + 1]   exec_off (shared memory)
+  int32_t* tile_base;   // [m]        per-expert prefix of tile my_tile (shared memory)
+};
+
+// Algorithm 1 on one CTA (any multiple of 32 threads with blockDim >= m + G + n_shared);
+// k_plan runs it with 512 threads, k_route_fused with 256.
+template <int STAGE>
+__device__ __forceinline__ void plan_block(const int32_t* __restrict__ tile_cnt, int ntiles, int m, int way,
+                                           double ratio, int mode, int32_t* __restrict__ tile_base,
+                                           int32_t* __restrict__ counts, int32_t* __restrict__ exec_of_expert,
+                                           int32_t* __restrict__ expert_row_off, int32_t* __restrict__ exec_off,
+                                           int32_t* __restrict__ mtile_off, int64_t* __restrict__ stats,
+                                           int n_shared, int shared_rows, PlanExt ext, const PlanLocal* loc) {
+  const bool wg = loc == nullptr || loc->write_global;
+  if (!wg) tile_base = nullptr;
   // Expert parallelism (ext.knob_in): the knob travels with the all-gathered count rows
   // [R, m + 4] (tail [T, mode, ratio lo, ratio hi]); every rank plans with rank 0's, so
   // ranks whose host knobs differ (a per-rank SALC loop) still agree on the global plan.
@@ -597,14 +639,14 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
     mode = ext.knob_in[1];
     ratio = __hiloint2double(ext.knob_in[3], ext.knob_in[2]);
   }
-  if (ext.row_tail && threadIdx.x == 0) {   // this rank's gather row tail
+  if (wg && ext.row_tail && threadIdx.x == 0) {   // this rank's gather row tail
     ext.row_tail[0] = ext.row_T;
     ext.row_tail[1] = mode;
     ext.row_tail[2] = __double2loint(ratio);
     ext.row_tail[3] = __double2hiint(ratio);
   }
   const int ld = ext.ld > 0 ? ext.ld : m;   // row stride of tile_cnt
-  __shared__ __align__(16) int s_tc[kPlanStage];
+  __shared__ __align__(16) int s_tc[STAGE];
   __shared__ int s_cnt[kMaxExperts];
   __shared__ int s_sorted[kMaxExperts];
   __shared__ long long s_excl[kMaxExperts];
@@ -613,11 +655,12 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
   __shared__ int s_xoff[kMaxExec];
   __shared__ long long s_warp[33];
   const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
+  const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
   const int G = (m + way - 1) / way;
   const int E = m + G;
   const int n_tc = ntiles * m;
-  const bool staged = n_tc <= kPlanStage;
+  const bool staged = n_tc <= STAGE;
+  const bool keep_prefix = tile_base != nullptr || loc != nullptr;   // per-tile prefixes wanted
   // 16-byte cp.async needs a 16-byte-aligned source; a caller's counts row (bo_plan_counts /
   // bo_plan_from_counts take any int32 pointer) may be only 4-byte aligned
   const bool vec16 = (reinterpret_cast<uintptr_t>(tile_cnt) & 15u) == 0 && ld == m;
@@ -628,7 +671,7 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
   if (staged) {   // all loads in flight at once (cp.async), not one dependent load per iteration
     const int n16 = vec16 ? n_tc / 4 : 0;
     for (int i = tid; i < n16; i += blockDim.x) cp_async16(s_tc + 4 * i, tile_cnt + 4 * i);
-    for (int i = 4 * n16 + tid; i < n_tc; i += blockDim.x) s_tc[i] = __ldg(tile_cnt + (i / m) * ld + i % m);
+    for (int i = 4 * n16 + tid; i < n_tc; i += blockDim.x) s_tc[i] = __ldcg(tile_cnt + (i / m) * ld + i % m);
     cp_async_wait_all();
   }
   __syncthreads();
@@ -649,7 +692,7 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
     if (ch < nch) {
       int carry = 0;
       for (int c2 = 0; c2 < ch; ++c2) carry += s_chunk[c2 * m + e];
-      if (tile_base)
+      if (keep_prefix)
         for (int t = t0; t < t1; ++t) {
           const int v = s_tc[t * m + e];
           s_tc[t * m + e] = carry;
@@ -659,33 +702,35 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
         int tot = 0;
         for (int c2 = 0; c2 < nch; ++c2) tot += s_chunk[c2 * m + e];
         s_cnt[e] = tot;
-        counts[e] = tot;
+        if (wg) counts[e] = tot;
       }
     }
   } else
-  for (int e = warp; e < m; e += 16) {
+  for (int e = warp; e < m; e += nw) {
     int carry = 0;
     for (int t0 = 0; t0 < ntiles; t0 += 32) {
       const int t = t0 + lane;
-      const int v = t < ntiles ? (staged ? s_tc[t * m + e] : __ldg(tile_cnt + static_cast<int64_t>(t) * ld + e)) : 0;
+      const int v = t < ntiles ? (staged ? s_tc[t * m + e] : __ldcg(tile_cnt + static_cast<int64_t>(t) * ld + e)) : 0;
       int incl = v;
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
         const int o = __shfl_up_sync(0xffffffffu, incl, off);
         if (lane >= off) incl += o;
       }
-      if (tile_base && t < ntiles) {
+      if (keep_prefix && t < ntiles) {
         if (staged) s_tc[t * m + e] = carry + incl - v;   // written back coalesced below
-        else tile_base[static_cast<int64_t>(t) * m + e] = carry + incl - v;
+        else if (tile_base) tile_base[static_cast<int64_t>(t) * m + e] = carry + incl - v;
       }
       carry += __shfl_sync(0xffffffffu, incl, 31);
     }
     if (lane == 0) {
       s_cnt[e] = carry;
-      counts[e] = carry;
+      if (wg) counts[e] = carry;
     }
   }
   __syncthreads();
+  if (loc)   // the fused kernel's own tile (staged: the host guarantees ntiles * m <= STAGE)
+    for (int e = tid; e < m; e += blockDim.x) loc->tile_base[e] = s_tc[loc->my_tile * m + e];
   if (tile_base && staged) {   // per-tile prefixes: 16-byte coalesced stores instead of m-strided ones
     const int n16 = n_tc / 4;
     for (int i = tid; i < n16; i += blockDim.x)
@@ -734,7 +779,7 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
     else if (s_gsize[tid / way] == 1) x_me = tid;        // special case
     else x_me = m + tid / way;                           // united expert of group tid / way
     s_exec[tid] = x_me;
-    exec_of_expert[tid] = x_me;
+    if (wg) exec_of_expert[tid] = x_me;
   }
   __syncthreads();
   // 5. rows per executor, exec_off / mtile_off = exclusive scans over executors;
@@ -756,14 +801,18 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
   long long MT_total;
   const long long moff = block_excl_scan((rows + kBM - 1) / kBM, s_warp, &MT_total);
   const int Et = E + n_shared;
-  if (tid < Et) {
+  if (tid < Et && wg) {
     exec_off[tid] = static_cast<int>(xoff);
     mtile_off[tid] = static_cast<int>(moff);
   }
+  if (tid < Et && loc) loc->exec_off[tid] = static_cast<int>(xoff);
   if (tid < E) s_xoff[tid] = static_cast<int>(xoff);
   if (tid == 0) {
-    exec_off[Et] = static_cast<int>(R_total);
-    mtile_off[Et] = static_cast<int>(MT_total);
+    if (wg) {
+      exec_off[Et] = static_cast<int>(R_total);
+      mtile_off[Et] = static_cast<int>(MT_total);
+    }
+    if (loc) loc->exec_off[Et] = static_cast<int>(R_total);
   }
   R_total -= static_cast<long long>(n_shared) * shared_rows;   // routed rows only, for the statistics
   __syncthreads();
@@ -776,7 +825,8 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
         for (int e = (x_me - m) * way; e < tid; ++e)
           if (s_exec[e] == x_me) off += s_cnt[e];
     }
-    expert_row_off[tid] = off;
+    if (wg) expert_row_off[tid] = off;
+    if (loc) loc->row_off[tid] = off;
   }
   // 7. statistics (P:173 / P:194 access counts, rows per class)
   const int n_acc = __syncthreads_count(tid < E && rows > 0);
@@ -785,7 +835,7 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
   const int n_single = __syncthreads_count(in_s2 && x_me == tid);
   long long r_orig;
   block_excl_scan(tid < m ? rows : 0, s_warp, &r_orig);
-  if (tid == 0) {
+  if (tid == 0 && wg) {
     stats[0] = n_acc;
     stats[1] = n_s1;
     stats[2] = n_uni;
@@ -795,6 +845,17 @@ __global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_c
     stats[6] = S - R_total;
     stats[7] = S;
   }
+  __syncthreads();   // loc's arrays complete for every thread
+}
+
+__global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_cnt, int ntiles, int m, int way,
+                                              double ratio, int mode, int32_t* __restrict__ tile_base,
+                                              int32_t* __restrict__ counts, int32_t* __restrict__ exec_of_expert,
+                                              int32_t* __restrict__ expert_row_off, int32_t* __restrict__ exec_off,
+                                              int32_t* __restrict__ mtile_off, int64_t* __restrict__ stats,
+                                              int n_shared, int shared_rows, PlanExt ext) {
+  plan_block<kPlanStage>(tile_cnt, ntiles, m, way, ratio, mode, tile_base, counts, exec_of_expert, expert_row_off,
+                         exec_off, mtile_off, stats, n_shared, shared_rows, ext, nullptr);
 }
 
 cudaError_t launch_plan(const int32_t* tile_cnt, int ntiles, int m, int way, double ratio, int mode,
@@ -815,14 +876,14 @@ cudaError_t launch_plan(const int32_t* tile_cnt, int ntiles, int m, int way, dou
 // (row_base < 0: no row, e.g. dropped in full brownout).  nrep = 1 on one GPU;
 // under expert parallelism an assignment delegated to an f-sliced united
 // expert has one row per slice.
-__global__ void __launch_bounds__(256) k_permute(const int32_t* __restrict__ topk_id,
-                                                 const float* __restrict__ topk_w, int T, int K, int m, int tile,
-                                                 const int32_t* __restrict__ tile_base,
-                                                 const int32_t* __restrict__ row_base, int nrep,
-                                                 int32_t* __restrict__ row_of, int32_t* __restrict__ row_tok,
-                                                 float* __restrict__ row_w, const uint4* __restrict__ x,
-                                                 uint4* __restrict__ xp, int vec_per_row, int n_shared,
-                                                 const int32_t* __restrict__ shared_off) {
+// One token tile (256 threads); tb_row = the tile's per-expert exclusive prefix
+// (global memory in k_permute, shared memory in k_route_fused).
+__device__ __forceinline__ void permute_tile(const int32_t* __restrict__ topk_id, const float* __restrict__ topk_w,
+                                             int T, int K, int m, int tile, int tile_idx, const int32_t* tb_row,
+                                             const int32_t* row_base, int nrep, int32_t* __restrict__ row_of,
+                                             int32_t* __restrict__ row_tok, float* __restrict__ row_w,
+                                             const uint4* __restrict__ x, uint4* __restrict__ xp, int vec_per_row,
+                                             int n_shared, const int32_t* shared_off) {
   // row_of is [T, KR] with KR = K*nrep + n_shared: slot s replica rep at
   // s*nrep + rep, the shared experts' rows (Eq. 5 second term) after them.
   const int KR = K * nrep + n_shared;
@@ -830,8 +891,8 @@ __global__ void __launch_bounds__(256) k_permute(const int32_t* __restrict__ top
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < 8 * kMaxExperts; i += blockDim.x) (&wcnt[0][0])[i] = 0;
   __syncthreads();
-  const int64_t a0 = static_cast<int64_t>(blockIdx.x) * tile * K;
-  const int64_t a1 = min(static_cast<int64_t>(blockIdx.x + 1) * tile, static_cast<int64_t>(T)) * K;
+  const int64_t a0 = static_cast<int64_t>(tile_idx) * tile * K;
+  const int64_t a1 = min(static_cast<int64_t>(tile_idx + 1) * tile, static_cast<int64_t>(T)) * K;
   const int n = static_cast<int>(a1 - a0);
   const int per_warp = ((n + 8 * 32 - 1) / (8 * 32)) * 32;
   const int w0 = warp * per_warp;
@@ -868,7 +929,7 @@ __global__ void __launch_bounds__(256) k_permute(const int32_t* __restrict__ top
     __syncwarp();
     if (e >= 0) {
       const int64_t a = a0 + i;
-      const int rank = tile_base[static_cast<int64_t>(blockIdx.x) * m + e] + start + __popc(peers & lt);
+      const int rank = tb_row[e] + start + __popc(peers & lt);
       const float w = topk_w[a];
       const int64_t t = a / K;
       const int64_t slot0 = t * KR + (a - t * K) * nrep;
@@ -887,7 +948,7 @@ __global__ void __launch_bounds__(256) k_permute(const int32_t* __restrict__ top
   }
   // shared-expert rows of this tile: token t -> row shared_off[i] + t, weight 1
   if (n_shared > 0) {
-    const int t0 = blockIdx.x * tile;
+    const int t0 = tile_idx * tile;
     const int nt = min(tile, T - t0);
     for (int i = threadIdx.x; i < nt * n_shared; i += blockDim.x) {
       const int tt = i / n_shared, j = i - tt * n_shared;
@@ -903,7 +964,7 @@ __global__ void __launch_bounds__(256) k_permute(const int32_t* __restrict__ top
   // this CTA and is visible after the barrier.
   if (xp) {
     __syncthreads();
-    const int t0 = blockIdx.x * tile;
+    const int t0 = tile_idx * tile;
     const int nt = min(tile, T - t0);
     const int total = nt * vec_per_row;
     constexpr int U = 4;   // loads in flight per thread before the stores (the copy is latency-bound)
@@ -934,6 +995,18 @@ __global__ void __launch_bounds__(256) k_permute(const int32_t* __restrict__ top
   }
 }
 
+__global__ void __launch_bounds__(256) k_permute(const int32_t* __restrict__ topk_id,
+                                                 const float* __restrict__ topk_w, int T, int K, int m, int tile,
+                                                 const int32_t* __restrict__ tile_base,
+                                                 const int32_t* __restrict__ row_base, int nrep,
+                                                 int32_t* __restrict__ row_of, int32_t* __restrict__ row_tok,
+                                                 float* __restrict__ row_w, const uint4* __restrict__ x,
+                                                 uint4* __restrict__ xp, int vec_per_row, int n_shared,
+                                                 const int32_t* __restrict__ shared_off) {
+  permute_tile(topk_id, topk_w, T, K, m, tile, blockIdx.x, tile_base + static_cast<int64_t>(blockIdx.x) * m,
+               row_base, nrep, row_of, row_tok, row_w, x, xp, vec_per_row, n_shared, shared_off);
+}
+
 cudaError_t launch_permute(const int32_t* topk_id, const float* topk_w, int T, int K, int m, int tile,
                            const int32_t* tile_base, const int32_t* row_base, int nrep, int32_t* row_of,
                            int32_t* row_tok, float* row_w, cudaStream_t s, int dtype, const void* x, void* xp,
@@ -945,6 +1018,91 @@ cudaError_t launch_permute(const int32_t* topk_id, const float* topk_w, int T, i
                                    row_w, static_cast<const uint4*>(x), static_cast<uint4*>(xp), vec, n_shared,
                                    shared_off);
   return cudaGetLastError();
+}
+
+// ------------------------------------------------- fused decode routing
+// Decode-sized batches (m <= 32 on the split-warp router, gather inside the permute):
+// Eq. 8 + Eq. 7 + histogram, Algorithm 1, the permutation and concat_tokens
+// in ONE cooperative launch instead of three (Alg. 1 is
+// "negligible", so its launch and dependency gaps should not cost a kernel).
+// Phase 1 = one k_router_split tile per CTA; a grid barrier (the tile histograms of
+// every CTA are needed); phase 2: every CTA runs Algorithm 1 itself on the same
+// histograms (identical results; ntiles * m ints from L2, no second barrier), CTA 0
+// also writes the plan's global outputs; phase 3 = k_permute's tile with the tile
+// prefix, expert row offsets and shared-expert offsets from the CTA's own copy.
+template <typename T, int MAXM>
+__global__ void __launch_bounds__(256)
+    k_route_fused(const T* __restrict__ x, const T* __restrict__ Wr, int Tn, int d, int m, int K, int tpc,
+                  float* __restrict__ logits, int32_t* __restrict__ topk_id, float* __restrict__ topk_w,
+                  int32_t* __restrict__ tile_cnt, int way, double ratio, int mode, int32_t* __restrict__ tile_base,
+                  int32_t* __restrict__ counts, int32_t* __restrict__ exec_of_expert,
+                  int32_t* __restrict__ expert_row_off, int32_t* __restrict__ exec_off,
+                  int32_t* __restrict__ mtile_off, int64_t* __restrict__ stats, int n_shared,
+                  int32_t* __restrict__ row_of, int32_t* __restrict__ row_tok, float* __restrict__ row_w,
+                  uint4* __restrict__ xp, int vec_per_row) {
+  __shared__ int32_t s_row_off[MAXM];
+  __shared__ int32_t s_xoff[kRouteFusedMaxExec + 1];
+  __shared__ int32_t s_tb[MAXM];
+  router_split_tile<T, MAXM>(x, Wr, Tn, d, m, K, tpc, logits, topk_id, topk_w, tile_cnt, blockIdx.x);
+  cg::this_grid().sync();   // every tile histogram written (and visible)
+  PlanLocal loc{blockIdx.x == 0, static_cast<int>(blockIdx.x), s_row_off, s_xoff, s_tb};
+  plan_block<kPlanStageFused>(tile_cnt, gridDim.x, m, way, ratio, mode, tile_base, counts, exec_of_expert,
+                              expert_row_off, exec_off, mtile_off, stats, n_shared, Tn, PlanExt(), &loc);
+  const int E = m + (m + way - 1) / way;
+  permute_tile(topk_id, topk_w, Tn, K, m, tpc, blockIdx.x, s_tb, s_row_off, 1, row_of, row_tok, row_w,
+               reinterpret_cast<const uint4*>(x), xp, vec_per_row, n_shared, s_xoff + E);
+}
+
+template <typename T, int MAXM>
+static int route_fused_capacity(int num_sms) {
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_route_fused<T, MAXM>, 256, 0) != cudaSuccess) return 0;
+  return nb * num_sms;
+}
+
+bool route_fused_ok(int dtype, int m, int way, int T, int tpc, int n_shared, int num_sms) {
+  if (m > 32 || tpc <= 0 || T <= 0) return false;
+  const int ntiles = (T + tpc - 1) / tpc;
+  const int Et = m + (m + way - 1) / way + n_shared;
+  if (ntiles * m > kPlanStageFused || Et > kRouteFusedMaxExec) return false;
+  int cap;
+  if (dtype == 0) cap = m <= 8 ? route_fused_capacity<__nv_bfloat16, 8>(num_sms)
+                               : (m <= 16 ? route_fused_capacity<__nv_bfloat16, 16>(num_sms)
+                                          : route_fused_capacity<__nv_bfloat16, 32>(num_sms));
+  else cap = m <= 8 ? route_fused_capacity<float, 8>(num_sms)
+                    : (m <= 16 ? route_fused_capacity<float, 16>(num_sms) : route_fused_capacity<float, 32>(num_sms));
+  return ntiles <= cap;   // a cooperative grid must be co-resident
+}
+
+cudaError_t launch_route_fused(int dtype, const void* x, const void* Wr, int T, int d, int m, int K, int tpc,
+                               float* logits, int32_t* topk_id, float* topk_w, int32_t* tile_cnt, int way,
+                               double ratio, int mode, int32_t* tile_base, int32_t* counts, int32_t* exec_of_expert,
+                               int32_t* expert_row_off, int32_t* exec_off, int32_t* mtile_off, int64_t* stats,
+                               int n_shared, int32_t* row_of, int32_t* row_tok, float* row_w, void* xp,
+                               cudaStream_t s) {
+  const int ntiles = (T + tpc - 1) / tpc;
+  const int vec = d * (dtype == 0 ? 2 : 4) / 16;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(ntiles));
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  uint4* xpv = static_cast<uint4*>(xp);
+#define BO_RF(TYPE, M)                                                                                         \
+  return cudaLaunchKernelEx(&cfg, k_route_fused<TYPE, M>, static_cast<const TYPE*>(x),                         \
+                            static_cast<const TYPE*>(Wr), T, d, m, K, tpc, logits, topk_id, topk_w, tile_cnt,  \
+                            way, ratio, mode, tile_base, counts, exec_of_expert, expert_row_off, exec_off,     \
+                            mtile_off, stats, n_shared, row_of, row_tok, row_w, xpv, vec)
+  if (dtype == 0) {
+    if (m <= 8) BO_RF(__nv_bfloat16, 8); else if (m <= 16) BO_RF(__nv_bfloat16, 16); else BO_RF(__nv_bfloat16, 32);
+  } else {
+    if (m <= 8) BO_RF(float, 8); else if (m <= 16) BO_RF(float, 16); else BO_RF(float, 32);
+  }
+#undef BO_RF
 }
 
 // ----------------------------------------------------------------- gather

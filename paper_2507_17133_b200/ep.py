@@ -67,11 +67,17 @@ class EPContext:
         self.ws = torch.empty(L.total_bytes, dtype=torch.uint8, device=device)
         self.T = 0
 
-    def __del__(self):
+    def close(self):
+        """bo_ep_destroy (also on garbage collection).  Destroy every CUDA graph that
+        captured this context's forward first: such a graph holds the communicator's
+        persistent NCCL resources, and destroying the communicator under it blocks."""
         h = getattr(self, "_h", None)
         if h is not None and h.value:
             _lib.bo_ep_destroy(h)
             self._h = None
+
+    def __del__(self):
+        self.close()
 
     # -- static ---------------------------------------------------------------
     @property

@@ -354,13 +354,8 @@ def test_two_processes_one_gpu_gloo_real_kernels(padded):
     assert _rel(y.astype(np.float64), ref.y) <= 2e-2
 
 
-@pytest.mark.gpu
-@pytest.mark.parametrize("padded", [True, False], ids=["padded_graph", "exact"])
-def test_nccl_world1_library_forward(padded):
-    """The library-owned NCCL path (bo_ep_init + bo_ep_forward: ncclAllGather of
-    the count rows, grouped ncclSend / ncclRecv exchanges) on a world of one,
-    captured in a CUDA graph in padded mode.  Router inputs are exactly
-    representable, so the oracle's own Eq. 8 path is the reference."""
+def _nccl_world1_worker(padded, q):
+    """Child process of test_nccl_world1_library_forward: returns y's relative error."""
     from paper_2507_17133_b200.ep import EPContext
     cfg = GCFG
     ratio = 0.5
@@ -379,6 +374,7 @@ def test_nccl_world1_library_forward(padded):
     with torch.cuda.stream(s):
         y = ctx.forward(xin, Wre, ex, un)      # warm-up
     torch.cuda.synchronize()
+    graph = None
     if padded:
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=s):
@@ -390,4 +386,36 @@ def test_nccl_world1_library_forward(padded):
         with torch.cuda.stream(s):
             y = ctx.forward(xin, Wre, ex, un)
     torch.cuda.synchronize()
-    assert _rel(y.double().cpu().numpy(), want) <= 2e-2
+    err = _rel(y.double().cpu().numpy(), want)
+    # A graph that captured NCCL work holds the communicator's persistent resources:
+    # destroy it before the communicator (bo_ep_destroy; include/brownout.h).
+    del graph
+    torch.cuda.synchronize()
+    ctx.close()
+    q.put(float(err))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("padded", [True, False], ids=["padded_graph", "exact"])
+def test_nccl_world1_library_forward(padded):
+    """The library-owned NCCL path (bo_ep_init + bo_ep_forward: ncclAllGather of
+    the count rows, grouped ncclSend / ncclRecv exchanges) on a world of one,
+    captured in a CUDA graph in padded mode.  Router inputs are exactly
+    representable, so the oracle's own Eq. 8 path is the reference.  Runs in a
+    child process under a deadline, so a communicator that never finishes (or a
+    teardown that blocks) fails the test instead of hanging the suite."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_world1_worker, args=(padded, q))
+    p.start()
+    try:
+        err = q.get(timeout=300)
+    except Exception:
+        p.kill()
+        pytest.fail("NCCL world-1 forward did not finish within 300 s")
+    p.join(timeout=120)
+    if p.is_alive():
+        p.kill()
+        pytest.fail("NCCL world-1 process did not exit (communicator teardown blocked)")
+    assert p.exitcode == 0
+    assert err <= 2e-2

@@ -62,6 +62,14 @@ CASES = [
     (C("m32_k7_small", d=256, f=128, m=32, K=7, way=8, T=1300, ratio=0.5, dtype="bf16", config_id=67),
      {"BO_ROUTER_MMA": "0"}, "small"),
     (C("m8_fp32_small", d=64, f=128, m=8, K=2, way=4, T=32, ratio=0.5, dtype="fp32", config_id=68), {}, "split"),
+    # the split-warp router as its own launch (BO_ROUTE_FUSED=0), not inside k_route_fused
+    (C("m8_split_tpc1_unfused", d=512, f=128, m=8, K=2, way=4, T=100, ratio=0.5, dtype="bf16", config_id=75),
+     {"BO_ROUTE_FUSED": "0"}, "split"),
+    (C("m16_k3_split_tpc4_unfused", d=256, f=128, m=16, K=3, way=3, T=700, ratio=0.5, dtype="bf16",
+       config_id=76), {"BO_ROUTE_FUSED": "0"}, "split"),
+    # k_route_fused with shared experts' rows (Eq. 5 second term) and a ragged last group
+    (C("m12_k3_fused_w5", d=256, f=128, m=12, K=3, way=5, T=150, ratio=0.5, dtype="bf16", config_id=77), {},
+     "split"),
     (C("m32_tc_bn32", d=3072, f=128, m=32, K=4, way=8, T=200, ratio=0.5, dtype="bf16", config_id=69), {}, "tc"),
     (C("m64_k10_tc", d=256, f=128, m=64, K=10, way=5, T=390, ratio=0.5, dtype="bf16", config_id=70), {}, "tc"),
     (C("m128_k8_tc", d=512, f=128, m=128, K=8, way=4, T=390, ratio=0.5, dtype="bf16", config_id=71), {}, "tc"),
@@ -106,7 +114,15 @@ def test_every_router_exact_routing_and_output(case, ties, monkeypatch):
     cfg, env, kind = case
     _expect_kernel(kind, cfg)
     moe, y, dbg, ref = _run(cfg, env, monkeypatch, ties, cfg.ratio)
-    assert moe.last_kernels()[0] == "router_topk"
+    # decode-sized split-router steps run a1-a5 in one cooperative launch by default
+    fused = kind == "split" and env.get("BO_ROUTE_FUSED") != "0"
+    assert moe.last_kernels()[0] == ("route_fused" if fused else "router_topk"), moe.last_kernels()
+    st = dbg["stats"].cpu().numpy()
+    s = ref.plan.stats
+    assert list(st[:7]) == [s["executors_accessed"], s["n_s1"], s["n_united"], s["n_singleton"],
+                            s["rows_original"], s["rows_united"], s["rows_dropped"]]
+    mt = np.diff(ref.perm.exec_off)
+    assert np.array_equal(np.diff(dbg["mtile_off"].cpu().numpy()[:len(mt) + 1]), (mt + 127) // 128)
     Lg = dbg["logits"].cpu().double().numpy()
     assert np.array_equal(Lg, ref.logits), "Eq. 8 not exact on exactly representable inputs"
     if ties:   # the tie rule is really exercised: some token has equal logits around its K-th choice
@@ -172,6 +188,50 @@ def test_random_shapes_exact_router(cfg, ties, monkeypatch):
     assert np.array_equal(dbg["exec_of_expert"].cpu().numpy(), ref.plan.exec_of_expert)
     assert np.array_equal(dbg["exec_off"].cpu().numpy(), ref.perm.exec_off)
     assert np.array_equal(dbg["row_of"].cpu().numpy(), ref.perm.row_of)
+    yg, yr = _np(y), ref.y
+    den = np.where(np.abs(yr).max(1) == 0, 1.0, np.abs(yr).max(1))
+    assert (np.abs(yg - yr).max(1) / den).max() <= OUT_TOL
+
+
+@pytest.mark.parametrize("fused", ["1", "0"], ids=["route_fused", "separate"])
+@pytest.mark.parametrize("ratio", [0.0, 0.5, 1.0])
+def test_decode_routing_with_shared_experts(fused, ratio, monkeypatch):
+    """k_route_fused (Alg. 1 run by every CTA from the same tile histograms, the
+    permutation from each CTA's own copy of the plan) with the N_s shared experts of
+    Eq. 5 appended after the routed executors, against the oracle's own
+    Eq. 8 path; and the same step as separate launches."""
+    from paper_2507_17133_b200 import BrownoutMoE
+    monkeypatch.setenv("BO_ROUTE_FUSED", fused)
+    cfg = C("sh_fused", d=256, f=256, m=8, K=2, way=4, T=120, ratio=ratio, dtype="bf16", Ns=2, config_id=78)
+    x, Wr = S.make_exact_router_inputs(cfg, ties=True)
+    lay = S.make_layer(cfg)
+    uni = S.make_united_random(cfg)
+    moe = BrownoutMoE(cfg.d, cfg.f, cfg.m, cfg.K, cfg.way, dtype=cfg.dtype, max_tokens=cfg.T, num_shared=cfg.Ns)
+    moe.set_brownout(ratio)
+    g = {k: v.cuda() for k, v in lay.items()}
+    u = {k: v.cuda() for k, v in uni.items()}
+    y = moe.forward(x.cuda(), Wr.cuda(), (g["Wg"], g["Wu"], g["Wd"]), (u["UWg"], u["UWu"], u["UWd"]),
+                    shared=(g["SWg"], g["SWu"], g["SWd"]))
+    torch.cuda.synchronize()
+    assert moe.last_kernels()[0] == ("route_fused" if fused == "1" else "router_topk")
+    dbg = moe.debug_arrays(cfg.T)
+    ex = tuple(_np(lay[k]) for k in ("Wg", "Wu", "Wd"))
+    un = tuple(_np(uni[k]) for k in ("UWg", "UWu", "UWd"))
+    sh = tuple(_np(lay[k]) for k in ("SWg", "SWu", "SWd"))
+    ref = O.moe_forward(_np(x), _np(Wr), ex, un, cfg.K, cfg.way, ratio, shared=sh)
+    assert np.array_equal(dbg["topk_id"].cpu().numpy(), ref.ids)
+    assert np.array_equal(dbg["exec_of_expert"].cpu().numpy(), ref.plan.exec_of_expert)
+    T, K, Ns, E = cfg.T, cfg.K, cfg.Ns, cfg.m + cfg.G
+    eo = dbg["exec_off"].cpu().numpy()
+    R = int(ref.perm.exec_off[-1])
+    assert np.array_equal(eo[:E + 1], ref.perm.exec_off)
+    assert np.array_equal(eo[E:], R + T * np.arange(Ns + 1))     # shared executors: every token, in order
+    ro = dbg["row_of"].cpu().numpy().reshape(T, K + Ns)
+    assert np.array_equal(ro[:, :K].reshape(-1), ref.perm.row_of)
+    for j in range(Ns):
+        assert np.array_equal(ro[:, K + j], R + j * T + np.arange(T))
+    assert np.array_equal(dbg["row_tok"][:R].cpu().numpy(), ref.perm.row_tok)
+    assert np.array_equal(dbg["row_tok"][R:R + Ns * T].cpu().numpy(), np.tile(np.arange(T), Ns))
     yg, yr = _np(y), ref.y
     den = np.where(np.abs(yr).max(1) == 0, 1.0, np.abs(yr).max(1))
     assert (np.abs(yg - yr).max(1) / den).max() <= OUT_TOL
