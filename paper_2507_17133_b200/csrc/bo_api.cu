@@ -528,7 +528,7 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   const bool gather_in_permute = Rt <= kSplitRows * 2 && !c.dedup_united;
   // Decode-sized steps on the split-warp router: a1-a5 in one cooperative launch
   const int tpc = h->opt.router_split ? bo::router_split_tpc(static_cast<int>(T), h->num_sms) : 0;
-  const bool route_fused = h->opt.route_fused && !logits_in && gather_in_permute && Wr != nullptr &&
+  const bool route_fused = h->opt.route_fused && !logits_in && !c.dedup_united && Wr != nullptr &&
                            bo::router_small_ok(dt, m, d) && tpc > 0 &&
                            !(h->opt.router_mma && bo::router_mma_ok(dt, m, d, static_cast<int>(T), h->num_sms)) &&
                            bo::route_fused_ok(dt, m, c.way, static_cast<int>(T), tpc, Ns, h->num_sms);
@@ -537,11 +537,11 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
     prof.mark(launches, "route_fused");
     BO_CUDA(bo::launch_route_fused(dt, x, Wr, static_cast<int>(T), d, m, K, tpc, at<float>(ws, L.logits),
                                    at<int32_t>(ws, L.topk_id), at<float>(ws, L.topk_w), at<int32_t>(ws, L.tile_cnt),
-                                   c.way, h->ratio, h->mode, at<int32_t>(ws, L.tile_base),
-                                   at<int32_t>(ws, L.counts), at<int32_t>(ws, L.exec_of_expert),
-                                   at<int32_t>(ws, L.expert_row_off), at<int32_t>(ws, L.exec_off),
-                                   at<int32_t>(ws, L.mtile_off), at<int64_t>(ws, L.stats), Ns, row_of,
-                                   at<int32_t>(ws, L.row_tok), row_w, at<char>(ws, L.xp), s),
+                                   c.way, h->ratio, h->mode, at<int32_t>(ws, L.counts),
+                                   at<int32_t>(ws, L.exec_of_expert), at<int32_t>(ws, L.expert_row_off),
+                                   at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off),
+                                   at<int64_t>(ws, L.stats), Ns, row_of, at<int32_t>(ws, L.row_tok), row_w,
+                                   gather_in_permute ? at<char>(ws, L.xp) : nullptr, s),
             "route_fused");
     ++launches;
     h->route_T = T;

@@ -134,13 +134,14 @@ cudaError_t launch_permute(const int32_t* topk_id, const float* topk_w, int T, i
                            void* xp = nullptr, int d = 0, int n_shared = 0, const int32_t* shared_off = nullptr);
 
 // Decode-sized steps on one GPU: router (split-warp, m <= 32) + Eq. 7 + histogram, Alg. 1
-// and the permutation + gather in one cooperative launch (every plan output written as by
-// launch_plan / launch_permute).  route_fused_ok: the shapes fit and the grid is co-resident.
-constexpr int kRouteFusedMaxExec = 160;   // m + G + N_s executors the fused kernel's plan copy holds
+// and the permutation (+ the gather when xp != nullptr) in one cooperative launch, every
+// plan output written as by launch_plan / launch_permute (the per-tile prefixes stay in
+// shared memory).  route_fused_ok: the shapes fit and the grid is co-resident.
+constexpr int kRouteFusedMaxExec = 64;   // m + G + N_s executors (two per lane of the planning warp)
 bool route_fused_ok(int dtype, int m, int way, int T, int tpc, int n_shared, int num_sms);
 cudaError_t launch_route_fused(int dtype, const void* x, const void* Wr, int T, int d, int m, int K, int tpc,
                                float* logits, int32_t* topk_id, float* topk_w, int32_t* tile_cnt, int way,
-                               double ratio, int mode, int32_t* tile_base, int32_t* counts, int32_t* exec_of_expert,
+                               double ratio, int mode, int32_t* counts, int32_t* exec_of_expert,
                                int32_t* expert_row_off, int32_t* exec_off, int32_t* mtile_off, int64_t* stats,
                                int n_shared, int32_t* row_of, int32_t* row_tok, float* row_w, void* xp,
                                cudaStream_t s);

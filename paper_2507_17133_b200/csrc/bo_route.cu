@@ -608,30 +608,14 @@ __device__ __forceinline__ long long block_excl_scan(long long v, long long* s_w
   return r;
 }
 
-constexpr int kPlanStage = 8192;       // tile histograms staged in shared memory when ntiles*m fits
-constexpr int kPlanStageFused = 4096;  // the fused decode routing kernel's stage (static smem budget)
+constexpr int kPlanStage = 8192;    // tile histograms staged in shared memory when ntiles*m fits
 
-// What one CTA of the fused decode routing kernel keeps from the plan it computes
-// itself (every CTA plans redundantly from the same counts: no second grid barrier).
-struct PlanLocal {
-  bool write_global;    // this CTA also writes the plan's global outputs
-  int my_tile;          // token tile whose exclusive per-expert prefix is wanted
-  int32_t* row_off;     // [m]        expert_row_off (shared memory)
-  int32_t* exec_off;    // [Et + 1]   exec_off (shared memory)
-  int32_t* tile_base;   // [m]        per-expert prefix of tile my_tile (shared memory)
-};
-
-// Algorithm 1 on one CTA (any multiple of 32 threads with blockDim >= m + G + n_shared);
-// k_plan runs it with 512 threads, k_route_fused with 256.
-template <int STAGE>
-__device__ __forceinline__ void plan_block(const int32_t* __restrict__ tile_cnt, int ntiles, int m, int way,
-                                           double ratio, int mode, int32_t* __restrict__ tile_base,
-                                           int32_t* __restrict__ counts, int32_t* __restrict__ exec_of_expert,
-                                           int32_t* __restrict__ expert_row_off, int32_t* __restrict__ exec_off,
-                                           int32_t* __restrict__ mtile_off, int64_t* __restrict__ stats,
-                                           int n_shared, int shared_rows, PlanExt ext, const PlanLocal* loc) {
-  const bool wg = loc == nullptr || loc->write_global;
-  if (!wg) tile_base = nullptr;
+__global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_cnt, int ntiles, int m, int way,
+                                              double ratio, int mode, int32_t* __restrict__ tile_base,
+                                              int32_t* __restrict__ counts, int32_t* __restrict__ exec_of_expert,
+                                              int32_t* __restrict__ expert_row_off, int32_t* __restrict__ exec_off,
+                                              int32_t* __restrict__ mtile_off, int64_t* __restrict__ stats,
+                                              int n_shared, int shared_rows, PlanExt ext) {
   // Expert parallelism (ext.knob_in): the knob travels with the all-gathered count rows
   // [R, m + 4] (tail [T, mode, ratio lo, ratio hi]); every rank plans with rank 0's, so
   // ranks whose host knobs differ (a per-rank SALC loop) still agree on the global plan.
@@ -639,14 +623,14 @@ __device__ __forceinline__ void plan_block(const int32_t* __restrict__ tile_cnt,
     mode = ext.knob_in[1];
     ratio = __hiloint2double(ext.knob_in[3], ext.knob_in[2]);
   }
-  if (wg && ext.row_tail && threadIdx.x == 0) {   // this rank's gather row tail
+  if (ext.row_tail && threadIdx.x == 0) {   // this rank's gather row tail
     ext.row_tail[0] = ext.row_T;
     ext.row_tail[1] = mode;
     ext.row_tail[2] = __double2loint(ratio);
     ext.row_tail[3] = __double2hiint(ratio);
   }
   const int ld = ext.ld > 0 ? ext.ld : m;   // row stride of tile_cnt
-  __shared__ __align__(16) int s_tc[STAGE];
+  __shared__ __align__(16) int s_tc[kPlanStage];
   __shared__ int s_cnt[kMaxExperts];
   __shared__ int s_sorted[kMaxExperts];
   __shared__ long long s_excl[kMaxExperts];
@@ -655,12 +639,11 @@ __device__ __forceinline__ void plan_block(const int32_t* __restrict__ tile_cnt,
   __shared__ int s_xoff[kMaxExec];
   __shared__ long long s_warp[33];
   const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
+  const int warp = tid >> 5, lane = tid & 31;
   const int G = (m + way - 1) / way;
   const int E = m + G;
   const int n_tc = ntiles * m;
-  const bool staged = n_tc <= STAGE;
-  const bool keep_prefix = tile_base != nullptr || loc != nullptr;   // per-tile prefixes wanted
+  const bool staged = n_tc <= kPlanStage;
   // 16-byte cp.async needs a 16-byte-aligned source; a caller's counts row (bo_plan_counts /
   // bo_plan_from_counts take any int32 pointer) may be only 4-byte aligned
   const bool vec16 = (reinterpret_cast<uintptr_t>(tile_cnt) & 15u) == 0 && ld == m;
@@ -671,7 +654,7 @@ __device__ __forceinline__ void plan_block(const int32_t* __restrict__ tile_cnt,
   if (staged) {   // all loads in flight at once (cp.async), not one dependent load per iteration
     const int n16 = vec16 ? n_tc / 4 : 0;
     for (int i = tid; i < n16; i += blockDim.x) cp_async16(s_tc + 4 * i, tile_cnt + 4 * i);
-    for (int i = 4 * n16 + tid; i < n_tc; i += blockDim.x) s_tc[i] = __ldcg(tile_cnt + (i / m) * ld + i % m);
+    for (int i = 4 * n16 + tid; i < n_tc; i += blockDim.x) s_tc[i] = __ldg(tile_cnt + (i / m) * ld + i % m);
     cp_async_wait_all();
   }
   __syncthreads();
@@ -692,7 +675,7 @@ __device__ __forceinline__ void plan_block(const int32_t* __restrict__ tile_cnt,
     if (ch < nch) {
       int carry = 0;
       for (int c2 = 0; c2 < ch; ++c2) carry += s_chunk[c2 * m + e];
-      if (keep_prefix)
+      if (tile_base)
         for (int t = t0; t < t1; ++t) {
           const int v = s_tc[t * m + e];
           s_tc[t * m + e] = carry;
@@ -702,35 +685,33 @@ __device__ __forceinline__ void plan_block(const int32_t* __restrict__ tile_cnt,
         int tot = 0;
         for (int c2 = 0; c2 < nch; ++c2) tot += s_chunk[c2 * m + e];
         s_cnt[e] = tot;
-        if (wg) counts[e] = tot;
+        counts[e] = tot;
       }
     }
   } else
-  for (int e = warp; e < m; e += nw) {
+  for (int e = warp; e < m; e += 16) {
     int carry = 0;
     for (int t0 = 0; t0 < ntiles; t0 += 32) {
       const int t = t0 + lane;
-      const int v = t < ntiles ? (staged ? s_tc[t * m + e] : __ldcg(tile_cnt + static_cast<int64_t>(t) * ld + e)) : 0;
+      const int v = t < ntiles ? (staged ? s_tc[t * m + e] : __ldg(tile_cnt + static_cast<int64_t>(t) * ld + e)) : 0;
       int incl = v;
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
         const int o = __shfl_up_sync(0xffffffffu, incl, off);
         if (lane >= off) incl += o;
       }
-      if (keep_prefix && t < ntiles) {
+      if (tile_base && t < ntiles) {
         if (staged) s_tc[t * m + e] = carry + incl - v;   // written back coalesced below
-        else if (tile_base) tile_base[static_cast<int64_t>(t) * m + e] = carry + incl - v;
+        else tile_base[static_cast<int64_t>(t) * m + e] = carry + incl - v;
       }
       carry += __shfl_sync(0xffffffffu, incl, 31);
     }
     if (lane == 0) {
       s_cnt[e] = carry;
-      if (wg) counts[e] = carry;
+      counts[e] = carry;
     }
   }
   __syncthreads();
-  if (loc)   // the fused kernel's own tile (staged: the host guarantees ntiles * m <= STAGE)
-    for (int e = tid; e < m; e += blockDim.x) loc->tile_base[e] = s_tc[loc->my_tile * m + e];
   if (tile_base && staged) {   // per-tile prefixes: 16-byte coalesced stores instead of m-strided ones
     const int n16 = n_tc / 4;
     for (int i = tid; i < n16; i += blockDim.x)
@@ -779,7 +760,7 @@ __device__ __forceinline__ void plan_block(const int32_t* __restrict__ tile_cnt,
     else if (s_gsize[tid / way] == 1) x_me = tid;        // special case
     else x_me = m + tid / way;                           // united expert of group tid / way
     s_exec[tid] = x_me;
-    if (wg) exec_of_expert[tid] = x_me;
+    exec_of_expert[tid] = x_me;
   }
   __syncthreads();
   // 5. rows per executor, exec_off / mtile_off = exclusive scans over executors;
@@ -801,18 +782,14 @@ __device__ __forceinline__ void plan_block(const int32_t* __restrict__ tile_cnt,
   long long MT_total;
   const long long moff = block_excl_scan((rows + kBM - 1) / kBM, s_warp, &MT_total);
   const int Et = E + n_shared;
-  if (tid < Et && wg) {
+  if (tid < Et) {
     exec_off[tid] = static_cast<int>(xoff);
     mtile_off[tid] = static_cast<int>(moff);
   }
-  if (tid < Et && loc) loc->exec_off[tid] = static_cast<int>(xoff);
   if (tid < E) s_xoff[tid] = static_cast<int>(xoff);
   if (tid == 0) {
-    if (wg) {
-      exec_off[Et] = static_cast<int>(R_total);
-      mtile_off[Et] = static_cast<int>(MT_total);
-    }
-    if (loc) loc->exec_off[Et] = static_cast<int>(R_total);
+    exec_off[Et] = static_cast<int>(R_total);
+    mtile_off[Et] = static_cast<int>(MT_total);
   }
   R_total -= static_cast<long long>(n_shared) * shared_rows;   // routed rows only, for the statistics
   __syncthreads();
@@ -825,8 +802,7 @@ __device__ __forceinline__ void plan_block(const int32_t* __restrict__ tile_cnt,
         for (int e = (x_me - m) * way; e < tid; ++e)
           if (s_exec[e] == x_me) off += s_cnt[e];
     }
-    if (wg) expert_row_off[tid] = off;
-    if (loc) loc->row_off[tid] = off;
+    expert_row_off[tid] = off;
   }
   // 7. statistics (P:173 / P:194 access counts, rows per class)
   const int n_acc = __syncthreads_count(tid < E && rows > 0);
@@ -835,7 +811,7 @@ __device__ __forceinline__ void plan_block(const int32_t* __restrict__ tile_cnt,
   const int n_single = __syncthreads_count(in_s2 && x_me == tid);
   long long r_orig;
   block_excl_scan(tid < m ? rows : 0, s_warp, &r_orig);
-  if (tid == 0 && wg) {
+  if (tid == 0) {
     stats[0] = n_acc;
     stats[1] = n_s1;
     stats[2] = n_uni;
@@ -845,17 +821,6 @@ __device__ __forceinline__ void plan_block(const int32_t* __restrict__ tile_cnt,
     stats[6] = S - R_total;
     stats[7] = S;
   }
-  __syncthreads();   // loc's arrays complete for every thread
-}
-
-__global__ void __launch_bounds__(512) k_plan(const int32_t* __restrict__ tile_cnt, int ntiles, int m, int way,
-                                              double ratio, int mode, int32_t* __restrict__ tile_base,
-                                              int32_t* __restrict__ counts, int32_t* __restrict__ exec_of_expert,
-                                              int32_t* __restrict__ expert_row_off, int32_t* __restrict__ exec_off,
-                                              int32_t* __restrict__ mtile_off, int64_t* __restrict__ stats,
-                                              int n_shared, int shared_rows, PlanExt ext) {
-  plan_block<kPlanStage>(tile_cnt, ntiles, m, way, ratio, mode, tile_base, counts, exec_of_expert, expert_row_off,
-                         exec_off, mtile_off, stats, n_shared, shared_rows, ext, nullptr);
 }
 
 cudaError_t launch_plan(const int32_t* tile_cnt, int ntiles, int m, int way, double ratio, int mode,
@@ -1021,35 +986,205 @@ cudaError_t launch_permute(const int32_t* topk_id, const float* topk_w, int T, i
 }
 
 // ------------------------------------------------- fused decode routing
-// Decode-sized batches (m <= 32 on the split-warp router, gather inside the permute):
-// Eq. 8 + Eq. 7 + histogram, Algorithm 1, the permutation and concat_tokens
-// in ONE cooperative launch instead of three (Alg. 1 is
+// Decode-sized batches (m <= 32 on the split-warp router): Eq. 8 + Eq. 7 + histogram,
+// Algorithm 1, the permutation (and concat_tokens, when the gather rides in the
+// permute) in ONE cooperative launch instead of three (Alg. 1 is
 // "negligible", so its launch and dependency gaps should not cost a kernel).
-// Phase 1 = one k_router_split tile per CTA; a grid barrier (the tile histograms of
-// every CTA are needed); phase 2: every CTA runs Algorithm 1 itself on the same
-// histograms (identical results; ntiles * m ints from L2, no second barrier), CTA 0
-// also writes the plan's global outputs; phase 3 = k_permute's tile with the tile
-// prefix, expert row offsets and shared-expert offsets from the CTA's own copy.
+// Phase 1 = one k_router_split tile per CTA; a grid barrier (every tile histogram is
+// needed); phase 2: every CTA runs Algorithm 1 itself, warp-synchronously on warp 0
+// (lane = expert), on the same histograms (identical results, ntiles * m ints from L2,
+// no second barrier); CTA 0 also writes the plan's global outputs; phase 3 = k_permute's
+// tile with the tile prefix, expert row offsets and shared-expert offsets from the
+// CTA's own copy of the plan.
+
+// Algorithm 1 for m <= 32 experts and Et = m + G + N_s <= 64 executors on one
+// warp: lane e < m holds cnt_e (Alg. 1 input).  The same steps, readings and
+// outputs as k_plan: order by (cnt desc, id asc) (D5), exclusive prefix in that order,
+// S1 iff prefix < Tcov = S (1 - ratio) in fp64 (D1-D3), inactive experts nowhere (D6), S2
+// grouped by floor(e / way), single-member groups keep the original, full mode
+// drops S2 (-2), rows in (executor, expert, token) order (D11), the N_s shared executors
+// last with shared_rows rows each.  s_row_off[m], s_xoff[Et + 1] receive expert_row_off /
+// exec_off; write_global: also the global plan arrays.
+__device__ __forceinline__ void plan_small_warp(int cnt, int m, int way, double ratio, int mode, int n_shared,
+                                                int shared_rows, int32_t* s_row_off, int32_t* s_xoff,
+                                                bool write_global, int32_t* __restrict__ counts,
+                                                int32_t* __restrict__ exec_of_expert,
+                                                int32_t* __restrict__ expert_row_off, int32_t* __restrict__ exec_off,
+                                                int32_t* __restrict__ mtile_off, int64_t* __restrict__ stats) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int e = lane;
+  const bool ve = e < m;
+  const int G = (m + way - 1) / way, E = m + G, Et = E + n_shared;
+  const int c = ve ? cnt : 0;
+  // line 5: rank by (cnt desc, id asc); exclusive prefix in that order; S
+  int pos = 0;
+  for (int j = 0; j < m; ++j) {
+    const int cj = __shfl_sync(FULL, c, j);
+    pos += (cj > c) | ((cj == c) & (j < e));
+  }
+  long long excl = 0, S = 0;
+  for (int j = 0; j < m; ++j) {
+    const int cj = __shfl_sync(FULL, c, j);
+    const int pj = __shfl_sync(FULL, pos, j);
+    excl += pj < pos ? cj : 0;
+    S += cj;
+  }
+  // lines 6-15: S1 / S2 against Tcov in fp64
+  const double Tcov = static_cast<double>(S) * (1.0 - ratio);
+  const bool active = ve && c > 0;
+  const bool in_s1 = active && static_cast<double>(excl) < Tcov;
+  const bool in_s2 = active && !in_s1;
+  // line 23: |M_j| = S2 members of e's group
+  int gsize = 0;
+  for (int j = 0; j < m; ++j) {
+    const int s2j = __shfl_sync(FULL, static_cast<int>(in_s2), j);
+    gsize += (s2j && j / way == e / way) ? 1 : 0;
+  }
+  // lines 16-30: executor of each expert
+  int x_e = -1;
+  if (ve) {
+    if (in_s1) x_e = e;
+    else if (!in_s2) x_e = -1;
+    else if (mode == 1) x_e = -2;
+    else if (gsize == 1) x_e = e;
+    else x_e = m + e / way;
+  }
+  // rows of executors x0 = lane and x1 = lane + 32
+  const int x0 = lane, x1 = lane + 32;
+  int r0 = 0, r1 = 0;
+  for (int j = 0; j < m; ++j) {
+    const int xj = __shfl_sync(FULL, x_e, j);
+    const int cj = __shfl_sync(FULL, c, j);
+    r0 += xj == x0 ? cj : 0;
+    r1 += xj == x1 ? cj : 0;
+  }
+  if (x0 >= E && x0 < Et) r0 = shared_rows;
+  if (x1 >= E && x1 < Et) r1 = shared_rows;
+  if (x0 >= Et) r0 = 0;
+  if (x1 >= Et) r1 = 0;
+  // exclusive scans over the executors (rows and 128-row m-tiles)
+  auto scan2 = [&](int v0, int v1, int& ex0, int& ex1, int& total) {
+    int i0 = v0, i1 = v1;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int o0 = __shfl_up_sync(FULL, i0, off);
+      const int o1 = __shfl_up_sync(FULL, i1, off);
+      if (lane >= off) { i0 += o0; i1 += o1; }
+    }
+    const int t0 = __shfl_sync(FULL, i0, 31);
+    ex0 = i0 - v0;
+    ex1 = t0 + i1 - v1;
+    total = t0 + __shfl_sync(FULL, i1, 31);
+  };
+  int xo0, xo1, R_all, mo0, mo1, MT_all;
+  scan2(r0, r1, xo0, xo1, R_all);
+  scan2((r0 + kBM - 1) / kBM, (r1 + kBM - 1) / kBM, mo0, mo1, MT_all);
+  if (x0 <= Et) s_xoff[x0] = x0 == Et ? R_all : xo0;
+  if (x1 <= Et) s_xoff[x1] = x1 == Et ? R_all : xo1;
+  // expert_row_off: executor start + earlier members of the same executor (D11)
+  const int xs = x_e >= 0 ? x_e : 0;
+  const int st0 = __shfl_sync(FULL, xo0, xs & 31), st1 = __shfl_sync(FULL, xo1, xs & 31);
+  int off = x_e >= 0 ? (x_e < 32 ? st0 : st1) : -1;
+  int before = 0;   // rows of the same united executor's earlier members
+  for (int j = 0; j < m; ++j) {
+    const int xj = __shfl_sync(FULL, x_e, j);
+    const int cj = __shfl_sync(FULL, c, j);
+    before += (j < e && xj == x_e) ? cj : 0;
+  }
+  if (x_e >= m) off += before;
+  if (ve) s_row_off[e] = off;
+  // statistics (P:173 / P:194 access counts, rows per class)
+  const int n_acc = __popc(__ballot_sync(FULL, x0 < E && r0 > 0)) + __popc(__ballot_sync(FULL, x1 < E && r1 > 0));
+  const int n_uni = __popc(__ballot_sync(FULL, x0 >= m && x0 < E && r0 > 0)) +
+                    __popc(__ballot_sync(FULL, x1 >= m && x1 < E && r1 > 0));
+  const int n_s1 = __popc(__ballot_sync(FULL, in_s1));
+  const int n_single = __popc(__ballot_sync(FULL, in_s2 && x_e == e));
+  long long r_orig = (x0 < m ? r0 : 0) + (x1 < m ? r1 : 0);
+  long long r_routed = (x0 < E ? r0 : 0) + (x1 < E ? r1 : 0);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    r_orig += __shfl_xor_sync(FULL, r_orig, o);
+    r_routed += __shfl_xor_sync(FULL, r_routed, o);
+  }
+  if (write_global) {
+    if (ve) {
+      counts[e] = c;
+      exec_of_expert[e] = x_e;
+      expert_row_off[e] = off;
+    }
+    if (x0 < Et) { exec_off[x0] = xo0; mtile_off[x0] = mo0; }
+    if (x1 < Et) { exec_off[x1] = xo1; mtile_off[x1] = mo1; }
+    if (lane == 0) {
+      exec_off[Et] = R_all;
+      mtile_off[Et] = MT_all;
+      stats[0] = n_acc;
+      stats[1] = n_s1;
+      stats[2] = n_uni;
+      stats[3] = n_single;
+      stats[4] = r_orig;
+      stats[5] = r_routed - r_orig;
+      stats[6] = S - r_routed;
+      stats[7] = S;
+    }
+  }
+}
+
 template <typename T, int MAXM>
 __global__ void __launch_bounds__(256)
     k_route_fused(const T* __restrict__ x, const T* __restrict__ Wr, int Tn, int d, int m, int K, int tpc,
                   float* __restrict__ logits, int32_t* __restrict__ topk_id, float* __restrict__ topk_w,
-                  int32_t* __restrict__ tile_cnt, int way, double ratio, int mode, int32_t* __restrict__ tile_base,
-                  int32_t* __restrict__ counts, int32_t* __restrict__ exec_of_expert,
-                  int32_t* __restrict__ expert_row_off, int32_t* __restrict__ exec_off,
-                  int32_t* __restrict__ mtile_off, int64_t* __restrict__ stats, int n_shared,
-                  int32_t* __restrict__ row_of, int32_t* __restrict__ row_tok, float* __restrict__ row_w,
-                  uint4* __restrict__ xp, int vec_per_row) {
+                  int32_t* __restrict__ tile_cnt, int way, double ratio, int mode, int32_t* __restrict__ counts,
+                  int32_t* __restrict__ exec_of_expert, int32_t* __restrict__ expert_row_off,
+                  int32_t* __restrict__ exec_off, int32_t* __restrict__ mtile_off, int64_t* __restrict__ stats,
+                  int n_shared, int32_t* __restrict__ row_of, int32_t* __restrict__ row_tok,
+                  float* __restrict__ row_w, uint4* __restrict__ xp, int vec_per_row) {
+  __shared__ int32_t s_sum[2][8][MAXM];   // per-warp partial column sums: all tiles / tiles before mine
   __shared__ int32_t s_row_off[MAXM];
   __shared__ int32_t s_xoff[kRouteFusedMaxExec + 1];
   __shared__ int32_t s_tb[MAXM];
   router_split_tile<T, MAXM>(x, Wr, Tn, d, m, K, tpc, logits, topk_id, topk_w, tile_cnt, blockIdx.x);
   cg::this_grid().sync();   // every tile histogram written (and visible)
-  PlanLocal loc{blockIdx.x == 0, static_cast<int>(blockIdx.x), s_row_off, s_xoff, s_tb};
-  plan_block<kPlanStageFused>(tile_cnt, gridDim.x, m, way, ratio, mode, tile_base, counts, exec_of_expert,
-                              expert_row_off, exec_off, mtile_off, stats, n_shared, Tn, PlanExt(), &loc);
+  // Alg. 1 input cnt_e = sum over tiles; this tile's exclusive prefix = sum over the tiles before
+  // it.  Warp w takes tiles w, w + 8, ...; lane = expert; L2-coherent loads (same kernel).
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntiles = gridDim.x, me = blockIdx.x;
+  {
+    int all = 0, bef = 0;
+    if (lane < m) {
+      constexpr int U = 4;
+      for (int t0 = warp; t0 < ntiles; t0 += 8 * U) {
+        int v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int t = t0 + 8 * u;
+          v[u] = t < ntiles ? __ldcg(tile_cnt + static_cast<int64_t>(t) * m + lane) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          all += v[u];
+          bef += t0 + 8 * u < me ? v[u] : 0;
+        }
+      }
+      s_sum[0][warp][lane] = all;
+      s_sum[1][warp][lane] = bef;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    int cnt = 0, base = 0;
+    if (lane < m)
+      for (int w = 0; w < 8; ++w) {
+        cnt += s_sum[0][w][lane];
+        base += s_sum[1][w][lane];
+      }
+    if (lane < m) s_tb[lane] = base;
+    plan_small_warp(cnt, m, way, ratio, mode, n_shared, Tn, s_row_off, s_xoff, me == 0, counts, exec_of_expert,
+                    expert_row_off, exec_off, mtile_off, stats);
+  }
+  __syncthreads();
   const int E = m + (m + way - 1) / way;
-  permute_tile(topk_id, topk_w, Tn, K, m, tpc, blockIdx.x, s_tb, s_row_off, 1, row_of, row_tok, row_w,
+  permute_tile(topk_id, topk_w, Tn, K, m, tpc, me, s_tb, s_row_off, 1, row_of, row_tok, row_w,
                reinterpret_cast<const uint4*>(x), xp, vec_per_row, n_shared, s_xoff + E);
 }
 
@@ -1063,8 +1198,7 @@ static int route_fused_capacity(int num_sms) {
 bool route_fused_ok(int dtype, int m, int way, int T, int tpc, int n_shared, int num_sms) {
   if (m > 32 || tpc <= 0 || T <= 0) return false;
   const int ntiles = (T + tpc - 1) / tpc;
-  const int Et = m + (m + way - 1) / way + n_shared;
-  if (ntiles * m > kPlanStageFused || Et > kRouteFusedMaxExec) return false;
+  if (m + (m + way - 1) / way + n_shared > kRouteFusedMaxExec) return false;
   int cap;
   if (dtype == 0) cap = m <= 8 ? route_fused_capacity<__nv_bfloat16, 8>(num_sms)
                                : (m <= 16 ? route_fused_capacity<__nv_bfloat16, 16>(num_sms)
@@ -1076,7 +1210,7 @@ bool route_fused_ok(int dtype, int m, int way, int T, int tpc, int n_shared, int
 
 cudaError_t launch_route_fused(int dtype, const void* x, const void* Wr, int T, int d, int m, int K, int tpc,
                                float* logits, int32_t* topk_id, float* topk_w, int32_t* tile_cnt, int way,
-                               double ratio, int mode, int32_t* tile_base, int32_t* counts, int32_t* exec_of_expert,
+                               double ratio, int mode, int32_t* counts, int32_t* exec_of_expert,
                                int32_t* expert_row_off, int32_t* exec_off, int32_t* mtile_off, int64_t* stats,
                                int n_shared, int32_t* row_of, int32_t* row_tok, float* row_w, void* xp,
                                cudaStream_t s) {
@@ -1095,8 +1229,8 @@ cudaError_t launch_route_fused(int dtype, const void* x, const void* Wr, int T, 
 #define BO_RF(TYPE, M)                                                                                         \
   return cudaLaunchKernelEx(&cfg, k_route_fused<TYPE, M>, static_cast<const TYPE*>(x),                         \
                             static_cast<const TYPE*>(Wr), T, d, m, K, tpc, logits, topk_id, topk_w, tile_cnt,  \
-                            way, ratio, mode, tile_base, counts, exec_of_expert, expert_row_off, exec_off,     \
-                            mtile_off, stats, n_shared, row_of, row_tok, row_w, xpv, vec)
+                            way, ratio, mode, counts, exec_of_expert, expert_row_off, exec_off, mtile_off,     \
+                            stats, n_shared, row_of, row_tok, row_w, xpv, vec)
   if (dtype == 0) {
     if (m <= 8) BO_RF(__nv_bfloat16, 8); else if (m <= 16) BO_RF(__nv_bfloat16, 16); else BO_RF(__nv_bfloat16, 32);
   } else {

@@ -23,7 +23,11 @@ def main(path):
     # steps start at the router (first kernel of a forward)
     steps, cur = [], []
     for name, us in seq:
-        if ("router" in name or "EPI_ROUTER" in name) and cur:
+        # a forward starts at its router: k_router_*, the fused decode routing kernel, or the
+        # tcgen05 router (k_grouped_gemm with EPI_ROUTER = 2 as its third template argument)
+        starts = "router" in name or "route_fused" in name or \
+            (name.startswith("bo::k_grouped_gemm<") and name.split(",")[2].strip() == "2")
+        if starts and cur:
             steps.append(cur)
             cur = []
         if "united_mean" in name:
