@@ -544,7 +544,8 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   // R*d*2 bytes at HBM speed; measured r01).
   const bool gather_in_permute = Rt <= kSplitRows * 2 && !c.dedup_united;
   // Decode-sized steps on the split-warp router: a1-a5 in one cooperative launch
-  const int tpc = h->opt.router_split ? bo::router_split_tpc(static_cast<int>(T), h->num_sms) : 0;
+  const int tpc = h->opt.router_split && bo::router_split_tpc(static_cast<int>(T), h->num_sms) > 0
+                      ? bo::route_fused_tpc(static_cast<int>(T), h->num_sms) : 0;
   const bool route_fused = h->opt.route_fused && !logits_in && !c.dedup_united && Wr != nullptr &&
                            bo::router_small_ok(dt, m, d) && tpc > 0 &&
                            !(h->opt.router_mma && bo::router_mma_ok(dt, m, d, static_cast<int>(T), h->num_sms)) &&

@@ -148,6 +148,8 @@ cudaError_t launch_permute(const int32_t* topk_id, const float* topk_w, int T, i
 // plan output written as by launch_plan / launch_permute (the per-tile prefixes stay in
 // shared memory).  route_fused_ok: the shapes fit and the grid is co-resident.
 constexpr int kRouteFusedMaxExec = 64;   // m + G + N_s executors (two per lane of the planning warp)
+constexpr int kRouteFusedStage = 4096;   // tile histograms staged per CTA (ntiles * m)
+int route_fused_tpc(int T, int num_sms);   // tokens per CTA (1/2/4/8) keeping the grid within #SM; 0: none
 bool route_fused_ok(int dtype, int m, int way, int T, int tpc, int n_shared, int num_sms);
 cudaError_t launch_route_fused(int dtype, const void* x, const void* Wr, int T, int d, int m, int K, int tpc,
                                float* logits, int32_t* topk_id, float* topk_w, int32_t* tile_cnt, int way,

@@ -1139,6 +1139,7 @@ __global__ void __launch_bounds__(256)
                   int32_t* __restrict__ exec_off, int32_t* __restrict__ mtile_off, int64_t* __restrict__ stats,
                   int n_shared, int32_t* __restrict__ row_of, int32_t* __restrict__ row_tok,
                   float* __restrict__ row_w, uint4* __restrict__ xp, int vec_per_row) {
+  __shared__ __align__(16) int32_t s_tc[kRouteFusedStage];   // every tile histogram [ntiles, m]
   __shared__ int32_t s_sum[2][8][MAXM];   // per-warp partial column sums: all tiles / tiles before mine
   __shared__ int32_t s_row_off[MAXM];
   __shared__ int32_t s_xoff[kRouteFusedMaxExec + 1];
@@ -1146,29 +1147,24 @@ __global__ void __launch_bounds__(256)
   router_split_tile<T, MAXM>(x, Wr, Tn, d, m, K, tpc, logits, topk_id, topk_w, tile_cnt, blockIdx.x);
   cg::this_grid().sync();   // every tile histogram written (and visible)
   // Alg. 1 input cnt_e = sum over tiles; this tile's exclusive prefix = sum over the tiles before
-  // it.  Warp w takes tiles w, w + 8, ...; lane = expert; L2-coherent loads (same kernel).
+  // it.  All ntiles * m counts are staged with one round of L2-coherent 16-byte loads (written
+  // in this kernel: no .nc path), then warp w sums tiles w, w + 8, ... per expert (lane).
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntiles = gridDim.x, me = blockIdx.x;
-  {
+  const int n_tc = ntiles * m;
+  for (int i = threadIdx.x; i < n_tc / 4; i += blockDim.x)
+    reinterpret_cast<int4*>(s_tc)[i] = __ldcg(reinterpret_cast<const int4*>(tile_cnt) + i);
+  for (int i = (n_tc & ~3) + threadIdx.x; i < n_tc; i += blockDim.x) s_tc[i] = __ldcg(tile_cnt + i);
+  __syncthreads();
+  if (lane < m) {
     int all = 0, bef = 0;
-    if (lane < m) {
-      constexpr int U = 4;
-      for (int t0 = warp; t0 < ntiles; t0 += 8 * U) {
-        int v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int t = t0 + 8 * u;
-          v[u] = t < ntiles ? __ldcg(tile_cnt + static_cast<int64_t>(t) * m + lane) : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          all += v[u];
-          bef += t0 + 8 * u < me ? v[u] : 0;
-        }
-      }
-      s_sum[0][warp][lane] = all;
-      s_sum[1][warp][lane] = bef;
+    for (int t = warp; t < ntiles; t += 8) {
+      const int v = s_tc[t * m + lane];
+      all += v;
+      bef += t < me ? v : 0;
     }
+    s_sum[0][warp][lane] = all;
+    s_sum[1][warp][lane] = bef;
   }
   __syncthreads();
   if (warp == 0) {
@@ -1195,10 +1191,16 @@ static int route_fused_capacity(int num_sms) {
   return nb * num_sms;
 }
 
+int route_fused_tpc(int T, int num_sms) {
+  for (int tpc = 1; tpc <= 8; tpc *= 2)
+    if ((T + tpc - 1) / tpc <= num_sms) return tpc;   // one CTA per SM at most: a cheap grid barrier
+  return 0;
+}
+
 bool route_fused_ok(int dtype, int m, int way, int T, int tpc, int n_shared, int num_sms) {
   if (m > 32 || tpc <= 0 || T <= 0) return false;
   const int ntiles = (T + tpc - 1) / tpc;
-  if (m + (m + way - 1) / way + n_shared > kRouteFusedMaxExec) return false;
+  if (m + (m + way - 1) / way + n_shared > kRouteFusedMaxExec || ntiles * m > kRouteFusedStage) return false;
   int cap;
   if (dtype == 0) cap = m <= 8 ? route_fused_capacity<__nv_bfloat16, 8>(num_sms)
                                : (m <= 16 ? route_fused_capacity<__nv_bfloat16, 16>(num_sms)
