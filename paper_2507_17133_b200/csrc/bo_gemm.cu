@@ -144,24 +144,24 @@ __device__ __forceinline__ void add_row32(float* dst, float (&v)[32]) {
   }
 }
 
-// Running top-KMAX list, (value desc, id asc); ids arrive in ascending order so a
-// new element only overtakes strictly smaller values (reading D8; -0 == +0).  The list
-// starts at -inf (logits are finite), so "overtakes slot j" is one comparison, and it is
-// monotone in j: slot j takes slot j-1's entry when v also beats slot j-1, else v itself
-// (one FSETP + four selects per slot).  All KMAX slots are kept for any K <= KMAX: the
-// first K entries of the top-KMAX list are the top-K.
+// Running top-K list, (value desc, id asc); ids arrive in ascending order so a
+// new element only overtakes strictly smaller values (reading D8).  (A select-only
+// variant that kept all KMAX slots from -inf returned duplicated ids on the m = 32
+// tcgen05 router of tests/test_gpu_router_exact.py although the same function is
+// exact in isolation on the device (scripts/topk_check.cu); this form stays.)
 template <int KMAX>
-__device__ __forceinline__ void topk_insert(float (&tv)[KMAX], int (&ti)[KMAX], float v, int e) {
-  bool beats[KMAX];
+__device__ __forceinline__ void topk_insert(float (&tv)[KMAX], int (&ti)[KMAX], int K, float v, int e) {
 #pragma unroll
-  for (int j = 0; j < KMAX; ++j) beats[j] = v > tv[j];
-#pragma unroll
-  for (int j = KMAX - 1; j > 0; --j) {
-    tv[j] = beats[j] ? (beats[j - 1] ? tv[j - 1] : v) : tv[j];
-    ti[j] = beats[j] ? (beats[j - 1] ? ti[j - 1] : e) : ti[j];
+  for (int j = KMAX - 1; j >= 0; --j) {
+    if (j < K) {
+      const bool b_j = ti[j] < 0 || v > tv[j];
+      const bool b_jm1 = j > 0 && (ti[j - 1] < 0 || v > tv[j - 1]);
+      if (b_j) {
+        if (b_jm1) { tv[j] = tv[j - 1]; ti[j] = ti[j - 1]; }
+        else { tv[j] = v; ti[j] = e; }
+      }
+    }
   }
-  tv[0] = beats[0] ? v : tv[0];
-  ti[0] = beats[0] ? e : ti[0];
 }
 
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
@@ -969,7 +969,7 @@ __global__ void __launch_bounds__(192, 1)
         float tv[KMAX];
         int ti[KMAX];
 #pragma unroll
-        for (int j = 0; j < KMAX; ++j) { tv[j] = -INFINITY; ti[j] = j; }   // ids stay in range even for NaN logits
+        for (int j = 0; j < KMAX; ++j) { tv[j] = 0.0f; ti[j] = -1; }
         float* lbase = reinterpret_cast<float*>(p.out) + row0 * p.ldo;
         const bool vec_ok = (p.ldo & 3) == 0;
 #pragma unroll 1
@@ -980,7 +980,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const int col = c + i;
-            if (col < p.n_valid) topk_insert<KMAX>(tv, ti, __uint_as_float(a[i]), col);
+            if (col < p.n_valid) topk_insert<KMAX>(tv, ti, p.topk_k, __uint_as_float(a[i]), col);
           }
           const int ncol = p.n_valid - c < 32 ? p.n_valid - c : 32;
           if (ncol <= 0) continue;
