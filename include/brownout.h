@@ -87,8 +87,7 @@ typedef enum {
   BO_OPT_PDL = 13,           /* 1: GEMMs launch with programmatic dependent launch                   [1]    */
   BO_OPT_ROUTE_FUSED = 14,   /* 1: decode-sized m <= 32 steps run router + top-K + Alg. 1 + permute +
                                    gather as one cooperative launch                                   [1]    */
-  BO_OPT_DECODE_STREAMK = 15,/* 1: decode-sized GEMM1 on CTA pairs, stream-K over equal k-block shares  [1]    */
-  BO_OPT_COUNT = 16
+  BO_OPT_COUNT = 15
 } bo_engine_option;
 
 typedef struct {
@@ -144,8 +143,6 @@ typedef struct {
   size_t tile_xbase;      /* int32 [ntiles, E]  their exclusive prefix over tiles            */
   size_t ksplit;          /* int32 [1]          split count GEMM2 chose                 */
   size_t comb_cnt;        /* int32 [T, d/BN2]   arrival counters of the combine fused into GEMM2 (a8; BN2 = 256/128/64, GEMM2 tile width) */
-  size_t sk_part;         /* float [#SM, 128 rows, 256 cols] stream-K partial accumulators of decode GEMM1 (T*K <= 1024 only) */
-  size_t sk_flag;         /* int32 [#SM]        their arrival flags (zeroed before each GEMM1)          */
   int64_t T;              /* tokens the layout was computed for                          */
   int64_t ntiles;         /* histogram tiles the workspace is sized for (8 tokens each)  */
   int64_t num_executors;  /* E = m + G                                                   */

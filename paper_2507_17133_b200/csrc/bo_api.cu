@@ -143,10 +143,6 @@ bo_status compute_layout(const bo_handle* h, int64_t T, bo_ws_layout* L, bool ro
   L->tile_xbase = take(c.dedup_united && !route_only ? sizeof(int32_t) * ntiles * (m + G) : 0);
   L->ksplit = take(sizeof(int32_t));
   L->comb_cnt = take(route_only ? 0 : sizeof(int32_t) * T * (d / gemm2_bn(static_cast<int>(d))));
-  // decode-sized steps: one 128 x 256 fp32 stream-K partial and one flag per SM (GEMM1 on CTA pairs)
-  const bool sk = Rf > 0 && Rf <= kSplitRows;
-  L->sk_part = take(sk ? sizeof(float) * h->num_sms * bo::kSkPartElems : 0);
-  L->sk_flag = take(sk ? sizeof(int32_t) * h->num_sms : 0);
   L->total_bytes = off;
   L->T = T;
   L->ntiles = ntiles;
@@ -278,8 +274,7 @@ void set_comb(bo::GemmParams& p, const CombFuse* cf, int d, int nt2) {
 bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, const int32_t* exec_off,
                     const int32_t* mtile_off, const FfnClass& orig, const FfnClass& uni, const FfnClass& shr,
                     void* Hbuf, void* Y, cudaStream_t s, Prof& prof, int& launches, float* partial,
-                    int* ks_dev, const CombFuse* comb, const int32_t* comb_row_tok, bool force_pair2,
-                    float* sk_part, int* sk_flag) {
+                    int* ks_dev, const CombFuse* comb, const int32_t* comb_row_tok, bool force_pair2) {
   // partial != nullptr: GEMM2 runs split-K into fp32 partials [<=8, R, d] (the
   // caller combines them with launch_combine_partials); Y is then unused.
   const bo_config& c = h->cfg;
@@ -318,14 +313,9 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
         return st;
     }
     bo::GemmParams p{};
-    // 256 x 256 tiles on CTA pairs when rows are plentiful (prefill).  Decode-sized steps
-    // also run on pairs as stream-K (GemmParams::streamk): there the per-SM fill rate from L2
-    // (in-flight stage bytes / latency, ~110 GB/s) bounds the weight streaming once executors
-    // hold more than 128 rows, so the pair tile (each weight byte filled into 2 SMs instead of
-    // 2-3) with equal k-block shares per pair (no partial last wave) is the faster schedule.
-    const bool streamk = o.decode_streamk && o.cta_pairs && o.swap_tail && dt == 0 && bn == 256 &&
-                         R <= kSplitRows && sk_part != nullptr && sk_flag != nullptr;
-    const bool pair = o.cta_pairs && dt == 0 && bn == 256 && (R >= o.pair_rows1 || streamk);
+    // 256 x 256 tiles on CTA pairs when rows are plentiful (prefill); few-row
+    // (decode) steps keep 128-row tiles so that more tiles share the SMs.
+    const bool pair = o.cta_pairs && dt == 0 && bn == 256 && R >= o.pair_rows1;
     // swapped-operand tail tiles (pairs): maps [6..11] = 64-row gate / up boxes,
     // [12..14] = Xp in 16 / 32 / 64-row boxes
     const bool swap = pair && o.swap_tail;
@@ -378,12 +368,6 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.out = Hbuf;
     p.rows_total = static_cast<int>(R);
     set_comb(p, comb, d, d / gemm2_bn(d));   // GEMM1's prologue zeroes GEMM2's arrival counters
-    if (streamk) {   // the kernel decides on the device (stream-K only when the tiles outnumber the pairs)
-      p.streamk = 1;
-      p.sk_part = sk_part;
-      p.sk_flag = sk_flag;
-      BO_CUDA(cudaMemsetAsync(sk_flag, 0, sizeof(int) * h->num_sms, s), "stream-K flags");
-    }
     const int tile_m = pair ? 2 * bo::kBM : bo::kBM;
     const int64_t max_work = ((R + tile_m - 1) / tile_m + n_exec) * p.n_tiles;
     const int units = pair ? h->num_sms / 2 : h->num_sms;
@@ -477,7 +461,6 @@ const OptionSpec kOptions[BO_OPT_COUNT] = {
     {&EngineOptions::router_split, "BO_ROUTER_SPLIT", 0, 1},
     {&EngineOptions::pdl, "BO_PDL", 0, 1},
     {&EngineOptions::route_fused, "BO_ROUTE_FUSED", 0, 1},
-    {&EngineOptions::decode_streamk, "BO_DECODE_STREAMK", 0, 1},
 };
 
 void options_from_env(EngineOptions* o) {
@@ -635,9 +618,7 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   void* xp = at<char>(ws, L.xp);   // filled by the permute (small batches) or the gather kernel
   if ((st = ffn_stage(h, xp, Rt, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), orig, uni, shr,
                       at<char>(ws, L.h), yp, s, prof, launches, split ? at<float>(ws, L.partial) : nullptr,
-                      split ? at<int>(ws, L.ksplit) : nullptr, cfp, row_tok, decode_pair2,
-                      L.sk_part ? at<float>(ws, L.sk_part) : nullptr, L.sk_flag ? at<int>(ws, L.sk_flag) : nullptr)) !=
-      BO_OK)
+                      split ? at<int>(ws, L.ksplit) : nullptr, cfp, row_tok, decode_pair2)) != BO_OK)
     return st;
   // a8: combine (Eq. 5 sum over the token's K slots; split-K partials summed first)
   if (!fuse_comb) {

@@ -523,36 +523,6 @@ __global__ void __launch_bounds__(192, 1)
     kb0 = sp * per < nkb ? sp * per : nkb;
     kb1 = kb0 + per < nkb ? kb0 + per : nkb;
   };
-  // Stream-K (see GemmParams::streamk): this unit's share [u0, u1) of the base_work * nkb
-  // (tile, k-block) sequence; with more tiles than units a share spans >= nkb k-blocks, so a
-  // tile is cut at most once: its prefix (k-block 0 on) is the last segment of unit u, its
-  // suffix the first segment of unit u + 1.
-  constexpr bool kSK = CG == 2 && EPI == EPI_SWIGLU;
-  const int nkb_sk = p.Kdim / C::BK;
-  const bool sk = kSK && p.streamk && p.sk_part && !alt && p.Kdim == p.Kdim_u && ks == 1 && base_work > n_units;
-  int64_t sk_u0 = 0, sk_u1 = 0;
-  if (sk) {
-    const int64_t U = static_cast<int64_t>(base_work) * nkb_sk;
-    sk_u0 = U * unit / n_units;
-    sk_u1 = U * (unit + 1) / n_units;
-  }
-  enum { SEG_FULL = 0, SEG_FINISH = 1, SEG_CONTRIB = 2 };
-  // s-th segment of this unit: work item w, k-block range override [sk0, sk1) and its kind
-  auto segment = [&](int s, int& w, int& sk0, int& sk1, int& kind) -> bool {
-    if (!sk) {
-      w = unit + s * n_units;
-      kind = SEG_FULL;
-      return w < total_work;
-    }
-    const int64_t i = sk_u0 / nkb_sk + s;
-    if (i * nkb_sk >= sk_u1) return false;
-    w = static_cast<int>(i);
-    const int64_t lo = sk_u0 - i * nkb_sk, hi = sk_u1 - i * nkb_sk;
-    sk0 = lo > 0 ? static_cast<int>(lo) : 0;
-    sk1 = hi < nkb_sk ? static_cast<int>(hi) : nkb_sk;
-    kind = sk0 > 0 ? SEG_CONTRIB : (sk1 < nkb_sk ? SEG_FINISH : SEG_FULL);
-    return true;
-  };
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -565,10 +535,9 @@ __global__ void __launch_bounds__(192, 1)
       int stage = 0;
       uint32_t phase = 0;
       int x, mi, n, sp, kb0, kb1;
-      int w, sk0 = 0, sk1 = 0, kind;
-      for (int item = 0; segment(item, w, sk0, sk1, kind); ++item) {
+      int item = 0;
+      for (int w = unit; w < total_work; w += n_units, ++item) {
         decode(w, x, mi, n, sp, kb0, kb1);
-        if (sk) { kb0 = sk0; kb1 = sk1; }
         BO_STAMP(item, 0);
 #ifdef BO_PROBE
         if (blockIdx.x < kProbeCtas && item < kProbeItems)
@@ -640,11 +609,9 @@ __global__ void __launch_bounds__(192, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       int x, mi, n, sp, kb0, kb1;
-      int w, sk0 = 0, sk1 = 0, kind;
       int item = 0;
-      for (; segment(item, w, sk0, sk1, kind); ++item) {
+      for (int w = unit; w < total_work; w += n_units, ++item) {
         decode(w, x, mi, n, sp, kb0, kb1);
-        if (sk) { kb0 = sk0; kb1 = sk1; }
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
@@ -677,7 +644,7 @@ __global__ void __launch_bounds__(192, 1)
       }
       if constexpr (CG == 2) {
         // drain: the peer's last remote arrivals must land before the CTAs exit
-        const int iters = item;   // segments this unit ran
+        const int iters = total_work > unit ? (total_work - unit + n_units - 1) / n_units : 0;
         if (iters > 0) {
           const int last = iters - 1;
           mbar_wait(&tempty_bar[last & 1], (last >> 1) & 1);
@@ -712,12 +679,11 @@ __global__ void __launch_bounds__(192, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     int x, mi, n, sp, kb0, kb1;
-    int w, sk0 = 0, sk1 = 0, kind;
-    int item = 0;
-    for (; segment(item, w, sk0, sk1, kind); ++item) {
-      if (item > 0 && warp == 2 && lane == 0) BO_STAMP(item - 1, 3);   // the previous tile's epilogue is done
+    int item = -1;
+    for (int w = unit; w < total_work; w += n_units) {
+      if (item >= 0 && warp == 2 && lane == 0) BO_STAMP(item, 3);   // the previous tile's epilogue is done
+      ++item;
       decode(w, x, mi, n, sp, kb0, kb1);
-      if (sk) { kb0 = sk0; kb1 = sk1; }
       const int rows_x = s_eoff[x + 1] - s_eoff[x];
       const int r_local = mi * TILE_M + static_cast<int>(crank) * kBM + q * 32 + lane;
       const bool valid = r_local < rows_x;
@@ -729,53 +695,6 @@ __global__ void __launch_bounds__(192, 1)
       const int slab = mi * TILE_M + static_cast<int>(crank) * kBM + q * 32;
       const int nrows = rows_x - slab < 0 ? 0 : (rows_x - slab > 32 ? 32 : rows_x - slab);
       const int64_t row0 = static_cast<int64_t>(s_eoff[x]) + slab;
-      // stream-K: the partial accumulator this tile's finishing unit adds (the next unit's)
-      const float* skp = nullptr;
-      if constexpr (kSK) {
-        const int lrow = q * 32 + lane;   // TMEM lane of this thread
-        if (kind == SEG_CONTRIB) {
-          // dump every accumulator column the tile uses, then count this warp's arrival
-          const int ncols = swapped_tile(x, mi) ? ((tile_rows(x, mi) + 31) & ~31) : 2 * bh;
-          float* part = p.sk_part + static_cast<int64_t>(blockIdx.x) * kSkPartElems;
-#pragma unroll 1
-          for (int c = 0; c < ncols; c += 32) {
-            uint32_t v[32];
-            tmem_ld32(t0 + c, v);
-            tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 32; ++j) __stcg(part + (c + j) * 128 + lrow, __uint_as_float(v[j]));
-          }
-          tc_fence_before();
-          __threadfence();   // release: the partial precedes the count
-          __syncwarp();
-          if (lane == 0) {
-            atomicAdd(p.sk_flag + blockIdx.x, 1);
-            if (leader) mbar_arrive(&tempty_bar[acc]);
-            else mbar_arrive_remote(&tempty_bar[acc], 0);
-          }
-          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-          continue;
-        }
-        if (kind == SEG_FINISH) {
-          // the next unit computed this tile's remaining k-blocks first: wait for its 4 warps
-          const int* flag = p.sk_flag + blockIdx.x + 2;
-          if (lane == 0) {
-            int v;
-            do {
-              asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-            } while (v < 4);
-          }
-          __syncwarp();
-          skp = p.sk_part + static_cast<int64_t>(blockIdx.x + 2) * kSkPartElems + lrow;
-        }
-      }
-      // acc[j] += the stream-K partial of accumulator column col + j (finishing tiles only)
-      auto add_part = [&](uint32_t (&a)[32], int col) {
-        if (skp) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) a[j] = __float_as_uint(__uint_as_float(a[j]) + __ldcg(skp + (col + j) * 128));
-        }
-      };
       bool swapped = false;
       if constexpr (kSwap) {
         if (swapped_tile(x, mi)) {
@@ -796,7 +715,6 @@ __global__ void __launch_bounds__(192, 1)
             uint32_t v[32];
             tmem_ld32(t0 + c, v);
             tmem_ld_wait();
-            add_part(v, c);
             float hv[32];
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
@@ -841,8 +759,6 @@ __global__ void __launch_bounds__(192, 1)
           tmem_ld32(t0 + c, g);
           tmem_ld32(t0 + bh + c, u);
           tmem_ld_wait();
-          add_part(g, c);
-          add_part(u, bh + c);
           float h[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) h[i] = silu_f(__uint_as_float(g[i])) * __uint_as_float(u[i]);
@@ -1077,8 +993,7 @@ __global__ void __launch_bounds__(192, 1)
 
 #ifdef BO_PROBE
   if (warp == 2 && lane == 0) {
-    int last = -1, w_, a_, b_, k_;
-    while (segment(last + 1, w_, a_, b_, k_)) ++last;
+    const int last = total_work > unit ? (total_work - unit + n_units - 1) / n_units - 1 : -1;
     if (last >= 0) BO_STAMP(last, 3);
   }
 #endif

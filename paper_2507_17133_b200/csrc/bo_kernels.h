@@ -70,17 +70,7 @@ struct GemmParams {
   // Maps [6..11] then hold 64-row gate / up boxes and [12..14] 16 / 32 / 64-row boxes of A (Xp).
   int swap_tail;
   int tma_store;            // EPI_WEIGHTED: full 32-row slabs leave through TMA bulk stores (map B[6], 32 x 32 box, 64B swizzle)
-  // Stream-K (SwiGLU on CTA pairs, decode-sized steps): when the plan's tiles outnumber the
-  // pairs, every pair takes an equal contiguous share of the (tile, k-block) sequence.  A
-  // tile cut in two is finished by the pair that owns its first k-block (it runs it last):
-  // the next pair computes the tile's remaining k-blocks first, dumps the fp32 accumulator to
-  // sk_part[its unit][crank] and counts its 4 epilogue warps in sk_flag[unit * 2 + crank];
-  // the finishing pair adds it before the SwiGLU.  sk_flag is zeroed before every launch.
-  int streamk;
-  float* sk_part;           // [units * 2][kSkPartElems]
-  int* sk_flag;             // [units * 2]
 };
-constexpr int kSkPartElems = 256 * 128;   // fp32 accumulator of one CTA: 256 columns x 128 rows
 
 // Combine of split-K fp32 partials: y[t] = [x_t] + sum_slots sum_splits P[sp][row].
 cudaError_t launch_combine_partials(int dtype, const float* partial, const int* ks, int64_t R, const void* x, int T,
