@@ -312,9 +312,10 @@ __device__ __forceinline__ void combine_token_cols(const GemmParams& p, const T*
 #ifdef BO_PROBE
 // Instrumentation build only (build.py --variant probe): per (launch class, CTA, work item)
 // globaltimer stamps [producer starts the tile, MMA has its first stage, MMA committed the
-// last k-block, epilogue done] and the tile id (x | mi << 10 | n << 16).
+// last k-block, epilogue done, MMA has the accumulator (tempty), producer issued the first
+// k-block (empty slot)] and the tile id (x | mi << 10 | n << 16).
 constexpr int kProbeCtas = 160, kProbeItems = 48;
-__device__ unsigned long long g_probe[2][kProbeCtas][kProbeItems][4];
+__device__ unsigned long long g_probe[2][kProbeCtas][kProbeItems][6];
 __device__ int g_probe_id[2][kProbeCtas][kProbeItems];
 #define BO_STAMP(j, k)                                                                      \
   do {                                                                                      \
@@ -573,6 +574,7 @@ __global__ void __launch_bounds__(192, 1)
         }
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
+          if (kb == kb0) BO_STAMP(item, 5);
           uint8_t* sa = smem + stage * C::STAGE_BYTES;
           uint8_t* sb = sa + C::A_BYTES;
           if constexpr (CG == 1) {
@@ -614,6 +616,7 @@ __global__ void __launch_bounds__(192, 1)
         decode(w, x, mi, n, sp, kb0, kb1);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
+        BO_STAMP(item, 4);
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
         uint32_t idesc_t = idesc;
         if constexpr (kSwap) {

@@ -39,7 +39,7 @@ for _ in range(4):
     moe.forward(x, lay["Wr"], (lay["Wg"], lay["Wu"], lay["Wd"]), (uni["UWg"], uni["UWu"], uni["UWd"]), shared=shared)
 torch.cuda.synchronize()
 NC, NI = 160, 48
-stamps = np.zeros((2, NC, NI, 4), dtype=np.uint64)
+stamps = np.zeros((2, NC, NI, 6), dtype=np.uint64)
 ids = np.zeros((2, NC, NI), dtype=np.int32)
 lib = B._lib
 lib.bo_probe_copy.argtypes = [C.c_void_p, C.c_void_p]
@@ -62,7 +62,7 @@ for cls in range(2):
                 tid = int(ids[cls, c, j])
                 items.append({"cta": c, "item": j, "x": tid & 1023, "mi": (tid >> 10) & 63, "n": tid >> 16,
                               "start": rel[c, j, 0], "first": rel[c, j, 1], "mma_done": rel[c, j, 2],
-                              "epi_done": rel[c, j, 3]})
+                              "epi_done": rel[c, j, 3], "tempty": rel[c, j, 4], "issue0": rel[c, j, 5]})
     end = np.nanmax(rel[:, :, 3])
     cta_end = [np.nanmax(rel[c, :, 3]) for c in range(NC) if valid[c].any()]
     cta_first = [rel[c, 0, 1] for c in range(NC) if valid[c].any()]
