@@ -32,6 +32,10 @@ struct GemmShape {
                                                                           : 512;
 };
 
+// Work items per unit whose (executor, m-tile, n-tile, split) is decoded once in the prologue
+// (later items, if any, are decoded when reached).
+constexpr int kSchedItems = 256;
+
 template <typename T, int BN, int CG = 1>
 struct GemmCfg {
   static constexpr int BM = kBM;                         // rows per CTA (the pair covers CG * 128)
@@ -41,7 +45,8 @@ struct GemmCfg {
   static constexpr int B_BYTES = (BN / CG) * 128;       // each CTA of a pair holds half of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int BAR_BYTES = 1024;                 // mbarriers + TMEM slot
-  static constexpr int SCHED_BYTES = ((2 * (kMaxExec + 1) * 4) + 127) / 128 * 128;   // keeps the staging 16B-aligned
+  // executor offsets + m-tile prefix, then this unit's packed work list (keeps the staging 16B-aligned)
+  static constexpr int SCHED_BYTES = ((2 * (kMaxExec + 1) + kSchedItems) * 4 + 127) / 128 * 128;
   static constexpr int EPI_ROW = 32 * (int)sizeof(T) + 16;   // staged 32-column row chunk + bank pad
   static constexpr int EPI_BYTES = 4 * 32 * EPI_ROW          // one staging tile per epilogue warp
                                    + 1024 + 4 * 4096;          // + two dense 2 KB TMA-store boxes per warp (1 KB aligned)
@@ -355,6 +360,7 @@ __global__ void __launch_bounds__(192, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
   int* s_mtile = reinterpret_cast<int*>(smem + STAGES * C::STAGE_BYTES + C::BAR_BYTES);
   int* s_eoff = s_mtile + (kMaxExec + 1);
+  int* s_sched = s_eoff + (kMaxExec + 1);   // [kSchedItems] this unit's decoded work list
   uint8_t* s_epi = smem + STAGES * C::STAGE_BYTES + C::BAR_BYTES + C::SCHED_BYTES;
   // per-warp 4 KB region (1 KB aligned): TMA-store boxes (GEMM2), swizzled logits staging (router)
   uint8_t* s_box = smem + ((STAGES * C::STAGE_BYTES + C::BAR_BYTES + C::SCHED_BYTES + 4 * 32 * C::EPI_ROW + 1023) & ~1023);
@@ -524,6 +530,40 @@ __global__ void __launch_bounds__(192, 1)
     kb0 = sp * per < nkb ? sp * per : nkb;
     kb1 = kb0 + per < nkb ? kb0 + per : nkb;
   };
+  // This unit's work list, decoded by all threads at once: the binary search over the
+  // executors sat on the MMA warp's critical path between tiles (0.5-0.9 us per tile with
+  // 5-57 executors, probe build), ~10 % of a 12-k-block C4 GEMM2 tile.  Packed as
+  // x | mi << 10 | n << 20 | sp << 29; -1 = decode when reached (a field does not fit).
+  {
+    const int n_my = total_work > unit ? (total_work - unit + n_units - 1) / n_units : 0;
+    const int n_tab = n_my < kSchedItems ? n_my : kSchedItems;
+    for (int j = threadIdx.x; j < n_tab; j += blockDim.x) {
+      int x, mi, n, sp, a, b;
+      decode(unit + j * n_units, x, mi, n, sp, a, b);
+      s_sched[j] = (x < 1024 && mi < 1024 && n < 512 && sp < 4) ? (x | (mi << 10) | (n << 20) | (sp << 29)) : -1;
+    }
+    __syncthreads();
+  }
+  auto item_at = [&](int j, int w, int& x, int& mi, int& n, int& sp, int& kb0, int& kb1) {
+    const int e = j < kSchedItems ? s_sched[j] : -1;
+    if (e < 0) {
+      decode(w, x, mi, n, sp, kb0, kb1);
+      return;
+    }
+    x = e & 1023;
+    mi = (e >> 10) & 1023;
+    n = (e >> 20) & 511;
+    sp = e >> 29;
+    const int nkb = kblocks(x);
+    if (ks == 1) {
+      kb0 = 0;
+      kb1 = nkb;
+    } else {
+      const int per = (nkb + ks - 1) / ks;
+      kb0 = sp * per < nkb ? sp * per : nkb;
+      kb1 = kb0 + per < nkb ? kb0 + per : nkb;
+    }
+  };
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
@@ -538,7 +578,7 @@ __global__ void __launch_bounds__(192, 1)
       int x, mi, n, sp, kb0, kb1;
       int item = 0;
       for (int w = unit; w < total_work; w += n_units, ++item) {
-        decode(w, x, mi, n, sp, kb0, kb1);
+        item_at(item, w, x, mi, n, sp, kb0, kb1);
         BO_STAMP(item, 0);
 #ifdef BO_PROBE
         if (blockIdx.x < kProbeCtas && item < kProbeItems)
@@ -613,7 +653,7 @@ __global__ void __launch_bounds__(192, 1)
       int x, mi, n, sp, kb0, kb1;
       int item = 0;
       for (int w = unit; w < total_work; w += n_units, ++item) {
-        decode(w, x, mi, n, sp, kb0, kb1);
+        item_at(item, w, x, mi, n, sp, kb0, kb1);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         BO_STAMP(item, 4);
@@ -686,7 +726,7 @@ __global__ void __launch_bounds__(192, 1)
     for (int w = unit; w < total_work; w += n_units) {
       if (item >= 0 && warp == 2 && lane == 0) BO_STAMP(item, 3);   // the previous tile's epilogue is done
       ++item;
-      decode(w, x, mi, n, sp, kb0, kb1);
+      item_at(item, w, x, mi, n, sp, kb0, kb1);
       const int rows_x = s_eoff[x + 1] - s_eoff[x];
       const int r_local = mi * TILE_M + static_cast<int>(crank) * kBM + q * 32 + lane;
       const bool valid = r_local < rows_x;
