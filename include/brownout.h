@@ -87,9 +87,7 @@ typedef enum {
   BO_OPT_PDL = 13,           /* 1: GEMMs launch with programmatic dependent launch                   [1]    */
   BO_OPT_ROUTE_FUSED = 14,   /* 1: decode-sized m <= 32 steps run router + top-K + Alg. 1 + permute +
                                    gather as one cooperative launch                                   [1]    */
-  BO_OPT_DECODE_SWAP = 15,   /* 1: decode-sized bf16 steps run each executor as one swapped CTA-pair tile
-                                   (weights on M, all its rows on N) when its rows fit (<= 288)       [1]    */
-  BO_OPT_COUNT = 16
+  BO_OPT_COUNT = 15
 } bo_engine_option;
 
 typedef struct {

@@ -274,8 +274,7 @@ void set_comb(bo::GemmParams& p, const CombFuse* cf, int d, int nt2) {
 bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, const int32_t* exec_off,
                     const int32_t* mtile_off, const FfnClass& orig, const FfnClass& uni, const FfnClass& shr,
                     void* Hbuf, void* Y, cudaStream_t s, Prof& prof, int& launches, float* partial,
-                    int* ks_dev, const CombFuse* comb, const int32_t* comb_row_tok, bool force_pair2,
-                    bool decode_swap) {
+                    int* ks_dev, const CombFuse* comb, const int32_t* comb_row_tok, bool force_pair2) {
   // partial != nullptr: GEMM2 runs split-K into fp32 partials [<=8, R, d] (the
   // caller combines them with launch_combine_partials); Y is then unused.
   const bo_config& c = h->cfg;
@@ -316,12 +315,10 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     bo::GemmParams p{};
     // 256 x 256 tiles on CTA pairs when rows are plentiful (prefill); few-row
     // (decode) steps keep 128-row tiles so that more tiles share the SMs.
-    // decode_swap: the *_DEC instantiation on pairs (GemmParams::swap_all)
-    const bool dec = decode_swap && o.cta_pairs && dt == 0 && bn == 256;
-    const bool pair = o.cta_pairs && dt == 0 && bn == 256 && (R >= o.pair_rows1 || dec);
+    const bool pair = o.cta_pairs && dt == 0 && bn == 256 && R >= o.pair_rows1;
     // swapped-operand tail tiles (pairs): maps [6..11] = 64-row gate / up boxes,
     // [12..14] = Xp in 16 / 32 / 64-row boxes
-    const bool swap = pair && (o.swap_tail || dec);
+    const bool swap = pair && o.swap_tail;
     if (swap) {
       for (int k = 0; k < 3; ++k) {
         const int width = k == 1 ? f_u : f;
@@ -375,17 +372,14 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     const int64_t max_work = ((R + tile_m - 1) / tile_m + n_exec) * p.n_tiles;
     const int units = pair ? h->num_sms / 2 : h->num_sms;
     const int grid = static_cast<int>(max_work < units ? max_work : units) * (pair ? 2 : 1);
-    p.swap_all = dec ? 1 : 0;
     prof.mark(launches, "gemm1_swiglu");
-    BO_CUDA(bo::launch_grouped_gemm(dt, dec ? bo::EPI_SWIGLU_DEC : (pair ? bo::EPI_SWIGLU_PAIR : bo::EPI_SWIGLU), bn,
-                                    mA, mb, p, grid, s, o.pdl),
+    BO_CUDA(bo::launch_grouped_gemm(dt, pair ? bo::EPI_SWIGLU_PAIR : bo::EPI_SWIGLU, bn, mA, mb, p, grid, s, o.pdl),
             "gemm1");
     ++launches;
   }
   {
     const int bn = gemm2_bn(d);
-    const bool dec = decode_swap && o.cta_pairs && dt == 0 && bn == 256;
-    const bool pair = o.cta_pairs && dt == 0 && bn == 256 && (R >= o.pair_rows2 || force_pair2 || dec);   // each CTA of a pair stages BN/2 of B
+    const bool pair = o.cta_pairs && dt == 0 && bn == 256 && (R >= o.pair_rows2 || force_pair2);   // each CTA of a pair stages BN/2 of B
     const uint32_t box_b = pair ? bn / 2 : bn;
     CUtensorMap mA;
     bo::BMaps mb;
@@ -415,11 +409,7 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.exec_off = exec_off;
     p.mtile_off = mtile_off;
     p.out = Y;
-    if (dec) {   // row operand (H) in 16 / 32 / 64-row boxes for the swapped tiles' second part
-      for (int i = 0; i < 3; ++i)
-        if ((st = make_map(&mb.m[12 + i], Hbuf, c.dtype, R, f, 16u << i)) != BO_OK) return st;
-      p.swap_all = 1;
-    } else if (o.tma_store && dt == 0 && !partial) {
+    if (o.tma_store && dt == 0 && !partial) {
       if ((st = make_map_store32(&mb.m[6], Y, static_cast<uint64_t>(R), static_cast<uint64_t>(d))) != BO_OK) return st;
       p.tma_store = 1;
     }
@@ -440,8 +430,8 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     const int units = pair ? h->num_sms / 2 : h->num_sms;
     const int grid = static_cast<int>(max_work < units ? max_work : units) * (pair ? 2 : 1);
     prof.mark(launches, comb ? "gemm2_weighted_combine" : "gemm2_weighted");
-    BO_CUDA(bo::launch_grouped_gemm(dt, dec ? bo::EPI_WEIGHTED_DEC : (pair ? bo::EPI_WEIGHTED_PAIR : bo::EPI_WEIGHTED),
-                                    bn, mA, mb, p, grid, s, o.pdl),
+    BO_CUDA(bo::launch_grouped_gemm(dt, pair ? bo::EPI_WEIGHTED_PAIR : bo::EPI_WEIGHTED, bn, mA, mb, p, grid, s,
+                                    o.pdl),
             "gemm2");
     ++launches;
   }
@@ -471,7 +461,6 @@ const OptionSpec kOptions[BO_OPT_COUNT] = {
     {&EngineOptions::router_split, "BO_ROUTER_SPLIT", 0, 1},
     {&EngineOptions::pdl, "BO_PDL", 0, 1},
     {&EngineOptions::route_fused, "BO_ROUTE_FUSED", 0, 1},
-    {&EngineOptions::decode_swap, "BO_DECODE_SWAP", 0, 1},
 };
 
 void options_from_env(EngineOptions* o) {
@@ -605,10 +594,7 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   const bool decode_pair2 = o.decode_pair2 && o.cta_pairs && dt == 0 && Rt <= kSplitRows &&
                             h->mode == BO_PARTIAL && Ns == 0 &&
                             static_cast<double>(Rt) >= 256.0 * (est_exec < 1.0 ? 1.0 : est_exec);
-  // Decode-sized bf16 steps: both FFN GEMMs on the decode instantiation (every executor one
-  // swapped tile when its rows fit, GemmParams::swap_all), GEMM2 with split-K partials
-  const bool decode_swap = o.decode_swap && o.cta_pairs && dt == 0 && Rt <= kSplitRows;
-  const bool split = (o.gemm2_splitk || decode_pair2 || decode_swap) && Rt <= kSplitRows;
+  const bool split = (o.gemm2_splitk || decode_pair2) && Rt <= kSplitRows;
   // a8 fused into GEMM2's epilogue unless split-K partials need their own combine
   // Auto: fused only where it measured faster (interleaved A/B, profiles/r01_ab_fused_combine.json):
   // prefill-sized steps with <= 2 rows per token (C2: GEMM2 + combine -5 %); with K = 8 (C4) the
@@ -632,7 +618,7 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   void* xp = at<char>(ws, L.xp);   // filled by the permute (small batches) or the gather kernel
   if ((st = ffn_stage(h, xp, Rt, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), orig, uni, shr,
                       at<char>(ws, L.h), yp, s, prof, launches, split ? at<float>(ws, L.partial) : nullptr,
-                      split ? at<int>(ws, L.ksplit) : nullptr, cfp, row_tok, decode_pair2, decode_swap)) != BO_OK)
+                      split ? at<int>(ws, L.ksplit) : nullptr, cfp, row_tok, decode_pair2)) != BO_OK)
     return st;
   // a8: combine (Eq. 5 sum over the token's K slots; split-K partials summed first)
   if (!fuse_comb) {

@@ -36,23 +36,20 @@ struct GemmShape {
 // (later items, if any, are decoded when reached).
 constexpr int kSchedItems = 256;
 
-// SA > 0: the decode instantiation (CTA pairs): every tile may be swapped, with up to SA
-// token rows per CTA in the B region (tiles of up to 2 * SA rows in one pass).
-template <typename T, int BN, int CG = 1, int SA = 0>
+template <typename T, int BN, int CG = 1>
 struct GemmCfg {
   static constexpr int BM = kBM;                         // rows per CTA (the pair covers CG * 128)
   static constexpr int BK = 128 / (int)sizeof(T);       // one 128-byte swizzle row
   static constexpr int UK = 32 / (int)sizeof(T);        // MMA K per instruction
   static constexpr int A_BYTES = BM * 128;
-  static constexpr int B_ROWS = (BN / CG) > SA ? (BN / CG) : SA;   // each CTA of a pair holds half of B
-  static constexpr int B_BYTES = B_ROWS * 128;
+  static constexpr int B_BYTES = (BN / CG) * 128;       // each CTA of a pair holds half of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int BAR_BYTES = 1024;                 // mbarriers + TMEM slot
   // executor offsets + m-tile prefix, then this unit's packed work list (keeps the staging 16B-aligned)
   static constexpr int SCHED_BYTES = ((2 * (kMaxExec + 1) + kSchedItems) * 4 + 127) / 128 * 128;
   static constexpr int EPI_ROW = 32 * (int)sizeof(T) + 16;   // staged 32-column row chunk + bank pad
   static constexpr int EPI_BYTES = 4 * 32 * EPI_ROW          // one staging tile per epilogue warp
-                                   + (SA ? 0 : 1024 + 4 * 4096);   // + two dense 2 KB TMA-store boxes per warp (1 KB aligned)
+                                   + 1024 + 4 * 4096;          // + two dense 2 KB TMA-store boxes per warp (1 KB aligned)
   static constexpr int OTHER = 1024 /*align slack*/ + BAR_BYTES + SCHED_BYTES + EPI_BYTES;
   static constexpr int STAGES_RAW = (227 * 1024 - OTHER) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
@@ -336,7 +333,7 @@ __device__ int g_probe_id[2][kProbeCtas][kProbeItems];
   } while (0)
 #endif
 
-template <typename T, int BN, int EPI, int KMAX, int CG, int SA = 0>
+template <typename T, int BN, int EPI, int KMAX, int CG>
 __global__ void __launch_bounds__(192, 1)
     k_grouped_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ BMaps tmB, const GemmParams p) {
   // CG = 1: one CTA computes a 128 x BN tile with tcgen05.mma.cta_group::1.
@@ -345,9 +342,7 @@ __global__ void __launch_bounds__(192, 1)
   //         128 rows of A and half of B (BN/2 rows), halving the shared-memory
   //         and L2 traffic per MMA; each CTA's TMEM holds its 128 rows.
   static_assert(CG == 1 || (CG == 2 && EPI != EPI_ROUTER && sizeof(T) == 2), "pair mode: bf16 FFN GEMMs");
-  static_assert(SA == 0 || (CG == 2 && SA > 128 && SA <= 256 && (EPI == EPI_SWIGLU || EPI == EPI_WEIGHTED)),
-                "decode instantiation: CTA pairs, FFN GEMMs");
-  using C = GemmCfg<T, BN, CG, SA>;
+  using C = GemmCfg<T, BN, CG>;
   constexpr int STAGES = C::STAGES;
   constexpr int TMEM_COLS = GemmShape<BN, EPI>::kTmemCols;
   constexpr uint32_t IDESC = idesc_f32acc<T>(128 * CG, BN);
@@ -363,7 +358,6 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* tfull_bar = empty_bar + STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
-  int* s_dec = reinterpret_cast<int*>(tmem_slot + 1);   // [decode swap-all mode, its widest tile's N]
   int* s_mtile = reinterpret_cast<int*>(smem + STAGES * C::STAGE_BYTES + C::BAR_BYTES);
   int* s_eoff = s_mtile + (kMaxExec + 1);
   int* s_sched = s_eoff + (kMaxExec + 1);   // [kSchedItems] this unit's decoded work list
@@ -424,37 +418,10 @@ __global__ void __launch_bounds__(192, 1)
   }
   __syncthreads();
   if (warp == 2) {
-    // Decode swap-all mode (SA > 0): when every executor's rows fit one swapped tile
-    // (<= 2 SA, rounded up to 32), each executor is ONE m-tile: its weight rows on the
-    // MMA's M side, all its rows on N (<= 256 per MMA, a second MMA beyond), so each
-    // weight byte enters exactly one SM pair, together with all the rows it multiplies.
-    bool dec = false;
-    int nsmax = 0;
-    if constexpr (SA > 0) {
-      if (p.swap_all && !p.a_shared) {
-        int mx = 0;
-        for (int i = lane; i < nexec; i += 32) {
-          const int r = s_eoff[i + 1] - s_eoff[i];
-          mx = r > mx ? r : mx;
-        }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-          const int t = __shfl_xor_sync(0xffffffffu, mx, off);
-          mx = t > mx ? t : mx;
-        }
-        nsmax = (mx + 31) & ~31;
-        dec = nsmax > 0 && nsmax <= 2 * SA;
-      }
-    }
-    if (lane == 0) {
-      s_dec[0] = dec ? 1 : 0;
-      s_dec[1] = nsmax;
-    }
     int carry = 0;
     for (int i0 = 0; i0 < nexec; i0 += 32) {
       const int i = i0 + lane;
-      const int rows_i = i < nexec ? s_eoff[i + 1] - s_eoff[i] : 0;
-      const int v = dec ? (rows_i > 0 ? 1 : 0) : (rows_i + TILE_M - 1) / TILE_M;
+      const int v = i < nexec ? (s_eoff[i + 1] - s_eoff[i] + TILE_M - 1) / TILE_M : 0;
       int incl = v;
 #pragma unroll
       for (int off = 1; off < 32; off <<= 1) {
@@ -470,9 +437,6 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  // decode swap-all mode; tiles wider than 256 rows need both accumulator buffers' columns
-  const bool dec = SA > 0 && s_dec[0] != 0;
-  const int nbuf = dec && s_dec[1] > 256 ? 1 : 2;
 
   // Executor classes: originals [0, mo), united [mo, mu), shared [mu, nexec).
   // United experts may differ in n-tiles, reduction length and B rows
@@ -515,13 +479,13 @@ __global__ void __launch_bounds__(192, 1)
   // them).  The MMA and the shared-memory traffic then scale with rin instead of a
   // full 256-row tile.  Three TMA boxes per k-block (gate, up, rows): the TMA issue
   // cost of 16-row boxes (8-12 per k-block) made such a tile slower than a full one.
-  constexpr bool kSwap = CG == 2 && (EPI == EPI_SWIGLU || (SA > 0 && EPI == EPI_WEIGHTED));
-  const bool swap_ok = kSwap && EPI == EPI_SWIGLU && p.swap_tail && !alt && !p.a_shared;
-  auto tile_rows = [&](int x, int mi) {   // rows of executor x in m-tile mi (decode mode: all of them)
+  constexpr bool kSwap = CG == 2 && EPI == EPI_SWIGLU;
+  const bool swap_ok = kSwap && p.swap_tail && !alt && !p.a_shared;
+  auto tile_rows = [&](int x, int mi) {   // rows of executor x in m-tile mi
     const int r = s_eoff[x + 1] - s_eoff[x] - mi * TILE_M;
-    return dec ? r : (r < TILE_M ? r : TILE_M);
+    return r < TILE_M ? r : TILE_M;
   };
-  auto swapped_tile = [&](int x, int mi) { return dec || (swap_ok && tile_rows(x, mi) < TILE_M); };
+  auto swapped_tile = [&](int x, int mi) { return swap_ok && tile_rows(x, mi) < TILE_M; };
   const int stage_tx = C::A_BYTES + (EPI == EPI_SWIGLU ? 2 * bh : BN) * 128 / CG;   // bytes per CTA per stage
   const int base_work = start_of(nexec);
   auto kblocks = [&](int x) { return (x < mo || x >= mu ? p.Kdim : p.Kdim_u) / C::BK; };
@@ -628,36 +592,21 @@ __global__ void __launch_bounds__(192, 1)
                                   : (cls == 1 ? (x - mo) * p.b_rows_u : (x - mu) * p.b_rows_per_exec);
         if constexpr (kSwap) {
           if (swapped_tile(x, mi)) {
-            // N = the tile's rows rounded up to 32: the first MMA takes n1 <= 256 of them,
-            // the second (decode tiles past 256 rows) the rest; each CTA stages half of each
-            // part (rows [0, 128) of its B region, then from row 128), one box per part of
-            // >= the half (16 / 32 / 64 / 128 rows; rows past it land unused).
-            const int ns = (tile_rows(x, mi) + 31) & ~31;
-            const int n1 = ns > 256 ? 256 : ns, n2 = ns - n1;
-            const int tok0 = s_eoff[x] + mi * TILE_M;
-            const int trow1 = tok0 + static_cast<int>(crank) * (n1 / 2);
-            const int trow2 = tok0 + n1 + static_cast<int>(crank) * (n2 / 2);
-            auto box_of = [](int r) { return r <= 16 ? 16 : (r <= 32 ? 32 : (r <= 64 ? 64 : 128)); };
-            const int tb1 = box_of(n1 / 2), tb2 = n2 > 0 ? box_of(n2 / 2) : 0;
-            const CUtensorMap* mt1 = tb1 == 128 ? &tmA : &tmB.m[tb1 == 16 ? 12 : (tb1 == 32 ? 13 : 14)];
-            const CUtensorMap* mt2 = tb2 == 128 ? &tmA : &tmB.m[tb2 == 16 ? 12 : (tb2 == 32 ? 13 : 14)];
-            // weights on M: SwiGLU = 64 gate + 64 up rows of this CTA's 64 output columns;
-            // GEMM2 = this CTA's 128 Wd rows (output columns) of the pair's BN
-            const int wrow = EPI == EPI_SWIGLU ? brow + n * 128 + static_cast<int>(crank) * 64
-                                               : brow + n * BN + static_cast<int>(crank) * 128;
+            const int rin = tile_rows(x, mi);
+            const int nsh = ((rin + 31) & ~31) / 2;   // token rows staged by this CTA (N / 2)
+            const int wrow = brow + n * 128 + static_cast<int>(crank) * 64;
+            const int trow = s_eoff[x] + mi * TILE_M + static_cast<int>(crank) * nsh;
+            // one box of >= nsh rows (16 / 32 / 64 / 128; rows past nsh land unused)
+            const int tbox = nsh <= 16 ? 16 : (nsh <= 32 ? 32 : (nsh <= 64 ? 64 : 128));
+            const CUtensorMap* mt = tbox == 128 ? &tmA : &tmB.m[tbox == 16 ? 12 : (tbox == 32 ? 13 : 14)];
             for (int kb = kb0; kb < kb1; ++kb) {
               mbar_wait(&empty_bar[stage], phase ^ 1);
               uint8_t* sa = smem + stage * C::STAGE_BYTES;
-              if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * (C::A_BYTES + (tb1 + tb2) * 128));
+              if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * (C::A_BYTES + tbox * 128));
               else mbar_arrive_remote(&full_bar[stage], 0);
-              if constexpr (EPI == EPI_SWIGLU) {
-                tma_load_2d_pair(sa, &tmB.m[6 + 2 * cls], &full_bar[stage], kb * C::BK, wrow, pol_b);
-                tma_load_2d_pair(sa + 64 * 128, &tmB.m[7 + 2 * cls], &full_bar[stage], kb * C::BK, wrow, pol_b);
-              } else {
-                tma_load_2d_pair(sa, &tmB.m[2 * cls], &full_bar[stage], kb * C::BK, wrow, pol_b);
-              }
-              tma_load_2d_pair(sa + C::A_BYTES, mt1, &full_bar[stage], kb * C::BK, trow1, pol_a);
-              if (tb2) tma_load_2d_pair(sa + C::A_BYTES + 128 * 128, mt2, &full_bar[stage], kb * C::BK, trow2, pol_a);
+              tma_load_2d_pair(sa, &tmB.m[6 + 2 * cls], &full_bar[stage], kb * C::BK, wrow, pol_b);
+              tma_load_2d_pair(sa + 64 * 128, &tmB.m[7 + 2 * cls], &full_bar[stage], kb * C::BK, wrow, pol_b);
+              tma_load_2d_pair(sa + C::A_BYTES, mt, &full_bar[stage], kb * C::BK, trow, pol_a);
               if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
             continue;
@@ -709,15 +658,9 @@ __global__ void __launch_bounds__(192, 1)
         tc_fence_after();
         BO_STAMP(item, 4);
         const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
-        uint32_t idesc_t = idesc, idesc_2 = 0;
-        int n2 = 0;   // decode tiles past 256 rows: a second MMA into accumulator columns 256..
+        uint32_t idesc_t = idesc;
         if constexpr (kSwap) {
-          if (swapped_tile(x, mi)) {
-            const int ns = (tile_rows(x, mi) + 31) & ~31;
-            idesc_t = idesc_f32acc<T>(256, ns > 256 ? 256 : ns);
-            n2 = ns > 256 ? ns - 256 : 0;
-            if (n2) idesc_2 = idesc_f32acc<T>(256, n2);
-          }
+          if (swapped_tile(x, mi)) idesc_t = idesc_f32acc<T>(256, (tile_rows(x, mi) + 31) & ~31);
         }
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
@@ -730,12 +673,8 @@ __global__ void __launch_bounds__(192, 1)
             const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
             if constexpr (CG == 1)
               mma_ss<T>(sdesc_k_sw128(a_addr + k * 32), sdesc_k_sw128(b_addr + k * 32), d_tmem, idesc, accum);
-            else {
+            else
               mma_ss_pair_bf16(sdesc_k_sw128(a_addr + k * 32), sdesc_k_sw128(b_addr + k * 32), d_tmem, idesc_t, accum);
-              if (n2)
-                mma_ss_pair_bf16(sdesc_k_sw128(a_addr + k * 32), sdesc_k_sw128(b_addr + 128 * 128 + k * 32),
-                                 d_tmem + 256, idesc_2, accum);
-            }
           }
           if constexpr (CG == 1) tc_commit(&empty_bar[stage]);
           else tc_commit_pair(&empty_bar[stage]);   // frees the stage in both CTAs
@@ -744,14 +683,14 @@ __global__ void __launch_bounds__(192, 1)
         if constexpr (CG == 1) tc_commit(&tfull_bar[acc]);
         else tc_commit_pair(&tfull_bar[acc]);       // both CTAs' epilogues
         BO_STAMP(item, 2);
-        if (++acc == nbuf) { acc = 0; acc_phase ^= 1; }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
       if constexpr (CG == 2) {
         // drain: the peer's last remote arrivals must land before the CTAs exit
         const int iters = total_work > unit ? (total_work - unit + n_units - 1) / n_units : 0;
         if (iters > 0) {
           const int last = iters - 1;
-          mbar_wait(&tempty_bar[last % nbuf], (last / nbuf) & 1);
+          mbar_wait(&tempty_bar[last & 1], (last >> 1) & 1);
         }
       }
     }
@@ -873,56 +812,6 @@ __global__ void __launch_bounds__(192, 1)
           __syncwarp();
         }
       } else if constexpr (EPI == EPI_WEIGHTED) {
-        if constexpr (SA > 0) {
-          if (dec) {
-            // Decode swapped tile: lane = output column (this CTA's 128 Wd rows), TMEM column
-            // = the executor's row; Yp[row, col] = row_w[row] * acc (Eq. 6), or the split's
-            // fp32 partial (summed by the combine), one 128-byte row segment per row and store.
-            const int rin = tile_rows(x, mi);
-            const int ns = (rin + 31) & ~31;
-            const int col = n * BN + static_cast<int>(crank) * 128 + q * 32 + lane;
-            const int64_t tok0 = static_cast<int64_t>(s_eoff[x]) + mi * TILE_M;
-#pragma unroll 1
-            for (int c = 0; c < ns; c += 32) {
-              uint32_t v[32];
-              tmem_ld32(t0 + c, v);
-              tmem_ld_wait();
-              const float wl = c + lane < rin ? (p.row_w ? p.row_w[tok0 + c + lane] : p.alpha) : 0.0f;
-              if (p.ksplit_max > 1) {
-                float* outp = p.partial + (static_cast<int64_t>(sp) * p.rows_total + tok0 + c) * p.ldo + col;
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                  const float w = __shfl_sync(0xffffffffu, wl, j);
-                  if (c + j < rin) outp[static_cast<int64_t>(j) * p.ldo] = kb1 > kb0 ? __uint_as_float(v[j]) * w : 0.0f;
-                }
-              } else {
-#pragma unroll
-                for (int j = 0; j < 32; ++j)
-                  *reinterpret_cast<T*>(stage + j * C::EPI_ROW + lane * (int)sizeof(T)) =
-                      static_cast<T>(__uint_as_float(v[j]) * __shfl_sync(0xffffffffu, wl, j));
-                __syncwarp();
-                T* out = reinterpret_cast<T*>(p.out) + n * BN + static_cast<int>(crank) * 128 + q * 32;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  const int pc = i * 32 + lane, tk = pc >> 2, part = pc & 3;
-                  if (c + tk < rin) {
-                    const uint4 val = *reinterpret_cast<const uint4*>(stage + tk * C::EPI_ROW + part * 16);
-                    st_global_hint(out + (tok0 + c + tk) * p.ldo + part * (16 / (int)sizeof(T)), val, pol_out);
-                  }
-                }
-                __syncwarp();
-              }
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-              if (leader) mbar_arrive(&tempty_bar[acc]);
-              else mbar_arrive_remote(&tempty_bar[acc], 0);
-            }
-            if (++acc == nbuf) { acc = 0; acc_phase ^= 1; }
-            continue;
-          }
-        }
         const float wr = valid ? (p.row_w ? p.row_w[grow] : p.alpha) : 0.0f;
         if (p.ksplit_max > 1 || p.f32_mode) {   // split-K: fp32 partial of split sp, row-scaled (Eq. 6)
           float* outp = p.partial + (static_cast<int64_t>(sp) * p.rows_total + grow) * p.ldo + n * BN;
@@ -950,7 +839,7 @@ __global__ void __launch_bounds__(192, 1)
             if (CG == 1 || leader) mbar_arrive(&tempty_bar[acc]);
             else mbar_arrive_remote(&tempty_bar[acc], 0);
           }
-          if (++acc == nbuf) { acc = 0; acc_phase ^= 1; }
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
           continue;
         }
         T* out = reinterpret_cast<T*>(p.out) + n * BN;
@@ -1003,7 +892,7 @@ __global__ void __launch_bounds__(192, 1)
             if (CG == 1 || leader) mbar_arrive(&tempty_bar[acc]);
             else mbar_arrive_remote(&tempty_bar[acc], 0);
           }
-          if (++acc == nbuf) { acc = 0; acc_phase ^= 1; }
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
           // Release this warp's Yp rows (every lane fences its own stores, then the
           // warp barrier), count each row's BN columns against its token; the warp
           // whose arrival completes a token (all BN columns of every slot landed)
@@ -1132,7 +1021,7 @@ __global__ void __launch_bounds__(192, 1)
           p.tile_cnt[static_cast<int64_t>(mi) * p.n_valid + e] = cnt;
         }
         epi_bar();   // the staging rows are reused by the next tile
-        if (++acc == nbuf) { acc = 0; acc_phase ^= 1; }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         continue;
       }
       tc_fence_before();
@@ -1141,7 +1030,7 @@ __global__ void __launch_bounds__(192, 1)
         if (CG == 1 || leader) mbar_arrive(&tempty_bar[acc]);
         else mbar_arrive_remote(&tempty_bar[acc], 0);
       }
-      if (++acc == nbuf) { acc = 0; acc_phase ^= 1; }
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }
 
@@ -1179,12 +1068,12 @@ static cudaError_t ensure_smem_attr(K kern, int bytes, std::atomic<uint64_t>& do
   return e;
 }
 
-template <typename T, int BN, int EPI, int KMAX = 0, int CG = 1, int SA = 0>
+template <typename T, int BN, int EPI, int KMAX = 0, int CG = 1>
 static cudaError_t launch_t(const CUtensorMap& A, const BMaps& B, const GemmParams& p, int grid, cudaStream_t s,
                             bool pdl) {
-  using C = GemmCfg<T, BN, CG, SA>;
+  using C = GemmCfg<T, BN, CG>;
   static std::atomic<uint64_t> attr_done{0};
-  auto kern = k_grouped_gemm<T, BN, EPI, KMAX, CG, SA>;
+  auto kern = k_grouped_gemm<T, BN, EPI, KMAX, CG>;
   cudaError_t e = ensure_smem_attr(kern, C::SMEM, attr_done);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -1216,13 +1105,7 @@ static cudaError_t launch_t(const CUtensorMap& A, const BMaps& B, const GemmPara
 template <typename T>
 static cudaError_t dispatch(int epi, int bn, const CUtensorMap& A, const BMaps& B, const GemmParams& p, int grid,
                             cudaStream_t s, bool pdl) {
-  if (epi == EPI_SWIGLU_DEC) {
-    if constexpr (sizeof(T) == 2)
-      if (bn == 256) return launch_t<T, 256, EPI_SWIGLU, 0, 2, kDecodeRows>(A, B, p, grid, s, pdl);
-  } else if (epi == EPI_WEIGHTED_DEC) {
-    if constexpr (sizeof(T) == 2)
-      if (bn == 256) return launch_t<T, 256, EPI_WEIGHTED, 0, 2, kDecodeRows>(A, B, p, grid, s, pdl);
-  } else if (epi == EPI_SWIGLU_PAIR) {
+  if (epi == EPI_SWIGLU_PAIR) {
     if constexpr (sizeof(T) == 2)
       if (bn == 256) return launch_t<T, 256, EPI_SWIGLU, 0, 2>(A, B, p, grid, s, pdl);
   } else if (epi == EPI_WEIGHTED_PAIR) {

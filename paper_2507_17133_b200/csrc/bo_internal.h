@@ -30,7 +30,6 @@ struct EngineOptions {
   int32_t router_split = 1;    // decode-sized m <= 32 batches: split-warp router
   int32_t pdl = 1;             // programmatic dependent launch of the GEMMs
   int32_t route_fused = 1;     // decode-sized m <= 32: routing, Alg. 1, permute + gather in one launch
-  int32_t decode_swap = 1;     // decode-sized bf16 steps: FFN GEMMs on the swapped decode instantiation
 };
 
 struct bo_handle {
@@ -135,6 +134,6 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
                     const int32_t* mtile_off, const FfnClass& orig, const FfnClass& uni, const FfnClass& shr,
                     void* Hbuf, void* Y, cudaStream_t s, Prof& prof, int& launches, float* partial = nullptr,
                     int* ks_dev = nullptr, const CombFuse* comb = nullptr, const int32_t* comb_row_tok = nullptr,
-                    bool force_pair2 = false, bool decode_swap = false);
+                    bool force_pair2 = false);
 
 }  // namespace bo_impl

@@ -13,11 +13,7 @@ constexpr int kMaxExperts = 256;
 constexpr int kMaxExec = 512;   // m + G
 
 enum Epi : int { EPI_SWIGLU = 0, EPI_WEIGHTED = 1, EPI_ROUTER = 2,
-                 EPI_SWIGLU_PAIR = 3, EPI_WEIGHTED_PAIR = 4,    // *_PAIR: cta_group::2, grid even
-                 EPI_SWIGLU_DEC = 5, EPI_WEIGHTED_DEC = 6 };    // *_DEC: pairs, decode swap-all instantiation
-// Decode instantiation: up to this many token rows per CTA in a swapped tile (tiles of up to
-// 2 x kDecodeRows rows of one executor in one pass; GemmParams::swap_all).
-constexpr int kDecodeRows = 144;
+                 EPI_SWIGLU_PAIR = 3, EPI_WEIGHTED_PAIR = 4 };   // *_PAIR: cta_group::2, grid even
 
 struct GemmParams {
   int Kdim;              // reduction length (executors < m_orig)
@@ -74,11 +70,6 @@ struct GemmParams {
   // Maps [6..11] then hold 64-row gate / up boxes and [12..14] 16 / 32 / 64-row boxes of A (Xp).
   int swap_tail;
   int tma_store;            // EPI_WEIGHTED: full 32-row slabs leave through TMA bulk stores (map B[6], 32 x 32 box, 64B swizzle)
-  // *_DEC instantiations: when every executor holds <= 2 kDecodeRows rows, each executor is
-  // one swapped m-tile (weights on M, all of its rows on N: each weight byte enters one CTA
-  // pair together with every row it multiplies).  Maps as for swap_tail; [12..14] = 16 / 32 /
-  // 64-row boxes of the row operand (Xp for GEMM1, H for GEMM2); tma_store must be 0.
-  int swap_all;
 };
 
 // Combine of split-K fp32 partials: y[t] = [x_t] + sum_slots sum_splits P[sp][row].
