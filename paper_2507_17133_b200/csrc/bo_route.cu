@@ -1359,53 +1359,6 @@ __global__ void __launch_bounds__(256) k_combine(const T* __restrict__ yp, const
   }
 }
 
-// The same Eq. 5 sum with the token's KR <= KRB row indices read first and every row load
-// of the vector issued before the in-order accumulation (KRB loads in flight per thread
-// instead of one dependent round trip per slot); arithmetic and order as k_combine, so
-// the result is bitwise the same.
-template <typename T, int KRB>
-__global__ void __launch_bounds__(256) k_combine_mlp(const T* __restrict__ yp, const T* __restrict__ x, int Tn,
-                                                     int d, int KR, const int32_t* __restrict__ row_of,
-                                                     int add_residual, T* __restrict__ y) {
-  const int nvec = d / 8;
-  const int64_t total = static_cast<int64_t>(Tn) * nvec;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
-    const int64_t t = i / nvec;
-    const int c = static_cast<int>(i - t * nvec);
-    int r[KRB];
-#pragma unroll
-    for (int s = 0; s < KRB; ++s) r[s] = s < KR ? __ldg(row_of + t * KR + s) : -1;
-    float v[KRB][8];
-#pragma unroll
-    for (int s = 0; s < KRB; ++s)
-      if (r[s] >= 0) Vec8<T>::load(yp + static_cast<int64_t>(r[s]) * d + c * 8, v[s]);
-    float acc[8];
-    if (add_residual) {
-      Vec8<T>::load(x + t * d + c * 8, acc);
-    } else {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) acc[k] = 0.0f;
-    }
-#pragma unroll
-    for (int s = 0; s < KRB; ++s)   // slot order, then slice order (Eq. 5 sum)
-      if (r[s] >= 0) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) acc[k] += v[s][k];
-      }
-    Vec8<T>::store(y + t * d + c * 8, acc);
-  }
-}
-
-template <typename T>
-static void combine_dispatch(int blocks, const T* yp, const T* x, int T_, int d, int KR, const int32_t* row_of,
-                             int add_residual, T* y, cudaStream_t s) {
-  if (KR <= 2) k_combine_mlp<T, 2><<<blocks, 256, 0, s>>>(yp, x, T_, d, KR, row_of, add_residual, y);
-  else if (KR <= 4) k_combine_mlp<T, 4><<<blocks, 256, 0, s>>>(yp, x, T_, d, KR, row_of, add_residual, y);
-  else if (KR <= 8) k_combine_mlp<T, 8><<<blocks, 256, 0, s>>>(yp, x, T_, d, KR, row_of, add_residual, y);
-  else k_combine<T><<<blocks, 256, 0, s>>>(yp, x, T_, d, KR, row_of, add_residual, y);
-}
-
 cudaError_t launch_combine(int dtype, const void* yp, const void* x, int T, int d, int KR, const int32_t* row_of,
                            int add_residual, void* y, int num_sms, cudaStream_t s) {
   if (T == 0) return cudaSuccess;
@@ -1413,12 +1366,13 @@ cudaError_t launch_combine(int dtype, const void* yp, const void* x, int T, int 
   int64_t blocks = (total + 255) / 256;
   if (blocks > num_sms * 8) blocks = num_sms * 8;
   if (dtype == 0)
-    combine_dispatch<__nv_bfloat16>(static_cast<int>(blocks), static_cast<const __nv_bfloat16*>(yp),
-                                    static_cast<const __nv_bfloat16*>(x), T, d, KR, row_of, add_residual,
-                                    static_cast<__nv_bfloat16*>(y), s);
+    k_combine<__nv_bfloat16><<<static_cast<int>(blocks), 256, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(yp), static_cast<const __nv_bfloat16*>(x), T, d, KR, row_of, add_residual,
+        static_cast<__nv_bfloat16*>(y));
   else
-    combine_dispatch<float>(static_cast<int>(blocks), static_cast<const float*>(yp), static_cast<const float*>(x), T,
-                            d, KR, row_of, add_residual, static_cast<float*>(y), s);
+    k_combine<float><<<static_cast<int>(blocks), 256, 0, s>>>(static_cast<const float*>(yp),
+                                                              static_cast<const float*>(x), T, d, KR, row_of,
+                                                              add_residual, static_cast<float*>(y));
   return cudaGetLastError();
 }
 
