@@ -57,7 +57,9 @@ def main():
     for name, f in [
         ("decode", lambda: run(small)),
         ("decode_ratio1", lambda: run(small, ratio=1.0)),
-        ("router_gpu", lambda: run(small, logits=False)),
+        ("router_gpu", lambda: run(small, logits=False)),   # k_route_fused (decode-sized, m <= 32)
+        ("router_gpu_unfused", lambda: run_env({"BO_ROUTE_FUSED": "0"}, small, logits=False)),
+        ("router_gpu_fused_shared", lambda: run(shared, logits=False)),
         ("prefill_pairs_fused_combine", lambda: run(pair)),   # GEMM1 swapped tail tiles (default)
         ("decode_gemm2_splitk", lambda: run_env({"BO_GEMM2_SPLITK": "1"}, small)),
         ("fp32", lambda: run(fp32)),

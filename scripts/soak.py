@@ -23,7 +23,8 @@ from oracle import brownout_oracle as O  # noqa: E402
 KNOBS = [{}, {"BO_FUSED_COMBINE": "1"}, {"BO_FUSED_COMBINE": "0"}, {"BO_CTA_PAIRS": "0"}, {"BO_GEMM2_SPLITK": "1"},
          {"BO_TILE_ALT": "0"}, {"BO_DECODE_PAIR2": "0"},
          {"BO_PAIR_ROWS1": "1", "BO_PAIR_ROWS2": "1"}, {"BO_B_POLICY": "1"},
-         {"BO_PAIR_ROWS1": "1", "BO_SWAP_TAIL": "0"}, {"BO_TMA_STORE": "0", "BO_PDL": "0"}]
+         {"BO_PAIR_ROWS1": "1", "BO_SWAP_TAIL": "0"}, {"BO_TMA_STORE": "0", "BO_PDL": "0"},
+         {"BO_ROUTE_FUSED": "0"}]
 
 
 def case(rng, i):
@@ -41,10 +42,13 @@ def case(rng, i):
     cfg = S.LayerConfig(f"soak{i}", d=d, f=f, m=m, K=K, way=way, T=T, ratio=ratio, dtype=dt,
                         sigma=float(rng.choice([0.0, 0.5, 1.0])), config_id=500 + i, Ns=Ns)
     knob = KNOBS[int(rng.integers(0, len(KNOBS)))]
-    return cfg, mode, dedup, bool(rng.random() < 0.3), knob
+    # 30 %: the production router (Eq. 8 on the GPU, the fused decode routing launch for small
+    # T) on exactly representable inputs, compared with the oracle's own Eq. 8 path
+    prod = bool(rng.random() < 0.3)
+    return cfg, mode, dedup, bool(rng.random() < 0.3), knob, prod
 
 
-def run(cfg, mode, dedup, residual, knob):
+def run(cfg, mode, dedup, residual, knob, prod=False):
     from paper_2507_17133_b200 import BrownoutMoE
     old = {k: os.environ.get(k) for k in knob}
     os.environ.update(knob)
@@ -61,20 +65,25 @@ def run(cfg, mode, dedup, residual, knob):
     uni = S.make_united_random(cfg)
     x = S.make_tokens(cfg, batch_index=cfg.config_id)
     L = S.make_logits(cfg.T, cfg.m, seed=cfg.config_id, sigma=cfg.sigma)
+    Wr = lay["Wr"]
+    if prod:
+        x, Wr = S.make_exact_router_inputs(cfg, ties=cfg.config_id % 2 == 0)
+        prod = S.exactness_bound(x, Wr) < 2.0 ** 11   # else injected logits as usual
     moe.set_brownout(cfg.ratio, mode)
     g = {k: v.cuda() for k, v in lay.items()}
     u = {k: v.cuda() for k, v in uni.items()}
     sh = (g["SWg"], g["SWu"], g["SWd"]) if cfg.Ns else None
-    y = moe.forward(x.cuda(), g["Wr"], (g["Wg"], g["Wu"], g["Wd"]), (u["UWg"], u["UWu"], u["UWd"]),
-                    logits=L.cuda(), shared=sh)
+    y = moe.forward(x.cuda(), Wr.cuda(), (g["Wg"], g["Wu"], g["Wd"]), (u["UWg"], u["UWu"], u["UWd"]),
+                    logits=None if prod else L.cuda(), shared=sh)
     torch.cuda.synchronize()
     dbg = moe.debug_arrays(cfg.T)
     npd = lambda t: t.detach().cpu().double().numpy()
     ex = tuple(npd(lay[k]) for k in ("Wg", "Wu", "Wd"))
     un = tuple(npd(uni[k]) for k in ("UWg", "UWu", "UWd"))
     shn = tuple(npd(lay[k]) for k in ("SWg", "SWu", "SWd")) if cfg.Ns else None
-    ref = O.moe_forward(npd(x), None, ex, un, cfg.K, cfg.way, cfg.ratio, mode=O.FULL if mode == "full" else O.PARTIAL,
-                        logits=L.double().numpy(), add_residual=residual, dedup=dedup, shared=shn)
+    ref = O.moe_forward(npd(x), npd(Wr) if prod else None, ex, un, cfg.K, cfg.way, cfg.ratio,
+                        mode=O.FULL if mode == "full" else O.PARTIAL, logits=None if prod else L.double().numpy(),
+                        add_residual=residual, dedup=dedup, shared=shn)
     errs = []
     if not np.array_equal(dbg["topk_id"].cpu().numpy(), ref.ids):
         errs.append("topk")
@@ -102,14 +111,15 @@ def main():
     rng = np.random.default_rng(args.seed)
     fails = 0
     for i in range(args.n):
-        cfg, mode, dedup, residual, knob = case(rng, i)
+        cfg, mode, dedup, residual, knob, prod = case(rng, i)
         try:
-            errs = run(cfg, mode, dedup, residual, knob)
+            errs = run(cfg, mode, dedup, residual, knob, prod)
         except Exception as ex:   # noqa: BLE001
             errs = [f"exception {type(ex).__name__}: {ex}"]
         if errs:
             fails += 1
-            print("FAIL", cfg, mode, "dedup" if dedup else "", "res" if residual else "", knob, errs, flush=True)
+            print("FAIL", cfg, mode, "dedup" if dedup else "", "res" if residual else "", "router" if prod else "",
+                  knob, errs, flush=True)
     print(f"soak: {args.n - fails}/{args.n} passed", flush=True)
     sys.exit(1 if fails else 0)
 
