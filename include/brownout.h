@@ -87,8 +87,7 @@ typedef enum {
   BO_OPT_PDL = 13,           /* 1: GEMMs launch with programmatic dependent launch                   [1]    */
   BO_OPT_ROUTE_FUSED = 14,   /* 1: decode-sized m <= 32 steps run router + top-K + Alg. 1 + permute +
                                    gather as one cooperative launch                                   [1]    */
-  BO_OPT_HALF_TAIL = 15,     /* 1: GEMM2 on CTA pairs runs a partial last wave's tiles as two halves    [1]    */
-  BO_OPT_COUNT = 16
+  BO_OPT_COUNT = 15
 } bo_engine_option;
 
 typedef struct {

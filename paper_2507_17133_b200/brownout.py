@@ -25,7 +25,7 @@ BO_UNITED_MEAN = 0
 # bo_engine_option (include/brownout.h): name -> id
 ENGINE_OPTIONS = {n: i for i, n in enumerate((
     "cta_pairs", "pair_rows1", "pair_rows2", "tile_alt", "swap_tail", "decode_pair2", "gemm2_splitk",
-    "fused_combine", "tma_store", "store_hint", "b_policy", "router_mma", "router_split", "pdl", "route_fused", "half_tail"))}
+    "fused_combine", "tma_store", "store_hint", "b_policy", "router_mma", "router_split", "pdl", "route_fused"))}
 
 EXPORTED = (
     "bo_create", "bo_destroy", "bo_workspace_size", "bo_workspace_layout", "bo_build_united", "bo_set_shared_experts",

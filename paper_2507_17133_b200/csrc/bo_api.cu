@@ -390,12 +390,8 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
       const uint64_t rows = static_cast<uint64_t>(q.stack > 0 ? q.stack : 1) * d;
       if ((st = make_map(&mb.m[2 * k], ptr(*cls[k], 2), c.dtype, rows, kdim, box_b)) != BO_OK) return st;
       mb.m[2 * k + 1] = mb.m[2 * k];
-      // half-width last wave (pairs): BN/4 Wd rows per CTA
-      if (pair && o.half_tail && (st = make_map(&mb.m[7 + k], ptr(*cls[k], 2), c.dtype, rows, kdim, bn / 4)) != BO_OK)
-        return st;
     }
     bo::GemmParams p{};
-    p.half_tail = pair && o.half_tail ? 1 : 0;
     p.Kdim = f;
     p.n_tiles = d / bn;
     p.Kdim_u = f_u;
@@ -465,7 +461,6 @@ const OptionSpec kOptions[BO_OPT_COUNT] = {
     {&EngineOptions::router_split, "BO_ROUTER_SPLIT", 0, 1},
     {&EngineOptions::pdl, "BO_PDL", 0, 1},
     {&EngineOptions::route_fused, "BO_ROUTE_FUSED", 0, 1},
-    {&EngineOptions::half_tail, "BO_HALF_TAIL", 0, 1},
 };
 
 void options_from_env(EngineOptions* o) {

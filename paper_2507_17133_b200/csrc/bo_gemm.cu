@@ -507,25 +507,12 @@ __global__ void __launch_bounds__(192, 1)
     }
     if (p.ksplit_max > 1 && blockIdx.x == 0 && threadIdx.x == 0) *p.ks_out = ks;
   }
-  // Half-width last wave (GEMM2 on CTA pairs, GemmParams::half_tail): the X = base_work mod
-  // units tiles that would form a partial last wave are cut into two BN/2-column halves
-  // each, no fix-up needed (disjoint columns), so 2X <= units pairs take half a tile
-  // instead of X taking a whole one (C2: 544 tiles on 74 pairs, 7.35 -> 7.5 instead of 8).
-  int hsplit = 0;
-  if constexpr (EPI == EPI_WEIGHTED && CG == 2) {
-    if (p.half_tail && ks == 1) {
-      const int X = base_work % n_units;
-      if (X > 0 && 2 * X <= n_units) hsplit = X;
-    }
-  }
-  const int total_work = base_work * ks + hsplit;
+  const int total_work = base_work * ks;
 
   // work item -> tile (executor x, m-tile mi fastest, n-tile n) + k-block range
   // [kb0, kb1) of split sp; units take items unit, unit + n_units, ... (the
-  // concurrently running CTAs share each weight tile through L2).  A half item (hsplit)
-  // decodes to its tile; half_of(w) tells which columns.
+  // concurrently running CTAs share each weight tile through L2)
   auto decode = [&](int w, int& x, int& mi, int& n, int& sp, int& kb0, int& kb1) {
-    if (hsplit && w >= base_work - hsplit) w = base_work - hsplit + ((w - (base_work - hsplit)) >> 1);
     const int tw = w / ks;
     sp = w - tw * ks;
     int lo = 0, hi = nexec;
@@ -543,7 +530,6 @@ __global__ void __launch_bounds__(192, 1)
     kb0 = sp * per < nkb ? sp * per : nkb;
     kb1 = kb0 + per < nkb ? kb0 + per : nkb;
   };
-  auto half_of = [&](int w) { return hsplit && w >= base_work - hsplit ? ((w - (base_work - hsplit)) & 1) : -1; };
   // This unit's work list, decoded by all threads at once: the binary search over the
   // executors sat on the MMA warp's critical path between tiles (0.5-0.9 us per tile with
   // 5-57 executors, probe build), ~10 % of a 12-k-block C4 GEMM2 tile.  Packed as
@@ -642,16 +628,12 @@ __global__ void __launch_bounds__(192, 1)
             }
           } else {
             // Both CTAs load their halves; completion is counted on the leader's barrier.
-            const int hf = half_of(w);   // GEMM2 half item: BN/4 Wd rows per CTA (maps [7 + class])
-            if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * (hf >= 0 ? C::A_BYTES + (BN / 4) * 128 : stage_tx));
+            if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * stage_tx);
             else mbar_arrive_remote(&full_bar[stage], 0);
             tma_load_2d_pair(sa, &tmA, &full_bar[stage], kb * C::BK, arow, pol_a);
             if constexpr (EPI == EPI_SWIGLU) {
               // leader: gate rows, peer: up rows of the same f-columns -> D[:, 0:BN/2] = gate, D[:, BN/2:] = up
               tma_load_2d_pair(sb, leader ? mb0 : mb1, &full_bar[stage], kb * C::BK, brow + n * bh, pol_b);
-            } else if (hf >= 0) {
-              tma_load_2d_pair(sb, &tmB.m[7 + cls], &full_bar[stage], kb * C::BK,
-                               brow + n * BN + hf * (BN / 2) + static_cast<int>(crank) * (BN / 4), pol_b);
             } else {
               tma_load_2d_pair(sb, mb0, &full_bar[stage], kb * C::BK,
                                brow + n * BN + static_cast<int>(crank) * (BN / 2), pol_b);
@@ -679,9 +661,6 @@ __global__ void __launch_bounds__(192, 1)
         uint32_t idesc_t = idesc;
         if constexpr (kSwap) {
           if (swapped_tile(x, mi)) idesc_t = idesc_f32acc<T>(256, (tile_rows(x, mi) + 31) & ~31);
-        }
-        if constexpr (EPI == EPI_WEIGHTED && CG == 2) {
-          if (half_of(w) >= 0) idesc_t = idesc_f32acc<T>(256, BN / 2);
         }
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
@@ -863,18 +842,14 @@ __global__ void __launch_bounds__(192, 1)
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
           continue;
         }
-        // a half item (GemmParams::half_tail) holds BN/2 columns, from column hc0 of the n-tile
-        const int hf = half_of(w);
-        const int hc0 = hf > 0 ? BN / 2 : 0;
-        const int ncols = hf >= 0 ? BN / 2 : BN;
-        T* out = reinterpret_cast<T*>(p.out) + n * BN + hc0;
+        T* out = reinterpret_cast<T*>(p.out) + n * BN;
         // TMA bulk stores for full slabs (no fused combine, which re-reads the rows at once):
         // thread = row writes its 64 bytes into a dense 32 x 32 box (64B swizzle: 16-byte
         // chunk q of row r at q ^ ((r >> 1) & 3), conflict-free), one elected lane stores
         // the box; two boxes per warp alternate.
         const bool tma_out = sizeof(T) == 2 && p.tma_store && nrows == 32 && !p.comb_cnt;
 #pragma unroll 1
-        for (int c = 0; c < ncols; c += 32) {
+        for (int c = 0; c < BN; c += 32) {
           uint32_t a[32];
           tmem_ld32(t0 + c, a);
           tmem_ld_wait();
@@ -897,7 +872,7 @@ __global__ void __launch_bounds__(192, 1)
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              tma_store_2d(&tmB.m[6], tb, n * BN + hc0 + c, static_cast<int>(row0));
+              tma_store_2d(&tmB.m[6], tb, n * BN + c, static_cast<int>(row0));
               bulk_commit();
             }
             continue;
@@ -919,9 +894,9 @@ __global__ void __launch_bounds__(192, 1)
           }
           if (++acc == 2) { acc = 0; acc_phase ^= 1; }
           // Release this warp's Yp rows (every lane fences its own stores, then the
-          // warp barrier), count each row's columns (BN, or BN/2 for a half item) against
-          // its token; the warp whose arrival completes a token (all BN columns of every
-          // slot landed) sums its rows for this n-tile.
+          // warp barrier), count each row's BN columns against its token; the warp
+          // whose arrival completes a token (all BN columns of every slot landed)
+          // sums its rows for this n-tile.
           __threadfence();
           __syncwarp();
           int t = -1;
@@ -934,7 +909,7 @@ __global__ void __launch_bounds__(192, 1)
             need += rr[sl] >= 0 ? 1 : 0;
           }
           const bool last =
-              valid && atomicAdd(p.comb_cnt + static_cast<int64_t>(t) * p.comb_nt + n, ncols) == need * BN - ncols;
+              valid && atomicAdd(p.comb_cnt + static_cast<int64_t>(t) * p.comb_nt + n, BN) == need * BN - BN;
           const uint32_t done = __ballot_sync(0xffffffffu, last);
           if (done) {
             __threadfence();   // acquire: the other rows' stores precede their counts

@@ -30,7 +30,6 @@ struct EngineOptions {
   int32_t router_split = 1;    // decode-sized m <= 32 batches: split-warp router
   int32_t pdl = 1;             // programmatic dependent launch of the GEMMs
   int32_t route_fused = 1;     // decode-sized m <= 32: routing, Alg. 1, permute + gather in one launch
-  int32_t half_tail = 1;       // GEMM2 on pairs: a partial last wave's tiles run as BN/2-column halves
 };
 
 struct bo_handle {

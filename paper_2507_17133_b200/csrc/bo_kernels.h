@@ -70,9 +70,6 @@ struct GemmParams {
   // Maps [6..11] then hold 64-row gate / up boxes and [12..14] 16 / 32 / 64-row boxes of A (Xp).
   int swap_tail;
   int tma_store;            // EPI_WEIGHTED: full 32-row slabs leave through TMA bulk stores (map B[6], 32 x 32 box, 64B swizzle)
-  // EPI_WEIGHTED on CTA pairs: the X = tiles mod pairs tiles of a partial last wave run as
-  // two BN/2-column halves each (when 2X <= pairs); maps [7..9] = B boxes of BN/4 rows per class
-  int half_tail;
 };
 
 // Combine of split-K fp32 partials: y[t] = [x_t] + sum_slots sum_splits P[sp][row].
