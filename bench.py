@@ -61,7 +61,7 @@ class ClockSampler:
     }
 
     def __init__(self, index):
-        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.samples, self.reasons, self.max_mhz, self.power_w = [], set(), None, []
         self._stop = threading.Event()
         self._th = None
         try:
@@ -77,6 +77,7 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM))
+                self.power_w.append(self.nvml.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
                 r = self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for bit, name in self.REASONS.items():
                     if r & bit:
@@ -99,8 +100,16 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
-        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(self.samples)}
+        out = {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+               "sm_mhz_min": min(self.samples), "reasons": sorted(self.reasons - {"gpu_idle"}),
+               "samples": len(self.samples)}
+        if self.power_w:
+            out["power_w_median"] = statistics.median(self.power_w)
+            try:
+                out["power_limit_w"] = self.nvml.nvmlDeviceGetEnforcedPowerLimit(self.h) / 1000.0
+            except Exception:
+                pass
+        return out
 
 
 # --------------------------------------------------------------- workload
