@@ -1184,10 +1184,18 @@ __global__ void __launch_bounds__(256)
                reinterpret_cast<const uint4*>(x), xp, vec_per_row, n_shared, s_xoff + E);
 }
 
+// Co-resident CTAs of the cooperative grid (resident CTAs per SM x #SM), queried once per
+// device and kept (the forward is on the host's per-call path).
 template <typename T, int MAXM>
 static int route_fused_capacity(int num_sms) {
-  int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_route_fused<T, MAXM>, 256, 0) != cudaSuccess) return 0;
+  static std::atomic<int> per_sm[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  int nb = dev < 64 ? per_sm[dev].load(std::memory_order_relaxed) : 0;
+  if (nb <= 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_route_fused<T, MAXM>, 256, 0) != cudaSuccess) return 0;
+    if (dev < 64) per_sm[dev].store(nb, std::memory_order_relaxed);
+  }
   return nb * num_sms;
 }
 
