@@ -841,6 +841,12 @@ def run_ep(args, cfg, rank, world, local, pk):
         out["batch_sweep"] = sw
     if rank == 0:
         print(json.dumps(out), flush=True)
+    # the timed regions' graphs are gone (locals of timed()); release the library's NCCL
+    # communicators before the process group (a communicator destroyed under a live graph
+    # that captured it blocks: include/brownout.h bo_ep_destroy)
+    torch.cuda.synchronize()
+    for c in (ctx_small, ctx_big):
+        c.close()
     dist.destroy_process_group()
 
 
