@@ -511,7 +511,9 @@ def main():
 
     local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
-    dist_on = world > 1
+    # BO_BENCH_EP=1: the expert-parallel bench path even on a world of one (test rigs: the
+    # library's NCCL forward, graph capture and teardown on a single GPU)
+    dist_on = world > 1 or os.environ.get("BO_BENCH_EP") == "1"
     if dist_on:
         backend = os.environ.get("BO_DIST_BACKEND", "nccl")   # gloo: 2 ranks on 1 GPU (test rigs)
         if backend == "nccl":
@@ -751,18 +753,22 @@ def run_ep(args, cfg, rank, world, local, pk):
         for _ in range(warmup):
             fwd(T, x, y)
         torch.cuda.synchronize()
-        graph = None
-        if nccl and ctx_for(T).padded:   # sync-free: K steps in one graph
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph):
-                for _ in range(steps):
-                    fwd(T, x, y)
         ev = None
         if ffn_events:   # the library records GEMM1 / GEMM2 boundaries of the rank-local grouped FFN
             ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
             for e3 in ev:
                 for e in e3:
                     e.record()
+            torch.cuda.synchronize()
+        graph = None
+        if nccl and ctx_for(T).padded:   # sync-free: K steps in one graph (the event records inside it)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                for i in range(steps):
+                    if ev:
+                        moe.set_profile_events(ev[i])
+                    fwd(T, x, y)
+            moe.set_profile_events(None)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         dist.barrier()
         torch.cuda.synchronize()
@@ -791,12 +797,24 @@ def run_ep(args, cfg, rank, world, local, pk):
     c = ctx_for(cfg.T)
     rows = c.local_rows()
     n_o = c.info["e1"] - c.info["e0"]
-    ffn_flops = 6.0 * cfg.d * (cfg.f * sum(rows[:n_o]) + c.info["f_united"] * sum(rows[n_o:]))
-    ach = ffn_flops / (ffn_ms / 1e3) / 1e12 if ffn_ms else None
-    roof = {"kernel": "gemm1_swiglu + gemm2_weighted (rank-local executors)", "bound": "tensor",
-            "achieved": ach, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
-            "frac": ach / pk["bf16_tflops"] if ach else None, "peak_note": "burst bf16; " + pk["source"],
-            "algorithmic_per_launch": ffn_flops, "traffic": None}
+    f_of = [cfg.f] * n_o + [c.info["f_united"]] * (len(rows) - n_o)
+    ffn_flops = 6.0 * cfg.d * sum(r * fx for r, fx in zip(rows, f_of))
+    # weights of the rank's accessed executors + its rows in (Xp) and out (Yp) + H written and read
+    ffn_bytes = sum(3.0 * cfg.d * fx * 2 for r, fx in zip(rows, f_of) if r > 0) + \
+        sum(r * (2 * cfg.d * 2 + 2 * fx * 2) for r, fx in zip(rows, f_of))
+    tensor_bound = ffn_flops / max(ffn_bytes, 1.0) > pk["bf16_tflops"] * 1e12 / (pk["hbm_gbs"] * 1e9)
+    if tensor_bound:
+        ach = ffn_flops / (ffn_ms / 1e3) / 1e12 if ffn_ms else None
+        roof = {"kernel": "gemm1_swiglu + gemm2_weighted (rank-local executors)", "bound": "tensor",
+                "achieved": ach, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": ach / pk["bf16_tflops"] if ach else None, "peak_note": "burst bf16; " + pk["source"],
+                "algorithmic_per_launch": ffn_flops, "traffic": None}
+    else:
+        ach = ffn_bytes / (ffn_ms / 1e3) / 1e9 if ffn_ms else None
+        roof = {"kernel": "gemm1_swiglu + gemm2_weighted (rank-local executors)", "bound": "hbm",
+                "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / pk["hbm_gbs"] if ach else None, "peak_note": pk["source"],
+                "algorithmic_per_launch": ffn_bytes, "traffic": None}
     out = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (seeded; random-init Mixtral-shaped weights)",
