@@ -95,6 +95,7 @@ int gemm_smem_bytes(int dtype, int epi, int bn);
 
 constexpr int kTileMin = 8;     // smallest token tile (workspace histograms are sized for it)
 constexpr int kTileSmall = 32;  // token tile of the injected-logits top-k
+constexpr int kPermRowsSmem = 1024;   // (token, slot) rows of a permute tile kept in shared memory for its gather
 
 cudaError_t launch_topk_hist(const float* logits, int T, int m, int K, int tile, int32_t* topk_id, float* topk_w,
                              int32_t* tile_cnt, cudaStream_t s);

@@ -853,6 +853,11 @@ __device__ __forceinline__ void permute_tile(const int32_t* __restrict__ topk_id
   // s*nrep + rep, the shared experts' rows (Eq. 5 second term) after them.
   const int KR = K * nrep + n_shared;
   __shared__ int wcnt[8][kMaxExperts];
+  // the tile's rows for the fused gather below (the gather's row reads then come from shared
+  // memory instead of an L2 round trip per (vector, slot) on row_of just written)
+  __shared__ int s_rows[kPermRowsSmem];
+  const bool rows_smem = xp != nullptr && tile * KR <= kPermRowsSmem;
+  const int t0_tile = tile_idx * tile;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < 8 * kMaxExperts; i += blockDim.x) (&wcnt[0][0])[i] = 0;
   __syncthreads();
@@ -900,13 +905,12 @@ __device__ __forceinline__ void permute_tile(const int32_t* __restrict__ topk_id
       const int64_t slot0 = t * KR + (a - t * K) * nrep;
       for (int rep = 0; rep < nrep; ++rep) {
         const int base_r = row_base[e * nrep + rep];
-        if (base_r >= 0) {
-          const int r = base_r + rank;
-          row_of[slot0 + rep] = r;
+        const int r = base_r >= 0 ? base_r + rank : -1;
+        row_of[slot0 + rep] = r;
+        if (rows_smem) s_rows[(t - t0_tile) * KR + (a - t * K) * nrep + rep] = r;
+        if (r >= 0) {
           if (row_tok) row_tok[r] = static_cast<int32_t>(t);
           row_w[r] = w;
-        } else {
-          row_of[slot0 + rep] = -1;
         }
       }
     }
@@ -920,6 +924,7 @@ __device__ __forceinline__ void permute_tile(const int32_t* __restrict__ topk_id
       const int64_t t = t0 + tt;
       const int r = shared_off[j] + static_cast<int>(t);
       row_of[t * KR + K * nrep + j] = r;
+      if (rows_smem) s_rows[tt * KR + K * nrep + j] = r;
       if (row_tok) row_tok[r] = static_cast<int32_t>(t);
       row_w[r] = 1.0f;
     }
@@ -951,7 +956,7 @@ __device__ __forceinline__ void permute_tile(const int32_t* __restrict__ topk_id
           const int c = i - tt * vec_per_row;
           const int64_t t = t0 + tt;
           for (int s = 0; s < KR; ++s) {
-            const int r = row_of[t * KR + s];
+            const int r = rows_smem ? s_rows[tt * KR + s] : row_of[t * KR + s];
             if (r >= 0) xp[static_cast<int64_t>(r) * vec_per_row + c] = v[u];
           }
         }
