@@ -87,7 +87,8 @@ typedef enum {
   BO_OPT_PDL = 13,           /* 1: GEMMs launch with programmatic dependent launch                   [1]    */
   BO_OPT_ROUTE_FUSED = 14,   /* 1: decode-sized m <= 32 steps run router + top-K + Alg. 1 + permute +
                                    gather as one cooperative launch                                   [1]    */
-  BO_OPT_COUNT = 15
+  BO_OPT_TAIL_SPLIT = 15,    /* 1: prefill GEMM2 on pairs shares a partial last wave out by k-blocks    [1]    */
+  BO_OPT_COUNT = 16
 } bo_engine_option;
 
 typedef struct {
@@ -143,6 +144,8 @@ typedef struct {
   size_t tile_xbase;      /* int32 [ntiles, E]  their exclusive prefix over tiles            */
   size_t ksplit;          /* int32 [1]          split count GEMM2 chose                 */
   size_t comb_cnt;        /* int32 [T, d/BN2]   arrival counters of the combine fused into GEMM2 (a8; BN2 = 256/128/64, GEMM2 tile width) */
+  size_t sk_part;         /* float [#SM, 256, 128] GEMM2 last-wave-split partials (T*K+N_s*T >= 2048 only)  */
+  size_t sk_flag;         /* int32 [#SM]        their arrival counts (zeroed before each GEMM2)           */
   int64_t T;              /* tokens the layout was computed for                          */
   int64_t ntiles;         /* histogram tiles the workspace is sized for (8 tokens each)  */
   int64_t num_executors;  /* E = m + G                                                   */

@@ -25,7 +25,7 @@ BO_UNITED_MEAN = 0
 # bo_engine_option (include/brownout.h): name -> id
 ENGINE_OPTIONS = {n: i for i, n in enumerate((
     "cta_pairs", "pair_rows1", "pair_rows2", "tile_alt", "swap_tail", "decode_pair2", "gemm2_splitk",
-    "fused_combine", "tma_store", "store_hint", "b_policy", "router_mma", "router_split", "pdl", "route_fused"))}
+    "fused_combine", "tma_store", "store_hint", "b_policy", "router_mma", "router_split", "pdl", "route_fused", "tail_split"))}
 
 EXPORTED = (
     "bo_create", "bo_destroy", "bo_workspace_size", "bo_workspace_layout", "bo_build_united", "bo_set_shared_experts",
@@ -58,7 +58,7 @@ class bo_ws_layout(C.Structure):
     _fields_ = [(n, C.c_size_t) for n in ("total_bytes", "logits", "topk_id", "topk_w", "tile_cnt", "tile_base",
                                           "counts", "exec_of_expert", "expert_row_off", "exec_off", "mtile_off",
                                           "stats", "row_of", "row_tok", "row_w", "xp", "h", "yp", "partial",
-                                          "tile_xcnt", "tile_xbase", "ksplit", "comb_cnt")] + \
+                                          "tile_xcnt", "tile_xbase", "ksplit", "comb_cnt", "sk_part", "sk_flag")] + \
                [("T", C.c_int64), ("ntiles", C.c_int64), ("num_executors", C.c_int64)]
 
 

@@ -143,6 +143,10 @@ bo_status compute_layout(const bo_handle* h, int64_t T, bo_ws_layout* L, bool ro
   L->tile_xbase = take(c.dedup_united && !route_only ? sizeof(int32_t) * ntiles * (m + G) : 0);
   L->ksplit = take(sizeof(int32_t));
   L->comb_cnt = take(route_only ? 0 : sizeof(int32_t) * T * (d / gemm2_bn(static_cast<int>(d))));
+  // GEMM2's last-wave split (CTA pairs, prefill-sized): one fp32 accumulator and one flag per SM
+  const bool ts = Rf >= kTailSplitRows;
+  L->sk_part = take(ts ? sizeof(float) * h->num_sms * bo::kSkPartElems : 0);
+  L->sk_flag = take(ts ? sizeof(int32_t) * h->num_sms : 0);
   L->total_bytes = off;
   L->T = T;
   L->ntiles = ntiles;
@@ -274,7 +278,8 @@ void set_comb(bo::GemmParams& p, const CombFuse* cf, int d, int nt2) {
 bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, const int32_t* exec_off,
                     const int32_t* mtile_off, const FfnClass& orig, const FfnClass& uni, const FfnClass& shr,
                     void* Hbuf, void* Y, cudaStream_t s, Prof& prof, int& launches, float* partial,
-                    int* ks_dev, const CombFuse* comb, const int32_t* comb_row_tok, bool force_pair2) {
+                    int* ks_dev, const CombFuse* comb, const int32_t* comb_row_tok, bool force_pair2,
+                    float* sk_part, int* sk_flag) {
   // partial != nullptr: GEMM2 runs split-K into fp32 partials [<=8, R, d] (the
   // caller combines them with launch_combine_partials); Y is then unused.
   const bo_config& c = h->cfg;
@@ -415,6 +420,12 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     }
     p.row_w = row_w;
     p.rows_total = static_cast<int>(R);
+    if (pair && o.tail_split && sk_part && sk_flag && !partial) {   // the kernel decides on the device
+      p.tail_split = 1;
+      p.sk_part = sk_part;
+      p.sk_flag = sk_flag;
+      BO_CUDA(cudaMemsetAsync(sk_flag, 0, sizeof(int) * h->num_sms, s), "tail-split flags");
+    }
     if (comb) {
       set_comb(p, comb, d, d / bn);
       p.row_tok = comb_row_tok;
@@ -461,6 +472,7 @@ const OptionSpec kOptions[BO_OPT_COUNT] = {
     {&EngineOptions::router_split, "BO_ROUTER_SPLIT", 0, 1},
     {&EngineOptions::pdl, "BO_PDL", 0, 1},
     {&EngineOptions::route_fused, "BO_ROUTE_FUSED", 0, 1},
+    {&EngineOptions::tail_split, "BO_TAIL_SPLIT", 0, 1},
 };
 
 void options_from_env(EngineOptions* o) {
@@ -618,7 +630,9 @@ bo_status forward_impl(bo_handle* h, const void* x, int64_t T, const void* Wr, c
   void* xp = at<char>(ws, L.xp);   // filled by the permute (small batches) or the gather kernel
   if ((st = ffn_stage(h, xp, Rt, row_w, at<int32_t>(ws, L.exec_off), at<int32_t>(ws, L.mtile_off), orig, uni, shr,
                       at<char>(ws, L.h), yp, s, prof, launches, split ? at<float>(ws, L.partial) : nullptr,
-                      split ? at<int>(ws, L.ksplit) : nullptr, cfp, row_tok, decode_pair2)) != BO_OK)
+                      split ? at<int>(ws, L.ksplit) : nullptr, cfp, row_tok, decode_pair2,
+                      Rt >= kTailSplitRows ? at<float>(ws, L.sk_part) : nullptr,
+                      Rt >= kTailSplitRows ? at<int>(ws, L.sk_flag) : nullptr)) != BO_OK)
     return st;
   // a8: combine (Eq. 5 sum over the token's K slots; split-K partials summed first)
   if (!fuse_comb) {

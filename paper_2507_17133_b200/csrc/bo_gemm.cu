@@ -508,6 +508,53 @@ __global__ void __launch_bounds__(192, 1)
     if (p.ksplit_max > 1 && blockIdx.x == 0 && threadIdx.x == 0) *p.ks_out = ks;
   }
   const int total_work = base_work * ks;
+  // Last-wave split (GEMM2 on CTA pairs, GemmParams::tail_split): the X = tiles mod units
+  // tiles of a partial last wave are not handed out whole; their X * nkb k-blocks are shared
+  // out evenly over ALL units after each unit's whole tiles (units u take [U u / n, U (u+1) / n)).
+  // A share (>= 8 k-blocks, < nkb) covers at most two tiles, so a unit holds at most one
+  // contributor piece (a tile's later k-blocks: fp32 partial to sk_part[blockIdx], counted in
+  // sk_flag[blockIdx]) and one finishing piece (from k-block 0: it adds the partials of the
+  // following units holding the tile's other pieces, in unit order, then runs the epilogue).
+  // Only for long reductions (>= 64 k-blocks per tile, e.g. C2's 224), where a piece's
+  // 128 KB partial is small against its work.
+  int tsx = 0;          // tiles of the split last wave
+  int nkb_t = 0;
+  int64_t tsU = 0;      // their k-blocks
+  if constexpr (EPI == EPI_WEIGHTED && CG == 2) {
+    if (p.tail_split && p.sk_part && ks == 1 && p.Kdim == p.Kdim_u && !p.f32_mode) {
+      nkb_t = p.Kdim / C::BK;
+      const int X = base_work % n_units;
+      if (nkb_t >= 64 && X > 0 && static_cast<int64_t>(X) * nkb_t >= 8LL * n_units) {
+        tsx = X;
+        tsU = static_cast<int64_t>(X) * nkb_t;
+      }
+    }
+  }
+  const int n_whole = base_work - tsx;   // tiles handed out whole, round robin
+  const int n_my_whole = n_whole > unit ? (n_whole - unit + n_units - 1) / n_units : 0;
+  auto ts_lo = [&](int u) { return tsU * u / n_units; };   // first split k-block of unit u
+  enum { SEG_FULL = 0, SEG_FINISH = 1, SEG_CONTRIB = 2 };
+  // s-th segment of this unit: work item w, k-block override [s0, s1) (tail pieces) and kind
+  auto segment = [&](int s, int& w, int& s0, int& s1, int& kind) -> bool {
+    kind = SEG_FULL;
+    if (!tsx) {
+      w = unit + s * n_units;
+      return w < total_work;
+    }
+    if (s < n_my_whole) {
+      w = unit + s * n_units;
+      return true;
+    }
+    const int64_t lo = ts_lo(unit), hi = ts_lo(unit + 1);
+    const int64_t i = lo / nkb_t + (s - n_my_whole);
+    if (i * nkb_t >= hi) return false;
+    w = n_whole + static_cast<int>(i);
+    const int64_t a = lo - i * nkb_t, b = hi - i * nkb_t;
+    s0 = a > 0 ? static_cast<int>(a) : 0;
+    s1 = b < nkb_t ? static_cast<int>(b) : nkb_t;
+    kind = s0 > 0 ? SEG_CONTRIB : (s1 < nkb_t ? SEG_FINISH : SEG_FULL);
+    return true;
+  };
 
   // work item -> tile (executor x, m-tile mi fastest, n-tile n) + k-block range
   // [kb0, kb1) of split sp; units take items unit, unit + n_units, ... (the
@@ -534,9 +581,10 @@ __global__ void __launch_bounds__(192, 1)
   // executors sat on the MMA warp's critical path between tiles (0.5-0.9 us per tile with
   // 5-57 executors, probe build), ~10 % of a 12-k-block C4 GEMM2 tile.  Packed as
   // x | mi << 10 | n << 20 | sp << 29; -1 = decode when reached (a field does not fit).
+  // (with the last-wave split only the whole tiles are listed; the pieces decode when reached)
+  const int n_my = tsx ? n_my_whole : (total_work > unit ? (total_work - unit + n_units - 1) / n_units : 0);
+  const int n_tab = n_my < kSchedItems ? n_my : kSchedItems;
   {
-    const int n_my = total_work > unit ? (total_work - unit + n_units - 1) / n_units : 0;
-    const int n_tab = n_my < kSchedItems ? n_my : kSchedItems;
     for (int j = threadIdx.x; j < n_tab; j += blockDim.x) {
       int x, mi, n, sp, a, b;
       decode(unit + j * n_units, x, mi, n, sp, a, b);
@@ -545,7 +593,7 @@ __global__ void __launch_bounds__(192, 1)
     __syncthreads();
   }
   auto item_at = [&](int j, int w, int& x, int& mi, int& n, int& sp, int& kb0, int& kb1) {
-    const int e = j < kSchedItems ? s_sched[j] : -1;
+    const int e = j < n_tab ? s_sched[j] : -1;
     if (e < 0) {
       decode(w, x, mi, n, sp, kb0, kb1);
       return;
@@ -576,9 +624,10 @@ __global__ void __launch_bounds__(192, 1)
       int stage = 0;
       uint32_t phase = 0;
       int x, mi, n, sp, kb0, kb1;
-      int item = 0;
-      for (int w = unit; w < total_work; w += n_units, ++item) {
+      int w, s0 = 0, s1 = 0, kind;
+      for (int item = 0; segment(item, w, s0, s1, kind); ++item) {
         item_at(item, w, x, mi, n, sp, kb0, kb1);
+        if (item >= n_my_whole && tsx) { kb0 = s0; kb1 = s1; }
         BO_STAMP(item, 0);
 #ifdef BO_PROBE
         if (blockIdx.x < kProbeCtas && item < kProbeItems)
@@ -651,9 +700,11 @@ __global__ void __launch_bounds__(192, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       int x, mi, n, sp, kb0, kb1;
+      int w, s0 = 0, s1 = 0, kind;
       int item = 0;
-      for (int w = unit; w < total_work; w += n_units, ++item) {
+      for (; segment(item, w, s0, s1, kind); ++item) {
         item_at(item, w, x, mi, n, sp, kb0, kb1);
+        if (item >= n_my_whole && tsx) { kb0 = s0; kb1 = s1; }
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         BO_STAMP(item, 4);
@@ -687,7 +738,7 @@ __global__ void __launch_bounds__(192, 1)
       }
       if constexpr (CG == 2) {
         // drain: the peer's last remote arrivals must land before the CTAs exit
-        const int iters = total_work > unit ? (total_work - unit + n_units - 1) / n_units : 0;
+        const int iters = item;   // segments this unit ran
         if (iters > 0) {
           const int last = iters - 1;
           mbar_wait(&tempty_bar[last & 1], (last >> 1) & 1);
@@ -722,11 +773,12 @@ __global__ void __launch_bounds__(192, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     int x, mi, n, sp, kb0, kb1;
-    int item = -1;
-    for (int w = unit; w < total_work; w += n_units) {
-      if (item >= 0 && warp == 2 && lane == 0) BO_STAMP(item, 3);   // the previous tile's epilogue is done
-      ++item;
+    int w, s0 = 0, s1 = 0, kind;
+    int item = 0;
+    for (; segment(item, w, s0, s1, kind); ++item) {
+      if (item > 0 && warp == 2 && lane == 0) BO_STAMP(item - 1, 3);   // the previous tile's epilogue is done
       item_at(item, w, x, mi, n, sp, kb0, kb1);
+      if (item >= n_my_whole && tsx) { kb0 = s0; kb1 = s1; }
       const int rows_x = s_eoff[x + 1] - s_eoff[x];
       const int r_local = mi * TILE_M + static_cast<int>(crank) * kBM + q * 32 + lane;
       const bool valid = r_local < rows_x;
@@ -812,6 +864,57 @@ __global__ void __launch_bounds__(192, 1)
           __syncwarp();
         }
       } else if constexpr (EPI == EPI_WEIGHTED) {
+        // last-wave split (tail_split): a contributor piece hands its fp32 accumulator to the
+        // tile's finishing unit; a finishing piece waits for and adds the later pieces' partials
+        int c_first = 0, c_last = -1;
+        if constexpr (CG == 2) {
+          const int lrow = q * 32 + lane;   // TMEM lane of this thread
+          if (kind == SEG_CONTRIB) {
+            float* part = p.sk_part + static_cast<int64_t>(blockIdx.x) * kSkPartElems;
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 32) {
+              uint32_t v[32];
+              tmem_ld32(t0 + c, v);
+              tmem_ld_wait();
+#pragma unroll
+              for (int j = 0; j < 32; ++j) __stcg(part + (c + j) * 128 + lrow, __uint_as_float(v[j]));
+            }
+            tc_fence_before();
+            __threadfence();   // release: the partial precedes the count
+            __syncwarp();
+            if (lane == 0) {
+              atomicAdd(p.sk_flag + blockIdx.x, 1);
+              if (leader) mbar_arrive(&tempty_bar[acc]);
+              else mbar_arrive_remote(&tempty_bar[acc], 0);
+            }
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            continue;
+          }
+          if (kind == SEG_FINISH) {
+            const int64_t tile_end = static_cast<int64_t>(w - n_whole + 1) * nkb_t;
+            c_first = unit + 1;
+            c_last = unit;
+            while (c_last + 1 < n_units && ts_lo(c_last + 1) < tile_end) ++c_last;
+            if (lane == 0)
+              for (int cu = c_first; cu <= c_last; ++cu) {
+                const int* flag = p.sk_flag + cu * 2 + static_cast<int>(crank);
+                int v;
+                do {
+                  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+                } while (v < 4);
+              }
+            __syncwarp();
+          }
+        }
+        // acc[j] += the later pieces' partials of accumulator column col + j, in unit order
+        auto add_parts = [&](uint32_t (&a)[32], int col) {
+          for (int cu = c_first; cu <= c_last; ++cu) {
+            const float* part = p.sk_part + static_cast<int64_t>(cu * 2 + static_cast<int>(crank)) * kSkPartElems +
+                                q * 32 + lane;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) a[j] = __float_as_uint(__uint_as_float(a[j]) + __ldcg(part + (col + j) * 128));
+          }
+        };
         const float wr = valid ? (p.row_w ? p.row_w[grow] : p.alpha) : 0.0f;
         if (p.ksplit_max > 1 || p.f32_mode) {   // split-K: fp32 partial of split sp, row-scaled (Eq. 6)
           float* outp = p.partial + (static_cast<int64_t>(sp) * p.rows_total + grow) * p.ldo + n * BN;
@@ -853,6 +956,7 @@ __global__ void __launch_bounds__(192, 1)
           uint32_t a[32];
           tmem_ld32(t0 + c, a);
           tmem_ld_wait();
+          add_parts(a, c);
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(a[i]) * wr;
@@ -1036,7 +1140,8 @@ __global__ void __launch_bounds__(192, 1)
 
 #ifdef BO_PROBE
   if (warp == 2 && lane == 0) {
-    const int last = total_work > unit ? (total_work - unit + n_units - 1) / n_units - 1 : -1;
+    int last = -1, w_, a_, b_, k_;
+    while (segment(last + 1, w_, a_, b_, k_)) ++last;
     if (last >= 0) BO_STAMP(last, 3);
   }
 #endif

@@ -30,6 +30,7 @@ struct EngineOptions {
   int32_t router_split = 1;    // decode-sized m <= 32 batches: split-warp router
   int32_t pdl = 1;             // programmatic dependent launch of the GEMMs
   int32_t route_fused = 1;     // decode-sized m <= 32: routing, Alg. 1, permute + gather in one launch
+  int32_t tail_split = 1;      // GEMM2 on pairs: a partial last wave shared out by k-blocks over every pair
 };
 
 struct bo_handle {
@@ -54,6 +55,7 @@ namespace bo_impl {
 
 constexpr int64_t kSplitRows = 1024;   // GEMM2 split-K (decode) only for R <= this
 constexpr int kSplitMax = 8;
+constexpr int64_t kTailSplitRows = 2048;   // workspace carries GEMM2's last-wave-split partials from here
 
 bo_status fail(bo_status s, const char* fmt, ...);
 bo_status cuda_fail(cudaError_t e, const char* what);
@@ -134,6 +136,6 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
                     const int32_t* mtile_off, const FfnClass& orig, const FfnClass& uni, const FfnClass& shr,
                     void* Hbuf, void* Y, cudaStream_t s, Prof& prof, int& launches, float* partial = nullptr,
                     int* ks_dev = nullptr, const CombFuse* comb = nullptr, const int32_t* comb_row_tok = nullptr,
-                    bool force_pair2 = false);
+                    bool force_pair2 = false, float* sk_part = nullptr, int* sk_flag = nullptr);
 
 }  // namespace bo_impl

@@ -70,7 +70,14 @@ struct GemmParams {
   // Maps [6..11] then hold 64-row gate / up boxes and [12..14] 16 / 32 / 64-row boxes of A (Xp).
   int swap_tail;
   int tma_store;            // EPI_WEIGHTED: full 32-row slabs leave through TMA bulk stores (map B[6], 32 x 32 box, 64B swizzle)
+  // EPI_WEIGHTED on CTA pairs: a partial last wave's tiles shared out by k-blocks over every
+  // pair (see the kernel); sk_part [units * 2][kSkPartElems] fp32 partials, sk_flag [units * 2]
+  // arrival counts (4 epilogue warps), zeroed before every launch.
+  int tail_split;
+  float* sk_part;
+  int* sk_flag;
 };
+constexpr int kSkPartElems = 256 * 128;   // one CTA's fp32 accumulator: 256 columns x 128 rows
 
 // Combine of split-K fp32 partials: y[t] = [x_t] + sum_slots sum_splits P[sp][row].
 cudaError_t launch_combine_partials(int dtype, const float* partial, const int* ks, int64_t R, const void* x, int T,
