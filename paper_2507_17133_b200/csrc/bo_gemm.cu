@@ -358,6 +358,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* tfull_bar = empty_bar + STAGES;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint64_t* fix_bar = tempty_bar + 3;   // last-wave split: a contributor's partial landed in the (idle) ring
   int* s_mtile = reinterpret_cast<int*>(smem + STAGES * C::STAGE_BYTES + C::BAR_BYTES);
   int* s_eoff = s_mtile + (kMaxExec + 1);
   int* s_sched = s_eoff + (kMaxExec + 1);   // [kSchedItems] this unit's decoded work list
@@ -381,6 +382,7 @@ __global__ void __launch_bounds__(192, 1)
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], 4 * CG);   // pair: epilogue warps of both CTAs arrive on the leader's
     }
+    mbar_init(fix_bar, 1);
     fence_barrier_init();
   }
   if (warp == 0 && lane == 0) {
@@ -866,7 +868,6 @@ __global__ void __launch_bounds__(192, 1)
       } else if constexpr (EPI == EPI_WEIGHTED) {
         // last-wave split (tail_split): a contributor piece hands its fp32 accumulator to the
         // tile's finishing unit; a finishing piece waits for and adds the later pieces' partials
-        int c_first = 0, c_last = -1;
         if constexpr (CG == 2) {
           const int lrow = q * 32 + lane;   // TMEM lane of this thread
           if (kind == SEG_CONTRIB) {
@@ -891,30 +892,46 @@ __global__ void __launch_bounds__(192, 1)
             continue;
           }
           if (kind == SEG_FINISH) {
+            // Add the later pieces' partials into the accumulator, in unit order: each is
+            // brought into the stage ring (idle: this is the unit's last piece and its MMAs
+            // have completed) by one bulk copy, then every warp adds its lanes' columns and
+            // writes them back to TMEM.
             const int64_t tile_end = static_cast<int64_t>(w - n_whole + 1) * nkb_t;
-            c_first = unit + 1;
-            c_last = unit;
+            const int c_first = unit + 1;
+            int c_last = unit;
             while (c_last + 1 < n_units && ts_lo(c_last + 1) < tile_end) ++c_last;
-            if (lane == 0)
-              for (int cu = c_first; cu <= c_last; ++cu) {
+            const float* ring = reinterpret_cast<const float*>(smem);
+            for (int cu = c_first; cu <= c_last; ++cu) {
+              epi_bar();   // every warp has read the previous partial (and the ring is idle)
+              if (warp == 2 && lane == 0) {
                 const int* flag = p.sk_flag + cu * 2 + static_cast<int>(crank);
                 int v;
                 do {
                   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
                 } while (v < 4);
+                fence_proxy_async_global();   // the partial's generic writes before the async-proxy read
+                fence_proxy_async_smem();     // our generic reads of the ring before its async overwrite
+                mbar_arrive_expect_tx(fix_bar, kSkPartElems * 4);
+                bulk_g2s(smem, p.sk_part + static_cast<int64_t>(cu * 2 + static_cast<int>(crank)) * kSkPartElems,
+                         kSkPartElems * 4, fix_bar);
               }
-            __syncwarp();
+              mbar_wait(fix_bar, static_cast<uint32_t>((cu - c_first) & 1));
+#pragma unroll 1
+              for (int c = 0; c < BN; c += 32) {
+                uint32_t a[32];
+                tmem_ld32(t0 + c, a);
+                tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  a[j] = __float_as_uint(__uint_as_float(a[j]) + ring[(c + j) * 128 + lrow]);
+                tmem_st32(t0 + c, a);
+              }
+              tmem_st_wait();
+            }
+            tc_fence_before();
+            tc_fence_after();
           }
         }
-        // acc[j] += the later pieces' partials of accumulator column col + j, in unit order
-        auto add_parts = [&](uint32_t (&a)[32], int col) {
-          for (int cu = c_first; cu <= c_last; ++cu) {
-            const float* part = p.sk_part + static_cast<int64_t>(cu * 2 + static_cast<int>(crank)) * kSkPartElems +
-                                q * 32 + lane;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) a[j] = __float_as_uint(__uint_as_float(a[j]) + __ldcg(part + (col + j) * 128));
-          }
-        };
         const float wr = valid ? (p.row_w ? p.row_w[grow] : p.alpha) : 0.0f;
         if (p.ksplit_max > 1 || p.f32_mode) {   // split-K: fp32 partial of split sp, row-scaled (Eq. 6)
           float* outp = p.partial + (static_cast<int64_t>(sp) * p.rows_total + grow) * p.ldo + n * BN;
@@ -956,7 +973,6 @@ __global__ void __launch_bounds__(192, 1)
           uint32_t a[32];
           tmem_ld32(t0 + c, a);
           tmem_ld_wait();
-          add_parts(a, c);
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(a[i]) * wr;
