@@ -53,6 +53,9 @@ def main():
                          config_id=73)
     shared = S.LayerConfig("sh", d=256, f=256, m=8, K=2, way=4, T=150, ratio=0.5, dtype="bf16", sigma=0.5,
                            config_id=74, Ns=2)
+    # GEMM2's last-wave split: 48 pair tiles of 64 k-blocks shared out over the pairs
+    tail = S.LayerConfig("ts", d=512, f=4096, m=8, K=2, way=4, T=3000, ratio=0.0, dtype="bf16", sigma=0.3,
+                         config_id=101)
     bad = 0
     for name, f in [
         ("decode", lambda: run(small)),
@@ -61,6 +64,7 @@ def main():
         ("router_gpu_unfused", lambda: run_env({"BO_ROUTE_FUSED": "0"}, small, logits=False)),
         ("router_gpu_fused_shared", lambda: run(shared, logits=False)),
         ("prefill_pairs_fused_combine", lambda: run(pair)),   # GEMM1 swapped tail tiles (default)
+        ("prefill_gemm2_tail_split", lambda: run(tail)),
         ("decode_gemm2_splitk", lambda: run_env({"BO_GEMM2_SPLITK": "1"}, small)),
         ("fp32", lambda: run(fp32)),
         ("qwen_like_tc_router", lambda: run(qwen, logits=False)),
