@@ -844,6 +844,9 @@ __global__ void __launch_bounds__(192, 1)
               __syncwarp();
             }
           }
+          // the gate warp has read the last half before the up warp reuses its staging tile
+          // (the next tile's stage_row32); racecheck flagged the write-after-read without it
+          pair_bar(bid);
         }
       }
       if constexpr (EPI == EPI_SWIGLU) {
