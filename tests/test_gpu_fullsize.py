@@ -7,7 +7,7 @@ can compute one token at a time:
   * routing / Alg. 1 plan / permutation: bit-exact for ALL tokens, given the
     same injected fp32 logits (seeded generator, not the CUDA path);
   * outputs: 512 seeded sampled tokens (C3's 256: all) within 2e-2 of the fp64
-    oracle, at every ratio of the sweep (C2: 0 / 0.25 / 0.5 / 1, C3: 0 / 0.5 / 1);
+    oracle, at every ratio of the sweep (C2: 0 / 0.25 / 0.5 / 1, C3: 0 / 0.5 / 1; C4: 0 / 0.5 / 1);
   * router GEMM (Eq. 8) on the sampled tokens within 1e-3 (1 + |s|) of fp64;
   * the production router end to end (no injected logits) on exactly
     representable inputs (synthetic.make_exact_router_inputs): logits of ALL
@@ -38,7 +38,7 @@ def _f32np(t):
 
 FULL_CASES = ([("mixtral_prefill", r) for r in (0.0, 0.25, 0.5, 1.0)] +
               [("mixtral_decode", r) for r in (0.0, 0.5, 1.0)] +
-              [("qwen3_30b_a3b_prefill", 0.5), ("qwen15_moe_a27b_prefill", 0.8)])
+              [("qwen3_30b_a3b_prefill", r) for r in (0.0, 0.5, 1.0)] + [("qwen15_moe_a27b_prefill", 0.8)])
 
 
 @pytest.mark.parametrize("name,ratio", FULL_CASES)
