@@ -414,11 +414,6 @@ bo_status ffn_stage(bo_handle* h, const void* X, int64_t R, const float* row_w, 
     p.exec_off = exec_off;
     p.mtile_off = mtile_off;
     p.out = Y;
-    if (pair && partial && o.swap_tail) {   // split-K GEMM2 on pairs: swapped tail tiles (H in 16/32/64-row boxes)
-      for (int i = 0; i < 3; ++i)
-        if ((st = make_map(&mb.m[12 + i], Hbuf, c.dtype, R, f, 16u << i)) != BO_OK) return st;
-      p.swap_tail2 = 1;
-    }
     if (o.tma_store && dt == 0 && !partial) {
       if ((st = make_map_store32(&mb.m[6], Y, static_cast<uint64_t>(R), static_cast<uint64_t>(d))) != BO_OK) return st;
       p.tma_store = 1;

@@ -481,11 +481,8 @@ __global__ void __launch_bounds__(192, 1)
   // them).  The MMA and the shared-memory traffic then scale with rin instead of a
   // full 256-row tile.  Three TMA boxes per k-block (gate, up, rows): the TMA issue
   // cost of 16-row boxes (8-12 per k-block) made such a tile slower than a full one.
-  // GEMM2 (EPI_WEIGHTED) likewise with split-K partials (decode-sized steps,
-  // GemmParams::swap_tail2): this CTA's 128 Wd rows (output columns) on M, the tile's H rows
-  // on N; the epilogue writes the split's fp32 partial transposed back to row-major.
-  constexpr bool kSwap = CG == 2 && (EPI == EPI_SWIGLU || EPI == EPI_WEIGHTED);
-  bool swap_ok = kSwap && EPI == EPI_SWIGLU && p.swap_tail && !alt && !p.a_shared;   // GEMM2: set after ks
+  constexpr bool kSwap = CG == 2 && EPI == EPI_SWIGLU;
+  const bool swap_ok = kSwap && p.swap_tail && !alt && !p.a_shared;
   auto tile_rows = [&](int x, int mi) {   // rows of executor x in m-tile mi
     const int r = s_eoff[x + 1] - s_eoff[x] - mi * TILE_M;
     return r < TILE_M ? r : TILE_M;
@@ -511,7 +508,6 @@ __global__ void __launch_bounds__(192, 1)
       }
     }
     if (p.ksplit_max > 1 && blockIdx.x == 0 && threadIdx.x == 0) *p.ks_out = ks;
-    if constexpr (CG == 2) swap_ok = p.swap_tail2 && ks > 1 && !p.a_shared && !p.f32_mode;
   }
   const int total_work = base_work * ks;
   // Last-wave split (GEMM2 on CTA pairs, GemmParams::tail_split): the X = tiles mod units
@@ -649,10 +645,7 @@ __global__ void __launch_bounds__(192, 1)
           if (swapped_tile(x, mi)) {
             const int rin = tile_rows(x, mi);
             const int nsh = ((rin + 31) & ~31) / 2;   // token rows staged by this CTA (N / 2)
-            // SwiGLU: 64 gate + 64 up rows of this CTA's 64 output columns; GEMM2: this CTA's
-            // 128 Wd rows (the pair's usual B half box)
-            const int wrow = EPI == EPI_SWIGLU ? brow + n * 128 + static_cast<int>(crank) * 64
-                                               : brow + n * BN + static_cast<int>(crank) * 128;
+            const int wrow = brow + n * 128 + static_cast<int>(crank) * 64;
             const int trow = s_eoff[x] + mi * TILE_M + static_cast<int>(crank) * nsh;
             // one box of >= nsh rows (16 / 32 / 64 / 128; rows past nsh land unused)
             const int tbox = nsh <= 16 ? 16 : (nsh <= 32 ? 32 : (nsh <= 64 ? 64 : 128));
@@ -662,12 +655,8 @@ __global__ void __launch_bounds__(192, 1)
               uint8_t* sa = smem + stage * C::STAGE_BYTES;
               if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * (C::A_BYTES + tbox * 128));
               else mbar_arrive_remote(&full_bar[stage], 0);
-              if constexpr (EPI == EPI_SWIGLU) {
-                tma_load_2d_pair(sa, &tmB.m[6 + 2 * cls], &full_bar[stage], kb * C::BK, wrow, pol_b);
-                tma_load_2d_pair(sa + 64 * 128, &tmB.m[7 + 2 * cls], &full_bar[stage], kb * C::BK, wrow, pol_b);
-              } else {
-                tma_load_2d_pair(sa, mb0, &full_bar[stage], kb * C::BK, wrow, pol_b);
-              }
+              tma_load_2d_pair(sa, &tmB.m[6 + 2 * cls], &full_bar[stage], kb * C::BK, wrow, pol_b);
+              tma_load_2d_pair(sa + 64 * 128, &tmB.m[7 + 2 * cls], &full_bar[stage], kb * C::BK, wrow, pol_b);
               tma_load_2d_pair(sa + C::A_BYTES, mt, &full_bar[stage], kb * C::BK, trow, pol_a);
               if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
@@ -804,7 +793,7 @@ __global__ void __launch_bounds__(192, 1)
       const int nrows = rows_x - slab < 0 ? 0 : (rows_x - slab > 32 ? 32 : rows_x - slab);
       const int64_t row0 = static_cast<int64_t>(s_eoff[x]) + slab;
       bool swapped = false;
-      if constexpr (kSwap && EPI == EPI_SWIGLU) {
+      if constexpr (kSwap) {
         if (swapped_tile(x, mi)) {
           // D^T tile: lane = weight row, TMEM column = the tile's row.  Warp q < 2 holds
           // the gate rows of columns colb..colb+31, warp q + 2 their up rows: the up warp
@@ -947,38 +936,6 @@ __global__ void __launch_bounds__(192, 1)
           }
         }
         const float wr = valid ? (p.row_w ? p.row_w[grow] : p.alpha) : 0.0f;
-        if constexpr (CG == 2) {
-          if (swapped_tile(x, mi)) {
-            // swapped tail tile (split-K): lane = output column, TMEM column = the tile's row;
-            // the split's fp32 partial, row-scaled (Eq. 6), stored back row-major (for each
-            // row the warp's 32 lanes write 32 consecutive columns)
-            const int rin = tile_rows(x, mi);
-            const int ns = (rin + 31) & ~31;
-            const int64_t tok0 = static_cast<int64_t>(s_eoff[x]) + mi * TILE_M;
-            float* outp = p.partial + (static_cast<int64_t>(sp) * p.rows_total + tok0) * p.ldo + n * BN +
-                          static_cast<int>(crank) * 128 + q * 32 + lane;
-#pragma unroll 1
-            for (int c = 0; c < ns; c += 32) {
-              uint32_t v[32];
-              tmem_ld32(t0 + c, v);
-              tmem_ld_wait();
-              const float wl = c + lane < rin ? (p.row_w ? p.row_w[tok0 + c + lane] : p.alpha) : 0.0f;
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                const float wj = __shfl_sync(0xffffffffu, wl, j);
-                if (c + j < rin) outp[static_cast<int64_t>(c + j) * p.ldo] = kb1 > kb0 ? __uint_as_float(v[j]) * wj : 0.0f;
-              }
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-              if (leader) mbar_arrive(&tempty_bar[acc]);
-              else mbar_arrive_remote(&tempty_bar[acc], 0);
-            }
-            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
-            continue;
-          }
-        }
         if (p.ksplit_max > 1 || p.f32_mode) {   // split-K: fp32 partial of split sp, row-scaled (Eq. 6)
           float* outp = p.partial + (static_cast<int64_t>(sp) * p.rows_total + grow) * p.ldo + n * BN;
           const float scale = kb1 > kb0 ? wr : 0.0f;   // an empty k-range contributes 0 (stale TMEM)

@@ -69,7 +69,6 @@ struct GemmParams {
   // M side and its rows (rounded up to 32) on N, so a ragged tile costs its rows, not 256.
   // Maps [6..11] then hold 64-row gate / up boxes and [12..14] 16 / 32 / 64-row boxes of A (Xp).
   int swap_tail;
-  int swap_tail2;           // EPI_WEIGHTED on pairs with split-K: ragged last m-tiles swapped too (maps [12..14] = H boxes)
   int tma_store;            // EPI_WEIGHTED: full 32-row slabs leave through TMA bulk stores (map B[6], 32 x 32 box, 64B swizzle)
   // EPI_WEIGHTED on CTA pairs: a partial last wave's tiles shared out by k-blocks over every
   // pair (see the kernel); sk_part [units * 2][kSkPartElems] fp32 partials, sk_flag [units * 2]
