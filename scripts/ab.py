@@ -44,12 +44,14 @@ def main():
             torch.cuda.empty_cache()
             cache[wname] = bench.Layer(cfg, "cuda")
         layer = cache[wname]
-        moes, weights = {}, {}
+        moes, weights, wss = {}, {}, {}
         base_w = (layer.lay, layer.united)
+        base_ws = layer.ws
         for arm, env in arms.items():
             if arm == "A":
                 moes[arm] = layer.moe
                 weights[arm] = base_w
+                wss[arm] = base_ws
                 continue
             env = dict(env)
             old = {k: os.environ.get(k) for k in env}
@@ -67,6 +69,7 @@ def main():
                 else:
                     os.environ[k] = v
             moes[arm] = moe
+            wss[arm] = moe.workspace(layer.T, "cuda")   # an arm's options may change the layout
         moe_a = layer.moe
         res = {arm: {"ms": [], "k": []} for arm in arms}
         names = list(arms)
@@ -75,12 +78,14 @@ def main():
             for arm in order:
                 layer.moe = moes[arm]
                 layer.lay, layer.united = weights[arm]
+                layer.ws = wss[arm]
                 layer.moe.set_brownout(float(ratio))
                 ms, kern = bench.time_steps(layer, args.steps, 3, False)
                 res[arm]["ms"].append(ms / args.steps)
                 res[arm]["k"].append(kern)
         layer.moe = moe_a
         layer.lay, layer.united = base_w
+        layer.ws = base_ws
         summ = {}
         for arm in names:
             ks = {}
