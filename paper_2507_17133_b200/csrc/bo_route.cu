@@ -1135,6 +1135,25 @@ __device__ __forceinline__ void plan_small_warp(int cnt, int m, int way, double 
   }
 }
 
+#ifdef BO_PROBE
+// Instrumentation build only: globaltimer stamps of each CTA's phases in the last
+// k_route_fused launch [entry, router tile done, grid barrier passed, histograms staged,
+// plan done, permute done].
+__device__ unsigned long long g_rf_probe[1024][6];
+#define BO_RF_STAMP(k)                                                                \
+  do {                                                                                \
+    if (threadIdx.x == 0 && blockIdx.x < 1024) {                                      \
+      unsigned long long t_;                                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
+      g_rf_probe[blockIdx.x][k] = t_;                                                 \
+    }                                                                                 \
+  } while (0)
+#else
+#define BO_RF_STAMP(k) \
+  do {                 \
+  } while (0)
+#endif
+
 template <typename T, int MAXM>
 __global__ void __launch_bounds__(256)
     k_route_fused(const T* __restrict__ x, const T* __restrict__ Wr, int Tn, int d, int m, int K, int tpc,
@@ -1149,8 +1168,11 @@ __global__ void __launch_bounds__(256)
   __shared__ int32_t s_row_off[MAXM];
   __shared__ int32_t s_xoff[kRouteFusedMaxExec + 1];
   __shared__ int32_t s_tb[MAXM];
+  BO_RF_STAMP(0);
   router_split_tile<T, MAXM>(x, Wr, Tn, d, m, K, tpc, logits, topk_id, topk_w, tile_cnt, blockIdx.x);
+  BO_RF_STAMP(1);
   cg::this_grid().sync();   // every tile histogram written (and visible)
+  BO_RF_STAMP(2);
   // Alg. 1 input cnt_e = sum over tiles; this tile's exclusive prefix = sum over the tiles before
   // it.  All ntiles * m counts are staged with one round of L2-coherent 16-byte loads (written
   // in this kernel: no .nc path), then warp w sums tiles w, w + 8, ... per expert (lane).
@@ -1161,6 +1183,7 @@ __global__ void __launch_bounds__(256)
     reinterpret_cast<int4*>(s_tc)[i] = __ldcg(reinterpret_cast<const int4*>(tile_cnt) + i);
   for (int i = (n_tc & ~3) + threadIdx.x; i < n_tc; i += blockDim.x) s_tc[i] = __ldcg(tile_cnt + i);
   __syncthreads();
+  BO_RF_STAMP(3);
   if (lane < m) {
     int all = 0, bef = 0;
     for (int t = warp; t < ntiles; t += 8) {
@@ -1184,10 +1207,19 @@ __global__ void __launch_bounds__(256)
                     expert_row_off, exec_off, mtile_off, stats);
   }
   __syncthreads();
+  BO_RF_STAMP(4);
   const int E = m + (m + way - 1) / way;
   permute_tile(topk_id, topk_w, Tn, K, m, tpc, me, s_tb, s_row_off, 1, row_of, row_tok, row_w,
                reinterpret_cast<const uint4*>(x), xp, vec_per_row, n_shared, s_xoff + E);
+  __syncthreads();
+  BO_RF_STAMP(5);
 }
+
+#ifdef BO_PROBE
+extern "C" __attribute__((visibility("default"))) int bo_probe_rf_copy(void* stamps) {
+  return cudaMemcpyFromSymbol(stamps, g_rf_probe, sizeof(g_rf_probe)) != cudaSuccess;
+}
+#endif
 
 // Co-resident CTAs of the cooperative grid (resident CTAs per SM x #SM), queried once per
 // device and kept (the forward is on the host's per-call path).
