@@ -5,6 +5,7 @@
 
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <string>
@@ -75,14 +76,25 @@ P* at(void* ws, size_t off) {
   return reinterpret_cast<P*>(static_cast<char*>(ws) + off);
 }
 
-// Per-kernel profiling events (bo_set_profile_events); graph-capture aware.
+// Per-kernel profiling events (bo_set_profile_events); graph-capture aware.  Also NVTX
+// ranges (header-only NVTX3; no-ops unless a tool such as Nsight Systems is attached):
+// one "bo" range per entry-point call, one nested range per kernel launch named as in
+// bo_last_kernels.
 struct Prof {
   bo_handle* h;
   cudaStream_t s;
   bool on = false;
   unsigned flags = 0;
   cudaError_t err = cudaSuccess;
+  bool nvtx_open = false;
+  Prof(const Prof&) = delete;
+  Prof& operator=(const Prof&) = delete;
+  ~Prof() {
+    if (nvtx_open) nvtxRangePop();
+    nvtxRangePop();
+  }
   Prof(bo_handle* h_, cudaStream_t s_, int max_launches) : h(h_), s(s_) {
+    nvtxRangePushA("bo");
     on = h->prof_events && h->prof_n >= max_launches + 1;
     if (on) {
       cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
@@ -94,6 +106,9 @@ struct Prof {
   // event i precedes launch i; `name` (forward path) is appended to the handle's kernel list
   void mark(int i, const char* name = nullptr) {
     if (name) {
+      if (nvtx_open) nvtxRangePop();
+      nvtxRangePushA(name);
+      nvtx_open = true;
       if (!h->last_kernels.empty()) h->last_kernels += ",";
       h->last_kernels += name;
     }
