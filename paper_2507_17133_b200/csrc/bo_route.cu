@@ -260,7 +260,11 @@ __global__ void __launch_bounds__(256) k_router_small(const T* __restrict__ x, c
 // staging), partial logits reduced in a fixed order through shared memory.
 // One token tile (tpc tokens, 256 threads) of the split-warp router; also the
 // first phase of the fused decode routing kernel (k_route_fused).
-template <typename T, int MAXM>
+// BULK: the tile's x rows and all of Wr are first brought into (dynamic) shared memory by
+// TMA bulk copies on one mbarrier (Wr at offset 0, then the tpc rows): per-thread global
+// loads keep only ~10-16 KB in flight per SM (the phase probe put this tile at 7.5 us on C3),
+// the copy engine the whole 80 KB at once.
+template <typename T, int MAXM, bool BULK = false>
 __device__ __forceinline__ void router_split_tile(const T* __restrict__ x, const T* __restrict__ Wr, int Tn, int d,
                                                   int m, int K, int tpc, float* __restrict__ logits,
                                                   int32_t* __restrict__ topk_id, float* __restrict__ topk_w,
@@ -280,15 +284,40 @@ __device__ __forceinline__ void router_split_tile(const T* __restrict__ x, const
   float acc[MAXM];
 #pragma unroll
   for (int e = 0; e < MAXM; ++e) acc[e] = 0.0f;
+  const uint4* xsrc = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(t) * d);
+  const uint4* wsrc = reinterpret_cast<const uint4*>(Wr);
+  if constexpr (BULK) {
+    extern __shared__ __align__(128) uint8_t rs_dyn[];
+    __shared__ __align__(8) uint64_t rs_bar;
+    const uint32_t wbytes = static_cast<uint32_t>(m) * d * sizeof(T);
+    const uint32_t rbytes = static_cast<uint32_t>(d) * sizeof(T);
+    if (threadIdx.x == 0) {
+      mbar_init(&rs_bar, 1);
+      fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int t0 = tile_idx * tpc;
+      const int nt = Tn - t0 < tpc ? Tn - t0 : tpc;
+      mbar_arrive_expect_tx(&rs_bar, wbytes + static_cast<uint32_t>(nt) * rbytes);
+      bulk_g2s(rs_dyn, Wr, wbytes, &rs_bar);
+      for (int i = 0; i < nt; ++i)
+        bulk_g2s(rs_dyn + wbytes + i * rbytes, x + static_cast<int64_t>(t0 + i) * d, rbytes, &rs_bar);
+    }
+    mbar_wait(&rs_bar, 0);
+    xsrc = reinterpret_cast<const uint4*>(rs_dyn + wbytes + tl * rbytes);
+    wsrc = reinterpret_cast<const uint4*>(rs_dyn);
+  }
+  auto ldv = [](const uint4* p) { return BULK ? *p : __ldg(p); };
   if (t < Tn) {
-    const uint4* xr = reinterpret_cast<const uint4*>(x + static_cast<int64_t>(t) * d);
-    const uint4* wr = reinterpret_cast<const uint4*>(Wr);
+    const uint4* xr = xsrc;
+    const uint4* wr = wsrc;
     for (int c0 = v0 + lane; c0 < v1; c0 += 32 * U) {
       uint4 xv[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int c = c0 + 32 * u;
-        xv[u] = c < v1 ? __ldg(xr + c) : make_uint4(0, 0, 0, 0);
+        xv[u] = c < v1 ? ldv(xr + c) : make_uint4(0, 0, 0, 0);
       }
 #pragma unroll
       for (int e0 = 0; e0 < MAXM; e0 += 8) {
@@ -299,7 +328,7 @@ __device__ __forceinline__ void router_split_tile(const T* __restrict__ x, const
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const int c = c0 + 32 * u;
-              wv[u][j] = (c < v1 && e0 + j < m) ? __ldg(wr + static_cast<int64_t>(e0 + j) * nvec + c)
+              wv[u][j] = (c < v1 && e0 + j < m) ? ldv(wr + static_cast<int64_t>(e0 + j) * nvec + c)
                                                 : make_uint4(0, 0, 0, 0);
             }
 #pragma unroll
@@ -351,13 +380,17 @@ __device__ __forceinline__ void router_split_tile(const T* __restrict__ x, const
   }
 }
 
-template <typename T, int MAXM>
+template <typename T, int MAXM, bool BULK>
 __global__ void __launch_bounds__(256) k_router_split(const T* __restrict__ x, const T* __restrict__ Wr, int Tn,
                                                       int d, int m, int K, int tpc, float* __restrict__ logits,
                                                       int32_t* __restrict__ topk_id, float* __restrict__ topk_w,
                                                       int32_t* __restrict__ tile_cnt) {
-  router_split_tile<T, MAXM>(x, Wr, Tn, d, m, K, tpc, logits, topk_id, topk_w, tile_cnt, blockIdx.x);
+  router_split_tile<T, MAXM, BULK>(x, Wr, Tn, d, m, K, tpc, logits, topk_id, topk_w, tile_cnt, blockIdx.x);
 }
+
+template <typename K>
+static cudaError_t smem_attr_once(K kern, int bytes, std::atomic<uint64_t>& done);
+static int router_bulk_bytes(int dtype, int m, int d, int tpc);
 
 // Prefill-sized batches, m <= 32, bf16: Eq. 8 on the tensor cores with
 // mma.sync m16n8k16 (bf16 x bf16 -> fp32).  N = m is far too narrow for a
@@ -506,9 +539,22 @@ cudaError_t launch_router_split(int dtype, const void* x, const void* Wr, int T,
                                 float* logits, int32_t* topk_id, float* topk_w, int32_t* tile_cnt, cudaStream_t s) {
   const int ntiles = (T + tpc - 1) / tpc;
   if (ntiles == 0) return cudaSuccess;
-#define BO_RS(TYPE, M)                                                                                       \
-  k_router_split<TYPE, M><<<ntiles, 256, 0, s>>>(static_cast<const TYPE*>(x), static_cast<const TYPE*>(Wr), T, \
-                                                 d, m, K, tpc, logits, topk_id, topk_w, tile_cnt)
+  const int bulk = router_bulk_bytes(dtype, m, d, tpc);
+#define BO_RS(TYPE, M)                                                                                         \
+  do {                                                                                                         \
+    if (bulk) {                                                                                                \
+      static std::atomic<uint64_t> done{0};                                                                    \
+      const cudaError_t e = smem_attr_once(k_router_split<TYPE, M, true>, 176 * 1024, done);                   \
+      if (e != cudaSuccess) return e;                                                                          \
+      k_router_split<TYPE, M, true><<<ntiles, 256, bulk, s>>>(static_cast<const TYPE*>(x),                     \
+                                                              static_cast<const TYPE*>(Wr), T, d, m, K, tpc,   \
+                                                              logits, topk_id, topk_w, tile_cnt);              \
+    } else {                                                                                                   \
+      k_router_split<TYPE, M, false><<<ntiles, 256, 0, s>>>(static_cast<const TYPE*>(x),                       \
+                                                            static_cast<const TYPE*>(Wr), T, d, m, K, tpc,     \
+                                                            logits, topk_id, topk_w, tile_cnt);                \
+    }                                                                                                          \
+  } while (0)
   if (dtype == 0) {
     if (m <= 8) BO_RS(__nv_bfloat16, 8); else if (m <= 16) BO_RS(__nv_bfloat16, 16); else BO_RS(__nv_bfloat16, 32);
   } else {
@@ -1154,7 +1200,7 @@ __device__ unsigned long long g_rf_probe[1024][6];
   } while (0)
 #endif
 
-template <typename T, int MAXM>
+template <typename T, int MAXM, bool BULK>
 __global__ void __launch_bounds__(256)
     k_route_fused(const T* __restrict__ x, const T* __restrict__ Wr, int Tn, int d, int m, int K, int tpc,
                   float* __restrict__ logits, int32_t* __restrict__ topk_id, float* __restrict__ topk_w,
@@ -1169,7 +1215,7 @@ __global__ void __launch_bounds__(256)
   __shared__ int32_t s_xoff[kRouteFusedMaxExec + 1];
   __shared__ int32_t s_tb[MAXM];
   BO_RF_STAMP(0);
-  router_split_tile<T, MAXM>(x, Wr, Tn, d, m, K, tpc, logits, topk_id, topk_w, tile_cnt, blockIdx.x);
+  router_split_tile<T, MAXM, BULK>(x, Wr, Tn, d, m, K, tpc, logits, topk_id, topk_w, tile_cnt, blockIdx.x);
   BO_RF_STAMP(1);
   cg::this_grid().sync();   // every tile histogram written (and visible)
   BO_RF_STAMP(2);
@@ -1230,7 +1276,8 @@ static int route_fused_capacity(int num_sms) {
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
   int nb = dev < 64 ? per_sm[dev].load(std::memory_order_relaxed) : 0;
   if (nb <= 0) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_route_fused<T, MAXM>, 256, 0) != cudaSuccess) return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_route_fused<T, MAXM, false>, 256, 0) != cudaSuccess)
+      return 0;
     if (dev < 64) per_sm[dev].store(nb, std::memory_order_relaxed);
   }
   return nb * num_sms;
@@ -1252,7 +1299,16 @@ bool route_fused_ok(int dtype, int m, int way, int T, int tpc, int n_shared, int
                                           : route_fused_capacity<__nv_bfloat16, 32>(num_sms));
   else cap = m <= 8 ? route_fused_capacity<float, 8>(num_sms)
                     : (m <= 16 ? route_fused_capacity<float, 16>(num_sms) : route_fused_capacity<float, 32>(num_sms));
-  return ntiles <= cap;   // a cooperative grid must be co-resident
+  return ntiles <= cap;   // a cooperative grid must be co-resident (the BULK variant's dynamic
+                          // shared memory still fits one CTA per SM: ntiles <= #SM by route_fused_tpc)
+}
+
+// Dynamic shared memory of the BULK router tile (Wr + the tile's x rows), or 0 when it does
+// not fit next to the static arrays (the tile then loads from global memory directly).
+static int router_bulk_bytes(int dtype, int m, int d, int tpc) {
+  const int64_t eb = dtype == 0 ? 2 : 4;
+  const int64_t b = (static_cast<int64_t>(m) + tpc) * d * eb;
+  return b <= 176 * 1024 ? static_cast<int>(b) : 0;
 }
 
 cudaError_t launch_route_fused(int dtype, const void* x, const void* Wr, int T, int d, int m, int K, int tpc,
@@ -1273,11 +1329,21 @@ cudaError_t launch_route_fused(int dtype, const void* x, const void* Wr, int T, 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   uint4* xpv = static_cast<uint4*>(xp);
+  const int bulk = router_bulk_bytes(dtype, m, d, tpc);
+  cfg.dynamicSmemBytes = static_cast<size_t>(bulk);
 #define BO_RF(TYPE, M)                                                                                         \
-  return cudaLaunchKernelEx(&cfg, k_route_fused<TYPE, M>, static_cast<const TYPE*>(x),                         \
-                            static_cast<const TYPE*>(Wr), T, d, m, K, tpc, logits, topk_id, topk_w, tile_cnt,  \
-                            way, ratio, mode, counts, exec_of_expert, expert_row_off, exec_off, mtile_off,     \
-                            stats, n_shared, row_of, row_tok, row_w, xpv, vec)
+  do {                                                                                                         \
+    if (bulk) {                                                                                                \
+      static std::atomic<uint64_t> done{0};                                                                    \
+      const cudaError_t e = smem_attr_once(k_route_fused<TYPE, M, true>, 176 * 1024, done);                    \
+      if (e != cudaSuccess) return e;                                                                          \
+    }                                                                                                          \
+    return cudaLaunchKernelEx(&cfg, bulk ? k_route_fused<TYPE, M, true> : k_route_fused<TYPE, M, false>,      \
+                              static_cast<const TYPE*>(x), static_cast<const TYPE*>(Wr), T, d, m, K, tpc, logits, \
+                              topk_id, topk_w, tile_cnt, way, ratio, mode, counts, exec_of_expert,             \
+                              expert_row_off, exec_off, mtile_off, stats, n_shared, row_of, row_tok, row_w, xpv, \
+                              vec);                                                                            \
+  } while (0)
   if (dtype == 0) {
     if (m <= 8) BO_RF(__nv_bfloat16, 8); else if (m <= 16) BO_RF(__nv_bfloat16, 16); else BO_RF(__nv_bfloat16, 32);
   } else {
