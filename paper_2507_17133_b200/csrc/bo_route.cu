@@ -1255,8 +1255,31 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   BO_RF_STAMP(4);
   const int E = m + (m + way - 1) / way;
+  // BULK: the tile's x rows are already in shared memory (router phase); concat_tokens
+  // then leaves as one TMA bulk store per (token, row) instead of the permute's
+  // per-thread copy loop
   permute_tile(topk_id, topk_w, Tn, K, m, tpc, me, s_tb, s_row_off, 1, row_of, row_tok, row_w,
-               reinterpret_cast<const uint4*>(x), xp, vec_per_row, n_shared, s_xoff + E);
+               reinterpret_cast<const uint4*>(x), BULK ? nullptr : xp, vec_per_row, n_shared, s_xoff + E);
+  if constexpr (BULK) {
+    if (xp) {
+      __syncthreads();   // row_of of the tile written (this CTA)
+      extern __shared__ __align__(128) uint8_t rs_dyn[];
+      const int KR = K + n_shared;
+      const uint32_t rbytes = static_cast<uint32_t>(vec_per_row) * 16u;
+      const uint8_t* xs = rs_dyn + static_cast<size_t>(m) * rbytes;   // after Wr (m rows)
+      const int t0 = me * tpc;
+      const int nt = Tn - t0 < tpc ? Tn - t0 : tpc;
+      if (threadIdx.x < nt * KR) {
+        const int i = threadIdx.x / KR, sl = threadIdx.x - i * KR;
+        const int r = row_of[static_cast<int64_t>(t0 + i) * KR + sl];
+        if (r >= 0) {
+          bulk_s2g(reinterpret_cast<uint8_t*>(xp) + static_cast<int64_t>(r) * rbytes, xs + i * rbytes, rbytes);
+          bulk_commit();
+          bulk_wait_all();   // complete before the grid ends (the next kernel's TMA reads Xp)
+        }
+      }
+    }
+  }
   __syncthreads();
   BO_RF_STAMP(5);
 }
